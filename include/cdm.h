@@ -1,0 +1,170 @@
+/*
+ * cdm.h -- C-ABI of libcdm, the B200 (sm_100a) decode hot path of "a Compiler-based Framework to
+ * Unleash Compressed Data Movement for Modern GPUs" (arxiv 2602.08190).
+ *
+ * The paper's problem statement (Sec. 3 Design): columns are compressed on the CPU
+ * with nested lightweight codecs and stored in CPU memory; the framework "facilitates the efficient
+ * movement of compressed data across the PCIe interconnect, followed by an ultra-fast, device-specific
+ * decompression phase", with "optimized overlap between PCIe data transfers and on-device
+ * decompression".  The three calls of that statement are:
+ *   describe a column's encoding cascade   -> cdm_cascade_create   (Table 2 notation)
+ *   submit compressed chunks from pinned host memory -> cdm_submit / cdm_submit_batch
+ *                                             (Pipelining Layer, Johnson order)
+ *   receive decoded device buffers          -> cdm_wait / cdm_synchronize (caller-owned device memory)
+ * plus a device-resident batch API (cdm_batch_*) that decodes chunks already in HBM, used to measure
+ * the kernels alone.
+ *
+ * Conventions.
+ *  - All pointers are plain host or device pointers; sizes are bytes unless stated.  No torch types.
+ *  - Every call returns cdm_status; nothing throws or aborts across the ABI.  Argument errors are
+ *    reported synchronously; data errors found on the device (dictionary index out of range, run
+ *    lengths not summing to the row count, LZ4 offsets/lengths out of bounds) are reported by
+ *    cdm_wait / cdm_batch_results as CDM_E_CORRUPT with cdm_result.error_bits set.  Kernels never
+ *    read or write out of bounds, even on corrupt input.
+ *  - cdm_last_error() returns a thread-local human-readable detail of the last failing call.
+ *  - Chunks are CDM1 containers: self-contained row groups of
+ *    < 2^31 rows, little-endian, 16-byte aligned zero-padded streams.
+ *  - Threading: one engine per (process, device).  An engine is NOT thread-safe: serialise calls on
+ *    one engine.  Cascades are immutable and may be shared by engines and threads.
+ */
+#ifndef CDM_H
+#define CDM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CDM_API __attribute__((visibility("default")))
+#else
+#define CDM_API
+#endif
+
+typedef enum {
+  CDM_OK = 0,
+  CDM_E_INVALID_ARG = 1,  /* null/misaligned pointer, bad size, bad option */
+  CDM_E_PARSE = 2,        /* cascade text does not parse / arity error (Table 2 grammar) */
+  CDM_E_UNSUPPORTED = 3,  /* a valid cascade with no fused device plan, or dtype mismatch */
+  CDM_E_CORRUPT = 4,      /* bad magic/version/bounds (host check) or device-detected data error */
+  CDM_E_CAPACITY = 5,     /* output buffer or staging slot too small */
+  CDM_E_CUDA = 6,         /* a CUDA runtime call failed (detail in cdm_last_error) */
+  CDM_E_OOM = 7,          /* device or pinned allocation failed */
+  CDM_E_BUSY = 8          /* unknown / already-consumed ticket */
+} cdm_status;
+
+/* Decoded element types (SURVEY Sec. 8d "Decoded types"). */
+typedef enum {
+  CDM_I32 = 0,      /* int32 (identifiers, date32 days since 1970-01-01) */
+  CDM_I64 = 1,      /* int64 (order keys) */
+  CDM_F64 = 2,      /* IEEE float64 (decimals) */
+  CDM_FIXED = 3,    /* fixed-width byte rows, width bytes each (CHAR(n)) */
+  CDM_VARBYTES = 4  /* variable-length bytes + int32 offsets[rows+1] (VARCHAR) */
+} cdm_dtype;
+
+/* Device error bits (cdm_result.error_bits). */
+#define CDM_ERR_DICT_INDEX 0x1u   /* a dictionary index >= number of entries */
+#define CDM_ERR_RUN_SUM 0x2u      /* RLE counts do not sum to the node's element count */
+#define CDM_ERR_LZ4 0x4u          /* malformed LZ4 block: offset 0 / before start, over-run, truncation */
+#define CDM_ERR_LENGTHS 0x8u      /* VARBYTES lengths do not sum to the payload size */
+#define CDM_ERR_WIDTH 0x10u       /* a bit width unusable for the stream it packs */
+
+typedef struct cdm_engine cdm_engine;
+typedef struct cdm_cascade cdm_cascade;
+typedef struct cdm_batch cdm_batch;
+
+typedef struct {
+  uint32_t n_slots;       /* device staging ring depth, >= 2 (default 4) */
+  uint64_t slot_bytes;    /* bytes per staging slot; a chunk must fit one slot (default 64 MiB) */
+  void *copy_stream;      /* cudaStream_t for H2D copies, or NULL: the engine creates one */
+  void *decode_stream;    /* cudaStream_t for decode kernels, or NULL: the engine creates one */
+  double pcie_gbps;       /* H2D link estimate for Johnson costs t_i (default 55 GB/s) */
+  double decode_gbps;     /* decoded-bytes/s estimate for Johnson costs d_i (default 3000 GB/s) */
+  uint32_t order_policy;  /* 0 = submission order, 1 = Johnson's rule */
+  uint32_t reserved;
+} cdm_engine_opts;
+
+typedef struct {
+  uint64_t rows;              /* rows decoded */
+  uint64_t payload_bytes;     /* decoded payload bytes written to dev_out */
+  uint64_t offsets_bytes;     /* decoded offsets bytes written to dev_offsets (VARBYTES) */
+  uint64_t compressed_bytes;  /* bytes of the chunk (what crossed PCIe) */
+  uint64_t chunk_id;          /* from the chunk header */
+  uint32_t error_bits;        /* CDM_ERR_* found on the device, 0 if clean */
+  uint32_t status;            /* cdm_status of this chunk */
+} cdm_result;
+
+typedef struct {
+  const cdm_cascade *cascade;  /* compiled cascade the chunk was encoded with */
+  const void *host_chunk;      /* CDM1 chunk in host memory (pinned for cdm_submit*); headers are read here */
+  const void *dev_chunk;       /* the same bytes already resident in device memory (cdm_batch_*), else NULL */
+  size_t chunk_bytes;          /* chunk size in bytes (>= header total) */
+  void *dev_out;               /* device output, >= payload bytes; 16-byte aligned */
+  size_t dev_out_bytes;
+  void *dev_offsets;           /* VARBYTES: device int32[rows+1]; else NULL */
+  size_t dev_offsets_bytes;
+} cdm_job;
+
+CDM_API const char *cdm_status_str(cdm_status s);
+CDM_API const char *cdm_last_error(void);
+CDM_API const char *cdm_version(void);
+
+/* ---- cascades (Nesting Layer; fusion rules PAPER.md:277-278) ----
+ * spec: Table 2 notation, e.g. "Dict|BitPack", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]",
+ * "Str|[LZ4,BitPack]" (case-insensitive, "Bit-packing"/"Dictionary encoding" accepted).
+ * The cascade is compiled into a fused plan of at most three kernel launches per chunk; a cascade
+ * that parses but has no fused device plan returns CDM_E_UNSUPPORTED.  width: row bytes for
+ * CDM_FIXED, ignored otherwise. */
+CDM_API cdm_status cdm_cascade_create(const char *spec, cdm_dtype dtype, uint32_t width, cdm_cascade **out);
+CDM_API cdm_status cdm_cascade_destroy(cdm_cascade *c);
+/* canonical text (e.g. "DICT|[RAW,BITPACK|RAW]") + " => " + the fused plan, into buf (NUL-terminated) */
+CDM_API cdm_status cdm_cascade_describe(const cdm_cascade *c, char *buf, size_t cap);
+
+/* Host-only parse + validation of a chunk header (no device work). */
+CDM_API cdm_status cdm_chunk_info(const void *host_chunk, size_t bytes, cdm_result *out);
+/* Host-only: validate a chunk against a cascade exactly as cdm_submit / cdm_batch_create will (header,
+ * node tree == cascade, stream bounds, per-codec sizes); no device memory is touched. */
+CDM_API cdm_status cdm_chunk_check(const cdm_cascade *c, const void *host_chunk, size_t bytes);
+
+/* ---- engine: staging ring + copy/decode streams (Pipelining Layer) ---- */
+CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opts *opts, cdm_engine **out);
+CDM_API cdm_status cdm_engine_destroy(cdm_engine *e);  /* waits for in-flight work */
+
+/* Asynchronously copy one chunk H2D into a staging slot (copy stream) and decode it (decode stream)
+ * after the copy's event.  host_chunk must stay valid and unmodified until the ticket completes. */
+CDM_API cdm_status cdm_submit(cdm_engine *e, const cdm_job *job, uint64_t *ticket);
+/* Submit n jobs; with order_policy = 1 they are issued in Johnson order (tickets[i] is job i's). */
+CDM_API cdm_status cdm_submit_batch(cdm_engine *e, const cdm_job *jobs, size_t n, uint64_t *tickets);
+/* Block until the ticket's decode finished; fills *out.  CDM_E_CORRUPT if error_bits != 0. */
+CDM_API cdm_status cdm_wait(cdm_engine *e, uint64_t ticket, cdm_result *out);
+/* Wait for everything submitted so far (results stay retrievable with cdm_wait). */
+CDM_API cdm_status cdm_synchronize(cdm_engine *e);
+/* H3 as a pure host function: Johnson's rule over jobs with transfer costs t[i] and
+ * decode costs d[i]; writes the issue order (a permutation of 0..n-1) to order[].  Jobs with t <= d come
+ * first by ascending t, the rest by descending d, ties by index.  O(n log n). */
+CDM_API cdm_status cdm_johnson_order(const double *t, const double *d, size_t n, size_t *order);
+
+/* ---- device-resident batches: chunks already in HBM (job.dev_chunk), decoded by grouped launches ----
+ * create: parses/validates headers on the host and sizes scratch (no device work is enqueued);
+ * launch: enqueues the fused decode of every job on `stream` (cudaStream_t, NULL = engine decode
+ *         stream); capturable into a CUDA graph; returns the number of kernel launches in *n_launches;
+ * results: synchronises `stream` and reads the per-chunk device error words. */
+CDM_API cdm_status cdm_batch_create(cdm_engine *e, const cdm_job *jobs, size_t n, cdm_batch **out);
+CDM_API cdm_status cdm_batch_launch(cdm_batch *b, void *stream, uint32_t *n_launches);
+CDM_API cdm_status cdm_batch_results(cdm_batch *b, void *stream, cdm_result *results);
+CDM_API cdm_status cdm_batch_destroy(cdm_batch *b);
+
+/* ---- instrumentation ---- */
+/* Record CUDA events around each kernel family launched by cdm_batch_launch (0 = off).  After
+ * cdm_batch_results, cdm_batch_kernel_ms() returns the accumulated per-family milliseconds over all
+ * launches since the last reset: index 0 FP (H5), 1 delta/offset scan (H6), 2 RLE (H7), 3 LZ4 (H8),
+ * 4 raw copies. */
+CDM_API cdm_status cdm_batch_set_timing(cdm_batch *b, int enable);
+CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch *b, double *ms5, uint64_t *launches5);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDM_H */

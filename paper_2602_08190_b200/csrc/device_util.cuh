@@ -1,0 +1,216 @@
+// device_util.cuh -- sm_100a device helpers shared by the decode kernels (never by the oracle).
+//
+//  * LSB-first contiguous bit-field extraction (reading R1) from shared or global words.
+//  * 1-D TMA bulk copies global->shared completing on an mbarrier (cp.async.bulk + expect_tx).
+//  * Tile tickets + epoch-tagged decoupled look-back (single-pass scan; Merrill & Garland style) used by
+//    the scan-dependent ("Group-Parallel") kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cdm {
+namespace dev {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+// ------------------------------------------------------------------ bit extraction
+// Field i of width w (0..64) from 32-bit little-endian words `wd` (bit k of the stream is bit (k&31) of
+// word k>>5).  Reads words [k>>5, (k>>5)+2]; callers guarantee those words are readable.
+__device__ __forceinline__ uint64_t extract_bits(const uint32_t* wd, uint64_t bitoff, uint32_t w) {
+  const uint64_t wi = bitoff >> 5;
+  const uint32_t sh = uint32_t(bitoff & 31);
+  const uint32_t a = wd[wi], b = wd[wi + 1];
+  const uint32_t lo = __funnelshift_r(a, b, sh);
+  if (w <= 32) return w == 32 ? lo : (lo & ((1u << w) - 1u));
+  const uint32_t c = wd[wi + 2];
+  const uint32_t hi = __funnelshift_r(b, c, sh);
+  const uint64_t v = (uint64_t(hi) << 32) | lo;
+  return w == 64 ? v : (v & ((1ull << w) - 1ull));
+}
+
+// Same, through the read-only path from global memory (small streams: RLE counts/values).
+__device__ __forceinline__ uint64_t extract_bits_global(const uint32_t* __restrict__ wd, uint64_t bitoff,
+                                                        uint32_t w) {
+  if (w == 0) return 0;
+  const uint64_t wi = bitoff >> 5;
+  const uint32_t sh = uint32_t(bitoff & 31);
+  const uint32_t a = __ldg(wd + wi), b = __ldg(wd + wi + 1);
+  const uint32_t lo = __funnelshift_r(a, b, sh);
+  if (w <= 32) return w == 32 ? lo : (lo & ((1u << w) - 1u));
+  const uint32_t c = __ldg(wd + wi + 2);
+  const uint32_t hi = __funnelshift_r(b, c, sh);
+  const uint64_t v = (uint64_t(hi) << 32) | lo;
+  return w == 64 ? v : (v & ((1ull << w) - 1ull));
+}
+
+// ------------------------------------------------------------------ mbarrier + TMA bulk copy
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+// 1-D bulk copy (TMA engine) of `bytes` (multiple of 16, 16-aligned src/dst) completing on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------------ vector stores
+__device__ __forceinline__ void st_v4_u32(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void st_v2_u64(void* p, uint64_t a, uint64_t b) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+// ------------------------------------------------------------------ tickets + look-back
+// A launch-wide 64-bit counter: high 32 bits = epoch, low 32 bits = next ticket.  One atomicAdd hands a
+// CTA both its tile ticket and the launch epoch; the CTA drawing the last ticket (`last`) bumps the epoch
+// and resets the ticket, so the counter needs no memset and survives CUDA-graph replays.
+__device__ __forceinline__ void take_ticket(unsigned long long* ctr, uint32_t last, uint32_t* ticket,
+                                            uint32_t* epoch) {
+  const unsigned long long v = atomicAdd(ctr, 1ull);
+  *ticket = uint32_t(v & 0xFFFFFFFFull);
+  *epoch = uint32_t(v >> 32) & 0x3FFFFFFFu;
+  if (*ticket == last) atomicExch(ctr, (unsigned long long)(*epoch + 1) << 32);
+}
+
+// flag word = (epoch << 2) | state
+constexpr uint32_t LB_AGG = 1, LB_INC = 2;
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Look-back state for up to two 64-bit components per tile (scan of counts, and of weighted deltas).
+struct LookbackState {
+  uint32_t* flag;   // [tiles]
+  uint64_t* agg0;   // [tiles]
+  uint64_t* agg1;   // [tiles] (may be null when one component)
+  uint64_t* inc0;   // [tiles]
+  uint64_t* inc1;   // [tiles]
+};
+
+// Publish a tile's aggregate (state AGG) -- values first, then the flag with release semantics.
+template <int NC>
+__device__ __forceinline__ void lb_publish(const LookbackState& s, uint32_t gt, uint32_t epoch, uint32_t state,
+                                           uint64_t v0, uint64_t v1) {
+  if (state == LB_AGG) {
+    st_relaxed_u64(s.agg0 + gt, v0);
+    if (NC > 1) st_relaxed_u64(s.agg1 + gt, v1);
+  } else {
+    st_relaxed_u64(s.inc0 + gt, v0);
+    if (NC > 1) st_relaxed_u64(s.inc1 + gt, v1);
+  }
+  st_release_u32(s.flag + gt, (epoch << 2) | state);
+}
+
+// Single-warp decoupled look-back: lanes probe 32 predecessors at a time (gt-1-lane), accumulate the
+// AGG values up to the nearest INC.  `first_gt` is the chunk's first tile (whose prefix is 0).  Must be
+// called by all 32 lanes of one warp; returns the exclusive prefix (both components) in every lane.
+template <int NC>
+__device__ __forceinline__ void lb_lookback(const LookbackState& s, uint32_t gt, uint32_t first_gt, uint32_t epoch,
+                                            uint64_t* p0, uint64_t* p1) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t acc0 = 0, acc1 = 0;
+  int64_t base = int64_t(gt) - 1;  // highest predecessor not yet folded
+  while (base >= int64_t(first_gt)) {
+    const int64_t me = base - lane;
+    uint32_t st = LB_INC;  // lanes below the chunk start act as a terminating INC with value 0
+    uint64_t a0 = 0, a1 = 0;
+    if (me >= int64_t(first_gt)) {
+      uint32_t f;
+      do {
+        f = ld_acquire_u32(s.flag + me);
+      } while (((f >> 2) != epoch) || (f & 3u) == 0);
+      st = f & 3u;
+      if (st == LB_INC) {
+        a0 = ld_relaxed_u64(s.inc0 + me);
+        if (NC > 1) a1 = ld_relaxed_u64(s.inc1 + me);
+      } else {
+        a0 = ld_relaxed_u64(s.agg0 + me);
+        if (NC > 1) a1 = ld_relaxed_u64(s.agg1 + me);
+      }
+    }
+    // the nearest INC (smallest lane index with state INC) terminates the walk
+    const uint32_t incmask = __ballot_sync(FULL, st == LB_INC);
+    const uint32_t stop = incmask ? uint32_t(__ffs(incmask) - 1) : 32u;
+    if (lane > stop) { a0 = 0; a1 = 0; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(FULL, a0, o);
+      if (NC > 1) a1 += __shfl_xor_sync(FULL, a1, o);
+    }
+    acc0 += a0;
+    acc1 += a1;
+    if (incmask) break;
+    base -= 32;
+  }
+  *p0 = acc0;
+  *p1 = acc1;
+}
+
+// ------------------------------------------------------------------ block scans (256 threads)
+// Exclusive scan of one u64 per thread across the CTA; returns the exclusive prefix, *total = sum.
+template <int NT>
+__device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* smem_warp /*[NT/32]*/,
+                                                        uint64_t* total) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= uint32_t(o)) x += y;
+  }
+  if (lane == 31) smem_warp[warp] = x;
+  __syncthreads();
+  uint64_t wp = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < NT / 32; k++) {
+    const uint64_t s = smem_warp[k];
+    if (uint32_t(k) < warp) wp += s;
+    tot += s;
+  }
+  __syncthreads();
+  *total = tot;
+  return wp + x - v;
+}
+
+}  // namespace dev
+}  // namespace cdm

@@ -1,0 +1,189 @@
+// kernels_fp.cu -- H5: element-parallel ("Fully-Parallel") fused decode.
+//
+//   out[i] = MAP( FOR + bits[i*w, i*w+w) )           MAP in { cast, dict[.], (double)(.)/10^d }
+//
+// The paper fuses consecutive Fully-Parallel kernels (bit-unpack + dictionary / Float2Int,
+// PAPER.md:277, Eq. 2) so the plain-size intermediate never touches HBM.  B200 shape
+// (DESIGN.md "H5"): persistent CTAs (grid = SMs x resident CTAs) walk 4096-value tiles; the tile's
+// packed bytes (512*w B, 16-aligned by construction) are staged into shared memory by the TMA engine
+// (cp.async.bulk + mbarrier), double-buffered so tile k+1 streams in while tile k is unpacked; each
+// thread unpacks 4 consecutive values per group with funnel shifts and writes them with one 16-byte
+// store (int32 / f32) or two (int64 / f64), so a warp writes 512 or 1024 contiguous bytes per group.
+#include "device_util.cuh"
+#include "kernels.h"
+
+namespace cdm {
+namespace {
+
+using namespace dev;
+
+__constant__ double kPow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                                  1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+
+__device__ __forceinline__ int find_desc_fp(const FpBatch& B, uint32_t tile) {
+  int lo = 0, hi = int(B.n) - 1;
+  while (lo < hi) {  // last desc with tile0 <= tile
+    const int mid = (lo + hi + 1) >> 1;
+    if (B.d[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t stage_bytes(const FpDesc& D, uint32_t lt) {
+  const uint64_t stream_bytes = ((uint64_t(D.n) * D.w + 7) / 8 + 15) & ~15ull;  // padded extent
+  const uint64_t start = uint64_t(lt) * (kFpTile / 8) * D.w;
+  const uint64_t want = uint64_t(kFpTile / 8) * D.w;
+  const uint64_t have = stream_bytes > start ? stream_bytes - start : 0;
+  return uint32_t(want < have ? want : have);
+}
+
+// Byte-granular dictionary copy for entry widths other than 4/8 (CHAR(n) rows).
+__device__ __forceinline__ void copy_row(uint8_t* dst, const uint8_t* __restrict__ src, uint32_t E) {
+  for (uint32_t b = 0; b < E; b++) dst[b] = __ldg(src + b);
+}
+
+__global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ FpBatch B) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const uint32_t tid = threadIdx.x;
+  // stage size is set by the host from the batch's largest w: dynamic smem = 2 stages
+  uint32_t stage_bytes_alloc;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(stage_bytes_alloc));
+  stage_bytes_alloc /= 2;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  uint32_t tile = blockIdx.x;
+  // prologue: stage the first tile
+  if (tid == 0 && tile < B.total_tiles) {
+    const int di = find_desc_fp(B, tile);
+    const FpDesc& D = B.d[di];
+    const uint32_t lt = tile - D.tile0;
+    const uint32_t nb = stage_bytes(D, lt);
+    mbar_arrive_expect_tx(&bar[0], nb);
+    if (nb) tma_load_1d(smem, D.packed + uint64_t(lt) * (kFpTile / 8) * D.w, nb, &bar[0]);
+  }
+  for (uint32_t it = 0; tile < B.total_tiles; it++, tile += gridDim.x) {
+    const uint32_t s = it & 1;
+    const uint32_t next = tile + gridDim.x;
+    if (tid == 0 && next < B.total_tiles) {  // stage s^1 was released by the __syncthreads ending it-1
+      const int dn = find_desc_fp(B, next);
+      const FpDesc& Dn = B.d[dn];
+      const uint32_t ltn = next - Dn.tile0;
+      const uint32_t nb = stage_bytes(Dn, ltn);
+      mbar_arrive_expect_tx(&bar[s ^ 1], nb);
+      if (nb) tma_load_1d(smem + (s ^ 1) * stage_bytes_alloc, Dn.packed + uint64_t(ltn) * (kFpTile / 8) * Dn.w, nb,
+                          &bar[s ^ 1]);
+    }
+    const int di = find_desc_fp(B, tile);
+    const FpDesc& D = B.d[di];
+    const uint32_t lt = tile - D.tile0;
+    mbar_wait(&bar[s], (it >> 1) & 1);
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(smem + s * stage_bytes_alloc);
+    const uint32_t w = D.w;
+    const uint64_t tile_start = uint64_t(lt) * kFpTile;
+    const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
+    bool bad_index = false;
+
+#pragma unroll 1
+    for (uint32_t k = 0; k < 4; k++) {
+      const uint32_t i0 = k * 1024 + tid * 4;  // 4 consecutive values
+      if (i0 >= valid) break;
+      uint64_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) v[j] = D.base + (w ? extract_bits(wd, uint64_t(i0 + j) * w, w) : 0ull);
+      const uint64_t gi = tile_start + i0;
+      const bool full = i0 + 4 <= valid;
+      if (D.mode == FP_INT) {
+        if (D.out_bytes == 4) {
+          uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
+          if (full) st_v4_u32(o, uint32_t(v[0]), uint32_t(v[1]), uint32_t(v[2]), uint32_t(v[3]));
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint32_t(v[j]);
+        } else if (D.out_bytes == 8) {
+          uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+          if (full) { st_v2_u64(o, v[0], v[1]); st_v2_u64(o + 2, v[2], v[3]); }
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = v[j];
+        } else if (D.out_bytes == 2) {
+          uint16_t* o = reinterpret_cast<uint16_t*>(D.out) + gi;
+          _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint16_t(v[j]);
+        } else {
+          uint8_t* o = reinterpret_cast<uint8_t*>(D.out) + gi;
+          if (full) *reinterpret_cast<uint32_t*>(o) = (v[0] & 0xFF) | ((v[1] & 0xFF) << 8) | ((v[2] & 0xFF) << 16) | ((v[3] & 0xFF) << 24);
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint8_t(v[j]);
+        }
+      } else if (D.mode == FP_DICT) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          if (v[j] >= D.entries) { bad_index = true; v[j] = 0; }
+        }
+        if (D.out_bytes == 8) {
+          const uint64_t* dict = reinterpret_cast<const uint64_t*>(D.dict);
+          uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+          if (full) {
+            st_v2_u64(o, __ldg(dict + v[0]), __ldg(dict + v[1]));
+            st_v2_u64(o + 2, __ldg(dict + v[2]), __ldg(dict + v[3]));
+          } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
+        } else if (D.out_bytes == 4) {
+          const uint32_t* dict = reinterpret_cast<const uint32_t*>(D.dict);
+          uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
+          if (full) st_v4_u32(o, __ldg(dict + v[0]), __ldg(dict + v[1]), __ldg(dict + v[2]), __ldg(dict + v[3]));
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
+        } else {
+          const uint32_t E = D.out_bytes;
+          uint8_t* o = reinterpret_cast<uint8_t*>(D.out) + gi * E;
+          _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) copy_row(o + j * E, D.dict + v[j] * E, E);
+        }
+      } else {  // FP_F2I: one IEEE division per element (no reciprocal: bit-exact, R13)
+        const double p = kPow10[D.d];
+        double f[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) f[j] = double(int64_t(v[j])) / p;
+        uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+        if (full) {
+          st_v2_u64(o, __double_as_longlong(f[0]), __double_as_longlong(f[1]));
+          st_v2_u64(o + 2, __double_as_longlong(f[2]), __double_as_longlong(f[3]));
+        } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __double_as_longlong(f[j]);
+      }
+    }
+    if (bad_index) atomicOr(B.err + D.err_idx, 0x1u);
+    __syncthreads();  // everyone is done with stage s before it is refilled
+  }
+}
+
+}  // namespace
+
+int device_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
+  if (!b.total_tiles) return cudaSuccess;
+  const uint32_t stage = ((kFpTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words for extraction
+  const uint32_t smem = 2 * stage;
+  static uint32_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp_kernel, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint32_t grid = uint32_t(device_sms() * per_sm);
+  if (grid > b.total_tiles) grid = b.total_tiles;
+  fp_kernel<<<grid, kThreads, smem, s>>>(b);
+  return cudaGetLastError();
+}
+
+}  // namespace cdm

@@ -1,0 +1,218 @@
+// plan.h -- H1: cascade text (Table 2 notation) -> fused decode plan.
+//
+// The runtime's own parser (the encoder and the oracle have theirs).  Grammar:
+//   node := NAME [ "(" k=v {, k=v} ")" ] [ "|" ( node | "[" node {, node} "]" ) ]
+// Codec names are case-insensitive with non-alphanumerics ignored ("Bit-packing", "Dictionary encoding").
+// Arity completion (reading R30): 0 children -> all outputs Raw; 1 child binds the primary
+// stream (Dict->indices, RLE->values, Str->bytes); BitPack and LZ4 children are always Raw.
+//
+// Fusion ("fusing Fully-Parallel patterns to nearby patterns"): FP chains collapse into
+// one map (H5); an FP producer of RLE values is absorbed into the expansion and an FP producer of counts
+// into the counts scan (H7); Delta over BitPack is one single-pass scan (H6); LZ4 is a fusion barrier.
+#pragma once
+#include <cctype>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "format.h"
+
+namespace cdm {
+
+struct TNode {
+  uint8_t codec = RAW;
+  std::vector<std::unique_ptr<TNode>> kids;
+};
+
+inline int codec_from_name(const std::string& raw) {
+  std::string b;
+  for (char ch : raw)
+    if (std::isalnum(static_cast<unsigned char>(ch))) b += char(std::tolower(static_cast<unsigned char>(ch)));
+  if (b == "raw") return RAW;
+  if (b == "bitpack" || b == "bitpacking" || b == "for") return BITPACK;
+  if (b == "dict" || b == "dictionary" || b == "dictionaryencoding") return DICT;
+  if (b == "float2int") return FLOAT2INT;
+  if (b == "delta" || b == "deltaencoding") return DELTA;
+  if (b == "rle") return RLE;
+  if (b == "lz4") return LZ4;
+  if (b == "str" || b == "string" || b == "varchar") return STR;
+  return -1;
+}
+
+struct CascadeParser {
+  const std::string& s;
+  size_t pos = 0;
+  std::string err;
+  explicit CascadeParser(const std::string& t) : s(t) {}
+  void ws() { while (pos < s.size() && std::isspace(static_cast<unsigned char>(s[pos]))) pos++; }
+  bool fail(const std::string& m) { if (err.empty()) err = "parse error at " + std::to_string(pos) + ": " + m; return false; }
+
+  std::unique_ptr<TNode> node() {
+    ws();
+    std::string name;
+    while (pos < s.size() && (std::isalnum(static_cast<unsigned char>(s[pos])) || s[pos] == '-' || s[pos] == '_' ||
+                              (s[pos] == ' ' && !name.empty() && pos + 1 < s.size() &&
+                               std::isalpha(static_cast<unsigned char>(s[pos + 1]))))) {
+      name += s[pos++];
+    }
+    if (name.empty()) { fail("expected codec name"); return nullptr; }
+    int c = codec_from_name(name);
+    if (c < 0) { err = "unknown codec '" + name + "'"; return nullptr; }
+    auto t = std::make_unique<TNode>();
+    t->codec = uint8_t(c);
+    ws();
+    if (pos < s.size() && s[pos] == '(') {  // options: accepted and ignored by the decoder
+      while (pos < s.size() && s[pos] != ')') pos++;
+      if (pos >= s.size()) { fail("expected ')'"); return nullptr; }
+      pos++;
+      ws();
+    }
+    if (pos < s.size() && s[pos] == '|') {
+      pos++;
+      ws();
+      if (pos < s.size() && s[pos] == '[') {
+        pos++;
+        for (;;) {
+          if (t->kids.size() == 2) { fail("too many children"); return nullptr; }
+          auto ch = node();
+          if (!ch) return nullptr;
+          t->kids.push_back(std::move(ch));
+          ws();
+          if (pos < s.size() && s[pos] == ',') { pos++; continue; }
+          if (pos < s.size() && s[pos] == ']') { pos++; break; }
+          fail("expected ',' or ']'");
+          return nullptr;
+        }
+      } else {
+        auto ch = node();
+        if (!ch) return nullptr;
+        t->kids.push_back(std::move(ch));
+      }
+    }
+    return t;
+  }
+};
+
+inline std::unique_ptr<TNode> mk_raw() { auto t = std::make_unique<TNode>(); t->codec = RAW; return t; }
+
+inline bool complete_tree(TNode* t, std::string* err) {
+  auto& k = t->kids;
+  switch (t->codec) {
+    case RAW:
+      if (!k.empty()) { *err = "arity error: Raw takes no children"; return false; }
+      return true;
+    case BITPACK:
+      if (k.empty()) k.push_back(mk_raw());
+      if (k.size() != 1 || k[0]->codec != RAW) { *err = "arity error: BitPack's only child is Raw"; return false; }
+      return true;
+    case LZ4:
+      if (!k.empty()) { *err = "arity error: LZ4 takes no children"; return false; }
+      k.push_back(mk_raw());
+      k.push_back(mk_raw());
+      return true;
+    case DICT:
+      if (k.empty()) { k.push_back(mk_raw()); k.push_back(mk_raw()); }
+      else if (k.size() == 1) k.insert(k.begin(), mk_raw());
+      if (k[0]->codec != RAW) { *err = "arity error: Dict's dictionary stream is Raw"; return false; }
+      break;
+    case FLOAT2INT:
+    case DELTA:
+      if (k.empty()) k.push_back(mk_raw());
+      if (k.size() != 1) { *err = "arity error: Float2Int/Delta take one child"; return false; }
+      break;
+    case RLE:
+    case STR:
+      if (k.empty()) { k.push_back(mk_raw()); k.push_back(mk_raw()); }
+      else if (k.size() == 1) k.push_back(mk_raw());
+      break;
+    default:
+      *err = "unknown codec";
+      return false;
+  }
+  for (auto& c : k)
+    if (!complete_tree(c.get(), err)) return false;
+  return true;
+}
+
+inline const char* codec_name(uint8_t c) {
+  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR"};
+  return c < 8 ? N[c] : "?";
+}
+
+inline void render_tree(const TNode* t, std::string* out) {
+  *out += codec_name(t->codec);
+  if (t->kids.empty()) return;
+  *out += "|";
+  if (t->kids.size() == 1) { render_tree(t->kids[0].get(), out); return; }
+  *out += "[";
+  for (size_t i = 0; i < t->kids.size(); i++) {
+    if (i) *out += ",";
+    render_tree(t->kids[i].get(), out);
+  }
+  *out += "]";
+}
+
+inline uint64_t fnv1a64(const std::string& s) {
+  uint64_t h = 14695981039346656037ull;
+  for (unsigned char ch : s) { h ^= ch; h *= 1099511628211ull; }
+  return h;
+}
+
+// ------------------------------------------------------------------ fused plans
+enum class PlanKind : uint8_t { RawCopy, Fp, Scan, Rle, Str };
+
+struct Plan {
+  PlanKind kind = PlanKind::RawCopy;
+  uint8_t fp_mode = 0;   // FpMode
+  uint8_t vmode = 0;     // RleValueMode
+  bool str_lz4 = false;
+  std::string text;      // human-readable fused plan
+};
+
+// Recognise the fused shapes; anything else is a valid cascade without a device plan.
+inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* err) {
+  auto is = [](const TNode* t, uint8_t c) { return t && t->codec == c; };
+  auto bp = [&](const TNode* t) { return is(t, BITPACK); };
+  auto kid = [](const TNode* t, size_t i) -> const TNode* { return i < t->kids.size() ? t->kids[i].get() : nullptr; };
+  if (dtype == T_VARBYTES) {
+    if (is(r, STR) && bp(kid(r, 1)) && (is(kid(r, 0), LZ4) || is(kid(r, 0), RAW))) {
+      p->kind = PlanKind::Str;
+      p->str_lz4 = is(kid(r, 0), LZ4);
+      p->text = p->str_lz4 ? "scan_offsets(unpack lengths) + lz4_warp_decode" : "scan_offsets(unpack lengths) + copy";
+      return true;
+    }
+    *err = "VARBYTES needs Str|[LZ4,BitPack] or Str|[Raw,BitPack]";
+    return false;
+  }
+  if (is(r, STR) || is(r, LZ4)) { *err = "Str/LZ4 roots need a VARBYTES column"; return false; }
+  if (is(r, RAW)) { p->kind = PlanKind::RawCopy; p->text = "copy"; return true; }
+  if (bp(r)) { p->kind = PlanKind::Fp; p->fp_mode = 0; p->text = "fp(unpack+FOR+cast)"; return true; }
+  if (is(r, DICT) && bp(kid(r, 1))) { p->kind = PlanKind::Fp; p->fp_mode = 1; p->text = "fp(unpack+FOR+dict gather)"; return true; }
+  if (is(r, FLOAT2INT) && bp(kid(r, 0))) { p->kind = PlanKind::Fp; p->fp_mode = 2; p->text = "fp(unpack+FOR+float2int)"; return true; }
+  if (is(r, DELTA) && bp(kid(r, 0))) { p->kind = PlanKind::Scan; p->text = "scan(unpack+FOR+delta, decoupled look-back)"; return true; }
+  auto is_delta_rle = [&](const TNode* t) {
+    return is(t, DELTA) && is(kid(t, 0), RLE) && bp(kid(kid(t, 0), 0)) && bp(kid(kid(t, 0), 1));
+  };
+  if (is_delta_rle(r)) {
+    p->kind = PlanKind::Rle; p->vmode = 4;
+    p->text = "rle(arithmetic runs: unpack dv,dc + 2-component look-back + expand)";
+    return true;
+  }
+  if (is(r, RLE) && bp(kid(r, 1))) {
+    const TNode* v = kid(r, 0);
+    p->kind = PlanKind::Rle;
+    if (bp(v)) { p->vmode = 0; p->text = "rle(unpack counts+values, look-back, expand)"; return true; }
+    if (is(v, DICT) && bp(kid(v, 1))) { p->vmode = 1; p->text = "rle(values = dict gather fused, look-back, expand)"; return true; }
+    if (is(v, FLOAT2INT) && bp(kid(v, 0))) { p->vmode = 2; p->text = "rle(values = float2int fused, look-back, expand)"; return true; }
+    if (is_delta_rle(v)) {
+      p->vmode = 3;
+      p->text = "inner_scan(delta|rle run table) + rle(values = closed form, look-back, expand)";
+      return true;
+    }
+  }
+  *err = "no fused device plan for this cascade";
+  return false;
+}
+
+}  // namespace cdm

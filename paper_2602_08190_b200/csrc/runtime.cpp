@@ -1,0 +1,1032 @@
+// runtime.cpp -- libcdm: the C-ABI (include/cdm.h) over the sm_100a decode kernels.
+//
+//  H1  cascade text -> fused plan                      (plan.h)
+//  H2  CDM1 chunk parse/validation + binding to a plan  (format.h)
+//  H3  Johnson order of chunk jobs
+//  H4  H2D copies into a device staging ring on a copy stream, decode on a decode stream after the
+//      copy's event (overlap of PCIe transfers and on-device decompression)
+//  H5-H8 grouped kernel launches (kernels_*.cu), H9 per-chunk device error words.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "cdm.h"
+#include "format.h"
+#include "kernels.h"
+#include "plan.h"
+
+using namespace cdm;
+
+// ============================================================================ errors
+static thread_local std::string g_last;
+static cdm_status fail(cdm_status s, const std::string& m) {
+  g_last = m;
+  return s;
+}
+#define CUDA_TRY(x)                                                                      \
+  do {                                                                                   \
+    cudaError_t _e = (x);                                                                \
+    if (_e != cudaSuccess) return fail(CDM_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" CDM_API const char* cdm_status_str(cdm_status s) {
+  switch (s) {
+    case CDM_OK: return "ok";
+    case CDM_E_INVALID_ARG: return "invalid argument";
+    case CDM_E_PARSE: return "cascade parse error";
+    case CDM_E_UNSUPPORTED: return "unsupported";
+    case CDM_E_CORRUPT: return "corrupt chunk";
+    case CDM_E_CAPACITY: return "capacity";
+    case CDM_E_CUDA: return "cuda error";
+    case CDM_E_OOM: return "out of memory";
+    case CDM_E_BUSY: return "busy / unknown ticket";
+  }
+  return "unknown";
+}
+extern "C" CDM_API const char* cdm_last_error(void) { return g_last.c_str(); }
+extern "C" CDM_API const char* cdm_version(void) { return "cdm 0.1 (sm_100a)"; }
+
+// ============================================================================ cascades
+struct cdm_cascade {
+  std::string canonical;
+  uint64_t hash = 0;
+  uint8_t dtype = 0;
+  uint32_t width = 0;
+  Plan plan;
+};
+
+static uint32_t dtype_width(uint8_t dtype, uint32_t width) {
+  switch (dtype) {
+    case T_I32: return 4;
+    case T_I64: case T_F64: return 8;
+    case T_FIXED: return width;
+    case T_VARBYTES: return 1;
+  }
+  return 0;
+}
+
+extern "C" CDM_API cdm_status cdm_cascade_create(const char* spec, cdm_dtype dtype, uint32_t width, cdm_cascade** out) {
+  if (!spec || !out) return fail(CDM_E_INVALID_ARG, "null argument");
+  if (dtype > CDM_VARBYTES) return fail(CDM_E_INVALID_ARG, "bad dtype");
+  if (dtype == CDM_FIXED && width == 0) return fail(CDM_E_INVALID_ARG, "FIXED needs width > 0");
+  std::string text(spec);
+  CascadeParser P(text);
+  auto root = P.node();
+  if (!root) return fail(CDM_E_PARSE, P.err);
+  P.ws();
+  if (P.pos != text.size()) return fail(CDM_E_PARSE, "parse error at " + std::to_string(P.pos) + ": trailing input");
+  std::string err;
+  if (!complete_tree(root.get(), &err)) return fail(CDM_E_PARSE, err);
+  auto c = std::make_unique<cdm_cascade>();
+  render_tree(root.get(), &c->canonical);
+  c->hash = fnv1a64(c->canonical);
+  c->dtype = uint8_t(dtype);
+  c->width = dtype == CDM_FIXED ? width : dtype_width(uint8_t(dtype), 0);
+  if (!compile_plan(root.get(), uint8_t(dtype), &c->plan, &err)) return fail(CDM_E_UNSUPPORTED, c->canonical + ": " + err);
+  *out = c.release();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_cascade_destroy(cdm_cascade* c) {
+  delete c;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_cascade_describe(const cdm_cascade* c, char* buf, size_t cap) {
+  if (!c || !buf || !cap) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::string s = c->canonical + " => " + c->plan.text;
+  if (s.size() + 1 > cap) return fail(CDM_E_CAPACITY, "buffer too small");
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return CDM_OK;
+}
+
+// ============================================================================ chunk binding
+namespace {
+
+struct BPB {  // a bound BitPack node
+  uint64_t off = 0;  // packed stream offset within the chunk
+  uint64_t n = 0;
+  uint32_t w = 0;
+  uint64_t base = 0;
+};
+
+struct Bound {
+  const cdm_cascade* casc = nullptr;
+  PlanKind kind = PlanKind::RawCopy;
+  uint8_t fp_mode = 0, vmode = 0;
+  uint64_t rows = 0, payload = 0, offsets_bytes = 0, total = 0, chunk_id = 0;
+  uint32_t W = 0;
+  BPB main, counts, inner_dv, inner_dc;
+  uint64_t dict_off = 0;
+  uint32_t entries = 0;
+  uint8_t d = 0;
+  uint64_t delta_base = 0, inner_base = 0;
+  uint32_t nruns = 0, n_inner = 0;
+  bool lz4 = false;
+  uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
+  uint32_t n_sub = 0;
+  const uint8_t* dev_chunk = nullptr;
+  void* out = nullptr;
+  void* offs = nullptr;
+};
+
+struct Tree {
+  const Chunk& c;
+  std::vector<std::vector<int>> kids;
+  std::string err;
+  explicit Tree(const Chunk& ch) : c(ch), kids(ch.nodes.size()) {}
+  int walk(size_t* idx) {
+    if (*idx >= c.nodes.size()) { err = "node table: missing nodes"; return -1; }
+    int me = int((*idx)++);
+    for (uint32_t k = 0; k < c.nodes[me].nchild; k++) {
+      int ch = walk(idx);
+      if (ch < 0) return -1;
+      kids[me].push_back(ch);
+    }
+    return me;
+  }
+  void render(int i, std::string* out) const {
+    *out += codec_name(c.nodes[i].codec);
+    if (kids[i].empty()) return;
+    *out += "|";
+    if (kids[i].size() == 1) { render(kids[i][0], out); return; }
+    *out += "[";
+    for (size_t k = 0; k < kids[i].size(); k++) {
+      if (k) *out += ",";
+      render(kids[i][k], out);
+    }
+    *out += "]";
+  }
+};
+
+std::string raw_stream(const Chunk& c, const Tree& t, int i, uint32_t eb, uint64_t* off, uint64_t* n) {
+  const Node& nd = c.nodes[i];
+  if (nd.codec != RAW) return "node " + std::to_string(i) + ": expected Raw";
+  if (nd.stream >= c.streams.size()) return "node " + std::to_string(i) + ": stream out of range";
+  if (nd.elem_bytes == 0 || (eb && nd.elem_bytes != eb)) return "node " + std::to_string(i) + ": raw element bytes";
+  const Stream& s = c.streams[nd.stream];
+  if (nd.n > s.bytes / nd.elem_bytes || nd.n * nd.elem_bytes != s.bytes)
+    return "node " + std::to_string(i) + ": raw stream length mismatch";
+  *off = s.offset;
+  *n = nd.n;
+  (void)t;
+  return "";
+}
+
+std::string bind_bp(const Chunk& c, const Tree& t, int i, uint64_t n_expect, uint32_t max_w, BPB* b) {
+  const Node& nd = c.nodes[i];
+  if (nd.codec != BITPACK || t.kids[i].size() != 1) return "node " + std::to_string(i) + ": expected BitPack";
+  if (nd.n != n_expect) return "node " + std::to_string(i) + ": BitPack element count mismatch";
+  if (nd.w() > max_w) return "node " + std::to_string(i) + ": bit width " + std::to_string(nd.w()) + " too large";
+  uint64_t off, bytes;
+  std::string e = raw_stream(c, t, t.kids[i][0], 1, &off, &bytes);
+  if (!e.empty()) return e;
+  if ((nd.n * nd.w() + 7) / 8 > bytes) return "node " + std::to_string(i) + ": packed stream too short";
+  b->off = off;
+  b->n = nd.n;
+  b->w = nd.w();
+  b->base = nd.u64_at8();
+  return "";
+}
+
+cdm_status bind_job(const cdm_job& job, Bound* b) {
+  if (!job.cascade || !job.host_chunk) return fail(CDM_E_INVALID_ARG, "job needs a cascade and a host chunk");
+  const cdm_cascade* cs = job.cascade;
+  Chunk c;
+  std::string e = parse_chunk(job.host_chunk, job.chunk_bytes, &c);
+  if (!e.empty()) return fail(CDM_E_CORRUPT, e);
+  if (c.cascade_hash != cs->hash) return fail(CDM_E_CORRUPT, "chunk was encoded with another cascade (hash mismatch)");
+  if (c.dtype != cs->dtype) return fail(CDM_E_CORRUPT, "chunk dtype differs from the cascade's");
+  Tree t(c);
+  size_t idx = 0;
+  if (c.nodes.empty() || t.walk(&idx) != 0 || idx != c.nodes.size()) return fail(CDM_E_CORRUPT, t.err.empty() ? "node table: unused nodes" : t.err);
+  for (size_t i = 0; i < c.nodes.size(); i++) {
+    static const int arity[8] = {0, 1, 2, 1, 1, 2, 2, 2};
+    if (c.nodes[i].codec > STR || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
+      return fail(CDM_E_CORRUPT, "node " + std::to_string(i) + ": bad codec or arity");
+  }
+  std::string canon;
+  t.render(0, &canon);
+  if (canon != cs->canonical) return fail(CDM_E_CORRUPT, "chunk tree " + canon + " != cascade " + cs->canonical);
+  const uint32_t W = dtype_width(c.dtype, c.width);
+  if (c.dtype == T_FIXED && c.width != cs->width) return fail(CDM_E_CORRUPT, "FIXED width differs from the cascade's");
+  if (W == 0) return fail(CDM_E_CORRUPT, "zero width");
+  b->casc = cs;
+  b->kind = cs->plan.kind;
+  b->fp_mode = cs->plan.fp_mode;
+  b->vmode = cs->plan.vmode;
+  b->rows = c.rows;
+  b->payload = c.payload_bytes;
+  b->offsets_bytes = c.offsets_bytes;
+  b->total = c.total_bytes;
+  b->chunk_id = c.chunk_id;
+  b->W = W;
+  const Node& r = c.nodes[0];
+  if (r.n != c.rows) return fail(CDM_E_CORRUPT, "root element count != rows");
+  if (c.dtype != T_VARBYTES && c.payload_bytes != c.rows * W) return fail(CDM_E_CORRUPT, "payload bytes != rows * width");
+  auto bad = [&](const std::string& m) { return fail(CDM_E_CORRUPT, m); };
+  auto need_w48 = [&]() { return W == 4 || W == 8; };
+
+  switch (b->kind) {
+    case PlanKind::RawCopy: {
+      uint64_t n;
+      if (!(e = raw_stream(c, t, 0, W, &b->raw_off, &n)).empty()) return bad(e);
+      break;
+    }
+    case PlanKind::Fp: {
+      if (b->fp_mode == FP_INT) {
+        if (!(W == 1 || W == 2 || W == 4 || W == 8)) return fail(CDM_E_UNSUPPORTED, "BitPack output width must be 1/2/4/8");
+        if (!(e = bind_bp(c, t, 0, c.rows, 64, &b->main)).empty()) return bad(e);
+      } else if (b->fp_mode == FP_DICT) {
+        int di = t.kids[0][0], ii = t.kids[0][1];
+        uint64_t dn;
+        if (!(e = raw_stream(c, t, di, W, &b->dict_off, &dn)).empty()) return bad(e);
+        b->entries = r.u32_at0();
+        if (r.u32_at4() != W || dn != b->entries) return bad("dictionary shape mismatch");
+        if (!(e = bind_bp(c, t, ii, c.rows, 64, &b->main)).empty()) return bad(e);
+      } else {
+        if (c.dtype != T_F64) return fail(CDM_E_UNSUPPORTED, "Float2Int needs F64 output");
+        b->d = r.params[0];
+        if (b->d > 22) return bad("Float2Int exponent > 22");
+        if (!(e = bind_bp(c, t, t.kids[0][0], c.rows, 64, &b->main)).empty()) return bad(e);
+      }
+      break;
+    }
+    case PlanKind::Scan: {
+      if (!need_w48()) return fail(CDM_E_UNSUPPORTED, "Delta output width must be 4 or 8");
+      b->delta_base = r.u64_at8();
+      if (!(e = bind_bp(c, t, t.kids[0][0], c.rows, 64, &b->main)).empty()) return bad(e);
+      break;
+    }
+    case PlanKind::Rle: {
+      if (!need_w48()) return fail(CDM_E_UNSUPPORTED, "RLE output width must be 4 or 8");
+      if (b->vmode == V_LINEAR) {  // Delta | RLE | [BitPack dv, BitPack dc]
+        b->delta_base = r.u64_at8();
+        int ri = t.kids[0][0];
+        const Node& rl = c.nodes[ri];
+        if (rl.n != c.rows) return bad("Delta child count mismatch");
+        b->nruns = rl.u32_at0();
+        if (!(e = bind_bp(c, t, t.kids[ri][0], b->nruns, 64, &b->main)).empty()) return bad(e);
+        if (!(e = bind_bp(c, t, t.kids[ri][1], b->nruns, 32, &b->counts)).empty()) return bad(e);
+        break;
+      }
+      b->nruns = r.u32_at0();
+      int vi = t.kids[0][0], ci = t.kids[0][1];
+      if (!(e = bind_bp(c, t, ci, b->nruns, 32, &b->counts)).empty()) return bad(e);
+      const Node& v = c.nodes[vi];
+      if (b->vmode == V_BP) {
+        if (!(e = bind_bp(c, t, vi, b->nruns, 64, &b->main)).empty()) return bad(e);
+      } else if (b->vmode == V_DICT) {
+        uint64_t dn;
+        if (v.n != b->nruns) return bad("RLE values count mismatch");
+        if (!(e = raw_stream(c, t, t.kids[vi][0], W, &b->dict_off, &dn)).empty()) return bad(e);
+        b->entries = v.u32_at0();
+        if (v.u32_at4() != W || dn != b->entries) return bad("dictionary shape mismatch");
+        if (!(e = bind_bp(c, t, t.kids[vi][1], b->nruns, 64, &b->main)).empty()) return bad(e);
+      } else if (b->vmode == V_F2I) {
+        if (c.dtype != T_F64) return fail(CDM_E_UNSUPPORTED, "Float2Int needs F64 output");
+        if (v.n != b->nruns) return bad("RLE values count mismatch");
+        b->d = v.params[0];
+        if (b->d > 22) return bad("Float2Int exponent > 22");
+        if (!(e = bind_bp(c, t, t.kids[vi][0], b->nruns, 64, &b->main)).empty()) return bad(e);
+      } else {  // V_DRLE: values = Delta | RLE | [BitPack dv, BitPack dc]
+        if (v.n != b->nruns) return bad("RLE values count mismatch");
+        b->inner_base = v.u64_at8();
+        int ri = t.kids[vi][0];
+        const Node& rl = c.nodes[ri];
+        if (rl.n != b->nruns) return bad("inner RLE count mismatch");
+        b->n_inner = rl.u32_at0();
+        if (b->nruns && !b->n_inner) return bad("inner RLE has no runs");
+        if (!(e = bind_bp(c, t, t.kids[ri][0], b->n_inner, 64, &b->inner_dv)).empty()) return bad(e);
+        if (!(e = bind_bp(c, t, t.kids[ri][1], b->n_inner, 32, &b->inner_dc)).empty()) return bad(e);
+      }
+      break;
+    }
+    case PlanKind::Str: {
+      if (c.offsets_bytes != 4 * (c.rows + 1)) return bad("offsets bytes != 4 * (rows + 1)");
+      if (c.payload_bytes >= (1ull << 31)) return fail(CDM_E_UNSUPPORTED, "VARBYTES payload >= 2^31 per chunk");
+      int bi = t.kids[0][0], li = t.kids[0][1];
+      if (!(e = bind_bp(c, t, li, c.rows, 64, &b->main)).empty()) return bad(e);
+      const Node& bn = c.nodes[bi];
+      if (bn.n != c.payload_bytes) return bad("Str bytes count != payload bytes");
+      if (bn.codec == LZ4) {
+        b->lz4 = true;
+        uint64_t pn, tn;
+        if (!(e = raw_stream(c, t, t.kids[bi][0], 1, &b->lz_pay_off, &pn)).empty()) return bad(e);
+        if (!(e = raw_stream(c, t, t.kids[bi][1], 12, &b->lz_tab_off, &tn)).empty()) return bad(e);
+        b->lz_pay_bytes = pn;
+        b->n_sub = bn.u32_at0();
+        if (tn != b->n_sub) return bad("LZ4 table entries != n_sub");
+        if (c.payload_bytes && !b->n_sub) return bad("LZ4 without sub-chunks");
+      } else {
+        uint64_t n;
+        if (!(e = raw_stream(c, t, bi, 1, &b->bytes_off, &n)).empty()) return bad(e);
+      }
+      break;
+    }
+  }
+  if (job.dev_out_bytes == SIZE_MAX) return CDM_OK;  // cdm_chunk_check: host validation only
+  // output buffers
+  if (b->payload && !job.dev_out) return fail(CDM_E_INVALID_ARG, "dev_out is null");
+  if (job.dev_out_bytes < b->payload) return fail(CDM_E_CAPACITY, "dev_out smaller than the payload");
+  if (reinterpret_cast<uintptr_t>(job.dev_out) % 16) return fail(CDM_E_INVALID_ARG, "dev_out must be 16-byte aligned");
+  if (b->kind == PlanKind::Str) {
+    if (!job.dev_offsets || job.dev_offsets_bytes < b->offsets_bytes) return fail(CDM_E_CAPACITY, "dev_offsets too small");
+  }
+  b->out = job.dev_out;
+  b->offs = job.dev_offsets;
+  b->dev_chunk = static_cast<const uint8_t*>(job.dev_chunk);
+  return CDM_OK;
+}
+
+uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ============================================================================ scratch layout
+struct Alloc {  // bump allocator over one device arena; pass 1 sizes, pass 2 assigns
+  uint8_t* base = nullptr;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+// ============================================================================ device batches
+enum Family { F_FP = 0, F_SCAN = 1, F_RLE = 2, F_LZ4 = 3, F_COPY = 4 };
+
+struct cdm_batch {
+  cdm_engine* e = nullptr;
+  int device = 0;
+  std::vector<Bound> jobs;
+  std::vector<FpBatch> fp;
+  std::vector<uint32_t> fp_maxw;
+  std::vector<ScanBatch> scan;
+  std::vector<InnerBatch> inner;
+  std::vector<RleBatch> rle;
+  std::vector<Lz4Batch> lz4;
+  struct Copy { void* dst; const void* src; size_t bytes; };
+  std::vector<Copy> copies;
+  std::vector<void*> zero_offsets;  // VARBYTES with rows == 0: offsets[0] = 0
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0, zero_bytes = 0;
+  bool own_arena = true;
+  uint32_t* err_dev = nullptr;
+  uint32_t* err_host = nullptr;
+  bool own_err_host = true;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { int fam; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  double fam_ms[5] = {0, 0, 0, 0, 0};
+  uint64_t fam_launches[5] = {0, 0, 0, 0, 0};
+  ~cdm_batch() {
+    if (own_arena && arena) cudaFree(arena);
+    if (own_err_host && err_host) cudaFreeHost(err_host);
+    for (auto ev : ev_pool) cudaEventDestroy(ev);
+  }
+};
+
+namespace {
+
+// Build all launch descriptors for `jobs` over an arena laid out by `A` (pass 1: A.base == nullptr).
+// Returns the arena bytes; `zero_bytes` = prefix of the arena that must start zeroed.
+size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
+  const size_t nj = B->jobs.size();
+  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->inner.clear(); B->rle.clear(); B->lz4.clear();
+  B->copies.clear(); B->zero_offsets.clear();
+  // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
+  B->err_dev = A.take<uint32_t>(nj ? nj : 1);
+  std::vector<int> fpj, scj, rlj, drj, lzj;
+  for (size_t i = 0; i < nj; i++) {
+    const Bound& b = B->jobs[i];
+    switch (b.kind) {
+      case PlanKind::Fp: if (b.rows) fpj.push_back(int(i)); break;
+      case PlanKind::Scan: if (b.rows) scj.push_back(int(i)); break;
+      case PlanKind::Rle:
+        if (b.rows) { rlj.push_back(int(i)); if (b.vmode == V_DRLE) drj.push_back(int(i)); }
+        break;
+      case PlanKind::Str:
+        if (b.rows) scj.push_back(int(i)); else B->zero_offsets.push_back(b.offs);
+        if (b.lz4 && b.payload) lzj.push_back(int(i));
+        if (!b.lz4 && b.payload) B->copies.push_back({b.out, b.dev_chunk + b.bytes_off, size_t(b.payload)});
+        break;
+      case PlanKind::RawCopy:
+        if (b.payload) B->copies.push_back({b.out, b.dev_chunk + b.raw_off, size_t(b.payload)});
+        break;
+    }
+  }
+  auto groups = [](const std::vector<int>& v) {
+    std::vector<std::vector<int>> g;
+    for (size_t i = 0; i < v.size(); i += kMaxBatch)
+      g.emplace_back(v.begin() + i, v.begin() + std::min(v.size(), i + size_t(kMaxBatch)));
+    return g;
+  };
+  // FP
+  for (auto& g : groups(fpj)) {
+    FpBatch fb{};
+    fb.err = B->err_dev;
+    uint32_t tiles = 0, maxw = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      FpDesc& d = fb.d[fb.n++];
+      d.packed = b.dev_chunk + b.main.off;
+      d.dict = b.fp_mode == FP_DICT ? b.dev_chunk + b.dict_off : nullptr;
+      d.out = b.out;
+      d.base = b.main.base;
+      d.n = uint32_t(b.rows);
+      d.entries = b.entries;
+      d.tile0 = tiles;
+      d.err_idx = uint32_t(j);
+      d.w = uint16_t(b.main.w);
+      d.out_bytes = uint16_t(b.W);
+      d.mode = b.fp_mode;
+      d.d = b.d;
+      tiles += uint32_t(div_up(b.rows, kFpTile));
+      maxw = std::max(maxw, b.main.w);
+    }
+    fb.total_tiles = tiles;
+    B->fp.push_back(fb);
+    B->fp_maxw.push_back(maxw);
+  }
+  // scan (delta + VARBYTES offsets)
+  for (auto& g : groups(scj)) {
+    ScanBatch sb{};
+    sb.err = B->err_dev;
+    uint32_t tiles = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      ScanDesc& d = sb.d[sb.n++];
+      d.packed = b.dev_chunk + b.main.off;
+      d.for_base = b.main.base;
+      d.n = uint32_t(b.rows);
+      d.tile0 = tiles;
+      d.ntiles = uint32_t(div_up(b.rows, kScanTile));
+      d.err_idx = uint32_t(j);
+      d.w = uint16_t(b.main.w);
+      if (b.kind == PlanKind::Str) {
+        d.out = b.offs; d.base = b.payload; d.out_bytes = 4; d.mode = SCAN_OFFSETS;
+      } else {
+        d.out = b.out; d.base = b.delta_base; d.out_bytes = uint8_t(b.W); d.mode = SCAN_DELTA;
+      }
+      tiles += d.ntiles;
+    }
+    sb.total_tiles = tiles;
+    sb.ticket = A.take<unsigned long long>(1);
+    sb.flag = A.take<uint32_t>(tiles);
+    B->scan.push_back(sb);
+  }
+  // inner pre-pass
+  for (auto& g : groups(drj)) {
+    InnerBatch ib{};
+    ib.err = B->err_dev;
+    uint32_t tiles = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      InnerDesc& d = ib.d[ib.n++];
+      d.dv_packed = b.dev_chunk + b.inner_dv.off;
+      d.dc_packed = b.dev_chunk + b.inner_dc.off;
+      d.dv_base = b.inner_dv.base;
+      d.dc_base = b.inner_dc.base;
+      d.dv_w = uint16_t(b.inner_dv.w);
+      d.dc_w = uint16_t(b.inner_dc.w);
+      d.base = b.inner_base;
+      d.n_inner = b.n_inner;
+      d.n_outer = b.nruns;
+      d.tile0 = tiles;
+      d.ntiles = uint32_t(div_up(b.n_inner, kRleTile));
+      d.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
+      d.err_idx = uint32_t(j);
+      tiles += d.ntiles;
+    }
+    ib.total_tiles = tiles;
+    ib.ticket = A.take<unsigned long long>(1);
+    ib.flag = A.take<uint32_t>(tiles);
+    B->inner.push_back(ib);
+  }
+  // rle
+  for (auto& g : groups(rlj)) {
+    RleBatch rb{};
+    rb.err = B->err_dev;
+    uint32_t tiles = 0, slots = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      RleDesc& d = rb.d[rb.n++];
+      d.cnt_packed = b.dev_chunk + b.counts.off;
+      d.cnt_base = b.counts.base;
+      d.cnt_w = uint16_t(b.counts.w);
+      d.val_packed = b.vmode == V_DRLE ? nullptr : b.dev_chunk + b.main.off;
+      d.val_base = b.main.base;
+      d.val_w = uint16_t(b.main.w);
+      d.dict = b.vmode == V_DICT ? b.dev_chunk + b.dict_off : nullptr;
+      d.entries = b.entries;
+      d.d = b.d;
+      d.vmode = b.vmode;
+      d.out = b.out;
+      d.out_bytes = uint8_t(b.W);
+      d.delta_base = b.delta_base;
+      d.n = uint32_t(b.rows);
+      d.nruns = b.nruns;
+      d.n_inner = b.n_inner;
+      d.tile0 = tiles;
+      d.ntiles = uint32_t(div_up(b.nruns, kRleTile));
+      d.err_idx = uint32_t(j);
+      tiles += d.ntiles;
+      slots += uint32_t(b.rows / kRleBigLimit) + 1;
+    }
+    rb.total_tiles = tiles;
+    rb.ticket = A.take<unsigned long long>(1);
+    rb.flag = A.take<uint32_t>(tiles);
+    rb.big.counter = A.take<unsigned long long>(1);
+    rb.big.done = A.take<uint32_t>(1);
+    rb.big.max_slots = slots;
+    B->rle.push_back(rb);
+  }
+  *zero_bytes = A.off;
+  // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
+  for (auto& sb : B->scan) { sb.agg = A.take<uint64_t>(sb.total_tiles); sb.inc = A.take<uint64_t>(sb.total_tiles); }
+  for (auto& ib : B->inner) {
+    ib.agg0 = A.take<uint64_t>(ib.total_tiles); ib.agg1 = A.take<uint64_t>(ib.total_tiles);
+    ib.inc0 = A.take<uint64_t>(ib.total_tiles); ib.inc1 = A.take<uint64_t>(ib.total_tiles);
+  }
+  std::map<int, InnerDesc*> inner_of;
+  for (auto& ib : B->inner)
+    for (uint32_t k = 0; k < ib.n; k++) {
+      InnerDesc& d = ib.d[k];
+      d.S = A.take<uint32_t>(d.n_inner);
+      d.Q = A.take<uint64_t>(d.n_inner);
+      d.DV = A.take<uint64_t>(d.n_inner);
+      d.tstart = A.take<uint32_t>(d.outer_tiles);
+      inner_of[int(d.err_idx)] = &d;
+    }
+  for (auto& rb : B->rle) {
+    rb.agg0 = A.take<uint64_t>(rb.total_tiles); rb.agg1 = A.take<uint64_t>(rb.total_tiles);
+    rb.inc0 = A.take<uint64_t>(rb.total_tiles); rb.inc1 = A.take<uint64_t>(rb.total_tiles);
+    rb.big.entries = A.take<RleBig::Entry>(rb.big.max_slots);
+    rb.big.soffs = A.take<uint32_t>(size_t(rb.big.max_slots) * (kRleTile + 1));
+    rb.big.vals = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
+    rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
+    for (uint32_t k = 0; k < rb.n; k++) {
+      RleDesc& d = rb.d[k];
+      if (d.vmode == V_DRLE) {
+        InnerDesc* in = inner_of[int(d.err_idx)];
+        d.S = in->S; d.Q = in->Q; d.DV = in->DV; d.tstart = in->tstart;
+      }
+    }
+  }
+  // LZ4
+  for (auto& g : groups(lzj)) {
+    Lz4Batch lb{};
+    lb.err = B->err_dev;
+    uint32_t subs = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      Lz4Desc& d = lb.d[lb.n++];
+      d.payload = b.dev_chunk + b.lz_pay_off;
+      d.table = b.dev_chunk + b.lz_tab_off;
+      d.out = static_cast<uint8_t*>(b.out);
+      d.payload_bytes = b.lz_pay_bytes;
+      d.n = b.payload;
+      d.n_sub = b.n_sub;
+      d.sub0 = subs;
+      d.err_idx = uint32_t(j);
+      subs += b.n_sub;
+    }
+    lb.total_subs = subs;
+    B->lz4.push_back(lb);
+  }
+  return A.off + 256;
+}
+
+cdm_status batch_build(cdm_batch* B, uint8_t* external_arena, size_t external_bytes) {
+  Alloc pass1;
+  size_t zb = 0;
+  size_t bytes = layout_batch(B, pass1, &zb);
+  if (external_arena) {
+    if (bytes > external_bytes) return fail(CDM_E_CAPACITY, "scratch arena too small");
+    B->arena = external_arena;
+    B->own_arena = false;
+  } else {
+    cudaError_t ce = cudaMalloc(&B->arena, bytes);
+    if (ce != cudaSuccess) return fail(CDM_E_OOM, std::string("scratch cudaMalloc: ") + cudaGetErrorString(ce));
+    CUDA_TRY(cudaMemset(B->arena, 0, zb));
+  }
+  B->arena_bytes = bytes;
+  B->zero_bytes = zb;
+  Alloc pass2;
+  pass2.base = B->arena;
+  layout_batch(B, pass2, &zb);
+  return CDM_OK;
+}
+
+cudaEvent_t ev_get(cdm_batch* B, size_t k) {
+  while (B->ev_pool.size() <= k) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    B->ev_pool.push_back(e);
+  }
+  return B->ev_pool[k];
+}
+
+cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
+  uint32_t n = 0;
+  size_t evk = B->pending.size() * 2;
+  auto t0 = [&](int fam, bool any) -> cudaEvent_t {
+    if (!B->timing || !any) return nullptr;
+    cudaEvent_t a = ev_get(B, evk++);
+    cudaEventRecord(a, s);
+    (void)fam;
+    return a;
+  };
+  auto t1 = [&](int fam, cudaEvent_t a) {
+    if (!a) return;
+    cudaEvent_t b = ev_get(B, evk++);
+    cudaEventRecord(b, s);
+    B->pending.push_back({fam, a, b});
+  };
+  CUDA_TRY(cudaMemsetAsync(B->err_dev, 0, sizeof(uint32_t) * std::max<size_t>(1, B->jobs.size()), s));
+  cudaEvent_t a = t0(F_FP, !B->fp.empty());
+  for (size_t i = 0; i < B->fp.size(); i++) { CUDA_TRY(launch_fp(B->fp[i], B->fp_maxw[i], s)); n++; B->fam_launches[F_FP]++; }
+  t1(F_FP, a);
+  a = t0(F_SCAN, !B->scan.empty());
+  for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, s)); n++; B->fam_launches[F_SCAN]++; }
+  t1(F_SCAN, a);
+  a = t0(F_RLE, !B->rle.empty());
+  for (auto& ib : B->inner) { CUDA_TRY(launch_inner(ib, s)); n++; B->fam_launches[F_RLE]++; }
+  for (auto& rb : B->rle) {
+    CUDA_TRY(launch_rle(rb, s));
+    CUDA_TRY(launch_rle_big(rb, s));
+    n += 2;
+    B->fam_launches[F_RLE] += 2;
+  }
+  t1(F_RLE, a);
+  a = t0(F_LZ4, !B->lz4.empty());
+  for (auto& lb : B->lz4) { CUDA_TRY(launch_lz4(lb, s)); n++; B->fam_launches[F_LZ4]++; }
+  t1(F_LZ4, a);
+  a = t0(F_COPY, !B->copies.empty() || !B->zero_offsets.empty());
+  for (auto& c : B->copies) { CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, s)); B->fam_launches[F_COPY]++; }
+  for (void* p : B->zero_offsets) CUDA_TRY(cudaMemsetAsync(p, 0, 4, s));
+  t1(F_COPY, a);
+  if (nl) *nl = n;
+  return CDM_OK;
+}
+
+void fill_results(const cdm_batch* B, const uint32_t* errw, cdm_result* res) {
+  for (size_t i = 0; i < B->jobs.size(); i++) {
+    const Bound& b = B->jobs[i];
+    cdm_result& r = res[i];
+    r.rows = b.rows;
+    r.payload_bytes = b.payload;
+    r.offsets_bytes = b.offsets_bytes;
+    r.compressed_bytes = b.total;
+    r.chunk_id = b.chunk_id;
+    r.error_bits = errw[i];
+    r.status = errw[i] ? CDM_E_CORRUPT : CDM_OK;
+  }
+}
+
+}  // namespace
+
+// ============================================================================ engine
+struct cdm_engine {
+  int device = 0;
+  cudaStream_t copy = nullptr, decode = nullptr;
+  bool own_copy = false, own_decode = false;
+  cdm_engine_opts opts{};
+  struct Slot {
+    uint8_t* dev = nullptr;
+    cudaEvent_t copied = nullptr, freed = nullptr;
+    bool used = false;
+    uint8_t* arena = nullptr;  // per-slot decode scratch (chunks decode one at a time per slot)
+    size_t arena_bytes = 0;
+  };
+  std::vector<Slot> slots;
+  uint32_t next_slot = 0;
+  struct Ticket {
+    cdm_result res{};
+    cudaEvent_t done = nullptr;
+    uint32_t slot = 0;
+    uint32_t err_pos = 0;
+    bool harvested = false;
+    std::unique_ptr<cdm_batch> batch;
+  };
+  std::map<uint64_t, Ticket> tickets;
+  std::map<uint32_t, uint64_t> slot_ticket;  // slot -> last ticket decoded in it
+  uint64_t next_ticket = 1;
+  uint32_t* err_host = nullptr;  // pinned ring of per-ticket error words
+  uint32_t err_ring = 0;
+  std::map<uint32_t, uint64_t> err_owner;  // ring position -> ticket whose word lives there
+};
+
+static cdm_status harvest(cdm_engine* e, cdm_engine::Ticket& t) {
+  if (t.harvested) return CDM_OK;
+  CUDA_TRY(cudaEventSynchronize(t.done));
+  uint32_t w = e->err_host[t.err_pos];
+  t.res.error_bits = w;
+  t.res.status = w ? CDM_E_CORRUPT : CDM_OK;
+  t.harvested = true;
+  t.batch.reset();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opts* opts, cdm_engine** out) {
+  if (!out) return fail(CDM_E_INVALID_ARG, "null out");
+  auto e = std::make_unique<cdm_engine>();
+  e->device = device;
+  cdm_engine_opts o{};
+  if (opts) o = *opts;
+  if (o.n_slots == 0) o.n_slots = 4;
+  if (o.n_slots < 2) return fail(CDM_E_INVALID_ARG, "n_slots must be >= 2");
+  if (o.slot_bytes == 0) o.slot_bytes = 64ull << 20;
+  if (o.pcie_gbps <= 0) o.pcie_gbps = 55.0;
+  if (o.decode_gbps <= 0) o.decode_gbps = 3000.0;
+  e->opts = o;
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaFree(nullptr));  // create the context
+  if (o.copy_stream) e->copy = static_cast<cudaStream_t>(o.copy_stream);
+  else { CUDA_TRY(cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking)); e->own_copy = true; }
+  if (o.decode_stream) e->decode = static_cast<cudaStream_t>(o.decode_stream);
+  else { CUDA_TRY(cudaStreamCreateWithFlags(&e->decode, cudaStreamNonBlocking)); e->own_decode = true; }
+  e->slots.resize(o.n_slots);
+  for (auto& s : e->slots) {
+    if (cudaMalloc(&s.dev, o.slot_bytes) != cudaSuccess) return fail(CDM_E_OOM, "staging slot cudaMalloc failed");
+    CUDA_TRY(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
+  }
+  e->err_ring = 1024;
+  CUDA_TRY(cudaHostAlloc(&e->err_host, sizeof(uint32_t) * e->err_ring, cudaHostAllocDefault));
+  *out = e.release();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_engine_destroy(cdm_engine* e) {
+  if (!e) return CDM_OK;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->copy);
+  cudaStreamSynchronize(e->decode);
+  for (auto& kv : e->tickets) if (kv.second.done) cudaEventDestroy(kv.second.done);
+  e->tickets.clear();
+  for (auto& s : e->slots) {
+    cudaFree(s.dev);
+    cudaFree(s.arena);
+    cudaEventDestroy(s.copied);
+    cudaEventDestroy(s.freed);
+  }
+  if (e->err_host) cudaFreeHost(e->err_host);
+  if (e->own_copy) cudaStreamDestroy(e->copy);
+  if (e->own_decode) cudaStreamDestroy(e->decode);
+  delete e;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_chunk_info(const void* host_chunk, size_t bytes, cdm_result* out) {
+  if (!out) return fail(CDM_E_INVALID_ARG, "null out");
+  Chunk c;
+  std::string e = parse_chunk(host_chunk, bytes, &c);
+  if (!e.empty()) return fail(CDM_E_CORRUPT, e);
+  std::memset(out, 0, sizeof *out);
+  out->rows = c.rows;
+  out->payload_bytes = c.payload_bytes;
+  out->offsets_bytes = c.offsets_bytes;
+  out->compressed_bytes = c.total_bytes;
+  out->chunk_id = c.chunk_id;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_chunk_check(const cdm_cascade* c, const void* host_chunk, size_t bytes) {
+  if (!c || !host_chunk) return fail(CDM_E_INVALID_ARG, "null argument");
+  cdm_job job{};
+  job.cascade = c;
+  job.host_chunk = host_chunk;
+  job.chunk_bytes = bytes;
+  job.dev_out_bytes = SIZE_MAX;
+  Bound b;
+  return bind_job(job, &b);
+}
+
+static cdm_status submit_one(cdm_engine* e, const cdm_job& job, uint64_t* ticket) {
+  Bound b;
+  cdm_status st = bind_job(job, &b);
+  if (st) return st;
+  if (b.total > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "chunk larger than a staging slot");
+  const uint32_t si = e->next_slot;
+  e->next_slot = (e->next_slot + 1) % uint32_t(e->slots.size());
+  cdm_engine::Slot& s = e->slots[si];
+  // the slot's previous chunk must be decoded before its bytes are overwritten: the copy stream waits
+  // on the slot's `freed` event (no host stall)
+  if (s.used) CUDA_TRY(cudaStreamWaitEvent(e->copy, s.freed, 0));
+  const uint64_t id = e->next_ticket++;
+  const uint32_t pos = uint32_t(id % e->err_ring);
+  {  // the pinned error word at `pos` may still belong to an unharvested ticket
+    auto ow = e->err_owner.find(pos);
+    if (ow != e->err_owner.end()) {
+      auto t = e->tickets.find(ow->second);
+      if (t != e->tickets.end()) { st = harvest(e, t->second); if (st) return st; }
+    }
+    e->err_owner[pos] = id;
+  }
+  // H4: PCIe H2D copy of the compressed chunk on the copy stream
+  CUDA_TRY(cudaMemcpyAsync(s.dev, job.host_chunk, b.total, cudaMemcpyHostToDevice, e->copy));
+  CUDA_TRY(cudaEventRecord(s.copied, e->copy));
+  CUDA_TRY(cudaStreamWaitEvent(e->decode, s.copied, 0));
+  // decode from the slot with the slot's own scratch arena
+  auto batch = std::make_unique<cdm_batch>();
+  batch->e = e;
+  batch->device = e->device;
+  b.dev_chunk = s.dev;
+  batch->jobs.push_back(b);
+  Alloc sizing;
+  size_t zb = 0;
+  size_t need = layout_batch(batch.get(), sizing, &zb);
+  if (need > s.arena_bytes) {
+    if (s.arena) { CUDA_TRY(cudaStreamSynchronize(e->decode)); cudaFree(s.arena); s.arena = nullptr; }
+    size_t cap = std::max(need, size_t(1) << 20);
+    if (cudaMalloc(&s.arena, cap) != cudaSuccess) return fail(CDM_E_OOM, "scratch cudaMalloc failed");
+    s.arena_bytes = cap;
+  }
+  st = batch_build(batch.get(), s.arena, s.arena_bytes);
+  if (st) return st;
+  CUDA_TRY(cudaMemsetAsync(s.arena, 0, batch->zero_bytes, e->decode));  // fresh tickets/flags per chunk
+  uint32_t nl = 0;
+  st = batch_enqueue(batch.get(), e->decode, &nl);
+  if (st) return st;
+  CUDA_TRY(cudaMemcpyAsync(e->err_host + pos, batch->err_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, e->decode));
+  CUDA_TRY(cudaEventRecord(s.freed, e->decode));
+  s.used = true;
+  cdm_engine::Ticket& t = e->tickets[id];
+  CUDA_TRY(cudaEventCreateWithFlags(&t.done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(t.done, e->decode));
+  t.slot = si;
+  t.err_pos = pos;
+  t.res.rows = b.rows;
+  t.res.payload_bytes = b.payload;
+  t.res.offsets_bytes = b.offsets_bytes;
+  t.res.compressed_bytes = b.total;
+  t.res.chunk_id = b.chunk_id;
+  t.batch = std::move(batch);
+  e->slot_ticket[si] = id;
+  *ticket = id;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_submit(cdm_engine* e, const cdm_job* job, uint64_t* ticket) {
+  if (!e || !job || !ticket) return fail(CDM_E_INVALID_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  return submit_one(e, *job, ticket);
+}
+
+// H3: Johnson's rule on (t_i = compressed / PCIe, d_i = decoded / decode rate):
+// jobs with t <= d first ascending t, then the rest descending d; ties by submission index.
+static void johnson(const double* tt, const double* dd, size_t n, std::vector<size_t>* order) {
+  std::vector<size_t> first, second;
+  for (size_t i = 0; i < n; i++) (tt[i] <= dd[i] ? first : second).push_back(i);
+  std::stable_sort(first.begin(), first.end(), [&](size_t a, size_t b) { return tt[a] < tt[b]; });
+  std::stable_sort(second.begin(), second.end(), [&](size_t a, size_t b) { return dd[a] > dd[b]; });
+  *order = first;
+  order->insert(order->end(), second.begin(), second.end());
+}
+
+extern "C" CDM_API cdm_status cdm_johnson_order(const double* t, const double* d, size_t n, size_t* order) {
+  if (n && (!t || !d || !order)) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::vector<size_t> o;
+  johnson(t, d, n, &o);
+  for (size_t i = 0; i < n; i++) order[i] = o[i];
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* jobs, size_t n, uint64_t* tickets) {
+  if (!e || (n && (!jobs || !tickets))) return fail(CDM_E_INVALID_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  std::vector<size_t> order(n);
+  std::iota(order.begin(), order.end(), size_t(0));
+  if (e->opts.order_policy == 1) {
+    std::vector<double> tt(n), dd(n);
+    for (size_t i = 0; i < n; i++) {
+      cdm_result info{};
+      cdm_status st = cdm_chunk_info(jobs[i].host_chunk, jobs[i].chunk_bytes, &info);
+      if (st) return st;
+      tt[i] = double(info.compressed_bytes) / (e->opts.pcie_gbps * 1e9);
+      dd[i] = double(info.payload_bytes + info.offsets_bytes) / (e->opts.decode_gbps * 1e9);
+    }
+    johnson(tt.data(), dd.data(), n, &order);
+  }
+  for (size_t k = 0; k < n; k++) {
+    cdm_status st = submit_one(e, jobs[order[k]], &tickets[order[k]]);
+    if (st) return st;
+  }
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_wait(cdm_engine* e, uint64_t ticket, cdm_result* out) {
+  if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
+  auto it = e->tickets.find(ticket);
+  if (it == e->tickets.end()) return fail(CDM_E_BUSY, "unknown or consumed ticket");
+  cdm_status st = harvest(e, it->second);
+  if (st) return st;
+  if (out) *out = it->second.res;
+  cdm_status r = it->second.res.error_bits ? CDM_E_CORRUPT : CDM_OK;
+  if (r) g_last = "chunk " + std::to_string(it->second.res.chunk_id) + ": device error bits " + std::to_string(it->second.res.error_bits);
+  cudaEventDestroy(it->second.done);
+  e->tickets.erase(it);
+  return r;
+}
+
+extern "C" CDM_API cdm_status cdm_synchronize(cdm_engine* e) {
+  if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
+  CUDA_TRY(cudaStreamSynchronize(e->copy));
+  CUDA_TRY(cudaStreamSynchronize(e->decode));
+  for (auto& kv : e->tickets) {
+    cdm_status st = harvest(e, kv.second);
+    if (st) return st;
+  }
+  return CDM_OK;
+}
+
+// ============================================================================ device batch API
+extern "C" CDM_API cdm_status cdm_batch_create(cdm_engine* e, const cdm_job* jobs, size_t n, cdm_batch** out) {
+  if (!e || !out || (n && !jobs)) return fail(CDM_E_INVALID_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  auto B = std::make_unique<cdm_batch>();
+  B->e = e;
+  B->device = e->device;
+  for (size_t i = 0; i < n; i++) {
+    if (!jobs[i].dev_chunk) return fail(CDM_E_INVALID_ARG, "job " + std::to_string(i) + ": dev_chunk is null");
+    if (reinterpret_cast<uintptr_t>(jobs[i].dev_chunk) % 16) return fail(CDM_E_INVALID_ARG, "dev_chunk must be 16-byte aligned");
+    Bound b;
+    cdm_status st = bind_job(jobs[i], &b);
+    if (st) { g_last = "job " + std::to_string(i) + ": " + g_last; return st; }
+    B->jobs.push_back(b);
+  }
+  cdm_status st = batch_build(B.get(), nullptr, 0);
+  if (st) return st;
+  CUDA_TRY(cudaHostAlloc(&B->err_host, sizeof(uint32_t) * std::max<size_t>(1, n), cudaHostAllocDefault));
+  *out = B.release();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_launch(cdm_batch* b, void* stream, uint32_t* n_launches) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  CUDA_TRY(cudaSetDevice(b->device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : b->e->decode;
+  return batch_enqueue(b, s, n_launches);
+}
+
+extern "C" CDM_API cdm_status cdm_batch_results(cdm_batch* b, void* stream, cdm_result* results) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  CUDA_TRY(cudaSetDevice(b->device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : b->e->decode;
+  CUDA_TRY(cudaMemcpyAsync(b->err_host, b->err_dev, sizeof(uint32_t) * std::max<size_t>(1, b->jobs.size()),
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto& p : b->pending) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+    b->fam_ms[p.fam] += ms;
+  }
+  b->pending.clear();
+  if (results) fill_results(b, b->err_host, results);
+  for (size_t i = 0; i < b->jobs.size(); i++)
+    if (b->err_host[i]) {
+      g_last = "job " + std::to_string(i) + ": device error bits " + std::to_string(b->err_host[i]);
+      return CDM_E_CORRUPT;
+    }
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_destroy(cdm_batch* b) {
+  if (!b) return CDM_OK;
+  cudaSetDevice(b->device);
+  delete b;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_set_timing(cdm_batch* b, int enable) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  b->timing = enable != 0;
+  for (int i = 0; i < 5; i++) { b->fam_ms[i] = 0; b->fam_launches[i] = 0; }
+  b->pending.clear();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch* b, double* ms5, uint64_t* launches5) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  for (int i = 0; i < 5; i++) {
+    if (ms5) ms5[i] = b->fam_ms[i];
+    if (launches5) launches5[i] = b->fam_launches[i];
+  }
+  return CDM_OK;
+}

@@ -1,0 +1,383 @@
+"""GPU parity: the CUDA path (through the C-ABI) == the CPU oracle, element by element (-m gpu).
+
+Every chunk is decoded twice on the device -- through the pipelined engine from pinned host memory
+(cdm_submit_batch) and through the device-resident batch API (cdm_batch_*) -- and compared byte for byte
+with oracle/ on the same seeded inputs.  Integer/byte work must be bit-exact and Float2Int is one IEEE
+division on both sides, so the tolerance is zero everywhere.  Outputs are pre-filled
+with a sentinel so an element that is never written, or written outside [0, n), is caught.
+"""
+import struct
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import cdm1
+import oracle
+from paper_2602_08190_b200 import cdm, encoder
+from paper_2602_08190_b200.inputs import (TPCH, Column, I32, I64, config1_column, rle_column,
+                                          uniform_bits_column)
+
+pytestmark = pytest.mark.gpu
+
+SENTINEL = 0xA5
+
+
+@pytest.fixture(scope="module")
+def engine():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    e = cdm.Engine(0, n_slots=3, slot_bytes=256 << 20)
+    yield e
+    e.close()
+
+
+def _outputs(chunk):
+    info = cdm.chunk_info(chunk)
+    out = torch.full((max(16, (info["payload_bytes"] + 15) // 16 * 16 + 64),), SENTINEL, dtype=torch.uint8,
+                     device="cuda")
+    offs = None
+    if info["offsets_bytes"]:
+        offs = torch.full((info["offsets_bytes"] // 4 + 4,), -7, dtype=torch.int32, device="cuda")
+    return out, offs, info
+
+
+def gpu_decode(engine, casc, chunks, resident=False, expect_error=False):
+    """Decode chunks on the GPU; returns [(payload numpy, offsets numpy|None, result dict)]."""
+    decs, bufs = [], []
+    for ch in chunks:
+        out, offs, info = _outputs(ch)
+        d = cdm.Decode(casc, cdm.pinned(ch), out, offs)
+        if resident:
+            d.dev_chunk = torch.from_numpy(ch).cuda()
+        decs.append(d)
+        bufs.append((out, offs, info))
+    if resident:
+        b = cdm.Batch(engine, decs)
+        b.launch()
+        res = b.results(raise_on_error=not expect_error)
+        b.close()
+    else:
+        tickets = engine.submit_batch(decs)
+        res = [engine.wait(t, raise_on_error=not expect_error) for t in tickets]
+    torch.cuda.synchronize()
+    outs = []
+    for (out, offs, info), r in zip(bufs, res):
+        o = out.cpu().numpy()
+        p = info["payload_bytes"]
+        # nothing written past the payload
+        if not expect_error:
+            assert np.all(o[p:] == SENTINEL), "write beyond the payload"
+        outs.append((o[:p], None if offs is None else offs.cpu().numpy(), r))
+    return outs
+
+
+def check_parity(engine, spec, col_or_chunks, dtype=None, width=0, rows_per_chunk=None, both=True):
+    if isinstance(col_or_chunks, Column):
+        col = col_or_chunks
+        chunks = encoder.encode_chunks(spec, col, rows_per_chunk or max(col.rows, 1))
+        dtype, width = col.dtype, col.width
+    else:
+        chunks = col_or_chunks
+    casc = cdm.Cascade(spec, dtype, width)
+    modes = [False, True] if both else [True]
+    for resident in modes:
+        got = gpu_decode(engine, casc, chunks, resident=resident)
+        for ch, (payload, offs, r) in zip(chunks, got):
+            exp, exp_offs = oracle.decode_chunk(ch)
+            assert r["error_bits"] == 0
+            assert payload.size == exp.size
+            if not np.array_equal(payload, exp):
+                bad = int(np.flatnonzero(payload != exp)[0])
+                raise AssertionError(f"{spec} resident={resident}: first mismatch at byte {bad} "
+                                     f"(got {payload[bad]}, oracle {exp[bad]})")
+            if exp_offs is not None:
+                assert np.array_equal(offs[: exp_offs.size], exp_offs), f"{spec}: offsets differ"
+    return chunks
+
+
+# ------------------------------------------------------------------------------ TPC-H columns, all cascades
+TPCH_CASES = [
+    ("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"),
+    ("l_orderkey", "Delta|RLE|[BitPack,BitPack]"),
+    ("l_orderkey", "Delta|BitPack"),
+    ("l_orderkey", "BitPack"),
+    ("l_partkey", "BitPack"),
+    ("l_suppkey", "BitPack"),
+    ("l_linenumber", "BitPack"),
+    ("l_quantity", "Dict|BitPack"),
+    ("l_discount", "Dict|BitPack"),
+    ("l_tax", "Float2Int|BitPack"),
+    ("l_extendedprice", "Float2Int|BitPack"),
+    ("l_returnflag", "Dict|BitPack"),
+    ("l_linestatus", "Dict|BitPack"),
+    ("l_shipdate", "Dict|BitPack"),
+    ("l_shipinstruct", "Dict|BitPack"),
+    ("l_shipmode", "Dict|BitPack"),
+    ("l_comment", "Str|[LZ4,BitPack]"),
+    ("l_comment", "Str|[Raw,BitPack]"),
+    ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"),
+    ("o_custkey", "BitPack"),
+    ("o_orderstatus", "Dict|BitPack"),
+    ("o_totalprice", "Float2Int|BitPack"),
+    ("o_orderdate", "RLE|[Dict|BitPack,BitPack]"),
+    ("o_orderpriority", "Dict|BitPack"),
+    ("o_clerk", "Dict|BitPack"),
+    ("o_shippriority", "RLE|[BitPack,BitPack]"),
+    ("o_comment", "Str|[LZ4,BitPack]"),
+    ("o_totalprice", "RLE|[Float2Int|BitPack,BitPack]"),
+    ("l_orderkey", "Raw"),
+]
+
+
+@pytest.mark.parametrize("name,spec", TPCH_CASES)
+def test_tpch_columns(engine, name, spec):
+    col = TPCH(0.02).column(name)  # 120k lineitem rows: several tiles per chunk and a ragged tail
+    check_parity(engine, spec, col, rows_per_chunk=50_001)
+
+
+# ------------------------------------------------------------------------------ golden vectors on the GPU
+def test_golden_vectors_gpu(engine, golden):
+    g = golden("orderkey_nested.json")
+    iv, ic, oc = g["bitpack_inner_values"], g["bitpack_inner_counts"], g["bitpack_outer_counts"]
+    inner = cdm1.Node(cdm1.RLE, 10, [
+        cdm1.Node(cdm1.BITPACK, 4, [cdm1.raw(bytes.fromhex(iv["bytes"]))], w=iv["w"], base=iv["for"]),
+        cdm1.Node(cdm1.BITPACK, 4, [cdm1.raw(bytes.fromhex(ic["bytes"]))], w=ic["w"], base=ic["for"])],
+        nruns=4, maxrun=7)
+    root = cdm1.Node(cdm1.RLE, 20, [
+        cdm1.Node(cdm1.DELTA, 10, [inner], base=g["delta_base"]),
+        cdm1.Node(cdm1.BITPACK, 10, [cdm1.raw(bytes.fromhex(oc["bytes"]))], w=oc["w"], base=oc["for"])],
+        nruns=10, maxrun=4)
+    spec = g["cascade"]
+    h = _hash(spec)
+    ch = cdm1.build(root, cdm1.I64, 8, 20, cascade_hash=h)
+    casc = cdm.Cascade(spec, cdm.I64)
+    (payload, _, r), = gpu_decode(engine, casc, [ch], resident=True)
+    assert payload.view(np.int64).tolist() == g["column"]
+
+    s = golden("spec_bitpack.json")
+    ch = cdm1.build(cdm1.Node(cdm1.BITPACK, 4, [cdm1.raw(bytes.fromhex(s["bitpack"]["bytes"]))], w=3, base=3),
+                    cdm1.I32, 4, 4, cascade_hash=_hash("BitPack"))
+    (payload, _, r), = gpu_decode(engine, cdm.Cascade("BitPack", cdm.I32), [ch], resident=True)
+    assert payload.view(np.int32).tolist() == s["column"]
+
+
+def _hash(spec):
+    h = 14695981039346656037
+    for b in encoder.canonical(spec).encode():
+        h = ((h ^ b) * 1099511628211) & ((1 << 64) - 1)
+    return h
+
+
+# ------------------------------------------------------------------------------ bit widths / tile edges
+@pytest.mark.parametrize("w", list(range(0, 65)))
+def test_bitpack_every_width_tile_edges(engine, w):
+    n = 3 * 4096 + 77
+    col = uniform_bits_column(n, w, I64)
+    chunks = [encoder.encode("BitPack", Column("x", I64, 8, m, col.data[:m])) for m in (1, 4095, 4096, 4097, n)]
+    check_parity(engine, "BitPack", chunks, I64, both=False)
+    if w <= 32:
+        c32 = uniform_bits_column(n, w, I32)
+        check_parity(engine, "BitPack", [encoder.encode("BitPack", c32)], I32, both=False)
+
+
+def test_config1_parity(engine):
+    check_parity(engine, "BitPack", config1_column())
+
+
+@pytest.mark.parametrize("w", [1, 3, 8, 17, 33, 64])
+def test_delta_scan_many_tiles(engine, w):
+    rng = np.random.default_rng(w)
+    n = 300_000
+    d = rng.integers(0, 1 << min(w, 62), size=n, dtype=np.uint64).astype(np.int64)
+    col = Column("walk", I64, 8, n, np.cumsum(d))
+    check_parity(engine, "Delta|BitPack", col, rows_per_chunk=123_457)
+    col32 = Column("walk32", I32, 4, n, np.cumsum(d).astype(np.int32))
+    check_parity(engine, "Delta|BitPack", col32, rows_per_chunk=200_000)
+
+
+# ------------------------------------------------------------------------------ RLE distributions
+RLE_DISTS = ["even-1", "even-2", "even-4", "even-64", "even-1024", "random-1-8", "random-1-1000",
+             "outlier-1024-1", "outlier-100000-0.01", "mixed-even-2+random-1-64", "mixed-outlier-1024-1+even-8",
+             "single"]
+
+
+@pytest.mark.parametrize("dist", RLE_DISTS)
+def test_rle_distributions(engine, dist):
+    col = rle_column(dist, 1_000_003, I64)
+    check_parity(engine, "RLE|[BitPack,BitPack]", col, rows_per_chunk=600_000)
+    col32 = rle_column(dist, 400_000, I32)
+    check_parity(engine, "RLE|[BitPack,BitPack]", col32, both=False)
+
+
+def test_giant_runs(engine):
+    # o_shippriority-like: one run per chunk and runs far above the big-tile limit
+    n = 5_000_000
+    col = Column("zeros", I32, 4, n, np.zeros(n, dtype=np.int32))
+    check_parity(engine, "RLE|[BitPack,BitPack]", col, rows_per_chunk=4_194_304, both=False)
+    counts = np.array([3, 2_000_000, 1, 1, 70_000, 5, 999_999], dtype=np.int64)
+    vals = np.arange(len(counts), dtype=np.int64) * 7 + 1
+    col = Column("big", I64, 8, int(counts.sum()), np.repeat(vals, counts))
+    check_parity(engine, "RLE|[BitPack,BitPack]", col, both=False)
+    check_parity(engine, "Delta|RLE|[BitPack,BitPack]", col, both=False)
+
+
+def test_rle_zero_length_runs(engine):
+    """Foreign encoders may emit zero-length runs; the decoder must skip them (decode parity only)."""
+    rng = np.random.default_rng(12)
+    nr = 5000
+    counts = rng.integers(0, 4, size=nr)
+    counts[100:200] = 0
+    vals = rng.integers(0, 1 << 20, size=nr)
+    n = int(counts.sum())
+    spec = "RLE|[BitPack,BitPack]"
+    root = cdm1.Node(cdm1.RLE, n, [cdm1.bitpack(vals, 20, 0), cdm1.bitpack(counts, 2, 0)], nruns=nr, maxrun=3)
+    ch = cdm1.build(root, cdm1.I64, 8, n, cascade_hash=_hash(spec))
+    check_parity(engine, spec, [ch], I64)
+
+
+def test_nested_orderkey_sf1_full(engine):
+    """Config 2's l_orderkey at full SF=1 size, every element against the oracle."""
+    col = TPCH(1).column("l_orderkey")
+    check_parity(engine, "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", col, rows_per_chunk=1 << 22)
+
+
+def test_config2_full(engine):
+    g = TPCH(1)
+    for name in ("l_quantity", "l_discount"):
+        check_parity(engine, "Dict|BitPack", g.column(name), rows_per_chunk=1 << 22, both=False)
+
+
+# ------------------------------------------------------------------------------ LZ4
+@pytest.mark.parametrize("sub", [4096, 65536, 1 << 20])
+def test_lz4_subchunk_sizes(engine, sub):
+    col = TPCH(0.01).column("l_comment")
+    check_parity(engine, f"Str|[LZ4(sub={sub}),BitPack]", col, rows_per_chunk=40_000, both=False)
+
+
+def test_lz4_overlapping_matches(engine):
+    from test_oracle_pins import _seq
+    blocks, sizes = [], []
+    for off, mlen in [(1, 4), (1, 300), (2, 19), (3, 1000), (5, 5), (7, 270), (31, 100), (32, 100), (33, 700)]:
+        lit = bytes(range(65, 65 + off + 2))
+        blocks.append(_seq(lit, off, mlen) + _seq(b"END", None, None))
+        sizes.append(len(lit) + mlen + 3)
+    payload = b"".join(blocks)
+    tab = b""
+    pos = 0
+    for blk, dl in zip(blocks, sizes):
+        tab += struct.pack("<III", pos, len(blk), dl)
+        pos += len(blk)
+    n = sum(sizes)
+    lens = [n // 2, n - n // 2]
+    spec = "Str|[LZ4,BitPack]"
+    root = cdm1.Node(cdm1.STR, 2, [
+        cdm1.Node(cdm1.LZ4, n, [cdm1.raw(payload), cdm1.raw(tab, eb=12)], nsub=len(blocks), sub=1 << 16),
+        cdm1.bitpack(lens, 16, 0)])
+    ch = cdm1.build(root, cdm1.VARBYTES, 1, 2, payload=n, cascade_hash=_hash(spec))
+    check_parity(engine, spec, [ch], cdm.VARBYTES)
+
+
+# ------------------------------------------------------------------------------ edge cases + corrupt data
+def test_empty_and_tiny(engine):
+    for n in (0, 1, 2, 31, 33):
+        col = config1_column(n)
+        check_parity(engine, "BitPack", col)
+        check_parity(engine, "Delta|BitPack", col)
+        check_parity(engine, "RLE|[BitPack,BitPack]", col)
+    g = TPCH(0.0001)
+    c = g.column("l_comment")
+    empty = Column("e", cdm.VARBYTES, 1, 0, c.data[:0], c.offsets[:1] * 0)
+    check_parity(engine, "Str|[LZ4,BitPack]", [encoder.encode("Str|[LZ4,BitPack]", empty)], cdm.VARBYTES)
+
+
+def test_corrupt_dict_index_sets_error(engine):
+    spec = "Dict|BitPack"
+    root = cdm1.Node(cdm1.DICT, 5000, [cdm1.raw(np.arange(4, dtype=np.int64).tobytes(), eb=8),
+                                       cdm1.bitpack([i % 5 for i in range(5000)], 3, 0)], entries=4, E=8)
+    ch = cdm1.build(root, cdm1.I64, 8, 5000, cascade_hash=_hash(spec))
+    casc = cdm.Cascade(spec, cdm.I64)
+    for resident in (False, True):
+        (_, _, r), = gpu_decode(engine, casc, [ch], resident=resident, expect_error=True)
+        assert r["error_bits"] & cdm.ERR_DICT_INDEX
+
+
+def test_corrupt_run_sum_sets_error(engine):
+    spec = "RLE|[BitPack,BitPack]"
+    for counts in ([3] * 4000, [3] * 4000 + [10 ** 6]):
+        n = 12_001
+        root = cdm1.Node(cdm1.RLE, n, [cdm1.bitpack(list(range(len(counts))), 20, 0),
+                                       cdm1.bitpack(counts, 20, 0)], nruns=len(counts), maxrun=max(counts))
+        ch = cdm1.build(root, cdm1.I64, 8, n, cascade_hash=_hash(spec))
+        (payload, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.I64), [ch], resident=True, expect_error=True)
+        assert r["error_bits"] & cdm.ERR_RUN_SUM
+
+
+def test_corrupt_lz4_sets_error(engine):
+    from test_oracle_pins import _seq
+    spec = "Str|[LZ4,BitPack]"
+    for blk, dl in [(_seq(b"ABCDEFGH", 9, 4) + _seq(b"", None, None), 12),
+                    (_seq(b"ABCDEFGH", 0, 4) + _seq(b"", None, None), 12),
+                    (_seq(b"ABCDEFGH", 2, 40) + _seq(b"", None, None), 20)]:
+        tab = struct.pack("<III", 0, len(blk), dl)
+        root = cdm1.Node(cdm1.STR, 1, [cdm1.Node(cdm1.LZ4, dl, [cdm1.raw(blk), cdm1.raw(tab, eb=12)], nsub=1, sub=1 << 16),
+                                       cdm1.bitpack([dl], 5, 0)])
+        ch = cdm1.build(root, cdm1.VARBYTES, 1, 1, payload=dl, cascade_hash=_hash(spec))
+        (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.VARBYTES), [ch], resident=True, expect_error=True)
+        assert r["error_bits"] & cdm.ERR_LZ4
+
+
+def test_host_rejects_foreign_cascade(engine):
+    col = config1_column(1000)
+    ch = encoder.encode("Delta|BitPack", col)
+    with pytest.raises(cdm.CdmError):
+        gpu_decode(engine, cdm.Cascade("BitPack", cdm.I32), [ch])
+
+
+# ------------------------------------------------------------------------------ pipeline invariance
+def test_order_and_slots_do_not_change_bytes():
+    """Pipelining changes time, never bytes: FIFO vs Johnson, 2 vs 6 slots."""
+    col = TPCH(0.02).column("l_extendedprice")
+    chunks = encoder.encode_chunks("Float2Int|BitPack", col, 10_000)
+    ref = [oracle.decode_chunk(c)[0] for c in chunks]
+    for order, slots in ((0, 2), (1, 6)):
+        e = cdm.Engine(0, n_slots=slots, order_policy=order)
+        got = gpu_decode(e, cdm.Cascade("Float2Int|BitPack", cdm.F64), chunks)
+        e.close()
+        for (p, _, _), r in zip(got, ref):
+            assert np.array_equal(p, r)
+
+
+def test_repeated_launches_graph_safe(engine):
+    """The epoch|ticket counters survive repeated launches of one batch (and CUDA-graph replays)."""
+    col = TPCH(0.05).column("l_orderkey")
+    spec = "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"
+    chunks = encoder.encode_chunks(spec, col, 100_000)
+    casc = cdm.Cascade(spec, cdm.I64)
+    decs, outs = [], []
+    for ch in chunks:
+        out, offs, _ = _outputs(ch)
+        decs.append(cdm.Decode(casc, ch, out, offs, dev_chunk=torch.from_numpy(ch).cuda()))
+        outs.append(out)
+    b = cdm.Batch(engine, decs)
+    s = torch.cuda.Stream()
+    for _ in range(5):
+        for o in outs:
+            o.fill_(SENTINEL)
+        b.launch(s)
+        b.results(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        b.launch(s)
+    for _ in range(3):
+        for o in outs:
+            o.fill_(SENTINEL)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        b.results(s)
+        for ch, o in zip(chunks, outs):
+            exp, _ = oracle.decode_chunk(ch)
+            assert np.array_equal(o.cpu().numpy()[: exp.size], exp)
+    b.close()
