@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""bench.py -- effective decoded GB/s of the cascaded-columnar decode hot path on B200.
+
+Workload (BASELINE.json configs[1], "config 2"): TPC-H SF=1 lineitem numeric columns, synthetic
+dbgen-like data (paper_2602_08190_b200.inputs), row groups of 2^22 rows:
+    l_orderkey   RLE|[Delta|RLE|[BitPack,BitPack],BitPack]   int64   (H7 + inner pre-pass)
+    l_quantity   Dict|BitPack                                 float64 (H5)
+    l_discount   Dict|BitPack                                 float64 (H5)
+One step = decode every chunk of the three columns (all hot-path rows this workload touches).
+
+  value  device-resident: compressed chunks already in HBM, decoded bytes / device time (CUDA events on
+         the launching stream around cdm_batch_launch; L2 flushed by a 256 MiB write between steps,
+         outside the events).
+  e2e    through the public C-ABI from PINNED HOST memory: cdm_submit_batch (H2D copies on the copy
+         stream overlapped with decode, Johnson order) + cdm_wait (D2H of each chunk's error word).
+  roofline  the dominant kernel family (by device time) against the measured HBM copy peak.
+  cpu_baseline  the CPU oracle (oracle/, plain C, chunk-parallel) on the same chunks.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling -- every rank decodes its own independent
+SF=1 shard (seed offset by rank); the only collective is the final NCCL all-reduce of
+(rows, decoded bytes, compressed bytes, error bits) plus a MAX of the device time.
+
+--impl reference: the reference arm of this tier is the CPU oracle, timed as it stands on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "effective decoded GB/s (host-compressed→device-decoded) at 1/2/4/8 B200 vs roofline"
+WORKLOAD = [("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"),
+            ("l_quantity", "Dict|BitPack"),
+            ("l_discount", "Dict|BitPack")]
+CHUNK_ROWS = 1 << 22
+SF = 1.0
+FAMILY_NAMES = ["fp", "scan", "rle", "lz4", "copy"]
+FAMILY_KERNELS = {"fp": "fp_kernel", "scan": "scan_kernel", "rle": "inner_kernel+rle_kernel+rle_big_kernel",
+                  "lz4": "lz4_kernel", "copy": "cudaMemcpyAsync D2D"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="cdm", choices=["cdm", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=2.0, help="wall seconds of the oracle sample")
+    return p.parse_args()
+
+
+def build_workload(rank: int):
+    """Generate + encode this rank's shard (untimed).  Returns list of (name, spec, dtype, width, chunks)."""
+    from paper_2602_08190_b200 import encoder
+    from paper_2602_08190_b200.inputs import TPCH, MASTER_SEED
+    g = TPCH(SF, MASTER_SEED + 1000 * rank)
+    cols = []
+    for name, spec in WORKLOAD:
+        col = g.column(name)
+        chunks = encoder.encode_chunks(spec, col, CHUNK_ROWS, first_chunk_id=1000 * rank)
+        cols.append((name, spec, col.dtype, col.width, chunks, col.nbytes()))
+    return cols
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled through NVML every 2 ms during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.sm = []
+        self.max_mhz = None
+        self.reasons = set()
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001 -- no NVML: clocks unknown
+            self.nv = None
+        return self
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 2 ms"}
+
+
+def measure_h2d(torch, nbytes=256 << 20, reps=5):
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    best = 1e9
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            a.record()
+            d.copy_(h, non_blocking=True)
+            b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return nbytes / best / 1e6
+
+
+def cpu_baseline(cols, seconds: float):
+    """The oracle as it stands: plain C decode of the same chunks, chunk-parallel on the host cores."""
+    import oracle
+    chunks = [c for (_, _, _, _, chs, _) in cols for c in chs]
+    decoded = sum(int(oracle.oracle._header(c)[3]) for c in chunks)
+    threads = min(os.cpu_count() or 1, len(chunks))
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        oracle.decode_many(chunks, nthreads=threads)
+        passes += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": decoded * passes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"{passes} full pass(es) over the {len(chunks)} config-2 chunks ({decoded / 1e6:.1f} MB decoded "
+                      f"each) with {threads} threads, {dt:.2f} s wall"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on this arm's workload, K timed steps after W warm-up steps."""
+    if rank != 0:
+        return
+    cols = build_workload(0)
+    import oracle
+    chunks = [c for (_, _, _, _, chs, _) in cols for c in chs]
+    decoded = sum(int(oracle.oracle._header(c)[3]) for c in chunks)
+    threads = min(os.cpu_count() or 1, len(chunks))
+    for _ in range(args.warmup):
+        oracle.decode_many(chunks, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.decode_many(chunks, nthreads=threads)
+    dt = time.perf_counter() - t0
+    v = decoded * args.steps / dt / 1e9
+    line = {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "config 2: TPC-H SF=1 lineitem numeric (l_orderkey, l_quantity, l_discount)",
+                       "chunk_rows": CHUNK_ROWS, "decoded_bytes_per_step": decoded},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "oracle",
+                             "sample": f"each step = one full oracle pass over the {len(chunks)} config-2 chunks"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2602_08190_b200 import cdm
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cols = build_workload(rank)
+    compressed = sum(int(c.size) for (_, _, _, _, chs, _) in cols for c in chs)
+    decoded = sum(int(cdm.chunk_info(c)["payload_bytes"]) for (_, _, _, _, chs, _) in cols for c in chs)
+    n_chunks = sum(len(chs) for (_, _, _, _, chs, _) in cols)
+
+    eng = cdm.Engine(local, n_slots=4, slot_bytes=64 << 20, order_policy=1)
+    stream = torch.cuda.Stream()
+    # the compressed columns live back to back in ONE pinned host buffer (as a column store would keep them)
+    sizes = [int(c.size) for (_, _, _, _, chs, _) in cols for c in chs]
+    pinned_all = torch.empty(sum(sizes), dtype=torch.uint8).pin_memory()
+    pin_np = pinned_all.numpy()
+    decs_dev, decs_host, outs = [], [], []
+    pos = 0
+    for name, spec, dtype, width, chunks, _ in cols:
+        casc = cdm.Cascade(spec, dtype, width)
+        for ch in chunks:
+            out, offs = cdm.output_buffers(ch)
+            pin_np[pos:pos + ch.size] = ch
+            host = pinned_all[pos:pos + ch.size]
+            pos += ch.size
+            dev = torch.from_numpy(ch).cuda()
+            decs_dev.append(cdm.Decode(casc, host, out, offs, dev_chunk=dev))
+            decs_host.append(cdm.Decode(casc, host, out, offs))
+            outs.append(out)
+    batch = cdm.Batch(eng, decs_dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    # ---------------------------------------------------------------- device-resident (value)
+    for _ in range(args.warmup):
+        batch.launch(stream)
+    batch.results(stream)
+    batch.set_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()                     # L2 flush (256 MiB write), outside the events
+                ev[k][0].record(stream)
+                launches += batch.launch(stream)  # the whole hot path for this workload
+                ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    res = batch.results(stream)
+    kern = batch.kernel_ms()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    err_bits = 0
+    for r in res:
+        err_bits |= r["error_bits"]
+
+    # ---------------------------------------------------------------- end to end from pinned host (e2e)
+    for _ in range(max(1, args.warmup)):
+        for t in eng.submit_batch(decs_host):
+            eng.wait(t)
+    e2e_steps = max(3, args.steps // 4)
+    torch.cuda.synchronize()
+    e2e_total = 0.0
+    for _ in range(e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tickets = eng.submit_batch(decs_host)
+        for t in tickets:
+            r = eng.wait(t)
+            err_bits |= r["error_bits"]
+        e2e_total += time.perf_counter() - t0
+    h2d_gbs = measure_h2d(torch)
+
+    # ---------------------------------------------------------------- reduce over ranks (metadata only)
+    dev_s = dev_ms / 1e3
+    if world > 1:
+        meta = torch.tensor([decoded, compressed, n_chunks, err_bits], dtype=torch.int64, device="cuda")
+        dist.all_reduce(meta, op=dist.ReduceOp.SUM)
+        tmax = torch.tensor([dev_s, e2e_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tot_decoded, tot_comp, tot_chunks, tot_err = [int(x) for x in meta.tolist()]
+        dev_s, e2e_total = [float(x) for x in tmax.tolist()]
+    else:
+        tot_decoded, tot_comp, tot_chunks, tot_err = decoded, compressed, n_chunks, err_bits
+
+    if rank == 0:
+        value = tot_decoded * args.steps / dev_s / 1e9
+        e2e = tot_decoded * e2e_steps / e2e_total / 1e9
+        peak, peak_src = load_peaks()
+        # dominant kernel family by device time; algorithmic bytes = compressed read + decoded written
+        fam_ms = {FAMILY_NAMES[i]: kern[FAMILY_NAMES[i]] for i in range(5)}
+        fam_bytes = {"fp": 0, "scan": 0, "rle": 0, "lz4": 0, "copy": 0}
+        for d in decs_dev:
+            info = cdm.chunk_info(d.host_chunk)
+            plan = d.cascade.describe().split(" => ")[1]
+            fam = "rle" if plan.startswith(("rle", "inner")) else ("scan" if plan.startswith("scan") else
+                                                                    ("fp" if plan.startswith("fp") else "copy"))
+            fam_bytes[fam] += info["compressed_bytes"] + info["payload_bytes"] + info["offsets_bytes"]
+        dom = max(fam_ms, key=lambda f: fam_ms[f][0])
+        dom_ms, dom_launch = fam_ms[dom]
+        per_step_ms = dom_ms / args.steps
+        achieved = fam_bytes[dom] / (per_step_ms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(dom)
+        cr = tot_decoded / tot_comp
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3 / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {
+                "workload": "config 2: TPC-H SF=1 lineitem numeric columns (l_orderkey RLE|[Delta|RLE|[BitPack,"
+                            "BitPack],BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack), per rank",
+                "sf_per_rank": SF, "chunk_rows": CHUNK_ROWS, "chunks_per_rank": n_chunks,
+                "decoded_bytes_per_step": tot_decoded, "compressed_bytes_per_step": tot_comp,
+                "compression_ratio": round(cr, 2), "parallelism": f"dp{world} (independent shards)",
+                "l2": "flushed between timed steps by a 256 MiB write outside the CUDA events",
+                "timing": "sum of per-step CUDA-event device times on the launching stream; max over ranks",
+                "wall_s_timed_loop": round(wall, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": FAMILY_KERNELS[dom],
+                         "algorithmic_bytes_per_step": fam_bytes[dom], "kernel_ms_per_step": round(per_step_ms, 4),
+                         "peak_source": peak_src,
+                         "families_ms_per_step": {f: round(fam_ms[f][0] / args.steps, 4) for f in fam_ms if fam_ms[f][1]}},
+            "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": tot_comp,
+                    "d2h_bytes_per_step": 4 * tot_chunks, "pcie_h2d_gbs_measured": round(h2d_gbs, 1),
+                    "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_gbs, 1),
+                    "how": "cdm_submit_batch from pinned host (H2D + decode, Johnson order) + cdm_wait per chunk"},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "errors": tot_err,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cols, args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    batch.close()
+    eng.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

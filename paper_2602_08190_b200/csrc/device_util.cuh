@@ -98,92 +98,85 @@ __device__ __forceinline__ void take_ticket(unsigned long long* ctr, uint32_t la
   if (*ticket == last) atomicExch(ctr, (unsigned long long)(*epoch + 1) << 32);
 }
 
-// flag word = (epoch << 2) | state
+// Look-back word: 16 bytes {flag = (epoch << 2) | state, c (u32, saturating count), w (u64, wrapping)},
+// published with ONE 128-bit relaxed store and probed with ONE 128-bit load, so a reader never sees a flag
+// without its values and no fence is needed (the CUB ScanTileState 16-byte TxnWord idiom).
 constexpr uint32_t LB_AGG = 1, LB_INC = 2;
 
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ void lb_store(uint4* p, uint32_t flag, uint32_t c, uint64_t w) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(flag), "r"(c),
+               "r"(uint32_t(w)), "r"(uint32_t(w >> 32))
+               : "memory");
+}
+__device__ __forceinline__ uint4 lb_load(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+
+__device__ __forceinline__ uint32_t sat32(uint64_t x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(x); }
+
+__device__ __forceinline__ void lb_publish(uint4* words, uint32_t gt, uint32_t epoch, uint32_t state, uint64_t c,
+                                           uint64_t w) {
+  lb_store(words + gt, (epoch << 2) | state, sat32(c), w);
 }
 
-// Look-back state for up to two 64-bit components per tile (scan of counts, and of weighted deltas).
-struct LookbackState {
-  uint32_t* flag;   // [tiles]
-  uint64_t* agg0;   // [tiles]
-  uint64_t* agg1;   // [tiles] (may be null when one component)
-  uint64_t* inc0;   // [tiles]
-  uint64_t* inc1;   // [tiles]
-};
-
-// Publish a tile's aggregate (state AGG) -- values first, then the flag with release semantics.
-template <int NC>
-__device__ __forceinline__ void lb_publish(const LookbackState& s, uint32_t gt, uint32_t epoch, uint32_t state,
-                                           uint64_t v0, uint64_t v1) {
-  if (state == LB_AGG) {
-    st_relaxed_u64(s.agg0 + gt, v0);
-    if (NC > 1) st_relaxed_u64(s.agg1 + gt, v1);
-  } else {
-    st_relaxed_u64(s.inc0 + gt, v0);
-    if (NC > 1) st_relaxed_u64(s.inc1 + gt, v1);
-  }
-  st_release_u32(s.flag + gt, (epoch << 2) | state);
-}
-
-// Single-warp decoupled look-back: lanes probe 32 predecessors at a time (gt-1-lane), accumulate the
-// AGG values up to the nearest INC.  `first_gt` is the chunk's first tile (whose prefix is 0).  Must be
-// called by all 32 lanes of one warp; returns the exclusive prefix (both components) in every lane.
-template <int NC>
-__device__ __forceinline__ void lb_lookback(const LookbackState& s, uint32_t gt, uint32_t first_gt, uint32_t epoch,
-                                            uint64_t* p0, uint64_t* p1) {
+// Single-warp decoupled look-back: lanes probe 32 predecessors at a time (gt-1-lane) and fold the AGG
+// values up to the nearest INC.  `first_gt` is the chunk's first tile (prefix 0).  Called by all 32 lanes
+// of one warp; returns the exclusive prefix in every lane (count saturating at 2^32-1, w mod 2^64).
+__device__ __forceinline__ void lb_lookback(const uint4* words, uint32_t gt, uint32_t first_gt, uint32_t epoch,
+                                            uint64_t* pc, uint64_t* pw) {
   const uint32_t lane = threadIdx.x & 31;
-  uint64_t acc0 = 0, acc1 = 0;
+  uint64_t acc_c = 0, acc_w = 0;
   int64_t base = int64_t(gt) - 1;  // highest predecessor not yet folded
   while (base >= int64_t(first_gt)) {
     const int64_t me = base - lane;
     uint32_t st = LB_INC;  // lanes below the chunk start act as a terminating INC with value 0
-    uint64_t a0 = 0, a1 = 0;
+    uint64_t c = 0, w = 0;
     if (me >= int64_t(first_gt)) {
-      uint32_t f;
+      uint4 v;
       do {
-        f = ld_acquire_u32(s.flag + me);
-      } while (((f >> 2) != epoch) || (f & 3u) == 0);
-      st = f & 3u;
-      if (st == LB_INC) {
-        a0 = ld_relaxed_u64(s.inc0 + me);
-        if (NC > 1) a1 = ld_relaxed_u64(s.inc1 + me);
-      } else {
-        a0 = ld_relaxed_u64(s.agg0 + me);
-        if (NC > 1) a1 = ld_relaxed_u64(s.agg1 + me);
-      }
+        v = lb_load(words + me);
+      } while ((v.x >> 2) != epoch || (v.x & 3u) == 0);
+      st = v.x & 3u;
+      c = v.y;
+      w = (uint64_t(v.w) << 32) | v.z;
     }
-    // the nearest INC (smallest lane index with state INC) terminates the walk
     const uint32_t incmask = __ballot_sync(FULL, st == LB_INC);
     const uint32_t stop = incmask ? uint32_t(__ffs(incmask) - 1) : 32u;
-    if (lane > stop) { a0 = 0; a1 = 0; }
+    if (lane > stop) { c = 0; w = 0; }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(FULL, a0, o);
-      if (NC > 1) a1 += __shfl_xor_sync(FULL, a1, o);
+      c += __shfl_xor_sync(FULL, c, o);
+      w += __shfl_xor_sync(FULL, w, o);
     }
-    acc0 += a0;
-    acc1 += a1;
+    acc_c += c;
+    acc_w += w;
     if (incmask) break;
     base -= 32;
   }
-  *p0 = acc0;
-  *p1 = acc1;
+  *pc = sat32(acc_c);
+  *pw = acc_w;
+}
+
+// The whole protocol for one tile, run by warp 0: publish AGG (or INC for the chunk's first tile), look
+// back, publish INC.  Returns the tile's exclusive prefix (count, w) in every lane.
+__device__ __forceinline__ void lb_tile(uint4* words, uint32_t gt, uint32_t first_gt, uint32_t epoch, uint64_t agg_c,
+                                        uint64_t agg_w, uint64_t* pc, uint64_t* pw) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t c = 0, w = 0;
+  if (gt == first_gt) {
+    if (lane == 0) lb_publish(words, gt, epoch, LB_INC, agg_c, agg_w);
+  } else {
+    if (lane == 0) lb_publish(words, gt, epoch, LB_AGG, agg_c, agg_w);
+    lb_lookback(words, gt, first_gt, epoch, &c, &w);
+    if (lane == 0) lb_publish(words, gt, epoch, LB_INC, c + agg_c, w + agg_w);
+  }
+  *pc = c;
+  *pw = w;
 }
 
 // ------------------------------------------------------------------ block scans (256 threads)

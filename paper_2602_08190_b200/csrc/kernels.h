@@ -12,7 +12,9 @@ namespace cdm {
 constexpr int kMaxBatch = 32;      // descriptors per launch (more chunks -> more launches)
 constexpr int kFpTile = 4096;      // H5 values per tile = 256 threads x 16
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
-constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
+constexpr int kRleTile = 2048;     // H7 runs per tile = 256 threads x 8
+constexpr int kInnerTile = 2048;   // Delta|RLE pre-pass inner runs per tile = 256 threads x 8
+constexpr int kRleWindow = 768;    // DRLE inner-run window staged per outer tile (larger: global search)
 constexpr uint32_t kRleBigLimit = 1u << 15;  // a tile with more output rows is expanded by rle_big
 constexpr uint32_t kRleBigPiece = 8192;       // rows per rle_big work item
 constexpr int kThreads = 256;
@@ -66,9 +68,7 @@ struct ScanBatch {
   uint32_t total_tiles;
   uint32_t* err;
   unsigned long long* ticket;  // epoch|ticket counter
-  uint32_t* flag;
-  uint64_t* agg;
-  uint64_t* inc;
+  uint4* lb;                   // [total_tiles] 16-byte look-back words
   ScanDesc d[kMaxBatch];
 };
 
@@ -132,17 +132,15 @@ struct RleBatch {
   uint32_t total_tiles;
   uint32_t* err;
   unsigned long long* ticket;
-  uint32_t* flag;
-  uint64_t* agg0;
-  uint64_t* agg1;
-  uint64_t* inc0;
-  uint64_t* inc1;
+  uint4* lb;
+  uint32_t big_enabled;          // 0: rle_big is not launched -> oversize tiles are expanded in place
   RleBig big;
   RleDesc d[kMaxBatch];
 };
 
 // Delta|RLE inner pre-pass (V_DRLE): scan over inner runs j producing S_j (outer-run start), Q_j
-// (base + sum_{k<j} dv_k dc_k), DV_j and tstart[t] (inner run holding outer run t*kRleTile).
+// (base + sum_{k<j} dv_k dc_k), DV_j and tstart[t] (inner run holding outer run t*kRleTile; entry
+// tstart[outer_tiles] = n_inner - 1 closes the last window).
 struct InnerDesc {
   const uint8_t* dv_packed;
   const uint8_t* dc_packed;
@@ -169,11 +167,7 @@ struct InnerBatch {
   uint32_t total_tiles;
   uint32_t* err;
   unsigned long long* ticket;
-  uint32_t* flag;
-  uint64_t* agg0;
-  uint64_t* agg1;
-  uint64_t* inc0;
-  uint64_t* inc1;
+  uint4* lb;
   InnerDesc d[kMaxBatch];
 };
 

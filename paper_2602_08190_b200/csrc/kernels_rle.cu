@@ -5,7 +5,7 @@
 // The paper runs PyTorch cumsum on the counts, then a Group-Parallel kernel whose <L,S,C> geometry makes
 // several blocks co-process one big group or one block walk several small groups.
 // B200 design, one pass over the runs:
-//  * rle_kernel: a CTA owns 1024 consecutive runs (ticketed).  It unpacks the counts (FOR + bits), the
+//  * rle_kernel: a CTA owns 2048 consecutive runs (ticketed).  It unpacks the counts (FOR + bits), the
 //    run values through the fused nested provider (BitPack, Dict|BitPack, Float2Int|BitPack, the
 //    closed form of Delta|RLE, or arithmetic runs for a root Delta|RLE), scans the counts in the CTA
 //    and obtains the tile's output offset by decoupled look-back -- the cumsum never touches HBM.
@@ -27,7 +27,6 @@ namespace {
 using namespace dev;
 
 constexpr int K = kRleTile;
-constexpr int kRunsPerThread = K / kThreads;  // 4
 
 __constant__ double kPow10r[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                    1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
@@ -89,6 +88,8 @@ __device__ __forceinline__ void expand_warp(const uint32_t* soffs, uint32_t nr, 
 }
 
 // ------------------------------------------------------------------------------------------ pre-pass
+constexpr int kIPer = kInnerTile / kThreads;  // 8 inner runs per thread
+
 __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__ InnerBatch B) {
   __shared__ uint64_t warp_s[kThreads / 32];
   __shared__ uint32_t tile_s, epoch_s;
@@ -105,15 +106,15 @@ __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__
   if (gt >= B.total_tiles) return;
   const InnerDesc& D = B.d[find_desc(B, gt)];
   const uint32_t lt = gt - D.tile0;
-  const uint32_t j0 = lt * K;
-  const uint32_t nvalid = min(uint32_t(K), D.n_inner - j0);
+  const uint32_t j0 = lt * kInnerTile;
+  const uint32_t nvalid = min(uint32_t(kInnerTile), D.n_inner - j0);
 
-  uint64_t dc[kRunsPerThread], dv[kRunsPerThread];
+  uint64_t dc[kIPer], dv[kIPer];
   uint64_t sc = 0, sw = 0;
   bool bad = false;
 #pragma unroll
-  for (int r = 0; r < kRunsPerThread; r++) {
-    const uint32_t k = tid * kRunsPerThread + r;
+  for (int r = 0; r < kIPer; r++) {
+    const uint32_t k = tid * kIPer + r;
     dc[r] = 0;
     dv[r] = 0;
     if (k < nvalid) {
@@ -129,31 +130,26 @@ __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__
   const uint64_t ec = block_excl_scan_u64<kThreads>(sc, warp_s, &tc);
   const uint64_t ew = block_excl_scan_u64<kThreads>(sw, warp_s, &tw);
   if (tid < 32) {
-    LookbackState st{B.flag, B.agg0, B.agg1, B.inc0, B.inc1};
-    uint64_t p0 = 0, p1 = 0;
-    if (lt == 0) {
-      if (tid == 0) lb_publish<2>(st, gt, epoch, LB_INC, tc, tw);
-    } else {
-      if (tid == 0) lb_publish<2>(st, gt, epoch, LB_AGG, tc, tw);
-      lb_lookback<2>(st, gt, D.tile0, epoch, &p0, &p1);
-      if (tid == 0) lb_publish<2>(st, gt, epoch, LB_INC, p0 + tc, p1 + tw);
-    }
+    uint64_t p0, p1;
+    lb_tile(B.lb, gt, D.tile0, epoch, tc, tw, &p0, &p1);
     if (tid == 0) {
       pc_s = p0;
       pw_s = p1;
-      if (lt + 1 == D.ntiles && p0 + tc != D.n_outer) atomicOr(B.err + D.err_idx, 0x2u);
+      if (lt + 1 == D.ntiles) {
+        if (p0 + tc != D.n_outer) atomicOr(B.err + D.err_idx, 0x2u);
+        D.tstart[D.outer_tiles] = D.n_inner - 1;  // closes the last outer tile's window
+      }
     }
   }
   if (bad) atomicOr(B.err + D.err_idx, 0x2u);
   __syncthreads();
   uint64_t c = pc_s + ec, wsum = pw_s + ew;
 #pragma unroll
-  for (int r = 0; r < kRunsPerThread; r++) {
-    const uint32_t k = tid * kRunsPerThread + r;
+  for (int r = 0; r < kIPer; r++) {
+    const uint32_t k = tid * kIPer + r;
     if (k < nvalid) {
       const uint32_t j = j0 + k;
-      const uint32_t S = uint32_t(min(c, uint64_t(D.n_outer)));
-      D.S[j] = S;
+      D.S[j] = uint32_t(min(c, uint64_t(D.n_outer)));
       D.Q[j] = D.base + wsum;
       D.DV[j] = dv[r];
       if (dc[r] && c < D.n_outer) {  // outer tiles whose first run lies in this inner run
@@ -167,13 +163,17 @@ __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__
 }
 
 // ------------------------------------------------------------------------------------------ main
-__global__ void __launch_bounds__(kThreads) rle_kernel(const __grid_constant__ RleBatch B) {
+constexpr int kRPer = K / kThreads;  // 8 runs per thread
+
+__global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ uint32_t soffs_s[K + 1];
   __shared__ uint64_t vals_s[K];
-  __shared__ uint64_t slopes_s[K];
-  __shared__ uint32_t iS_s[K + 1];
-  __shared__ uint64_t iQ_s[K + 1];
-  __shared__ uint64_t iDV_s[K + 1];
+  __shared__ __align__(16) uint8_t aux_s[K * 8];  // slopes (V_LINEAR) or the inner-run window (V_DRLE)
+  uint64_t* slopes_s = reinterpret_cast<uint64_t*>(aux_s);
+  uint64_t* iQ_s = reinterpret_cast<uint64_t*>(aux_s);
+  uint64_t* iDV_s = iQ_s + (kRleWindow + 1);
+  uint32_t* iS_s = reinterpret_cast<uint32_t*>(iDV_s + (kRleWindow + 1));
+  static_assert((kRleWindow + 1) * 20 <= K * 8, "window must fit the aux buffer");
   __shared__ uint64_t warp_s[kThreads / 32];
   __shared__ uint32_t tile_s, epoch_s, skip_s, win_s, j0i_s;
   __shared__ uint64_t pc_s, pw_s;
@@ -194,67 +194,77 @@ __global__ void __launch_bounds__(kThreads) rle_kernel(const __grid_constant__ R
   const uint8_t vmode = D.vmode;
   uint32_t errbits = 0;
 
-  // V_DRLE: stage the inner-run window covering outer runs [g0, g0 + nr)
+  // V_DRLE: inner runs [tstart[lt], tstart[lt+1]] hold every outer run of this tile
+  const uint32_t* wS = iS_s;
+  const uint64_t* wQ = iQ_s;
+  const uint64_t* wDV = iDV_s;
   if (vmode == V_DRLE) {
     if (tid == 0) {
-      uint32_t j0i = D.tstart[lt];
+      uint32_t j0i = D.tstart[lt], j1i = D.tstart[lt + 1];
       if (j0i >= D.n_inner) { j0i = 0; errbits |= 0x2u; }
+      if (j1i >= D.n_inner || j1i < j0i) { j1i = D.n_inner - 1; }
       j0i_s = j0i;
-      win_s = min(uint32_t(K + 1), D.n_inner - j0i);
+      win_s = j1i - j0i + 1;
     }
     __syncthreads();
-    for (uint32_t k = tid; k < win_s; k += kThreads) {
-      iS_s[k] = D.S[j0i_s + k];
-      iQ_s[k] = D.Q[j0i_s + k];
-      iDV_s[k] = D.DV[j0i_s + k];
+    const uint32_t j0i = j0i_s, win = win_s;
+    if (win <= kRleWindow + 1) {
+      for (uint32_t k = tid; k < win; k += kThreads) {
+        iS_s[k] = D.S[j0i + k];
+        iQ_s[k] = D.Q[j0i + k];
+        iDV_s[k] = D.DV[j0i + k];
+      }
+      __syncthreads();
+    } else {  // unusual data (many tiny inner runs): search the pre-pass arrays in global memory
+      wS = D.S + j0i;
+      wQ = D.Q + j0i;
+      wDV = D.DV + j0i;
     }
-    __syncthreads();
   }
 
-  uint64_t cnt[kRunsPerThread], val[kRunsPerThread];
+  uint64_t cnt[kRPer], val[kRPer];
   uint64_t sc = 0, sw = 0;
-#pragma unroll
-  for (int r = 0; r < kRunsPerThread; r++) {
-    const uint32_t k = tid * kRunsPerThread + r;
-    cnt[r] = 0;
-    val[r] = 0;
-    if (k < nr) {
-      const uint64_t g = g0 + k;
-      cnt[r] = D.cnt_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.cnt_packed), g * D.cnt_w, D.cnt_w);
-      if (cnt[r] > D.n) { errbits |= 0x2u; cnt[r] = 0; }
-      if (vmode == V_DRLE) {
-        uint32_t a = 0, b = win_s - 1;  // last window run with S <= g
-        while (a < b) {
-          const uint32_t mid = (a + b + 1) >> 1;
-          if (iS_s[mid] <= g) a = mid; else b = mid - 1;
-        }
-        uint64_t S = iS_s[a], Q = iQ_s[a], dv = iDV_s[a];
-        const uint32_t ji = j0i_s + a;
-        if (a + 1 == win_s && ji + 1 < D.n_inner && D.S[ji + 1] <= g) {  // zero-length inner runs: global search
-          uint32_t lo = ji + 1, hi = D.n_inner - 1;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (D.S[mid] <= g) lo = mid; else hi = mid - 1;
-          }
-          S = D.S[lo]; Q = D.Q[lo]; dv = D.DV[lo];
-        }
-        val[r] = Q + (g - S + 1) * dv;
-      } else {
-        const uint64_t x = D.val_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.val_packed), g * D.val_w, D.val_w);
-        if (vmode == V_BP || vmode == V_LINEAR) {
-          val[r] = x;
-        } else if (vmode == V_DICT) {
-          uint64_t idx = x;
-          if (idx >= D.entries) { errbits |= 0x1u; idx = 0; }
-          val[r] = D.out_bytes == 8 ? __ldg(reinterpret_cast<const unsigned long long*>(D.dict) + idx)
-                                    : uint64_t(__ldg(reinterpret_cast<const uint32_t*>(D.dict) + idx));
-        } else {  // V_F2I
-          val[r] = uint64_t(__double_as_longlong(double(int64_t(x)) / kPow10r[D.d]));
-        }
+  {
+    const uint32_t kb = tid * kRPer;
+    uint32_t a = 0;
+    if (vmode == V_DRLE && kb < nr) {  // first window run with S <= g, then walk forward
+      const uint32_t g = g0 + kb;
+      uint32_t hi = win_s - 1;
+      while (a < hi) {
+        const uint32_t mid = (a + hi + 1) >> 1;
+        if (wS[mid] <= g) a = mid; else hi = mid - 1;
       }
     }
-    sc += cnt[r];
-    if (vmode == V_LINEAR) sw += val[r] * cnt[r];
+#pragma unroll
+    for (int r = 0; r < kRPer; r++) {
+      const uint32_t k = kb + r;
+      cnt[r] = 0;
+      val[r] = 0;
+      if (k < nr) {
+        const uint64_t g = g0 + k;
+        cnt[r] = D.cnt_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.cnt_packed), g * D.cnt_w, D.cnt_w);
+        if (cnt[r] > D.n) { errbits |= 0x2u; cnt[r] = 0; }
+        if (vmode == V_DRLE) {
+          while (a + 1 < win_s && wS[a + 1] <= g) a++;
+          val[r] = wQ[a] + (g - wS[a] + 1) * wDV[a];
+        } else {
+          const uint64_t x = D.val_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.val_packed),
+                                                              g * D.val_w, D.val_w);
+          if (vmode == V_BP || vmode == V_LINEAR) {
+            val[r] = x;
+          } else if (vmode == V_DICT) {
+            uint64_t idx = x;
+            if (idx >= D.entries) { errbits |= 0x1u; idx = 0; }
+            val[r] = D.out_bytes == 8 ? __ldg(reinterpret_cast<const unsigned long long*>(D.dict) + idx)
+                                      : uint64_t(__ldg(reinterpret_cast<const uint32_t*>(D.dict) + idx));
+          } else {  // V_F2I
+            val[r] = uint64_t(__double_as_longlong(double(int64_t(x)) / kPow10r[D.d]));
+          }
+        }
+      }
+      sc += cnt[r];
+      if (vmode == V_LINEAR) sw += val[r] * cnt[r];
+    }
   }
   uint64_t T, W = 0;
   const uint64_t ec = block_excl_scan_u64<kThreads>(sc, warp_s, &T);
@@ -262,25 +272,8 @@ __global__ void __launch_bounds__(kThreads) rle_kernel(const __grid_constant__ R
   if (vmode == V_LINEAR) ew = block_excl_scan_u64<kThreads>(sw, warp_s, &W);
 
   if (tid < 32) {
-    LookbackState st{B.flag, B.agg0, B.agg1, B.inc0, B.inc1};
-    uint64_t p0 = 0, p1 = 0;
-    if (vmode == V_LINEAR) {
-      if (lt == 0) {
-        if (tid == 0) lb_publish<2>(st, gt, epoch, LB_INC, T, W);
-      } else {
-        if (tid == 0) lb_publish<2>(st, gt, epoch, LB_AGG, T, W);
-        lb_lookback<2>(st, gt, D.tile0, epoch, &p0, &p1);
-        if (tid == 0) lb_publish<2>(st, gt, epoch, LB_INC, p0 + T, p1 + W);
-      }
-    } else {
-      if (lt == 0) {
-        if (tid == 0) lb_publish<1>(st, gt, epoch, LB_INC, T, 0);
-      } else {
-        if (tid == 0) lb_publish<1>(st, gt, epoch, LB_AGG, T, 0);
-        lb_lookback<1>(st, gt, D.tile0, epoch, &p0, &p1);
-        if (tid == 0) lb_publish<1>(st, gt, epoch, LB_INC, p0 + T, 0);
-      }
-    }
+    uint64_t p0, p1;
+    lb_tile(B.lb, gt, D.tile0, epoch, T, W, &p0, &p1);
     if (tid == 0) {
       pc_s = p0;
       pw_s = p1;
@@ -297,8 +290,8 @@ __global__ void __launch_bounds__(kThreads) rle_kernel(const __grid_constant__ R
   {
     uint64_t c = ec, wv = pw_s + ew;
 #pragma unroll
-    for (int r = 0; r < kRunsPerThread; r++) {
-      const uint32_t k = tid * kRunsPerThread + r;
+    for (int r = 0; r < kRPer; r++) {
+      const uint32_t k = tid * kRPer + r;
       if (k < nr) {
         soffs_s[k] = uint32_t(c);
         if (vmode == V_LINEAR) {
@@ -318,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) rle_kernel(const __grid_constant__ R
   const uint32_t O = uint32_t(pc_s);
   const uint32_t Tt = uint32_t(T);
   const uint64_t* slopes = vmode == V_LINEAR ? slopes_s : nullptr;
-  if (Tt <= kRleBigLimit) {
+  if (Tt <= kRleBigLimit || !B.big_enabled) {
     uint8_t* out = reinterpret_cast<uint8_t*>(D.out) + uint64_t(O) * D.out_bytes;
     const uint32_t warp = tid >> 5;
     const uint32_t span = ((Tt + kThreads - 1) / kThreads) * 32;

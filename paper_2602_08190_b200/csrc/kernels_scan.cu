@@ -83,15 +83,8 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
 
   // decoupled look-back (warp 0)
   if (tid < 32) {
-    LookbackState st{B.flag, B.agg, nullptr, B.inc, nullptr};
-    uint64_t p0 = 0, p1 = 0;
-    if (lt == 0) {
-      if (tid == 0) lb_publish<1>(st, gt, epoch, LB_INC, tile_total, 0);
-    } else {
-      if (tid == 0) lb_publish<1>(st, gt, epoch, LB_AGG, tile_total, 0);
-      lb_lookback<1>(st, gt, D.tile0, epoch, &p0, &p1);
-      if (tid == 0) lb_publish<1>(st, gt, epoch, LB_INC, p0 + tile_total, 0);
-    }
+    uint64_t pc, p0;
+    lb_tile(B.lb, gt, D.tile0, epoch, 0, tile_total, &pc, &p0);
     if (tid == 0) {
       prefix_s = p0;
       if (D.mode == SCAN_OFFSETS && lt + 1 == D.ntiles && p0 + tile_total != D.base)

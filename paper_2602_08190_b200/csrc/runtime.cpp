@@ -130,7 +130,7 @@ struct Bound {
   uint32_t entries = 0;
   uint8_t d = 0;
   uint64_t delta_base = 0, inner_base = 0;
-  uint32_t nruns = 0, n_inner = 0;
+  uint32_t nruns = 0, n_inner = 0, max_run = 0;
   bool lz4 = false;
   uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
   uint32_t n_sub = 0;
@@ -275,11 +275,13 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
         const Node& rl = c.nodes[ri];
         if (rl.n != c.rows) return bad("Delta child count mismatch");
         b->nruns = rl.u32_at0();
+        b->max_run = rl.u32_at4();
         if (!(e = bind_bp(c, t, t.kids[ri][0], b->nruns, 64, &b->main)).empty()) return bad(e);
         if (!(e = bind_bp(c, t, t.kids[ri][1], b->nruns, 32, &b->counts)).empty()) return bad(e);
         break;
       }
       b->nruns = r.u32_at0();
+      b->max_run = r.u32_at4();
       int vi = t.kids[0][0], ci = t.kids[0][1];
       if (!(e = bind_bp(c, t, ci, b->nruns, 32, &b->counts)).empty()) return bad(e);
       const Node& v = c.nodes[vi];
@@ -367,6 +369,7 @@ struct Alloc {  // bump allocator over one device arena; pass 1 sizes, pass 2 as
 
 // ============================================================================ device batches
 enum Family { F_FP = 0, F_SCAN = 1, F_RLE = 2, F_LZ4 = 3, F_COPY = 4 };
+static cudaStream_t engine_family_stream(cdm_engine* e, int fam);
 
 struct cdm_batch {
   cdm_engine* e = nullptr;
@@ -387,6 +390,9 @@ struct cdm_batch {
   uint32_t* err_dev = nullptr;
   uint32_t* err_host = nullptr;
   bool own_err_host = true;
+  // fork/join events: independent kernel families run concurrently on the engine's family streams
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -395,6 +401,8 @@ struct cdm_batch {
   double fam_ms[5] = {0, 0, 0, 0, 0};
   uint64_t fam_launches[5] = {0, 0, 0, 0, 0};
   ~cdm_batch() {
+    if (fork) cudaEventDestroy(fork);
+    for (auto ev : join) if (ev) cudaEventDestroy(ev);
     if (own_arena && arena) cudaFree(arena);
     if (own_err_host && err_host) cudaFreeHost(err_host);
     for (auto ev : ev_pool) cudaEventDestroy(ev);
@@ -487,7 +495,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     }
     sb.total_tiles = tiles;
     sb.ticket = A.take<unsigned long long>(1);
-    sb.flag = A.take<uint32_t>(tiles);
+    sb.lb = A.take<uint4>(tiles);
     B->scan.push_back(sb);
   }
   // inner pre-pass
@@ -508,14 +516,14 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.n_inner = b.n_inner;
       d.n_outer = b.nruns;
       d.tile0 = tiles;
-      d.ntiles = uint32_t(div_up(b.n_inner, kRleTile));
+      d.ntiles = uint32_t(div_up(b.n_inner, kInnerTile));
       d.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
       d.err_idx = uint32_t(j);
       tiles += d.ntiles;
     }
     ib.total_tiles = tiles;
     ib.ticket = A.take<unsigned long long>(1);
-    ib.flag = A.take<uint32_t>(tiles);
+    ib.lb = A.take<uint4>(tiles);
     B->inner.push_back(ib);
   }
   // rle
@@ -547,10 +555,13 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.err_idx = uint32_t(j);
       tiles += d.ntiles;
       slots += uint32_t(b.rows / kRleBigLimit) + 1;
+      // the header's max run bounds a tile's output; only then can rle_big be skipped (a lying header
+      // only costs speed: oversize tiles are then expanded in place)
+      if (uint64_t(kRleTile) * b.max_run > kRleBigLimit) rb.big_enabled = 1;
     }
     rb.total_tiles = tiles;
     rb.ticket = A.take<unsigned long long>(1);
-    rb.flag = A.take<uint32_t>(tiles);
+    rb.lb = A.take<uint4>(tiles);
     rb.big.counter = A.take<unsigned long long>(1);
     rb.big.done = A.take<uint32_t>(1);
     rb.big.max_slots = slots;
@@ -558,11 +569,6 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   }
   *zero_bytes = A.off;
   // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
-  for (auto& sb : B->scan) { sb.agg = A.take<uint64_t>(sb.total_tiles); sb.inc = A.take<uint64_t>(sb.total_tiles); }
-  for (auto& ib : B->inner) {
-    ib.agg0 = A.take<uint64_t>(ib.total_tiles); ib.agg1 = A.take<uint64_t>(ib.total_tiles);
-    ib.inc0 = A.take<uint64_t>(ib.total_tiles); ib.inc1 = A.take<uint64_t>(ib.total_tiles);
-  }
   std::map<int, InnerDesc*> inner_of;
   for (auto& ib : B->inner)
     for (uint32_t k = 0; k < ib.n; k++) {
@@ -570,12 +576,10 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.S = A.take<uint32_t>(d.n_inner);
       d.Q = A.take<uint64_t>(d.n_inner);
       d.DV = A.take<uint64_t>(d.n_inner);
-      d.tstart = A.take<uint32_t>(d.outer_tiles);
+      d.tstart = A.take<uint32_t>(d.outer_tiles + 1);
       inner_of[int(d.err_idx)] = &d;
     }
   for (auto& rb : B->rle) {
-    rb.agg0 = A.take<uint64_t>(rb.total_tiles); rb.agg1 = A.take<uint64_t>(rb.total_tiles);
-    rb.inc0 = A.take<uint64_t>(rb.total_tiles); rb.inc1 = A.take<uint64_t>(rb.total_tiles);
     rb.big.entries = A.take<RleBig::Entry>(rb.big.max_slots);
     rb.big.soffs = A.take<uint32_t>(size_t(rb.big.max_slots) * (kRleTile + 1));
     rb.big.vals = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
@@ -645,42 +649,65 @@ cudaEvent_t ev_get(cdm_batch* B, size_t k) {
 cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   uint32_t n = 0;
   size_t evk = B->pending.size() * 2;
-  auto t0 = [&](int fam, bool any) -> cudaEvent_t {
-    if (!B->timing || !any) return nullptr;
-    cudaEvent_t a = ev_get(B, evk++);
-    cudaEventRecord(a, s);
-    (void)fam;
-    return a;
-  };
-  auto t1 = [&](int fam, cudaEvent_t a) {
-    if (!a) return;
-    cudaEvent_t b = ev_get(B, evk++);
-    cudaEventRecord(b, s);
-    B->pending.push_back({fam, a, b});
-  };
+  const bool has[5] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty(),
+                       !B->copies.empty() || !B->zero_offsets.empty()};
+  int nfam = 0;
+  for (bool h : has) nfam += h;
   CUDA_TRY(cudaMemsetAsync(B->err_dev, 0, sizeof(uint32_t) * std::max<size_t>(1, B->jobs.size()), s));
-  cudaEvent_t a = t0(F_FP, !B->fp.empty());
-  for (size_t i = 0; i < B->fp.size(); i++) { CUDA_TRY(launch_fp(B->fp[i], B->fp_maxw[i], s)); n++; B->fam_launches[F_FP]++; }
-  t1(F_FP, a);
-  a = t0(F_SCAN, !B->scan.empty());
-  for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, s)); n++; B->fam_launches[F_SCAN]++; }
-  t1(F_SCAN, a);
-  a = t0(F_RLE, !B->rle.empty());
-  for (auto& ib : B->inner) { CUDA_TRY(launch_inner(ib, s)); n++; B->fam_launches[F_RLE]++; }
-  for (auto& rb : B->rle) {
-    CUDA_TRY(launch_rle(rb, s));
-    CUDA_TRY(launch_rle_big(rb, s));
-    n += 2;
-    B->fam_launches[F_RLE] += 2;
+  // fork: with several families each runs on its own stream (the latency-bound scan/RLE chains overlap
+  // the bandwidth-bound FP kernel); a single family stays on `s`
+  const bool fork = nfam > 1 && B->e;
+  if (fork) {
+    if (!B->fork) {
+      CUDA_TRY(cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming));
+      for (auto& ev : B->join) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(B->fork, s));
   }
-  t1(F_RLE, a);
-  a = t0(F_LZ4, !B->lz4.empty());
-  for (auto& lb : B->lz4) { CUDA_TRY(launch_lz4(lb, s)); n++; B->fam_launches[F_LZ4]++; }
-  t1(F_LZ4, a);
-  a = t0(F_COPY, !B->copies.empty() || !B->zero_offsets.empty());
-  for (auto& c : B->copies) { CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, s)); B->fam_launches[F_COPY]++; }
-  for (void* p : B->zero_offsets) CUDA_TRY(cudaMemsetAsync(p, 0, 4, s));
-  t1(F_COPY, a);
+  for (int fam = 0; fam < 5; fam++) {
+    if (!has[fam]) continue;
+    cudaStream_t fs = fork ? engine_family_stream(B->e, fam) : s;
+    if (fork) CUDA_TRY(cudaStreamWaitEvent(fs, B->fork, 0));
+    cudaEvent_t ta = nullptr;
+    if (B->timing) { ta = ev_get(B, evk++); CUDA_TRY(cudaEventRecord(ta, fs)); }
+    switch (fam) {
+      case F_FP:
+        for (size_t i = 0; i < B->fp.size(); i++) { CUDA_TRY(launch_fp(B->fp[i], B->fp_maxw[i], fs)); n++; B->fam_launches[F_FP]++; }
+        break;
+      case F_SCAN:
+        for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, fs)); n++; B->fam_launches[F_SCAN]++; }
+        break;
+      case F_RLE:
+        for (auto& ib : B->inner) { CUDA_TRY(launch_inner(ib, fs)); n++; B->fam_launches[F_RLE]++; }
+        for (auto& rb : B->rle) {
+          CUDA_TRY(launch_rle(rb, fs));
+          n++;
+          B->fam_launches[F_RLE]++;
+          if (rb.big_enabled) {
+            CUDA_TRY(launch_rle_big(rb, fs));
+            n++;
+            B->fam_launches[F_RLE]++;
+          }
+        }
+        break;
+      case F_LZ4:
+        for (auto& lb : B->lz4) { CUDA_TRY(launch_lz4(lb, fs)); n++; B->fam_launches[F_LZ4]++; }
+        break;
+      case F_COPY:
+        for (auto& c : B->copies) { CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, fs)); B->fam_launches[F_COPY]++; }
+        for (void* p : B->zero_offsets) CUDA_TRY(cudaMemsetAsync(p, 0, 4, fs));
+        break;
+    }
+    if (B->timing) {
+      cudaEvent_t tb = ev_get(B, evk++);
+      CUDA_TRY(cudaEventRecord(tb, fs));
+      B->pending.push_back({fam, ta, tb});
+    }
+    if (fork) {
+      CUDA_TRY(cudaEventRecord(B->join[fam], fs));
+      CUDA_TRY(cudaStreamWaitEvent(s, B->join[fam], 0));
+    }
+  }
   if (nl) *nl = n;
   return CDM_OK;
 }
@@ -711,35 +738,49 @@ struct cdm_engine {
     uint8_t* dev = nullptr;
     cudaEvent_t copied = nullptr, freed = nullptr;
     bool used = false;
-    uint8_t* arena = nullptr;  // per-slot decode scratch (chunks decode one at a time per slot)
+    uint8_t* arena = nullptr;  // decode scratch of the group held by this slot
     size_t arena_bytes = 0;
   };
   std::vector<Slot> slots;
   uint32_t next_slot = 0;
+  struct Group {  // chunks copied + decoded together from one slot
+    cudaEvent_t done = nullptr;
+    uint32_t err_pos = 0, njobs = 0, pending = 0;
+    bool harvested = false;
+  };
   struct Ticket {
     cdm_result res{};
-    cudaEvent_t done = nullptr;
-    uint32_t slot = 0;
-    uint32_t err_pos = 0;
-    bool harvested = false;
-    std::unique_ptr<cdm_batch> batch;
+    uint64_t group = 0;
+    uint32_t index = 0;  // position in the group
   };
+  std::map<uint64_t, Group> groups;
   std::map<uint64_t, Ticket> tickets;
-  std::map<uint32_t, uint64_t> slot_ticket;  // slot -> last ticket decoded in it
-  uint64_t next_ticket = 1;
-  uint32_t* err_host = nullptr;  // pinned ring of per-ticket error words
-  uint32_t err_ring = 0;
-  std::map<uint32_t, uint64_t> err_owner;  // ring position -> ticket whose word lives there
+  uint64_t next_ticket = 1, next_group = 1;
+  std::vector<cudaEvent_t> event_pool;
+  cudaStream_t fam[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // concurrent kernel families
+  uint32_t* err_host = nullptr;  // pinned ring of per-chunk error words
+  uint32_t err_ring = 0, err_next = 0;
+  std::map<uint32_t, uint64_t> err_owner;  // ring start position -> group whose words live there
 };
 
-static cdm_status harvest(cdm_engine* e, cdm_engine::Ticket& t) {
-  if (t.harvested) return CDM_OK;
-  CUDA_TRY(cudaEventSynchronize(t.done));
-  uint32_t w = e->err_host[t.err_pos];
-  t.res.error_bits = w;
-  t.res.status = w ? CDM_E_CORRUPT : CDM_OK;
-  t.harvested = true;
-  t.batch.reset();
+static cudaStream_t engine_family_stream(cdm_engine* e, int fam) { return e->fam[fam]; }
+
+static cdm_status harvest_group(cdm_engine* e, uint64_t gid) {
+  auto it = e->groups.find(gid);
+  if (it == e->groups.end()) return CDM_OK;
+  cdm_engine::Group& g = it->second;
+  if (g.harvested) return CDM_OK;
+  CUDA_TRY(cudaEventSynchronize(g.done));
+  for (auto& kv : e->tickets)
+    if (kv.second.group == gid) {
+      const uint32_t w = e->err_host[g.err_pos + kv.second.index];
+      kv.second.res.error_bits = w;
+      kv.second.res.status = w ? CDM_E_CORRUPT : CDM_OK;
+    }
+  g.harvested = true;
+  e->event_pool.push_back(g.done);
+  g.done = nullptr;
+  e->err_owner.erase(g.err_pos);
   return CDM_OK;
 }
 
@@ -761,13 +802,14 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   else { CUDA_TRY(cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking)); e->own_copy = true; }
   if (o.decode_stream) e->decode = static_cast<cudaStream_t>(o.decode_stream);
   else { CUDA_TRY(cudaStreamCreateWithFlags(&e->decode, cudaStreamNonBlocking)); e->own_decode = true; }
+  for (auto& fs : e->fam) CUDA_TRY(cudaStreamCreateWithFlags(&fs, cudaStreamNonBlocking));
   e->slots.resize(o.n_slots);
   for (auto& s : e->slots) {
     if (cudaMalloc(&s.dev, o.slot_bytes) != cudaSuccess) return fail(CDM_E_OOM, "staging slot cudaMalloc failed");
     CUDA_TRY(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
   }
-  e->err_ring = 1024;
+  e->err_ring = 4096;
   CUDA_TRY(cudaHostAlloc(&e->err_host, sizeof(uint32_t) * e->err_ring, cudaHostAllocDefault));
   *out = e.release();
   return CDM_OK;
@@ -778,8 +820,8 @@ extern "C" CDM_API cdm_status cdm_engine_destroy(cdm_engine* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->copy);
   cudaStreamSynchronize(e->decode);
-  for (auto& kv : e->tickets) if (kv.second.done) cudaEventDestroy(kv.second.done);
-  e->tickets.clear();
+  for (auto& kv : e->groups) if (kv.second.done) cudaEventDestroy(kv.second.done);
+  for (auto ev : e->event_pool) cudaEventDestroy(ev);
   for (auto& s : e->slots) {
     cudaFree(s.dev);
     cudaFree(s.arena);
@@ -787,6 +829,7 @@ extern "C" CDM_API cdm_status cdm_engine_destroy(cdm_engine* e) {
     cudaEventDestroy(s.freed);
   }
   if (e->err_host) cudaFreeHost(e->err_host);
+  for (auto fs : e->fam) if (fs) { cudaStreamSynchronize(fs); cudaStreamDestroy(fs); }
   if (e->own_copy) cudaStreamDestroy(e->copy);
   if (e->own_decode) cudaStreamDestroy(e->decode);
   delete e;
@@ -818,37 +861,53 @@ extern "C" CDM_API cdm_status cdm_chunk_check(const cdm_cascade* c, const void* 
   return bind_job(job, &b);
 }
 
-static cdm_status submit_one(cdm_engine* e, const cdm_job& job, uint64_t* ticket) {
-  Bound b;
-  cdm_status st = bind_job(job, &b);
-  if (st) return st;
-  if (b.total > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "chunk larger than a staging slot");
+// H4: one group = consecutive jobs copied into one staging slot (a single H2D copy when their host bytes
+// are contiguous) and decoded by one multi-chunk batch after the copy's event.  The copy stream waits on
+// the slot's `freed` event, so copies of later groups run ahead of decodes without host stalls.
+static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std::vector<const cdm_job*>& js,
+                               uint64_t* tickets_out) {
   const uint32_t si = e->next_slot;
   e->next_slot = (e->next_slot + 1) % uint32_t(e->slots.size());
   cdm_engine::Slot& s = e->slots[si];
-  // the slot's previous chunk must be decoded before its bytes are overwritten: the copy stream waits
-  // on the slot's `freed` event (no host stall)
   if (s.used) CUDA_TRY(cudaStreamWaitEvent(e->copy, s.freed, 0));
-  const uint64_t id = e->next_ticket++;
-  const uint32_t pos = uint32_t(id % e->err_ring);
-  {  // the pinned error word at `pos` may still belong to an unharvested ticket
-    auto ow = e->err_owner.find(pos);
-    if (ow != e->err_owner.end()) {
-      auto t = e->tickets.find(ow->second);
-      if (t != e->tickets.end()) { st = harvest(e, t->second); if (st) return st; }
+  // Lay the chunks out in the slot in host-address order: host-contiguous neighbours (gap < 4 KiB,
+  // 16-byte aligned) keep their relative offsets and share one H2D copy; others start a new copy at the
+  // next 256-byte boundary.  Decode order inside the batch does not depend on this layout.
+  std::vector<size_t> by_addr(bs.size());
+  std::iota(by_addr.begin(), by_addr.end(), size_t(0));
+  std::sort(by_addr.begin(), by_addr.end(), [&](size_t a, size_t b) { return js[a]->host_chunk < js[b]->host_chunk; });
+  std::vector<size_t> off(bs.size());
+  size_t pos = 0, k = 0;
+  while (k < by_addr.size()) {
+    const size_t first = by_addr[k];
+    const uint8_t* h0 = static_cast<const uint8_t*>(js[first]->host_chunk);
+    pos = (pos + 255) & ~size_t(255);
+    off[first] = pos;
+    size_t end = bs[first].total;  // bytes of the merged copy so far (relative to h0)
+    size_t m = k + 1;
+    while (m < by_addr.size()) {
+      const size_t j = by_addr[m];
+      const uint8_t* h = static_cast<const uint8_t*>(js[j]->host_chunk);
+      const size_t rel = size_t(h - h0);
+      if (rel < end || rel > end + 4096 || rel % 16 || pos + rel + bs[j].total > e->opts.slot_bytes) break;
+      off[j] = pos + rel;
+      end = rel + bs[j].total;
+      m++;
     }
-    e->err_owner[pos] = id;
+    if (pos + end > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "group larger than a staging slot");
+    CUDA_TRY(cudaMemcpyAsync(s.dev + pos, h0, end, cudaMemcpyHostToDevice, e->copy));
+    pos += end;
+    k = m;
   }
-  // H4: PCIe H2D copy of the compressed chunk on the copy stream
-  CUDA_TRY(cudaMemcpyAsync(s.dev, job.host_chunk, b.total, cudaMemcpyHostToDevice, e->copy));
   CUDA_TRY(cudaEventRecord(s.copied, e->copy));
   CUDA_TRY(cudaStreamWaitEvent(e->decode, s.copied, 0));
-  // decode from the slot with the slot's own scratch arena
   auto batch = std::make_unique<cdm_batch>();
   batch->e = e;
   batch->device = e->device;
-  b.dev_chunk = s.dev;
-  batch->jobs.push_back(b);
+  for (size_t j = 0; j < bs.size(); j++) {
+    bs[j].dev_chunk = s.dev + off[j];
+    batch->jobs.push_back(bs[j]);
+  }
   Alloc sizing;
   size_t zb = 0;
   size_t need = layout_batch(batch.get(), sizing, &zb);
@@ -858,35 +917,65 @@ static cdm_status submit_one(cdm_engine* e, const cdm_job& job, uint64_t* ticket
     if (cudaMalloc(&s.arena, cap) != cudaSuccess) return fail(CDM_E_OOM, "scratch cudaMalloc failed");
     s.arena_bytes = cap;
   }
-  st = batch_build(batch.get(), s.arena, s.arena_bytes);
+  cdm_status st = batch_build(batch.get(), s.arena, s.arena_bytes);
   if (st) return st;
-  CUDA_TRY(cudaMemsetAsync(s.arena, 0, batch->zero_bytes, e->decode));  // fresh tickets/flags per chunk
+  CUDA_TRY(cudaMemsetAsync(s.arena, 0, batch->zero_bytes, e->decode));  // fresh tickets/flags per group
   uint32_t nl = 0;
   st = batch_enqueue(batch.get(), e->decode, &nl);
   if (st) return st;
-  CUDA_TRY(cudaMemcpyAsync(e->err_host + pos, batch->err_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, e->decode));
+  // pinned error words for this group (contiguous ring slice; an old group still there is harvested)
+  const uint32_t nj = uint32_t(bs.size());
+  if (nj > e->err_ring) return fail(CDM_E_CAPACITY, "too many chunks in one group");
+  if (e->err_next + nj > e->err_ring) e->err_next = 0;
+  const uint32_t ep = e->err_next;
+  e->err_next += nj;
+  for (auto it = e->err_owner.begin(); it != e->err_owner.end();) {
+    const uint32_t p0 = it->first;
+    const auto& g = e->groups[it->second];
+    if (p0 < ep + nj && p0 + g.njobs > ep) {
+      const uint64_t gid = it->second;
+      ++it;
+      st = harvest_group(e, gid);
+      if (st) return st;
+    } else {
+      ++it;
+    }
+  }
+  CUDA_TRY(cudaMemcpyAsync(e->err_host + ep, batch->err_dev, sizeof(uint32_t) * nj, cudaMemcpyDeviceToHost, e->decode));
   CUDA_TRY(cudaEventRecord(s.freed, e->decode));
   s.used = true;
-  cdm_engine::Ticket& t = e->tickets[id];
-  CUDA_TRY(cudaEventCreateWithFlags(&t.done, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventRecord(t.done, e->decode));
-  t.slot = si;
-  t.err_pos = pos;
-  t.res.rows = b.rows;
-  t.res.payload_bytes = b.payload;
-  t.res.offsets_bytes = b.offsets_bytes;
-  t.res.compressed_bytes = b.total;
-  t.res.chunk_id = b.chunk_id;
-  t.batch = std::move(batch);
-  e->slot_ticket[si] = id;
-  *ticket = id;
+  const uint64_t gid = e->next_group++;
+  cdm_engine::Group& g = e->groups[gid];
+  if (!e->event_pool.empty()) { g.done = e->event_pool.back(); e->event_pool.pop_back(); }
+  else CUDA_TRY(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(g.done, e->decode));
+  g.err_pos = ep;
+  g.njobs = nj;
+  g.pending = nj;
+  e->err_owner[ep] = gid;
+  for (uint32_t j = 0; j < nj; j++) {
+    const uint64_t id = e->next_ticket++;
+    cdm_engine::Ticket& t = e->tickets[id];
+    t.group = gid;
+    t.index = j;
+    t.res.rows = bs[j].rows;
+    t.res.payload_bytes = bs[j].payload;
+    t.res.offsets_bytes = bs[j].offsets_bytes;
+    t.res.compressed_bytes = bs[j].total;
+    t.res.chunk_id = bs[j].chunk_id;
+    tickets_out[j] = id;
+  }
   return CDM_OK;
 }
 
 extern "C" CDM_API cdm_status cdm_submit(cdm_engine* e, const cdm_job* job, uint64_t* ticket) {
   if (!e || !job || !ticket) return fail(CDM_E_INVALID_ARG, "null argument");
   CUDA_TRY(cudaSetDevice(e->device));
-  return submit_one(e, *job, ticket);
+  std::vector<Bound> bs(1);
+  cdm_status st = bind_job(*job, &bs[0]);
+  if (st) return st;
+  if (bs[0].total > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "chunk larger than a staging slot");
+  return submit_group(e, bs, {job}, ticket);
 }
 
 // H3: Johnson's rule on (t_i = compressed / PCIe, d_i = decoded / decode rate):
@@ -911,22 +1000,45 @@ extern "C" CDM_API cdm_status cdm_johnson_order(const double* t, const double* d
 extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* jobs, size_t n, uint64_t* tickets) {
   if (!e || (n && (!jobs || !tickets))) return fail(CDM_E_INVALID_ARG, "null argument");
   CUDA_TRY(cudaSetDevice(e->device));
+  std::vector<Bound> all(n);
+  uint64_t total = 0;
+  for (size_t i = 0; i < n; i++) {
+    cdm_status st = bind_job(jobs[i], &all[i]);
+    if (st) { g_last = "job " + std::to_string(i) + ": " + g_last; return st; }
+    if (all[i].total > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "chunk larger than a staging slot");
+    total += all[i].total;
+  }
   std::vector<size_t> order(n);
   std::iota(order.begin(), order.end(), size_t(0));
   if (e->opts.order_policy == 1) {
     std::vector<double> tt(n), dd(n);
     for (size_t i = 0; i < n; i++) {
-      cdm_result info{};
-      cdm_status st = cdm_chunk_info(jobs[i].host_chunk, jobs[i].chunk_bytes, &info);
-      if (st) return st;
-      tt[i] = double(info.compressed_bytes) / (e->opts.pcie_gbps * 1e9);
-      dd[i] = double(info.payload_bytes + info.offsets_bytes) / (e->opts.decode_gbps * 1e9);
+      tt[i] = double(all[i].total) / (e->opts.pcie_gbps * 1e9);
+      dd[i] = double(all[i].payload + all[i].offsets_bytes) / (e->opts.decode_gbps * 1e9);
     }
     johnson(tt.data(), dd.data(), n, &order);
   }
-  for (size_t k = 0; k < n; k++) {
-    cdm_status st = submit_one(e, jobs[order[k]], &tickets[order[k]]);
+  // groups: consecutive jobs (in issue order) up to a target size, so several groups pipeline
+  const uint64_t target = std::min<uint64_t>(e->opts.slot_bytes, std::max<uint64_t>(2ull << 20, total / 8));
+  size_t k = 0;
+  while (k < n) {
+    std::vector<Bound> bs;
+    std::vector<const cdm_job*> js;
+    uint64_t bytes = 0;
+    size_t m = k;
+    while (m < n && js.size() < size_t(kMaxBatch)) {
+      const uint64_t add = ((all[order[m]].total + 255) & ~uint64_t(255)) + 4096;
+      if (!js.empty() && (bytes + add > e->opts.slot_bytes || bytes >= target)) break;
+      bytes += add;
+      bs.push_back(all[order[m]]);
+      js.push_back(&jobs[order[m]]);
+      m++;
+    }
+    std::vector<uint64_t> tk(bs.size());
+    cdm_status st = submit_group(e, bs, js, tk.data());
     if (st) return st;
+    for (size_t j = 0; j < bs.size(); j++) tickets[order[k + j]] = tk[j];
+    k = m;
   }
   return CDM_OK;
 }
@@ -935,13 +1047,15 @@ extern "C" CDM_API cdm_status cdm_wait(cdm_engine* e, uint64_t ticket, cdm_resul
   if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
   auto it = e->tickets.find(ticket);
   if (it == e->tickets.end()) return fail(CDM_E_BUSY, "unknown or consumed ticket");
-  cdm_status st = harvest(e, it->second);
+  const uint64_t gid = it->second.group;
+  cdm_status st = harvest_group(e, gid);
   if (st) return st;
   if (out) *out = it->second.res;
   cdm_status r = it->second.res.error_bits ? CDM_E_CORRUPT : CDM_OK;
   if (r) g_last = "chunk " + std::to_string(it->second.res.chunk_id) + ": device error bits " + std::to_string(it->second.res.error_bits);
-  cudaEventDestroy(it->second.done);
   e->tickets.erase(it);
+  auto g = e->groups.find(gid);
+  if (g != e->groups.end() && --g->second.pending == 0) e->groups.erase(g);
   return r;
 }
 
@@ -949,8 +1063,10 @@ extern "C" CDM_API cdm_status cdm_synchronize(cdm_engine* e) {
   if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
   CUDA_TRY(cudaStreamSynchronize(e->copy));
   CUDA_TRY(cudaStreamSynchronize(e->decode));
-  for (auto& kv : e->tickets) {
-    cdm_status st = harvest(e, kv.second);
+  std::vector<uint64_t> gids;
+  for (auto& kv : e->groups) gids.push_back(kv.first);
+  for (uint64_t gid : gids) {
+    cdm_status st = harvest_group(e, gid);
     if (st) return st;
   }
   return CDM_OK;
