@@ -179,6 +179,22 @@ __device__ __forceinline__ void lb_tile(uint4* words, uint32_t gt, uint32_t firs
   *pw = w;
 }
 
+// ------------------------------------------------------------------ tracing (CDM_TRACE)
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+// stamp phase k of tile gt (thread 0 only; no-op unless the launch carries a trace buffer)
+__device__ __forceinline__ void trace_stamp(uint64_t* trace, uint32_t gt, int k) {
+  if (trace && threadIdx.x == 0) trace[uint64_t(gt) * 8 + k] = k == 7 ? smid() : globaltimer();
+}
+
 // ------------------------------------------------------------------ block scans (256 threads)
 // Exclusive scan of one u64 per thread across the CTA; returns the exclusive prefix, *total = sum.
 template <int NT>

@@ -66,6 +66,7 @@ struct ScanDesc {
 struct ScanBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   unsigned long long* ticket;  // epoch|ticket counter
   uint4* lb;                   // [total_tiles] 16-byte look-back words
@@ -130,6 +131,7 @@ struct RleBig {  // queue of oversize tiles, expanded by rle_big
 struct RleBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   unsigned long long* ticket;
   uint4* lb;
@@ -165,6 +167,7 @@ struct InnerDesc {
 struct InnerBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   unsigned long long* ticket;
   uint4* lb;

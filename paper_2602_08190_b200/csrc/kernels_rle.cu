@@ -104,10 +104,17 @@ __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__
   __syncthreads();
   const uint32_t gt = tile_s, epoch = epoch_s;
   if (gt >= B.total_tiles) return;
+  trace_stamp(B.trace, gt, 0);
+  trace_stamp(B.trace, gt, 7);
   const InnerDesc& D = B.d[find_desc(B, gt)];
   const uint32_t lt = gt - D.tile0;
   const uint32_t j0 = lt * kInnerTile;
   const uint32_t nvalid = min(uint32_t(kInnerTile), D.n_inner - j0);
+  if (B.trace && tid == 0) {  // stamp 5: descriptor fields resident
+    volatile uint64_t sink = D.dc_base + D.dv_base + D.dc_w + D.dv_w + uint64_t(D.dc_packed) + D.n_outer;
+    (void)sink;
+    trace_stamp(B.trace, gt, 5);
+  }
 
   uint64_t dc[kIPer], dv[kIPer];
   uint64_t sc = 0, sw = 0;
@@ -126,12 +133,15 @@ __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__
     sc += dc[r];
     sw += dv[r] * dc[r];
   }
+  trace_stamp(B.trace, gt, 1);
   uint64_t tc, tw;
   const uint64_t ec = block_excl_scan_u64<kThreads>(sc, warp_s, &tc);
   const uint64_t ew = block_excl_scan_u64<kThreads>(sw, warp_s, &tw);
+  trace_stamp(B.trace, gt, 2);
   if (tid < 32) {
     uint64_t p0, p1;
     lb_tile(B.lb, gt, D.tile0, epoch, tc, tw, &p0, &p1);
+    trace_stamp(B.trace, gt, 3);
     if (tid == 0) {
       pc_s = p0;
       pw_s = p1;
@@ -160,6 +170,7 @@ __global__ void __launch_bounds__(kThreads) inner_kernel(const __grid_constant__
     c += dc[r];
     wsum += dv[r] * dc[r];
   }
+  trace_stamp(B.trace, gt, 4);
 }
 
 // ------------------------------------------------------------------------------------------ main
@@ -187,6 +198,8 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
   __syncthreads();
   const uint32_t gt = tile_s, epoch = epoch_s;
   if (gt >= B.total_tiles) return;
+  trace_stamp(B.trace, gt, 0);
+  trace_stamp(B.trace, gt, 7);
   const RleDesc& D = B.d[find_desc(B, gt)];
   const uint32_t lt = gt - D.tile0;
   const uint32_t g0 = lt * K;
@@ -222,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
     }
   }
 
+  trace_stamp(B.trace, gt, 5);  // window staged
   uint64_t cnt[kRPer], val[kRPer];
   uint64_t sc = 0, sw = 0;
   {
@@ -266,14 +280,17 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       if (vmode == V_LINEAR) sw += val[r] * cnt[r];
     }
   }
+  trace_stamp(B.trace, gt, 1);
   uint64_t T, W = 0;
   const uint64_t ec = block_excl_scan_u64<kThreads>(sc, warp_s, &T);
   uint64_t ew = 0;
   if (vmode == V_LINEAR) ew = block_excl_scan_u64<kThreads>(sw, warp_s, &W);
+  trace_stamp(B.trace, gt, 2);
 
   if (tid < 32) {
     uint64_t p0, p1;
     lb_tile(B.lb, gt, D.tile0, epoch, T, W, &p0, &p1);
+    trace_stamp(B.trace, gt, 3);
     if (tid == 0) {
       pc_s = p0;
       pw_s = p1;
@@ -317,6 +334,8 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
     const uint32_t span = ((Tt + kThreads - 1) / kThreads) * 32;
     const uint32_t pb = min(Tt, warp * span), pe = min(Tt, pb + span);
     expand_warp(soffs_s, nr, vals_s, slopes, pb, pe, out, D.out_bytes);
+    __syncthreads();
+    trace_stamp(B.trace, gt, 4);
   } else {
     __shared__ uint32_t slot_s;
     if (tid == 0) {

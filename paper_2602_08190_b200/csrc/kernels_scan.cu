@@ -50,6 +50,8 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
   __syncthreads();
   const uint32_t gt = tile_s, epoch = epoch_s;
   if (gt >= B.total_tiles) return;
+  trace_stamp(B.trace, gt, 0);
+  trace_stamp(B.trace, gt, 7);
   const ScanDesc& D = B.d[find_desc_scan(B, gt)];
   const uint32_t lt = gt - D.tile0;
   const uint32_t w = D.w;
@@ -78,13 +80,16 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
     run += x;
     v[j] = run;  // inclusive within the thread
   }
+  trace_stamp(B.trace, gt, 1);
   uint64_t tile_total;
   const uint64_t texcl = block_excl_scan_u64<kThreads>(run, warp_s, &tile_total);
+  trace_stamp(B.trace, gt, 2);
 
   // decoupled look-back (warp 0)
   if (tid < 32) {
     uint64_t pc, p0;
     lb_tile(B.lb, gt, D.tile0, epoch, 0, tile_total, &pc, &p0);
+    trace_stamp(B.trace, gt, 3);
     if (tid == 0) {
       prefix_s = p0;
       if (D.mode == SCAN_OFFSETS && lt + 1 == D.ntiles && p0 + tile_total != D.base)
@@ -129,6 +134,8 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
     for (uint32_t i = tid; i < valid; i += kThreads) o[i] = int32_t(uint32_t(res_s[i]));
     if (lt == 0 && tid == 0) reinterpret_cast<int32_t*>(D.out)[0] = 0;
   }
+  __syncthreads();
+  trace_stamp(B.trace, gt, 4);
 }
 
 }  // namespace

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -568,6 +569,12 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     B->rle.push_back(rb);
   }
   *zero_bytes = A.off;
+  // ---- non-zeroed region: optional per-tile trace (env CDM_TRACE=<csv path>)
+  if (std::getenv("CDM_TRACE")) {
+    for (auto& sb : B->scan) sb.trace = A.take<uint64_t>(size_t(sb.total_tiles) * 8);
+    for (auto& ib : B->inner) ib.trace = A.take<uint64_t>(size_t(ib.total_tiles) * 8);
+    for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
+  }
   // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
   std::map<int, InnerDesc*> inner_of;
   for (auto& ib : B->inner)
@@ -870,9 +877,9 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
   e->next_slot = (e->next_slot + 1) % uint32_t(e->slots.size());
   cdm_engine::Slot& s = e->slots[si];
   if (s.used) CUDA_TRY(cudaStreamWaitEvent(e->copy, s.freed, 0));
-  // Lay the chunks out in the slot in host-address order: host-contiguous neighbours (gap < 4 KiB,
-  // 16-byte aligned) keep their relative offsets and share one H2D copy; others start a new copy at the
-  // next 256-byte boundary.  Decode order inside the batch does not depend on this layout.
+  // Lay the chunks out in the slot in host-address order: exactly contiguous host neighbours keep their
+  // relative offsets and share one H2D copy (if the driver rejects a copy spanning two host allocations,
+  // the run is copied chunk by chunk).  Decode order inside the batch does not depend on this layout.
   std::vector<size_t> by_addr(bs.size());
   std::iota(by_addr.begin(), by_addr.end(), size_t(0));
   std::sort(by_addr.begin(), by_addr.end(), [&](size_t a, size_t b) { return js[a]->host_chunk < js[b]->host_chunk; });
@@ -883,19 +890,28 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
     const uint8_t* h0 = static_cast<const uint8_t*>(js[first]->host_chunk);
     pos = (pos + 255) & ~size_t(255);
     off[first] = pos;
-    size_t end = bs[first].total;  // bytes of the merged copy so far (relative to h0)
+    size_t end = bs[first].total;
     size_t m = k + 1;
     while (m < by_addr.size()) {
       const size_t j = by_addr[m];
-      const uint8_t* h = static_cast<const uint8_t*>(js[j]->host_chunk);
-      const size_t rel = size_t(h - h0);
-      if (rel < end || rel > end + 4096 || rel % 16 || pos + rel + bs[j].total > e->opts.slot_bytes) break;
-      off[j] = pos + rel;
-      end = rel + bs[j].total;
+      if (static_cast<const uint8_t*>(js[j]->host_chunk) != h0 + end || bs[j].total % 16 ||
+          pos + end + bs[j].total > e->opts.slot_bytes)
+        break;
+      off[j] = pos + end;
+      end += bs[j].total;
       m++;
     }
     if (pos + end > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "group larger than a staging slot");
-    CUDA_TRY(cudaMemcpyAsync(s.dev + pos, h0, end, cudaMemcpyHostToDevice, e->copy));
+    cudaError_t ce = cudaMemcpyAsync(s.dev + pos, h0, end, cudaMemcpyHostToDevice, e->copy);
+    if (ce == cudaErrorInvalidValue && m > k + 1) {
+      cudaGetLastError();
+      for (size_t q = k; q < m; q++) {
+        const size_t j = by_addr[q];
+        CUDA_TRY(cudaMemcpyAsync(s.dev + off[j], js[j]->host_chunk, bs[j].total, cudaMemcpyHostToDevice, e->copy));
+      }
+    } else if (ce != cudaSuccess) {
+      return fail(CDM_E_CUDA, std::string("H2D copy: ") + cudaGetErrorString(ce));
+    }
     pos += end;
     k = m;
   }
@@ -1101,6 +1117,27 @@ extern "C" CDM_API cdm_status cdm_batch_launch(cdm_batch* b, void* stream, uint3
   return batch_enqueue(b, s, n_launches);
 }
 
+// CDM_TRACE: append "kernel,launch,tile,t_start,t_unpacked,t_scanned,t_lookback,t_end,smid" rows (ns)
+static void dump_trace(cdm_batch* b, const char* path) {
+  FILE* f = std::fopen(path, "a");
+  if (!f) return;
+  auto dump = [&](const char* name, int li, uint64_t* dev, uint32_t tiles) {
+    if (!dev || !tiles) return;
+    std::vector<uint64_t> h(size_t(tiles) * 8);
+    if (cudaMemcpy(h.data(), dev, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    for (uint32_t t = 0; t < tiles; t++) {
+      const uint64_t* r = &h[size_t(t) * 8];
+      std::fprintf(f, "%s,%d,%u,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", name, li, t, (unsigned long long)r[0],
+                   (unsigned long long)r[1], (unsigned long long)r[2], (unsigned long long)r[3],
+                   (unsigned long long)r[4], (unsigned long long)r[7], (unsigned long long)r[5]);
+    }
+  };
+  for (size_t i = 0; i < b->scan.size(); i++) dump("scan", int(i), b->scan[i].trace, b->scan[i].total_tiles);
+  for (size_t i = 0; i < b->inner.size(); i++) dump("inner", int(i), b->inner[i].trace, b->inner[i].total_tiles);
+  for (size_t i = 0; i < b->rle.size(); i++) dump("rle", int(i), b->rle[i].trace, b->rle[i].total_tiles);
+  std::fclose(f);
+}
+
 extern "C" CDM_API cdm_status cdm_batch_results(cdm_batch* b, void* stream, cdm_result* results) {
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   CUDA_TRY(cudaSetDevice(b->device));
@@ -1114,6 +1151,7 @@ extern "C" CDM_API cdm_status cdm_batch_results(cdm_batch* b, void* stream, cdm_
     b->fam_ms[p.fam] += ms;
   }
   b->pending.clear();
+  if (const char* path = std::getenv("CDM_TRACE")) dump_trace(b, path);
   if (results) fill_results(b, b->err_host, results);
   for (size_t i = 0; i < b->jobs.size(); i++)
     if (b->err_host[i]) {
