@@ -39,13 +39,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "effective decoded GB/s (host-compressed→device-decoded) at 1/2/4/8 B200 vs roofline"
-WORKLOAD = [("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"),
-            ("l_quantity", "Dict|BitPack"),
-            ("l_discount", "Dict|BitPack")]
+WORKLOADS = {
+    # BASELINE configs[1] (the default / headline): TPC-H SF=1 lineitem numeric columns
+    "config2": dict(sf=1.0, dtype="int64", cols=[("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"),
+                                                  ("l_quantity", "Dict|BitPack"),
+                                                  ("l_discount", "Dict|BitPack")],
+                    desc="config 2: TPC-H SF=1 lineitem numeric columns (l_orderkey RLE|[Delta|RLE|[BitPack,BitPack],"
+                         "BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack)"),
+    # BASELINE configs[2]: TPC-H SF=10 lineitem string columns (dictionary CHAR(n) + chunk-parallel LZ4)
+    "config3": dict(sf=10.0, dtype="u8", cols=[("l_shipmode", "Dict|BitPack"), ("l_returnflag", "Dict|BitPack"),
+                                                ("l_comment", "Str|[LZ4,BitPack]")],
+                    desc="config 3: TPC-H SF=10 lineitem string columns (l_shipmode/l_returnflag Dict|BitPack CHAR(n), "
+                         "l_comment Str|[LZ4(64 KiB sub-chunks),BitPack])"),
+    # BASELINE configs[0]: the oracle-sized parity case (launch-bound: 4 MB decoded)
+    "config1": dict(sf=None, dtype="int32", cols=[("config1", "BitPack")],
+                    desc="config 1: 1M int32, FOR + 8-bit bit-packing, one chunk"),
+}
 CHUNK_ROWS = 1 << 22
-SF = 1.0
 FAMILY_NAMES = ["fp", "scan", "rle", "lz4", "copy"]
-FAMILY_KERNELS = {"fp": "fp_kernel", "scan": "scan_kernel", "rle": "inner_kernel+rle_kernel+rle_big_kernel",
+FAMILY_KERNELS = {"fp": "fp_kernel", "scan": "scan_kernel", "rle": "rle_prep_kernel+rle_kernel(+rle_big_kernel)",
                   "lz4": "lz4_kernel", "copy": "cudaMemcpyAsync D2D"}
 
 
@@ -57,17 +69,19 @@ def parse():
     p.add_argument("--impl", default="cdm", choices=["cdm", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=2.0, help="wall seconds of the oracle sample")
+    p.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     return p.parse_args()
 
 
-def build_workload(rank: int):
+def build_workload(rank: int, workload: str = "config2"):
     """Generate + encode this rank's shard (untimed).  Returns list of (name, spec, dtype, width, chunks)."""
     from paper_2602_08190_b200 import encoder
-    from paper_2602_08190_b200.inputs import TPCH, MASTER_SEED
-    g = TPCH(SF, MASTER_SEED + 1000 * rank)
+    from paper_2602_08190_b200.inputs import TPCH, MASTER_SEED, config1_column
+    wl = WORKLOADS[workload]
+    g = TPCH(wl["sf"], MASTER_SEED + 1000 * rank) if wl["sf"] else None
     cols = []
-    for name, spec in WORKLOAD:
-        col = g.column(name)
+    for name, spec in wl["cols"]:
+        col = config1_column() if name == "config1" else g.column(name)
         chunks = encoder.encode_chunks(spec, col, CHUNK_ROWS, first_chunk_id=1000 * rank)
         cols.append((name, spec, col.dtype, col.width, chunks, col.nbytes()))
     return cols
@@ -146,11 +160,18 @@ def measure_h2d(torch, nbytes=256 << 20, reps=5):
     return nbytes / best / 1e6
 
 
+def _decoded_bytes(chunk) -> int:
+    """payload + offsets bytes from a chunk header (the oracle writes both)."""
+    import oracle
+    dtype, _, rows, payload = oracle.oracle._header(chunk)
+    return int(payload) + (4 * (int(rows) + 1) if dtype == 4 else 0)
+
+
 def cpu_baseline(cols, seconds: float):
     """The oracle as it stands: plain C decode of the same chunks, chunk-parallel on the host cores."""
     import oracle
     chunks = [c for (_, _, _, _, chs, _) in cols for c in chs]
-    decoded = sum(int(oracle.oracle._header(c)[3]) for c in chunks)
+    decoded = sum(_decoded_bytes(c) for c in chunks)
     threads = min(os.cpu_count() or 1, len(chunks))
     t0 = time.perf_counter()
     passes = 0
@@ -161,7 +182,7 @@ def cpu_baseline(cols, seconds: float):
             break
     dt = time.perf_counter() - t0
     return {"value": decoded * passes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": f"{passes} full pass(es) over the {len(chunks)} config-2 chunks ({decoded / 1e6:.1f} MB decoded "
+            "sample": f"{passes} full pass(es) over the {len(chunks)} workload chunks ({decoded / 1e6:.1f} MB decoded "
                       f"each) with {threads} threads, {dt:.2f} s wall"}
 
 
@@ -169,10 +190,11 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle on this arm's workload, K timed steps after W warm-up steps."""
     if rank != 0:
         return
-    cols = build_workload(0)
+    cols = build_workload(0, args.workload)
+    wl = WORKLOADS[args.workload]
     import oracle
     chunks = [c for (_, _, _, _, chs, _) in cols for c in chs]
-    decoded = sum(int(oracle.oracle._header(c)[3]) for c in chunks)
+    decoded = sum(_decoded_bytes(c) for c in chunks)
     threads = min(os.cpu_count() or 1, len(chunks))
     for _ in range(args.warmup):
         oracle.decode_many(chunks, nthreads=threads)
@@ -183,11 +205,11 @@ def run_reference(args, rank, world):
     v = decoded * args.steps / dt / 1e9
     line = {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": "config 2: TPC-H SF=1 lineitem numeric (l_orderkey, l_quantity, l_discount)",
-                       "chunk_rows": CHUNK_ROWS, "decoded_bytes_per_step": decoded},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"],
+            "data": "synthetic", "config": {"workload": wl["desc"], "chunk_rows": CHUNK_ROWS,
+                                            "decoded_bytes_per_step": decoded},
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "oracle",
-                             "sample": f"each step = one full oracle pass over the {len(chunks)} config-2 chunks"},
+                             "sample": f"each step = one full oracle pass over the {len(chunks)} workload chunks"},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -208,9 +230,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    cols = build_workload(rank)
+    cols = build_workload(rank, args.workload)
+    wl = WORKLOADS[args.workload]
     compressed = sum(int(c.size) for (_, _, _, _, chs, _) in cols for c in chs)
-    decoded = sum(int(cdm.chunk_info(c)["payload_bytes"]) for (_, _, _, _, chs, _) in cols for c in chs)
+    decoded = sum(int(cdm.chunk_info(c)["payload_bytes"]) + int(cdm.chunk_info(c)["offsets_bytes"])
+                  for (_, _, _, _, chs, _) in cols for c in chs)
     n_chunks = sum(len(chs) for (_, _, _, _, chs, _) in cols)
 
     eng = cdm.Engine(local, n_slots=4, slot_bytes=64 << 20, order_policy=1)
@@ -302,9 +326,15 @@ def main():
         for d in decs_dev:
             info = cdm.chunk_info(d.host_chunk)
             plan = d.cascade.describe().split(" => ")[1]
-            fam = "rle" if plan.startswith(("rle", "inner")) else ("scan" if plan.startswith("scan") else
-                                                                    ("fp" if plan.startswith("fp") else "copy"))
-            fam_bytes[fam] += info["compressed_bytes"] + info["payload_bytes"] + info["offsets_bytes"]
+            if plan.startswith(("rle", "inner")):
+                fam_bytes["rle"] += info["compressed_bytes"] + info["payload_bytes"]
+            elif plan.startswith("fp"):
+                fam_bytes["fp"] += info["compressed_bytes"] + info["payload_bytes"]
+            elif "lz4" in plan:  # Str: the scan writes the offsets, the LZ4 kernel the payload bytes
+                fam_bytes["scan"] += info["offsets_bytes"]
+                fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
+            else:
+                fam_bytes["copy"] += info["compressed_bytes"] + info["payload_bytes"]
         dom = max(fam_ms, key=lambda f: fam_ms[f][0])
         dom_ms, dom_launch = fam_ms[dom]
         per_step_ms = dom_ms / args.steps
@@ -318,11 +348,10 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3 / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
             "config": {
-                "workload": "config 2: TPC-H SF=1 lineitem numeric columns (l_orderkey RLE|[Delta|RLE|[BitPack,"
-                            "BitPack],BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack), per rank",
-                "sf_per_rank": SF, "chunk_rows": CHUNK_ROWS, "chunks_per_rank": n_chunks,
+                "workload": wl["desc"] + ", per rank",
+                "sf_per_rank": wl["sf"], "chunk_rows": CHUNK_ROWS, "chunks_per_rank": n_chunks,
                 "decoded_bytes_per_step": tot_decoded, "compressed_bytes_per_step": tot_comp,
                 "compression_ratio": round(cr, 2), "parallelism": f"dp{world} (independent shards)",
                 "l2": "flushed between timed steps by a 256 MiB write outside the CUDA events",

@@ -43,6 +43,29 @@ __device__ __forceinline__ uint64_t extract_bits_global(const uint32_t* __restri
   return w == 64 ? v : (v & ((1ull << w) - 1ull));
 }
 
+// Batched form for memory-level parallelism: U fields (bit offsets off[u], same width w) -- all 3U word loads
+// are issued before any use (no branches between them), then the fields are assembled.  Reads up to two
+// words past a field; the 16-byte stream slack keeps that in bounds.
+template <int U>
+__device__ __forceinline__ void extract_bits_global_batch(const uint32_t* __restrict__ wd, const uint64_t (&off)[U],
+                                                          uint32_t w, uint64_t (&out)[U]) {
+  uint32_t a[U], b[U], c[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const uint64_t wi = off[u] >> 5;
+    a[u] = __ldg(wd + wi);
+    b[u] = __ldg(wd + wi + 1);
+    c[u] = __ldg(wd + wi + 2);
+  }
+  const uint64_t mask = w >= 64 ? ~0ull : ((1ull << w) - 1ull);
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const uint32_t sh = uint32_t(off[u] & 31);
+    const uint64_t v = (uint64_t(__funnelshift_r(b[u], c[u], sh)) << 32) | __funnelshift_r(a[u], b[u], sh);
+    out[u] = w ? (v & mask) : 0ull;
+  }
+}
+
 // ------------------------------------------------------------------ mbarrier + TMA bulk copy
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -12,9 +12,11 @@ namespace cdm {
 constexpr int kMaxBatch = 32;      // descriptors per launch (more chunks -> more launches)
 constexpr int kFpTile = 4096;      // H5 values per tile = 256 threads x 16
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
-constexpr int kRleTile = 2048;     // H7 runs per tile = 256 threads x 8
-constexpr int kInnerTile = 2048;   // Delta|RLE pre-pass inner runs per tile = 256 threads x 8
-constexpr int kRleWindow = 768;    // DRLE inner-run window staged per outer tile (larger: global search)
+constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
+constexpr int kPrepOuterTile = 8 * 2048;  // rle_prep OUTER: 8 warps x 2048 runs (two rle tiles each)
+constexpr int kPrepInnerTile = 8 * 1024;  // rle_prep INNER: 8 warps x 1024 inner runs
+constexpr int kRleOutBytes = 44 * 1024;    // rle_kernel: a tile's output is staged in shared memory (dynamic)
+constexpr int kRleWindow = 384;    // DRLE inner-run window staged per outer tile (larger: global search)
 constexpr uint32_t kRleBigLimit = 1u << 15;  // a tile with more output rows is expanded by rle_big
 constexpr uint32_t kRleBigPiece = 8192;       // rows per rle_big work item
 constexpr int kThreads = 256;
@@ -87,10 +89,11 @@ struct RleDesc {
   const uint8_t* val_packed;  // V_BP/V_DICT/V_F2I: packed values or indices; V_LINEAR: packed dv
   const uint8_t* dict;
   void* out;
-  const uint32_t* S;          // V_DRLE pre-pass outputs
+  const uint32_t* S;          // V_DRLE inner run table (from rle_prep)
   const uint64_t* Q;
   const uint64_t* DV;
   const uint32_t* tstart;
+  const uint4* prefix;        // per outer tile exclusive prefix {flag, count, w} (from rle_prep)
   uint64_t cnt_base;
   uint64_t val_base;
   uint64_t delta_base;        // V_LINEAR: Delta base
@@ -133,45 +136,52 @@ struct RleBatch {
   uint32_t total_tiles;
   uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
-  unsigned long long* ticket;
-  uint4* lb;
   uint32_t big_enabled;          // 0: rle_big is not launched -> oversize tiles are expanded in place
+  uint32_t debug;                // CDM_DEBUG_RLE bits (experiments only): 1 = skip output stores
   RleBig big;
   RleDesc d[kMaxBatch];
 };
 
-// Delta|RLE inner pre-pass (V_DRLE): scan over inner runs j producing S_j (outer-run start), Q_j
-// (base + sum_{k<j} dv_k dc_k), DV_j and tstart[t] (inner run holding outer run t*kRleTile; entry
-// tstart[outer_tiles] = n_inner - 1 closes the last window).
-struct InnerDesc {
-  const uint8_t* dv_packed;
-  const uint8_t* dc_packed;
-  uint32_t* S;
+// rle_prep: every look-back of the RLE family in ONE launch, over tiny per-tile aggregates only.
+//  PREP_OUTER: per outer tile of kRleTile runs, sum of counts (and of dv*count for arithmetic runs) ->
+//              exclusive prefix per tile, so rle_kernel never waits on a predecessor.
+//  PREP_INNER: Delta|RLE value lineage (V_DRLE): per inner run j, S_j (first outer run), Q_j (base +
+//              sum_{k<j} dv_k dc_k), DV_j, and tstart[t] (inner run holding outer run t*kRleTile;
+//              tstart[outer_tiles] = n_inner - 1 closes the last window).
+enum PrepKind : uint8_t { PREP_OUTER = 0, PREP_INNER = 1 };
+
+struct PrepDesc {
+  const uint8_t* a_packed;    // OUTER: counts;  INNER: dc
+  const uint8_t* b_packed;    // OUTER(linear): dv; INNER: dv
+  uint4* prefix;              // OUTER: [ntiles] exclusive prefixes
+  uint32_t* S;                // INNER outputs
   uint64_t* Q;
   uint64_t* DV;
   uint32_t* tstart;
-  uint64_t dv_base;
-  uint64_t dc_base;
-  uint64_t base;          // Delta base
-  uint32_t n_inner;
-  uint32_t n_outer;       // = outer RLE runs = sum of dc
+  uint64_t a_base;
+  uint64_t b_base;
+  uint64_t base;              // INNER: Delta base
+  uint32_t n_items;           // OUTER: runs; INNER: inner runs
+  uint32_t total;             // OUTER: rows (sum of counts); INNER: outer runs (sum of dc)
   uint32_t tile0;
   uint32_t ntiles;
-  uint32_t outer_tiles;   // ceil(n_outer / kRleTile)
+  uint32_t outer_tiles;       // INNER: ceil(outer runs / kRleTile); OUTER: ceil(runs / kRleTile)
   uint32_t err_idx;
-  uint16_t dv_w;
-  uint16_t dc_w;
-  uint8_t pad[4];
+  uint16_t a_w;
+  uint16_t b_w;
+  uint8_t kind;               // PrepKind
+  uint8_t linear;             // OUTER: also accumulate dv*count
+  uint8_t pad[6];
 };
 
-struct InnerBatch {
+struct PrepBatch {
   uint32_t n;
   uint32_t total_tiles;
-  uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
+  uint64_t* trace;
   uint32_t* err;
   unsigned long long* ticket;
   uint4* lb;
-  InnerDesc d[kMaxBatch];
+  PrepDesc d[kMaxBatch];
 };
 
 // ---------------------------------------------------------------- H8: chunk-sequential LZ4
@@ -197,7 +207,7 @@ struct Lz4Batch {
 // ---------------------------------------------------------------- launchers (return cudaGetLastError)
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
-cudaError_t launch_inner(const InnerBatch& b, cudaStream_t s);
+cudaError_t launch_rle_prep(const PrepBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, cudaStream_t s);

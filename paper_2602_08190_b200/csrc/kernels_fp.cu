@@ -37,11 +37,6 @@ __device__ __forceinline__ uint32_t stage_bytes(const FpDesc& D, uint32_t lt) {
   return uint32_t(want < have ? want : have);
 }
 
-// Byte-granular dictionary copy for entry widths other than 4/8 (CHAR(n) rows).
-__device__ __forceinline__ void copy_row(uint8_t* dst, const uint8_t* __restrict__ src, uint32_t E) {
-  for (uint32_t b = 0; b < E; b++) dst[b] = __ldg(src + b);
-}
-
 __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ FpBatch B) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
@@ -89,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
     const uint64_t tile_start = uint64_t(lt) * kFpTile;
     const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
     bool bad_index = false;
+    bool bytes_path = false;
 
 #pragma unroll 1
     for (uint32_t k = 0; k < 4; k++) {
@@ -134,9 +130,7 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
           if (full) st_v4_u32(o, __ldg(dict + v[0]), __ldg(dict + v[1]), __ldg(dict + v[2]), __ldg(dict + v[3]));
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
         } else {
-          const uint32_t E = D.out_bytes;
-          uint8_t* o = reinterpret_cast<uint8_t*>(D.out) + gi * E;
-          _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) copy_row(o + j * E, D.dict + v[j] * E, E);
+          bytes_path = true;  // CHAR(n) rows: 16-byte output chunks below
         }
       } else {  // FP_F2I: one IEEE division per element (no reciprocal: bit-exact, R13)
         const double p = kPow10[D.d];
@@ -148,6 +142,44 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
           st_v2_u64(o, __double_as_longlong(f[0]), __double_as_longlong(f[1]));
           st_v2_u64(o + 2, __double_as_longlong(f[2]), __double_as_longlong(f[3]));
         } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __double_as_longlong(f[j]);
+      }
+    }
+    if (bytes_path) {
+      // FP_DICT with E-byte rows (E not 4/8): the tile's output (valid*E bytes, 16-aligned since 4096*E is a
+      // multiple of 16) is produced as 16-byte chunks; each thread walks the bytes of its chunk tracking
+      // (row, column) and extracts a row's index only when the row changes.
+      const uint32_t E = D.out_bytes;
+      const uint64_t inv = (0x100000000ull + E - 1) / E;  // ceil(2^32 / E): exact for positions < 2^17
+      const uint32_t total = valid * E;
+      uint8_t* obase = reinterpret_cast<uint8_t*>(D.out) + tile_start * E;
+      const uint8_t* __restrict__ dict = D.dict;
+      for (uint32_t c = tid; c * 16 < total; c += kThreads) {
+        const uint32_t p0 = c * 16;
+        uint32_t row = uint32_t((uint64_t(p0) * inv) >> 32), col = p0 - row * E;
+        uint64_t idx = D.base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
+        if (idx >= D.entries) { bad_index = true; idx = 0; }
+        uint32_t word[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (uint32_t b = 0; b < 16; b++) {
+          if (p0 + b < total) {
+            word[b >> 2] |= uint32_t(__ldg(dict + idx * E + col)) << (8 * (b & 3));
+            if (++col == E) {
+              col = 0;
+              row++;
+              if (row < valid) {
+                idx = D.base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
+                if (idx >= D.entries) { bad_index = true; idx = 0; }
+              }
+            }
+          }
+        }
+        if (p0 + 16 <= total) {
+          st_v4_u32(obase + p0, word[0], word[1], word[2], word[3]);
+        } else {
+#pragma unroll
+          for (uint32_t b = 0; b < 16; b++)
+            if (p0 + b < total) obase[p0 + b] = uint8_t(word[b >> 2] >> (8 * (b & 3)));
+        }
       }
     }
     if (bad_index) atomicOr(B.err + D.err_idx, 0x1u);

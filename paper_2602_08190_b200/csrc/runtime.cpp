@@ -379,7 +379,7 @@ struct cdm_batch {
   std::vector<FpBatch> fp;
   std::vector<uint32_t> fp_maxw;
   std::vector<ScanBatch> scan;
-  std::vector<InnerBatch> inner;
+  std::vector<PrepBatch> prep;
   std::vector<RleBatch> rle;
   std::vector<Lz4Batch> lz4;
   struct Copy { void* dst; const void* src; size_t bytes; };
@@ -416,7 +416,7 @@ namespace {
 // Returns the arena bytes; `zero_bytes` = prefix of the arena that must start zeroed.
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
-  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->inner.clear(); B->rle.clear(); B->lz4.clear();
+  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->prep.clear(); B->rle.clear(); B->lz4.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
   B->err_dev = A.take<uint32_t>(nj ? nj : 1);
@@ -499,33 +499,65 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     sb.lb = A.take<uint4>(tiles);
     B->scan.push_back(sb);
   }
-  // inner pre-pass
-  for (auto& g : groups(drj)) {
-    InnerBatch ib{};
-    ib.err = B->err_dev;
-    uint32_t tiles = 0;
-    for (int j : g) {
-      const Bound& b = B->jobs[j];
-      InnerDesc& d = ib.d[ib.n++];
-      d.dv_packed = b.dev_chunk + b.inner_dv.off;
-      d.dc_packed = b.dev_chunk + b.inner_dc.off;
-      d.dv_base = b.inner_dv.base;
-      d.dc_base = b.inner_dc.base;
-      d.dv_w = uint16_t(b.inner_dv.w);
-      d.dc_w = uint16_t(b.inner_dc.w);
-      d.base = b.inner_base;
-      d.n_inner = b.n_inner;
-      d.n_outer = b.nruns;
-      d.tile0 = tiles;
-      d.ntiles = uint32_t(div_up(b.n_inner, kInnerTile));
-      d.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
-      d.err_idx = uint32_t(j);
-      tiles += d.ntiles;
+  // rle_prep: an OUTER descriptor per RLE chunk (tile prefixes) + an INNER one per Delta|RLE value lineage
+  struct PrepRef { int job; bool inner; };
+  std::vector<PrepDesc> pd;
+  std::vector<PrepRef> pref;
+  for (int j : rlj) {
+    const Bound& b = B->jobs[j];
+    PrepDesc o{};
+    o.kind = PREP_OUTER;
+    o.a_packed = b.dev_chunk + b.counts.off;
+    o.a_base = b.counts.base;
+    o.a_w = uint16_t(b.counts.w);
+    o.linear = b.vmode == V_LINEAR;
+    if (o.linear) { o.b_packed = b.dev_chunk + b.main.off; o.b_base = b.main.base; o.b_w = uint16_t(b.main.w); }
+    o.n_items = b.nruns;
+    o.total = uint32_t(b.rows);
+    o.ntiles = uint32_t(div_up(b.nruns, kPrepOuterTile));
+    o.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
+    o.err_idx = uint32_t(j);
+    pd.push_back(o);
+    pref.push_back({j, false});
+    if (b.vmode == V_DRLE) {
+      PrepDesc in{};
+      in.kind = PREP_INNER;
+      in.a_packed = b.dev_chunk + b.inner_dc.off;
+      in.a_base = b.inner_dc.base;
+      in.a_w = uint16_t(b.inner_dc.w);
+      in.b_packed = b.dev_chunk + b.inner_dv.off;
+      in.b_base = b.inner_dv.base;
+      in.b_w = uint16_t(b.inner_dv.w);
+      in.base = b.inner_base;
+      in.n_items = b.n_inner;
+      in.total = b.nruns;
+      in.ntiles = uint32_t(div_up(b.n_inner, kPrepInnerTile));
+      in.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
+      in.err_idx = uint32_t(j);
+      pd.push_back(in);
+      pref.push_back({j, true});
     }
-    ib.total_tiles = tiles;
-    ib.ticket = A.take<unsigned long long>(1);
-    ib.lb = A.take<uint4>(tiles);
-    B->inner.push_back(ib);
+  }
+  std::vector<std::vector<int>> pgroups;
+  for (size_t i = 0; i < pd.size(); i += kMaxBatch) {
+    std::vector<int> g;
+    for (size_t k = i; k < std::min(pd.size(), i + size_t(kMaxBatch)); k++) g.push_back(int(k));
+    pgroups.push_back(g);
+  }
+  for (auto& g : pgroups) {
+    PrepBatch pb{};
+    pb.err = B->err_dev;
+    uint32_t tiles = 0;
+    for (int k : g) {
+      PrepDesc d = pd[k];
+      d.tile0 = tiles;
+      tiles += d.ntiles;
+      pb.d[pb.n++] = d;
+    }
+    pb.total_tiles = tiles;
+    pb.ticket = A.take<unsigned long long>(1);
+    pb.lb = A.take<uint4>(tiles);
+    B->prep.push_back(pb);
   }
   // rle
   for (auto& g : groups(rlj)) {
@@ -561,8 +593,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       if (uint64_t(kRleTile) * b.max_run > kRleBigLimit) rb.big_enabled = 1;
     }
     rb.total_tiles = tiles;
-    rb.ticket = A.take<unsigned long long>(1);
-    rb.lb = A.take<uint4>(tiles);
+    if (const char* dbg = std::getenv("CDM_DEBUG_RLE")) rb.debug = uint32_t(std::atoi(dbg));
     rb.big.counter = A.take<unsigned long long>(1);
     rb.big.done = A.take<uint32_t>(1);
     rb.big.max_slots = slots;
@@ -572,19 +603,25 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   // ---- non-zeroed region: optional per-tile trace (env CDM_TRACE=<csv path>)
   if (std::getenv("CDM_TRACE")) {
     for (auto& sb : B->scan) sb.trace = A.take<uint64_t>(size_t(sb.total_tiles) * 8);
-    for (auto& ib : B->inner) ib.trace = A.take<uint64_t>(size_t(ib.total_tiles) * 8);
+    for (auto& pb : B->prep) pb.trace = A.take<uint64_t>(size_t(pb.total_tiles) * 8);
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
   // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
-  std::map<int, InnerDesc*> inner_of;
-  for (auto& ib : B->inner)
-    for (uint32_t k = 0; k < ib.n; k++) {
-      InnerDesc& d = ib.d[k];
-      d.S = A.take<uint32_t>(d.n_inner);
-      d.Q = A.take<uint64_t>(d.n_inner);
-      d.DV = A.take<uint64_t>(d.n_inner);
-      d.tstart = A.take<uint32_t>(d.outer_tiles + 1);
-      inner_of[int(d.err_idx)] = &d;
+  // per RLE chunk: tile prefixes (OUTER) and the inner run table (INNER)
+  std::map<int, PrepDesc*> outer_of, inner_of;
+  for (auto& pb : B->prep)
+    for (uint32_t k = 0; k < pb.n; k++) {
+      PrepDesc& d = pb.d[k];
+      if (d.kind == PREP_OUTER) {
+        d.prefix = A.take<uint4>(d.outer_tiles);
+        outer_of[int(d.err_idx)] = &d;
+      } else {
+        d.S = A.take<uint32_t>(d.n_items);
+        d.Q = A.take<uint64_t>(d.n_items);
+        d.DV = A.take<uint64_t>(d.n_items);
+        d.tstart = A.take<uint32_t>(d.outer_tiles + 1);
+        inner_of[int(d.err_idx)] = &d;
+      }
     }
   for (auto& rb : B->rle) {
     rb.big.entries = A.take<RleBig::Entry>(rb.big.max_slots);
@@ -593,8 +630,9 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
     for (uint32_t k = 0; k < rb.n; k++) {
       RleDesc& d = rb.d[k];
+      d.prefix = outer_of[int(d.err_idx)]->prefix;
       if (d.vmode == V_DRLE) {
-        InnerDesc* in = inner_of[int(d.err_idx)];
+        PrepDesc* in = inner_of[int(d.err_idx)];
         d.S = in->S; d.Q = in->Q; d.DV = in->DV; d.tstart = in->tstart;
       }
     }
@@ -663,7 +701,8 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   CUDA_TRY(cudaMemsetAsync(B->err_dev, 0, sizeof(uint32_t) * std::max<size_t>(1, B->jobs.size()), s));
   // fork: with several families each runs on its own stream (the latency-bound scan/RLE chains overlap
   // the bandwidth-bound FP kernel); a single family stays on `s`
-  const bool fork = nfam > 1 && B->e;
+  static const bool serial = std::getenv("CDM_SERIAL") != nullptr;
+  const bool fork = nfam > 1 && B->e && !serial;
   if (fork) {
     if (!B->fork) {
       CUDA_TRY(cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming));
@@ -685,7 +724,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, fs)); n++; B->fam_launches[F_SCAN]++; }
         break;
       case F_RLE:
-        for (auto& ib : B->inner) { CUDA_TRY(launch_inner(ib, fs)); n++; B->fam_launches[F_RLE]++; }
+        for (auto& pb : B->prep) { CUDA_TRY(launch_rle_prep(pb, fs)); n++; B->fam_launches[F_RLE]++; }
         for (auto& rb : B->rle) {
           CUDA_TRY(launch_rle(rb, fs));
           n++;
@@ -871,25 +910,33 @@ extern "C" CDM_API cdm_status cdm_chunk_check(const cdm_cascade* c, const void* 
 // H4: one group = consecutive jobs copied into one staging slot (a single H2D copy when their host bytes
 // are contiguous) and decoded by one multi-chunk batch after the copy's event.  The copy stream waits on
 // the slot's `freed` event, so copies of later groups run ahead of decodes without host stalls.
-static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std::vector<const cdm_job*>& js,
-                               uint64_t* tickets_out) {
+struct PendingGroup {
+  uint32_t slot = 0;
+  std::vector<Bound> bs;
+  std::vector<const cdm_job*> js;
+};
+
+// Phase 1: enqueue the group's H2D copies into its slot (copy stream) and record the slot's `copied` event.
+static cdm_status group_copy(cdm_engine* e, PendingGroup& pg) {
   const uint32_t si = e->next_slot;
   e->next_slot = (e->next_slot + 1) % uint32_t(e->slots.size());
+  pg.slot = si;
   cdm_engine::Slot& s = e->slots[si];
   if (s.used) CUDA_TRY(cudaStreamWaitEvent(e->copy, s.freed, 0));
+  auto& bs = pg.bs;
+  auto& js = pg.js;
   // Lay the chunks out in the slot in host-address order: exactly contiguous host neighbours keep their
   // relative offsets and share one H2D copy (if the driver rejects a copy spanning two host allocations,
   // the run is copied chunk by chunk).  Decode order inside the batch does not depend on this layout.
   std::vector<size_t> by_addr(bs.size());
   std::iota(by_addr.begin(), by_addr.end(), size_t(0));
   std::sort(by_addr.begin(), by_addr.end(), [&](size_t a, size_t b) { return js[a]->host_chunk < js[b]->host_chunk; });
-  std::vector<size_t> off(bs.size());
   size_t pos = 0, k = 0;
   while (k < by_addr.size()) {
     const size_t first = by_addr[k];
     const uint8_t* h0 = static_cast<const uint8_t*>(js[first]->host_chunk);
     pos = (pos + 255) & ~size_t(255);
-    off[first] = pos;
+    bs[first].dev_chunk = s.dev + pos;
     size_t end = bs[first].total;
     size_t m = k + 1;
     while (m < by_addr.size()) {
@@ -897,7 +944,7 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
       if (static_cast<const uint8_t*>(js[j]->host_chunk) != h0 + end || bs[j].total % 16 ||
           pos + end + bs[j].total > e->opts.slot_bytes)
         break;
-      off[j] = pos + end;
+      bs[j].dev_chunk = s.dev + pos + end;
       end += bs[j].total;
       m++;
     }
@@ -907,7 +954,8 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
       cudaGetLastError();
       for (size_t q = k; q < m; q++) {
         const size_t j = by_addr[q];
-        CUDA_TRY(cudaMemcpyAsync(s.dev + off[j], js[j]->host_chunk, bs[j].total, cudaMemcpyHostToDevice, e->copy));
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(bs[j].dev_chunk), js[j]->host_chunk, bs[j].total,
+                                 cudaMemcpyHostToDevice, e->copy));
       }
     } else if (ce != cudaSuccess) {
       return fail(CDM_E_CUDA, std::string("H2D copy: ") + cudaGetErrorString(ce));
@@ -916,14 +964,19 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
     k = m;
   }
   CUDA_TRY(cudaEventRecord(s.copied, e->copy));
+  s.used = true;
+  return CDM_OK;
+}
+
+// Phase 2: the decode stream waits for the copy, runs the group's fused kernels, reads back the error words.
+static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* tickets_out) {
+  cdm_engine::Slot& s = e->slots[pg.slot];
+  auto& bs = pg.bs;
   CUDA_TRY(cudaStreamWaitEvent(e->decode, s.copied, 0));
   auto batch = std::make_unique<cdm_batch>();
   batch->e = e;
   batch->device = e->device;
-  for (size_t j = 0; j < bs.size(); j++) {
-    bs[j].dev_chunk = s.dev + off[j];
-    batch->jobs.push_back(bs[j]);
-  }
+  for (auto& b : bs) batch->jobs.push_back(b);
   Alloc sizing;
   size_t zb = 0;
   size_t need = layout_batch(batch.get(), sizing, &zb);
@@ -959,7 +1012,6 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
   }
   CUDA_TRY(cudaMemcpyAsync(e->err_host + ep, batch->err_dev, sizeof(uint32_t) * nj, cudaMemcpyDeviceToHost, e->decode));
   CUDA_TRY(cudaEventRecord(s.freed, e->decode));
-  s.used = true;
   const uint64_t gid = e->next_group++;
   cdm_engine::Group& g = e->groups[gid];
   if (!e->event_pool.empty()) { g.done = e->event_pool.back(); e->event_pool.pop_back(); }
@@ -982,6 +1034,16 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
     tickets_out[j] = id;
   }
   return CDM_OK;
+}
+
+static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std::vector<const cdm_job*>& js,
+                               uint64_t* tickets_out) {
+  PendingGroup pg;
+  pg.bs = bs;
+  pg.js = js;
+  cdm_status st = group_copy(e, pg);
+  if (st) return st;
+  return group_decode(e, pg, tickets_out);
 }
 
 extern "C" CDM_API cdm_status cdm_submit(cdm_engine* e, const cdm_job* job, uint64_t* ticket) {
@@ -1036,25 +1098,39 @@ extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* job
   }
   // groups: consecutive jobs (in issue order) up to a target size, so several groups pipeline
   const uint64_t target = std::min<uint64_t>(e->opts.slot_bytes, std::max<uint64_t>(2ull << 20, total / 8));
+  std::vector<PendingGroup> groups;
+  std::vector<size_t> first_job;
   size_t k = 0;
   while (k < n) {
-    std::vector<Bound> bs;
-    std::vector<const cdm_job*> js;
+    PendingGroup pg;
     uint64_t bytes = 0;
     size_t m = k;
-    while (m < n && js.size() < size_t(kMaxBatch)) {
-      const uint64_t add = ((all[order[m]].total + 255) & ~uint64_t(255)) + 4096;
-      if (!js.empty() && (bytes + add > e->opts.slot_bytes || bytes >= target)) break;
+    while (m < n && pg.js.size() < size_t(kMaxBatch)) {
+      const uint64_t add = ((all[order[m]].total + 255) & ~uint64_t(255));
+      if (!pg.js.empty() && (bytes + add > e->opts.slot_bytes || bytes >= target)) break;
       bytes += add;
-      bs.push_back(all[order[m]]);
-      js.push_back(&jobs[order[m]]);
+      pg.bs.push_back(all[order[m]]);
+      pg.js.push_back(&jobs[order[m]]);
       m++;
     }
-    std::vector<uint64_t> tk(bs.size());
-    cdm_status st = submit_group(e, bs, js, tk.data());
-    if (st) return st;
-    for (size_t j = 0; j < bs.size(); j++) tickets[order[k + j]] = tk[j];
+    first_job.push_back(k);
+    groups.push_back(std::move(pg));
     k = m;
+  }
+  // the copy engine runs up to n_slots groups ahead of the decodes: copies are enqueued before the host
+  // spends time building a group's launches
+  const size_t ahead = e->slots.size();
+  size_t copied = 0;
+  for (size_t g = 0; g < groups.size(); g++) {
+    while (copied < groups.size() && copied < g + ahead) {
+      cdm_status st = group_copy(e, groups[copied]);
+      if (st) return st;
+      copied++;
+    }
+    std::vector<uint64_t> tk(groups[g].bs.size());
+    cdm_status st = group_decode(e, groups[g], tk.data());
+    if (st) return st;
+    for (size_t j = 0; j < tk.size(); j++) tickets[order[first_job[g] + j]] = tk[j];
   }
   return CDM_OK;
 }
@@ -1133,7 +1209,7 @@ static void dump_trace(cdm_batch* b, const char* path) {
     }
   };
   for (size_t i = 0; i < b->scan.size(); i++) dump("scan", int(i), b->scan[i].trace, b->scan[i].total_tiles);
-  for (size_t i = 0; i < b->inner.size(); i++) dump("inner", int(i), b->inner[i].trace, b->inner[i].total_tiles);
+  for (size_t i = 0; i < b->prep.size(); i++) dump("prep", int(i), b->prep[i].trace, b->prep[i].total_tiles);
   for (size_t i = 0; i < b->rle.size(); i++) dump("rle", int(i), b->rle[i].trace, b->rle[i].total_tiles);
   std::fclose(f);
 }

@@ -308,37 +308,62 @@ static int enc_bitpack(builder *b, col_t in) {
 
 static uint32_t g_sort_eb;
 static const uint8_t *g_sort_base;
-static int cmp_idx(const void *a, const void *c) {
-  uint64_t i = *(const uint64_t *)a, j = *(const uint64_t *)c;
-  int r = memcmp(g_sort_base + i * g_sort_eb, g_sort_base + j * g_sort_eb, g_sort_eb);
-  return r ? r : (i < j ? -1 : (i > j));
+static int cmp_elem(const void *a, const void *c) { return memcmp(a, c, g_sort_eb); }
+
+static uint64_t hash_bytes(const uint8_t *p, uint32_t n) {
+  uint64_t h = 14695981039346656037ull;
+  for (uint32_t i = 0; i < n; i++) { h ^= p[i]; h *= 1099511628211ull; }
+  return h ^ (h >> 29);
 }
 
-/* Dictionary: unique elements sorted by unsigned bytes; indices into the dictionary. */
+/* Dictionary: unique elements sorted by unsigned bytes; indices into the dictionary.
+ * Unique elements are found with an open-addressing hash table (O(n)), then only the uniques are sorted. */
 static int enc_dict(builder *b, const tnode *t, col_t in) {
   uint32_t eb = in.is_int ? 8 : in.eb;
-  uint64_t *perm = (uint64_t *)malloc((in.n ? in.n : 1) * sizeof(uint64_t));
+  uint64_t cap = 16;
+  while (cap < 2 * (in.n ? in.n : 1) && cap < (1ull << 33)) cap <<= 1;
+  /* table of first-occurrence element indices, +1 (0 = empty) */
+  uint64_t *tab = (uint64_t *)calloc(cap, sizeof(uint64_t));
   int64_t *idx = (int64_t *)malloc((in.n ? in.n : 1) * sizeof(int64_t));
-  if (!perm || !idx) { free(perm); free(idx); return fail(E_OOM, "out of memory"); }
-  for (uint64_t i = 0; i < in.n; i++) perm[i] = i;
-  g_sort_eb = eb; g_sort_base = in.data;
-  qsort(perm, in.n, sizeof(uint64_t), cmp_idx);
-  uint8_t *dict = (uint8_t *)malloc((in.n ? in.n : 1) * eb);
-  uint64_t entries = 0;
-  for (uint64_t k = 0; k < in.n; k++) {
-    const uint8_t *e = in.data + perm[k] * eb;
-    if (!entries || memcmp(dict + (entries - 1) * eb, e, eb)) { memcpy(dict + entries * eb, e, eb); entries++; }
-    idx[perm[k]] = (int64_t)(entries - 1);
+  uint8_t *uniq = (uint8_t *)malloc((in.n ? in.n : 1) * eb);
+  uint64_t *slot_of = (uint64_t *)malloc((in.n ? in.n : 1) * sizeof(uint64_t));
+  if (!tab || !idx || !uniq || !slot_of) { free(tab); free(idx); free(uniq); free(slot_of); return fail(E_OOM, "out of memory"); }
+  uint64_t nu = 0;
+  for (uint64_t i = 0; i < in.n; i++) {
+    const uint8_t *e = in.data + i * eb;
+    uint64_t h = hash_bytes(e, eb) & (cap - 1);
+    for (;;) {
+      if (!tab[h]) { memcpy(uniq + nu * eb, e, eb); tab[h] = ++nu; break; }
+      if (!memcmp(uniq + (tab[h] - 1) * eb, e, eb)) break;
+      h = (h + 1) & (cap - 1);
+    }
+    slot_of[i] = tab[h] - 1;  /* provisional (first-appearance) id */
   }
-  free(perm);
-  if (entries > 0xFFFFFFFFull) { free(dict); free(idx); return fail(E_UNSUPPORTED, "dictionary too large"); }
+  /* sort the uniques by bytes; remap provisional ids to sorted positions */
+  uint8_t *sorted = (uint8_t *)malloc((nu ? nu : 1) * eb);
+  memcpy(sorted, uniq, nu * eb);
+  g_sort_eb = eb;
+  qsort(sorted, nu, eb, cmp_elem);
+  uint64_t *remap = (uint64_t *)malloc((nu ? nu : 1) * sizeof(uint64_t));
+  for (uint64_t u = 0; u < nu; u++) {
+    /* binary search uniq[u] in sorted */
+    uint64_t lo = 0, hi = nu;
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) / 2;
+      if (memcmp(sorted + mid * eb, uniq + u * eb, eb) < 0) lo = mid + 1; else hi = mid;
+    }
+    remap[u] = lo;
+  }
+  for (uint64_t i = 0; i < in.n; i++) idx[i] = (int64_t)remap[slot_of[i]];
+  free(tab); free(uniq); free(slot_of); free(remap);
+  if (nu > 0xFFFFFFFFull) { free(sorted); free(idx); return fail(E_UNSUPPORTED, "dictionary too large"); }
   node_rec r; memset(&r, 0, sizeof r);
   r.codec = C_DICT; r.nchild = 2; r.stream = 0xFFFF; r.n = in.n;
-  uint32_t ent32 = (uint32_t)entries; memcpy(r.p, &ent32, 4); memcpy(r.p + 4, &eb, 4);
+  uint32_t ent32 = (uint32_t)nu; memcpy(r.p, &ent32, 4); memcpy(r.p + 4, &eb, 4);
   add_node(b, r);
-  col_t dc = {entries, eb, 0, dict, NULL};
+  col_t dc = {nu, eb, 0, sorted, NULL};
   int rc = enc_raw(b, dc);
-  free(dict);
+  free(sorted);
   if (rc) { free(idx); return rc; }
   return enc_int_child(b, t->child[1], idx, in.n);
 }

@@ -23,10 +23,14 @@ for name, spec, dtype, width, chunks, _ in cols:
         decs.append(cdm.Decode(casc, ch, out, offs, dev_chunk=torch.from_numpy(ch).cuda()))
 b = cdm.Batch(eng, decs)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+import time
 for _ in range(3):
     flush.zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     b.launch()
     b.results()
+    print("step wall ms %.3f" % ((time.perf_counter() - t0) * 1e3))
 rows = [l.strip().split(",") for l in open(path)]
 import collections
 by = collections.defaultdict(list)
