@@ -48,9 +48,9 @@ WORKLOADS = {
                          "BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack)"),
     # BASELINE configs[2]: TPC-H SF=10 lineitem string columns (dictionary CHAR(n) + chunk-parallel LZ4)
     "config3": dict(sf=10.0, dtype="u8", cols=[("l_shipmode", "Dict|BitPack"), ("l_returnflag", "Dict|BitPack"),
-                                                ("l_comment", "Str|[LZ4,BitPack]")],
+                                                ("l_comment", "Str|[LZ4(sub=16384),BitPack]")],
                     desc="config 3: TPC-H SF=10 lineitem string columns (l_shipmode/l_returnflag Dict|BitPack CHAR(n), "
-                         "l_comment Str|[LZ4(64 KiB sub-chunks),BitPack])"),
+                         "l_comment Str|[LZ4(16 KiB sub-chunks),BitPack])"),
     # BASELINE configs[0]: the oracle-sized parity case (launch-bound: 4 MB decoded)
     "config1": dict(sf=None, dtype="int32", cols=[("config1", "BitPack")],
                     desc="config 1: 1M int32, FOR + 8-bit bit-packing, one chunk"),

@@ -194,7 +194,7 @@ struct Lz4Desc {
   uint32_t n_sub;
   uint32_t sub0;           // first global sub-chunk index
   uint32_t err_idx;
-  uint32_t pad;
+  uint32_t uniform;        // > 0: every sub-chunk but the last decompresses to exactly this many bytes
 };
 
 struct Lz4Batch {
@@ -210,7 +210,7 @@ cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
 cudaError_t launch_rle_prep(const PrepBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
-cudaError_t launch_lz4(const Lz4Batch& b, cudaStream_t s);
+cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);
 int device_sms();
 
 }  // namespace cdm

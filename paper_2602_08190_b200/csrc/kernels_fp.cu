@@ -84,10 +84,10 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
     const uint64_t tile_start = uint64_t(lt) * kFpTile;
     const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
     bool bad_index = false;
-    bool bytes_path = false;
+    const bool bytes_path = D.mode == FP_DICT && D.out_bytes != 4 && D.out_bytes != 8;  // CHAR(n) rows
 
 #pragma unroll 1
-    for (uint32_t k = 0; k < 4; k++) {
+    for (uint32_t k = 0; k < 4 && !bytes_path; k++) {
       const uint32_t i0 = k * 1024 + tid * 4;  // 4 consecutive values
       if (i0 >= valid) break;
       uint64_t v[4];
@@ -129,8 +129,6 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
           uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
           if (full) st_v4_u32(o, __ldg(dict + v[0]), __ldg(dict + v[1]), __ldg(dict + v[2]), __ldg(dict + v[3]));
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
-        } else {
-          bytes_path = true;  // CHAR(n) rows: 16-byte output chunks below
         }
       } else {  // FP_F2I: one IEEE division per element (no reciprocal: bit-exact, R13)
         const double p = kPow10[D.d];

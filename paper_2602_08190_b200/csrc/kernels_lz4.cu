@@ -8,6 +8,8 @@
 // 32 lanes together, and a match of length L at offset o is copied in parallel with
 // out[p + k] = out[p - o + (k mod o)], which is exact even when the match overlaps its own output.
 // Every length and offset is bounds-checked; a malformed block sets CDM_ERR_LZ4 and stops that warp.
+#include <cstdlib>
+
 #include "device_util.cuh"
 #include "kernels.h"
 
@@ -37,9 +39,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_kernel(const __grid_con
 
   // output offset = sum of the preceding sub-chunks' decompressed lengths (warp-parallel)
   uint64_t off = 0;
-  for (uint32_t k = lane; k < s; k += 32) off += __ldg(tab + 3 * k + 2);
+  if (D.uniform) {
+    off = uint64_t(s) * D.uniform;  // host-verified uniform sub-chunk sizes
+  } else {
+    for (uint32_t k = lane; k < s; k += 32) off += __ldg(tab + 3 * k + 2);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(FULL, off, o);
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(FULL, off, o);
+  }
   const uint32_t co = __ldg(tab + 3 * s), cl = __ldg(tab + 3 * s + 1), dl = __ldg(tab + 3 * s + 2);
   bool bad = uint64_t(co) + cl > D.payload_bytes || off + dl > D.n;
   if (s + 1 == D.n_sub && off + dl != D.n) bad = true;
@@ -103,10 +109,185 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_kernel(const __grid_con
   if (bad && lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
 }
 
+// ------------------------------------------------------------------------------------------ smem decoder
+// Sub-chunks of <= kLz4SmemMax decompressed bytes are decoded into a per-warp shared-memory window: match
+// sources are then shared-memory reads instead of L2 round trips.  Each sequence is parsed from one
+// coalesced 32-byte window of the compressed stream held across the lanes (token, literals, offset
+// fetched with shuffles); long literal runs / extension bytes fall back to broadcast loads.  The finished
+// window is copied out with 16-byte stores: it is placed at byte offset (dst & 15) inside its buffer so
+// shared and global addresses share their alignment.
+constexpr uint32_t kLz4SmemMax = 32768;
+
+__device__ __forceinline__ uint32_t ldb(const uint8_t* __restrict__ p) { return __ldg(p); }
+
+// A two-window reader over the compressed stream held across the warp's lanes: bytes [pos, pos+64) live in
+// (cur, nxt), one byte per lane each, and the window after them is already in flight (pre), so the next
+// sequence's bytes are usually a shuffle away.
+struct Lz4Reader {
+  const uint8_t* __restrict__ in;
+  uint32_t cl, pos;
+  uint32_t cur, nxt, pre;
+  __device__ __forceinline__ uint32_t load(uint32_t q, uint32_t lane) const {
+    return (q + lane < cl) ? uint32_t(__ldg(in + q + lane)) : 0u;
+  }
+  __device__ __forceinline__ void init(const uint8_t* p, uint32_t n, uint32_t lane) {
+    in = p; cl = n; pos = 0;
+    cur = load(0, lane); nxt = load(32, lane); pre = load(64, lane);
+  }
+  // make q < pos + 32 (q's byte and the 32 after it are resident)
+  __device__ __forceinline__ void advance(uint32_t q, uint32_t lane) {
+    while (q >= pos + 32) {
+      cur = nxt; nxt = pre; pos += 32;
+      pre = load(pos + 64, lane);
+    }
+  }
+  // byte at q (uniform across lanes), q in [pos, pos + 64)
+  __device__ __forceinline__ uint32_t at(uint32_t q) const {
+    const uint32_t d = q - pos;
+    const uint32_t a = __shfl_sync(FULL, cur, d & 31), b = __shfl_sync(FULL, nxt, d & 31);
+    return d < 32 ? a : b;
+  }
+  // per-lane byte at q + lane (q + 31 < pos + 64)
+  __device__ __forceinline__ uint32_t lane_at(uint32_t q, uint32_t lane) const {
+    const uint32_t d = q + lane - pos;
+    const uint32_t a = __shfl_sync(FULL, cur, d & 31), b = __shfl_sync(FULL, nxt, d & 31);
+    return d < 32 ? a : b;
+  }
+};
+
+__global__ void lz4_smem_kernel(const __grid_constant__ Lz4Batch B, uint32_t cap) {
+  extern __shared__ __align__(16) uint8_t lzbuf[];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  const uint32_t gs = blockIdx.x * wpc + wib;
+  if (gs >= B.total_subs) return;
+  const Lz4Desc& D = B.d[find_desc_lz4(B, gs)];
+  const uint32_t s = gs - D.sub0;
+  const uint32_t* tab = reinterpret_cast<const uint32_t*>(D.table);
+  uint64_t off = 0;
+  if (D.uniform) {
+    off = uint64_t(s) * D.uniform;  // host-verified uniform sub-chunk sizes
+  } else {
+    for (uint32_t k = lane; k < s; k += 32) off += __ldg(tab + 3 * k + 2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(FULL, off, o);
+  }
+  const uint32_t co = __ldg(tab + 3 * s), cl = __ldg(tab + 3 * s + 1), dl = __ldg(tab + 3 * s + 2);
+  bool bad = uint64_t(co) + cl > D.payload_bytes || off + dl > D.n || dl > cap;
+  if (s + 1 == D.n_sub && off + dl != D.n) bad = true;
+  if (bad) {
+    if (lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
+    return;
+  }
+  uint8_t* gdst = D.out + off;
+  const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(gdst) & 15);
+  uint8_t* win = lzbuf + wib * (cap + 16) + mis;
+  Lz4Reader R;
+  R.init(D.payload + co, cl, lane);
+  uint32_t ip = 0, op = 0;
+  for (;;) {
+    if (ip >= cl) { bad = true; break; }
+    R.advance(ip, lane);
+    const uint32_t token = R.at(ip);
+    uint32_t lit = token >> 4;
+    ip++;
+    if (lit == 15) {
+      uint32_t b;
+      do {
+        if (ip >= cl) { bad = true; break; }
+        R.advance(ip, lane);
+        b = R.at(ip++);
+        lit += b;
+      } while (b == 255);
+      if (bad) break;
+    }
+    if (lit > cl - ip || lit > dl - op) { bad = true; break; }
+    // literals: 32 per step, from the reader's windows
+    for (uint32_t k = 0; k < lit; k += 32) {
+      R.advance(ip + k, lane);
+      const uint32_t v = R.lane_at(ip + k, lane);
+      if (k + lane < lit) win[op + k + lane] = uint8_t(v);
+    }
+    ip += lit;
+    op += lit;
+    if (ip == cl) break;  // the last sequence carries literals only
+    if (cl - ip < 2) { bad = true; break; }
+    R.advance(ip, lane);
+    const uint32_t moff = R.at(ip) | (R.at(ip + 1) << 8);
+    ip += 2;
+    if (moff == 0 || moff > op) { bad = true; break; }
+    uint32_t ml = token & 15;
+    if (ml == 15) {
+      uint32_t b;
+      do {
+        if (ip >= cl) { bad = true; break; }
+        R.advance(ip, lane);
+        b = R.at(ip++);
+        ml += b;
+      } while (b == 255);
+      if (bad) break;
+    }
+    ml += 4;
+    if (ml > dl - op) { bad = true; break; }
+    __syncwarp();  // literal bytes written by other lanes are visible to the match copy
+    if (moff >= 32 || moff >= ml) {
+      for (uint32_t base = 0; base < ml; base += 32) {
+        const uint32_t k = base + lane;
+        if (k < ml) win[op + k] = win[op - moff + k];
+        __syncwarp();
+      }
+    } else {  // period moff < 32 and overlapping: out[op+k] = out[op - moff + (k mod moff)]
+      uint32_t m = lane % moff;
+      const uint32_t step = 32 % moff;
+      for (uint32_t base = 0; base < ml; base += 32) {
+        const uint32_t k = base + lane;
+        if (k < ml) win[op + k] = win[op - moff + m];
+        m += step;
+        if (m >= moff) m -= moff;
+      }
+      __syncwarp();
+    }
+    op += ml;
+  }
+  if (!bad && op != dl) bad = true;
+  if (bad) {
+    if (lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
+    return;
+  }
+  __syncwarp();
+  // copy-out: unaligned head bytes, 16-byte body, tail bytes
+  const uint32_t head = min(dl, (16u - mis) & 15u);
+  if (lane < head) gdst[lane] = win[lane];
+  const uint32_t body = (dl - head) & ~15u;
+  for (uint32_t o = head + lane * 16; o < head + body; o += 32 * 16) {
+    const uint4 v = *reinterpret_cast<const uint4*>(win + o);
+    st_v4_u32(gdst + o, v.x, v.y, v.z, v.w);
+  }
+  const uint32_t t = head + body + lane;
+  if (t < dl) gdst[t] = win[t];
+}
+
 }  // namespace
 
-cudaError_t launch_lz4(const Lz4Batch& b, cudaStream_t s) {
+cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
   if (!b.total_subs) return cudaSuccess;
+  // The shared-memory variant is opt-in (CDM_LZ4_SMEM=1): measured on config 3 (16 KiB sub-chunks) it is
+  // 2.5x slower than the global-memory kernel (12 vs 64 resident warps per SM; both are issue-bound).
+  static const bool use_smem = std::getenv("CDM_LZ4_SMEM") != nullptr;
+  if (max_sub <= kLz4SmemMax && use_smem) {
+    // warps per CTA such that 3 CTAs fit an SM's shared memory
+    const uint32_t cap = (max_sub + 15) & ~15u;
+    uint32_t wpc = 8;
+    while (wpc > 1 && 3ull * wpc * (cap + 16) > 220 * 1024) wpc >>= 1;
+    const uint32_t smem = wpc * (cap + 16);
+    static uint32_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(lz4_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      configured = smem;
+    }
+    const uint32_t grid = (b.total_subs + wpc - 1) / wpc;
+    lz4_smem_kernel<<<grid, wpc * 32, smem, s>>>(b, cap);
+    return cudaGetLastError();
+  }
   const uint32_t grid = (b.total_subs + kWarpsPerCta - 1) / kWarpsPerCta;
   lz4_kernel<<<grid, kWarpsPerCta * 32, 0, s>>>(b);
   return cudaGetLastError();

@@ -134,7 +134,7 @@ struct Bound {
   uint32_t nruns = 0, n_inner = 0, max_run = 0;
   bool lz4 = false;
   uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
-  uint32_t n_sub = 0;
+  uint32_t n_sub = 0, lz_sub_bytes = 0, lz_uniform = 0;
   const uint8_t* dev_chunk = nullptr;
   void* out = nullptr;
   void* offs = nullptr;
@@ -328,6 +328,13 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
         if (!(e = raw_stream(c, t, t.kids[bi][1], 12, &b->lz_tab_off, &tn)).empty()) return bad(e);
         b->lz_pay_bytes = pn;
         b->n_sub = bn.u32_at0();
+        // largest decompressed sub-chunk, read from the host copy of the table (selects the kernel variant)
+        const uint8_t* tab = static_cast<const uint8_t*>(job.host_chunk) + b->lz_tab_off;
+        for (uint32_t k = 0; k < b->n_sub; k++) b->lz_sub_bytes = std::max(b->lz_sub_bytes, rd32(tab + 12ull * k + 8));
+        // uniform sub-chunks (the encoder's layout): sub-chunk s starts at s * size, no prefix needed
+        b->lz_uniform = b->n_sub ? rd32(tab + 8) : 0;
+        for (uint32_t k = 0; k + 1 < b->n_sub && b->lz_uniform; k++)
+          if (rd32(tab + 12ull * k + 8) != b->lz_uniform) b->lz_uniform = 0;
         if (tn != b->n_sub) return bad("LZ4 table entries != n_sub");
         if (c.payload_bytes && !b->n_sub) return bad("LZ4 without sub-chunks");
       } else {
@@ -382,6 +389,7 @@ struct cdm_batch {
   std::vector<PrepBatch> prep;
   std::vector<RleBatch> rle;
   std::vector<Lz4Batch> lz4;
+  std::vector<uint32_t> lz4_max_sub;
   struct Copy { void* dst; const void* src; size_t bytes; };
   std::vector<Copy> copies;
   std::vector<void*> zero_offsets;  // VARBYTES with rows == 0: offsets[0] = 0
@@ -416,7 +424,7 @@ namespace {
 // Returns the arena bytes; `zero_bytes` = prefix of the arena that must start zeroed.
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
-  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->prep.clear(); B->rle.clear(); B->lz4.clear();
+  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->prep.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
   B->err_dev = A.take<uint32_t>(nj ? nj : 1);
@@ -641,9 +649,10 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (auto& g : groups(lzj)) {
     Lz4Batch lb{};
     lb.err = B->err_dev;
-    uint32_t subs = 0;
+    uint32_t subs = 0, max_sub = 0;
     for (int j : g) {
       const Bound& b = B->jobs[j];
+      max_sub = std::max(max_sub, b.lz_sub_bytes);
       Lz4Desc& d = lb.d[lb.n++];
       d.payload = b.dev_chunk + b.lz_pay_off;
       d.table = b.dev_chunk + b.lz_tab_off;
@@ -652,11 +661,13 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.n = b.payload;
       d.n_sub = b.n_sub;
       d.sub0 = subs;
+      d.uniform = b.lz_uniform;
       d.err_idx = uint32_t(j);
       subs += b.n_sub;
     }
     lb.total_subs = subs;
     B->lz4.push_back(lb);
+    B->lz4_max_sub.push_back(max_sub);
   }
   return A.off + 256;
 }
@@ -737,7 +748,11 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         }
         break;
       case F_LZ4:
-        for (auto& lb : B->lz4) { CUDA_TRY(launch_lz4(lb, fs)); n++; B->fam_launches[F_LZ4]++; }
+        for (size_t i = 0; i < B->lz4.size(); i++) {
+          CUDA_TRY(launch_lz4(B->lz4[i], B->lz4_max_sub[i], fs));
+          n++;
+          B->fam_launches[F_LZ4]++;
+        }
         break;
       case F_COPY:
         for (auto& c : B->copies) { CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, fs)); B->fam_launches[F_COPY]++; }

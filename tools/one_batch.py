@@ -8,7 +8,10 @@ import bench  # noqa: E402
 from paper_2602_08190_b200 import cdm  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-cols = bench.build_workload(0)
+workload = sys.argv[2] if len(sys.argv) > 2 else "config2"
+if len(sys.argv) > 3:  # override the l_comment LZ4 sub-chunk size
+    bench.WORKLOADS[workload]["cols"] = [(n, s.replace("LZ4(sub=16384)", f"LZ4(sub={sys.argv[3]})")) for n, s in bench.WORKLOADS[workload]["cols"]]
+cols = bench.build_workload(0, workload)
 eng = cdm.Engine(0)
 decs = []
 for name, spec, dtype, width, chunks, _ in cols:
