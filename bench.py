@@ -293,11 +293,13 @@ def main():
     e2e_steps = max(3, args.steps // 4)
     torch.cuda.synchronize()
     e2e_total = 0.0
+    e2e_submit = 0.0
     for _ in range(e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tickets = eng.submit_batch(decs_host)
+        e2e_submit += time.perf_counter() - t0
         for t in tickets:
             r = eng.wait(t)
             err_bits |= r["error_bits"]
@@ -365,6 +367,7 @@ def main():
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": tot_comp,
                     "d2h_bytes_per_step": 4 * tot_chunks, "pcie_h2d_gbs_measured": round(h2d_gbs, 1),
                     "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_gbs, 1),
+                    "host_submit_ms_per_step": round(e2e_submit * 1e3 / e2e_steps, 4),
                     "how": "cdm_submit_batch from pinned host (H2D + decode, Johnson order) + cdm_wait per chunk"},
             "gpu_launches": launches,
             "clocks": clocks.summary(),

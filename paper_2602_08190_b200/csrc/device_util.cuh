@@ -92,6 +92,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Order this thread's earlier generic-proxy shared-memory accesses (made visible CTA-wide by a preceding
+// barrier) before subsequent async-proxy (TMA) writes to the same buffer.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // 1-D bulk copy (TMA engine) of `bytes` (multiple of 16, 16-aligned src/dst) completing on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -37,14 +37,11 @@ __device__ __forceinline__ uint32_t stage_bytes(const FpDesc& D, uint32_t lt) {
   return uint32_t(want < have ? want : have);
 }
 
-__global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ FpBatch B) {
+__global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ FpBatch B, uint32_t stage_bytes_alloc) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
   const uint32_t tid = threadIdx.x;
-  // stage size is set by the host from the batch's largest w: dynamic smem = 2 stages
-  uint32_t stage_bytes_alloc;
-  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(stage_bytes_alloc));
-  stage_bytes_alloc /= 2;
+  // stage_bytes_alloc: set by the host from the batch's largest w; dynamic smem = 2 stages
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -71,6 +68,7 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
       const FpDesc& Dn = B.d[dn];
       const uint32_t ltn = next - Dn.tile0;
       const uint32_t nb = stage_bytes(Dn, ltn);
+      fence_proxy_async();  // generic reads of stage s^1 (iteration it-1) precede the TMA refill
       mbar_arrive_expect_tx(&bar[s ^ 1], nb);
       if (nb) tma_load_1d(smem + (s ^ 1) * stage_bytes_alloc, Dn.packed + uint64_t(ltn) * (kFpTile / 8) * Dn.w, nb,
                           &bar[s ^ 1]);
@@ -212,7 +210,7 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   uint32_t grid = uint32_t(device_sms() * per_sm);
   if (grid > b.total_tiles) grid = b.total_tiles;
-  fp_kernel<<<grid, kThreads, smem, s>>>(b);
+  fp_kernel<<<grid, kThreads, smem, s>>>(b, stage);
   return cudaGetLastError();
 }
 

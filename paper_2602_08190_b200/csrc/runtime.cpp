@@ -1112,7 +1112,9 @@ extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* job
     johnson(tt.data(), dd.data(), n, &order);
   }
   // groups: consecutive jobs (in issue order) up to a target size, so several groups pipeline
-  const uint64_t target = std::min<uint64_t>(e->opts.slot_bytes, std::max<uint64_t>(2ull << 20, total / 8));
+  uint64_t min_group = 2ull << 20;
+  if (const char* g = std::getenv("CDM_GROUP_MIN_BYTES")) min_group = std::strtoull(g, nullptr, 10);
+  const uint64_t target = std::min<uint64_t>(e->opts.slot_bytes, std::max<uint64_t>(min_group, total / 8));
   std::vector<PendingGroup> groups;
   std::vector<size_t> first_job;
   size_t k = 0;

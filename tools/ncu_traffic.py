@@ -1,0 +1,35 @@
+"""Per kernel family: DRAM bytes (read + write) per launch from an ncu --set full report -> profiles/ncu_traffic.json.
+usage: python tools/ncu_traffic.py gpurun_out/prof_X.ncu-rep [out.json]"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep = sys.argv[1]
+out = sys.argv[2] if len(sys.argv) > 2 else "profiles/ncu_traffic.json"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h = rows[0]
+k, rd, wr, dur = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                       "gpu__time_duration.sum"))
+units = rows[1]
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+fam = {"fp_kernel": "fp", "scan_kernel": "scan", "rle_prep_kernel": "rle", "rle_kernel": "rle", "rle_big_kernel": "rle",
+       "lz4_kernel": "lz4", "lz4_smem_kernel": "lz4"}
+acc = {}
+detail = []
+for r in rows[2:]:
+    name = r[k].split("::")[-1].split("(")[0]
+    f = fam.get(name)
+    if not f:
+        continue
+    b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]
+    acc[f] = acc.get(f, 0) + b
+    detail.append({"kernel": name, "dram_bytes": b, "us": float(r[dur].replace(",", ""))})
+res = {f: int(v) for f, v in acc.items()}
+res["_detail"] = detail
+res["_how"] = ("ncu --set full (cache control on: caches flushed before each replayed kernel), one config-2 device "
+               "batch, CDM_SERIAL=1; sum over the family's launches of dram__bytes_read.sum + dram__bytes_write.sum")
+json.dump(res, open(out, "w"), indent=1)
+print(json.dumps(res, indent=1))
