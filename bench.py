@@ -57,7 +57,7 @@ WORKLOADS = {
 }
 CHUNK_ROWS = 1 << 22
 FAMILY_NAMES = ["fp", "scan", "rle", "lz4", "copy"]
-FAMILY_KERNELS = {"fp": "fp_kernel", "scan": "scan_kernel", "rle": "rle_prep_kernel+rle_kernel(+rle_big_kernel)",
+FAMILY_KERNELS = {"fp": "fp_kernel", "scan": "scan_kernel", "rle": "rle_sums_kernel+rle_kernel(+rle_big_kernel)",
                   "lz4": "lz4_kernel", "copy": "cudaMemcpyAsync D2D"}
 
 

@@ -208,6 +208,10 @@ __device__ __forceinline__ void lb_tile(uint4* words, uint32_t gt, uint32_t firs
 }
 
 // ------------------------------------------------------------------ tracing (CDM_TRACE)
+// Programmatic dependent launch (no-ops when the launch did not enable it).
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

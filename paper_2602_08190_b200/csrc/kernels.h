@@ -13,10 +13,8 @@ constexpr int kMaxBatch = 32;      // descriptors per launch (more chunks -> mor
 constexpr int kFpTile = 4096;      // H5 values per tile = 256 threads x 16
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
 constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
-constexpr int kPrepOuterTile = 8 * 2048;  // rle_prep OUTER: 8 warps x 2048 runs (two rle tiles each)
-constexpr int kPrepInnerTile = 8 * 1024;  // rle_prep INNER: 8 warps x 1024 inner runs
 constexpr int kRleOutBytes = 44 * 1024;    // rle_kernel: a tile's output is staged in shared memory (dynamic)
-constexpr int kRleWindow = 384;    // DRLE inner-run window staged per outer tile (larger: global search)
+constexpr int kRleWindow = 1024;   // V_DRLE inner runs scanned into shared memory per pass
 constexpr uint32_t kRleBigLimit = 1u << 15;  // a tile with more output rows is expanded by rle_big
 constexpr uint32_t kRleBigPiece = 8192;       // rows per rle_big work item
 constexpr int kThreads = 256;
@@ -89,11 +87,12 @@ struct RleDesc {
   const uint8_t* val_packed;  // V_BP/V_DICT/V_F2I: packed values or indices; V_LINEAR: packed dv
   const uint8_t* dict;
   void* out;
-  const uint32_t* S;          // V_DRLE inner run table (from rle_prep)
-  const uint64_t* Q;
-  const uint64_t* DV;
-  const uint32_t* tstart;
-  const uint4* prefix;        // per outer tile exclusive prefix {flag, count, w} (from rle_prep)
+  const uint8_t* idv_packed;  // V_DRLE inner dv / dc
+  const uint8_t* idc_packed;
+  const uint4* anchor;        // V_DRLE per outer tile {j0, S_j0, Q_j0}: window start (rle_sums)
+  const uint4* prefix;        // per outer tile exclusive prefix {_, count, w} (rle_sums)
+  uint64_t idv_base;
+  uint64_t idc_base;
   uint64_t cnt_base;
   uint64_t val_base;
   uint64_t delta_base;        // V_LINEAR: Delta base
@@ -106,10 +105,12 @@ struct RleDesc {
   uint32_t err_idx;
   uint16_t cnt_w;
   uint16_t val_w;
+  uint16_t idv_w;
+  uint16_t idc_w;
   uint8_t vmode;
   uint8_t out_bytes;          // 4 or 8
   uint8_t d;
-  uint8_t pad[5];
+  uint8_t pad[1];
 };
 
 struct RleBig {  // queue of oversize tiles, expanded by rle_big
@@ -142,46 +143,42 @@ struct RleBatch {
   RleDesc d[kMaxBatch];
 };
 
-// rle_prep: every look-back of the RLE family in ONE launch, over tiny per-tile aggregates only.
-//  PREP_OUTER: per outer tile of kRleTile runs, sum of counts (and of dv*count for arithmetic runs) ->
-//              exclusive prefix per tile, so rle_kernel never waits on a predecessor.
-//  PREP_INNER: Delta|RLE value lineage (V_DRLE): per inner run j, S_j (first outer run), Q_j (base +
-//              sum_{k<j} dv_k dc_k), DV_j, and tstart[t] (inner run holding outer run t*kRleTile;
-//              tstart[outer_tiles] = n_inner - 1 closes the last window).
-enum PrepKind : uint8_t { PREP_OUTER = 0, PREP_INNER = 1 };
+// rle_sums: per-tile sums of the RLE family, fully parallel (no look-back).  The LAST CTA to finish a
+// chunk (threadfence + atomic counter, reset afterwards) scans that chunk's tile sums:
+//   outer tiles (kRleTile runs): prefix[t] = {_, sum of counts before t, sum of dv*count before t}
+//   inner tiles (kInnerTile inner runs, Delta|RLE value lineage): anchor[t] = {j0, S, Q lo, Q hi} for the
+//     inner tile holding outer run t*kRleTile: its first inner run j0, the outer run S where j0 starts and
+//     Q = base + sum of dv*dc before j0 (written by the inner tile itself while scanning: no search).
+constexpr int kInnerTile = 256;           // inner runs per inner tile sum
+constexpr int kSumsUnitOuter = 8 * 1024;  // outer runs per rle_sums CTA (8 warps x one 1024-run tile)
+constexpr int kSumsUnitInner = 8 * 256;   // inner runs per rle_sums CTA (8 warps x one inner tile)
 
-struct PrepDesc {
-  const uint8_t* a_packed;    // OUTER: counts;  INNER: dc
-  const uint8_t* b_packed;    // OUTER(linear): dv; INNER: dv
-  uint4* prefix;              // OUTER: [ntiles] exclusive prefixes
-  uint32_t* S;                // INNER outputs
-  uint64_t* Q;
-  uint64_t* DV;
-  uint32_t* tstart;
-  uint64_t a_base;
-  uint64_t b_base;
-  uint64_t base;              // INNER: Delta base
-  uint32_t n_items;           // OUTER: runs; INNER: inner runs
-  uint32_t total;             // OUTER: rows (sum of counts); INNER: outer runs (sum of dc)
-  uint32_t tile0;
-  uint32_t ntiles;
-  uint32_t outer_tiles;       // INNER: ceil(outer runs / kRleTile); OUTER: ceil(runs / kRleTile)
+struct SumsChunk {
+  const uint8_t* cnt_packed;   // outer counts
+  const uint8_t* dv_packed;    // V_LINEAR: outer dv (slopes); V_DRLE: inner dv
+  const uint8_t* dc_packed;    // V_DRLE: inner dc
+  uint64_t cnt_base, dv_base, dc_base;
+  uint64_t base;               // V_DRLE: Delta base of the value lineage
+  uint64_t* tsum;              // [outer_tiles][2] count, w
+  uint64_t* isum;              // [inner_tiles][2] dc, dv*dc
+  uint4* prefix;               // [outer_tiles]
+  uint4* anchor;               // [outer_tiles]
+  uint32_t* done;              // completion counter of this chunk
+  uint32_t nruns, rows, n_inner;
+  uint32_t outer_tiles, inner_tiles;
+  uint32_t unit0;              // first global unit of this chunk
+  uint32_t outer_units, inner_units;
   uint32_t err_idx;
-  uint16_t a_w;
-  uint16_t b_w;
-  uint8_t kind;               // PrepKind
-  uint8_t linear;             // OUTER: also accumulate dv*count
-  uint8_t pad[6];
+  uint16_t cnt_w, dv_w, dc_w;
+  uint8_t linear, drle;
 };
 
-struct PrepBatch {
+struct SumsBatch {
   uint32_t n;
-  uint32_t total_tiles;
+  uint32_t total_units;
   uint64_t* trace;
   uint32_t* err;
-  unsigned long long* ticket;
-  uint4* lb;
-  PrepDesc d[kMaxBatch];
+  SumsChunk d[kMaxBatch];
 };
 
 // ---------------------------------------------------------------- H8: chunk-sequential LZ4
@@ -207,7 +204,7 @@ struct Lz4Batch {
 // ---------------------------------------------------------------- launchers (return cudaGetLastError)
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
-cudaError_t launch_rle_prep(const PrepBatch& b, cudaStream_t s);
+cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);

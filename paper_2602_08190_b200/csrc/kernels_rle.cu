@@ -5,20 +5,23 @@
 // The paper runs PyTorch cumsum on the counts, then a Group-Parallel kernel whose <L,S,C> geometry lets
 // several blocks co-process one big group or one block walk several small groups.  The
 // B200 design splits the family into:
-//  * rle_prep_kernel: ALL look-backs of the family in one launch, over tiny aggregates only: per outer tile
-//    of 2048 runs the sum of counts (plus sum dv*count for arithmetic runs), and for the Delta|RLE value
-//    lineage of l_orderkey the inner run table S_j, Q_j = base + sum_{k<j} dv_k dc_k, dv_j.  Its tiles do no
-//    expansion, so their look-back chains resolve in a few microseconds.
+//  * rle_sums_kernel: NO look-back.  Every warp sums one tile fully in parallel: an outer tile of 1024
+//    runs (sum of counts, plus sum dv*count for arithmetic runs) or an inner tile of 256 Delta|RLE inner
+//    runs (l_orderkey's value lineage: sum dc, sum dv*dc).  The LAST CTA of a chunk (threadfence + counter)
+//    scans the chunk's few thousand tile sums into tile output offsets, per-inner-tile (S, Q) bases and,
+//    per outer tile, the inner tile holding its first run (anchor).
 //  * rle_kernel: one CTA per outer tile, no inter-tile dependency: it stages the tile's packed counts and
 //    values in shared memory, computes the run values through the fused nested provider (BitPack,
-//    Dict|BitPack, Float2Int|BitPack, the Delta|RLE closed form value(g) = Q_j + (g - S_j + 1) dv_j, or
-//    arithmetic runs for a root Delta|RLE), scans the counts in the CTA, reads its output offset from the
-//    prep prefix and expands: each warp maps a 128-row window to runs with 4 ballots + 4 redux.or over the
-//    next 128 run starts and every lane writes 4 consecutive rows with 16-byte stores.
+//    Dict|BitPack, Float2Int|BitPack, the Delta|RLE closed form value(g) = Q_j + (g - S_j + 1) dv_j with
+//    S_j, Q_j block-scanned locally from the anchor tile, or arithmetic runs for a root Delta|RLE), scans
+//    the counts in the CTA, reads its output offset from the sums prefix and expands the runs into a
+//    shared-memory image of its output, copied out with aligned 16-byte stores.
 //  * rle_big_kernel: tiles with more than kRleBigLimit output rows (giant runs: o_shippriority is one run
 //    per chunk) are split into 8192-row pieces over every SM ("multiple GPU blocks
 //    co-process a single group"); launched only when a chunk header's max run allows it.
 // Invariant checked on the device: sum(count) == n (CDM_ERR_RUN_SUM); writes never leave [0, n).
+#include <cstdlib>
+
 #include "device_util.cuh"
 #include "kernels.h"
 
@@ -28,7 +31,6 @@ namespace {
 using namespace dev;
 
 constexpr int K = kRleTile;
-static_assert(kPrepOuterTile == 16 * kRleTile, "two rle tiles per prep warp");
 
 __constant__ double kPow10r[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                    1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
@@ -172,157 +174,152 @@ __device__ __forceinline__ void expand_warp(const uint32_t* soffs, uint32_t nr, 
   }
 }
 
-// ------------------------------------------------------------------------------------------ prep
-// Warp-level sums over lane-strided items (coalesced extraction of consecutive fields).
+// ------------------------------------------------------------------------------------------ sums
 __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
-__device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
+
+// Sums of items [i0, i1) of stream a (and sum of b*a when with_b): lane-strided, 8 items per lane per step
+// with all their loads in flight.  Returns the warp totals in every lane; `bad` flags an a > cap.
+__device__ __forceinline__ void warp_range_sums(const uint32_t* ap, uint64_t abase, uint32_t aw, const uint32_t* bp,
+                                                uint64_t bbase, uint32_t bw, bool with_b, uint64_t i0, uint64_t i1,
+                                                uint64_t cap, uint64_t* sa, uint64_t* sba, bool* bad) {
   const uint32_t lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(FULL, v, o);
-    if (lane >= uint32_t(o)) v += y;
-  }
-  return v;
-}
-
-__global__ void __launch_bounds__(kThreads) rle_prep_kernel(const __grid_constant__ PrepBatch B) {
-  __shared__ PrepDesc D;
-  __shared__ uint64_t wc_s[kThreads / 32], ww_s[kThreads / 32];
-  __shared__ uint32_t tile_s, epoch_s;
-  __shared__ uint64_t pc_s, pw_s;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    uint32_t t, e;
-    take_ticket(B.ticket, B.total_tiles - 1, &t, &e);
-    tile_s = t;
-    epoch_s = e;
-  }
-  __syncthreads();
-  const uint32_t gt = tile_s, epoch = epoch_s;
-  if (gt >= B.total_tiles) return;
-  trace_stamp(B.trace, gt, 0);
-  trace_stamp(B.trace, gt, 7);
-  stage_desc(&D, &B.d[find_desc(B, gt)]);
-  __syncthreads();
-  const uint32_t lt = gt - D.tile0;
-  const bool inner = D.kind == PREP_INNER;
-  const bool with_b = inner || D.linear;
-  const uint32_t IW = inner ? kPrepInnerTile / 8 : kPrepOuterTile / 8;  // items per warp
-  const uint64_t wbase = uint64_t(lt) * (8 * IW) + uint64_t(warp) * IW;
-  const uint32_t* ap = reinterpret_cast<const uint32_t*>(D.a_packed);
-  const uint32_t* bp = reinterpret_cast<const uint32_t*>(D.b_packed);
-
-  // pass 1: per-warp sums (lane l takes items wbase + 32k + l: consecutive lanes read consecutive fields);
-  // 8 items per lane per step with all their loads in flight
-  uint64_t sc = 0, sw = 0, sc0 = 0, sw0 = 0;  // sc0/sw0: the warp's first rle tile (OUTER)
-  bool bad = false;
   constexpr int U = 8;
-  static_assert(kRleTile % (32 * U) == 0, "batches must not straddle rle tiles");
-  for (uint32_t k = 0; k < IW; k += 32 * U) {
-    if (k == uint32_t(K)) { sc0 = sc; sw0 = sw; }
+  uint64_t s1 = 0, s2 = 0;
+  for (uint64_t k = i0; k < i1; k += 32 * U) {
     uint64_t offa[U], offb[U], av[U], bv[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint64_t j = min(wbase + k + u * 32 + lane, uint64_t(D.n_items ? D.n_items - 1 : 0));
-      offa[u] = j * D.a_w;
-      offb[u] = j * D.b_w;
+      const uint64_t j = min(k + u * 32 + lane, i1 - 1);
+      offa[u] = j * aw;
+      offb[u] = j * bw;
     }
-    extract_bits_global_batch<U>(ap, offa, D.a_w, av);
-    if (with_b) extract_bits_global_batch<U>(bp, offb, D.b_w, bv);
+    extract_bits_global_batch<U>(ap, offa, aw, av);
+    if (with_b) extract_bits_global_batch<U>(bp, offb, bw, bv);
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint64_t j = wbase + k + u * 32 + lane;
-      if (j < D.n_items) {
-        uint64_t a = D.a_base + av[u];
-        const uint64_t b = with_b ? D.b_base + bv[u] : 0ull;
-        if (a > D.total) { bad = true; a = 0; }
-        sc += a;
-        sw += b * a;
+      if (k + u * 32 + lane < i1) {
+        uint64_t x = abase + av[u];
+        if (x > cap) { *bad = true; x = 0; }
+        s1 += x;
+        if (with_b) s2 += (bbase + bv[u]) * x;
       }
     }
   }
-  if (IW <= uint32_t(K)) { sc0 = sc; sw0 = sw; }
-  sc = warp_sum(sc);
-  sw = warp_sum(sw);
-  sc0 = warp_sum(sc0);
-  sw0 = warp_sum(sw0);
-  if (lane == 0) { wc_s[warp] = sc; ww_s[warp] = sw; }
-  __syncthreads();
-  uint64_t ec = 0, ew = 0, tc = 0, tw = 0;
+  *sa = warp_sum(s1);
+  *sba = warp_sum(s2);
+}
+
+// Exclusive scan (2 components) of n pairs v[2i], v[2i+1] by one CTA, in passes of kThreads*8 with carry;
+// calls emit(i, excl0, excl1, v0, v1) for every i; returns totals.
+template <typename Emit>
+__device__ __forceinline__ void cta_scan_pairs(const uint64_t* v, uint32_t n, uint64_t* warp_s, uint64_t* tot0,
+                                               uint64_t* tot1, Emit emit) {
+  uint64_t c0 = 0, c1 = 0;
+  for (uint32_t base = 0; base < n; base += kThreads * 8) {
+    const uint32_t i0 = base + threadIdx.x * 8;
+    uint64_t a[8], b[8], s0 = 0, s1 = 0;
 #pragma unroll
-  for (int w2 = 0; w2 < kThreads / 32; w2++) {
-    if (uint32_t(w2) < warp) { ec += wc_s[w2]; ew += ww_s[w2]; }
-    tc += wc_s[w2];
-    tw += ww_s[w2];
-  }
-  trace_stamp(B.trace, gt, 1);
-  trace_stamp(B.trace, gt, 2);
-  if (warp == 0) {
-    uint64_t p0, p1;
-    lb_tile(B.lb, gt, D.tile0, epoch, tc, tw, &p0, &p1);
-    if (lane == 0) {
-      pc_s = p0;
-      pw_s = p1;
-      if (lt + 1 == D.ntiles && p0 + tc != D.total) atomicOr(B.err + D.err_idx, 0x2u);
-      if (inner && lt + 1 == D.ntiles) D.tstart[D.outer_tiles] = D.n_items - 1;  // closes the last window
+    for (int r = 0; r < 8; r++) {
+      a[r] = (i0 + r < n) ? v[2 * (i0 + r)] : 0ull;
+      b[r] = (i0 + r < n) ? v[2 * (i0 + r) + 1] : 0ull;
+      s0 += a[r];
+      s1 += b[r];
     }
-    trace_stamp(B.trace, gt, 3);
+    uint64_t t0, t1;
+    const uint64_t e0 = block_excl_scan_u64<kThreads>(s0, warp_s, &t0);
+    const uint64_t e1 = block_excl_scan_u64<kThreads>(s1, warp_s, &t1);
+    uint64_t x0 = c0 + e0, x1 = c1 + e1;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      if (i0 + r < n) emit(i0 + r, x0, x1, a[r], b[r]);
+      x0 += a[r];
+      x1 += b[r];
+    }
+    c0 += t0;
+    c1 += t1;
+  }
+  *tot0 = c0;
+  *tot1 = c1;
+}
+
+__global__ void __launch_bounds__(kThreads) rle_sums_kernel(const __grid_constant__ SumsBatch B) {
+  __shared__ SumsChunk D;
+  __shared__ uint64_t warp_s[kThreads / 32];
+  __shared__ uint32_t last_s;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t unit = blockIdx.x;
+  {
+    int lo = 0, hi = int(B.n) - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (B.d[mid].unit0 <= unit) lo = mid; else hi = mid - 1;
+    }
+    stage_desc(&D, &B.d[lo]);
+  }
+  __syncthreads();
+  trace_stamp(B.trace, unit, 0);
+  trace_stamp(B.trace, unit, 7);
+  grid_launch_dependents();  // rle_kernel may start staging its chunk data now
+  const uint32_t local = unit - D.unit0;
+  bool bad = false;
+  if (local < D.outer_units) {  // warp w: outer tile local*8 + w
+    const uint32_t t = local * 8 + warp;
+    if (t < D.outer_tiles) {
+      const uint64_t i0 = uint64_t(t) * kRleTile, i1 = min(i0 + kRleTile, uint64_t(D.nruns));
+      uint64_t sc, sw;
+      warp_range_sums(reinterpret_cast<const uint32_t*>(D.cnt_packed), D.cnt_base, D.cnt_w,
+                      reinterpret_cast<const uint32_t*>(D.dv_packed), D.dv_base, D.dv_w, D.linear, i0, i1, D.rows,
+                      &sc, &sw, &bad);
+      if (lane == 0) { D.tsum[2 * t] = sc; D.tsum[2 * t + 1] = sw; }
+    }
+  } else {  // warp w: inner tile (local - outer_units)*8 + w
+    const uint32_t it = (local - D.outer_units) * 8 + warp;
+    if (it < D.inner_tiles) {
+      const uint64_t i0 = uint64_t(it) * kInnerTile, i1 = min(i0 + kInnerTile, uint64_t(D.n_inner));
+      uint64_t sc, sw;
+      warp_range_sums(reinterpret_cast<const uint32_t*>(D.dc_packed), D.dc_base, D.dc_w,
+                      reinterpret_cast<const uint32_t*>(D.dv_packed), D.dv_base, D.dv_w, true, i0, i1, D.nruns,
+                      &sc, &sw, &bad);
+      if (lane == 0) { D.isum[2 * it] = sc; D.isum[2 * it + 1] = sw; }
+    }
   }
   if (bad) atomicOr(B.err + D.err_idx, 0x2u);
+  trace_stamp(B.trace, unit, 1);
+  // the last CTA of this chunk scans its tile sums (classic threadfence + counter)
   __syncthreads();
-  uint64_t cc = pc_s + ec, cw = pw_s + ew;  // prefix at this warp's first item
-  if (!inner) {  // the warp's rle tiles (IW / K of them): exclusive prefixes
-    if (lane == 0) {
-      for (uint32_t h = 0; h * K < IW; h++) {
-        const uint64_t first = wbase + uint64_t(h) * K;
-        if (first >= D.n_items) break;
-        const uint64_t c = h ? cc + sc0 : cc, w = h ? cw + sw0 : cw;
-        D.prefix[first / K] = make_uint4(0u, sat32(c), uint32_t(w), uint32_t(w >> 32));
-      }
-    }
-  } else {  // pass 2: S_j, Q_j, DV_j per inner run (warp scans), tile starts
-    constexpr int U2 = 4;
-    for (uint32_t k = 0; k < IW; k += 32 * U2) {
-      uint64_t offa[U2], offb[U2], avs[U2], bvs[U2];
-#pragma unroll
-      for (int u = 0; u < U2; u++) {
-        const uint64_t j = min(wbase + k + u * 32 + lane, uint64_t(D.n_items ? D.n_items - 1 : 0));
-        offa[u] = j * D.a_w;
-        offb[u] = j * D.b_w;
-      }
-      extract_bits_global_batch<U2>(ap, offa, D.a_w, avs);
-      extract_bits_global_batch<U2>(bp, offb, D.b_w, bvs);
-#pragma unroll
-      for (int u = 0; u < U2; u++) {
-        const uint64_t j = wbase + k + u * 32 + lane;
-        uint64_t av = 0, bv = 0;
-        if (j < D.n_items) {
-          av = D.a_base + avs[u];
-          bv = D.b_base + bvs[u];
-          if (av > D.total) av = 0;
-        }
-        const uint64_t ic = warp_incl_scan(av), iw = warp_incl_scan(bv * av);
-        const uint64_t c = cc + ic - av, wv = cw + iw - bv * av;
-        if (j < D.n_items) {
-          D.S[j] = uint32_t(min(c, uint64_t(D.total)));
-          D.Q[j] = D.base + wv;
-          D.DV[j] = bv;
-          if (av && c < D.total) {  // outer tiles whose first run lies in this inner run
-            const uint64_t last = min(c + av, uint64_t(D.total)) - 1;
-            for (uint64_t t = (c + K - 1) / K; t <= last / K && t < D.outer_tiles; t++) D.tstart[t] = uint32_t(j);
-          }
-        }
-        cc += __shfl_sync(FULL, ic, 31);
-        cw += __shfl_sync(FULL, iw, 31);
-      }
-    }
+  if (tid == 0) {
+    __threadfence();
+    last_s = atomicAdd(D.done, 1u) == D.outer_units + D.inner_units - 1;
   }
   __syncthreads();
-  trace_stamp(B.trace, gt, 4);
+  if (!last_s) return;
+  __threadfence();
+  trace_stamp(B.trace, unit, 2);
+  uint64_t tc, tw;
+  uint4* prefix = D.prefix;
+  cta_scan_pairs(D.tsum, D.outer_tiles, warp_s, &tc, &tw, [&](uint32_t t, uint64_t c, uint64_t w, uint64_t, uint64_t) {
+    prefix[t] = make_uint4(0u, sat32(c), uint32_t(w), uint32_t(w >> 32));
+  });
+  if (tid == 0 && tc != D.rows) atomicOr(B.err + D.err_idx, 0x2u);
+  if (D.drle) {
+    // inner tile i covers outer runs [S0, S1): it anchors every outer tile whose first run lies there
+    uint4* anchor = D.anchor;
+    const uint64_t nr = D.nruns, base = D.base;
+    uint64_t ic, iw;
+    cta_scan_pairs(D.isum, D.inner_tiles, warp_s, &ic, &iw, [&](uint32_t i, uint64_t c, uint64_t w, uint64_t dc, uint64_t) {
+      const uint64_t S0 = min(c, nr), S1 = min(c + dc, nr);
+      const uint64_t Q = base + w;
+      const uint4 rec = make_uint4(i * uint32_t(kInnerTile), uint32_t(S0), uint32_t(Q), uint32_t(Q >> 32));
+      for (uint64_t t = (S0 + K - 1) / K; t * K < S1; t++) anchor[t] = rec;
+    });
+    if (tid == 0 && ic != D.nruns) atomicOr(B.err + D.err_idx, 0x2u);
+  }
+  if (tid == 0) atomicExch(D.done, 0u);  // graph replays / next launch
+  trace_stamp(B.trace, unit, 4);
 }
 
 // ------------------------------------------------------------------------------------------ main
@@ -335,18 +332,19 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
   extern __shared__ __align__(16) uint8_t outbuf[];  // kRleOutBytes + 16: the tile's output image
   __shared__ RleDesc D;
   __shared__ uint32_t cnt_s[K / 2 + 8];  // staged packed counts when w <= 16 (else read through L1)
-  // aux: inner-run window (V_DRLE) | staged packed values (V_BP/V_DICT/V_F2I) | slopes (V_LINEAR)
+  // aux: staged packed values (V_BP/V_DICT/V_F2I) | slopes (V_LINEAR)
   __shared__ __align__(16) uint8_t aux_s[K * 8 + 64];
   __shared__ uint32_t rc_s[K];  // run counts
   __shared__ uint64_t rv_s[K];  // run first values
-  uint64_t* iQ_s = reinterpret_cast<uint64_t*>(aux_s);
-  uint64_t* iDV_s = iQ_s + (kRleWindow + 1);
-  uint32_t* iS_s = reinterpret_cast<uint32_t*>(iDV_s + (kRleWindow + 1));
   uint32_t* valbits_s = reinterpret_cast<uint32_t*>(aux_s);
   uint64_t* slope_s = reinterpret_cast<uint64_t*>(aux_s);
-  static_assert((kRleWindow + 1) * 20 <= K * 8, "window must fit the aux buffer");
+  // V_DRLE window (S_j, Q_j, dv_j of scanned inner runs) lives in the output image, unused until expansion
+  uint64_t* iQ_s = reinterpret_cast<uint64_t*>(outbuf);
+  uint64_t* iDV_s = iQ_s + kRleWindow;
+  uint32_t* iS_s = reinterpret_cast<uint32_t*>(iDV_s + kRleWindow);
+  static_assert(kRleWindow * 20 <= kRleOutBytes, "window must fit the output image");
   __shared__ uint64_t warp_s[kThreads / 32];
-  __shared__ uint32_t skip_s, win_s, j0i_s;
+  __shared__ uint32_t skip_s;
   const uint32_t tid = threadIdx.x;
   const uint32_t gt = blockIdx.x;
   trace_stamp(B.trace, gt, 0);
@@ -360,37 +358,13 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
   const bool linear = vmode == V_LINEAR;
   const uint32_t ob = D.out_bytes;
   uint32_t errbits = 0;
-  const uint4 pf = D.prefix[lt];  // tile output offset from rle_prep, issued early
-
-  // stage packed counts (and values) of this tile; V_DRLE stages inner runs [tstart[lt], tstart[lt+1]]
+  // stage packed counts (and values) of this tile: chunk data only, so this overlaps the tail of rle_sums
+  // (programmatic dependent launch); everything rle_sums writes is read after griddepcontrol.wait
   const bool cnt_staged = D.cnt_w <= 16;
   if (cnt_staged) stage_bits(cnt_s, D.cnt_packed, g0, nr, D.cnt_w);
   if (vmode == V_BP || vmode == V_DICT || vmode == V_F2I) stage_bits(valbits_s, D.val_packed, g0, nr, D.val_w);
-  const uint32_t* wS = iS_s;
-  const uint64_t* wQ = iQ_s;
-  const uint64_t* wDV = iDV_s;
-  if (vmode == V_DRLE) {
-    if (tid == 0) {
-      uint32_t j0i = D.tstart[lt], j1i = D.tstart[lt + 1];
-      if (j0i >= D.n_inner) { j0i = 0; errbits |= 0x2u; }
-      if (j1i >= D.n_inner || j1i < j0i) j1i = D.n_inner - 1;
-      j0i_s = j0i;
-      win_s = j1i - j0i + 1;
-    }
-    __syncthreads();
-    const uint32_t j0i = j0i_s, win = win_s;
-    if (win <= kRleWindow + 1) {
-      for (uint32_t k = tid; k < win; k += kThreads) {
-        iS_s[k] = D.S[j0i + k];
-        iQ_s[k] = D.Q[j0i + k];
-        iDV_s[k] = D.DV[j0i + k];
-      }
-    } else {  // unusual data (many tiny inner runs): search the prep arrays in global memory
-      wS = D.S + j0i;
-      wQ = D.Q + j0i;
-      wDV = D.DV + j0i;
-    }
-  }
+  grid_dependency_wait();
+  const uint4 pf = D.prefix[lt];  // tile output offset from rle_sums
   __syncthreads();
   trace_stamp(B.trace, gt, 5);
 
@@ -399,42 +373,106 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
   uint32_t cnt[kRPer];
   uint64_t val[kRPer];
   uint64_t sc = 0, sw = 0;
-  {
-    uint32_t a = 0;
-    if (vmode == V_DRLE && kb < nr) a = run_search(wS, 0, win_s - 1, g0 + kb);
 #pragma unroll
-    for (int r = 0; r < kRPer; r++) {
-      const uint32_t k = kb + r;
-      uint64_t c = 0, v = 0;
-      if (k < nr) {
-        const uint64_t g = g0 + k;
-        c = D.cnt_base +
-            (cnt_staged ? (D.cnt_w ? extract_bits(cnt_s, uint64_t(k) * D.cnt_w, D.cnt_w) : 0ull)
-                        : extract_bits_global(reinterpret_cast<const uint32_t*>(D.cnt_packed), g * D.cnt_w, D.cnt_w));
-        if (c > D.n) { errbits |= 0x2u; c = 0; }
-        if (vmode == V_DRLE) {
-          while (a + 1 < win_s && wS[a + 1] <= g) a++;
-          v = wQ[a] + (g - wS[a] + 1) * wDV[a];
-        } else if (linear) {
-          v = D.val_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.val_packed), g * D.val_w, D.val_w);
-        } else {
-          const uint64_t x = D.val_base + (D.val_w ? extract_bits(valbits_s, uint64_t(k) * D.val_w, D.val_w) : 0ull);
-          if (vmode == V_BP) {
-            v = x;
-          } else if (vmode == V_DICT) {
-            uint64_t idx = x;
-            if (idx >= D.entries) { errbits |= 0x1u; idx = 0; }
-            v = ob == 8 ? __ldg(reinterpret_cast<const unsigned long long*>(D.dict) + idx)
-                        : uint64_t(__ldg(reinterpret_cast<const uint32_t*>(D.dict) + idx));
-          } else {  // V_F2I
-            v = uint64_t(__double_as_longlong(double(int64_t(x)) / kPow10r[D.d]));
+  for (int r = 0; r < kRPer; r++) {
+    const uint32_t k = kb + r;
+    uint64_t c = 0, v = 0;
+    if (k < nr) {
+      const uint64_t g = g0 + k;
+      c = D.cnt_base +
+          (cnt_staged ? (D.cnt_w ? extract_bits(cnt_s, uint64_t(k) * D.cnt_w, D.cnt_w) : 0ull)
+                      : extract_bits_global(reinterpret_cast<const uint32_t*>(D.cnt_packed), g * D.cnt_w, D.cnt_w));
+      if (c > D.n) { errbits |= 0x2u; c = 0; }
+      if (linear) {
+        v = D.val_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.val_packed), g * D.val_w, D.val_w);
+      } else if (vmode != V_DRLE) {
+        const uint64_t x = D.val_base + (D.val_w ? extract_bits(valbits_s, uint64_t(k) * D.val_w, D.val_w) : 0ull);
+        if (vmode == V_BP) {
+          v = x;
+        } else if (vmode == V_DICT) {
+          uint64_t idx = x;
+          if (idx >= D.entries) { errbits |= 0x1u; idx = 0; }
+          v = ob == 8 ? __ldg(reinterpret_cast<const unsigned long long*>(D.dict) + idx)
+                      : uint64_t(__ldg(reinterpret_cast<const uint32_t*>(D.dict) + idx));
+        } else {  // V_F2I
+          v = uint64_t(__double_as_longlong(double(int64_t(x)) / kPow10r[D.d]));
+        }
+      }
+    }
+    cnt[r] = uint32_t(c);
+    val[r] = v;
+    sc += c;
+    if (linear) sw += v * c;
+  }
+  if (vmode == V_DRLE) {
+    // values of outer runs g = Q_j + (g - S_j + 1) dv_j, j the inner run holding g: the inner runs from the
+    // anchor tile on are scanned into a shared-memory window (pass after pass until every run is covered)
+    const uint4 rec = D.anchor[lt];  // same address in every thread: one broadcast load
+    uint32_t ws = rec.x;
+    uint64_t Sbase = rec.y, Qbase = (uint64_t(rec.w) << 32) | rec.z;
+    uint32_t pending = 0;  // bit r: run r still needs its value
+#pragma unroll
+    for (int r = 0; r < kRPer; r++)
+      if (kb + r < nr) pending |= 1u << r;
+    for (int pass = 0;; pass++) {
+      const uint32_t nload = ws < D.n_inner ? min(uint32_t(kRleWindow), D.n_inner - ws) : 0u;
+      // blocked load: thread t takes inner runs ws + 4t .. +3
+      uint64_t dcv[4], dvv[4], lc = 0, lw = 0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t k = tid * 4 + q;
+        dcv[q] = 0;
+        dvv[q] = 0;
+        if (k < nload) {
+          const uint64_t j = ws + k;
+          dcv[q] = D.idc_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.idc_packed), j * D.idc_w, D.idc_w);
+          dvv[q] = D.idv_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.idv_packed), j * D.idv_w, D.idv_w);
+          if (dcv[q] > D.nruns) dcv[q] = 0;
+        }
+        lc += dcv[q];
+        lw += dvv[q] * dcv[q];
+      }
+      uint64_t tcs, tws;
+      const uint64_t ec2 = block_excl_scan_u64<kThreads>(lc, warp_s, &tcs);
+      const uint64_t ew2 = block_excl_scan_u64<kThreads>(lw, warp_s, &tws);
+      {
+        uint64_t c = Sbase + ec2, w = Qbase + ew2;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const uint32_t k = tid * 4 + q;
+          if (k < kRleWindow) {
+            iS_s[k] = uint32_t(min(c, uint64_t(0xFFFFFFFFu)));
+            iQ_s[k] = w;
+            iDV_s[k] = dvv[q];
+          }
+          c += dcv[q];
+          w += dvv[q] * dcv[q];
+        }
+      }
+      __syncthreads();
+      const uint64_t Send = Sbase + tcs;
+      if (pending && nload) {
+        uint32_t a = 0;
+#pragma unroll
+        for (int r = 0; r < kRPer; r++) {
+          const uint64_t g = g0 + kb + r;
+          if ((pending >> r & 1u) && g < Send && g >= iS_s[0]) {
+            if (a == 0) a = run_search(iS_s, 0, nload - 1, uint32_t(g));
+            while (a + 1 < nload && iS_s[a + 1] <= g) a++;
+            val[r] = iQ_s[a] + (g - iS_s[a] + 1) * iDV_s[a];
+            pending &= ~(1u << r);
           }
         }
       }
-      cnt[r] = uint32_t(c);
-      val[r] = v;
-      sc += c;
-      if (linear) sw += v * c;
+      const bool more = __syncthreads_or(pending != 0);
+      if (!more) break;
+      if (!nload || pass > 64) {  // the inner runs do not cover this tile: corrupt
+        errbits |= 0x2u;
+        break;
+      }
+      ws += nload;
+      Sbase = Send;
+      Qbase += tws;
     }
   }
   trace_stamp(B.trace, gt, 1);
@@ -611,9 +649,9 @@ __global__ void __launch_bounds__(kThreads) rle_big_kernel(const __grid_constant
 
 }  // namespace
 
-cudaError_t launch_rle_prep(const PrepBatch& b, cudaStream_t s) {
-  if (!b.total_tiles) return cudaSuccess;
-  rle_prep_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
+cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s) {
+  if (!b.total_units) return cudaSuccess;
+  rle_sums_kernel<<<b.total_units, kThreads, 0, s>>>(b);
   return cudaGetLastError();
 }
 
@@ -624,8 +662,20 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
     cudaFuncSetAttribute(rle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRleOutBytes + 16);
     configured = true;
   }
-  rle_kernel<<<b.total_tiles, kThreads, kRleOutBytes + 16, s>>>(b);
-  return cudaGetLastError();
+  // programmatic dependent launch: rle_kernel's prologue overlaps rle_sums (CDM_PDL=0 disables)
+  static const bool pdl = !(std::getenv("CDM_PDL") && std::getenv("CDM_PDL")[0] == '0');
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(b.total_tiles);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kRleOutBytes + 16;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rle_kernel, b);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s) {

@@ -386,7 +386,7 @@ struct cdm_batch {
   std::vector<FpBatch> fp;
   std::vector<uint32_t> fp_maxw;
   std::vector<ScanBatch> scan;
-  std::vector<PrepBatch> prep;
+  std::vector<SumsBatch> sums;
   std::vector<RleBatch> rle;
   std::vector<Lz4Batch> lz4;
   std::vector<uint32_t> lz4_max_sub;
@@ -424,7 +424,7 @@ namespace {
 // Returns the arena bytes; `zero_bytes` = prefix of the arena that must start zeroed.
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
-  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->prep.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
+  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
   B->err_dev = A.take<uint32_t>(nj ? nj : 1);
@@ -507,65 +507,39 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     sb.lb = A.take<uint4>(tiles);
     B->scan.push_back(sb);
   }
-  // rle_prep: an OUTER descriptor per RLE chunk (tile prefixes) + an INNER one per Delta|RLE value lineage
-  struct PrepRef { int job; bool inner; };
-  std::vector<PrepDesc> pd;
-  std::vector<PrepRef> pref;
-  for (int j : rlj) {
-    const Bound& b = B->jobs[j];
-    PrepDesc o{};
-    o.kind = PREP_OUTER;
-    o.a_packed = b.dev_chunk + b.counts.off;
-    o.a_base = b.counts.base;
-    o.a_w = uint16_t(b.counts.w);
-    o.linear = b.vmode == V_LINEAR;
-    if (o.linear) { o.b_packed = b.dev_chunk + b.main.off; o.b_base = b.main.base; o.b_w = uint16_t(b.main.w); }
-    o.n_items = b.nruns;
-    o.total = uint32_t(b.rows);
-    o.ntiles = uint32_t(div_up(b.nruns, kPrepOuterTile));
-    o.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
-    o.err_idx = uint32_t(j);
-    pd.push_back(o);
-    pref.push_back({j, false});
-    if (b.vmode == V_DRLE) {
-      PrepDesc in{};
-      in.kind = PREP_INNER;
-      in.a_packed = b.dev_chunk + b.inner_dc.off;
-      in.a_base = b.inner_dc.base;
-      in.a_w = uint16_t(b.inner_dc.w);
-      in.b_packed = b.dev_chunk + b.inner_dv.off;
-      in.b_base = b.inner_dv.base;
-      in.b_w = uint16_t(b.inner_dv.w);
-      in.base = b.inner_base;
-      in.n_items = b.n_inner;
-      in.total = b.nruns;
-      in.ntiles = uint32_t(div_up(b.n_inner, kPrepInnerTile));
-      in.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
-      in.err_idx = uint32_t(j);
-      pd.push_back(in);
-      pref.push_back({j, true});
+  // rle_sums: per RLE chunk the outer tile sums (+ the inner tile sums of a Delta|RLE value lineage)
+  for (auto& g : groups(rlj)) {
+    SumsBatch sb{};
+    sb.err = B->err_dev;
+    uint32_t units = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      SumsChunk& d = sb.d[sb.n++];
+      d.cnt_packed = b.dev_chunk + b.counts.off;
+      d.cnt_base = b.counts.base;
+      d.cnt_w = uint16_t(b.counts.w);
+      d.linear = b.vmode == V_LINEAR;
+      d.drle = b.vmode == V_DRLE;
+      if (d.linear) { d.dv_packed = b.dev_chunk + b.main.off; d.dv_base = b.main.base; d.dv_w = uint16_t(b.main.w); }
+      if (d.drle) {
+        d.dv_packed = b.dev_chunk + b.inner_dv.off; d.dv_base = b.inner_dv.base; d.dv_w = uint16_t(b.inner_dv.w);
+        d.dc_packed = b.dev_chunk + b.inner_dc.off; d.dc_base = b.inner_dc.base; d.dc_w = uint16_t(b.inner_dc.w);
+        d.base = b.inner_base;
+        d.n_inner = b.n_inner;
+        d.inner_tiles = uint32_t(div_up(b.n_inner, kInnerTile));
+      }
+      d.nruns = b.nruns;
+      d.rows = uint32_t(b.rows);
+      d.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
+      d.outer_units = uint32_t(div_up(d.outer_tiles, 8));
+      d.inner_units = uint32_t(div_up(d.inner_tiles, 8));
+      d.unit0 = units;
+      d.err_idx = uint32_t(j);
+      d.done = A.take<uint32_t>(1);
+      units += d.outer_units + d.inner_units;
     }
-  }
-  std::vector<std::vector<int>> pgroups;
-  for (size_t i = 0; i < pd.size(); i += kMaxBatch) {
-    std::vector<int> g;
-    for (size_t k = i; k < std::min(pd.size(), i + size_t(kMaxBatch)); k++) g.push_back(int(k));
-    pgroups.push_back(g);
-  }
-  for (auto& g : pgroups) {
-    PrepBatch pb{};
-    pb.err = B->err_dev;
-    uint32_t tiles = 0;
-    for (int k : g) {
-      PrepDesc d = pd[k];
-      d.tile0 = tiles;
-      tiles += d.ntiles;
-      pb.d[pb.n++] = d;
-    }
-    pb.total_tiles = tiles;
-    pb.ticket = A.take<unsigned long long>(1);
-    pb.lb = A.take<uint4>(tiles);
-    B->prep.push_back(pb);
+    sb.total_units = units;
+    B->sums.push_back(sb);
   }
   // rle
   for (auto& g : groups(rlj)) {
@@ -611,25 +585,22 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   // ---- non-zeroed region: optional per-tile trace (env CDM_TRACE=<csv path>)
   if (std::getenv("CDM_TRACE")) {
     for (auto& sb : B->scan) sb.trace = A.take<uint64_t>(size_t(sb.total_tiles) * 8);
-    for (auto& pb : B->prep) pb.trace = A.take<uint64_t>(size_t(pb.total_tiles) * 8);
+    for (auto& pb : B->sums) pb.trace = A.take<uint64_t>(size_t(pb.total_units) * 8);
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
   // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
-  // per RLE chunk: tile prefixes (OUTER) and the inner run table (INNER)
-  std::map<int, PrepDesc*> outer_of, inner_of;
-  for (auto& pb : B->prep)
+  // per RLE chunk: tile sums and the scans the last CTA of rle_sums writes
+  std::map<int, const SumsChunk*> sums_of;
+  for (auto& pb : B->sums)
     for (uint32_t k = 0; k < pb.n; k++) {
-      PrepDesc& d = pb.d[k];
-      if (d.kind == PREP_OUTER) {
-        d.prefix = A.take<uint4>(d.outer_tiles);
-        outer_of[int(d.err_idx)] = &d;
-      } else {
-        d.S = A.take<uint32_t>(d.n_items);
-        d.Q = A.take<uint64_t>(d.n_items);
-        d.DV = A.take<uint64_t>(d.n_items);
-        d.tstart = A.take<uint32_t>(d.outer_tiles + 1);
-        inner_of[int(d.err_idx)] = &d;
+      SumsChunk& d = pb.d[k];
+      d.tsum = A.take<uint64_t>(size_t(d.outer_tiles) * 2);
+      d.prefix = A.take<uint4>(d.outer_tiles);
+      if (d.drle) {
+        d.isum = A.take<uint64_t>(size_t(d.inner_tiles) * 2);
+        d.anchor = A.take<uint4>(d.outer_tiles);
       }
+      sums_of[int(d.err_idx)] = &d;
     }
   for (auto& rb : B->rle) {
     rb.big.entries = A.take<RleBig::Entry>(rb.big.max_slots);
@@ -638,10 +609,13 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
     for (uint32_t k = 0; k < rb.n; k++) {
       RleDesc& d = rb.d[k];
-      d.prefix = outer_of[int(d.err_idx)]->prefix;
+      const SumsChunk* sc = sums_of[int(d.err_idx)];
+      d.prefix = sc->prefix;
       if (d.vmode == V_DRLE) {
-        PrepDesc* in = inner_of[int(d.err_idx)];
-        d.S = in->S; d.Q = in->Q; d.DV = in->DV; d.tstart = in->tstart;
+        const Bound& b = B->jobs[d.err_idx];
+        d.anchor = sc->anchor;
+        d.idv_packed = b.dev_chunk + b.inner_dv.off; d.idv_base = b.inner_dv.base; d.idv_w = uint16_t(b.inner_dv.w);
+        d.idc_packed = b.dev_chunk + b.inner_dc.off; d.idc_base = b.inner_dc.base; d.idc_w = uint16_t(b.inner_dc.w);
       }
     }
   }
@@ -735,7 +709,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, fs)); n++; B->fam_launches[F_SCAN]++; }
         break;
       case F_RLE:
-        for (auto& pb : B->prep) { CUDA_TRY(launch_rle_prep(pb, fs)); n++; B->fam_launches[F_RLE]++; }
+        for (auto& pb : B->sums) { CUDA_TRY(launch_rle_sums(pb, fs)); n++; B->fam_launches[F_RLE]++; }
         for (auto& rb : B->rle) {
           CUDA_TRY(launch_rle(rb, fs));
           n++;
@@ -1226,7 +1200,7 @@ static void dump_trace(cdm_batch* b, const char* path) {
     }
   };
   for (size_t i = 0; i < b->scan.size(); i++) dump("scan", int(i), b->scan[i].trace, b->scan[i].total_tiles);
-  for (size_t i = 0; i < b->prep.size(); i++) dump("prep", int(i), b->prep[i].trace, b->prep[i].total_tiles);
+  for (size_t i = 0; i < b->sums.size(); i++) dump("sums", int(i), b->sums[i].trace, b->sums[i].total_units);
   for (size_t i = 0; i < b->rle.size(); i++) dump("rle", int(i), b->rle[i].trace, b->rle[i].total_tiles);
   std::fclose(f);
 }

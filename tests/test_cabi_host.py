@@ -32,7 +32,7 @@ def test_kernels_are_sm100a_sass():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True, text=True).stdout
-    for k in ("fp_kernel", "scan_kernel", "rle_kernel", "rle_big_kernel", "rle_prep_kernel", "lz4_kernel"):
+    for k in ("fp_kernel", "scan_kernel", "rle_kernel", "rle_big_kernel", "rle_sums_kernel", "lz4_kernel"):
         assert k in sass
     assert "UBLKCP" in sass  # TMA bulk copies (cp.async.bulk) in the FP / scan kernels
 

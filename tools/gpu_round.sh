@@ -10,7 +10,7 @@ if [ "$2" == "ncu" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
      --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 5 --warmup 2 --no-cpu-baseline > /dev/null 2>&1
   echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fp_kernel|rle_kernel|inner_kernel|scan_kernel" \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fp_kernel|rle_kernel|rle_sums_kernel|scan_kernel" \
      -s 12 -c 6 -o gpurun_out/prof_${TAG} -f python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ncu_full_${TAG}.log 2>&1
   echo "ncu full rc=$?"
 fi

@@ -15,7 +15,7 @@ k, rd, wr, dur = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "d
                                        "gpu__time_duration.sum"))
 units = rows[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-fam = {"fp_kernel": "fp", "scan_kernel": "scan", "rle_prep_kernel": "rle", "rle_kernel": "rle", "rle_big_kernel": "rle",
+fam = {"fp_kernel": "fp", "scan_kernel": "scan", "rle_sums_kernel": "rle", "rle_kernel": "rle", "rle_big_kernel": "rle",
        "lz4_kernel": "lz4", "lz4_smem_kernel": "lz4"}
 acc = {}
 detail = []
