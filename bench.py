@@ -11,8 +11,11 @@ One step = decode every chunk of the three columns (all hot-path rows this workl
   value  device-resident: compressed chunks already in HBM, decoded bytes / device time (CUDA events on
          the launching stream around cdm_batch_launch; L2 flushed by a 256 MiB write between steps,
          outside the events).
-  e2e    through the public C-ABI from PINNED HOST memory: cdm_submit_batch (H2D copies on the copy
-         stream overlapped with decode, Johnson order) + cdm_wait (D2H of each chunk's error word).
+  e2e    through the public C-ABI from PINNED HOST memory: cdm_pipeline_launch (the H4 schedule -- H2D
+         copies in Johnson order overlapped with the fused decodes of earlier groups -- captured once as a
+         CUDA graph) + cdm_pipeline_results (each chunk's error word read on the host).  The same schedule
+         enqueued group by group by the host (cdm_submit_batch + cdm_wait) is reported under
+         e2e.submit_batch.
   roofline  the dominant kernel family (by device time) against the measured HBM copy peak.
   cpu_baseline  the CPU oracle (oracle/, plain C, chunk-parallel) on the same chunks.
 
@@ -287,12 +290,28 @@ def main():
         err_bits |= r["error_bits"]
 
     # ---------------------------------------------------------------- end to end from pinned host (e2e)
+    # (a) cdm_pipeline: the H4 schedule (Johnson order, groups, copies overlapped with decodes) captured
+    #     once as a CUDA graph; every step re-copies all compressed bytes from pinned host memory, decodes
+    #     them and reads the per-chunk error words back (the headline e2e)
+    # (b) cdm_submit_batch + cdm_wait: the same schedule enqueued by the host group by group (reported too)
+    pipe = cdm.Pipeline(eng, decs_host)
     for _ in range(max(1, args.warmup)):
+        pipe.launch(stream)
+        pipe.results()
         for t in eng.submit_batch(decs_host):
             eng.wait(t)
     e2e_steps = max(3, args.steps // 4)
     torch.cuda.synchronize()
     e2e_total = 0.0
+    for _ in range(e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pipe.launch(stream)
+        for r in pipe.results(raise_on_error=False):
+            err_bits |= r["error_bits"]
+        e2e_total += time.perf_counter() - t0
+    sub_total = 0.0
     e2e_submit = 0.0
     for _ in range(e2e_steps):
         flush.zero_()
@@ -301,9 +320,10 @@ def main():
         tickets = eng.submit_batch(decs_host)
         e2e_submit += time.perf_counter() - t0
         for t in tickets:
-            r = eng.wait(t)
+            r = eng.wait(t, raise_on_error=False)
             err_bits |= r["error_bits"]
-        e2e_total += time.perf_counter() - t0
+        sub_total += time.perf_counter() - t0
+    pipe.close()
     h2d_gbs = measure_h2d(torch)
 
     # ---------------------------------------------------------------- reduce over ranks (metadata only)
@@ -311,16 +331,17 @@ def main():
     if world > 1:
         meta = torch.tensor([decoded, compressed, n_chunks, err_bits], dtype=torch.int64, device="cuda")
         dist.all_reduce(meta, op=dist.ReduceOp.SUM)
-        tmax = torch.tensor([dev_s, e2e_total], dtype=torch.float64, device="cuda")
+        tmax = torch.tensor([dev_s, e2e_total, sub_total], dtype=torch.float64, device="cuda")
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tot_decoded, tot_comp, tot_chunks, tot_err = [int(x) for x in meta.tolist()]
-        dev_s, e2e_total = [float(x) for x in tmax.tolist()]
+        dev_s, e2e_total, sub_total = [float(x) for x in tmax.tolist()]
     else:
         tot_decoded, tot_comp, tot_chunks, tot_err = decoded, compressed, n_chunks, err_bits
 
     if rank == 0:
         value = tot_decoded * args.steps / dev_s / 1e9
         e2e = tot_decoded * e2e_steps / e2e_total / 1e9
+        e2e_sub = tot_decoded * e2e_steps / sub_total / 1e9
         peak, peak_src = load_peaks()
         # dominant kernel family by device time; algorithmic bytes = compressed read + decoded written
         fam_ms = {FAMILY_NAMES[i]: kern[FAMILY_NAMES[i]] for i in range(5)}
@@ -367,8 +388,12 @@ def main():
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": tot_comp,
                     "d2h_bytes_per_step": 4 * tot_chunks, "pcie_h2d_gbs_measured": round(h2d_gbs, 1),
                     "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_gbs, 1),
-                    "host_submit_ms_per_step": round(e2e_submit * 1e3 / e2e_steps, 4),
-                    "how": "cdm_submit_batch from pinned host (H2D + decode, Johnson order) + cdm_wait per chunk"},
+                    "how": "cdm_pipeline_launch + cdm_pipeline_results per step: H2D copies of every compressed "
+                           "chunk from pinned host + fused decodes (Johnson order, groups overlapped) + per-chunk "
+                           "error words to host, as one CUDA graph captured at setup",
+                    "submit_batch": {"value": round(e2e_sub, 2),
+                                     "host_submit_ms_per_step": round(e2e_submit * 1e3 / e2e_steps, 4),
+                                     "how": "cdm_submit_batch + cdm_wait per chunk (host enqueues each group)"}},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "errors": tot_err,

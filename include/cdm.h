@@ -74,14 +74,19 @@ typedef enum {
 typedef struct cdm_engine cdm_engine;
 typedef struct cdm_cascade cdm_cascade;
 typedef struct cdm_batch cdm_batch;
+typedef struct cdm_pipeline cdm_pipeline;
 
 typedef struct {
   uint32_t n_slots;       /* device staging ring depth, >= 2 (default 4) */
   uint64_t slot_bytes;    /* bytes per staging slot; a chunk must fit one slot (default 64 MiB) */
   void *copy_stream;      /* cudaStream_t for H2D copies, or NULL: the engine creates one */
-  void *decode_stream;    /* cudaStream_t for decode kernels, or NULL: the engine creates one */
+  void *decode_stream;    /* cudaStream_t for decode kernels: every group decodes in order on it; NULL: the
+                             engine gives each staging slot its own decode stream, so groups held by
+                             different slots decode concurrently (the default) */
   double pcie_gbps;       /* H2D link estimate for Johnson costs t_i (default 55 GB/s) */
-  double decode_gbps;     /* decoded-bytes/s estimate for Johnson costs d_i (default 3000 GB/s) */
+  double decode_gbps;     /* element-parallel decode rate for Johnson costs d_i (default 5000 GB/s); the
+                             other kernel families are costed at fixed fractions of it measured on B200
+                             (scan 1/2, RLE 1/8, LZ4 1/40, raw copy 1) */
   uint32_t order_policy;  /* 0 = submission order, 1 = Johnson's rule */
   uint32_t reserved;
 } cdm_engine_opts;
@@ -155,6 +160,22 @@ CDM_API cdm_status cdm_batch_create(cdm_engine *e, const cdm_job *jobs, size_t n
 CDM_API cdm_status cdm_batch_launch(cdm_batch *b, void *stream, uint32_t *n_launches);
 CDM_API cdm_status cdm_batch_results(cdm_batch *b, void *stream, cdm_result *results);
 CDM_API cdm_status cdm_batch_destroy(cdm_batch *b);
+
+/* ---- pipelines: a fixed job set from PINNED host memory, captured once into a CUDA graph ----
+ * The H4 schedule of cdm_submit_batch (Johnson order, groups, H2D copies overlapped with the fused
+ * decodes of earlier groups) recorded as one graph: every launch re-copies each job's
+ * host_chunk (which must be pinned and may change contents, not size or structure, between launches)
+ * and decodes it into the job's dev_out / dev_offsets.  Staging and scratch are owned by the pipeline.
+ * create: binds/validates every job on the host, allocates, captures and instantiates (no device work);
+ *         CDM_E_CAPACITY if one chunk exceeds the engine's slot_bytes;
+ * launch: one cudaGraphLaunch on `stream` (cudaStream_t, NULL = engine decode stream): the copies and
+ *         decodes are ordered after the stream's prior work and the stream waits for them;
+ * results: synchronises that stream and fills results[i] for job i from the error words the graph
+ *         wrote to mapped pinned memory; CDM_E_CORRUPT if any job has error bits. */
+CDM_API cdm_status cdm_pipeline_create(cdm_engine *e, const cdm_job *jobs, size_t n, cdm_pipeline **out);
+CDM_API cdm_status cdm_pipeline_launch(cdm_pipeline *p, void *stream);
+CDM_API cdm_status cdm_pipeline_results(cdm_pipeline *p, cdm_result *results);
+CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
 
 /* ---- instrumentation ---- */
 /* Record CUDA events around each kernel family launched by cdm_batch_launch (0 = off).  After

@@ -22,7 +22,8 @@ FAMILIES = ["fp", "scan", "rle", "lz4", "copy"]
 SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_create", "cdm_cascade_destroy",
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
            "cdm_submit_batch", "cdm_wait", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
-           "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms"]
+           "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
+           "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy"]
 
 
 class EngineOpts(ctypes.Structure):
@@ -86,6 +87,10 @@ def lib():
         "cdm_batch_destroy": [vp],
         "cdm_batch_set_timing": [vp, st],
         "cdm_batch_kernel_ms": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)],
+        "cdm_pipeline_create": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(vp)],
+        "cdm_pipeline_launch": [vp, vp],
+        "cdm_pipeline_results": [vp, ctypes.POINTER(Result)],
+        "cdm_pipeline_destroy": [vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -172,21 +177,29 @@ class Decode:
     dev_chunk: object = None
 
     def cjob(self) -> Job:
-        return Job(self.cascade.h.value, _ptr(self.host_chunk), _ptr(self.dev_chunk), _nbytes(self.host_chunk),
-                   _ptr(self.dev_out), _nbytes(self.dev_out), _ptr(self.dev_offsets), _nbytes(self.dev_offsets))
+        # the buffers are held by this object, so their addresses are fixed: marshal once
+        key = (self.cascade.h.value, id(self.host_chunk), id(self.dev_chunk), id(self.dev_out), id(self.dev_offsets))
+        cj = self.__dict__.get("_cj")
+        if cj is None or cj[0] != key:
+            cj = (key, Job(self.cascade.h.value, _ptr(self.host_chunk), _ptr(self.dev_chunk), _nbytes(self.host_chunk),
+                           _ptr(self.dev_out), _nbytes(self.dev_out), _ptr(self.dev_offsets),
+                           _nbytes(self.dev_offsets)))
+            self.__dict__["_cj"] = cj
+        return cj[1]
 
 
 class Engine:
     """cdm_engine_create: staging ring + copy/decode streams on one device."""
 
     def __init__(self, device: int = 0, n_slots: int = 4, slot_bytes: int = 64 << 20, copy_stream=None,
-                 decode_stream=None, order_policy: int = 1, pcie_gbps: float = 55.0, decode_gbps: float = 3000.0):
+                 decode_stream=None, order_policy: int = 1, pcie_gbps: float = 55.0, decode_gbps: float = 5000.0):
         o = EngineOpts(n_slots, slot_bytes, _stream_ptr(copy_stream), _stream_ptr(decode_stream), pcie_gbps,
                        decode_gbps, order_policy, 0)
         h = ctypes.c_void_p()
         _check(lib().cdm_engine_create(device, ctypes.byref(o), ctypes.byref(h)))
         self.h = h
         self._keep = []
+        self._arrays = {}
 
     def submit(self, d: Decode) -> int:
         t = ctypes.c_uint64()
@@ -196,8 +209,15 @@ class Engine:
 
     def submit_batch(self, ds: list[Decode]) -> list[int]:
         n = len(ds)
-        jobs = (Job * n)(*[d.cjob() for d in ds])
-        tickets = (ctypes.c_uint64 * n)()
+        cjs = [d.cjob() for d in ds]
+        key = tuple(id(j) for j in cjs)
+        cached = self._arrays.get(key)
+        if cached is None:  # the same list resubmitted (a scan loop) reuses its marshalled job array
+            cached = ((Job * n)(*cjs), (ctypes.c_uint64 * n)(), cjs)
+            if len(self._arrays) > 64:
+                self._arrays.clear()
+            self._arrays[key] = cached
+        jobs, tickets, _ = cached
         _check(lib().cdm_submit_batch(self.h, jobs, n, tickets))
         return list(tickets)
 
@@ -256,6 +276,38 @@ class Batch:
     def close(self) -> None:
         if getattr(self, "h", None) and _lib is not None:
             _lib.cdm_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+class Pipeline:
+    """cdm_pipeline_create/launch/results: the H2D + decode schedule of a fixed job set from PINNED host
+    memory, captured once into a CUDA graph; each launch re-copies and re-decodes every job."""
+
+    def __init__(self, engine: Engine, ds: list[Decode]):
+        n = len(ds)
+        self.n = n
+        self._ds = ds
+        jobs = (Job * max(n, 1))(*[d.cjob() for d in ds])
+        h = ctypes.c_void_p()
+        _check(lib().cdm_pipeline_create(engine.h, jobs, n, ctypes.byref(h)))
+        self.h = h
+        self._res = (Result * max(n, 1))()
+
+    def launch(self, stream=None) -> None:
+        _check(lib().cdm_pipeline_launch(self.h, _stream_ptr(stream)))
+
+    def results(self, raise_on_error: bool = True) -> list[dict]:
+        rc = lib().cdm_pipeline_results(self.h, self._res)
+        if rc and (raise_on_error or rc != 4):
+            _check(rc)
+        return [self._res[i].as_dict() for i in range(self.n)]
+
+    def close(self) -> None:
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.cdm_pipeline_destroy(self.h)
             self.h = None
 
     def __del__(self):

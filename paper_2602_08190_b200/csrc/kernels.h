@@ -4,6 +4,7 @@
 // passed by value as __grid_constant__ parameters (no descriptor upload), tiles of all chunks are
 // enumerated globally (desc.tile0 = first global tile of the chunk).
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -208,6 +209,10 @@ cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);
+// engine bookkeeping: zero a 16-byte-aligned scratch prefix; move error words into mapped pinned memory
+// (copy, then zero them for the next launch)
+cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);
+cudaError_t launch_harvest(uint32_t* err, uint32_t* host_mapped, uint32_t n, cudaStream_t s);
 int device_sms();
 
 }  // namespace cdm

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -377,7 +378,6 @@ struct Alloc {  // bump allocator over one device arena; pass 1 sizes, pass 2 as
 
 // ============================================================================ device batches
 enum Family { F_FP = 0, F_SCAN = 1, F_RLE = 2, F_LZ4 = 3, F_COPY = 4 };
-static cudaStream_t engine_family_stream(cdm_engine* e, int fam);
 
 struct cdm_batch {
   cdm_engine* e = nullptr;
@@ -399,6 +399,9 @@ struct cdm_batch {
   uint32_t* err_dev = nullptr;
   uint32_t* err_host = nullptr;
   bool own_err_host = true;
+  bool zeroed_by_caller = false;  // the engine zeroes the scratch prefix before waiting for the copy
+  uint32_t* err_external = nullptr;  // pipelines: error words live in one array shared by all groups
+  cudaStream_t* fam = nullptr;     // the family streams concurrent kernel families fork onto
   // fork/join events: independent kernel families run concurrently on the engine's family streams
   cudaEvent_t fork = nullptr;
   cudaEvent_t join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -427,7 +430,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
-  B->err_dev = A.take<uint32_t>(nj ? nj : 1);
+  B->err_dev = B->err_external ? B->err_external : A.take<uint32_t>(nj ? nj : 1);
   std::vector<int> fpj, scj, rlj, drj, lzj;
   for (size_t i = 0; i < nj; i++) {
     const Bound& b = B->jobs[i];
@@ -581,7 +584,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     rb.big.max_slots = slots;
     B->rle.push_back(rb);
   }
-  *zero_bytes = A.off;
+  *zero_bytes = (A.off + 15) & ~size_t(15);  // launch_zero works in 16-byte words (the next take pads to 256)
   // ---- non-zeroed region: optional per-tile trace (env CDM_TRACE=<csv path>)
   if (std::getenv("CDM_TRACE")) {
     for (auto& sb : B->scan) sb.trace = A.take<uint64_t>(size_t(sb.total_tiles) * 8);
@@ -683,11 +686,14 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
                        !B->copies.empty() || !B->zero_offsets.empty()};
   int nfam = 0;
   for (bool h : has) nfam += h;
-  CUDA_TRY(cudaMemsetAsync(B->err_dev, 0, sizeof(uint32_t) * std::max<size_t>(1, B->jobs.size()), s));
+  // error words, tickets, look-back words and counters start at zero (one tiny kernel, not a memset)
+  if (!B->zeroed_by_caller) CUDA_TRY(launch_zero(B->arena, B->zero_bytes, s));
   // fork: with several families each runs on its own stream (the latency-bound scan/RLE chains overlap
   // the bandwidth-bound FP kernel); a single family stays on `s`
   static const bool serial = std::getenv("CDM_SERIAL") != nullptr;
-  const bool fork = nfam > 1 && B->e && !serial;
+  // the RLE family always forks: its stream has the lowest priority, so the short bandwidth-bound kernels
+  // of later groups (and the engine's bookkeeping kernels) get SMs as soon as an RLE CTA retires
+  const bool fork = (nfam > 1 || has[F_RLE]) && B->fam && !serial;
   if (fork) {
     if (!B->fork) {
       CUDA_TRY(cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming));
@@ -697,7 +703,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   }
   for (int fam = 0; fam < 5; fam++) {
     if (!has[fam]) continue;
-    cudaStream_t fs = fork ? engine_family_stream(B->e, fam) : s;
+    cudaStream_t fs = fork ? B->fam[fam] : s;
     if (fork) CUDA_TRY(cudaStreamWaitEvent(fs, B->fork, 0));
     cudaEvent_t ta = nullptr;
     if (B->timing) { ta = ev_get(B, evk++); CUDA_TRY(cudaEventRecord(ta, fs)); }
@@ -775,6 +781,11 @@ struct cdm_engine {
     bool used = false;
     uint8_t* arena = nullptr;  // decode scratch of the group held by this slot
     size_t arena_bytes = 0;
+    // decode + family streams of this slot: groups in different slots decode concurrently (a latency-bound
+    // RLE group does not hold back the bandwidth-bound group behind it); shared when the user passed one
+    cudaStream_t ds = nullptr;
+    cudaStream_t fam[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool own_streams = false;
   };
   std::vector<Slot> slots;
   uint32_t next_slot = 0;
@@ -793,12 +804,12 @@ struct cdm_engine {
   uint64_t next_ticket = 1, next_group = 1;
   std::vector<cudaEvent_t> event_pool;
   cudaStream_t fam[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // concurrent kernel families
-  uint32_t* err_host = nullptr;  // pinned ring of per-chunk error words
+  uint32_t* err_host = nullptr;  // pinned (mapped) ring of per-chunk error words
+  uint32_t* err_mapped = nullptr;  // its device alias: harvest_kernel stores there
   uint32_t err_ring = 0, err_next = 0;
   std::map<uint32_t, uint64_t> err_owner;  // ring start position -> group whose words live there
 };
 
-static cudaStream_t engine_family_stream(cdm_engine* e, int fam) { return e->fam[fam]; }
 
 static cdm_status harvest_group(cdm_engine* e, uint64_t gid) {
   auto it = e->groups.find(gid);
@@ -829,7 +840,7 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   if (o.n_slots < 2) return fail(CDM_E_INVALID_ARG, "n_slots must be >= 2");
   if (o.slot_bytes == 0) o.slot_bytes = 64ull << 20;
   if (o.pcie_gbps <= 0) o.pcie_gbps = 55.0;
-  if (o.decode_gbps <= 0) o.decode_gbps = 3000.0;
+  if (o.decode_gbps <= 0) o.decode_gbps = 5000.0;
   e->opts = o;
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaFree(nullptr));  // create the context
@@ -837,15 +848,33 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   else { CUDA_TRY(cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking)); e->own_copy = true; }
   if (o.decode_stream) e->decode = static_cast<cudaStream_t>(o.decode_stream);
   else { CUDA_TRY(cudaStreamCreateWithFlags(&e->decode, cudaStreamNonBlocking)); e->own_decode = true; }
-  for (auto& fs : e->fam) CUDA_TRY(cudaStreamCreateWithFlags(&fs, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;  // numerically: least (lowest) and greatest (highest) priority
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  auto make_fams = [&](cudaStream_t* fam) -> cudaError_t {
+    for (int f = 0; f < 5; f++) {
+      cudaError_t ce = cudaStreamCreateWithPriority(&fam[f], cudaStreamNonBlocking, f == F_RLE ? prio_lo : prio_hi);
+      if (ce != cudaSuccess) return ce;
+    }
+    return cudaSuccess;
+  };
+  CUDA_TRY(make_fams(e->fam));
   e->slots.resize(o.n_slots);
   for (auto& s : e->slots) {
+    if (o.decode_stream) {  // the caller's decode stream orders every group
+      s.ds = e->decode;
+      for (int f = 0; f < 5; f++) s.fam[f] = e->fam[f];
+    } else {
+      CUDA_TRY(cudaStreamCreateWithPriority(&s.ds, cudaStreamNonBlocking, prio_hi));
+      CUDA_TRY(make_fams(s.fam));
+      s.own_streams = true;
+    }
     if (cudaMalloc(&s.dev, o.slot_bytes) != cudaSuccess) return fail(CDM_E_OOM, "staging slot cudaMalloc failed");
     CUDA_TRY(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
   }
   e->err_ring = 4096;
-  CUDA_TRY(cudaHostAlloc(&e->err_host, sizeof(uint32_t) * e->err_ring, cudaHostAllocDefault));
+  CUDA_TRY(cudaHostAlloc(&e->err_host, sizeof(uint32_t) * e->err_ring, cudaHostAllocMapped));
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->err_mapped), e->err_host, 0));
   *out = e.release();
   return CDM_OK;
 }
@@ -858,6 +887,11 @@ extern "C" CDM_API cdm_status cdm_engine_destroy(cdm_engine* e) {
   for (auto& kv : e->groups) if (kv.second.done) cudaEventDestroy(kv.second.done);
   for (auto ev : e->event_pool) cudaEventDestroy(ev);
   for (auto& s : e->slots) {
+    if (s.own_streams) {
+      cudaStreamSynchronize(s.ds);
+      cudaStreamDestroy(s.ds);
+      for (auto fs : s.fam) { cudaStreamSynchronize(fs); cudaStreamDestroy(fs); }
+    }
     cudaFree(s.dev);
     cudaFree(s.arena);
     cudaEventDestroy(s.copied);
@@ -961,25 +995,28 @@ static cdm_status group_copy(cdm_engine* e, PendingGroup& pg) {
 static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* tickets_out) {
   cdm_engine::Slot& s = e->slots[pg.slot];
   auto& bs = pg.bs;
-  CUDA_TRY(cudaStreamWaitEvent(e->decode, s.copied, 0));
   auto batch = std::make_unique<cdm_batch>();
   batch->e = e;
   batch->device = e->device;
+  batch->fam = s.fam;
   for (auto& b : bs) batch->jobs.push_back(b);
   Alloc sizing;
   size_t zb = 0;
   size_t need = layout_batch(batch.get(), sizing, &zb);
   if (need > s.arena_bytes) {
-    if (s.arena) { CUDA_TRY(cudaStreamSynchronize(e->decode)); cudaFree(s.arena); s.arena = nullptr; }
+    if (s.arena) { CUDA_TRY(cudaStreamSynchronize(s.ds)); cudaFree(s.arena); s.arena = nullptr; }
     size_t cap = std::max(need, size_t(1) << 20);
     if (cudaMalloc(&s.arena, cap) != cudaSuccess) return fail(CDM_E_OOM, "scratch cudaMalloc failed");
     s.arena_bytes = cap;
   }
   cdm_status st = batch_build(batch.get(), s.arena, s.arena_bytes);
   if (st) return st;
-  CUDA_TRY(cudaMemsetAsync(s.arena, 0, batch->zero_bytes, e->decode));  // fresh tickets/flags per group
+  // fresh error words / counters for this group, zeroed while the group's copy is still in flight
+  CUDA_TRY(launch_zero(s.arena, batch->zero_bytes, s.ds));
+  batch->zeroed_by_caller = true;
+  CUDA_TRY(cudaStreamWaitEvent(s.ds, s.copied, 0));
   uint32_t nl = 0;
-  st = batch_enqueue(batch.get(), e->decode, &nl);
+  st = batch_enqueue(batch.get(), s.ds, &nl);
   if (st) return st;
   // pinned error words for this group (contiguous ring slice; an old group still there is harvested)
   const uint32_t nj = uint32_t(bs.size());
@@ -999,13 +1036,13 @@ static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* ticket
       ++it;
     }
   }
-  CUDA_TRY(cudaMemcpyAsync(e->err_host + ep, batch->err_dev, sizeof(uint32_t) * nj, cudaMemcpyDeviceToHost, e->decode));
-  CUDA_TRY(cudaEventRecord(s.freed, e->decode));
+  CUDA_TRY(launch_harvest(batch->err_dev, e->err_mapped + ep, nj, s.ds));
+  CUDA_TRY(cudaEventRecord(s.freed, s.ds));
   const uint64_t gid = e->next_group++;
   cdm_engine::Group& g = e->groups[gid];
   if (!e->event_pool.empty()) { g.done = e->event_pool.back(); e->event_pool.pop_back(); }
   else CUDA_TRY(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventRecord(g.done, e->decode));
+  CUDA_TRY(cudaEventRecord(g.done, s.ds));
   g.err_pos = ep;
   g.njobs = nj;
   g.pending = nj;
@@ -1045,6 +1082,20 @@ extern "C" CDM_API cdm_status cdm_submit(cdm_engine* e, const cdm_job* job, uint
   return submit_group(e, bs, {job}, ticket);
 }
 
+// Relative decode rate of a bound job's kernel family (measured on B200, config 2/3 bench lines): the
+// Johnson cost d_i must rank a Delta|RLE chunk (latency-bound expansion) above a Dict|BitPack chunk of
+// the same decoded size, or the slowest decode lands at the end of the pipeline.
+static double family_rate(const Bound& b) {
+  switch (b.kind) {
+    case PlanKind::Fp: return 1.0;
+    case PlanKind::Scan: return 0.5;
+    case PlanKind::Rle: return 0.125;
+    case PlanKind::Str: return b.lz4 ? 0.025 : 0.5;
+    case PlanKind::RawCopy: return 1.0;
+  }
+  return 1.0;
+}
+
 // H3: Johnson's rule on (t_i = compressed / PCIe, d_i = decoded / decode rate):
 // jobs with t <= d first ascending t, then the rest descending d; ties by submission index.
 static void johnson(const double* tt, const double* dd, size_t n, std::vector<size_t>* order) {
@@ -1064,41 +1115,54 @@ extern "C" CDM_API cdm_status cdm_johnson_order(const double* t, const double* d
   return CDM_OK;
 }
 
-extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* jobs, size_t n, uint64_t* tickets) {
-  if (!e || (n && (!jobs || !tickets))) return fail(CDM_E_INVALID_ARG, "null argument");
-  CUDA_TRY(cudaSetDevice(e->device));
+// H3 + H4 planning shared by cdm_submit_batch and cdm_pipeline_create: bind every job, order them by
+// Johnson's rule, cut the order into groups (each group = one staging region + one multi-chunk batch).
+static cdm_status plan_groups(cdm_engine* e, const cdm_job* jobs, size_t n, uint64_t cap_bytes,
+                              std::vector<PendingGroup>* groups_out, std::vector<size_t>* order_out,
+                              std::vector<size_t>* first_job_out) {
   std::vector<Bound> all(n);
   uint64_t total = 0;
   for (size_t i = 0; i < n; i++) {
     cdm_status st = bind_job(jobs[i], &all[i]);
     if (st) { g_last = "job " + std::to_string(i) + ": " + g_last; return st; }
-    if (all[i].total > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "chunk larger than a staging slot");
+    if (all[i].total > cap_bytes) return fail(CDM_E_CAPACITY, "chunk larger than a staging slot");
     total += all[i].total;
   }
-  std::vector<size_t> order(n);
+  std::vector<size_t>& order = *order_out;
+  order.resize(n);
   std::iota(order.begin(), order.end(), size_t(0));
   if (e->opts.order_policy == 1) {
     std::vector<double> tt(n), dd(n);
     for (size_t i = 0; i < n; i++) {
       tt[i] = double(all[i].total) / (e->opts.pcie_gbps * 1e9);
-      dd[i] = double(all[i].payload + all[i].offsets_bytes) / (e->opts.decode_gbps * 1e9);
+      dd[i] = double(all[i].payload + all[i].offsets_bytes) / (e->opts.decode_gbps * 1e9 * family_rate(all[i]));
     }
     johnson(tt.data(), dd.data(), n, &order);
   }
   // groups: consecutive jobs (in issue order) up to a target size, so several groups pipeline
   uint64_t min_group = 2ull << 20;
   if (const char* g = std::getenv("CDM_GROUP_MIN_BYTES")) min_group = std::strtoull(g, nullptr, 10);
-  const uint64_t target = std::min<uint64_t>(e->opts.slot_bytes, std::max<uint64_t>(min_group, total / 8));
-  std::vector<PendingGroup> groups;
-  std::vector<size_t> first_job;
+  const uint64_t target = std::min<uint64_t>(cap_bytes, std::max<uint64_t>(min_group, total / 8));
+  // a group also closes as soon as its decode estimate exceeds its copy estimate (with Johnson order
+  // those lead the pipeline: their decode should start as soon as their own bytes have arrived)
+  static const bool split_decode_heavy = !(std::getenv("CDM_GROUP_SPLIT") && std::getenv("CDM_GROUP_SPLIT")[0] == '0');
+  auto& groups = *groups_out;
+  auto& first_job = *first_job_out;
+  groups.clear();
+  first_job.clear();
   size_t k = 0;
   while (k < n) {
     PendingGroup pg;
     uint64_t bytes = 0;
+    double gt = 0, gd = 0;
     size_t m = k;
     while (m < n && pg.js.size() < size_t(kMaxBatch)) {
       const uint64_t add = ((all[order[m]].total + 255) & ~uint64_t(255));
-      if (!pg.js.empty() && (bytes + add > e->opts.slot_bytes || bytes >= target)) break;
+      if (!pg.js.empty() && (bytes + add > cap_bytes || bytes >= target)) break;
+      if (!pg.js.empty() && split_decode_heavy && gd > gt) break;
+      const Bound& bj = all[order[m]];
+      gt += double(bj.total) / (e->opts.pcie_gbps * 1e9);
+      gd += double(bj.payload + bj.offsets_bytes) / (e->opts.decode_gbps * 1e9 * family_rate(bj));
       bytes += add;
       pg.bs.push_back(all[order[m]]);
       pg.js.push_back(&jobs[order[m]]);
@@ -1108,6 +1172,16 @@ extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* job
     groups.push_back(std::move(pg));
     k = m;
   }
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* jobs, size_t n, uint64_t* tickets) {
+  if (!e || (n && (!jobs || !tickets))) return fail(CDM_E_INVALID_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  std::vector<PendingGroup> groups;
+  std::vector<size_t> order, first_job;
+  cdm_status st0 = plan_groups(e, jobs, n, e->opts.slot_bytes, &groups, &order, &first_job);
+  if (st0) return st0;
   // the copy engine runs up to n_slots groups ahead of the decodes: copies are enqueued before the host
   // spends time building a group's launches
   const size_t ahead = e->slots.size();
@@ -1123,6 +1197,231 @@ extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* job
     if (st) return st;
     for (size_t j = 0; j < tk.size(); j++) tickets[order[first_job[g] + j]] = tk[j];
   }
+  return CDM_OK;
+}
+
+// ============================================================================ pipelines (CUDA graphs)
+// The whole H2D -> decode schedule of a fixed job set, captured once into a CUDA graph: copies of every
+// group on one copy branch, each group's zero / fused kernels / error harvest on a decode branch that
+// depends on its own copy.  A launch is one cudaGraphLaunch, so the GPU runs the pipeline without the
+// host enqueueing each group (the submit path costs ~20 us of host time per group).
+struct cdm_pipeline {
+  cdm_engine* e = nullptr;
+  int device = 0;
+  size_t n = 0;
+  uint8_t* staging = nullptr;  // every group's chunks, back to back (no slot reuse inside a pipeline)
+  uint8_t* arena = nullptr;    // every group's decode scratch
+  uint32_t* err_host = nullptr, *err_mapped = nullptr;  // per job in ISSUE order, mapped pinned
+  uint32_t* err_dev = nullptr;  // per job in issue order: every group's kernels OR into their slice
+  std::vector<std::unique_ptr<cdm_batch>> batches;
+  std::vector<Bound> bound;    // per job (submission index)
+  std::vector<size_t> pos;     // issue position of job i
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> events;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t last_stream = nullptr;
+  ~cdm_pipeline() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (err_dev) cudaFree(err_dev);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto ev : events) cudaEventDestroy(ev);
+    for (auto st : streams) cudaStreamDestroy(st);
+    batches.clear();
+    if (staging) cudaFree(staging);
+    if (arena) cudaFree(arena);
+    if (err_host) cudaFreeHost(err_host);
+  }
+};
+
+extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* jobs, size_t n, cdm_pipeline** out) {
+  if (!e || !out || (n && !jobs)) return fail(CDM_E_INVALID_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  auto P = std::make_unique<cdm_pipeline>();
+  P->e = e;
+  P->device = e->device;
+  P->n = n;
+  std::vector<PendingGroup> groups;
+  std::vector<size_t> order, first_job;
+  cdm_status st = plan_groups(e, jobs, n, e->opts.slot_bytes, &groups, &order, &first_job);
+  if (st) return st;
+  // staging layout: group after group, chunks 256-aligned (one copy per chunk)
+  std::vector<size_t> stage_off;
+  size_t stage_bytes = 0;
+  for (auto& g : groups)
+    for (auto& b : g.bs) {
+      stage_off.push_back(stage_bytes);
+      stage_bytes += (b.total + 255) & ~size_t(255);
+    }
+  if (cudaMalloc(&P->staging, std::max<size_t>(stage_bytes, 256)) != cudaSuccess)
+    return fail(CDM_E_OOM, "pipeline staging cudaMalloc failed");
+  {
+    size_t q = 0;
+    for (auto& g : groups)
+      for (auto& b : g.bs) b.dev_chunk = P->staging + stage_off[q++];
+  }
+  // one batch per group over its own arena slice; error words in one array (issue order)
+  if (cudaMalloc(&P->err_dev, sizeof(uint32_t) * std::max<size_t>(1, n)) != cudaSuccess)
+    return fail(CDM_E_OOM, "pipeline error words cudaMalloc failed");
+  CUDA_TRY(cudaMemset(P->err_dev, 0, sizeof(uint32_t) * std::max<size_t>(1, n)));
+  std::vector<size_t> arena_off, zero_bytes;
+  size_t arena_bytes = 0;
+  for (size_t gi = 0; gi < groups.size(); gi++) {
+    auto& g = groups[gi];
+    auto B = std::make_unique<cdm_batch>();
+    B->e = e;
+    B->device = e->device;
+    B->err_external = P->err_dev + first_job[gi];
+    for (auto& b : g.bs) B->jobs.push_back(b);
+    Alloc sizing;
+    size_t zb = 0;
+    const size_t need = layout_batch(B.get(), sizing, &zb);
+    arena_off.push_back(arena_bytes);
+    arena_bytes += (need + 255) & ~size_t(255);
+    P->batches.push_back(std::move(B));
+  }
+  if (cudaMalloc(&P->arena, std::max<size_t>(arena_bytes, 256)) != cudaSuccess)
+    return fail(CDM_E_OOM, "pipeline scratch cudaMalloc failed");
+  // counters and look-back words reset themselves at the end of every launch; they start at zero once
+  CUDA_TRY(cudaMemset(P->arena, 0, std::max<size_t>(arena_bytes, 256)));
+  for (size_t g = 0; g < groups.size(); g++) {
+    cdm_batch* B = P->batches[g].get();
+    st = batch_build(B, P->arena + arena_off[g], arena_bytes - arena_off[g]);
+    if (st) return st;
+    B->zeroed_by_caller = true;
+  }
+  P->bound.resize(n);
+  P->pos.resize(n);
+  for (size_t g = 0; g < groups.size(); g++)
+    for (size_t j = 0; j < groups[g].bs.size(); j++) {
+      P->bound[order[first_job[g] + j]] = groups[g].bs[j];
+      P->pos[order[first_job[g] + j]] = first_job[g] + j;
+    }
+  CUDA_TRY(cudaHostAlloc(&P->err_host, sizeof(uint32_t) * std::max<size_t>(1, n), cudaHostAllocMapped));
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&P->err_mapped), P->err_host, 0));
+  std::memset(P->err_host, 0, sizeof(uint32_t) * std::max<size_t>(1, n));
+  // streams for the capture: origin, copy, and up to 4 decode lanes (each with its 5 family streams)
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  auto mk = [&](int prio) -> cudaStream_t {
+    cudaStream_t x = nullptr;
+    if (cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio) == cudaSuccess) P->streams.push_back(x);
+    return x;
+  };
+  auto mkev = [&]() -> cudaEvent_t {
+    cudaEvent_t x = nullptr;
+    if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) == cudaSuccess) P->events.push_back(x);
+    return x;
+  };
+  size_t max_lanes = 4;
+  if (const char* v = std::getenv("CDM_PIPE_LANES")) max_lanes = std::max(1, std::atoi(v));
+  const bool use_prio = !(std::getenv("CDM_PIPE_PRIO") && std::getenv("CDM_PIPE_PRIO")[0] == '0');
+  if (!use_prio) prio_lo = prio_hi = 0;
+  const size_t lanes = std::min<size_t>(std::max<size_t>(groups.size(), 1), max_lanes);
+  cudaStream_t origin = mk(prio_hi), copy = mk(prio_hi);
+  std::vector<cudaStream_t> ds(lanes);
+  std::vector<std::array<cudaStream_t, 5>> fam(lanes);
+  for (size_t l = 0; l < lanes; l++) {
+    ds[l] = mk(prio_hi);
+    for (int f = 0; f < 5; f++) fam[l][f] = mk(f == F_RLE ? prio_lo : prio_hi);
+  }
+  for (auto x : P->streams) if (!x) return fail(CDM_E_CUDA, "pipeline stream creation failed");
+  std::vector<cudaEvent_t> copied(groups.size());
+  for (auto& ev : copied) ev = mkev();
+  cudaEvent_t start = mkev(), copy_end = mkev();
+  std::vector<cudaEvent_t> lane_end(lanes);
+  for (auto& ev : lane_end) ev = mkev();
+  for (auto x : P->events) if (!x) return fail(CDM_E_CUDA, "pipeline event creation failed");
+
+  CUDA_TRY(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed));
+  auto abort_capture = [&](cdm_status s2) {
+    cudaGraph_t g2 = nullptr;
+    cudaStreamEndCapture(origin, &g2);
+    if (g2) cudaGraphDestroy(g2);
+    cudaGetLastError();
+    return s2;
+  };
+#define CAP_TRY(x)                                                                                   \
+  do {                                                                                               \
+    cudaError_t ce_ = (x);                                                                           \
+    if (ce_ != cudaSuccess) return abort_capture(fail(CDM_E_CUDA, std::string(#x ": ") + cudaGetErrorString(ce_))); \
+  } while (0)
+  CAP_TRY(cudaEventRecord(start, origin));
+  CAP_TRY(cudaStreamWaitEvent(copy, start, 0));
+  for (size_t l = 0; l < lanes; l++) CAP_TRY(cudaStreamWaitEvent(ds[l], start, 0));
+  // copy branch: Johnson order, one copy per chunk
+  for (size_t g = 0; g < groups.size(); g++) {
+    for (size_t j = 0; j < groups[g].bs.size(); j++)
+      CAP_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(groups[g].bs[j].dev_chunk), groups[g].js[j]->host_chunk,
+                              groups[g].bs[j].total, cudaMemcpyHostToDevice, copy));
+    CAP_TRY(cudaEventRecord(copied[g], copy));
+  }
+  CAP_TRY(cudaEventRecord(copy_end, copy));
+  // decode branches: group g on lane g % lanes
+  for (size_t g = 0; g < groups.size(); g++) {
+    const size_t l = g % lanes;
+    cdm_batch* B = P->batches[g].get();
+    B->fam = fam[l].data();
+    CAP_TRY(cudaStreamWaitEvent(ds[l], copied[g], 0));
+    uint32_t nl = 0;
+    cdm_status s2 = batch_enqueue(B, ds[l], &nl);
+    if (s2) return abort_capture(s2);
+  }
+  for (size_t l = 0; l < lanes; l++) {
+    CAP_TRY(cudaEventRecord(lane_end[l], ds[l]));
+    CAP_TRY(cudaStreamWaitEvent(origin, lane_end[l], 0));
+  }
+  CAP_TRY(cudaStreamWaitEvent(origin, copy_end, 0));
+  // one harvest at the end: every job's error word to mapped pinned memory, then zeroed for the next launch
+  CAP_TRY(launch_harvest(P->err_dev, P->err_mapped, uint32_t(n), origin));
+#undef CAP_TRY
+  CUDA_TRY(cudaStreamEndCapture(origin, &P->graph));
+  // kernel nodes keep the priority of the stream they were captured on (RLE lowest, the rest highest)
+  CUDA_TRY(cudaGraphInstantiate(&P->exec, P->graph, use_prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
+  *out = P.release();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_pipeline_launch(cdm_pipeline* p, void* stream) {
+  if (!p) return fail(CDM_E_INVALID_ARG, "null pipeline");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->e->decode;
+  CUDA_TRY(cudaGraphLaunch(p->exec, s));
+  p->last_stream = s;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_pipeline_results(cdm_pipeline* p, cdm_result* results) {
+  if (!p) return fail(CDM_E_INVALID_ARG, "null pipeline");
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (p->last_stream) CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+  bool bad = false;
+  for (size_t i = 0; i < p->n; i++) {
+    const uint32_t w = p->err_host[p->pos[i]];
+    if (results) {
+      const Bound& b = p->bound[i];
+      cdm_result& r = results[i];
+      r.rows = b.rows;
+      r.payload_bytes = b.payload;
+      r.offsets_bytes = b.offsets_bytes;
+      r.compressed_bytes = b.total;
+      r.chunk_id = b.chunk_id;
+      r.error_bits = w;
+      r.status = w ? CDM_E_CORRUPT : CDM_OK;
+    }
+    if (w && !bad) {
+      bad = true;
+      g_last = "job " + std::to_string(i) + ": device error bits " + std::to_string(w);
+    }
+  }
+  return bad ? CDM_E_CORRUPT : CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline* p) {
+  if (!p) return CDM_OK;
+  cudaSetDevice(p->device);
+  if (p->last_stream) cudaStreamSynchronize(p->last_stream);
+  delete p;
   return CDM_OK;
 }
 
@@ -1146,6 +1445,7 @@ extern "C" CDM_API cdm_status cdm_synchronize(cdm_engine* e) {
   if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
   CUDA_TRY(cudaStreamSynchronize(e->copy));
   CUDA_TRY(cudaStreamSynchronize(e->decode));
+  for (auto& s : e->slots) CUDA_TRY(cudaStreamSynchronize(s.ds));
   std::vector<uint64_t> gids;
   for (auto& kv : e->groups) gids.push_back(kv.first);
   for (uint64_t gid : gids) {
@@ -1161,6 +1461,7 @@ extern "C" CDM_API cdm_status cdm_batch_create(cdm_engine* e, const cdm_job* job
   CUDA_TRY(cudaSetDevice(e->device));
   auto B = std::make_unique<cdm_batch>();
   B->e = e;
+  B->fam = e->fam;
   B->device = e->device;
   for (size_t i = 0; i < n; i++) {
     if (!jobs[i].dev_chunk) return fail(CDM_E_INVALID_ARG, "job " + std::to_string(i) + ": dev_chunk is null");

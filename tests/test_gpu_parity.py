@@ -1,7 +1,8 @@
 """GPU parity: the CUDA path (through the C-ABI) == the CPU oracle, element by element (-m gpu).
 
-Every chunk is decoded twice on the device -- through the pipelined engine from pinned host memory
-(cdm_submit_batch) and through the device-resident batch API (cdm_batch_*) -- and compared byte for byte
+Every chunk is decoded three ways on the device -- through the pipelined engine from pinned host memory
+(cdm_submit_batch), through the same schedule captured as a CUDA graph (cdm_pipeline_*), and through the
+device-resident batch API (cdm_batch_*) -- and compared byte for byte
 with oracle/ on the same seeded inputs.  Integer/byte work must be bit-exact and Float2Int is one IEEE
 division on both sides, so the tolerance is zero everywhere.  Outputs are pre-filled
 with a sentinel so an element that is never written, or written outside [0, n), is caught.
@@ -44,16 +45,22 @@ def _outputs(chunk):
 
 
 def gpu_decode(engine, casc, chunks, resident=False, expect_error=False):
-    """Decode chunks on the GPU; returns [(payload numpy, offsets numpy|None, result dict)]."""
+    """Decode chunks on the GPU; returns [(payload numpy, offsets numpy|None, result dict)].
+    resident: False = cdm_submit_batch, True = cdm_batch_* on device copies, "pipeline" = cdm_pipeline_*."""
     decs, bufs = [], []
     for ch in chunks:
         out, offs, info = _outputs(ch)
         d = cdm.Decode(casc, cdm.pinned(ch), out, offs)
-        if resident:
+        if resident is True:
             d.dev_chunk = torch.from_numpy(ch).cuda()
         decs.append(d)
         bufs.append((out, offs, info))
-    if resident:
+    if resident == "pipeline":
+        p = cdm.Pipeline(engine, decs)
+        p.launch()
+        res = p.results(raise_on_error=not expect_error)
+        p.close()
+    elif resident:
         b = cdm.Batch(engine, decs)
         b.launch()
         res = b.results(raise_on_error=not expect_error)
@@ -81,7 +88,7 @@ def check_parity(engine, spec, col_or_chunks, dtype=None, width=0, rows_per_chun
     else:
         chunks = col_or_chunks
     casc = cdm.Cascade(spec, dtype, width)
-    modes = [False, True] if both else [True]
+    modes = [False, "pipeline", True] if both else [True]
     for resident in modes:
         got = gpu_decode(engine, casc, chunks, resident=resident)
         for ch, (payload, offs, r) in zip(chunks, got):
@@ -298,7 +305,7 @@ def test_corrupt_dict_index_sets_error(engine):
                                        cdm1.bitpack([i % 5 for i in range(5000)], 3, 0)], entries=4, E=8)
     ch = cdm1.build(root, cdm1.I64, 8, 5000, cascade_hash=_hash(spec))
     casc = cdm.Cascade(spec, cdm.I64)
-    for resident in (False, True):
+    for resident in (False, "pipeline", True):
         (_, _, r), = gpu_decode(engine, casc, [ch], resident=resident, expect_error=True)
         assert r["error_bits"] & cdm.ERR_DICT_INDEX
 
@@ -381,3 +388,51 @@ def test_repeated_launches_graph_safe(engine):
             exp, _ = oracle.decode_chunk(ch)
             assert np.array_equal(o.cpu().numpy()[: exp.size], exp)
     b.close()
+
+
+def test_pipeline_relaunch_and_error_positions(engine):
+    """A captured pipeline re-copies and re-decodes on every launch; error words map back to job order."""
+    g = TPCH(0.05)
+    specs = [("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("l_quantity", "Dict|BitPack"),
+             ("l_comment", "Str|[LZ4,BitPack]"), ("l_extendedprice", "Float2Int|BitPack")]
+    decs, outs, exps = [], [], []
+    for name, spec in specs:
+        col = g.column(name)
+        casc = cdm.Cascade(spec, col.dtype, col.width)
+        for ch in encoder.encode_chunks(spec, col, 120_000):
+            out, offs, _ = _outputs(ch)
+            decs.append(cdm.Decode(casc, cdm.pinned(ch), out, offs))
+            outs.append((out, offs))
+            exps.append(oracle.decode_chunk(ch))
+    # a corrupt Dict chunk in the middle of the job list
+    spec = "Dict|BitPack"
+    root = cdm1.Node(cdm1.DICT, 5000, [cdm1.raw(np.arange(4, dtype=np.int64).tobytes(), eb=8),
+                                       cdm1.bitpack([i % 5 for i in range(5000)], 3, 0)], entries=4, E=8)
+    bad = cdm1.build(root, cdm1.I64, 8, 5000, cascade_hash=_hash(spec))
+    bout, boffs, _ = _outputs(bad)
+    k = len(decs) // 2
+    decs.insert(k, cdm.Decode(cdm.Cascade(spec, cdm.I64), cdm.pinned(bad), bout, boffs))
+    p = cdm.Pipeline(engine, decs)
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        for out, offs in outs:
+            out.fill_(SENTINEL)
+            if offs is not None:
+                offs.fill_(-7)
+        torch.cuda.synchronize()
+        p.launch(s)
+        res = p.results(raise_on_error=False)
+        for i, r in enumerate(res):
+            assert bool(r["error_bits"]) == (i == k), (i, r)
+        j = 0
+        for i in range(len(decs)):
+            if i == k:
+                continue
+            (out, offs), (exp, exp_offs) = outs[j], exps[j]
+            assert np.array_equal(out.cpu().numpy()[: exp.size], exp)
+            if exp_offs is not None:
+                assert np.array_equal(offs.cpu().numpy()[: exp_offs.size], exp_offs)
+            j += 1
+    with pytest.raises(cdm.CdmError):
+        p.results()
+    p.close()
