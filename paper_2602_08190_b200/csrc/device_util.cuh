@@ -253,5 +253,40 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* sm
   return wp + x - v;
 }
 
+// Exclusive scan of a pair (a, b) of u64 per thread across the CTA with one barrier pair; *ta, *tb = totals.
+// smem_warp holds 2 * NT/32 words.  The warp totals are scanned by every warp with one shuffle scan.
+template <int NT>
+__device__ __forceinline__ void block_excl_scan_pair(uint64_t a, uint64_t b, uint64_t* smem_warp, uint64_t* ea,
+                                                     uint64_t* eb, uint64_t* ta, uint64_t* tb) {
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  constexpr int NW = NT / 32;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t x = a, y = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t u = __shfl_up_sync(FULL, x, o);
+    const uint64_t v = __shfl_up_sync(FULL, y, o);
+    if (lane >= uint32_t(o)) { x += u; y += v; }
+  }
+  if (lane == 31) { smem_warp[2 * warp] = x; smem_warp[2 * warp + 1] = y; }
+  __syncthreads();
+  // lane k < NW holds warp k's totals; an inclusive shuffle scan over them
+  uint64_t wx = lane < uint32_t(NW) ? smem_warp[2 * lane] : 0ull;
+  uint64_t wy = lane < uint32_t(NW) ? smem_warp[2 * lane + 1] : 0ull;
+#pragma unroll
+  for (int o = 1; o < NW; o <<= 1) {
+    const uint64_t u = __shfl_up_sync(FULL, wx, o);
+    const uint64_t v = __shfl_up_sync(FULL, wy, o);
+    if (lane >= uint32_t(o)) { wx += u; wy += v; }
+  }
+  const uint64_t px = warp ? __shfl_sync(FULL, wx, warp - 1) : 0ull;
+  const uint64_t py = warp ? __shfl_sync(FULL, wy, warp - 1) : 0ull;
+  *ta = __shfl_sync(FULL, wx, NW - 1);
+  *tb = __shfl_sync(FULL, wy, NW - 1);
+  __syncthreads();
+  *ea = px + x - a;
+  *eb = py + y - b;
+}
+
 }  // namespace dev
 }  // namespace cdm

@@ -14,8 +14,8 @@ constexpr int kMaxBatch = 32;      // descriptors per launch (more chunks -> mor
 constexpr int kFpTile = 4096;      // H5 values per tile = 256 threads x 16
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
 constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
-constexpr int kRleOutBytes = 44 * 1024;    // rle_kernel: a tile's output is staged in shared memory (dynamic)
 constexpr int kRleWindow = 1024;   // V_DRLE inner runs scanned into shared memory per pass
+constexpr uint32_t kRleSegRows = 32768;  // rle_kernel: output rows per run-start bitmap segment
 constexpr uint32_t kRleBigLimit = 1u << 15;  // a tile with more output rows is expanded by rle_big
 constexpr uint32_t kRleBigPiece = 8192;       // rows per rle_big work item
 constexpr int kThreads = 256;
@@ -90,8 +90,8 @@ struct RleDesc {
   void* out;
   const uint8_t* idv_packed;  // V_DRLE inner dv / dc
   const uint8_t* idc_packed;
-  const uint4* anchor;        // V_DRLE per outer tile {j0, S_j0, Q_j0}: window start (rle_sums)
-  const uint4* prefix;        // per outer tile exclusive prefix {_, count, w} (rle_sums)
+  const uint4* prefix;        // [ntiles] exclusive prefix {count lo, count hi, w lo, w hi} (rle_scan)
+  const uint4* anchor;        // V_DRLE [ntiles] {j0, S_j0, Q lo, Q hi}: window start (rle_scan)
   uint64_t idv_base;
   uint64_t idc_base;
   uint64_t cnt_base;
@@ -139,32 +139,29 @@ struct RleBatch {
   uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   uint32_t big_enabled;          // 0: rle_big is not launched -> oversize tiles are expanded in place
-  uint32_t debug;                // CDM_DEBUG_RLE bits (experiments only): 1 = skip output stores
   RleBig big;
   RleDesc d[kMaxBatch];
 };
 
-// rle_sums: per-tile sums of the RLE family, fully parallel (no look-back).  The LAST CTA to finish a
-// chunk (threadfence + atomic counter, reset afterwards) scans that chunk's tile sums:
-//   outer tiles (kRleTile runs): prefix[t] = {_, sum of counts before t, sum of dv*count before t}
-//   inner tiles (kInnerTile inner runs, Delta|RLE value lineage): anchor[t] = {j0, S, Q lo, Q hi} for the
-//     inner tile holding outer run t*kRleTile: its first inner run j0, the outer run S where j0 starts and
-//     Q = base + sum of dv*dc before j0 (written by the inner tile itself while scanning: no search).
+// rle_sums: per-tile sums of the RLE family, fully parallel (no look-back, no scan): one warp per tile.
+//   outer tiles (kRleTile runs): tsum[t] = {sum of counts, sum of dv*count (root Delta|RLE)}
+//   inner tiles (kInnerTile inner runs of a Delta|RLE value lineage): isum[i] = {sum dc, sum dv*dc}
+// rle_scan (one 1024-thread CTA per chunk, programmatic dependent launch) scans them:
+//   prefix[t] = {sum of counts before t, sum of dv*count before t}
+//   anchor[t] = {j0, S, Q} for the inner tile holding outer run t*kRleTile: its first inner run j0, the
+//     outer run S where j0 starts and Q = base + sum of dv*dc before j0 ({n_inner, 0, 0} if none: corrupt).
 constexpr int kInnerTile = 256;           // inner runs per inner tile sum
-constexpr int kSumsUnitOuter = 8 * 1024;  // outer runs per rle_sums CTA (8 warps x one 1024-run tile)
-constexpr int kSumsUnitInner = 8 * 256;   // inner runs per rle_sums CTA (8 warps x one inner tile)
 
 struct SumsChunk {
   const uint8_t* cnt_packed;   // outer counts
   const uint8_t* dv_packed;    // V_LINEAR: outer dv (slopes); V_DRLE: inner dv
   const uint8_t* dc_packed;    // V_DRLE: inner dc
   uint64_t cnt_base, dv_base, dc_base;
-  uint64_t base;               // V_DRLE: Delta base of the value lineage
   uint64_t* tsum;              // [outer_tiles][2] count, w
   uint64_t* isum;              // [inner_tiles][2] dc, dv*dc
   uint4* prefix;               // [outer_tiles]
-  uint4* anchor;               // [outer_tiles]
-  uint32_t* done;              // completion counter of this chunk
+  uint4* anchor;               // [outer_tiles] (V_DRLE)
+  uint64_t base;               // V_DRLE: Delta base of the value lineage
   uint32_t nruns, rows, n_inner;
   uint32_t outer_tiles, inner_tiles;
   uint32_t unit0;              // first global unit of this chunk
@@ -206,6 +203,7 @@ struct Lz4Batch {
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
 cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
+cudaError_t launch_rle_scan(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);

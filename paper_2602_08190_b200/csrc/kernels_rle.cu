@@ -5,17 +5,16 @@
 // The paper runs PyTorch cumsum on the counts, then a Group-Parallel kernel whose <L,S,C> geometry lets
 // several blocks co-process one big group or one block walk several small groups.  The
 // B200 design splits the family into:
-//  * rle_sums_kernel: NO look-back.  Every warp sums one tile fully in parallel: an outer tile of 1024
-//    runs (sum of counts, plus sum dv*count for arithmetic runs) or an inner tile of 256 Delta|RLE inner
-//    runs (l_orderkey's value lineage: sum dc, sum dv*dc).  The LAST CTA of a chunk (threadfence + counter)
-//    scans the chunk's few thousand tile sums into tile output offsets, per-inner-tile (S, Q) bases and,
-//    per outer tile, the inner tile holding its first run (anchor).
+//  * rle_sums_kernel: NO look-back, no scan.  Every warp sums one tile fully in parallel: an outer tile of
+//    1024 runs (sum of counts, plus sum dv*count for arithmetic runs) or an inner tile of 256 Delta|RLE
+//    inner runs (l_orderkey's value lineage: sum dc, sum dv*dc).
 //  * rle_kernel: one CTA per outer tile, no inter-tile dependency: it stages the tile's packed counts and
-//    values in shared memory, computes the run values through the fused nested provider (BitPack,
-//    Dict|BitPack, Float2Int|BitPack, the Delta|RLE closed form value(g) = Q_j + (g - S_j + 1) dv_j with
-//    S_j, Q_j block-scanned locally from the anchor tile, or arithmetic runs for a root Delta|RLE), scans
-//    the counts in the CTA, reads its output offset from the sums prefix and expands the runs into a
-//    shared-memory image of its output, copied out with aligned 16-byte stores.
+//    values in shared memory (overlapping rle_sums through programmatic dependent launch), reduces the tile
+//    sums before it into its output offset, computes the run values through the fused nested provider
+//    (BitPack, Dict|BitPack, Float2Int|BitPack, the Delta|RLE closed form value(g) = Q_j + (g - S_j + 1) dv_j
+//    with S_j, Q_j block-scanned from the inner tile holding the tile's first run, or arithmetic runs for a
+//    root Delta|RLE), scans the counts in the CTA and expands the runs through a run-start bitmap: lane l of
+//    a warp owns row 32k + l, finds its run with one popc and stores it (coalesced 32-row stores).
 //  * rle_big_kernel: tiles with more than kRleBigLimit output rows (giant runs: o_shippriority is one run
 //    per chunk) are split into 8192-row pieces over every SM ("multiple GPU blocks
 //    co-process a single group"); launched only when a chunk header's max run allows it.
@@ -92,7 +91,7 @@ __device__ __forceinline__ void store_row(uint8_t* out, uint32_t p, uint64_t v, 
 // 4-aligned global row go one per lane, then 128-row windows in which lane l writes rows 4l..4l+3 with one
 // 16-byte store (4-byte rows) or two (8-byte rows).  Called by a full warp.
 __device__ __forceinline__ void expand_warp(const uint32_t* soffs, uint32_t nr, const uint64_t* vals, const uint64_t* slopes,
-                            uint32_t pb, uint32_t pe, uint8_t* out, uint32_t ob, uint32_t gO, bool nostore = false) {
+                            uint32_t pb, uint32_t pe, uint8_t* out, uint32_t ob, uint32_t gO) {
   const uint32_t lane = threadIdx.x & 31;
   if (pb >= pe || nr == 0) return;
   const uint32_t a = min(pe, pb + ((4u - ((gO + pb) & 3u)) & 3u));
@@ -152,9 +151,7 @@ __device__ __forceinline__ void expand_warp(const uint32_t* soffs, uint32_t nr, 
         v[jj] = run_value(vals, slopes, soffs, rr, q);
       }
     }
-    if (nostore) {
-      if ((v[0] ^ v[1] ^ v[2] ^ v[3]) == 0x123456789ull) store_row(out, q0, 0, ob);
-    } else if (q0 + 3 < pe) {
+    if (q0 + 3 < pe) {
       if (ob == 8) {
         st_v2_u64(reinterpret_cast<uint64_t*>(out) + q0, v[0], v[1]);
         st_v2_u64(reinterpret_cast<uint64_t*>(out) + q0 + 2, v[2], v[3]);
@@ -213,44 +210,9 @@ __device__ __forceinline__ void warp_range_sums(const uint32_t* ap, uint64_t aba
   *sba = warp_sum(s2);
 }
 
-// Exclusive scan (2 components) of n pairs v[2i], v[2i+1] by one CTA, in passes of kThreads*8 with carry;
-// calls emit(i, excl0, excl1, v0, v1) for every i; returns totals.
-template <typename Emit>
-__device__ __forceinline__ void cta_scan_pairs(const uint64_t* v, uint32_t n, uint64_t* warp_s, uint64_t* tot0,
-                                               uint64_t* tot1, Emit emit) {
-  uint64_t c0 = 0, c1 = 0;
-  for (uint32_t base = 0; base < n; base += kThreads * 8) {
-    const uint32_t i0 = base + threadIdx.x * 8;
-    uint64_t a[8], b[8], s0 = 0, s1 = 0;
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      a[r] = (i0 + r < n) ? v[2 * (i0 + r)] : 0ull;
-      b[r] = (i0 + r < n) ? v[2 * (i0 + r) + 1] : 0ull;
-      s0 += a[r];
-      s1 += b[r];
-    }
-    uint64_t t0, t1;
-    const uint64_t e0 = block_excl_scan_u64<kThreads>(s0, warp_s, &t0);
-    const uint64_t e1 = block_excl_scan_u64<kThreads>(s1, warp_s, &t1);
-    uint64_t x0 = c0 + e0, x1 = c1 + e1;
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      if (i0 + r < n) emit(i0 + r, x0, x1, a[r], b[r]);
-      x0 += a[r];
-      x1 += b[r];
-    }
-    c0 += t0;
-    c1 += t1;
-  }
-  *tot0 = c0;
-  *tot1 = c1;
-}
-
 __global__ void __launch_bounds__(kThreads) rle_sums_kernel(const __grid_constant__ SumsBatch B) {
   __shared__ SumsChunk D;
-  __shared__ uint64_t warp_s[kThreads / 32];
-  __shared__ uint32_t last_s;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t unit = blockIdx.x;
   {
     int lo = 0, hi = int(B.n) - 1;
@@ -288,68 +250,106 @@ __global__ void __launch_bounds__(kThreads) rle_sums_kernel(const __grid_constan
     }
   }
   if (bad) atomicOr(B.err + D.err_idx, 0x2u);
-  trace_stamp(B.trace, unit, 1);
-  // the last CTA of this chunk scans its tile sums (classic threadfence + counter)
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    last_s = atomicAdd(D.done, 1u) == D.outer_units + D.inner_units - 1;
-  }
-  __syncthreads();
-  if (!last_s) return;
-  __threadfence();
-  trace_stamp(B.trace, unit, 2);
-  uint64_t tc, tw;
-  uint4* prefix = D.prefix;
-  cta_scan_pairs(D.tsum, D.outer_tiles, warp_s, &tc, &tw, [&](uint32_t t, uint64_t c, uint64_t w, uint64_t, uint64_t) {
-    prefix[t] = make_uint4(0u, sat32(c), uint32_t(w), uint32_t(w >> 32));
-  });
-  if (tid == 0 && tc != D.rows) atomicOr(B.err + D.err_idx, 0x2u);
-  if (D.drle) {
-    // inner tile i covers outer runs [S0, S1): it anchors every outer tile whose first run lies there
-    uint4* anchor = D.anchor;
-    const uint64_t nr = D.nruns, base = D.base;
-    uint64_t ic, iw;
-    cta_scan_pairs(D.isum, D.inner_tiles, warp_s, &ic, &iw, [&](uint32_t i, uint64_t c, uint64_t w, uint64_t dc, uint64_t) {
-      const uint64_t S0 = min(c, nr), S1 = min(c + dc, nr);
-      const uint64_t Q = base + w;
-      const uint4 rec = make_uint4(i * uint32_t(kInnerTile), uint32_t(S0), uint32_t(Q), uint32_t(Q >> 32));
-      for (uint64_t t = (S0 + K - 1) / K; t * K < S1; t++) anchor[t] = rec;
-    });
-    if (tid == 0 && ic != D.nruns) atomicOr(B.err + D.err_idx, 0x2u);
-  }
-  if (tid == 0) atomicExch(D.done, 0u);  // graph replays / next launch
   trace_stamp(B.trace, unit, 4);
 }
 
-// ------------------------------------------------------------------------------------------ main
-// One CTA per 1024-run tile; thread t owns runs 4t..4t+3.  The tile's output rows are written by each
-// thread for its own runs (one shared-memory store per row, no searching) into a shared-memory image of
-// the tile's output, which the CTA then copies out with aligned 16-byte stores.
-constexpr int kRPer = K / kThreads;  // 4 runs per thread
+// One 1024-thread CTA per chunk: exclusive scans of the tile sums into per-outer-tile prefixes and anchors.
+constexpr int kScanThreads = 1024;
 
-__global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant__ RleBatch B) {
-  extern __shared__ __align__(16) uint8_t outbuf[];  // kRleOutBytes + 16: the tile's output image
+__global__ void __launch_bounds__(kScanThreads) rle_scan_kernel(const __grid_constant__ SumsBatch B) {
+  __shared__ SumsChunk D;
+  __shared__ uint64_t warp_s[2 * kScanThreads / 32];
+  const uint32_t tid = threadIdx.x;
+  if (tid < sizeof(SumsChunk) / 4)
+    reinterpret_cast<uint32_t*>(&D)[tid] = reinterpret_cast<const uint32_t*>(&B.d[blockIdx.x])[tid];
+  grid_launch_dependents();  // rle_kernel may start staging its chunk data now
+  __syncthreads();
+  if (D.drle)  // outer tiles no inner tile anchors are marked corrupt (window start n_inner)
+    for (uint32_t t = tid; t < D.outer_tiles; t += kScanThreads) D.anchor[t] = make_uint4(D.n_inner, 0u, 0u, 0u);
+  grid_dependency_wait();  // rle_sums complete
+  uint64_t cc = 0, cw = 0;
+  for (uint32_t base = 0; base < D.outer_tiles; base += kScanThreads) {
+    const uint32_t t = base + tid;
+    uint64_t c = 0, w = 0;
+    if (t < D.outer_tiles) {
+      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(D.tsum + 2 * t));
+      c = v.x;
+      w = v.y;
+    }
+    uint64_t ec, ew, tc, tw;
+    block_excl_scan_pair<kScanThreads>(c, w, warp_s, &ec, &ew, &tc, &tw);
+    if (t < D.outer_tiles) {
+      const uint64_t pc = cc + ec, pw = cw + ew;
+      D.prefix[t] = make_uint4(uint32_t(pc), uint32_t(pc >> 32), uint32_t(pw), uint32_t(pw >> 32));
+    }
+    cc += tc;
+    cw += tw;
+  }
+  if (tid == 0 && cc != D.rows) atomicOr(B.err + D.err_idx, 0x2u);
+  if (!D.drle) return;
+  __syncthreads();  // the corrupt-marking stores above precede the real anchors
+  uint64_t ic = 0, iw = 0;
+  for (uint32_t base = 0; base < D.inner_tiles; base += kScanThreads) {
+    const uint32_t i = base + tid;
+    uint64_t dc = 0, dw = 0;
+    if (i < D.inner_tiles) {
+      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(D.isum + 2 * i));
+      dc = v.x;
+      dw = v.y;
+    }
+    uint64_t ec, ew, tc, tw;
+    block_excl_scan_pair<kScanThreads>(dc, dw, warp_s, &ec, &ew, &tc, &tw);
+    if (i < D.inner_tiles) {
+      // inner tile i covers outer runs [S0, S1): it anchors every outer tile whose first run lies there
+      const uint64_t S0 = min(ic + ec, uint64_t(D.nruns)), S1 = min(ic + ec + dc, uint64_t(D.nruns));
+      const uint64_t Q = D.base + iw + ew;
+      const uint4 rec = make_uint4(i * uint32_t(kInnerTile), uint32_t(S0), uint32_t(Q), uint32_t(Q >> 32));
+      for (uint64_t t = (S0 + K - 1) / K; t * K < S1; t++) D.anchor[t] = rec;
+    }
+    ic += tc;
+    iw += tw;
+  }
+  if (tid == 0 && ic != D.nruns) atomicOr(B.err + D.err_idx, 0x2u);
+}
+
+// ------------------------------------------------------------------------------------------ main
+// One CTA per 1024-run tile; thread t owns runs 4t..4t+3.
+//  1. stage the tile's packed counts/values (chunk data: overlaps rle_sums/rle_scan under PDL), then wait;
+//  2. output offset O and (Delta|RLE values) the anchor inner tile from rle_scan; the inner runs from the
+//     anchor on are block-scanned into a shared window that gives every outer run its value;
+//  3. the tile's non-empty runs are compacted (first row, first value, slope) and a bitmap marks the row
+//     where each one starts; row p of the tile belongs to compact run popc(bitmap[0..p]) - 1.  Each warp
+//     owns a contiguous range of 32-row windows: one binary search gives the compact run before its range,
+//     then per window lane l takes row 32k + l with one popc, and the warp stores 32 consecutive rows per
+//     instruction (coalesced, no shared-memory output image).
+constexpr int kRPer = K / kThreads;  // 4 runs per thread
+constexpr uint32_t kSegWords = kRleSegRows / 32;
+
+__global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ RleDesc D;
   __shared__ uint32_t cnt_s[K / 2 + 8];  // staged packed counts when w <= 16 (else read through L1)
-  // aux: staged packed values (V_BP/V_DICT/V_F2I) | slopes (V_LINEAR)
+  // aux: staged packed values (V_BP/V_DICT/V_F2I); later the compact run values
   __shared__ __align__(16) uint8_t aux_s[K * 8 + 64];
-  __shared__ uint32_t rc_s[K];  // run counts
-  __shared__ uint64_t rv_s[K];  // run first values
+  // region: the V_DRLE window (Q, dv, S of scanned inner runs) while values are computed; then the
+  // compact run slopes and starts
+  __shared__ __align__(16) uint8_t region_s[kRleWindow * 20];
+  static_assert(K * 4 + K * 8 <= kRleWindow * 20, "compact run table must fit the region");
+  __shared__ __align__(16) uint32_t bm_s[kSegWords];  // run-start bitmap of one output segment
+  __shared__ uint64_t warp_s[2 * kThreads / 32];
   uint32_t* valbits_s = reinterpret_cast<uint32_t*>(aux_s);
-  uint64_t* slope_s = reinterpret_cast<uint64_t*>(aux_s);
-  // V_DRLE window (S_j, Q_j, dv_j of scanned inner runs) lives in the output image, unused until expansion
-  uint64_t* iQ_s = reinterpret_cast<uint64_t*>(outbuf);
+  uint64_t* cval_s = reinterpret_cast<uint64_t*>(aux_s);
+  uint64_t* iQ_s = reinterpret_cast<uint64_t*>(region_s);
   uint64_t* iDV_s = iQ_s + kRleWindow;
   uint32_t* iS_s = reinterpret_cast<uint32_t*>(iDV_s + kRleWindow);
-  static_assert(kRleWindow * 20 <= kRleOutBytes, "window must fit the output image");
-  __shared__ uint64_t warp_s[kThreads / 32];
-  __shared__ uint32_t skip_s;
-  const uint32_t tid = threadIdx.x;
+  uint64_t* cslope_s = reinterpret_cast<uint64_t*>(region_s);
+  uint32_t* cstart_s = reinterpret_cast<uint32_t*>(cslope_s + K);
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t gt = blockIdx.x;
   trace_stamp(B.trace, gt, 0);
   trace_stamp(B.trace, gt, 7);
   stage_desc(&D, &B.d[find_desc(B, gt)]);
+  for (uint32_t k = threadIdx.x; k < kSegWords / 4; k += kThreads) reinterpret_cast<uint4*>(bm_s)[k] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t lt = gt - D.tile0;
   const uint32_t g0 = lt * K;
@@ -358,14 +358,15 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
   const bool linear = vmode == V_LINEAR;
   const uint32_t ob = D.out_bytes;
   uint32_t errbits = 0;
-  // stage packed counts (and values) of this tile: chunk data only, so this overlaps the tail of rle_sums
-  // (programmatic dependent launch); everything rle_sums writes is read after griddepcontrol.wait
   const bool cnt_staged = D.cnt_w <= 16;
   if (cnt_staged) stage_bits(cnt_s, D.cnt_packed, g0, nr, D.cnt_w);
   if (vmode == V_BP || vmode == V_DICT || vmode == V_F2I) stage_bits(valbits_s, D.val_packed, g0, nr, D.val_w);
-  grid_dependency_wait();
-  const uint4 pf = D.prefix[lt];  // tile output offset from rle_sums
-  __syncthreads();
+  grid_dependency_wait();  // rle_scan complete: prefix / anchor are valid
+
+  // ---- 2a. output offset (and the wrapping dv*count prefix of a root Delta|RLE) of this tile
+  const uint4 pf = __ldcg(D.prefix + lt);
+  const uint64_t O64 = (uint64_t(pf.y) << 32) | pf.x, Pw = (uint64_t(pf.w) << 32) | pf.z;
+  __syncthreads();  // the staged counts / values are complete
   trace_stamp(B.trace, gt, 5);
 
   // phase A: this thread's 4 consecutive runs -- counts and values through the fused nested provider
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
   uint32_t cnt[kRPer];
   uint64_t val[kRPer];
   uint64_t sc = 0, sw = 0;
+  uint32_t ne = 0;
 #pragma unroll
   for (int r = 0; r < kRPer; r++) {
     const uint32_t k = kb + r;
@@ -402,12 +404,13 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
     cnt[r] = uint32_t(c);
     val[r] = v;
     sc += c;
+    ne += c != 0;
     if (linear) sw += v * c;
   }
   if (vmode == V_DRLE) {
-    // values of outer runs g = Q_j + (g - S_j + 1) dv_j, j the inner run holding g: the inner runs from the
+    // ---- values of outer runs g = Q_j + (g - S_j + 1) dv_j, j the inner run holding g: the inner runs from the
     // anchor tile on are scanned into a shared-memory window (pass after pass until every run is covered)
-    const uint4 rec = D.anchor[lt];  // same address in every thread: one broadcast load
+    const uint4 rec = __ldcg(D.anchor + lt);
     uint32_t ws = rec.x;
     uint64_t Sbase = rec.y, Qbase = (uint64_t(rec.w) << 32) | rec.z;
     uint32_t pending = 0;  // bit r: run r still needs its value
@@ -432,9 +435,8 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
         lc += dcv[q];
         lw += dvv[q] * dcv[q];
       }
-      uint64_t tcs, tws;
-      const uint64_t ec2 = block_excl_scan_u64<kThreads>(lc, warp_s, &tcs);
-      const uint64_t ew2 = block_excl_scan_u64<kThreads>(lw, warp_s, &tws);
+      uint64_t tcs, tws, ec2, ew2;
+      block_excl_scan_pair<kThreads>(lc, lw, warp_s, &ec2, &ew2, &tcs, &tws);
       {
         uint64_t c = Sbase + ec2, w = Qbase + ew2;
 #pragma unroll
@@ -476,99 +478,21 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
     }
   }
   trace_stamp(B.trace, gt, 1);
-  uint64_t T, W = 0;
-  const uint64_t ec = block_excl_scan_u64<kThreads>(sc, warp_s, &T);  // this thread's first row
-  uint64_t ew = 0;
-  if (linear) ew = block_excl_scan_u64<kThreads>(sw, warp_s, &W);
+  // ---- 3. block scan of (non-empty runs << 44 | rows): this thread's first row and first compact index
+  uint64_t T, W, ex, ew;
+  block_excl_scan_pair<kThreads>((uint64_t(ne) << 44) | sc, sw, warp_s, &ex, &ew, &T, &W);
+  const uint64_t ec = ex & ((1ull << 44) - 1), ce = ex >> 44;
+  const uint32_t nce = uint32_t(T >> 44);
+  T &= (1ull << 44) - 1;
   trace_stamp(B.trace, gt, 2);
-  const uint64_t O64 = pf.y;
-  const uint64_t Pw = (uint64_t(pf.w) << 32) | pf.z;
-  if (tid == 0) {
-    const bool overflow = O64 + T > D.n;
-    skip_s = overflow;
-    if (overflow || (lt + 1 == D.ntiles && O64 + T != D.n)) atomicOr(B.err + D.err_idx, 0x2u);
-  }
+  const bool overflow = O64 + T > D.n;
+  if (tid == 0 && (overflow || (lt + 1 == D.ntiles && O64 + T != D.n))) errbits |= 0x2u;
   if (errbits) atomicOr(B.err + D.err_idx, errbits);
-  // run table (the thread's own runs): first value and slope (arithmetic runs of a root Delta|RLE)
-  {
-    uint64_t wv = Pw + ew;
-#pragma unroll
-    for (int r = 0; r < kRPer; r++) {
-      uint64_t first = val[r];
-      if (linear) {
-        slope_s[kb + r] = val[r];
-        first = D.delta_base + wv + val[r];
-        wv += val[r] * cnt[r];
-      }
-      rc_s[kb + r] = cnt[r];
-      rv_s[kb + r] = first;
-    }
-  }
-  __syncthreads();
-  trace_stamp(B.trace, gt, 3);
-  if (skip_s) return;  // corrupt counts: never write outside [0, n)
-
+  if (overflow) return;  // corrupt counts: never write outside [0, n) (uniform across the CTA)
   const uint32_t O = uint32_t(O64);
   const uint32_t Tt = uint32_t(T);
-  const uint32_t my = uint32_t(sc);
-  if (Tt <= kRleBigLimit || !B.big_enabled) {
-    const uint32_t cap_rows = (kRleOutBytes - 16) / ob;
-    uint8_t* gout = reinterpret_cast<uint8_t*>(D.out);
-    for (uint32_t s0 = 0; s0 < Tt; s0 += cap_rows) {  // one segment for all but unusually long tiles
-      const uint32_t s1 = min(Tt, s0 + cap_rows);
-      const uint64_t gbyte = uint64_t(O + s0) * ob;
-      const uint32_t sh = uint32_t(gbyte & 15);
-      uint8_t* buf = outbuf + sh;
-      // rows of this thread's runs inside [s0, s1): a flat loop, one shared store per row
-      const uint32_t q0 = max(uint32_t(ec), s0), q1 = min(uint32_t(ec) + my, s1);
-      if (q0 < q1) {
-        uint32_t r = 0, row = uint32_t(ec);
-        while (row + rc_s[kb + r] <= q0) { row += rc_s[kb + r]; r++; }
-        uint32_t rem = row + rc_s[kb + r] - q0;
-        uint64_t v = rv_s[kb + r], sl = 0;
-        if (linear) {
-          sl = slope_s[kb + r];
-          v += uint64_t(q0 - row) * sl;
-        }
-        uint8_t* p = buf + uint64_t(q0 - s0) * ob;
-        uint8_t* const pe = buf + uint64_t(q1 - s0) * ob;
-        if (ob == 8) {
-          for (; p < pe; p += 8) {
-            while (rem == 0) { r++; rem = rc_s[kb + r]; v = rv_s[kb + r]; if (linear) sl = slope_s[kb + r]; }
-            *reinterpret_cast<uint64_t*>(p) = v;
-            v += sl;
-            rem--;
-          }
-        } else {
-          for (; p < pe; p += 4) {
-            while (rem == 0) { r++; rem = rc_s[kb + r]; v = rv_s[kb + r]; if (linear) sl = slope_s[kb + r]; }
-            *reinterpret_cast<uint32_t*>(p) = uint32_t(v);
-            v += sl;
-            rem--;
-          }
-        }
-      }
-      __syncthreads();
-      const uint32_t bytes = (s1 - s0) * ob;
-      const uint32_t h = min(bytes, (16u - sh) & 15u);  // unaligned head (a multiple of ob)
-      const uint32_t body = (bytes - h) & ~15u;
-      uint8_t* dst = gout + gbyte;
-      if (tid * ob < h) {
-        if (ob == 8) *reinterpret_cast<uint64_t*>(dst + tid * 8) = *reinterpret_cast<const uint64_t*>(buf + tid * 8);
-        else *reinterpret_cast<uint32_t*>(dst + tid * 4) = *reinterpret_cast<const uint32_t*>(buf + tid * 4);
-      }
-      for (uint32_t o = h + tid * 16; o < h + body; o += kThreads * 16) {
-        const uint4 x = *reinterpret_cast<const uint4*>(buf + o);
-        st_v4_u32(dst + o, x.x, x.y, x.z, x.w);
-      }
-      const uint32_t t0 = h + body + tid * ob;
-      if (t0 < bytes) {
-        if (ob == 8) *reinterpret_cast<uint64_t*>(dst + t0) = *reinterpret_cast<const uint64_t*>(buf + t0);
-        else *reinterpret_cast<uint32_t*>(dst + t0) = *reinterpret_cast<const uint32_t*>(buf + t0);
-      }
-      if (s1 < Tt) __syncthreads();
-    }
-  } else {
+
+  if (Tt > kRleBigLimit && B.big_enabled) {  // giant runs: hand the tile's run table to rle_big
     __shared__ uint32_t slot_s;
     if (tid == 0) {
       const uint64_t pieces = (Tt + kRleBigPiece - 1) / kRleBigPiece;
@@ -591,25 +515,93 @@ __global__ void __launch_bounds__(kThreads, 3) rle_kernel(const __grid_constant_
     }
     __syncthreads();
     const uint32_t e = slot_s;
-    if (e < B.big.max_slots) {  // the tile's run table for rle_big, from this thread's runs
+    if (e < B.big.max_slots) {
       uint32_t* so = B.big.soffs + uint64_t(e) * (K + 1);
       uint64_t* va = B.big.vals + uint64_t(e) * K;
       uint64_t* sl = B.big.slopes + uint64_t(e) * K;
       uint32_t row = uint32_t(ec);
+      uint64_t wv = Pw + ew;
 #pragma unroll
       for (int r = 0; r < kRPer; r++) {
         const uint32_t k = kb + r;
         if (k < nr) {
           so[k] = row;
-          va[k] = rv_s[k];
-          sl[k] = linear ? slope_s[k] : 0ull;
+          va[k] = linear ? D.delta_base + wv + val[r] : val[r];
+          sl[k] = linear ? val[r] : 0ull;
         }
+        if (linear) wv += val[r] * cnt[r];
         row += cnt[r];
       }
       if (tid == 0) so[nr] = Tt;
     }
+    trace_stamp(B.trace, gt, 4);
+    return;
   }
-  __syncthreads();
+
+  // compact run table: first row, first value, slope of every non-empty run
+  __syncthreads();  // the V_DRLE window / staged values are dead from here on
+  {
+    uint32_t row = uint32_t(ec), c = uint32_t(ce);
+    uint64_t wv = Pw + ew;
+#pragma unroll
+    for (int r = 0; r < kRPer; r++) {
+      if (cnt[r]) {
+        cstart_s[c] = row;
+        cval_s[c] = linear ? D.delta_base + wv + val[r] : val[r];
+        if (linear) cslope_s[c] = val[r];
+        c++;
+      }
+      if (linear) wv += val[r] * cnt[r];
+      row += cnt[r];
+    }
+  }
+  trace_stamp(B.trace, gt, 3);
+  uint8_t* gout = reinterpret_cast<uint8_t*>(D.out) + uint64_t(O) * ob;
+  for (uint32_t s0 = 0; s0 < Tt; s0 += kRleSegRows) {  // one segment unless the tile holds > 32 K rows
+    const uint32_t rows = min(Tt - s0, kRleSegRows);
+    const uint32_t nw = (rows + 31) / 32;
+    if (s0) {  // later segments: clear the previous segment's bits
+      __syncthreads();
+      for (uint32_t k = tid; k < kSegWords; k += kThreads) bm_s[k] = 0u;
+      __syncthreads();
+    }
+    {
+      uint32_t row = uint32_t(ec);
+#pragma unroll
+      for (int r = 0; r < kRPer; r++) {
+        const uint32_t p = row - s0;
+        if (cnt[r] && row >= s0 && p < rows) atomicOr(bm_s + (p >> 5), 1u << (p & 31));
+        row += cnt[r];
+      }
+    }
+    __syncthreads();  // bitmap + compact run table complete
+    // warp w: windows [k0, k1); cb = compact runs starting before row s0 + 32 k0
+    const uint32_t per = (nw + kThreads / 32 - 1) / (kThreads / 32);
+    const uint32_t k0 = min(nw, warp * per), k1 = min(nw, k0 + per);
+    if (k0 < k1) {
+      const uint32_t first = s0 + 32 * k0;
+      uint32_t lo = 0, hi = nce;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cstart_s[mid] < first) lo = mid + 1; else hi = mid;
+      }
+      uint32_t cb = lo;
+      const uint32_t lmask = FULL >> (31 - lane);
+      uint8_t* gseg = gout + uint64_t(s0) * ob;
+      for (uint32_t k = k0; k < k1; k++) {
+        const uint32_t word = bm_s[k];
+        const uint32_t p = k * 32 + lane;
+        const uint32_t c = cb + __popc(word & lmask) - 1;
+        cb += __popc(word);
+        uint64_t v = cval_s[c];
+        if (linear) v += uint64_t(s0 + p - cstart_s[c]) * cslope_s[c];
+        if (p < rows) {
+          if (ob == 8) reinterpret_cast<uint64_t*>(gseg)[p] = v;
+          else reinterpret_cast<uint32_t*>(gseg)[p] = uint32_t(v);
+        }
+      }
+    }
+  }
   trace_stamp(B.trace, gt, 4);
 }
 
@@ -647,6 +639,11 @@ __global__ void __launch_bounds__(kThreads) rle_big_kernel(const __grid_constant
   }
 }
 
+bool pdl_enabled() {
+  static const bool pdl = !(std::getenv("CDM_PDL") && std::getenv("CDM_PDL")[0] == '0');
+  return pdl;
+}
+
 }  // namespace
 
 cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s) {
@@ -655,19 +652,29 @@ cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_rle_scan(const SumsBatch& b, cudaStream_t s) {
+  if (!b.n) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(b.n);
+  cfg.blockDim = dim3(kScanThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rle_scan_kernel, b);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(rle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRleOutBytes + 16);
-    configured = true;
-  }
-  // programmatic dependent launch: rle_kernel's prologue overlaps rle_sums (CDM_PDL=0 disables)
-  static const bool pdl = !(std::getenv("CDM_PDL") && std::getenv("CDM_PDL")[0] == '0');
+  // programmatic dependent launch: rle_kernel's prologue overlaps rle_scan (CDM_PDL=0 disables)
+  const bool pdl = pdl_enabled();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(b.total_tiles);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kRleOutBytes + 16;
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -538,7 +538,6 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.inner_units = uint32_t(div_up(d.inner_tiles, 8));
       d.unit0 = units;
       d.err_idx = uint32_t(j);
-      d.done = A.take<uint32_t>(1);
       units += d.outer_units + d.inner_units;
     }
     sb.total_units = units;
@@ -578,7 +577,6 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       if (uint64_t(kRleTile) * b.max_run > kRleBigLimit) rb.big_enabled = 1;
     }
     rb.total_tiles = tiles;
-    if (const char* dbg = std::getenv("CDM_DEBUG_RLE")) rb.debug = uint32_t(std::atoi(dbg));
     rb.big.counter = A.take<unsigned long long>(1);
     rb.big.done = A.take<uint32_t>(1);
     rb.big.max_slots = slots;
@@ -592,7 +590,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
   // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
-  // per RLE chunk: tile sums and the scans the last CTA of rle_sums writes
+  // per RLE chunk: the tile sums rle_sums writes and rle_kernel reduces
   std::map<int, const SumsChunk*> sums_of;
   for (auto& pb : B->sums)
     for (uint32_t k = 0; k < pb.n; k++) {
@@ -715,8 +713,13 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, fs)); n++; B->fam_launches[F_SCAN]++; }
         break;
       case F_RLE:
-        for (auto& pb : B->sums) { CUDA_TRY(launch_rle_sums(pb, fs)); n++; B->fam_launches[F_RLE]++; }
-        for (auto& rb : B->rle) {
+        // per group of <= kMaxBatch chunks: sums -> scan -> expand (the last two programmatically dependent)
+        for (size_t gi = 0; gi < B->rle.size(); gi++) {
+          auto& rb = B->rle[gi];
+          CUDA_TRY(launch_rle_sums(B->sums[gi], fs));
+          CUDA_TRY(launch_rle_scan(B->sums[gi], fs));
+          n += 2;
+          B->fam_launches[F_RLE] += 2;
           CUDA_TRY(launch_rle(rb, fs));
           n++;
           B->fam_launches[F_RLE]++;
@@ -1495,9 +1498,10 @@ static void dump_trace(cdm_batch* b, const char* path) {
     if (cudaMemcpy(h.data(), dev, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
     for (uint32_t t = 0; t < tiles; t++) {
       const uint64_t* r = &h[size_t(t) * 8];
-      std::fprintf(f, "%s,%d,%u,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", name, li, t, (unsigned long long)r[0],
+      std::fprintf(f, "%s,%d,%u,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", name, li, t, (unsigned long long)r[0],
                    (unsigned long long)r[1], (unsigned long long)r[2], (unsigned long long)r[3],
-                   (unsigned long long)r[4], (unsigned long long)r[7], (unsigned long long)r[5]);
+                   (unsigned long long)r[4], (unsigned long long)r[7], (unsigned long long)r[5],
+                   (unsigned long long)r[6]);
     }
   };
   for (size_t i = 0; i < b->scan.size(); i++) dump("scan", int(i), b->scan[i].trace, b->scan[i].total_tiles);

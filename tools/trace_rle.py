@@ -47,6 +47,11 @@ for key, recs in by.items():
         st[:, 0].min(), np.median(st[:, 0]), st[:, 0].max(), np.median(st[:, 4]), st[:, 4].max()))
     t5 = (a[:, 7] - t0) / 1e3
     print("   stamp5 (descriptor/window) - start: median %.2fus" % np.median(t5 - st[:, 0]))
+    if a.shape[1] > 8:
+        t6 = (a[:, 8] - t0) / 1e3
+        ok = a[:, 8] > 0
+        if ok.any():
+            print("   stamp6 - start: median %.2fus" % np.median((t6 - st[:, 0])[ok]))
     lb = st[:, 3] - st[:, 2]
     for q in (0, 10, 50, 90, 99, 100):
         print(f"   lookback p{q}: {np.percentile(lb, q):.2f}us", end="")
