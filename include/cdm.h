@@ -155,11 +155,17 @@ CDM_API cdm_status cdm_johnson_order(const double *t, const double *d, size_t n,
  * create: parses/validates headers on the host and sizes scratch (no device work is enqueued);
  * launch: enqueues the fused decode of every job on `stream` (cudaStream_t, NULL = engine decode
  *         stream); capturable into a CUDA graph; returns the number of kernel launches in *n_launches;
- * results: synchronises `stream` and reads the per-chunk device error words. */
+ * results: synchronises `stream` and reads the per-chunk device error words, then clears them: error
+ *          bits accumulate (OR) over all launches since the previous cdm_batch_results. */
 CDM_API cdm_status cdm_batch_create(cdm_engine *e, const cdm_job *jobs, size_t n, cdm_batch **out);
 CDM_API cdm_status cdm_batch_launch(cdm_batch *b, void *stream, uint32_t *n_launches);
 CDM_API cdm_status cdm_batch_results(cdm_batch *b, void *stream, cdm_result *results);
 CDM_API cdm_status cdm_batch_destroy(cdm_batch *b);
+/* Graph mode (enable != 0): the first cdm_batch_launch on a stream captures the whole enqueue into a CUDA
+ * graph, later launches on that stream replay it with one cudaGraphLaunch (re-captured when the stream or
+ * the timing setting changes; the jobs' buffers must stay where they were).  Removes the host launch
+ * overhead of the ~10 kernel launches + fork/join events per decode. */
+CDM_API cdm_status cdm_batch_set_graph(cdm_batch *b, int enable);
 
 /* ---- pipelines: a fixed job set from PINNED host memory, captured once into a CUDA graph ----
  * The H4 schedule of cdm_submit_batch (Johnson order, groups, H2D copies overlapped with the fused
@@ -184,6 +190,9 @@ CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
  * 4 raw copies. */
 CDM_API cdm_status cdm_batch_set_timing(cdm_batch *b, int enable);
 CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch *b, double *ms5, uint64_t *launches5);
+/* Graph mode + timing: every replay re-records the same events, so call this after each launch (it
+ * waits for that replay) to accumulate its per-family times; a replay not collected is not counted. */
+CDM_API cdm_status cdm_batch_collect_timing(cdm_batch *b);
 
 #ifdef __cplusplus
 }

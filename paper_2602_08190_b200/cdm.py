@@ -23,6 +23,7 @@ SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_creat
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
            "cdm_submit_batch", "cdm_wait", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
+           "cdm_batch_set_graph", "cdm_batch_collect_timing",
            "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy"]
 
 
@@ -87,6 +88,8 @@ def lib():
         "cdm_batch_destroy": [vp],
         "cdm_batch_set_timing": [vp, st],
         "cdm_batch_kernel_ms": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)],
+        "cdm_batch_set_graph": [vp, st],
+        "cdm_batch_collect_timing": [vp],
         "cdm_pipeline_create": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(vp)],
         "cdm_pipeline_launch": [vp, vp],
         "cdm_pipeline_results": [vp, ctypes.POINTER(Result)],
@@ -266,6 +269,12 @@ class Batch:
 
     def set_timing(self, on: bool) -> None:
         _check(lib().cdm_batch_set_timing(self.h, 1 if on else 0))
+
+    def set_graph(self, on: bool) -> None:
+        _check(lib().cdm_batch_set_graph(self.h, 1 if on else 0))
+
+    def collect_timing(self) -> None:
+        _check(lib().cdm_batch_collect_timing(self.h))
 
     def kernel_ms(self) -> dict:
         ms = (ctypes.c_double * 5)()

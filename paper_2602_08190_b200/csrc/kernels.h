@@ -14,7 +14,6 @@ constexpr int kMaxBatch = 32;      // descriptors per launch (more chunks -> mor
 constexpr int kFpTile = 4096;      // H5 values per tile = 256 threads x 16
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
 constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
-constexpr int kRleWindow = 1024;   // V_DRLE inner runs scanned into shared memory per pass
 constexpr uint32_t kRleSegRows = 32768;  // rle_kernel: output rows per run-start bitmap segment
 constexpr uint32_t kRleBigLimit = 1u << 15;  // a tile with more output rows is expanded by rle_big
 constexpr uint32_t kRleBigPiece = 8192;       // rows per rle_big work item
@@ -79,21 +78,19 @@ enum RleValueMode : uint8_t {
   V_BP = 0,      // values = FOR + bits
   V_DICT = 1,    // values = dict[FOR + bits]
   V_F2I = 2,     // values = (double)(FOR + bits) / 10^d
-  V_DRLE = 3,    // values = Delta|RLE|[BitPack,BitPack] closed form from the inner pre-pass
-  V_LINEAR = 4   // root Delta|RLE|[BitPack,BitPack]: run j is an arithmetic run (start, slope dv_j)
+  V_DRLE = 3,    // (host plan only) values = Delta|RLE|[BitPack,BitPack]: decoded by a level-0 V_LINEAR
+                 // job into an L2-resident run-value array, then expanded as V_RAW
+  V_LINEAR = 4,  // root Delta|RLE|[BitPack,BitPack]: run j is an arithmetic run (start, slope dv_j)
+  V_RAW = 5      // values = a plain u64 array (the level-0 output)
 };
 
 struct RleDesc {
   const uint8_t* cnt_packed;
-  const uint8_t* val_packed;  // V_BP/V_DICT/V_F2I: packed values or indices; V_LINEAR: packed dv
+  const uint8_t* val_packed;  // V_BP/V_DICT/V_F2I: packed values or indices; V_LINEAR: packed dv;
+                              // V_RAW: u64 run values (32-byte aligned)
   const uint8_t* dict;
   void* out;
-  const uint8_t* idv_packed;  // V_DRLE inner dv / dc
-  const uint8_t* idc_packed;
-  const uint4* prefix;        // [ntiles] exclusive prefix {count lo, count hi, w lo, w hi} (rle_scan)
-  const uint4* anchor;        // V_DRLE [ntiles] {j0, S_j0, Q lo, Q hi}: window start (rle_scan)
-  uint64_t idv_base;
-  uint64_t idc_base;
+  const uint64_t* tsum;       // [ntiles][2] per tile {sum of counts, sum of dv*count} (rle_sums)
   uint64_t cnt_base;
   uint64_t val_base;
   uint64_t delta_base;        // V_LINEAR: Delta base
@@ -102,12 +99,9 @@ struct RleDesc {
   uint32_t tile0;
   uint32_t ntiles;
   uint32_t entries;
-  uint32_t n_inner;
   uint32_t err_idx;
   uint16_t cnt_w;
   uint16_t val_w;
-  uint16_t idv_w;
-  uint16_t idc_w;
   uint8_t vmode;
   uint8_t out_bytes;          // 4 or 8
   uint8_t d;
@@ -143,32 +137,22 @@ struct RleBatch {
   RleDesc d[kMaxBatch];
 };
 
-// rle_sums: per-tile sums of the RLE family, fully parallel (no look-back, no scan): one warp per tile.
-//   outer tiles (kRleTile runs): tsum[t] = {sum of counts, sum of dv*count (root Delta|RLE)}
-//   inner tiles (kInnerTile inner runs of a Delta|RLE value lineage): isum[i] = {sum dc, sum dv*dc}
-// rle_scan (one 1024-thread CTA per chunk, programmatic dependent launch) scans them:
-//   prefix[t] = {sum of counts before t, sum of dv*count before t}
-//   anchor[t] = {j0, S, Q} for the inner tile holding outer run t*kRleTile: its first inner run j0, the
-//     outer run S where j0 starts and Q = base + sum of dv*dc before j0 ({n_inner, 0, 0} if none: corrupt).
-constexpr int kInnerTile = 256;           // inner runs per inner tile sum
-
+// rle_sums: per-tile sums of the RLE family, fully parallel (no look-back, no scan): one warp per 1024-run
+// tile, tsum[t] = {sum of counts, sum of dv*count (root Delta|RLE)}.  Each rle_kernel CTA reduces the sums
+// of the tiles before its own (a few KB from L2) into its output offset.
 struct SumsChunk {
-  const uint8_t* cnt_packed;   // outer counts
-  const uint8_t* dv_packed;    // V_LINEAR: outer dv (slopes); V_DRLE: inner dv
-  const uint8_t* dc_packed;    // V_DRLE: inner dc
-  uint64_t cnt_base, dv_base, dc_base;
-  uint64_t* tsum;              // [outer_tiles][2] count, w
-  uint64_t* isum;              // [inner_tiles][2] dc, dv*dc
-  uint4* prefix;               // [outer_tiles]
-  uint4* anchor;               // [outer_tiles] (V_DRLE)
-  uint64_t base;               // V_DRLE: Delta base of the value lineage
-  uint32_t nruns, rows, n_inner;
-  uint32_t outer_tiles, inner_tiles;
-  uint32_t unit0;              // first global unit of this chunk
-  uint32_t outer_units, inner_units;
+  const uint8_t* cnt_packed;   // counts
+  const uint8_t* dv_packed;    // V_LINEAR: dv (slopes)
+  uint64_t cnt_base, dv_base;
+  uint64_t* tsum;              // [tiles][2] count, w
+  uint32_t nruns, rows;
+  uint32_t tiles;
+  uint32_t unit0;              // first global unit (rle_sums CTA) of this chunk
+  uint32_t units;
   uint32_t err_idx;
-  uint16_t cnt_w, dv_w, dc_w;
-  uint8_t linear, drle;
+  uint16_t cnt_w, dv_w;
+  uint8_t linear;
+  uint8_t pad[3];
 };
 
 struct SumsBatch {
@@ -203,7 +187,6 @@ struct Lz4Batch {
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
 cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
-cudaError_t launch_rle_scan(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);

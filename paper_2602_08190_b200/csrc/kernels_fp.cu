@@ -9,6 +9,8 @@
 // (cp.async.bulk + mbarrier), double-buffered so tile k+1 streams in while tile k is unpacked; each
 // thread unpacks 4 consecutive values per group with funnel shifts and writes them with one 16-byte
 // store (int32 / f32) or two (int64 / f64), so a warp writes 512 or 1024 contiguous bytes per group.
+#include <cstdlib>
+
 #include "device_util.cuh"
 #include "kernels.h"
 
@@ -37,9 +39,16 @@ __device__ __forceinline__ uint32_t stage_bytes(const FpDesc& D, uint32_t lt) {
   return uint32_t(want < have ? want : have);
 }
 
-__global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ FpBatch B, uint32_t stage_bytes_alloc) {
+constexpr uint32_t kDictSmemBytes = 8192;  // dictionaries up to this size are gathered from shared memory
+
+// DM: dictionary gathers from shared memory (1: the tile's dictionary is copied there when the tile's
+// chunk changes) or through the read-only L1 path (0).
+template <int DM>
+__global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__ FpBatch B, uint32_t stage_bytes_alloc) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(16) uint64_t dict_s[DM == 1 ? kDictSmemBytes / 8 : 2];
+  int staged_di = -1;
   const uint32_t tid = threadIdx.x;
   // stage_bytes_alloc: set by the host from the batch's largest w; dynamic smem = 2 stages
 
@@ -75,56 +84,100 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
     }
     const int di = find_desc_fp(B, tile);
     const FpDesc& D = B.d[di];
+    // descriptor fields in registers (param-space reads with a dynamic index cost a load per use)
     const uint32_t lt = tile - D.tile0;
+    const uint32_t w = D.w, mode = D.mode, ob = D.out_bytes, entries = D.entries;
+    const uint64_t base = D.base;
+    const uint8_t* const dict8 = D.dict;
+    uint8_t* const out8 = reinterpret_cast<uint8_t*>(D.out);
     mbar_wait(&bar[s], (it >> 1) & 1);
     const uint32_t* wd = reinterpret_cast<const uint32_t*>(smem + s * stage_bytes_alloc);
-    const uint32_t w = D.w;
     const uint64_t tile_start = uint64_t(lt) * kFpTile;
     const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
     bool bad_index = false;
-    const bool bytes_path = D.mode == FP_DICT && D.out_bytes != 4 && D.out_bytes != 8;  // CHAR(n) rows
+    const bool bytes_path = mode == FP_DICT && ob != 4 && ob != 8;  // CHAR(n) rows
+    const bool dsm = DM == 1 && mode == FP_DICT && !bytes_path && entries * ob <= kDictSmemBytes;
+    if (dsm && di != staged_di) {  // uniform: every thread passed the barrier ending the previous tile
+      const uint4* src = reinterpret_cast<const uint4*>(dict8);
+      for (uint32_t q = tid; q < (entries * ob + 15) / 16; q += kThreads) reinterpret_cast<uint4*>(dict_s)[q] = __ldg(src + q);
+      __syncthreads();
+      staged_di = di;
+    }
+    // width class: the 4 consecutive fields of a thread lie in one 32-bit window (w <= 8) or one 64-bit
+    // window (w <= 16); wider fields are extracted one by one
+    const uint32_t cls = w <= 8 ? 0u : w <= 16 ? 1u : w <= 32 ? 2u : 3u;
+    const uint32_t m32 = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
 
 #pragma unroll 1
     for (uint32_t k = 0; k < 4 && !bytes_path; k++) {
       const uint32_t i0 = k * 1024 + tid * 4;  // 4 consecutive values
       if (i0 >= valid) break;
       uint64_t v[4];
+      const uint32_t b0 = i0 * w, wi = b0 >> 5, sh = b0 & 31;
+      if (cls == 0) {
+        const uint32_t x = __funnelshift_r(wd[wi], wd[wi + 1], sh);
 #pragma unroll
-      for (int j = 0; j < 4; j++) v[j] = D.base + (w ? extract_bits(wd, uint64_t(i0 + j) * w, w) : 0ull);
+        for (int j = 0; j < 4; j++) v[j] = base + ((x >> (j * w)) & m32);
+      } else if (cls == 1) {
+        const uint32_t a0 = wd[wi], a1 = wd[wi + 1], a2 = wd[wi + 2];
+        const uint64_t x = (uint64_t(__funnelshift_r(a1, a2, sh)) << 32) | __funnelshift_r(a0, a1, sh);
+#pragma unroll
+        for (int j = 0; j < 4; j++) v[j] = base + (uint32_t(x >> (j * w)) & m32);
+      } else if (cls == 2) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t bj = b0 + j * w;
+          v[j] = base + (__funnelshift_r(wd[bj >> 5], wd[(bj >> 5) + 1], bj & 31) & m32);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; j++) v[j] = base + extract_bits(wd, uint64_t(i0 + j) * w, w);
+      }
       const uint64_t gi = tile_start + i0;
       const bool full = i0 + 4 <= valid;
-      if (D.mode == FP_INT) {
-        if (D.out_bytes == 4) {
-          uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
+      if (mode == FP_INT) {
+        if (ob == 4) {
+          uint32_t* o = reinterpret_cast<uint32_t*>(out8) + gi;
           if (full) st_v4_u32(o, uint32_t(v[0]), uint32_t(v[1]), uint32_t(v[2]), uint32_t(v[3]));
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint32_t(v[j]);
-        } else if (D.out_bytes == 8) {
-          uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+        } else if (ob == 8) {
+          uint64_t* o = reinterpret_cast<uint64_t*>(out8) + gi;
           if (full) { st_v2_u64(o, v[0], v[1]); st_v2_u64(o + 2, v[2], v[3]); }
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = v[j];
-        } else if (D.out_bytes == 2) {
-          uint16_t* o = reinterpret_cast<uint16_t*>(D.out) + gi;
+        } else if (ob == 2) {
+          uint16_t* o = reinterpret_cast<uint16_t*>(out8) + gi;
           _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint16_t(v[j]);
         } else {
-          uint8_t* o = reinterpret_cast<uint8_t*>(D.out) + gi;
+          uint8_t* o = out8 + gi;
           if (full) *reinterpret_cast<uint32_t*>(o) = (v[0] & 0xFF) | ((v[1] & 0xFF) << 8) | ((v[2] & 0xFF) << 16) | ((v[3] & 0xFF) << 24);
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint8_t(v[j]);
         }
-      } else if (D.mode == FP_DICT) {
+      } else if (mode == FP_DICT) {
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-          if (v[j] >= D.entries) { bad_index = true; v[j] = 0; }
+          if (v[j] >= entries) { bad_index = true; v[j] = 0; }
         }
-        if (D.out_bytes == 8) {
-          const uint64_t* dict = reinterpret_cast<const uint64_t*>(D.dict);
-          uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+        if (dsm && ob == 8) {
+          uint64_t* o = reinterpret_cast<uint64_t*>(out8) + gi;
+          if (full) {
+            st_v2_u64(o, dict_s[v[0]], dict_s[v[1]]);
+            st_v2_u64(o + 2, dict_s[v[2]], dict_s[v[3]]);
+          } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = dict_s[v[j]];
+        } else if (dsm) {
+          const uint32_t* d32 = reinterpret_cast<const uint32_t*>(dict_s);
+          uint32_t* o = reinterpret_cast<uint32_t*>(out8) + gi;
+          if (full) st_v4_u32(o, d32[v[0]], d32[v[1]], d32[v[2]], d32[v[3]]);
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = d32[v[j]];
+        } else if (ob == 8) {
+          const uint64_t* dict = reinterpret_cast<const uint64_t*>(dict8);
+          uint64_t* o = reinterpret_cast<uint64_t*>(out8) + gi;
           if (full) {
             st_v2_u64(o, __ldg(dict + v[0]), __ldg(dict + v[1]));
             st_v2_u64(o + 2, __ldg(dict + v[2]), __ldg(dict + v[3]));
           } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
-        } else if (D.out_bytes == 4) {
-          const uint32_t* dict = reinterpret_cast<const uint32_t*>(D.dict);
-          uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
+        } else if (ob == 4) {
+          const uint32_t* dict = reinterpret_cast<const uint32_t*>(dict8);
+          uint32_t* o = reinterpret_cast<uint32_t*>(out8) + gi;
           if (full) st_v4_u32(o, __ldg(dict + v[0]), __ldg(dict + v[1]), __ldg(dict + v[2]), __ldg(dict + v[3]));
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
         }
@@ -133,7 +186,7 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
         double f[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) f[j] = double(int64_t(v[j])) / p;
-        uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+        uint64_t* o = reinterpret_cast<uint64_t*>(out8) + gi;
         if (full) {
           st_v2_u64(o, __double_as_longlong(f[0]), __double_as_longlong(f[1]));
           st_v2_u64(o + 2, __double_as_longlong(f[2]), __double_as_longlong(f[3]));
@@ -144,16 +197,16 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
       // FP_DICT with E-byte rows (E not 4/8): the tile's output (valid*E bytes, 16-aligned since 4096*E is a
       // multiple of 16) is produced as 16-byte chunks; each thread walks the bytes of its chunk tracking
       // (row, column) and extracts a row's index only when the row changes.
-      const uint32_t E = D.out_bytes;
+      const uint32_t E = ob;
       const uint64_t inv = (0x100000000ull + E - 1) / E;  // ceil(2^32 / E): exact for positions < 2^17
       const uint32_t total = valid * E;
-      uint8_t* obase = reinterpret_cast<uint8_t*>(D.out) + tile_start * E;
-      const uint8_t* __restrict__ dict = D.dict;
+      uint8_t* obase = out8 + tile_start * E;
+      const uint8_t* __restrict__ dict = dict8;
       for (uint32_t c = tid; c * 16 < total; c += kThreads) {
         const uint32_t p0 = c * 16;
         uint32_t row = uint32_t((uint64_t(p0) * inv) >> 32), col = p0 - row * E;
-        uint64_t idx = D.base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
-        if (idx >= D.entries) { bad_index = true; idx = 0; }
+        uint64_t idx = base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
+        if (idx >= entries) { bad_index = true; idx = 0; }
         uint32_t word[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (uint32_t b = 0; b < 16; b++) {
@@ -163,8 +216,8 @@ __global__ void __launch_bounds__(kThreads) fp_kernel(const __grid_constant__ Fp
               col = 0;
               row++;
               if (row < valid) {
-                idx = D.base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
-                if (idx >= D.entries) { bad_index = true; idx = 0; }
+                idx = base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
+                if (idx >= entries) { bad_index = true; idx = 0; }
               }
             }
           }
@@ -200,17 +253,22 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
   const uint32_t stage = ((kFpTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words for extraction
   const uint32_t smem = 2 * stage;
-  static uint32_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
+  static const int dm = std::getenv("CDM_FP_DICT") && std::getenv("CDM_FP_DICT")[0] == 'l' ? 0 : 1;
+  auto kern = dm ? fp_kernel<1> : fp_kernel<0>;
+  static uint32_t configured[2] = {0, 0};
+  if (smem > 40 * 1024 && smem > configured[dm]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured[dm] = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp_kernel, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   uint32_t grid = uint32_t(device_sms() * per_sm);
-  if (grid > b.total_tiles) grid = b.total_tiles;
-  fp_kernel<<<grid, kThreads, smem, s>>>(b, stage);
+  // CDM_FP_GRID=tiles: one CTA per tile (no persistence), so CTAs of a concurrent higher-priority family
+  // are scheduled as soon as any FP CTA retires
+  static const bool per_tile = std::getenv("CDM_FP_GRID") && std::getenv("CDM_FP_GRID")[0] == 't';
+  if (per_tile || grid > b.total_tiles) grid = b.total_tiles;
+  kern<<<grid, kThreads, smem, s>>>(b, stage);
   return cudaGetLastError();
 }
 

@@ -5,16 +5,17 @@
 // The paper runs PyTorch cumsum on the counts, then a Group-Parallel kernel whose <L,S,C> geometry lets
 // several blocks co-process one big group or one block walk several small groups.  The
 // B200 design splits the family into:
-//  * rle_sums_kernel: NO look-back, no scan.  Every warp sums one tile fully in parallel: an outer tile of
-//    1024 runs (sum of counts, plus sum dv*count for arithmetic runs) or an inner tile of 256 Delta|RLE
-//    inner runs (l_orderkey's value lineage: sum dc, sum dv*dc).
-//  * rle_kernel: one CTA per outer tile, no inter-tile dependency: it stages the tile's packed counts and
-//    values in shared memory (overlapping rle_sums through programmatic dependent launch), reduces the tile
-//    sums before it into its output offset, computes the run values through the fused nested provider
-//    (BitPack, Dict|BitPack, Float2Int|BitPack, the Delta|RLE closed form value(g) = Q_j + (g - S_j + 1) dv_j
-//    with S_j, Q_j block-scanned from the inner tile holding the tile's first run, or arithmetic runs for a
-//    root Delta|RLE), scans the counts in the CTA and expands the runs through a run-start bitmap: lane l of
-//    a warp owns row 32k + l, finds its run with one popc and stores it (coalesced 32-row stores).
+//  * rle_sums_kernel: NO look-back, no scan.  Every warp sums one 1024-run tile fully in parallel (sum of
+//    counts, plus sum dv*count for arithmetic runs).
+//  * rle_kernel: one CTA per tile, no inter-tile dependency: it stages the tile's packed counts and values
+//    in shared memory (overlapping rle_sums through programmatic dependent launch), reduces the tile sums
+//    before its own into its output offset (no scan kernel, no look-back), computes the run
+//    values through the fused nested provider (BitPack, Dict|BitPack, Float2Int|BitPack, arithmetic runs for
+//    a root Delta|RLE), scans the counts in the CTA and expands the runs through a run-start bitmap: lane l
+//    of a warp owns row 32k + l, finds its run with one popc and stores it (coalesced 32-row stores).
+//    A Delta|RLE value lineage (l_orderkey's RLE|[Delta|RLE|[BP,BP],BP]) is two levels of the same kernel:
+//    level 0 expands the inner arithmetic runs into the outer run values (an L2-resident u64 array, 1/4 of
+//    the output rows for l_orderkey), level 1 expands the outer runs reading them (V_RAW).
 //  * rle_big_kernel: tiles with more than kRleBigLimit output rows (giant runs: o_shippriority is one run
 //    per chunk) are split into 8192-row pieces over every SM ("multiple GPU blocks
 //    co-process a single group"); launched only when a chunk header's max run allows it.
@@ -210,8 +211,21 @@ __device__ __forceinline__ void warp_range_sums(const uint32_t* ap, uint64_t aba
   *sba = warp_sum(s2);
 }
 
-__global__ void __launch_bounds__(kThreads) rle_sums_kernel(const __grid_constant__ SumsBatch B) {
+// Cooperative copy of `nw` 32-bit words starting at word index w0 of `src` into shared memory (16-byte
+// vector loads: w0 is a multiple of 4 and the stream base is 16-byte aligned).
+__device__ __forceinline__ void stage_words(uint32_t* dst, const uint8_t* src, uint64_t w0, uint32_t nw) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src) + (w0 >> 2);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (uint32_t k = threadIdx.x; k < (nw + 3) / 4; k += kThreads) d4[k] = __ldg(s4 + k);
+}
+
+constexpr uint32_t kSumsRuns = 8 * K;                    // runs per rle_sums CTA (8 warps x one tile)
+constexpr uint32_t kSumsWords = kSumsRuns * 16 / 32 + 8;  // staged words per stream for w <= 16
+
+__global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_constant__ SumsBatch B) {
   __shared__ SumsChunk D;
+  __shared__ __align__(16) uint32_t cw_s[kSumsWords];  // the CTA's packed counts (w <= 16)
+  __shared__ __align__(16) uint32_t vw_s[kSumsWords];  // ... and packed slopes (root Delta|RLE, w <= 16)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t unit = blockIdx.x;
   {
@@ -225,149 +239,142 @@ __global__ void __launch_bounds__(kThreads) rle_sums_kernel(const __grid_constan
   __syncthreads();
   trace_stamp(B.trace, unit, 0);
   trace_stamp(B.trace, unit, 7);
-  grid_launch_dependents();  // rle_kernel may start staging its chunk data now
-  const uint32_t local = unit - D.unit0;
+  grid_launch_dependents();  // rle_kernel may start staging now
+  const uint32_t t0 = (unit - D.unit0) * 8;
+  const uint64_t r0 = uint64_t(t0) * K, r1 = min(r0 + kSumsRuns, uint64_t(D.nruns));
+  const uint32_t t = t0 + warp;  // warp w: tile t0 + w
   bool bad = false;
-  if (local < D.outer_units) {  // warp w: outer tile local*8 + w
-    const uint32_t t = local * 8 + warp;
-    if (t < D.outer_tiles) {
-      const uint64_t i0 = uint64_t(t) * kRleTile, i1 = min(i0 + kRleTile, uint64_t(D.nruns));
-      uint64_t sc, sw;
-      warp_range_sums(reinterpret_cast<const uint32_t*>(D.cnt_packed), D.cnt_base, D.cnt_w,
-                      reinterpret_cast<const uint32_t*>(D.dv_packed), D.dv_base, D.dv_w, D.linear, i0, i1, D.rows,
-                      &sc, &sw, &bad);
-      if (lane == 0) { D.tsum[2 * t] = sc; D.tsum[2 * t + 1] = sw; }
+  const bool staged = D.cnt_w <= 16 && (!D.linear || D.dv_w <= 16);
+  if (staged) {
+    // the CTA's 8 tiles are one contiguous bit range: stage it with coalesced 16-byte loads (one round trip)
+    const uint32_t n = uint32_t(r1 - r0);
+    if (D.cnt_w) stage_words(cw_s, D.cnt_packed, r0 * D.cnt_w / 32, (n * D.cnt_w + 31) / 32 + 2);
+    else if (threadIdx.x < 2) cw_s[threadIdx.x] = 0;
+    if (D.linear && D.dv_w) stage_words(vw_s, D.dv_packed, r0 * D.dv_w / 32, (n * D.dv_w + 31) / 32 + 2);
+    else if (threadIdx.x < 2) vw_s[threadIdx.x] = 0;
+    __syncthreads();
+    if (t < D.tiles) {
+      const uint32_t k0 = warp * K, k1 = min(k0 + K, n);
+      const uint32_t cw = D.cnt_w, vw = D.dv_w, cap = D.rows;
+      const uint32_t cm = (1u << cw) - 1u, vm = (1u << vw) - 1u;  // w <= 16
+      const uint64_t cb = D.cnt_base, vb = D.dv_base;
+      uint64_t s1 = 0, s2 = 0;
+      if (D.linear) {
+#pragma unroll 4
+        for (uint32_t k = k0 + lane; k < k1; k += 32) {
+          const uint32_t bc = k * cw, bv = k * vw;
+          uint64_t c = cb + (__funnelshift_r(cw_s[bc >> 5], cw_s[(bc >> 5) + 1], bc & 31) & cm);
+          if (c > cap) { bad = true; c = 0; }
+          s1 += c;
+          s2 += (vb + (__funnelshift_r(vw_s[bv >> 5], vw_s[(bv >> 5) + 1], bv & 31) & vm)) * c;
+        }
+      } else {
+#pragma unroll 4
+        for (uint32_t k = k0 + lane; k < k1; k += 32) {
+          const uint32_t bc = k * cw;
+          uint64_t c = cb + (__funnelshift_r(cw_s[bc >> 5], cw_s[(bc >> 5) + 1], bc & 31) & cm);
+          if (c > cap) { bad = true; c = 0; }
+          s1 += c;
+        }
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) { D.tsum[2 * t] = s1; D.tsum[2 * t + 1] = s2; }
     }
-  } else {  // warp w: inner tile (local - outer_units)*8 + w
-    const uint32_t it = (local - D.outer_units) * 8 + warp;
-    if (it < D.inner_tiles) {
-      const uint64_t i0 = uint64_t(it) * kInnerTile, i1 = min(i0 + kInnerTile, uint64_t(D.n_inner));
-      uint64_t sc, sw;
-      warp_range_sums(reinterpret_cast<const uint32_t*>(D.dc_packed), D.dc_base, D.dc_w,
-                      reinterpret_cast<const uint32_t*>(D.dv_packed), D.dv_base, D.dv_w, true, i0, i1, D.nruns,
-                      &sc, &sw, &bad);
-      if (lane == 0) { D.isum[2 * it] = sc; D.isum[2 * it + 1] = sw; }
-    }
+  } else if (t < D.tiles) {
+    const uint64_t i0 = uint64_t(t) * kRleTile, i1 = min(i0 + kRleTile, uint64_t(D.nruns));
+    uint64_t sc, sw;
+    warp_range_sums(reinterpret_cast<const uint32_t*>(D.cnt_packed), D.cnt_base, D.cnt_w,
+                    reinterpret_cast<const uint32_t*>(D.dv_packed), D.dv_base, D.dv_w, D.linear, i0, i1, D.rows,
+                    &sc, &sw, &bad);
+    if (lane == 0) { D.tsum[2 * t] = sc; D.tsum[2 * t + 1] = sw; }
   }
   if (bad) atomicOr(B.err + D.err_idx, 0x2u);
   trace_stamp(B.trace, unit, 4);
 }
 
-// One 1024-thread CTA per chunk: exclusive scans of the tile sums into per-outer-tile prefixes and anchors.
-constexpr int kScanThreads = 1024;
-
-__global__ void __launch_bounds__(kScanThreads) rle_scan_kernel(const __grid_constant__ SumsBatch B) {
-  __shared__ SumsChunk D;
-  __shared__ uint64_t warp_s[2 * kScanThreads / 32];
-  const uint32_t tid = threadIdx.x;
-  if (tid < sizeof(SumsChunk) / 4)
-    reinterpret_cast<uint32_t*>(&D)[tid] = reinterpret_cast<const uint32_t*>(&B.d[blockIdx.x])[tid];
-  grid_launch_dependents();  // rle_kernel may start staging its chunk data now
-  __syncthreads();
-  if (D.drle)  // outer tiles no inner tile anchors are marked corrupt (window start n_inner)
-    for (uint32_t t = tid; t < D.outer_tiles; t += kScanThreads) D.anchor[t] = make_uint4(D.n_inner, 0u, 0u, 0u);
-  grid_dependency_wait();  // rle_sums complete
-  uint64_t cc = 0, cw = 0;
-  for (uint32_t base = 0; base < D.outer_tiles; base += kScanThreads) {
-    const uint32_t t = base + tid;
-    uint64_t c = 0, w = 0;
-    if (t < D.outer_tiles) {
-      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(D.tsum + 2 * t));
-      c = v.x;
-      w = v.y;
-    }
-    uint64_t ec, ew, tc, tw;
-    block_excl_scan_pair<kScanThreads>(c, w, warp_s, &ec, &ew, &tc, &tw);
-    if (t < D.outer_tiles) {
-      const uint64_t pc = cc + ec, pw = cw + ew;
-      D.prefix[t] = make_uint4(uint32_t(pc), uint32_t(pc >> 32), uint32_t(pw), uint32_t(pw >> 32));
-    }
-    cc += tc;
-    cw += tw;
-  }
-  if (tid == 0 && cc != D.rows) atomicOr(B.err + D.err_idx, 0x2u);
-  if (!D.drle) return;
-  __syncthreads();  // the corrupt-marking stores above precede the real anchors
-  uint64_t ic = 0, iw = 0;
-  for (uint32_t base = 0; base < D.inner_tiles; base += kScanThreads) {
-    const uint32_t i = base + tid;
-    uint64_t dc = 0, dw = 0;
-    if (i < D.inner_tiles) {
-      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(D.isum + 2 * i));
-      dc = v.x;
-      dw = v.y;
-    }
-    uint64_t ec, ew, tc, tw;
-    block_excl_scan_pair<kScanThreads>(dc, dw, warp_s, &ec, &ew, &tc, &tw);
-    if (i < D.inner_tiles) {
-      // inner tile i covers outer runs [S0, S1): it anchors every outer tile whose first run lies there
-      const uint64_t S0 = min(ic + ec, uint64_t(D.nruns)), S1 = min(ic + ec + dc, uint64_t(D.nruns));
-      const uint64_t Q = D.base + iw + ew;
-      const uint4 rec = make_uint4(i * uint32_t(kInnerTile), uint32_t(S0), uint32_t(Q), uint32_t(Q >> 32));
-      for (uint64_t t = (S0 + K - 1) / K; t * K < S1; t++) D.anchor[t] = rec;
-    }
-    ic += tc;
-    iw += tw;
-  }
-  if (tid == 0 && ic != D.nruns) atomicOr(B.err + D.err_idx, 0x2u);
-}
-
 // ------------------------------------------------------------------------------------------ main
 // One CTA per 1024-run tile; thread t owns runs 4t..4t+3.
-//  1. stage the tile's packed counts/values (chunk data: overlaps rle_sums/rle_scan under PDL), then wait;
-//  2. output offset O and (Delta|RLE values) the anchor inner tile from rle_scan; the inner runs from the
-//     anchor on are block-scanned into a shared window that gives every outer run its value;
+//  1. stage the tile's packed counts/values (chunk data: overlaps rle_sums under PDL), then wait;
+//  2. output offset O = sum of the tile sums before this tile; run values through the fused nested provider (V_RAW: the run values a
+//     level-0 launch decoded from a Delta|RLE value lineage, read after the wait);
 //  3. the tile's non-empty runs are compacted (first row, first value, slope) and a bitmap marks the row
 //     where each one starts; row p of the tile belongs to compact run popc(bitmap[0..p]) - 1.  Each warp
-//     owns a contiguous range of 32-row windows: one binary search gives the compact run before its range,
-//     then per window lane l takes row 32k + l with one popc, and the warp stores 32 consecutive rows per
-//     instruction (coalesced, no shared-memory output image).
+//     owns a contiguous range of 32-row windows: a warp-wide popcount of the words before its range gives
+//     the compact run it starts in, then per window lane l takes row 32k + l with one popc, and the warp
+//     stores 32 consecutive rows per instruction (coalesced, no shared-memory output image).
+// Descriptor fields are copied into registers once (the shared copy would otherwise be re-read inside
+// every loop), and the compact tables are plain shared arrays (no generic-pointer address arithmetic).
 constexpr int kRPer = K / kThreads;  // 4 runs per thread
 constexpr uint32_t kSegWords = kRleSegRows / 32;
 
+__device__ __forceinline__ void stg_u64(void* p, uint64_t v) {
+  asm volatile("st.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void stg_u32(void* p, uint32_t v) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <bool TR>
 __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ RleDesc D;
-  __shared__ uint32_t cnt_s[K / 2 + 8];  // staged packed counts when w <= 16 (else read through L1)
-  // aux: staged packed values (V_BP/V_DICT/V_F2I); later the compact run values
-  __shared__ __align__(16) uint8_t aux_s[K * 8 + 64];
-  // region: the V_DRLE window (Q, dv, S of scanned inner runs) while values are computed; then the
-  // compact run slopes and starts
-  __shared__ __align__(16) uint8_t region_s[kRleWindow * 20];
-  static_assert(K * 4 + K * 8 <= kRleWindow * 20, "compact run table must fit the region");
+  __shared__ uint32_t cnt_s[K / 2 + 8];             // staged packed counts when w <= 16 (else read via L1)
+  __shared__ __align__(16) uint64_t aux_s[K + 8];   // staged packed values (V_BP/DICT/F2I); then compact values
+  __shared__ __align__(16) uint64_t cslope_s[K];    // compact run slopes (V_LINEAR)
+  __shared__ uint32_t cstart_s[K];                  // compact run first rows (tile-relative)
   __shared__ __align__(16) uint32_t bm_s[kSegWords];  // run-start bitmap of one output segment
   __shared__ uint64_t warp_s[2 * kThreads / 32];
-  uint32_t* valbits_s = reinterpret_cast<uint32_t*>(aux_s);
-  uint64_t* cval_s = reinterpret_cast<uint64_t*>(aux_s);
-  uint64_t* iQ_s = reinterpret_cast<uint64_t*>(region_s);
-  uint64_t* iDV_s = iQ_s + kRleWindow;
-  uint32_t* iS_s = reinterpret_cast<uint32_t*>(iDV_s + kRleWindow);
-  uint64_t* cslope_s = reinterpret_cast<uint64_t*>(region_s);
-  uint32_t* cstart_s = reinterpret_cast<uint32_t*>(cslope_s + K);
+  uint64_t* const trace = TR ? B.trace : nullptr;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t gt = blockIdx.x;
-  trace_stamp(B.trace, gt, 0);
-  trace_stamp(B.trace, gt, 7);
+  trace_stamp(trace, gt, 0);
+  trace_stamp(trace, gt, 7);
   stage_desc(&D, &B.d[find_desc(B, gt)]);
-  for (uint32_t k = threadIdx.x; k < kSegWords / 4; k += kThreads) reinterpret_cast<uint4*>(bm_s)[k] = make_uint4(0, 0, 0, 0);
+  reinterpret_cast<uint4*>(bm_s)[tid] = make_uint4(0, 0, 0, 0);
+  static_assert(kSegWords == 4 * kThreads, "one 16-byte bitmap store per thread");
   __syncthreads();
   const uint32_t lt = gt - D.tile0;
   const uint32_t g0 = lt * K;
   const uint32_t nr = min(uint32_t(K), D.nruns - g0);
-  const uint8_t vmode = D.vmode;
+  const uint32_t vmode = D.vmode;
   const bool linear = vmode == V_LINEAR;
   const uint32_t ob = D.out_bytes;
+  const uint32_t n = D.n;
+  const uint32_t cw = D.cnt_w, vw = D.val_w;
+  const uint64_t cbase = D.cnt_base, vbase = D.val_base;
+  const uint8_t* const cpk = D.cnt_packed;
+  const uint8_t* const vpk = D.val_packed;
   uint32_t errbits = 0;
-  const bool cnt_staged = D.cnt_w <= 16;
-  if (cnt_staged) stage_bits(cnt_s, D.cnt_packed, g0, nr, D.cnt_w);
-  if (vmode == V_BP || vmode == V_DICT || vmode == V_F2I) stage_bits(valbits_s, D.val_packed, g0, nr, D.val_w);
-  grid_dependency_wait();  // rle_scan complete: prefix / anchor are valid
+  const bool cnt_staged = cw <= 16;
+  const bool val_staged = vmode == V_BP || vmode == V_DICT || vmode == V_F2I;
+  if (cnt_staged) stage_bits(cnt_s, cpk, g0, nr, cw);
+  if (val_staged) stage_bits(reinterpret_cast<uint32_t*>(aux_s), vpk, g0, nr, vw);
+  grid_launch_dependents();  // a following level-1 launch may start its own staging
+  grid_dependency_wait();    // rle_sums (and a level-0 launch) complete: tile sums / V are valid
 
-  // ---- 2a. output offset (and the wrapping dv*count prefix of a root Delta|RLE) of this tile
-  const uint4 pf = __ldcg(D.prefix + lt);
-  const uint64_t O64 = (uint64_t(pf.y) << 32) | pf.x, Pw = (uint64_t(pf.w) << 32) | pf.z;
-  __syncthreads();  // the staged counts / values are complete
-  trace_stamp(B.trace, gt, 5);
+  // ---- 2. output offset (and the wrapping dv*count prefix of a root Delta|RLE) of this tile: the sum of the
+  // tile sums before it (L2-resident, written by rle_sums; loaded through L2 only)
+  uint64_t O64, Pw;
+  {
+    uint64_t pc = 0, pw = 0;
+    const ulonglong2* ts = reinterpret_cast<const ulonglong2*>(D.tsum);
+    for (uint32_t i = tid; i < lt; i += kThreads) {
+      const ulonglong2 v = __ldcg(ts + i);
+      pc += v.x;
+      pw += v.y;
+    }
+    pc = warp_sum(pc);
+    if (linear) pw = warp_sum(pw);
+    if (lane == 0) { warp_s[2 * warp] = pc; warp_s[2 * warp + 1] = pw; }
+    __syncthreads();  // also: the staged counts / values are complete
+    O64 = 0;
+    Pw = 0;
+#pragma unroll
+    for (int k = 0; k < kThreads / 32; k++) { O64 += warp_s[2 * k]; Pw += warp_s[2 * k + 1]; }
+    __syncthreads();  // warp_s is reused by the count scan
+  }
+  trace_stamp(trace, gt, 5);
 
   // phase A: this thread's 4 consecutive runs -- counts and values through the fused nested provider
   const uint32_t kb = tid * kRPer;
@@ -375,20 +382,38 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
   uint64_t val[kRPer];
   uint64_t sc = 0, sw = 0;
   uint32_t ne = 0;
+  const uint32_t cmask = cw >= 32 ? 0xFFFFFFFFu : (1u << cw) - 1u;
+  uint64_t raw[kRPer];
+  if (vmode == V_RAW) {  // level-0 output: 4 consecutive u64 (32-byte aligned)
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(vpk) + g0 + kb;
+    if (kb + kRPer <= nr) {
+      const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(src));
+      const ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2*>(src) + 1);
+      raw[0] = a.x; raw[1] = a.y; raw[2] = b.x; raw[3] = b.y;
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRPer; r++) raw[r] = kb + r < nr ? __ldcg(src + r) : 0ull;
+    }
+  }
 #pragma unroll
   for (int r = 0; r < kRPer; r++) {
     const uint32_t k = kb + r;
     uint64_t c = 0, v = 0;
     if (k < nr) {
       const uint64_t g = g0 + k;
-      c = D.cnt_base +
-          (cnt_staged ? (D.cnt_w ? extract_bits(cnt_s, uint64_t(k) * D.cnt_w, D.cnt_w) : 0ull)
-                      : extract_bits_global(reinterpret_cast<const uint32_t*>(D.cnt_packed), g * D.cnt_w, D.cnt_w));
-      if (c > D.n) { errbits |= 0x2u; c = 0; }
+      if (cnt_staged) {
+        const uint32_t bit = k * cw;
+        c = cbase + (__funnelshift_r(cnt_s[bit >> 5], cnt_s[(bit >> 5) + 1], bit & 31) & cmask);
+      } else {
+        c = cbase + extract_bits_global(reinterpret_cast<const uint32_t*>(cpk), g * cw, cw);
+      }
+      if (c > n) { errbits |= 0x2u; c = 0; }
       if (linear) {
-        v = D.val_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.val_packed), g * D.val_w, D.val_w);
-      } else if (vmode != V_DRLE) {
-        const uint64_t x = D.val_base + (D.val_w ? extract_bits(valbits_s, uint64_t(k) * D.val_w, D.val_w) : 0ull);
+        v = vbase + extract_bits_global(reinterpret_cast<const uint32_t*>(vpk), g * vw, vw);
+      } else if (vmode == V_RAW) {
+        v = raw[r];
+      } else {
+        const uint64_t x = vbase + (vw ? extract_bits(reinterpret_cast<const uint32_t*>(aux_s), uint64_t(k) * vw, vw) : 0ull);
         if (vmode == V_BP) {
           v = x;
         } else if (vmode == V_DICT) {
@@ -407,86 +432,17 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
     ne += c != 0;
     if (linear) sw += v * c;
   }
-  if (vmode == V_DRLE) {
-    // ---- values of outer runs g = Q_j + (g - S_j + 1) dv_j, j the inner run holding g: the inner runs from the
-    // anchor tile on are scanned into a shared-memory window (pass after pass until every run is covered)
-    const uint4 rec = __ldcg(D.anchor + lt);
-    uint32_t ws = rec.x;
-    uint64_t Sbase = rec.y, Qbase = (uint64_t(rec.w) << 32) | rec.z;
-    uint32_t pending = 0;  // bit r: run r still needs its value
-#pragma unroll
-    for (int r = 0; r < kRPer; r++)
-      if (kb + r < nr) pending |= 1u << r;
-    for (int pass = 0;; pass++) {
-      const uint32_t nload = ws < D.n_inner ? min(uint32_t(kRleWindow), D.n_inner - ws) : 0u;
-      // blocked load: thread t takes inner runs ws + 4t .. +3
-      uint64_t dcv[4], dvv[4], lc = 0, lw = 0;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint32_t k = tid * 4 + q;
-        dcv[q] = 0;
-        dvv[q] = 0;
-        if (k < nload) {
-          const uint64_t j = ws + k;
-          dcv[q] = D.idc_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.idc_packed), j * D.idc_w, D.idc_w);
-          dvv[q] = D.idv_base + extract_bits_global(reinterpret_cast<const uint32_t*>(D.idv_packed), j * D.idv_w, D.idv_w);
-          if (dcv[q] > D.nruns) dcv[q] = 0;
-        }
-        lc += dcv[q];
-        lw += dvv[q] * dcv[q];
-      }
-      uint64_t tcs, tws, ec2, ew2;
-      block_excl_scan_pair<kThreads>(lc, lw, warp_s, &ec2, &ew2, &tcs, &tws);
-      {
-        uint64_t c = Sbase + ec2, w = Qbase + ew2;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const uint32_t k = tid * 4 + q;
-          if (k < kRleWindow) {
-            iS_s[k] = uint32_t(min(c, uint64_t(0xFFFFFFFFu)));
-            iQ_s[k] = w;
-            iDV_s[k] = dvv[q];
-          }
-          c += dcv[q];
-          w += dvv[q] * dcv[q];
-        }
-      }
-      __syncthreads();
-      const uint64_t Send = Sbase + tcs;
-      if (pending && nload) {
-        uint32_t a = 0;
-#pragma unroll
-        for (int r = 0; r < kRPer; r++) {
-          const uint64_t g = g0 + kb + r;
-          if ((pending >> r & 1u) && g < Send && g >= iS_s[0]) {
-            if (a == 0) a = run_search(iS_s, 0, nload - 1, uint32_t(g));
-            while (a + 1 < nload && iS_s[a + 1] <= g) a++;
-            val[r] = iQ_s[a] + (g - iS_s[a] + 1) * iDV_s[a];
-            pending &= ~(1u << r);
-          }
-        }
-      }
-      const bool more = __syncthreads_or(pending != 0);
-      if (!more) break;
-      if (!nload || pass > 64) {  // the inner runs do not cover this tile: corrupt
-        errbits |= 0x2u;
-        break;
-      }
-      ws += nload;
-      Sbase = Send;
-      Qbase += tws;
-    }
-  }
-  trace_stamp(B.trace, gt, 1);
+  trace_stamp(trace, gt, 1);
   // ---- 3. block scan of (non-empty runs << 44 | rows): this thread's first row and first compact index
-  uint64_t T, W, ex, ew;
-  block_excl_scan_pair<kThreads>((uint64_t(ne) << 44) | sc, sw, warp_s, &ex, &ew, &T, &W);
-  const uint64_t ec = ex & ((1ull << 44) - 1), ce = ex >> 44;
+  uint64_t T, W, ex, ew = 0;
+  if (linear) block_excl_scan_pair<kThreads>((uint64_t(ne) << 44) | sc, sw, warp_s, &ex, &ew, &T, &W);
+  else ex = block_excl_scan_u64<kThreads>((uint64_t(ne) << 44) | sc, warp_s, &T);
+  const uint32_t ec = uint32_t(ex & ((1ull << 44) - 1)), ce = uint32_t(ex >> 44);
   const uint32_t nce = uint32_t(T >> 44);
   T &= (1ull << 44) - 1;
-  trace_stamp(B.trace, gt, 2);
-  const bool overflow = O64 + T > D.n;
-  if (tid == 0 && (overflow || (lt + 1 == D.ntiles && O64 + T != D.n))) errbits |= 0x2u;
+  trace_stamp(trace, gt, 2);
+  const bool overflow = O64 + T > n;
+  if (tid == 0 && (overflow || (lt + 1 == D.ntiles && O64 + T != n))) errbits |= 0x2u;
   if (errbits) atomicOr(B.err + D.err_idx, errbits);
   if (overflow) return;  // corrupt counts: never write outside [0, n) (uniform across the CTA)
   const uint32_t O = uint32_t(O64);
@@ -519,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       uint32_t* so = B.big.soffs + uint64_t(e) * (K + 1);
       uint64_t* va = B.big.vals + uint64_t(e) * K;
       uint64_t* sl = B.big.slopes + uint64_t(e) * K;
-      uint32_t row = uint32_t(ec);
+      uint32_t row = ec;
       uint64_t wv = Pw + ew;
 #pragma unroll
       for (int r = 0; r < kRPer; r++) {
@@ -534,20 +490,21 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       }
       if (tid == 0) so[nr] = Tt;
     }
-    trace_stamp(B.trace, gt, 4);
+    trace_stamp(trace, gt, 4);
     return;
   }
 
   // compact run table: first row, first value, slope of every non-empty run
-  __syncthreads();  // the V_DRLE window / staged values are dead from here on
+  __syncthreads();  // the staged values are dead from here on
   {
-    uint32_t row = uint32_t(ec), c = uint32_t(ce);
+    uint32_t row = ec, c = ce;
     uint64_t wv = Pw + ew;
+    const uint64_t dbase = D.delta_base;
 #pragma unroll
     for (int r = 0; r < kRPer; r++) {
       if (cnt[r]) {
         cstart_s[c] = row;
-        cval_s[c] = linear ? D.delta_base + wv + val[r] : val[r];
+        aux_s[c] = linear ? dbase + wv + val[r] : val[r];
         if (linear) cslope_s[c] = val[r];
         c++;
       }
@@ -555,18 +512,19 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       row += cnt[r];
     }
   }
-  trace_stamp(B.trace, gt, 3);
-  uint8_t* gout = reinterpret_cast<uint8_t*>(D.out) + uint64_t(O) * ob;
+  trace_stamp(trace, gt, 3);
+  uint8_t* const gout = reinterpret_cast<uint8_t*>(D.out) + uint64_t(O) * ob;
+  const uint32_t lmask = FULL >> (31 - lane);
   for (uint32_t s0 = 0; s0 < Tt; s0 += kRleSegRows) {  // one segment unless the tile holds > 32 K rows
     const uint32_t rows = min(Tt - s0, kRleSegRows);
     const uint32_t nw = (rows + 31) / 32;
     if (s0) {  // later segments: clear the previous segment's bits
       __syncthreads();
-      for (uint32_t k = tid; k < kSegWords; k += kThreads) bm_s[k] = 0u;
+      reinterpret_cast<uint4*>(bm_s)[tid] = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
     {
-      uint32_t row = uint32_t(ec);
+      uint32_t row = ec;
 #pragma unroll
       for (int r = 0; r < kRPer; r++) {
         const uint32_t p = row - s0;
@@ -578,31 +536,53 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
     // warp w: windows [k0, k1); cb = compact runs starting before row s0 + 32 k0
     const uint32_t per = (nw + kThreads / 32 - 1) / (kThreads / 32);
     const uint32_t k0 = min(nw, warp * per), k1 = min(nw, k0 + per);
-    if (k0 < k1) {
-      const uint32_t first = s0 + 32 * k0;
+    uint32_t c_lt = 0;  // compact runs starting before s0 (later segments only)
+    if (s0) {
       uint32_t lo = 0, hi = nce;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (cstart_s[mid] < first) lo = mid + 1; else hi = mid;
+        if (cstart_s[mid] < s0) lo = mid + 1; else hi = mid;
       }
-      uint32_t cb = lo;
-      const uint32_t lmask = FULL >> (31 - lane);
-      uint8_t* gseg = gout + uint64_t(s0) * ob;
-      for (uint32_t k = k0; k < k1; k++) {
-        const uint32_t word = bm_s[k];
-        const uint32_t p = k * 32 + lane;
-        const uint32_t c = cb + __popc(word & lmask) - 1;
-        cb += __popc(word);
-        uint64_t v = cval_s[c];
-        if (linear) v += uint64_t(s0 + p - cstart_s[c]) * cslope_s[c];
-        if (p < rows) {
-          if (ob == 8) reinterpret_cast<uint64_t*>(gseg)[p] = v;
-          else reinterpret_cast<uint32_t*>(gseg)[p] = uint32_t(v);
+      c_lt = lo;
+    }
+    uint32_t pc = 0;
+    for (uint32_t k = lane; k < k0; k += 32) pc += __popc(bm_s[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
+    uint32_t cb = c_lt + pc - 1;  // compact index of row (32 k0 - 1): lane rows then add their own bits
+    uint8_t* const gseg = gout + uint64_t(s0) * ob;
+    if (ob == 8) {
+      uint64_t* const o64 = reinterpret_cast<uint64_t*>(gseg);
+      if (linear) {
+        for (uint32_t k = k0; k < k1; k++) {
+          const uint32_t word = bm_s[k], p = k * 32 + lane;
+          const uint32_t c = cb + __popc(word & lmask);
+          cb += __popc(word);
+          const uint64_t v = aux_s[c] + uint64_t(s0 + p - cstart_s[c]) * cslope_s[c];
+          if (p < rows) stg_u64(o64 + p, v);
         }
+      } else {
+#pragma unroll 2
+        for (uint32_t k = k0; k < k1; k++) {
+          const uint32_t word = bm_s[k], p = k * 32 + lane;
+          const uint32_t c = cb + __popc(word & lmask);
+          cb += __popc(word);
+          if (p < rows) stg_u64(o64 + p, aux_s[c]);
+        }
+      }
+    } else {
+      uint32_t* const o32 = reinterpret_cast<uint32_t*>(gseg);
+      for (uint32_t k = k0; k < k1; k++) {
+        const uint32_t word = bm_s[k], p = k * 32 + lane;
+        const uint32_t c = cb + __popc(word & lmask);
+        cb += __popc(word);
+        uint64_t v = aux_s[c];
+        if (linear) v += uint64_t(s0 + p - cstart_s[c]) * cslope_s[c];
+        if (p < rows) stg_u32(o32 + p, uint32_t(v));
       }
     }
   }
-  trace_stamp(B.trace, gt, 4);
+  trace_stamp(trace, gt, 4);
 }
 
 // ------------------------------------------------------------------------------------------ big tiles
@@ -652,24 +632,9 @@ cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_rle_scan(const SumsBatch& b, cudaStream_t s) {
-  if (!b.n) return cudaSuccess;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(b.n);
-  cfg.blockDim = dim3(kScanThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, rle_scan_kernel, b);
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  // programmatic dependent launch: rle_kernel's prologue overlaps rle_scan (CDM_PDL=0 disables)
+  // programmatic dependent launch: rle_kernel's prologue overlaps rle_sums (CDM_PDL=0 disables)
   const bool pdl = pdl_enabled();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(b.total_tiles);
@@ -681,7 +646,7 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, rle_kernel, b);
+  cudaError_t e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false>, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

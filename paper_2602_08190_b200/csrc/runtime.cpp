@@ -132,7 +132,7 @@ struct Bound {
   uint32_t entries = 0;
   uint8_t d = 0;
   uint64_t delta_base = 0, inner_base = 0;
-  uint32_t nruns = 0, n_inner = 0, max_run = 0;
+  uint32_t nruns = 0, n_inner = 0, max_run = 0, inner_max_run = 0;
   bool lz4 = false;
   uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
   uint32_t n_sub = 0, lz_sub_bytes = 0, lz_uniform = 0;
@@ -309,6 +309,7 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
         const Node& rl = c.nodes[ri];
         if (rl.n != b->nruns) return bad("inner RLE count mismatch");
         b->n_inner = rl.u32_at0();
+        b->inner_max_run = rl.u32_at4();
         if (b->nruns && !b->n_inner) return bad("inner RLE has no runs");
         if (!(e = bind_bp(c, t, t.kids[ri][0], b->n_inner, 64, &b->inner_dv)).empty()) return bad(e);
         if (!(e = bind_bp(c, t, t.kids[ri][1], b->n_inner, 32, &b->inner_dc)).empty()) return bad(e);
@@ -379,6 +380,18 @@ struct Alloc {  // bump allocator over one device arena; pass 1 sizes, pass 2 as
 // ============================================================================ device batches
 enum Family { F_FP = 0, F_SCAN = 1, F_RLE = 2, F_LZ4 = 3, F_COPY = 4 };
 
+// Stream priority of a kernel family.  CDM_RLE_PRIO=hi: the latency-bound RLE chain (sums -> scan -> expand)
+// gets its CTAs scheduled first and the bandwidth-bound families fill the SMs it leaves idle; lo: the
+// reverse (short bandwidth-bound kernels of later pipeline groups are never queued behind RLE CTAs).
+static int fam_priority(int f, int lo, int hi) {
+  static const int mode = [] {
+    const char* v = std::getenv("CDM_RLE_PRIO");
+    return v && v[0] == 'h' ? 1 : 0;
+  }();
+  if (mode == 1) return f == F_RLE ? hi : lo;
+  return f == F_RLE ? lo : hi;
+}
+
 struct cdm_batch {
   cdm_engine* e = nullptr;
   int device = 0;
@@ -400,6 +413,10 @@ struct cdm_batch {
   uint32_t* err_host = nullptr;
   bool own_err_host = true;
   bool zeroed_by_caller = false;  // the engine zeroes the scratch prefix before waiting for the copy
+  // device-resident batches: the error words are cleared by cdm_batch_results (and at creation), not by a
+  // kernel in front of every launch -- the epoch-tagged scan words and self-resetting RLE counters in the
+  // zeroed region need no per-launch clearing
+  bool sticky_errors = false;
   uint32_t* err_external = nullptr;  // pipelines: error words live in one array shared by all groups
   cudaStream_t* fam = nullptr;     // the family streams concurrent kernel families fork onto
   // fork/join events: independent kernel families run concurrently on the engine's family streams
@@ -412,7 +429,22 @@ struct cdm_batch {
   std::vector<Pending> pending;
   double fam_ms[5] = {0, 0, 0, 0, 0};
   uint64_t fam_launches[5] = {0, 0, 0, 0, 0};
+  // graph mode (cdm_batch_set_graph): the enqueue is captured once per (stream, timing) and replayed
+  bool use_graph = false, capturing = false, graph_pending = false, graph_timing = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;
+  uint32_t graph_nl = 0;
+  uint64_t graph_fam_launches[5] = {0, 0, 0, 0, 0};
+  std::vector<Pending> graph_events;
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    gexec = nullptr;
+    graph = nullptr;
+  }
   ~cdm_batch() {
+    drop_graph();
     if (fork) cudaEventDestroy(fork);
     for (auto ev : join) if (ev) cudaEventDestroy(ev);
     if (own_arena && arena) cudaFree(arena);
@@ -431,14 +463,14 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
   B->err_dev = B->err_external ? B->err_external : A.take<uint32_t>(nj ? nj : 1);
-  std::vector<int> fpj, scj, rlj, drj, lzj;
+  std::vector<int> fpj, scj, rlj, lzj;
   for (size_t i = 0; i < nj; i++) {
     const Bound& b = B->jobs[i];
     switch (b.kind) {
       case PlanKind::Fp: if (b.rows) fpj.push_back(int(i)); break;
       case PlanKind::Scan: if (b.rows) scj.push_back(int(i)); break;
       case PlanKind::Rle:
-        if (b.rows) { rlj.push_back(int(i)); if (b.vmode == V_DRLE) drj.push_back(int(i)); }
+        if (b.rows) rlj.push_back(int(i));
         break;
       case PlanKind::Str:
         if (b.rows) scj.push_back(int(i)); else B->zero_offsets.push_back(b.offs);
@@ -510,77 +542,105 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     sb.lb = A.take<uint4>(tiles);
     B->scan.push_back(sb);
   }
-  // rle_sums: per RLE chunk the outer tile sums (+ the inner tile sums of a Delta|RLE value lineage)
-  for (auto& g : groups(rlj)) {
+  // RLE units: one per RLE job; a Delta|RLE value lineage (V_DRLE) adds a level-0 unit that expands the
+  // inner arithmetic runs into the outer run values V (an L2-resident u64 array), read by the job's level-1
+  // unit as V_RAW.  Every unit has its own tile sums / prefixes; level-0 launches precede level-1 ones.
+  struct RleUnit { int job; bool level0; };
+  std::vector<RleUnit> units;
+  for (int j : rlj) {
+    if (B->jobs[j].vmode == V_DRLE) units.push_back({j, true});
+    units.push_back({j, false});
+  }
+  auto unit_groups = [&](int level) {  // unit indices (level -1: all), <= kMaxBatch per group
+    std::vector<std::vector<int>> g;
+    for (int u = 0; u < int(units.size()); u++) {
+      if (level >= 0 && units[u].level0 != (level == 0)) continue;
+      if (g.empty() || g.back().size() == size_t(kMaxBatch)) g.emplace_back();
+      g.back().push_back(u);
+    }
+    return g;
+  };
+  std::vector<std::pair<int, int>> sums_at(units.size()), rle_at(units.size());  // (batch, desc) per unit
+  for (auto& g : unit_groups(-1)) {
     SumsBatch sb{};
     sb.err = B->err_dev;
-    uint32_t units = 0;
-    for (int j : g) {
-      const Bound& b = B->jobs[j];
+    uint32_t nunits = 0;
+    for (int u : g) {
+      const Bound& b = B->jobs[units[u].job];
+      sums_at[u] = {int(B->sums.size()), int(sb.n)};
       SumsChunk& d = sb.d[sb.n++];
-      d.cnt_packed = b.dev_chunk + b.counts.off;
-      d.cnt_base = b.counts.base;
-      d.cnt_w = uint16_t(b.counts.w);
-      d.linear = b.vmode == V_LINEAR;
-      d.drle = b.vmode == V_DRLE;
-      if (d.linear) { d.dv_packed = b.dev_chunk + b.main.off; d.dv_base = b.main.base; d.dv_w = uint16_t(b.main.w); }
-      if (d.drle) {
+      if (units[u].level0) {  // inner RLE: counts dc, slopes dv over the outer runs
+        d.cnt_packed = b.dev_chunk + b.inner_dc.off; d.cnt_base = b.inner_dc.base; d.cnt_w = uint16_t(b.inner_dc.w);
         d.dv_packed = b.dev_chunk + b.inner_dv.off; d.dv_base = b.inner_dv.base; d.dv_w = uint16_t(b.inner_dv.w);
-        d.dc_packed = b.dev_chunk + b.inner_dc.off; d.dc_base = b.inner_dc.base; d.dc_w = uint16_t(b.inner_dc.w);
-        d.base = b.inner_base;
-        d.n_inner = b.n_inner;
-        d.inner_tiles = uint32_t(div_up(b.n_inner, kInnerTile));
+        d.linear = 1;
+        d.nruns = b.n_inner;
+        d.rows = b.nruns;
+      } else {
+        d.cnt_packed = b.dev_chunk + b.counts.off; d.cnt_base = b.counts.base; d.cnt_w = uint16_t(b.counts.w);
+        d.linear = b.vmode == V_LINEAR;
+        if (d.linear) { d.dv_packed = b.dev_chunk + b.main.off; d.dv_base = b.main.base; d.dv_w = uint16_t(b.main.w); }
+        d.nruns = b.nruns;
+        d.rows = uint32_t(b.rows);
       }
-      d.nruns = b.nruns;
-      d.rows = uint32_t(b.rows);
-      d.outer_tiles = uint32_t(div_up(b.nruns, kRleTile));
-      d.outer_units = uint32_t(div_up(d.outer_tiles, 8));
-      d.inner_units = uint32_t(div_up(d.inner_tiles, 8));
-      d.unit0 = units;
-      d.err_idx = uint32_t(j);
-      units += d.outer_units + d.inner_units;
+      d.tiles = uint32_t(div_up(d.nruns, kRleTile));
+      d.units = uint32_t(div_up(d.tiles, 8));
+      d.unit0 = nunits;
+      d.err_idx = uint32_t(units[u].job);
+      nunits += d.units;
     }
-    sb.total_units = units;
+    sb.total_units = nunits;
     B->sums.push_back(sb);
   }
-  // rle
-  for (auto& g : groups(rlj)) {
-    RleBatch rb{};
-    rb.err = B->err_dev;
-    uint32_t tiles = 0, slots = 0;
-    for (int j : g) {
-      const Bound& b = B->jobs[j];
-      RleDesc& d = rb.d[rb.n++];
-      d.cnt_packed = b.dev_chunk + b.counts.off;
-      d.cnt_base = b.counts.base;
-      d.cnt_w = uint16_t(b.counts.w);
-      d.val_packed = b.vmode == V_DRLE ? nullptr : b.dev_chunk + b.main.off;
-      d.val_base = b.main.base;
-      d.val_w = uint16_t(b.main.w);
-      d.dict = b.vmode == V_DICT ? b.dev_chunk + b.dict_off : nullptr;
-      d.entries = b.entries;
-      d.d = b.d;
-      d.vmode = b.vmode;
-      d.out = b.out;
-      d.out_bytes = uint8_t(b.W);
-      d.delta_base = b.delta_base;
-      d.n = uint32_t(b.rows);
-      d.nruns = b.nruns;
-      d.n_inner = b.n_inner;
-      d.tile0 = tiles;
-      d.ntiles = uint32_t(div_up(b.nruns, kRleTile));
-      d.err_idx = uint32_t(j);
-      tiles += d.ntiles;
-      slots += uint32_t(b.rows / kRleBigLimit) + 1;
-      // the header's max run bounds a tile's output; only then can rle_big be skipped (a lying header
-      // only costs speed: oversize tiles are then expanded in place)
-      if (uint64_t(kRleTile) * b.max_run > kRleBigLimit) rb.big_enabled = 1;
+  for (int level = 0; level < 2; level++) {
+    for (auto& g : unit_groups(level)) {
+      RleBatch rb{};
+      rb.err = B->err_dev;
+      uint32_t tiles = 0, slots = 0;
+      for (int u : g) {
+        const Bound& b = B->jobs[units[u].job];
+        rle_at[u] = {int(B->rle.size()), int(rb.n)};
+        RleDesc& d = rb.d[rb.n++];
+        uint32_t max_run;
+        if (units[u].level0) {
+          d.cnt_packed = b.dev_chunk + b.inner_dc.off; d.cnt_base = b.inner_dc.base; d.cnt_w = uint16_t(b.inner_dc.w);
+          d.val_packed = b.dev_chunk + b.inner_dv.off; d.val_base = b.inner_dv.base; d.val_w = uint16_t(b.inner_dv.w);
+          d.vmode = V_LINEAR;
+          d.delta_base = b.inner_base;
+          d.out_bytes = 8;
+          d.n = b.nruns;
+          d.nruns = b.n_inner;
+          max_run = b.inner_max_run;  // d.out: the V array, assigned below
+        } else {
+          d.cnt_packed = b.dev_chunk + b.counts.off; d.cnt_base = b.counts.base; d.cnt_w = uint16_t(b.counts.w);
+          d.val_packed = b.vmode == V_DRLE ? nullptr : b.dev_chunk + b.main.off;  // V_RAW: assigned below
+          d.val_base = b.main.base;
+          d.val_w = uint16_t(b.main.w);
+          d.dict = b.vmode == V_DICT ? b.dev_chunk + b.dict_off : nullptr;
+          d.entries = b.entries;
+          d.d = b.d;
+          d.vmode = b.vmode == V_DRLE ? uint8_t(V_RAW) : b.vmode;
+          d.out = b.out;
+          d.out_bytes = uint8_t(b.W);
+          d.delta_base = b.delta_base;
+          d.n = uint32_t(b.rows);
+          d.nruns = b.nruns;
+          max_run = b.max_run;
+        }
+        d.tile0 = tiles;
+        d.ntiles = uint32_t(div_up(d.nruns, kRleTile));
+        d.err_idx = uint32_t(units[u].job);
+        tiles += d.ntiles;
+        slots += d.n / kRleBigLimit + 1;
+        // the header's max run bounds a tile's output; only then can rle_big be skipped (a lying header
+        // only costs speed: oversize tiles are then expanded in place)
+        if (uint64_t(kRleTile) * max_run > kRleBigLimit) rb.big_enabled = 1;
+      }
+      rb.total_tiles = tiles;
+      rb.big.counter = A.take<unsigned long long>(1);
+      rb.big.done = A.take<uint32_t>(1);
+      rb.big.max_slots = slots;
+      B->rle.push_back(rb);
     }
-    rb.total_tiles = tiles;
-    rb.big.counter = A.take<unsigned long long>(1);
-    rb.big.done = A.take<uint32_t>(1);
-    rb.big.max_slots = slots;
-    B->rle.push_back(rb);
   }
   *zero_bytes = (A.off + 15) & ~size_t(15);  // launch_zero works in 16-byte words (the next take pads to 256)
   // ---- non-zeroed region: optional per-tile trace (env CDM_TRACE=<csv path>)
@@ -589,36 +649,23 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     for (auto& pb : B->sums) pb.trace = A.take<uint64_t>(size_t(pb.total_units) * 8);
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
-  // ---- non-zeroed region: look-back values, big-tile slots, inner run tables
-  // per RLE chunk: the tile sums rle_sums writes and rle_kernel reduces
-  std::map<int, const SumsChunk*> sums_of;
-  for (auto& pb : B->sums)
-    for (uint32_t k = 0; k < pb.n; k++) {
-      SumsChunk& d = pb.d[k];
-      d.tsum = A.take<uint64_t>(size_t(d.outer_tiles) * 2);
-      d.prefix = A.take<uint4>(d.outer_tiles);
-      if (d.drle) {
-        d.isum = A.take<uint64_t>(size_t(d.inner_tiles) * 2);
-        d.anchor = A.take<uint4>(d.outer_tiles);
-      }
-      sums_of[int(d.err_idx)] = &d;
-    }
+  // ---- non-zeroed region: tile sums + prefixes per RLE unit, big-tile slots, level-0 run values
+  for (size_t u = 0; u < units.size(); u++) {
+    SumsChunk& d = B->sums[sums_at[u].first].d[sums_at[u].second];
+    d.tsum = A.take<uint64_t>(size_t(d.tiles) * 2);
+    B->rle[rle_at[u].first].d[rle_at[u].second].tsum = d.tsum;
+  }
+  for (size_t u = 0; u < units.size(); u++) {
+    if (!units[u].level0) continue;
+    uint64_t* V = A.take<uint64_t>(B->jobs[units[u].job].nruns + 4);
+    B->rle[rle_at[u].first].d[rle_at[u].second].out = V;
+    B->rle[rle_at[u + 1].first].d[rle_at[u + 1].second].val_packed = reinterpret_cast<const uint8_t*>(V);
+  }
   for (auto& rb : B->rle) {
     rb.big.entries = A.take<RleBig::Entry>(rb.big.max_slots);
     rb.big.soffs = A.take<uint32_t>(size_t(rb.big.max_slots) * (kRleTile + 1));
     rb.big.vals = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
     rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
-    for (uint32_t k = 0; k < rb.n; k++) {
-      RleDesc& d = rb.d[k];
-      const SumsChunk* sc = sums_of[int(d.err_idx)];
-      d.prefix = sc->prefix;
-      if (d.vmode == V_DRLE) {
-        const Bound& b = B->jobs[d.err_idx];
-        d.anchor = sc->anchor;
-        d.idv_packed = b.dev_chunk + b.inner_dv.off; d.idv_base = b.inner_dv.base; d.idv_w = uint16_t(b.inner_dv.w);
-        d.idc_packed = b.dev_chunk + b.inner_dc.off; d.idc_base = b.inner_dc.base; d.idc_w = uint16_t(b.inner_dc.w);
-      }
-    }
   }
   // LZ4
   for (auto& g : groups(lzj)) {
@@ -685,7 +732,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   int nfam = 0;
   for (bool h : has) nfam += h;
   // error words, tickets, look-back words and counters start at zero (one tiny kernel, not a memset)
-  if (!B->zeroed_by_caller) CUDA_TRY(launch_zero(B->arena, B->zero_bytes, s));
+  if (!B->zeroed_by_caller && !B->sticky_errors) CUDA_TRY(launch_zero(B->arena, B->zero_bytes, s));
   // fork: with several families each runs on its own stream (the latency-bound scan/RLE chains overlap
   // the bandwidth-bound FP kernel); a single family stays on `s`
   static const bool serial = std::getenv("CDM_SERIAL") != nullptr;
@@ -704,7 +751,9 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
     cudaStream_t fs = fork ? B->fam[fam] : s;
     if (fork) CUDA_TRY(cudaStreamWaitEvent(fs, B->fork, 0));
     cudaEvent_t ta = nullptr;
-    if (B->timing) { ta = ev_get(B, evk++); CUDA_TRY(cudaEventRecord(ta, fs)); }
+    // (in a graph capture the timing events become external event-record nodes, re-recorded by every replay)
+    const unsigned evflags = B->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (B->timing) { ta = ev_get(B, evk++); CUDA_TRY(cudaEventRecordWithFlags(ta, fs, evflags)); }
     switch (fam) {
       case F_FP:
         for (size_t i = 0; i < B->fp.size(); i++) { CUDA_TRY(launch_fp(B->fp[i], B->fp_maxw[i], fs)); n++; B->fam_launches[F_FP]++; }
@@ -713,13 +762,9 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, fs)); n++; B->fam_launches[F_SCAN]++; }
         break;
       case F_RLE:
-        // per group of <= kMaxBatch chunks: sums -> scan -> expand (the last two programmatically dependent)
-        for (size_t gi = 0; gi < B->rle.size(); gi++) {
-          auto& rb = B->rle[gi];
-          CUDA_TRY(launch_rle_sums(B->sums[gi], fs));
-          CUDA_TRY(launch_rle_scan(B->sums[gi], fs));
-          n += 2;
-          B->fam_launches[F_RLE] += 2;
+        // sums -> expand (level-0 batches first); the expansions are programmatically dependent launches
+        for (auto& pb : B->sums) { CUDA_TRY(launch_rle_sums(pb, fs)); n++; B->fam_launches[F_RLE]++; }
+        for (auto& rb : B->rle) {
           CUDA_TRY(launch_rle(rb, fs));
           n++;
           B->fam_launches[F_RLE]++;
@@ -744,7 +789,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
     }
     if (B->timing) {
       cudaEvent_t tb = ev_get(B, evk++);
-      CUDA_TRY(cudaEventRecord(tb, fs));
+      CUDA_TRY(cudaEventRecordWithFlags(tb, fs, evflags));
       B->pending.push_back({fam, ta, tb});
     }
     if (fork) {
@@ -855,7 +900,7 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   auto make_fams = [&](cudaStream_t* fam) -> cudaError_t {
     for (int f = 0; f < 5; f++) {
-      cudaError_t ce = cudaStreamCreateWithPriority(&fam[f], cudaStreamNonBlocking, f == F_RLE ? prio_lo : prio_hi);
+      cudaError_t ce = cudaStreamCreateWithPriority(&fam[f], cudaStreamNonBlocking, fam_priority(f, prio_lo, prio_hi));
       if (ce != cudaSuccess) return ce;
     }
     return cudaSuccess;
@@ -1326,7 +1371,7 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
   std::vector<std::array<cudaStream_t, 5>> fam(lanes);
   for (size_t l = 0; l < lanes; l++) {
     ds[l] = mk(prio_hi);
-    for (int f = 0; f < 5; f++) fam[l][f] = mk(f == F_RLE ? prio_lo : prio_hi);
+    for (int f = 0; f < 5; f++) fam[l][f] = mk(fam_priority(f, prio_lo, prio_hi));
   }
   for (auto x : P->streams) if (!x) return fail(CDM_E_CUDA, "pipeline stream creation failed");
   std::vector<cudaEvent_t> copied(groups.size());
@@ -1474,8 +1519,9 @@ extern "C" CDM_API cdm_status cdm_batch_create(cdm_engine* e, const cdm_job* job
     if (st) { g_last = "job " + std::to_string(i) + ": " + g_last; return st; }
     B->jobs.push_back(b);
   }
-  cdm_status st = batch_build(B.get(), nullptr, 0);
+  cdm_status st = batch_build(B.get(), nullptr, 0);  // zeroes the scratch prefix once
   if (st) return st;
+  B->sticky_errors = true;
   CUDA_TRY(cudaHostAlloc(&B->err_host, sizeof(uint32_t) * std::max<size_t>(1, n), cudaHostAllocDefault));
   *out = B.release();
   return CDM_OK;
@@ -1485,7 +1531,63 @@ extern "C" CDM_API cdm_status cdm_batch_launch(cdm_batch* b, void* stream, uint3
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   CUDA_TRY(cudaSetDevice(b->device));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : b->e->decode;
-  return batch_enqueue(b, s, n_launches);
+  if (!b->use_graph) return batch_enqueue(b, s, n_launches);
+  if (b->graph_pending) {  // the previous replay's timing was not collected: it is lost
+    b->graph_pending = false;
+  }
+  if (!b->gexec || b->gstream != s || b->graph_timing != b->timing) {
+    b->drop_graph();
+    uint64_t before[5];
+    for (int f = 0; f < 5; f++) before[f] = b->fam_launches[f];
+    const size_t pend0 = b->pending.size();
+    CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    b->capturing = true;
+    uint32_t nl = 0;
+    cdm_status st = batch_enqueue(b, s, &nl);
+    b->capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st) { if (g) cudaGraphDestroy(g); return st; }
+    if (ce != cudaSuccess) return fail(CDM_E_CUDA, std::string("batch graph capture: ") + cudaGetErrorString(ce));
+    b->graph = g;
+    CUDA_TRY(cudaGraphInstantiate(&b->gexec, g, 0));
+    b->gstream = s;
+    b->graph_timing = b->timing;
+    b->graph_nl = nl;
+    for (int f = 0; f < 5; f++) {
+      b->graph_fam_launches[f] = b->fam_launches[f] - before[f];
+      b->fam_launches[f] = before[f];
+    }
+    b->graph_events.assign(b->pending.begin() + pend0, b->pending.end());
+    b->pending.resize(pend0);
+  }
+  CUDA_TRY(cudaGraphLaunch(b->gexec, s));
+  for (int f = 0; f < 5; f++) b->fam_launches[f] += b->graph_fam_launches[f];
+  b->graph_pending = b->timing;
+  if (n_launches) *n_launches = b->graph_nl;
+  return CDM_OK;
+}
+
+// Graph mode with timing: the replay's per-family events are read after it completes (call between replays,
+// outside any caller-timed region).
+extern "C" CDM_API cdm_status cdm_batch_collect_timing(cdm_batch* b) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  if (!b->graph_pending) return CDM_OK;
+  for (auto& p : b->graph_events) {
+    CUDA_TRY(cudaEventSynchronize(p.b));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+    b->fam_ms[p.fam] += ms;
+  }
+  b->graph_pending = false;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_set_graph(cdm_batch* b, int enable) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  b->use_graph = enable != 0;
+  if (!b->use_graph) b->drop_graph();
+  return CDM_OK;
 }
 
 // CDM_TRACE: append "kernel,launch,tile,t_start,t_unpacked,t_scanned,t_lookback,t_end,smid" rows (ns)
@@ -1516,6 +1618,8 @@ extern "C" CDM_API cdm_status cdm_batch_results(cdm_batch* b, void* stream, cdm_
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : b->e->decode;
   CUDA_TRY(cudaMemcpyAsync(b->err_host, b->err_dev, sizeof(uint32_t) * std::max<size_t>(1, b->jobs.size()),
                            cudaMemcpyDeviceToHost, s));
+  if (b->sticky_errors)  // the next launch starts from clean error words
+    CUDA_TRY(cudaMemsetAsync(b->err_dev, 0, sizeof(uint32_t) * std::max<size_t>(1, b->jobs.size()), s));
   CUDA_TRY(cudaStreamSynchronize(s));
   for (auto& p : b->pending) {
     float ms = 0;

@@ -46,12 +46,13 @@ def _outputs(chunk):
 
 def gpu_decode(engine, casc, chunks, resident=False, expect_error=False):
     """Decode chunks on the GPU; returns [(payload numpy, offsets numpy|None, result dict)].
-    resident: False = cdm_submit_batch, True = cdm_batch_* on device copies, "pipeline" = cdm_pipeline_*."""
+    resident: False = cdm_submit_batch, True = cdm_batch_* on device copies, "pipeline" = cdm_pipeline_*,
+    "graph" = cdm_batch_* in graph mode (captured on the first launch, replayed on the second)."""
     decs, bufs = [], []
     for ch in chunks:
         out, offs, info = _outputs(ch)
         d = cdm.Decode(casc, cdm.pinned(ch), out, offs)
-        if resident is True:
+        if resident is True or resident == "graph":
             d.dev_chunk = torch.from_numpy(ch).cuda()
         decs.append(d)
         bufs.append((out, offs, info))
@@ -60,6 +61,21 @@ def gpu_decode(engine, casc, chunks, resident=False, expect_error=False):
         p.launch()
         res = p.results(raise_on_error=not expect_error)
         p.close()
+    elif resident == "graph":
+        b = cdm.Batch(engine, decs)
+        b.set_graph(True)
+        stream = torch.cuda.Stream()
+        for _ in range(2):  # capture + replay, then a replay over outputs reset to the sentinel
+            b.launch(stream)
+            res = b.results(stream, raise_on_error=not expect_error)
+            for out, offs, _ in bufs:
+                out.fill_(SENTINEL)
+                if offs is not None:
+                    offs.fill_(-7)
+            torch.cuda.synchronize()
+        b.launch(stream)
+        res = b.results(stream, raise_on_error=not expect_error)
+        b.close()
     elif resident:
         b = cdm.Batch(engine, decs)
         b.launch()
@@ -88,7 +104,7 @@ def check_parity(engine, spec, col_or_chunks, dtype=None, width=0, rows_per_chun
     else:
         chunks = col_or_chunks
     casc = cdm.Cascade(spec, dtype, width)
-    modes = [False, "pipeline", True] if both else [True]
+    modes = [False, "pipeline", True, "graph"] if both else [True]
     for resident in modes:
         got = gpu_decode(engine, casc, chunks, resident=resident)
         for ch, (payload, offs, r) in zip(chunks, got):
