@@ -130,6 +130,7 @@ struct RleBig {  // queue of oversize tiles, expanded by rle_big
 struct RleBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint32_t any_linear;           // some descriptor is V_LINEAR (the kernel variant with a slope table)
   uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   uint32_t big_enabled;          // 0: rle_big is not launched -> oversize tiles are expanded in place

@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     // window (w <= 16); wider fields are extracted one by one
     const uint32_t cls = w <= 8 ? 0u : w <= 16 ? 1u : w <= 32 ? 2u : 3u;
     const uint32_t m32 = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+    // dictionary index limits: field f is valid iff f < lim (base >= entries: none is)
+    const uint64_t lim = base < entries ? entries - base : 0ull;
+    const uint32_t base32 = uint32_t(base);
 
 #pragma unroll 1
     for (uint32_t k = 0; k < 4 && !bytes_path; k++) {
@@ -153,33 +156,39 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
           else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint8_t(v[j]);
         }
       } else if (mode == FP_DICT) {
+        // index = base + field, valid iff field < lim = entries - base (all 32-bit: w <= 32 here, and a
+        // dictionary has < 2^32 entries); an invalid index raises the error bit and reads entry 0
+        uint32_t idx[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-          if (v[j] >= entries) { bad_index = true; v[j] = 0; }
+          const uint64_t f = v[j] - base;
+          const bool ok = f < lim;
+          bad_index |= !ok;
+          idx[j] = ok ? base32 + uint32_t(f) : 0u;
         }
         if (dsm && ob == 8) {
           uint64_t* o = reinterpret_cast<uint64_t*>(out8) + gi;
           if (full) {
-            st_v2_u64(o, dict_s[v[0]], dict_s[v[1]]);
-            st_v2_u64(o + 2, dict_s[v[2]], dict_s[v[3]]);
-          } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = dict_s[v[j]];
+            st_v2_u64(o, dict_s[idx[0]], dict_s[idx[1]]);
+            st_v2_u64(o + 2, dict_s[idx[2]], dict_s[idx[3]]);
+          } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = dict_s[idx[j]];
         } else if (dsm) {
           const uint32_t* d32 = reinterpret_cast<const uint32_t*>(dict_s);
           uint32_t* o = reinterpret_cast<uint32_t*>(out8) + gi;
-          if (full) st_v4_u32(o, d32[v[0]], d32[v[1]], d32[v[2]], d32[v[3]]);
-          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = d32[v[j]];
+          if (full) st_v4_u32(o, d32[idx[0]], d32[idx[1]], d32[idx[2]], d32[idx[3]]);
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = d32[idx[j]];
         } else if (ob == 8) {
           const uint64_t* dict = reinterpret_cast<const uint64_t*>(dict8);
           uint64_t* o = reinterpret_cast<uint64_t*>(out8) + gi;
           if (full) {
-            st_v2_u64(o, __ldg(dict + v[0]), __ldg(dict + v[1]));
-            st_v2_u64(o + 2, __ldg(dict + v[2]), __ldg(dict + v[3]));
-          } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
+            st_v2_u64(o, __ldg(dict + idx[0]), __ldg(dict + idx[1]));
+            st_v2_u64(o + 2, __ldg(dict + idx[2]), __ldg(dict + idx[3]));
+          } else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + idx[j]);
         } else if (ob == 4) {
           const uint32_t* dict = reinterpret_cast<const uint32_t*>(dict8);
           uint32_t* o = reinterpret_cast<uint32_t*>(out8) + gi;
-          if (full) st_v4_u32(o, __ldg(dict + v[0]), __ldg(dict + v[1]), __ldg(dict + v[2]), __ldg(dict + v[3]));
-          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + v[j]);
+          if (full) st_v4_u32(o, __ldg(dict + idx[0]), __ldg(dict + idx[1]), __ldg(dict + idx[2]), __ldg(dict + idx[3]));
+          else _Pragma("unroll") for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = __ldg(dict + idx[j]);
         }
       } else {  // FP_F2I: one IEEE division per element (no reciprocal: bit-exact, R13)
         const double p = kPow10[D.d];
@@ -263,6 +272,11 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
+  // the persistent grid is capped at 2 CTAs per SM (CDM_FP_CTAS_PER_SM overrides): each CTA then walks ~5+
+  // tiles with its TMA double buffer full (measured faster than 4 CTAs/SM even alone), and SM slots stay
+  // free for a concurrent RLE chain
+  static const int cap = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 2;
+  if (cap > 0 && cap < per_sm) per_sm = cap;
   uint32_t grid = uint32_t(device_sms() * per_sm);
   // CDM_FP_GRID=tiles: one CTA per tile (no persistence), so CTAs of a concurrent higher-priority family
   // are scheduled as soon as any FP CTA retires

@@ -219,7 +219,10 @@ __device__ __forceinline__ void stage_words(uint32_t* dst, const uint8_t* src, u
   for (uint32_t k = threadIdx.x; k < (nw + 3) / 4; k += kThreads) d4[k] = __ldg(s4 + k);
 }
 
-constexpr uint32_t kSumsRuns = 8 * K;                    // runs per rle_sums CTA (8 warps x one tile)
+constexpr uint32_t kSumsWarpRuns = 1024;                    // runs per rle_sums warp (half a tile)
+constexpr uint32_t kSumsRuns = 8 * kSumsWarpRuns;           // runs per rle_sums CTA (4 tiles)
+constexpr uint32_t kSumsTiles = kSumsRuns / K;
+constexpr uint32_t kWarpsPerTile = K / kSumsWarpRuns;
 constexpr uint32_t kSumsWords = kSumsRuns * 16 / 32 + 8;  // staged words per stream for w <= 16
 
 __global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_constant__ SumsBatch B) {
@@ -240,10 +243,12 @@ __global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_cons
   trace_stamp(B.trace, unit, 0);
   trace_stamp(B.trace, unit, 7);
   grid_launch_dependents();  // rle_kernel may start staging now
-  const uint32_t t0 = (unit - D.unit0) * 8;
+  __shared__ uint64_t part_s[8][2];
+  const uint32_t t0 = (unit - D.unit0) * kSumsTiles;
   const uint64_t r0 = uint64_t(t0) * K, r1 = min(r0 + kSumsRuns, uint64_t(D.nruns));
-  const uint32_t t = t0 + warp;  // warp w: tile t0 + w
+  const uint32_t t = t0 + warp / kWarpsPerTile;  // the warps of tile t0 + t' sum its 1024-run parts
   bool bad = false;
+  uint64_t s1 = 0, s2 = 0;
   const bool staged = D.cnt_w <= 16 && (!D.linear || D.dv_w <= 16);
   if (staged) {
     // the CTA's 8 tiles are one contiguous bit range: stage it with coalesced 16-byte loads (one round trip)
@@ -254,11 +259,10 @@ __global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_cons
     else if (threadIdx.x < 2) vw_s[threadIdx.x] = 0;
     __syncthreads();
     if (t < D.tiles) {
-      const uint32_t k0 = warp * K, k1 = min(k0 + K, n);
+      const uint32_t k0 = min(n, warp * kSumsWarpRuns), k1 = min(k0 + kSumsWarpRuns, n);
       const uint32_t cw = D.cnt_w, vw = D.dv_w, cap = D.rows;
       const uint32_t cm = (1u << cw) - 1u, vm = (1u << vw) - 1u;  // w <= 16
       const uint64_t cb = D.cnt_base, vb = D.dv_base;
-      uint64_t s1 = 0, s2 = 0;
       if (D.linear) {
 #pragma unroll 4
         for (uint32_t k = k0 + lane; k < k1; k += 32) {
@@ -279,15 +283,24 @@ __global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_cons
       }
       s1 = warp_sum(s1);
       s2 = warp_sum(s2);
-      if (lane == 0) { D.tsum[2 * t] = s1; D.tsum[2 * t + 1] = s2; }
     }
   } else if (t < D.tiles) {
-    const uint64_t i0 = uint64_t(t) * kRleTile, i1 = min(i0 + kRleTile, uint64_t(D.nruns));
-    uint64_t sc, sw;
+    const uint64_t i0 = min(r1, r0 + uint64_t(warp) * kSumsWarpRuns), i1 = min(i0 + kSumsWarpRuns, r1);
     warp_range_sums(reinterpret_cast<const uint32_t*>(D.cnt_packed), D.cnt_base, D.cnt_w,
                     reinterpret_cast<const uint32_t*>(D.dv_packed), D.dv_base, D.dv_w, D.linear, i0, i1, D.rows,
-                    &sc, &sw, &bad);
-    if (lane == 0) { D.tsum[2 * t] = sc; D.tsum[2 * t + 1] = sw; }
+                    &s1, &s2, &bad);
+  }
+  if (lane == 0) { part_s[warp][0] = s1; part_s[warp][1] = s2; }
+  __syncthreads();
+  if (threadIdx.x < kSumsTiles && t0 + threadIdx.x < D.tiles) {
+    uint64_t a = 0, b = 0;
+#pragma unroll
+    for (uint32_t h = 0; h < kWarpsPerTile; h++) {
+      a += part_s[threadIdx.x * kWarpsPerTile + h][0];
+      b += part_s[threadIdx.x * kWarpsPerTile + h][1];
+    }
+    D.tsum[2 * (t0 + threadIdx.x)] = a;
+    D.tsum[2 * (t0 + threadIdx.x) + 1] = b;
   }
   if (bad) atomicOr(B.err + D.err_idx, 0x2u);
   trace_stamp(B.trace, unit, 4);
@@ -300,29 +313,34 @@ __global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_cons
 //     level-0 launch decoded from a Delta|RLE value lineage, read after the wait);
 //  3. the tile's non-empty runs are compacted (first row, first value, slope) and a bitmap marks the row
 //     where each one starts; row p of the tile belongs to compact run popc(bitmap[0..p]) - 1.  Each warp
-//     owns a contiguous range of 32-row windows: a warp-wide popcount of the words before its range gives
-//     the compact run it starts in, then per window lane l takes row 32k + l with one popc, and the warp
-//     stores 32 consecutive rows per instruction (coalesced, no shared-memory output image).
+//     owns a contiguous range of 64-row windows aligned to even global rows: a warp-wide popcount of the
+//     words before its range gives the compact run it starts in, then per window lane l takes rows
+//     2l, 2l+1 with two popcounts and one aligned vector store, so a warp stores 64 consecutive rows per
+//     instruction (coalesced, no shared-memory output image).
 // Descriptor fields are copied into registers once (the shared copy would otherwise be re-read inside
 // every loop), and the compact tables are plain shared arrays (no generic-pointer address arithmetic).
 constexpr int kRPer = K / kThreads;  // 4 runs per thread
-constexpr uint32_t kSegWords = kRleSegRows / 32;
+constexpr uint32_t kBmWords = kRleSegRows / 64 + 2;  // 64-bit bitmap words of one segment (+ the shift bit)
 
 __device__ __forceinline__ void stg_u64(void* p, uint64_t v) {
   asm volatile("st.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_v2_u32(void* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
 }
 __device__ __forceinline__ void stg_u32(void* p, uint32_t v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <bool TR>
+// LIN: the batch has arithmetic-run (V_LINEAR) descriptors; their slope table lives in dynamic shared memory
+template <bool TR, bool LIN>
 __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ RleDesc D;
   __shared__ uint32_t cnt_s[K / 2 + 8];             // staged packed counts when w <= 16 (else read via L1)
   __shared__ __align__(16) uint64_t aux_s[K + 8];   // staged packed values (V_BP/DICT/F2I); then compact values
-  __shared__ __align__(16) uint64_t cslope_s[K];    // compact run slopes (V_LINEAR)
+  extern __shared__ __align__(16) uint64_t cslope_s[];  // [K] compact run slopes (V_LINEAR batches only)
   __shared__ uint32_t cstart_s[K];                  // compact run first rows (tile-relative)
-  __shared__ __align__(16) uint32_t bm_s[kSegWords];  // run-start bitmap of one output segment
+  __shared__ __align__(16) uint64_t bm_s[kBmWords];  // run-start bitmap of one output segment
   __shared__ uint64_t warp_s[2 * kThreads / 32];
   uint64_t* const trace = TR ? B.trace : nullptr;
 
@@ -331,14 +349,14 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
   trace_stamp(trace, gt, 0);
   trace_stamp(trace, gt, 7);
   stage_desc(&D, &B.d[find_desc(B, gt)]);
-  reinterpret_cast<uint4*>(bm_s)[tid] = make_uint4(0, 0, 0, 0);
-  static_assert(kSegWords == 4 * kThreads, "one 16-byte bitmap store per thread");
+  for (uint32_t q = tid; q < kBmWords / 2; q += kThreads) reinterpret_cast<uint4*>(bm_s)[q] = make_uint4(0, 0, 0, 0);
+  static_assert(kBmWords % 2 == 0, "bitmap cleared in 16-byte words");
   __syncthreads();
   const uint32_t lt = gt - D.tile0;
   const uint32_t g0 = lt * K;
   const uint32_t nr = min(uint32_t(K), D.nruns - g0);
   const uint32_t vmode = D.vmode;
-  const bool linear = vmode == V_LINEAR;
+  const bool linear = LIN && vmode == V_LINEAR;
   const uint32_t ob = D.out_bytes;
   const uint32_t n = D.n;
   const uint32_t cw = D.cnt_w, vw = D.val_w;
@@ -514,13 +532,18 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
   }
   trace_stamp(trace, gt, 3);
   uint8_t* const gout = reinterpret_cast<uint8_t*>(D.out) + uint64_t(O) * ob;
-  const uint32_t lmask = FULL >> (31 - lane);
+  // 64-row windows aligned to EVEN global rows: bit b of a segment's bitmap is segment row b - a, a = parity
+  // of the segment's first global row, so lane l's pair of rows (bits 2l, 2l+1) is one aligned 16-byte
+  // (8-byte rows) or 8-byte (4-byte rows) store
+  const uint32_t b0 = 2 * lane;
+  const uint64_t lm0 = (2ull << b0) - 1ull;  // bits <= 2l
   for (uint32_t s0 = 0; s0 < Tt; s0 += kRleSegRows) {  // one segment unless the tile holds > 32 K rows
     const uint32_t rows = min(Tt - s0, kRleSegRows);
-    const uint32_t nw = (rows + 31) / 32;
+    const uint32_t a = (O + s0) & 1u;
+    const uint32_t nw = (rows + a + 63) / 64;
     if (s0) {  // later segments: clear the previous segment's bits
       __syncthreads();
-      reinterpret_cast<uint4*>(bm_s)[tid] = make_uint4(0, 0, 0, 0);
+      for (uint32_t q = tid; q < kBmWords / 2; q += kThreads) reinterpret_cast<uint4*>(bm_s)[q] = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
     {
@@ -528,12 +551,15 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
 #pragma unroll
       for (int r = 0; r < kRPer; r++) {
         const uint32_t p = row - s0;
-        if (cnt[r] && row >= s0 && p < rows) atomicOr(bm_s + (p >> 5), 1u << (p & 31));
+        if (cnt[r] && row >= s0 && p < rows) {
+          const uint32_t bb = p + a;
+          atomicOr(reinterpret_cast<uint32_t*>(bm_s) + (bb >> 5), 1u << (bb & 31));
+        }
         row += cnt[r];
       }
     }
     __syncthreads();  // bitmap + compact run table complete
-    // warp w: windows [k0, k1); cb = compact runs starting before row s0 + 32 k0
+    // warp w: windows [k0, k1); cb = compact index of the row before its first window
     const uint32_t per = (nw + kThreads / 32 - 1) / (kThreads / 32);
     const uint32_t k0 = min(nw, warp * per), k1 = min(nw, k0 + per);
     uint32_t c_lt = 0;  // compact runs starting before s0 (later segments only)
@@ -546,39 +572,37 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       c_lt = lo;
     }
     uint32_t pc = 0;
-    for (uint32_t k = lane; k < k0; k += 32) pc += __popc(bm_s[k]);
+    for (uint32_t k = lane; k < k0; k += 32) pc += __popcll(bm_s[k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
-    uint32_t cb = c_lt + pc - 1;  // compact index of row (32 k0 - 1): lane rows then add their own bits
+    uint32_t cb = c_lt + pc - 1;
     uint8_t* const gseg = gout + uint64_t(s0) * ob;
-    if (ob == 8) {
-      uint64_t* const o64 = reinterpret_cast<uint64_t*>(gseg);
+    for (uint32_t k = k0; k < k1; k++) {
+      const uint64_t wv = bm_s[k];
+      const uint32_t c0 = cb + __popcll(wv & lm0);
+      const uint32_t c1 = c0 + uint32_t((wv >> (b0 + 1)) & 1ull);
+      cb += __popcll(wv);
+      const int32_t p0 = int32_t(64 * k + b0) - int32_t(a);  // segment row of bit 2l
+      uint64_t v0 = aux_s[c0 == 0xFFFFFFFFu ? 0u : c0], v1 = aux_s[c1];
       if (linear) {
-        for (uint32_t k = k0; k < k1; k++) {
-          const uint32_t word = bm_s[k], p = k * 32 + lane;
-          const uint32_t c = cb + __popc(word & lmask);
-          cb += __popc(word);
-          const uint64_t v = aux_s[c] + uint64_t(s0 + p - cstart_s[c]) * cslope_s[c];
-          if (p < rows) stg_u64(o64 + p, v);
+        v0 += uint64_t(int64_t(s0) + p0 - cstart_s[c0 == 0xFFFFFFFFu ? 0u : c0]) * cslope_s[c0 == 0xFFFFFFFFu ? 0u : c0];
+        v1 += uint64_t(int64_t(s0) + p0 + 1 - cstart_s[c1]) * cslope_s[c1];
+      }
+      const bool ok0 = p0 >= 0 && p0 < int32_t(rows), ok1 = p0 + 1 < int32_t(rows) && p0 + 1 >= 0;
+      if (ob == 8) {
+        uint64_t* const o = reinterpret_cast<uint64_t*>(gseg) + p0;
+        if (ok0 && ok1) st_v2_u64(o, v0, v1);
+        else {
+          if (ok0) stg_u64(o, v0);
+          if (ok1) stg_u64(o + 1, v1);
         }
       } else {
-#pragma unroll 2
-        for (uint32_t k = k0; k < k1; k++) {
-          const uint32_t word = bm_s[k], p = k * 32 + lane;
-          const uint32_t c = cb + __popc(word & lmask);
-          cb += __popc(word);
-          if (p < rows) stg_u64(o64 + p, aux_s[c]);
+        uint32_t* const o = reinterpret_cast<uint32_t*>(gseg) + p0;
+        if (ok0 && ok1) st_v2_u32(o, uint32_t(v0), uint32_t(v1));
+        else {
+          if (ok0) stg_u32(o, uint32_t(v0));
+          if (ok1) stg_u32(o + 1, uint32_t(v1));
         }
-      }
-    } else {
-      uint32_t* const o32 = reinterpret_cast<uint32_t*>(gseg);
-      for (uint32_t k = k0; k < k1; k++) {
-        const uint32_t word = bm_s[k], p = k * 32 + lane;
-        const uint32_t c = cb + __popc(word & lmask);
-        cb += __popc(word);
-        uint64_t v = aux_s[c];
-        if (linear) v += uint64_t(s0 + p - cstart_s[c]) * cslope_s[c];
-        if (p < rows) stg_u32(o32 + p, uint32_t(v));
       }
     }
   }
@@ -639,14 +663,22 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(b.total_tiles);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = b.any_linear ? K * sizeof(uint64_t) : 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false>, b);
+  static bool configured = false;
+  if (!configured) {  // the slope table takes the linear variants past the 48 KB default
+    cudaFuncSetAttribute(rle_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * sizeof(uint64_t));
+    cudaFuncSetAttribute(rle_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * sizeof(uint64_t));
+    configured = true;
+  }
+  cudaError_t e;
+  if (b.any_linear) e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, true>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, true>, b);
+  else e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, false>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, false>, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

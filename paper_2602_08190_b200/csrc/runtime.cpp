@@ -583,7 +583,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         d.rows = uint32_t(b.rows);
       }
       d.tiles = uint32_t(div_up(d.nruns, kRleTile));
-      d.units = uint32_t(div_up(d.tiles, 8));
+      d.units = uint32_t(div_up(uint64_t(d.tiles) * kRleTile, 8192));  // rle_sums CTA: 8 warps x 1024 runs
       d.unit0 = nunits;
       d.err_idx = uint32_t(units[u].job);
       nunits += d.units;
@@ -629,6 +629,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         d.tile0 = tiles;
         d.ntiles = uint32_t(div_up(d.nruns, kRleTile));
         d.err_idx = uint32_t(units[u].job);
+        if (d.vmode == V_LINEAR) rb.any_linear = 1;
         tiles += d.ntiles;
         slots += d.n / kRleBigLimit + 1;
         // the header's max run bounds a tile's output; only then can rle_big be skipped (a lying header
