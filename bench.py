@@ -290,25 +290,30 @@ def main():
     for r in res:
         err_bits |= r["error_bits"]
 
-    # ---------------------------------------------------------------- per-family kernel time (roofline)
-    # the same graph re-captured with CUDA events around each kernel family on its launching stream; its
-    # per-replay event pairs are read between replays (the events themselves lengthen the step a little,
-    # so this pass is kept apart from the value pass)
-    batch.set_timing(True)
+    # ---------------------------------------------------------------- per-kernel / per-family time (roofline)
+    # the same graph re-captured with CUDA events around each kernel launch (mode 2: families one after
+    # another and the programmatically dependent RLE launches serialised, so every kernel is timed alone, as
+    # in the ncu launch list) and, in a second pass, around each kernel family (mode 1, concurrent);
+    # each replay's events are read between replays.  Kept apart from the value pass: in-graph events
+    # lengthen the step.
     tsteps = min(args.steps, 50)
-    for _ in range(2):
-        batch.launch(stream)
-        batch.collect_timing()
-    batch.set_timing(True)  # reset the accumulated times
-    for k in range(tsteps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
+    timing = {}
+    batch.set_graph(False)  # plain stream launches: an event record there is a light command (in a graph
+    for mode in (2, 1):     # an external event node costs ~2 us)
+        batch.set_timing(mode)
+        for _ in range(2):
             batch.launch(stream)
-        batch.collect_timing()
-    kern = batch.kernel_ms()
-    res = batch.results(stream)
-    for r in res:
-        err_bits |= r["error_bits"]
+        for r in batch.results(stream, raise_on_error=False):
+            err_bits |= r["error_bits"]
+        batch.set_timing(mode)  # reset the accumulated times
+        for k in range(tsteps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                batch.launch(stream)
+        for r in batch.results(stream, raise_on_error=False):  # reads every launch's events
+            err_bits |= r["error_bits"]
+        timing[mode] = batch.kernel_times() if mode == 2 else batch.kernel_ms()
+    kern, ktimes = timing[1], timing[2]
 
     # ---------------------------------------------------------------- end to end from pinned host (e2e)
     # (a) cdm_pipeline: the H4 schedule (Johnson order, groups, copies overlapped with decodes) captured
@@ -364,7 +369,8 @@ def main():
         e2e = tot_decoded * e2e_steps / e2e_total / 1e9
         e2e_sub = tot_decoded * e2e_steps / sub_total / 1e9
         peak, peak_src = load_peaks()
-        # dominant kernel family by device time; algorithmic bytes = compressed read + decoded written
+        # dominant kernel by device time; algorithmic bytes = compressed read + decoded written (Eq. 1) of
+        # the chunks that kernel decodes
         fam_ms = {FAMILY_NAMES[i]: kern[FAMILY_NAMES[i]] for i in range(5)}
         fam_bytes = {"fp": 0, "scan": 0, "rle": 0, "lz4": 0, "copy": 0}
         for d in decs_dev:
@@ -379,10 +385,14 @@ def main():
                 fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
             else:
                 fam_bytes["copy"] += info["compressed_bytes"] + info["payload_bytes"]
-        dom = max(fam_ms, key=lambda f: fam_ms[f][0])
-        dom_ms, dom_launch = fam_ms[dom]
+        kbytes = {"fp_kernel": fam_bytes["fp"], "scan_kernel": fam_bytes["scan"], "rle_kernel": fam_bytes["rle"],
+                  "lz4_kernel": fam_bytes["lz4"], "device_copy": fam_bytes["copy"]}
+        dom = max(ktimes, key=lambda k: ktimes[k][0])
+        dom_ms, dom_n = ktimes[dom]
         per_step_ms = dom_ms / tsteps
-        achieved = fam_bytes[dom] / (per_step_ms / 1e3) / 1e9
+        dom_bytes = kbytes.get(dom) or 0
+        achieved = dom_bytes / (per_step_ms / 1e3) / 1e9 if dom_bytes else 0.0
+        domf = max(fam_ms, key=lambda f: fam_ms[f][0])
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
@@ -403,12 +413,16 @@ def main():
                           "the launching stream; max over ranks",
                 "wall_s_timed_loop": round(wall, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": FAMILY_KERNELS[dom],
-                         "algorithmic_bytes_per_step": fam_bytes[dom], "kernel_ms_per_step": round(per_step_ms, 4),
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+                         "algorithmic_bytes_per_step": dom_bytes, "kernel_ms_per_step": round(per_step_ms, 4),
+                         "launches_per_step": round(dom_n / tsteps, 2),
+                         "kernels_ms_per_step": {k: round(v[0] / tsteps, 4) for k, v in ktimes.items() if v[1]},
                          "peak_source": peak_src,
                          "families_ms_per_step": {f: round(fam_ms[f][0] / tsteps, 4) for f in fam_ms if fam_ms[f][1]},
-                         "timing": f"CUDA events around each kernel family inside the step graph, {tsteps} replays "
-                                   "after L2 flushes (a separate pass: the in-graph events lengthen the step)"},
+                         "timing": f"CUDA events around each kernel launch, each kernel alone (kernels_ms), and "
+                                   f"around each concurrent kernel family (families_ms, dominant family {domf}), "
+                                   f"recorded on the launching streams over {tsteps} steps after L2 flushes each "
+                                   "(passes separate from the graph-timed value pass)"},
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": tot_comp,
                     "d2h_bytes_per_step": 4 * tot_chunks, "pcie_h2d_gbs_measured": round(h2d_gbs, 1),
                     "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_gbs, 1),

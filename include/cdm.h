@@ -184,12 +184,18 @@ CDM_API cdm_status cdm_pipeline_results(cdm_pipeline *p, cdm_result *results);
 CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
 
 /* ---- instrumentation ---- */
-/* Record CUDA events around each kernel family launched by cdm_batch_launch (0 = off).  After
- * cdm_batch_results, cdm_batch_kernel_ms() returns the accumulated per-family milliseconds over all
- * launches since the last reset: index 0 FP (H5), 1 delta/offset scan (H6), 2 RLE (H7), 3 LZ4 (H8),
- * 4 raw copies. */
+/* Record CUDA events around each kernel family (enable = 1) or around each kernel launch (enable = 2,
+ * which runs the families one after another and serialises programmatically dependent launches, so each
+ * launch is timed alone) issued by cdm_batch_launch; 0 = off; every
+ * call resets the accumulators.  After cdm_batch_results (or cdm_batch_collect_timing in graph mode):
+ * cdm_batch_kernel_ms() -> per-family milliseconds and launches: index 0 FP (H5), 1 delta/offset scan (H6),
+ *   2 RLE (H7), 3 LZ4 (H8), 4 raw copies;
+ * cdm_batch_kernel_times() -> per-kernel milliseconds and launches (mode 2): index 0 fp_kernel,
+ *   1 scan_kernel, 2 rle_sums_kernel, 3 rle_kernel level 0 (value lineage), 4 rle_kernel, 5 rle_big_kernel,
+ *   6 lz4_kernel, 7 device copies. */
 CDM_API cdm_status cdm_batch_set_timing(cdm_batch *b, int enable);
 CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch *b, double *ms5, uint64_t *launches5);
+CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms8, uint64_t *launches8);
 /* Graph mode + timing: every replay re-records the same events, so call this after each launch (it
  * waits for that replay) to accumulate its per-family times; a replay not collected is not counted. */
 CDM_API cdm_status cdm_batch_collect_timing(cdm_batch *b);

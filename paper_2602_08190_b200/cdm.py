@@ -18,12 +18,14 @@ STATUS = {0: "CDM_OK", 1: "CDM_E_INVALID_ARG", 2: "CDM_E_PARSE", 3: "CDM_E_UNSUP
           5: "CDM_E_CAPACITY", 6: "CDM_E_CUDA", 7: "CDM_E_OOM", 8: "CDM_E_BUSY"}
 ERR_DICT_INDEX, ERR_RUN_SUM, ERR_LZ4, ERR_LENGTHS, ERR_WIDTH = 0x1, 0x2, 0x4, 0x8, 0x10
 FAMILIES = ["fp", "scan", "rle", "lz4", "copy"]
+KERNELS = ["fp_kernel", "scan_kernel", "rle_sums_kernel", "rle_kernel(level0)", "rle_kernel", "rle_big_kernel",
+           "lz4_kernel", "device_copy"]
 
 SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_create", "cdm_cascade_destroy",
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
            "cdm_submit_batch", "cdm_wait", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
-           "cdm_batch_set_graph", "cdm_batch_collect_timing",
+           "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times",
            "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy"]
 
 
@@ -90,6 +92,7 @@ def lib():
         "cdm_batch_kernel_ms": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)],
         "cdm_batch_set_graph": [vp, st],
         "cdm_batch_collect_timing": [vp],
+        "cdm_batch_kernel_times": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)],
         "cdm_pipeline_create": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(vp)],
         "cdm_pipeline_launch": [vp, vp],
         "cdm_pipeline_results": [vp, ctypes.POINTER(Result)],
@@ -267,8 +270,9 @@ class Batch:
             _check(rc)
         return [res[i].as_dict() for i in range(self.n)]
 
-    def set_timing(self, on: bool) -> None:
-        _check(lib().cdm_batch_set_timing(self.h, 1 if on else 0))
+    def set_timing(self, on) -> None:
+        """False/0 off, True/1 per kernel family, 2 per kernel launch."""
+        _check(lib().cdm_batch_set_timing(self.h, int(on)))
 
     def set_graph(self, on: bool) -> None:
         _check(lib().cdm_batch_set_graph(self.h, 1 if on else 0))
@@ -281,6 +285,12 @@ class Batch:
         nl = (ctypes.c_uint64 * 5)()
         _check(lib().cdm_batch_kernel_ms(self.h, ms, nl))
         return {FAMILIES[i]: (ms[i], nl[i]) for i in range(5)}
+
+    def kernel_times(self) -> dict:
+        ms = (ctypes.c_double * 8)()
+        nl = (ctypes.c_uint64 * 8)()
+        _check(lib().cdm_batch_kernel_times(self.h, ms, nl))
+        return {KERNELS[i]: (ms[i], nl[i]) for i in range(8)}
 
     def close(self) -> None:
         if getattr(self, "h", None) and _lib is not None:

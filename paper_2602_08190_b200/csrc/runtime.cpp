@@ -392,6 +392,9 @@ static int fam_priority(int f, int lo, int hi) {
   return f == F_RLE ? lo : hi;
 }
 
+// kernel kinds of cdm_batch_kernel_times (include/cdm.h)
+enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, kKernelKinds };
+
 struct cdm_batch {
   cdm_engine* e = nullptr;
   int device = 0;
@@ -401,6 +404,7 @@ struct cdm_batch {
   std::vector<ScanBatch> scan;
   std::vector<SumsBatch> sums;
   std::vector<RleBatch> rle;
+  size_t rle_level0 = 0;  // rle[0, rle_level0) are level-0 (Delta|RLE value lineage) launches
   std::vector<Lz4Batch> lz4;
   std::vector<uint32_t> lz4_max_sub;
   struct Copy { void* dst; const void* src; size_t bytes; };
@@ -429,8 +433,12 @@ struct cdm_batch {
   std::vector<Pending> pending;
   double fam_ms[5] = {0, 0, 0, 0, 0};
   uint64_t fam_launches[5] = {0, 0, 0, 0, 0};
+  int timing_mode = 0;  // 1: events around each kernel family; 2: around each kernel launch
+  double k_ms[kKernelKinds] = {};
+  uint64_t k_n[kKernelKinds] = {};
   // graph mode (cdm_batch_set_graph): the enqueue is captured once per (stream, timing) and replayed
   bool use_graph = false, capturing = false, graph_pending = false, graph_timing = false;
+  int graph_mode = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
@@ -592,6 +600,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     B->sums.push_back(sb);
   }
   for (int level = 0; level < 2; level++) {
+    if (level == 1) B->rle_level0 = B->rle.size();
     for (auto& g : unit_groups(level)) {
       RleBatch rb{};
       rb.err = B->err_dev;
@@ -739,7 +748,8 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   static const bool serial = std::getenv("CDM_SERIAL") != nullptr;
   // the RLE family always forks: its stream has the lowest priority, so the short bandwidth-bound kernels
   // of later groups (and the engine's bookkeeping kernels) get SMs as soon as an RLE CTA retires
-  const bool fork = (nfam > 1 || has[F_RLE]) && B->fam && !serial;
+  // per-kernel timing (mode 2) runs the families one after another, so each launch's events time it alone
+  const bool fork = (nfam > 1 || has[F_RLE]) && B->fam && !serial && !(B->timing && B->timing_mode == 2);
   if (fork) {
     if (!B->fork) {
       CUDA_TRY(cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming));
@@ -754,41 +764,73 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
     cudaEvent_t ta = nullptr;
     // (in a graph capture the timing events become external event-record nodes, re-recorded by every replay)
     const unsigned evflags = B->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
-    if (B->timing) { ta = ev_get(B, evk++); CUDA_TRY(cudaEventRecordWithFlags(ta, fs, evflags)); }
+    const bool fam_t = B->timing && B->timing_mode != 2, ker_t = B->timing && B->timing_mode == 2;
+    if (fam_t) { ta = ev_get(B, evk++); CUDA_TRY(cudaEventRecordWithFlags(ta, fs, evflags)); }
+    // one launch, bracketed by its own events in per-kernel timing mode (which serialises PDL pairs)
+    auto timed = [&](int kind, auto&& launch) -> cdm_status {
+      cudaEvent_t ka = nullptr;
+      if (ker_t) { ka = ev_get(B, evk++); CUDA_TRY(cudaEventRecordWithFlags(ka, fs, evflags)); }
+      CUDA_TRY(launch());
+      if (ker_t) {
+        cudaEvent_t kb = ev_get(B, evk++);
+        CUDA_TRY(cudaEventRecordWithFlags(kb, fs, evflags));
+        B->pending.push_back({100 + kind, ka, kb});
+      }
+      return CDM_OK;
+    };
+    cdm_status st = CDM_OK;
     switch (fam) {
       case F_FP:
-        for (size_t i = 0; i < B->fp.size(); i++) { CUDA_TRY(launch_fp(B->fp[i], B->fp_maxw[i], fs)); n++; B->fam_launches[F_FP]++; }
+        for (size_t i = 0; i < B->fp.size() && !st; i++) {
+          st = timed(K_FP, [&] { return launch_fp(B->fp[i], B->fp_maxw[i], fs); });
+          n++; B->fam_launches[F_FP]++;
+        }
         break;
       case F_SCAN:
-        for (auto& sb : B->scan) { CUDA_TRY(launch_scan(sb, fs)); n++; B->fam_launches[F_SCAN]++; }
+        for (size_t i = 0; i < B->scan.size() && !st; i++) {
+          st = timed(K_SCAN, [&] { return launch_scan(B->scan[i], fs); });
+          n++; B->fam_launches[F_SCAN]++;
+        }
         break;
       case F_RLE:
         // sums -> expand (level-0 batches first); the expansions are programmatically dependent launches
-        for (auto& pb : B->sums) { CUDA_TRY(launch_rle_sums(pb, fs)); n++; B->fam_launches[F_RLE]++; }
-        for (auto& rb : B->rle) {
-          CUDA_TRY(launch_rle(rb, fs));
-          n++;
-          B->fam_launches[F_RLE]++;
-          if (rb.big_enabled) {
-            CUDA_TRY(launch_rle_big(rb, fs));
-            n++;
-            B->fam_launches[F_RLE]++;
+        for (size_t i = 0; i < B->sums.size() && !st; i++) {
+          st = timed(K_RLE_SUMS, [&] { return launch_rle_sums(B->sums[i], fs); });
+          n++; B->fam_launches[F_RLE]++;
+        }
+        for (size_t i = 0; i < B->rle.size() && !st; i++) {
+          auto& rb = B->rle[i];
+          st = timed(i < B->rle_level0 ? K_RLE_L0 : K_RLE_L1, [&] { return launch_rle(rb, fs); });
+          n++; B->fam_launches[F_RLE]++;
+          if (rb.big_enabled && !st) {
+            st = timed(K_RLE_BIG, [&] { return launch_rle_big(rb, fs); });
+            n++; B->fam_launches[F_RLE]++;
           }
         }
         break;
       case F_LZ4:
-        for (size_t i = 0; i < B->lz4.size(); i++) {
-          CUDA_TRY(launch_lz4(B->lz4[i], B->lz4_max_sub[i], fs));
-          n++;
-          B->fam_launches[F_LZ4]++;
+        for (size_t i = 0; i < B->lz4.size() && !st; i++) {
+          st = timed(K_LZ4, [&] { return launch_lz4(B->lz4[i], B->lz4_max_sub[i], fs); });
+          n++; B->fam_launches[F_LZ4]++;
         }
         break;
       case F_COPY:
-        for (auto& c : B->copies) { CUDA_TRY(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, fs)); B->fam_launches[F_COPY]++; }
-        for (void* p : B->zero_offsets) CUDA_TRY(cudaMemsetAsync(p, 0, 4, fs));
+        st = timed(K_COPY, [&] {
+          for (auto& c : B->copies) {
+            cudaError_t ce = cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, fs);
+            if (ce != cudaSuccess) return ce;
+            B->fam_launches[F_COPY]++;
+          }
+          for (void* p : B->zero_offsets) {
+            cudaError_t ce = cudaMemsetAsync(p, 0, 4, fs);
+            if (ce != cudaSuccess) return ce;
+          }
+          return cudaSuccess;
+        });
         break;
     }
-    if (B->timing) {
+    if (st) return st;
+    if (fam_t) {
       cudaEvent_t tb = ev_get(B, evk++);
       CUDA_TRY(cudaEventRecordWithFlags(tb, fs, evflags));
       B->pending.push_back({fam, ta, tb});
@@ -1536,7 +1578,7 @@ extern "C" CDM_API cdm_status cdm_batch_launch(cdm_batch* b, void* stream, uint3
   if (b->graph_pending) {  // the previous replay's timing was not collected: it is lost
     b->graph_pending = false;
   }
-  if (!b->gexec || b->gstream != s || b->graph_timing != b->timing) {
+  if (!b->gexec || b->gstream != s || b->graph_timing != b->timing || b->graph_mode != b->timing_mode) {
     b->drop_graph();
     uint64_t before[5];
     for (int f = 0; f < 5; f++) before[f] = b->fam_launches[f];
@@ -1554,6 +1596,7 @@ extern "C" CDM_API cdm_status cdm_batch_launch(cdm_batch* b, void* stream, uint3
     CUDA_TRY(cudaGraphInstantiate(&b->gexec, g, 0));
     b->gstream = s;
     b->graph_timing = b->timing;
+    b->graph_mode = b->timing_mode;
     b->graph_nl = nl;
     for (int f = 0; f < 5; f++) {
       b->graph_fam_launches[f] = b->fam_launches[f] - before[f];
@@ -1578,7 +1621,8 @@ extern "C" CDM_API cdm_status cdm_batch_collect_timing(cdm_batch* b) {
     CUDA_TRY(cudaEventSynchronize(p.b));
     float ms = 0;
     CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
-    b->fam_ms[p.fam] += ms;
+    if (p.fam >= 100) { b->k_ms[p.fam - 100] += ms; b->k_n[p.fam - 100]++; }
+    else b->fam_ms[p.fam] += ms;
   }
   b->graph_pending = false;
   return CDM_OK;
@@ -1625,7 +1669,8 @@ extern "C" CDM_API cdm_status cdm_batch_results(cdm_batch* b, void* stream, cdm_
   for (auto& p : b->pending) {
     float ms = 0;
     CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
-    b->fam_ms[p.fam] += ms;
+    if (p.fam >= 100) { b->k_ms[p.fam - 100] += ms; b->k_n[p.fam - 100]++; }
+    else b->fam_ms[p.fam] += ms;
   }
   b->pending.clear();
   if (const char* path = std::getenv("CDM_TRACE")) dump_trace(b, path);
@@ -1648,8 +1693,19 @@ extern "C" CDM_API cdm_status cdm_batch_destroy(cdm_batch* b) {
 extern "C" CDM_API cdm_status cdm_batch_set_timing(cdm_batch* b, int enable) {
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   b->timing = enable != 0;
+  b->timing_mode = enable;
   for (int i = 0; i < 5; i++) { b->fam_ms[i] = 0; b->fam_launches[i] = 0; }
+  for (int i = 0; i < kKernelKinds; i++) { b->k_ms[i] = 0; b->k_n[i] = 0; }
   b->pending.clear();
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms8, uint64_t* launches8) {
+  if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
+  for (int i = 0; i < kKernelKinds; i++) {
+    if (ms8) ms8[i] = b->k_ms[i];
+    if (launches8) launches8[i] = b->k_n[i];
+  }
   return CDM_OK;
 }
 

@@ -1,4 +1,5 @@
-"""Per kernel family: DRAM bytes (read + write) per launch from an ncu --set full report -> profiles/ncu_traffic.json.
+"""Per kernel: DRAM bytes (read + write) per step from an ncu --set full report -> profiles/ncu_traffic.json
+(keys = the kernel names bench.py reports: fp_kernel, rle_sums_kernel, rle_kernel(level0), rle_kernel, ...).
 usage: python tools/ncu_traffic.py gpurun_out/prof_X.ncu-rep [out.json]"""
 import csv
 import io
@@ -20,16 +21,19 @@ fam = {"fp_kernel": "fp", "scan_kernel": "scan", "rle_sums_kernel": "rle", "rle_
 acc = {}
 detail = []
 for r in rows[2:]:
-    name = r[k].split("::")[-1].split("(")[0]
-    f = fam.get(name)
-    if not f:
+    full = r[k]
+    name = full.split("::")[-1].split("(")[0].split("<")[0]
+    if name not in fam:
         continue
+    # rle_kernel<TRACE, LIN>: the LIN variant is the level-0 (value lineage) launch in these workloads
+    f = "rle_kernel(level0)" if name == "rle_kernel" and ", 1>" in full else name
     b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]
     acc[f] = acc.get(f, 0) + b
-    detail.append({"kernel": name, "dram_bytes": b, "us": float(r[dur].replace(",", ""))})
+    detail.append({"kernel": f, "dram_bytes": b, "us": float(r[dur].replace(",", ""))})
 res = {f: int(v) for f, v in acc.items()}
 res["_detail"] = detail
 res["_how"] = ("ncu --set full (cache control on: caches flushed before each replayed kernel), one config-2 device "
-               "batch, CDM_SERIAL=1; sum over the family's launches of dram__bytes_read.sum + dram__bytes_write.sum")
+               "batch, CDM_SERIAL=1; per kernel, the sum over its launches of dram__bytes_read.sum + "
+               "dram__bytes_write.sum")
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res, indent=1))
