@@ -9,5 +9,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
    --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 echo "ncu launches rc=$?"
 CDM_SERIAL=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fp_kernel|rle_kernel|rle_sums|scan_kernel|lz4_kernel" \
-   -s 5 -c 5 -o gpurun_out/prof_${TAG} -f python tools/one_batch.py 2 config2 > gpurun_out/ncu_full_${TAG}.log 2>&1
+   -c 4 -o gpurun_out/prof_${TAG} -f python tools/one_batch.py 1 config2 > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "ncu full rc=$?"
