@@ -109,6 +109,134 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_kernel(const __grid_con
   if (bad && lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
 }
 
+// ------------------------------------------------------------------------------------------ lane groups
+// 32/kLzG sub-chunks per warp, kLzG lanes each (default 4: eight sub-chunks per warp; CDM_LZ4_G=8/16): the warp-per-sub-chunk schedule spends ~130
+// warp instructions per LZ4 sequence of ~8 output bytes (31 lanes mostly idle on short sequences); eight
+// lanes match the typical sequence and four groups share every instruction.  Per sequence a group loads one
+// 8-byte window of the compressed stream (one byte per lane) that usually holds the token, the literals and
+// the offset (shuffled out within the group); literal and match bytes are copied 8 per step with
+// out[p + k] = out[p - o + (k mod o)] for overlapping short periods; __syncwarp(group mask) orders a
+// group's stores before its match reads.  Same bounds checks and error bit as lz4_kernel.
+template <uint32_t kLzG>  // lanes per sub-chunk
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 8) lz4_group_kernel(const __grid_constant__ Lz4Batch B) {
+  const uint32_t lane = threadIdx.x & 31, gl = lane & (kLzG - 1);
+  const uint32_t gmask = (kLzG == 32 ? FULL : ((1u << kLzG) - 1u)) << (lane & ~(kLzG - 1));
+  const uint32_t gs = (blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x) / kLzG;
+  if (gs >= B.total_subs) return;  // uniform within a group
+  const Lz4Desc& D = B.d[find_desc_lz4(B, gs)];
+  const uint32_t s = gs - D.sub0;
+  const uint32_t* tab = reinterpret_cast<const uint32_t*>(D.table);
+  uint64_t off = 0;
+  if (D.uniform) {
+    off = uint64_t(s) * D.uniform;
+  } else {
+    for (uint32_t k = gl; k < s; k += kLzG) off += __ldg(tab + 3 * k + 2);
+#pragma unroll
+    for (int o = kLzG / 2; o > 0; o >>= 1) off += __shfl_xor_sync(gmask, off, o, kLzG);
+  }
+  const uint32_t co = __ldg(tab + 3 * s), cl = __ldg(tab + 3 * s + 1), dl = __ldg(tab + 3 * s + 2);
+  bool bad = uint64_t(co) + cl > D.payload_bytes || off + dl > D.n;
+  if (s + 1 == D.n_sub && off + dl != D.n) bad = true;
+  if (bad) {
+    if (gl == 0) atomicOr(B.err + D.err_idx, 0x4u);
+    return;
+  }
+  const uint8_t* __restrict__ in = D.payload + co;
+  uint8_t* out = D.out + off;
+  uint32_t ip = 0, op = 0;
+  for (;;) {
+    if (ip >= cl) { bad = true; break; }
+    // window: compressed bytes [ip, ip + 8), one per lane
+    const uint32_t wb = ip + gl < cl ? uint32_t(__ldg(in + ip + gl)) : 0u;
+    const uint32_t token = __shfl_sync(gmask, wb, 0, kLzG);
+    uint32_t lit = token >> 4;
+    uint32_t q = ip + 1;
+    if (lit == 15) {
+      uint32_t b;
+      do {
+        if (q >= cl) { bad = true; break; }
+        b = __ldg(in + q++);
+        lit += b;
+      } while (b == 255);
+      if (bad) break;
+    }
+    if (lit > cl - q || lit > dl - op) { bad = true; break; }
+    if (q + lit <= ip + kLzG) {  // literals inside the window: lane gl takes window byte (q - ip) + gl
+      const uint32_t v = __shfl_sync(gmask, wb, (q - ip + gl) & (kLzG - 1), kLzG);
+      if (gl < lit) out[op + gl] = uint8_t(v);
+    } else {
+      for (uint32_t k = gl; k < lit; k += kLzG) out[op + k] = __ldg(in + q + k);
+    }
+    q += lit;
+    op += lit;
+    if (q == cl) break;  // the last sequence carries literals only
+    if (cl - q < 2) { bad = true; break; }
+    uint32_t moff;
+    if (q + 2 <= ip + kLzG) {
+      const uint32_t lo = __shfl_sync(gmask, wb, (q - ip) & (kLzG - 1), kLzG);
+      const uint32_t hi = __shfl_sync(gmask, wb, (q - ip + 1) & (kLzG - 1), kLzG);
+      moff = lo | (hi << 8);
+    } else {
+      moff = uint32_t(__ldg(in + q)) | (uint32_t(__ldg(in + q + 1)) << 8);
+    }
+    q += 2;
+    if (moff == 0 || moff > op) { bad = true; break; }
+    uint32_t ml = token & 15;
+    if (ml == 15) {
+      uint32_t b;
+      do {
+        if (q >= cl) { bad = true; break; }
+        b = __ldg(in + q++);
+        ml += b;
+      } while (b == 255);
+      if (bad) break;
+    }
+    ml += 4;
+    if (ml > dl - op) { bad = true; break; }
+    __syncwarp(gmask);  // literal bytes written by the group are visible to its match reads
+    if (moff >= ml) {
+      // no overlap: the whole match is already written -- issue up to 4 batches of loads, then the stores
+      // (one L2 round trip per 4*kLzG bytes instead of one per batch)
+      for (uint32_t base = 0; base < ml; base += 4 * kLzG) {
+        uint32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t k = base + j * kLzG + gl;
+          v[j] = k < ml ? uint32_t(out[op - moff + k]) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t k = base + j * kLzG + gl;
+          if (k < ml) out[op + k] = uint8_t(v[j]);
+        }
+      }
+      __syncwarp(gmask);
+    } else if (moff >= kLzG) {
+      // overlapping, period >= kLzG: the sources of a batch lie before the batch -> batches in order
+      for (uint32_t base = 0; base < ml; base += kLzG) {
+        const uint32_t k = base + gl;
+        if (k < ml) out[op + k] = out[op - moff + k];
+        __syncwarp(gmask);
+      }
+    } else {  // overlapping short period (moff < kLzG): every source byte lies in [op - moff, op)
+      uint32_t m = gl;  // gl mod moff without a division (gl < kLzG <= 16, moff >= 1)
+      while (m >= moff) m -= moff;
+      uint32_t st = kLzG;  // kLzG mod moff
+      while (st >= moff) st -= moff;
+      for (uint32_t k = gl; k < ml; k += kLzG) {
+        out[op + k] = out[op - moff + m];
+        m += st;
+        if (m >= moff) m -= moff;
+      }
+      __syncwarp(gmask);
+    }
+    op += ml;
+    ip = q;
+  }
+  if (!bad && op != dl) bad = true;
+  if (bad && gl == 0) atomicOr(B.err + D.err_idx, 0x4u);
+}
+
 // ------------------------------------------------------------------------------------------ smem decoder
 // Sub-chunks of <= kLz4SmemMax decompressed bytes are decoded into a per-warp shared-memory window: match
 // sources are then shared-memory reads instead of L2 round trips.  Each sequence is parsed from one
@@ -286,6 +414,17 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
     }
     const uint32_t grid = (b.total_subs + wpc - 1) / wpc;
     lz4_smem_kernel<<<grid, wpc * 32, smem, s>>>(b, cap);
+    return cudaGetLastError();
+  }
+  // lane groups (4 sub-chunks per warp) unless CDM_LZ4_WARP=1 selects one warp per sub-chunk
+  static const bool warp_mode = std::getenv("CDM_LZ4_WARP") != nullptr;
+  static const int G = std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 4;
+  if (!warp_mode) {
+    const uint32_t per_cta = kWarpsPerCta * 32 / G;
+    const uint32_t grid = (b.total_subs + per_cta - 1) / per_cta;
+    if (G == 4) lz4_group_kernel<4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else if (G == 16) lz4_group_kernel<16><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else lz4_group_kernel<8><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();
   }
   const uint32_t grid = (b.total_subs + kWarpsPerCta - 1) / kWarpsPerCta;
