@@ -54,6 +54,21 @@ WORKLOADS = {
                                                 ("l_comment", "Str|[LZ4(sub=16384),BitPack]")],
                     desc="config 3: TPC-H SF=10 lineitem string columns (l_shipmode/l_returnflag Dict|BitPack CHAR(n), "
                          "l_comment Str|[LZ4(16 KiB sub-chunks),BitPack])"),
+    # BASELINE configs[3]: every lineitem + orders column with the SURVEY Sec. 8d config-4 cascade map (Table 2
+    # mapped onto the hot-path codecs), at --sf (default 10; the paper's SF=100 needs ~24 GB of pinned host)
+    "config4": dict(sf=10.0, dtype="mixed", cols=[
+        ("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("l_partkey", "BitPack"),
+        ("l_suppkey", "BitPack"), ("l_linenumber", "BitPack"), ("l_quantity", "Dict|BitPack"),
+        ("l_extendedprice", "Float2Int|BitPack"), ("l_discount", "Dict|BitPack"), ("l_tax", "Dict|BitPack"),
+        ("l_returnflag", "Dict|BitPack"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
+        ("l_commitdate", "Dict|BitPack"), ("l_receiptdate", "Dict|BitPack"), ("l_shipinstruct", "Dict|BitPack"),
+        ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384),BitPack]"),
+        ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"), ("o_custkey", "BitPack"), ("o_orderstatus", "Dict|BitPack"),
+        ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"), ("o_orderpriority", "Dict|BitPack"),
+        ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
+        ("o_comment", "Str|[LZ4(sub=16384),BitPack]")],
+                    desc="config 4: TPC-H lineitem + orders, all 25 columns (SURVEY Sec. 8d cascade map: FP / "
+                         "scan / RLE / LZ4 families concurrently)"),
     # BASELINE configs[0]: the oracle-sized parity case (launch-bound: 4 MB decoded)
     "config1": dict(sf=None, dtype="int32", cols=[("config1", "BitPack")],
                     desc="config 1: 1M int32, FOR + 8-bit bit-packing, one chunk"),
@@ -73,21 +88,34 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=2.0, help="wall seconds of the oracle sample")
     p.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
-    return p.parse_args()
+    p.add_argument("--sf", type=float, default=None, help="scale factor override (config 2/3/4)")
+    a = p.parse_args()
+    if a.sf is not None:
+        WORKLOADS[a.workload]["sf"] = a.sf
+    return a
+
+
+def _encode_column(job):
+    """(sf, seed, rank, name, spec) -> (name, spec, dtype, width, chunks, plain bytes); runs in a worker."""
+    sf, seed, rank, name, spec = job
+    from paper_2602_08190_b200 import encoder
+    from paper_2602_08190_b200.inputs import TPCH, config1_column
+    col = config1_column() if name == "config1" else TPCH(sf, seed).column(name)
+    chunks = encoder.encode_chunks(spec, col, CHUNK_ROWS, first_chunk_id=1000 * rank)
+    return (name, spec, col.dtype, col.width, chunks, col.nbytes())
 
 
 def build_workload(rank: int, workload: str = "config2"):
-    """Generate + encode this rank's shard (untimed).  Returns list of (name, spec, dtype, width, chunks)."""
-    from paper_2602_08190_b200 import encoder
-    from paper_2602_08190_b200.inputs import TPCH, MASTER_SEED, config1_column
+    """Generate + encode this rank's shard (untimed), one column per worker process for multi-column
+    workloads.  Returns list of (name, spec, dtype, width, chunks, plain bytes)."""
+    from paper_2602_08190_b200.inputs import MASTER_SEED
     wl = WORKLOADS[workload]
-    g = TPCH(wl["sf"], MASTER_SEED + 1000 * rank) if wl["sf"] else None
-    cols = []
-    for name, spec in wl["cols"]:
-        col = config1_column() if name == "config1" else g.column(name)
-        chunks = encoder.encode_chunks(spec, col, CHUNK_ROWS, first_chunk_id=1000 * rank)
-        cols.append((name, spec, col.dtype, col.width, chunks, col.nbytes()))
-    return cols
+    jobs = [(wl["sf"], MASTER_SEED + 1000 * rank, rank, name, spec) for name, spec in wl["cols"]]
+    if len(jobs) > 3:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+            return pool.map(_encode_column, jobs)
+    return [_encode_column(j) for j in jobs]
 
 
 def load_peaks():
@@ -240,7 +268,9 @@ def main():
                   for (_, _, _, _, chs, _) in cols for c in chs)
     n_chunks = sum(len(chs) for (_, _, _, _, chs, _) in cols)
 
-    eng = cdm.Engine(local, n_slots=4, slot_bytes=64 << 20, order_policy=1)
+    max_chunk = max(int(c.size) for (_, _, _, _, chs, _) in cols for c in chs)
+    slot = max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20))  # a slot holds any one chunk
+    eng = cdm.Engine(local, n_slots=4, slot_bytes=slot, order_policy=1)
     stream = torch.cuda.Stream()
     # the compressed columns live back to back in ONE pinned host buffer (as a column store would keep them)
     sizes = [int(c.size) for (_, _, _, _, chs, _) in cols for c in chs]

@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     bool bad_index = false;
     const bool bytes_path = mode == FP_DICT && ob != 4 && ob != 8;  // CHAR(n) rows
     const bool dsm = DM == 1 && mode == FP_DICT && !bytes_path && entries * ob <= kDictSmemBytes;
-    if (dsm && di != staged_di) {  // uniform: every thread passed the barrier ending the previous tile
+    const bool dsmb = DM == 1 && bytes_path && uint64_t(entries) * ob + 8 <= kDictSmemBytes;
+    if ((dsm || dsmb) && di != staged_di) {  // uniform: every thread passed the barrier ending the previous tile
       const uint4* src = reinterpret_cast<const uint4*>(dict8);
       for (uint32_t q = tid; q < (entries * ob + 15) / 16; q += kThreads) reinterpret_cast<uint4*>(dict_s)[q] = __ldg(src + q);
       __syncthreads();
@@ -203,33 +204,49 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
       }
     }
     if (bytes_path) {
-      // FP_DICT with E-byte rows (E not 4/8): the tile's output (valid*E bytes, 16-aligned since 4096*E is a
-      // multiple of 16) is produced as 16-byte chunks; each thread walks the bytes of its chunk tracking
-      // (row, column) and extracts a row's index only when the row changes.
+      // FP_DICT with E-byte rows (CHAR(n), E not 4/8): the tile's output (valid*E bytes, 16-aligned since
+      // 4096*E is a multiple of 16) is produced as 16-byte chunks of four 32-bit words; each word is
+      // assembled from <= 4 pieces, a piece = the bytes of one row's entry starting at column col read with
+      // one unaligned 4-byte funnel read from the dictionary (shared memory when it fits, else L1/L2); a
+      // row's index is extracted only when the row changes.
       const uint32_t E = ob;
       const uint64_t inv = (0x100000000ull + E - 1) / E;  // ceil(2^32 / E): exact for positions < 2^17
       const uint32_t total = valid * E;
       uint8_t* obase = out8 + tile_start * E;
-      const uint8_t* __restrict__ dict = dict8;
+      auto fetch = [&](uint32_t row) -> uint32_t {
+        const uint64_t f = w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull;
+        if (f >= lim) { bad_index = true; return 0u; }
+        return base32 + uint32_t(f);
+      };
+      const uint32_t* dws = reinterpret_cast<const uint32_t*>(dict_s);
+      const uint32_t* dwg = reinterpret_cast<const uint32_t*>(dict8);
+      auto rd4 = [&](uint32_t off) -> uint32_t {  // dictionary bytes [off, off + 4), any alignment
+        const uint32_t q = off >> 2, sh = (off & 3) * 8;
+        const uint32_t lo = dsmb ? dws[q] : __ldg(dwg + q), hi = dsmb ? dws[q + 1] : __ldg(dwg + q + 1);
+        return __funnelshift_r(lo, hi, sh);
+      };
       for (uint32_t c = tid; c * 16 < total; c += kThreads) {
         const uint32_t p0 = c * 16;
         uint32_t row = uint32_t((uint64_t(p0) * inv) >> 32), col = p0 - row * E;
-        uint64_t idx = base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
-        if (idx >= entries) { bad_index = true; idx = 0; }
-        uint32_t word[4] = {0u, 0u, 0u, 0u};
+        uint32_t idx = fetch(row);
+        uint32_t word[4];
 #pragma unroll
-        for (uint32_t b = 0; b < 16; b++) {
-          if (p0 + b < total) {
-            word[b >> 2] |= uint32_t(__ldg(dict + idx * E + col)) << (8 * (b & 3));
-            if (++col == E) {
+        for (uint32_t j = 0; j < 4; j++) {
+          uint32_t acc = 0, filled = 0;
+          while (filled < 4 && p0 + 4 * j + filled < total) {
+            const uint32_t take = min(4u - filled, E - col);
+            const uint32_t v = rd4(idx * E + col);
+            const uint32_t m = take >= 4 ? 0xFFFFFFFFu : (1u << (8 * take)) - 1u;
+            acc |= (v & m) << (8 * filled);
+            filled += take;
+            col += take;
+            if (col == E) {
               col = 0;
               row++;
-              if (row < valid) {
-                idx = base + (w ? extract_bits(wd, uint64_t(row) * w, w) : 0ull);
-                if (idx >= entries) { bad_index = true; idx = 0; }
-              }
+              if (row < valid) idx = fetch(row);
             }
           }
+          word[j] = acc;
         }
         if (p0 + 16 <= total) {
           st_v4_u32(obase + p0, word[0], word[1], word[2], word[3]);

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_kernel(const __grid_con
 // out[p + k] = out[p - o + (k mod o)] for overlapping short periods; __syncwarp(group mask) orders a
 // group's stores before its match reads.  Same bounds checks and error bit as lz4_kernel.
 template <uint32_t kLzG>  // lanes per sub-chunk
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 8) lz4_group_kernel(const __grid_constant__ Lz4Batch B) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __grid_constant__ Lz4Batch B) {
   const uint32_t lane = threadIdx.x & 31, gl = lane & (kLzG - 1);
   const uint32_t gmask = (kLzG == 32 ? FULL : ((1u << kLzG) - 1u)) << (lane & ~(kLzG - 1));
   const uint32_t gs = (blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x) / kLzG;
@@ -194,7 +194,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 8) lz4_group_kernel(const _
     ml += 4;
     if (ml > dl - op) { bad = true; break; }
     __syncwarp(gmask);  // literal bytes written by the group are visible to its match reads
-    if (moff >= ml) {
+    if (moff >= ml && ml <= 2 * kLzG) {
+      // no overlap, short match (the common case): two loads per lane, then the stores
+      const uint32_t k1 = gl + kLzG;
+      const uint32_t v0 = (kLzG <= 4 || gl < ml) ? uint32_t(out[op - moff + gl]) : 0u;  // ml >= 4
+      const uint32_t v1 = k1 < ml ? uint32_t(out[op - moff + k1]) : 0u;
+      if (kLzG <= 4 || gl < ml) out[op + gl] = uint8_t(v0);
+      if (k1 < ml) out[op + k1] = uint8_t(v1);
+      __syncwarp(gmask);
+    } else if (moff >= ml) {
       // no overlap: the whole match is already written -- issue up to 4 batches of loads, then the stores
       // (one L2 round trip per 4*kLzG bytes instead of one per batch)
       for (uint32_t base = 0; base < ml; base += 4 * kLzG) {
