@@ -43,7 +43,9 @@ constexpr uint32_t kDictSmemBytes = 8192;  // dictionaries up to this size are g
 
 // DM: dictionary gathers from shared memory (1: the tile's dictionary is copied there when the tile's
 // chunk changes) or through the read-only L1 path (0).
-template <int DM>
+// TMA: the tile's packed bytes are staged in shared memory by the TMA engine, double-buffered across the
+// tiles of a persistent CTA (1), or read in place through L1 by each thread, one tile per CTA (0).
+template <int DM, bool TMA>
 __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__ FpBatch B, uint32_t stage_bytes_alloc) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
@@ -52,16 +54,16 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
   const uint32_t tid = threadIdx.x;
   // stage_bytes_alloc: set by the host from the batch's largest w; dynamic smem = 2 stages
 
-  if (tid == 0) {
+  if (TMA && tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  if (TMA) __syncthreads();
 
   uint32_t tile = blockIdx.x;
   // prologue: stage the first tile
-  if (tid == 0 && tile < B.total_tiles) {
+  if (TMA && tid == 0 && tile < B.total_tiles) {
     const int di = find_desc_fp(B, tile);
     const FpDesc& D = B.d[di];
     const uint32_t lt = tile - D.tile0;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
   for (uint32_t it = 0; tile < B.total_tiles; it++, tile += gridDim.x) {
     const uint32_t s = it & 1;
     const uint32_t next = tile + gridDim.x;
-    if (tid == 0 && next < B.total_tiles) {  // stage s^1 was released by the __syncthreads ending it-1
+    if (TMA && tid == 0 && next < B.total_tiles) {  // stage s^1 was released by the __syncthreads ending it-1
       const int dn = find_desc_fp(B, next);
       const FpDesc& Dn = B.d[dn];
       const uint32_t ltn = next - Dn.tile0;
@@ -90,8 +92,9 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     const uint64_t base = D.base;
     const uint8_t* const dict8 = D.dict;
     uint8_t* const out8 = reinterpret_cast<uint8_t*>(D.out);
-    mbar_wait(&bar[s], (it >> 1) & 1);
-    const uint32_t* wd = reinterpret_cast<const uint32_t*>(smem + s * stage_bytes_alloc);
+    if (TMA) mbar_wait(&bar[s], (it >> 1) & 1);
+    const uint32_t* wd = TMA ? reinterpret_cast<const uint32_t*>(smem + s * stage_bytes_alloc)
+                             : reinterpret_cast<const uint32_t*>(D.packed + uint64_t(lt) * (kFpTile / 8) * w);
     const uint64_t tile_start = uint64_t(lt) * kFpTile;
     const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
     bool bad_index = false;
@@ -164,7 +167,8 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
         for (int j = 0; j < 4; j++) {
           const uint64_t f = v[j] - base;
           const bool ok = f < lim;
-          bad_index |= !ok;
+          // fields past the tile's last row decode stale staging bytes: never an error, never stored
+          bad_index |= !ok && i0 + j < valid;
           idx[j] = ok ? base32 + uint32_t(f) : 0u;
         }
         if (dsm && ob == 8) {
@@ -280,11 +284,13 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   const uint32_t stage = ((kFpTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words for extraction
   const uint32_t smem = 2 * stage;
   static const int dm = std::getenv("CDM_FP_DICT") && std::getenv("CDM_FP_DICT")[0] == 'l' ? 0 : 1;
-  auto kern = dm ? fp_kernel<1> : fp_kernel<0>;
-  static uint32_t configured[2] = {0, 0};
-  if (smem > 40 * 1024 && smem > configured[dm]) {
+  static const bool tma = !(std::getenv("CDM_FP_TMA") && std::getenv("CDM_FP_TMA")[0] == '0');
+  auto kern = tma ? (dm ? fp_kernel<1, true> : fp_kernel<0, true>) : (dm ? fp_kernel<1, false> : fp_kernel<0, false>);
+  static uint32_t configured[4] = {0, 0, 0, 0};
+  const int ci = dm + 2 * tma;
+  if (tma && smem > 40 * 1024 && smem > configured[ci]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured[dm] = smem;
+    configured[ci] = smem;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
@@ -295,11 +301,12 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   static const int cap = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 2;
   if (cap > 0 && cap < per_sm) per_sm = cap;
   uint32_t grid = uint32_t(device_sms() * per_sm);
+  if (!tma) grid = b.total_tiles;  // one tile per CTA, read in place
   // CDM_FP_GRID=tiles: one CTA per tile (no persistence), so CTAs of a concurrent higher-priority family
   // are scheduled as soon as any FP CTA retires
   static const bool per_tile = std::getenv("CDM_FP_GRID") && std::getenv("CDM_FP_GRID")[0] == 't';
   if (per_tile || grid > b.total_tiles) grid = b.total_tiles;
-  kern<<<grid, kThreads, smem, s>>>(b, stage);
+  kern<<<grid, kThreads, tma ? smem : 0, s>>>(b, stage);
   return cudaGetLastError();
 }
 

@@ -452,3 +452,51 @@ def test_pipeline_relaunch_and_error_positions(engine):
     with pytest.raises(cdm.CdmError):
         p.results()
     p.close()
+
+
+# ------------------------------------------------------------------------------ every family in one graph
+def test_all_families_one_batch_graph_and_timing(engine):
+    """All 25 lineitem/orders cascades (config 4's map) in ONE device batch: FP, scan, RLE (two-level
+    value lineage + big runs) and LZ4 run concurrently inside one captured graph; replays and the
+    per-kernel timing mode (families serialised, events per launch) must not change a byte."""
+    import bench
+    g = TPCH(0.005)
+    chunks_all, decs, bufs = [], [], []
+    for name, spec in bench.WORKLOADS["config4"]["cols"]:
+        col = g.column(name)
+        casc = cdm.Cascade(spec, col.dtype, col.width)
+        for ch in encoder.encode_chunks(spec, col, 9_999):
+            out, offs, info = _outputs(ch)
+            decs.append(cdm.Decode(casc, cdm.pinned(ch), out, offs, dev_chunk=torch.from_numpy(ch).cuda()))
+            bufs.append((out, offs, info))
+            chunks_all.append(ch)
+    b = cdm.Batch(engine, decs)
+    b.set_graph(True)
+    stream = torch.cuda.Stream()
+    for mode in (0, 1, 2, 0):
+        b.set_timing(mode)
+        for out, offs, _ in bufs:
+            out.fill_(SENTINEL)
+            if offs is not None:
+                offs.fill_(-7)
+        torch.cuda.synchronize()
+        b.launch(stream)
+        b.collect_timing()
+        res = b.results(stream, raise_on_error=False)
+        bad = [(i, r["error_bits"]) for i, r in enumerate(res) if r["error_bits"]]
+        assert not bad, f"mode {mode}: error bits {bad}"
+        for ch, (out, offs, info) in zip(chunks_all, bufs):
+            exp, exp_offs = oracle.decode_chunk(ch)
+            got = out.cpu().numpy()[: exp.size]
+            assert np.array_equal(got, exp), f"mode {mode}: payload differs"
+            if exp_offs is not None:
+                assert np.array_equal(offs.cpu().numpy()[: exp_offs.size], exp_offs)
+        if mode == 2:
+            kt = b.kernel_times()
+            for k in ("fp_kernel", "scan_kernel", "rle_sums_kernel", "rle_kernel(level0)", "rle_kernel",
+                      "lz4_kernel"):
+                assert kt[k][1] >= 1 and kt[k][0] > 0, k
+        if mode == 1:
+            km = b.kernel_ms()
+            assert all(km[f][0] > 0 for f in ("fp", "scan", "rle", "lz4"))
+    b.close()
