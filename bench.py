@@ -60,15 +60,19 @@ WORKLOADS = {
         ("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("l_partkey", "BitPack"),
         ("l_suppkey", "BitPack"), ("l_linenumber", "BitPack"), ("l_quantity", "Dict|BitPack"),
         ("l_extendedprice", "Float2Int|BitPack"), ("l_discount", "Dict|BitPack"), ("l_tax", "Dict|BitPack"),
-        ("l_returnflag", "Dict|BitPack"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
+        ("l_returnflag", "ANS"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
         ("l_commitdate", "Dict|BitPack"), ("l_receiptdate", "Dict|BitPack"), ("l_shipinstruct", "Dict|BitPack"),
         ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384),BitPack]"),
         ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"), ("o_custkey", "BitPack"), ("o_orderstatus", "Dict|BitPack"),
         ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"), ("o_orderpriority", "Dict|BitPack"),
         ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
         ("o_comment", "Str|[LZ4(sub=16384),BitPack]")],
-                    desc="config 4: TPC-H lineitem + orders, all 25 columns (SURVEY Sec. 8d cascade map: FP / "
-                         "scan / RLE / LZ4 families concurrently)"),
+                    desc="config 4: TPC-H lineitem + orders, all 25 columns (SURVEY Sec. 8d cascade map, "
+                         "l_returnflag ANS per Table 2: FP / scan / RLE / LZ4 / ANS kernels concurrently)"),
+    # NEXT-1 microbenchmark: the paper's ANS instance -- an L_RETURNFLAG-distributed byte
+    # column under chunk-sequential range ANS (4 KiB chunks, one thread per chunk)
+    "ans": dict(sf=10.0, dtype="u8", cols=[("l_returnflag", "ANS(chunk=4096)"), ("l_linestatus", "ANS(chunk=4096)")],
+                desc="ANS: TPC-H lineitem l_returnflag + l_linestatus CHAR(1) under range ANS (4 KiB chunks)"),
     # BASELINE configs[0]: the oracle-sized parity case (launch-bound: 4 MB decoded)
     "config1": dict(sf=None, dtype="int32", cols=[("config1", "BitPack")],
                     desc="config 1: 1M int32, FOR + 8-bit bit-packing, one chunk"),
@@ -402,7 +406,7 @@ def main():
         # dominant kernel by device time; algorithmic bytes = compressed read + decoded written (Eq. 1) of
         # the chunks that kernel decodes
         fam_ms = {FAMILY_NAMES[i]: kern[FAMILY_NAMES[i]] for i in range(5)}
-        fam_bytes = {"fp": 0, "scan": 0, "rle": 0, "lz4": 0, "copy": 0}
+        fam_bytes = {"fp": 0, "scan": 0, "rle": 0, "lz4": 0, "copy": 0}  # lz4 = the chunk-sequential family
         for d in decs_dev:
             info = cdm.chunk_info(d.host_chunk)
             plan = d.cascade.describe().split(" => ")[1]
@@ -410,13 +414,16 @@ def main():
                 fam_bytes["rle"] += info["compressed_bytes"] + info["payload_bytes"]
             elif plan.startswith("fp"):
                 fam_bytes["fp"] += info["compressed_bytes"] + info["payload_bytes"]
-            elif "lz4" in plan:  # Str: the scan writes the offsets, the LZ4 kernel the payload bytes
+            elif "lz4" in plan or "ans" in plan:  # Str: the scan writes the offsets, LZ4/ANS the bytes
                 fam_bytes["scan"] += info["offsets_bytes"]
                 fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
+                fam_bytes["ans" if "ans" in plan else "lz4x"] = fam_bytes.get("ans" if "ans" in plan else "lz4x", 0) + \
+                    info["compressed_bytes"] + info["payload_bytes"]
             else:
                 fam_bytes["copy"] += info["compressed_bytes"] + info["payload_bytes"]
         kbytes = {"fp_kernel": fam_bytes["fp"], "scan_kernel": fam_bytes["scan"], "rle_kernel": fam_bytes["rle"],
-                  "lz4_kernel": fam_bytes["lz4"], "device_copy": fam_bytes["copy"]}
+                  "lz4_kernel": fam_bytes.get("lz4x", 0), "ans_kernel": fam_bytes.get("ans", 0),
+                  "device_copy": fam_bytes["copy"]}
         dom = max(ktimes, key=lambda k: ktimes[k][0])
         dom_ms, dom_n = ktimes[dom]
         per_step_ms = dom_ms / tsteps

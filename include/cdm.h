@@ -70,6 +70,7 @@ typedef enum {
 #define CDM_ERR_LZ4 0x4u          /* malformed LZ4 block: offset 0 / before start, over-run, truncation */
 #define CDM_ERR_LENGTHS 0x8u      /* VARBYTES lengths do not sum to the payload size */
 #define CDM_ERR_WIDTH 0x10u       /* a bit width unusable for the stream it packs */
+#define CDM_ERR_ANS 0x20u         /* an ANS chunk does not end at the initial state with every word read */
 
 typedef struct cdm_engine cdm_engine;
 typedef struct cdm_cascade cdm_cascade;
@@ -192,10 +193,10 @@ CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
  *   2 RLE (H7), 3 LZ4 (H8), 4 raw copies;
  * cdm_batch_kernel_times() -> per-kernel milliseconds and launches (mode 2): index 0 fp_kernel,
  *   1 scan_kernel, 2 rle_sums_kernel, 3 rle_kernel level 0 (value lineage), 4 rle_kernel, 5 rle_big_kernel,
- *   6 lz4_kernel, 7 device copies. */
+ *   6 lz4_kernel, 7 device copies, 8 ans_kernel (arrays of 9). */
 CDM_API cdm_status cdm_batch_set_timing(cdm_batch *b, int enable);
 CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch *b, double *ms5, uint64_t *launches5);
-CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms8, uint64_t *launches8);
+CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms9, uint64_t *launches9);
 /* Graph mode + timing: every replay re-records the same events, so call this after each launch (it
  * waits for that replay) to accumulate its per-family times; a replay not collected is not counted. */
 CDM_API cdm_status cdm_batch_collect_timing(cdm_batch *b);

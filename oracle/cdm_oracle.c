@@ -16,6 +16,12 @@
  *                  times; presum = cumsum(count) must end at n.
  *   LZ4            PAPER.md:179 (LZ77 family), :258-259 (Non-Parallel, independent chunks): the LZ4
  *                  block format, decoded byte by byte, one independent sub-chunk at a time.
+ *   ANS            PAPER.md:176 (entropy family), :260 ("each intermediate decode state ... depends on its
+ *                  predecessor", sequential within a chunk), reading R32: range
+ *                  ANS, state x in [2^16, 2^32); per symbol slot = x mod 2^tl, the symbol s with
+ *                  cum_s <= slot < cum_s + f_s (found by a linear scan), x = f_s (x div 2^tl) + slot - cum_s,
+ *                  then while x < 2^16: x = x*2^16 + next word; a chunk must end at x = 2^16 with every word
+ *                  read.
  *   Str            DESIGN.md reading R17: offsets_0 = 0, offsets_{i+1} = offsets_i + len_i.
  *   Nesting        PAPER.md:509 (Table 2 notation), decoded depth-first: children first, then parent
  *                  (no fusion exists in the oracle).
@@ -34,7 +40,7 @@
 
 /* oracle's own constants (the format spec is DESIGN.md's, restated here independently) */
 #define O_MAGIC 0x314D4443u
-enum { OC_RAW = 0, OC_BITPACK = 1, OC_DICT = 2, OC_FLOAT2INT = 3, OC_DELTA = 4, OC_RLE = 5, OC_LZ4 = 6, OC_STR = 7 };
+enum { OC_RAW = 0, OC_BITPACK = 1, OC_DICT = 2, OC_FLOAT2INT = 3, OC_DELTA = 4, OC_RLE = 5, OC_LZ4 = 6, OC_STR = 7, OC_ANS = 8 };
 enum { OT_I32 = 0, OT_I64 = 1, OT_F64 = 2, OT_FIXED = 3, OT_VARBYTES = 4 };
 enum { OK = 0, ERR_ARG = 1, ERR_UNSUPPORTED = 3, ERR_CORRUPT = 4, ERR_CAPACITY = 5, ERR_OOM = 7 };
 
@@ -283,6 +289,50 @@ static int decode_node(ochunk *c, uint32_t *idx, ostream *out) {
     out->n = n; out->eb = 1; out->is_int = 0; out->data = o;
     return OK;
   }
+  case OC_ANS: {
+    if (nch != 2) return bad(c, "node %llu: ANS needs 2 children, has %llu", me, nch);
+    uint32_t nchunks = rd32(pr), chunk = rd32(pr + 4), tl = pr[8];
+    if (tl < 8 || tl > 15 || chunk == 0) return bad(c, "node %llu: ANS params (table log %llu)", me, tl);
+    ostream wds, tab;
+    int rc = decode_node(c, idx, &wds);
+    if (rc) return rc;
+    rc = decode_node(c, idx, &tab);
+    if (rc) { free(wds.data); return rc; }
+    if (wds.eb != 2 || tab.eb != 1 || tab.n != 512 + 12ull * nchunks || (uint64_t)nchunks * chunk < n ||
+        (n && (uint64_t)(nchunks - 1) * chunk >= n) || (!n && nchunks)) {
+      free(wds.data); free(tab.data); return bad(c, "node %llu: ANS streams malformed (%llu)", me, tab.n);
+    }
+    const uint64_t M = 1ull << tl, L = 1ull << 16;
+    uint64_t f[256], cum[256], acc = 0;
+    for (int sy = 0; sy < 256; sy++) { f[sy] = rd16(tab.data + 2 * sy); cum[sy] = acc; acc += f[sy]; }
+    if (n && acc != M) { free(wds.data); free(tab.data); return bad(c, "node %llu: ANS frequencies sum to %llu", me, acc); }
+    uint8_t *o = (uint8_t *)alloc_n(n, 1);
+    if (!o) { free(wds.data); free(tab.data); return bad(c, "node %llu: cannot hold %llu bytes", me, n); }
+    for (uint32_t k = 0; k < nchunks; k++) {
+      const uint8_t *ce = tab.data + 512 + 12ull * k;
+      uint64_t w0 = rd32(ce), nw = rd32(ce + 4), x = rd32(ce + 8);
+      if (w0 + nw > wds.n) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: words beyond the stream (%llu)", k, w0 + nw); }
+      uint64_t pos = 0;
+      const uint64_t i0 = (uint64_t)k * chunk, i1 = i0 + chunk < n ? i0 + chunk : n;
+      for (uint64_t i = i0; i < i1; i++) {
+        const uint64_t slot = x % M;
+        int sy = 0;
+        while (sy < 256 && !(cum[sy] <= slot && slot < cum[sy] + f[sy])) sy++;
+        if (sy == 256) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: no symbol for slot %llu", k, slot); }
+        o[i] = (uint8_t)sy;
+        x = f[sy] * (x / M) + slot - cum[sy];
+        while (x < L) {
+          if (pos >= nw) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: words exhausted at byte %llu", k, i); }
+          x = (x << 16) | rd16(wds.data + 2 * (w0 + pos));
+          pos++;
+        }
+      }
+      if (x != L || pos != nw) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: final state %llu", k, x); }
+    }
+    free(wds.data); free(tab.data);
+    out->n = n; out->eb = 1; out->is_int = 0; out->data = o;
+    return OK;
+  }
   default:
     return bad(c, "node %llu: codec %llu not decodable here", me, codec);
   }
@@ -355,12 +405,14 @@ EXPORT int oracle_decode_chunk(const void *chunk, size_t bytes, void *out, size_
   } else {
     ostream r;
     if ((rc = decode_node(&c, &idx, &r))) return res->status = rc;
-    if (r.n != rows) { free(r.data); snprintf(res->detail, 200, "root decodes %llu of %llu rows", (unsigned long long)r.n, (unsigned long long)rows); return res->status = ERR_CORRUPT; }
+    /* a byte-stream root (ANS over FIXED(W) rows) decodes rows * W one-byte elements */
+    const int byte_root = !r.is_int && r.eb == 1 && W > 1 && r.n == rows * W;
+    if (r.n != rows && !byte_root) { free(r.data); snprintf(res->detail, 200, "root decodes %llu of %llu rows", (unsigned long long)r.n, (unsigned long long)rows); return res->status = ERR_CORRUPT; }
     if (payload != rows * W || out_cap < payload) { free(r.data); snprintf(res->detail, 200, "output capacity / payload size"); return res->status = ERR_CAPACITY; }
     uint8_t *o = (uint8_t *)out;
     if (r.is_int && W <= 8) {
       for (uint64_t i = 0; i < rows; i++) memcpy(o + i * W, r.data + 8 * i, W); /* low W bytes (LE) */
-    } else if (!r.is_int && r.eb == W) {
+    } else if (!r.is_int && (r.eb == W || byte_root)) {
       if (payload) memcpy(o, r.data, payload);
     } else {
       free(r.data); snprintf(res->detail, 200, "root element width %u != dtype width %u", r.eb, W); return res->status = ERR_CORRUPT;

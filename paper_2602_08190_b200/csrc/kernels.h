@@ -184,6 +184,28 @@ struct Lz4Batch {
   Lz4Desc d[kMaxBatch];
 };
 
+// ---------------------------------------------------------------- NEXT-1: chunk-sequential range ANS
+struct AnsDesc {
+  const uint16_t* words;   // 16-bit renormalisation words of all ANS chunks, each chunk's in decode order
+  const uint8_t* table;    // 256 x u16 frequencies, then per chunk {u32 first word, u32 words, u32 state}
+  uint8_t* out;            // decoded bytes
+  uint64_t n;              // decoded bytes
+  uint64_t n_words;
+  uint32_t nchunks;
+  uint32_t chunk;          // bytes per ANS chunk (multiple of 16)
+  uint32_t tile0;          // first global tile (kThreads chunks per tile)
+  uint32_t err_idx;
+  uint32_t tl;             // table log (8..12)
+  uint32_t pad;
+};
+
+struct AnsBatch {
+  uint32_t n;
+  uint32_t total_tiles;
+  uint32_t* err;
+  AnsDesc d[kMaxBatch];
+};
+
 // ---------------------------------------------------------------- launchers (return cudaGetLastError)
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
@@ -191,6 +213,7 @@ cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);
+cudaError_t launch_ans(const AnsBatch& b, cudaStream_t s);
 // engine bookkeeping: zero a 16-byte-aligned scratch prefix; move error words into mapped pinned memory
 // (copy, then zero them for the next launch)
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);

@@ -1,0 +1,118 @@
+// kernels_ans.cu -- NEXT-1: chunk-sequential ("Non-Parallel") range-ANS decode.
+//
+// "Each intermediate decode state in ANS depends on its predecessor ... opportunities for
+// parallelism arise by grouping their intermediate decode states from different chunks and dispatching
+// them in a SIMT manner".  This kernel is exactly that schedule: ONE THREAD PER ANS CHUNK, a warp advances
+// 32 independent chunk states in lockstep.  Format (reading R32): range ANS
+// with a 32-bit state x in [2^16, 2^32), 16-bit renormalisation words, one frequency table normalised to
+// 2^tl shared by the chunks of a CDM1 chunk; each ANS chunk stores its initial decoder state, its words in
+// decode order, and must end at state 2^16 with every word consumed (else CDM_ERR_ANS = 0x20).
+//
+// B200 shape: a CTA takes 256 consecutive chunks of one column chunk; it first expands the shared table
+// into a shared-memory slot table (2^tl packed entries {symbol, f - 1, slot - cum}, tl <= 12), so the
+// per-symbol step is one shared load + a multiply-add; every thread gathers 4 decoded bytes into a
+// register and writes them with one 4-byte store.
+#include "device_util.cuh"
+#include "kernels.h"
+
+namespace cdm {
+namespace {
+
+using namespace dev;
+
+constexpr uint32_t kAnsMaxTl = 12;
+
+__device__ __forceinline__ int find_desc_ans(const AnsBatch& B, uint32_t tile) {
+  int lo = 0, hi = int(B.n) - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (B.d[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ AnsBatch B) {
+  __shared__ uint32_t tab_s[1u << kAnsMaxTl];  // slot -> sym | (f - 1) << 8 | (slot - cum) << 20
+  __shared__ uint32_t cum_s[257];
+  __shared__ uint64_t warp_s[kThreads / 32];
+  const uint32_t tid = threadIdx.x;
+  const AnsDesc& D = B.d[find_desc_ans(B, blockIdx.x)];
+  const uint32_t tl = D.tl, M = 1u << tl;
+  const uint8_t* const table = D.table;
+  // cumulative frequencies (block scan of the 256 u16 frequencies)
+  {
+    const uint32_t f = tid < 256 ? uint32_t(__ldg(reinterpret_cast<const uint16_t*>(table) + tid)) : 0u;
+    uint64_t tot;
+    const uint32_t ex = uint32_t(block_excl_scan_u64<kThreads>(f, warp_s, &tot));
+    if (tid < 256) cum_s[tid] = ex;
+    if (tid == 0) cum_s[256] = uint32_t(tot);
+  }
+  __syncthreads();
+  const bool table_ok = cum_s[256] == M;
+  // slot table: the symbol of each slot (binary search over cum), its frequency and its offset in the range
+  for (uint32_t slot = tid; slot < M; slot += kThreads) {
+    uint32_t lo = 0, hi = 255;
+    while (lo < hi) {  // last symbol with cum <= slot
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (cum_s[mid] <= slot) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t f = cum_s[lo + 1] - cum_s[lo];
+    tab_s[slot] = lo | ((f - 1u) & 0xFFFu) << 8 | (slot - cum_s[lo]) << 20;
+  }
+  __syncthreads();
+  const uint32_t c = (blockIdx.x - D.tile0) * kThreads + tid;  // this thread's chunk
+  if (c >= D.nchunks) return;
+  bool bad = !table_ok;
+  const uint8_t* ce = table + 512 + 12ull * c;
+  const uint32_t w0 = __ldg(reinterpret_cast<const uint32_t*>(ce)), nw = __ldg(reinterpret_cast<const uint32_t*>(ce + 4));
+  uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(ce + 8));
+  if (uint64_t(w0) + nw > D.n_words) bad = true;
+  const uint64_t i0 = uint64_t(c) * D.chunk;
+  const uint32_t len = uint32_t(min(uint64_t(D.chunk), D.n - i0));
+  const uint16_t* __restrict__ wp = D.words + w0;
+  uint32_t pos = 0;
+  uint8_t* out = D.out + i0;
+  const uint32_t mask = M - 1u;
+  if (!bad) {
+    uint32_t i = 0;
+    for (; i + 4 <= len; i += 4) {  // 4 symbols -> one 4-byte store (chunks are 16-byte multiples)
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint32_t e = tab_s[x & mask];
+        word |= (e & 0xFFu) << (8 * j);
+        x = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+        if (x < (1u << 16)) {  // one step suffices: x >= 2^(16 - tl) here, tl <= 12
+          const uint32_t v = pos < nw ? uint32_t(__ldg(wp + pos)) : 0u;
+          bad |= pos >= nw;
+          pos++;
+          x = (x << 16) | v;
+        }
+      }
+      *reinterpret_cast<uint32_t*>(out + i) = word;
+    }
+    for (; i < len; i++) {  // the column chunk's ragged tail
+      const uint32_t e = tab_s[x & mask];
+      out[i] = uint8_t(e & 0xFFu);
+      x = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+      if (x < (1u << 16)) {
+        const uint32_t v = pos < nw ? uint32_t(__ldg(wp + pos)) : 0u;
+        bad |= pos >= nw;
+        pos++;
+        x = (x << 16) | v;
+      }
+    }
+    if (x != (1u << 16) || pos != nw) bad = true;
+  }
+  if (bad) atomicOr(B.err + D.err_idx, 0x20u);
+}
+
+}  // namespace
+
+cudaError_t launch_ans(const AnsBatch& b, cudaStream_t s) {
+  if (!b.total_tiles) return cudaSuccess;
+  ans_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
+  return cudaGetLastError();
+}
+
+}  // namespace cdm

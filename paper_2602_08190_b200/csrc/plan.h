@@ -37,6 +37,7 @@ inline int codec_from_name(const std::string& raw) {
   if (b == "rle") return RLE;
   if (b == "lz4") return LZ4;
   if (b == "str" || b == "string" || b == "varchar") return STR;
+  if (b == "ans" || b == "rans") return ANS;
   return -1;
 }
 
@@ -107,7 +108,8 @@ inline bool complete_tree(TNode* t, std::string* err) {
       if (k.size() != 1 || k[0]->codec != RAW) { *err = "arity error: BitPack's only child is Raw"; return false; }
       return true;
     case LZ4:
-      if (!k.empty()) { *err = "arity error: LZ4 takes no children"; return false; }
+    case ANS:
+      if (!k.empty()) { *err = "arity error: LZ4/ANS take no children"; return false; }
       k.push_back(mk_raw());
       k.push_back(mk_raw());
       return true;
@@ -136,8 +138,8 @@ inline bool complete_tree(TNode* t, std::string* err) {
 }
 
 inline const char* codec_name(uint8_t c) {
-  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR"};
-  return c < 8 ? N[c] : "?";
+  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS"};
+  return c < 9 ? N[c] : "?";
 }
 
 inline void render_tree(const TNode* t, std::string* out) {
@@ -160,13 +162,14 @@ inline uint64_t fnv1a64(const std::string& s) {
 }
 
 // ------------------------------------------------------------------ fused plans
-enum class PlanKind : uint8_t { RawCopy, Fp, Scan, Rle, Str };
+enum class PlanKind : uint8_t { RawCopy, Fp, Scan, Rle, Str, Ans };
 
 struct Plan {
   PlanKind kind = PlanKind::RawCopy;
   uint8_t fp_mode = 0;   // FpMode
   uint8_t vmode = 0;     // RleValueMode
   bool str_lz4 = false;
+  bool str_ans = false;
   std::string text;      // human-readable fused plan
 };
 
@@ -176,14 +179,23 @@ inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* er
   auto bp = [&](const TNode* t) { return is(t, BITPACK); };
   auto kid = [](const TNode* t, size_t i) -> const TNode* { return i < t->kids.size() ? t->kids[i].get() : nullptr; };
   if (dtype == T_VARBYTES) {
-    if (is(r, STR) && bp(kid(r, 1)) && (is(kid(r, 0), LZ4) || is(kid(r, 0), RAW))) {
+    if (is(r, STR) && bp(kid(r, 1)) && (is(kid(r, 0), LZ4) || is(kid(r, 0), RAW) || is(kid(r, 0), ANS))) {
       p->kind = PlanKind::Str;
       p->str_lz4 = is(kid(r, 0), LZ4);
-      p->text = p->str_lz4 ? "scan_offsets(unpack lengths) + lz4_warp_decode" : "scan_offsets(unpack lengths) + copy";
+      p->str_ans = is(kid(r, 0), ANS);
+      p->text = p->str_lz4 ? "scan_offsets(unpack lengths) + lz4_group_decode"
+              : p->str_ans ? "scan_offsets(unpack lengths) + ans_chunk_decode"
+                           : "scan_offsets(unpack lengths) + copy";
       return true;
     }
-    *err = "VARBYTES needs Str|[LZ4,BitPack] or Str|[Raw,BitPack]";
+    *err = "VARBYTES needs Str|[LZ4,BitPack], Str|[ANS,BitPack] or Str|[Raw,BitPack]";
     return false;
+  }
+  if (is(r, ANS)) {
+    if (dtype != T_FIXED) { *err = "an ANS root needs a FIXED(n) byte column"; return false; }
+    p->kind = PlanKind::Ans;
+    p->text = "ans_chunk_decode (one chunk per thread, SIMT)";
+    return true;
   }
   if (is(r, STR) || is(r, LZ4)) { *err = "Str/LZ4 roots need a VARBYTES column"; return false; }
   if (is(r, RAW)) { p->kind = PlanKind::RawCopy; p->text = "copy"; return true; }
@@ -207,7 +219,7 @@ inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* er
     if (is(v, FLOAT2INT) && bp(kid(v, 0))) { p->vmode = 2; p->text = "rle(values = float2int fused, look-back, expand)"; return true; }
     if (is_delta_rle(v)) {
       p->vmode = 3;
-      p->text = "inner_scan(delta|rle run table) + rle(values = closed form, look-back, expand)";
+      p->text = "rle level 0 (inner Delta|RLE -> run values in L2) + rle level 1 (expand, values = level-0 array)";
       return true;
     }
   }

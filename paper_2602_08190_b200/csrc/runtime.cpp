@@ -136,6 +136,9 @@ struct Bound {
   bool lz4 = false;
   uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
   uint32_t n_sub = 0, lz_sub_bytes = 0, lz_uniform = 0;
+  bool ans = false;  // NEXT-1: the bytes come from a range-ANS node (Str child or FIXED root)
+  uint64_t ans_w_off = 0, ans_w_n = 0, ans_tab_off = 0, ans_n = 0;
+  uint32_t ans_nchunks = 0, ans_chunk = 0, ans_tl = 0;
   const uint8_t* dev_chunk = nullptr;
   void* out = nullptr;
   void* offs = nullptr;
@@ -212,8 +215,8 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
   size_t idx = 0;
   if (c.nodes.empty() || t.walk(&idx) != 0 || idx != c.nodes.size()) return fail(CDM_E_CORRUPT, t.err.empty() ? "node table: unused nodes" : t.err);
   for (size_t i = 0; i < c.nodes.size(); i++) {
-    static const int arity[8] = {0, 1, 2, 1, 1, 2, 2, 2};
-    if (c.nodes[i].codec > STR || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
+    static const int arity[9] = {0, 1, 2, 1, 1, 2, 2, 2, 2};
+    if (c.nodes[i].codec > ANS || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
       return fail(CDM_E_CORRUPT, "node " + std::to_string(i) + ": bad codec or arity");
   }
   std::string canon;
@@ -233,10 +236,30 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
   b->chunk_id = c.chunk_id;
   b->W = W;
   const Node& r = c.nodes[0];
-  if (r.n != c.rows) return fail(CDM_E_CORRUPT, "root element count != rows");
+  // an ANS root decodes rows * W bytes of a FIXED(W) column
+  if (r.n != (b->kind == PlanKind::Ans ? c.rows * W : c.rows)) return fail(CDM_E_CORRUPT, "root element count != rows");
   if (c.dtype != T_VARBYTES && c.payload_bytes != c.rows * W) return fail(CDM_E_CORRUPT, "payload bytes != rows * width");
   auto bad = [&](const std::string& m) { return fail(CDM_E_CORRUPT, m); };
   auto need_w48 = [&]() { return W == 4 || W == 8; };
+  // range-ANS node ni: [words (u16), table (256 x u16 freqs + 12 B per chunk)], params {chunks, chunk bytes, tl}
+  auto bind_ans = [&](int ni) -> cdm_status {
+    const Node& an = c.nodes[ni];
+    uint64_t tn;
+    if (!(e = raw_stream(c, t, t.kids[ni][0], 2, &b->ans_w_off, &b->ans_w_n)).empty()) return bad(e);
+    if (!(e = raw_stream(c, t, t.kids[ni][1], 1, &b->ans_tab_off, &tn)).empty()) return bad(e);
+    b->ans = true;
+    b->ans_n = an.n;
+    b->ans_nchunks = an.u32_at0();
+    b->ans_chunk = an.u32_at4();
+    b->ans_tl = an.params[8];
+    if (b->ans_tl < 8 || b->ans_tl > 15) return bad("ANS table log out of range");
+    if (b->ans_tl > 12) return fail(CDM_E_UNSUPPORTED, "ANS table log > 12 (device slot table)");
+    if (!b->ans_chunk || b->ans_chunk % 16) return bad("ANS chunk size not a positive multiple of 16");
+    if (tn != 512 + 12ull * b->ans_nchunks) return bad("ANS table size");
+    const uint64_t cap = uint64_t(b->ans_nchunks) * b->ans_chunk;
+    if (cap < an.n || (an.n && cap - b->ans_chunk >= an.n) || (!an.n && b->ans_nchunks)) return bad("ANS chunk count");
+    return CDM_OK;
+  };
 
   switch (b->kind) {
     case PlanKind::RawCopy: {
@@ -316,6 +339,11 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
       }
       break;
     }
+    case PlanKind::Ans: {
+      cdm_status st = bind_ans(0);
+      if (st) return st;
+      break;
+    }
     case PlanKind::Str: {
       if (c.offsets_bytes != 4 * (c.rows + 1)) return bad("offsets bytes != 4 * (rows + 1)");
       if (c.payload_bytes >= (1ull << 31)) return fail(CDM_E_UNSUPPORTED, "VARBYTES payload >= 2^31 per chunk");
@@ -323,7 +351,10 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
       if (!(e = bind_bp(c, t, li, c.rows, 64, &b->main)).empty()) return bad(e);
       const Node& bn = c.nodes[bi];
       if (bn.n != c.payload_bytes) return bad("Str bytes count != payload bytes");
-      if (bn.codec == LZ4) {
+      if (bn.codec == ANS) {
+        cdm_status st = bind_ans(bi);
+        if (st) return st;
+      } else if (bn.codec == LZ4) {
         b->lz4 = true;
         uint64_t pn, tn;
         if (!(e = raw_stream(c, t, t.kids[bi][0], 1, &b->lz_pay_off, &pn)).empty()) return bad(e);
@@ -393,7 +424,7 @@ static int fam_priority(int f, int lo, int hi) {
 }
 
 // kernel kinds of cdm_batch_kernel_times (include/cdm.h)
-enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, kKernelKinds };
+enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, K_ANS, kKernelKinds };
 
 struct cdm_batch {
   cdm_engine* e = nullptr;
@@ -407,6 +438,7 @@ struct cdm_batch {
   size_t rle_level0 = 0;  // rle[0, rle_level0) are level-0 (Delta|RLE value lineage) launches
   std::vector<Lz4Batch> lz4;
   std::vector<uint32_t> lz4_max_sub;
+  std::vector<AnsBatch> ans;  // runs on the chunk-sequential (LZ4) family stream
   struct Copy { void* dst; const void* src; size_t bytes; };
   std::vector<Copy> copies;
   std::vector<void*> zero_offsets;  // VARBYTES with rows == 0: offsets[0] = 0
@@ -468,10 +500,11 @@ namespace {
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
   B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
+  B->ans.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
   B->err_dev = B->err_external ? B->err_external : A.take<uint32_t>(nj ? nj : 1);
-  std::vector<int> fpj, scj, rlj, lzj;
+  std::vector<int> fpj, scj, rlj, lzj, anj;
   for (size_t i = 0; i < nj; i++) {
     const Bound& b = B->jobs[i];
     switch (b.kind) {
@@ -483,7 +516,11 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       case PlanKind::Str:
         if (b.rows) scj.push_back(int(i)); else B->zero_offsets.push_back(b.offs);
         if (b.lz4 && b.payload) lzj.push_back(int(i));
-        if (!b.lz4 && b.payload) B->copies.push_back({b.out, b.dev_chunk + b.bytes_off, size_t(b.payload)});
+        if (b.ans && b.payload) anj.push_back(int(i));
+        if (!b.lz4 && !b.ans && b.payload) B->copies.push_back({b.out, b.dev_chunk + b.bytes_off, size_t(b.payload)});
+        break;
+      case PlanKind::Ans:
+        if (b.payload) anj.push_back(int(i));
         break;
       case PlanKind::RawCopy:
         if (b.payload) B->copies.push_back({b.out, b.dev_chunk + b.raw_off, size_t(b.payload)});
@@ -677,6 +714,29 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     rb.big.vals = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
     rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
   }
+  // ANS (kThreads chunks per tile)
+  for (auto& g : groups(anj)) {
+    AnsBatch ab{};
+    ab.err = B->err_dev;
+    uint32_t tiles = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      AnsDesc& d = ab.d[ab.n++];
+      d.words = reinterpret_cast<const uint16_t*>(b.dev_chunk + b.ans_w_off);
+      d.table = b.dev_chunk + b.ans_tab_off;
+      d.out = static_cast<uint8_t*>(b.out);
+      d.n = b.ans_n;
+      d.n_words = b.ans_w_n;
+      d.nchunks = b.ans_nchunks;
+      d.chunk = b.ans_chunk;
+      d.tl = b.ans_tl;
+      d.tile0 = tiles;
+      d.err_idx = uint32_t(j);
+      tiles += uint32_t(div_up(b.ans_nchunks, kThreads));
+    }
+    ab.total_tiles = tiles;
+    B->ans.push_back(ab);
+  }
   // LZ4
   for (auto& g : groups(lzj)) {
     Lz4Batch lb{};
@@ -737,7 +797,7 @@ cudaEvent_t ev_get(cdm_batch* B, size_t k) {
 cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   uint32_t n = 0;
   size_t evk = B->pending.size() * 2;
-  const bool has[5] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty(),
+  const bool has[5] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty() || !B->ans.empty(),
                        !B->copies.empty() || !B->zero_offsets.empty()};
   int nfam = 0;
   for (bool h : has) nfam += h;
@@ -808,9 +868,13 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
           }
         }
         break;
-      case F_LZ4:
+      case F_LZ4:  // the chunk-sequential family: LZ4 and range ANS
         for (size_t i = 0; i < B->lz4.size() && !st; i++) {
           st = timed(K_LZ4, [&] { return launch_lz4(B->lz4[i], B->lz4_max_sub[i], fs); });
+          n++; B->fam_launches[F_LZ4]++;
+        }
+        for (size_t i = 0; i < B->ans.size() && !st; i++) {
+          st = timed(K_ANS, [&] { return launch_ans(B->ans[i], fs); });
           n++; B->fam_launches[F_LZ4]++;
         }
         break;
@@ -1181,7 +1245,8 @@ static double family_rate(const Bound& b) {
     case PlanKind::Fp: return 1.0;
     case PlanKind::Scan: return 0.5;
     case PlanKind::Rle: return 0.125;
-    case PlanKind::Str: return b.lz4 ? 0.025 : 0.5;
+    case PlanKind::Str: return b.lz4 ? 0.025 : b.ans ? 0.02 : 0.5;
+    case PlanKind::Ans: return 0.02;
     case PlanKind::RawCopy: return 1.0;
   }
   return 1.0;
@@ -1700,11 +1765,11 @@ extern "C" CDM_API cdm_status cdm_batch_set_timing(cdm_batch* b, int enable) {
   return CDM_OK;
 }
 
-extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms8, uint64_t* launches8) {
+extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms9, uint64_t* launches9) {
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   for (int i = 0; i < kKernelKinds; i++) {
-    if (ms8) ms8[i] = b->k_ms[i];
-    if (launches8) launches8[i] = b->k_n[i];
+    if (ms9) ms9[i] = b->k_ms[i];
+    if (launches9) launches9[i] = b->k_n[i];
   }
   return CDM_OK;
 }

@@ -15,6 +15,7 @@
  *   Delta        base = x[0], d[0] = 0, d[i] = x[i]-x[i-1] mod 2^64
  *   RLE          maximal runs, values + counts
  *   LZ4          LZ4 block format per independent sub-chunk (liblz4)
+ *   ANS          range-ANS, 32-bit state / 16-bit words, shared table, chunks
  *   Str          VARBYTES -> [bytes, lengths]                                    (reading R17)
  * Container layout: DESIGN.md "CDM1 chunk container".
  */
@@ -31,7 +32,7 @@ extern int LZ4_compress_default(const char *src, char *dst, int srcSize, int dst
 extern int LZ4_compress_HC(const char *src, char *dst, int srcSize, int dstCapacity, int level);
 extern int LZ4_compressBound(int inputSize);
 
-enum { C_RAW = 0, C_BITPACK = 1, C_DICT = 2, C_FLOAT2INT = 3, C_DELTA = 4, C_RLE = 5, C_LZ4 = 6, C_STR = 7 };
+enum { C_RAW = 0, C_BITPACK = 1, C_DICT = 2, C_FLOAT2INT = 3, C_DELTA = 4, C_RLE = 5, C_LZ4 = 6, C_STR = 7, C_ANS = 8 };
 enum { D_I32 = 0, D_I64 = 1, D_F64 = 2, D_FIXED = 3, D_VARBYTES = 4 };
 enum { E_OK = 0, E_INVALID_ARG = 1, E_PARSE = 2, E_UNSUPPORTED = 3, E_CORRUPT = 4, E_CAPACITY = 5, E_OOM = 7 };
 
@@ -49,6 +50,8 @@ typedef struct tnode {
   struct tnode *child[2];
   uint32_t lz4_sub;   /* LZ4(sub=...) */
   int lz4_hc;         /* LZ4(hc=level) */
+  uint32_t ans_chunk; /* ANS(chunk=...) bytes per independently coded chunk */
+  uint32_t ans_tl;    /* ANS(tl=...) table log */
 } tnode;
 
 typedef struct { const char *s; size_t pos; int err; } parser;
@@ -67,6 +70,7 @@ static int codec_of(const char *name) {
   if (!strcmp(b, "rle")) return C_RLE;
   if (!strcmp(b, "lz4")) return C_LZ4;
   if (!strcmp(b, "str") || !strcmp(b, "string") || !strcmp(b, "varchar")) return C_STR;
+  if (!strcmp(b, "ans") || !strcmp(b, "rans")) return C_ANS;
   return -1;
 }
 
@@ -94,6 +98,8 @@ static tnode *parse_node(parser *p) {
   tnode *t = (tnode *)calloc(1, sizeof(tnode));
   t->codec = c;
   t->lz4_sub = 65536;
+  t->ans_chunk = 4096;
+  t->ans_tl = 12;
   skip_ws(p);
   if (p->s[p->pos] == '(') { /* options k=v,... */
     p->pos++;
@@ -112,6 +118,8 @@ static tnode *parse_node(parser *p) {
       p->pos = (size_t)(end - p->s);
       if (!strcmp(key, "sub")) t->lz4_sub = (uint32_t)v;
       else if (!strcmp(key, "hc")) t->lz4_hc = (int)v;
+      else if (!strcmp(key, "chunk")) t->ans_chunk = (uint32_t)v;
+      else if (!strcmp(key, "tl")) t->ans_tl = (uint32_t)v;
       skip_ws(p);
       if (p->s[p->pos] == ',') { p->pos++; continue; }
       if (p->s[p->pos] == ')') { p->pos++; break; }
@@ -143,7 +151,11 @@ static tnode *parse_node(parser *p) {
   return t;
 }
 
-static tnode *mk(int codec) { tnode *t = (tnode *)calloc(1, sizeof(tnode)); t->codec = codec; t->lz4_sub = 65536; return t; }
+static tnode *mk(int codec) {
+  tnode *t = (tnode *)calloc(1, sizeof(tnode));
+  t->codec = codec; t->lz4_sub = 65536; t->ans_chunk = 4096; t->ans_tl = 12;
+  return t;
+}
 
 /* Complete the tree to full arity (reading R30): 0 children -> all outputs Raw; 1 child binds
  * the primary stream (Dict->indices, RLE->values, Str->bytes); BitPack/LZ4 children are always Raw. */
@@ -156,6 +168,9 @@ static int complete(tnode *t) {
       return fail(E_PARSE, "arity error: BitPack's only child is Raw");
     case C_LZ4:
       if (t->nchild != 0) return fail(E_PARSE, "arity error: LZ4 takes no children");
+      t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; return 0;
+    case C_ANS:
+      if (t->nchild != 0) return fail(E_PARSE, "arity error: ANS takes no children");
       t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; return 0;
     case C_DICT:
       if (t->nchild == 0) { t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; }
@@ -176,7 +191,7 @@ static int complete(tnode *t) {
   return 0;
 }
 
-static const char *NAMES[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR"};
+static const char *NAMES[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS"};
 static void render(const tnode *t, char *buf, size_t cap) {
   strncat(buf, NAMES[t->codec], cap - strlen(buf) - 1);
   if (!t->nchild) return;
@@ -466,6 +481,86 @@ static int enc_lz4(builder *b, const tnode *t, col_t in) {
   return 0;
 }
 
+/* ANS (reading R32): range-ANS over a byte stream, cut
+ * into independently coded chunks of `chunk` bytes that share one table normalised to 2^tl.  32-bit state
+ * in [L, 2^32), L = 2^16, 16-bit renormalisation words.  Each chunk is encoded back to front starting from
+ * state L; its words are stored in decode order together with its final state, so a decoder starts from
+ * that state, reads the words forward and must end at state L having consumed every word.
+ * Streams: [0] u16 words of all chunks; [1] table = 256 x u16 frequencies, then per chunk
+ * {u32 first word, u32 words, u32 initial decoder state}.  Node params: u32 chunks, u32 chunk bytes, u8 tl. */
+static int enc_ans(builder *b, const tnode *t, col_t in) {
+  if (in.is_int) return fail(E_UNSUPPORTED, "ANS needs a byte stream");
+  const uint32_t tl = t->ans_tl, chunk = t->ans_chunk;
+  if (tl < 8 || tl > 15) return fail(E_INVALID_ARG, "ANS table log out of range [8, 15]");
+  if (chunk < 16 || chunk > (1u << 24) || (chunk & 15)) return fail(E_INVALID_ARG, "ANS chunk size: multiple of 16 in [16, 2^24]");
+  const uint64_t n = in.n * in.eb;
+  const uint8_t *src = in.data;
+  const uint32_t M = 1u << tl;
+  uint64_t cnt[256] = {0};
+  for (uint64_t i = 0; i < n; i++) cnt[src[i]]++;
+  uint32_t f[256] = {0}, cum[257];
+  if (n) {  /* normalise: floor(cnt*M/n), at least 1 for present symbols, then fix the sum on the largest */
+    int64_t sum = 0;
+    int big = 0;
+    for (int s = 0; s < 256; s++) {
+      if (!cnt[s]) continue;
+      uint64_t v = cnt[s] * M / n;
+      f[s] = (uint32_t)(v ? v : 1);
+      sum += f[s];
+      if (cnt[s] > cnt[big]) big = s;
+    }
+    while (sum != (int64_t)M) {
+      int s_adj = -1;  /* the largest frequency that can still move */
+      for (int s = 0; s < 256; s++)
+        if (f[s] && (sum < (int64_t)M || f[s] > 1) && (s_adj < 0 || f[s] > f[s_adj])) s_adj = s;
+      if (s_adj < 0) return fail(E_UNSUPPORTED, "ANS: more distinct symbols than 2^tl");
+      if (sum < (int64_t)M) { f[s_adj] += (uint32_t)((int64_t)M - sum); sum = M; }
+      else { f[s_adj]--; sum--; }
+    }
+    (void)big;
+  }
+  cum[0] = 0;
+  for (int s = 0; s < 256; s++) cum[s + 1] = cum[s] + f[s];
+  const uint64_t nch = (n + chunk - 1) / chunk;
+  const uint32_t L = 1u << 16;
+  /* worst case < 2 words per symbol */
+  uint16_t *words = (uint16_t *)malloc((2 * n + 16) * sizeof(uint16_t));
+  uint16_t *tmp = (uint16_t *)malloc((2 * (uint64_t)chunk + 16) * sizeof(uint16_t));
+  uint64_t tbytes = 512 + 12 * nch;
+  uint8_t *tab = (uint8_t *)calloc(tbytes + 16, 1);
+  if (!words || !tmp || !tab) { free(words); free(tmp); free(tab); return fail(E_OOM, "out of memory"); }
+  for (int s = 0; s < 256; s++) { uint16_t v = (uint16_t)f[s]; memcpy(tab + 2 * s, &v, 2); }
+  uint64_t wpos = 0;
+  for (uint64_t c = 0; c < nch; c++) {
+    const uint64_t c0 = c * chunk, c1 = (c0 + chunk < n) ? c0 + chunk : n;
+    uint32_t x = L;
+    uint64_t k = 0;
+    for (uint64_t i = c1; i-- > c0;) {
+      const uint32_t s = src[i], fs = f[s];
+      const uint64_t x_max = ((uint64_t)(L >> tl) << 16) * fs;
+      while ((uint64_t)x >= x_max) { tmp[k++] = (uint16_t)(x & 0xFFFF); x >>= 16; }
+      x = ((x / fs) << tl) + (x % fs) + cum[s];
+    }
+    const uint32_t first = (uint32_t)wpos, nw = (uint32_t)k;
+    for (uint64_t j = 0; j < k; j++) words[wpos++] = tmp[k - 1 - j];  /* decode order */
+    memcpy(tab + 512 + 12 * c, &first, 4); memcpy(tab + 512 + 12 * c + 4, &nw, 4); memcpy(tab + 512 + 12 * c + 8, &x, 4);
+    if (wpos > 0xFFFFFFFFull) { free(words); free(tmp); free(tab); return fail(E_UNSUPPORTED, "ANS payload too large"); }
+  }
+  free(tmp);
+  node_rec r; memset(&r, 0, sizeof r);
+  r.codec = C_ANS; r.nchild = 2; r.stream = 0xFFFF; r.n = n;
+  uint32_t nch32 = (uint32_t)nch;
+  memcpy(r.p, &nch32, 4); memcpy(r.p + 4, &chunk, 4); r.p[8] = (uint8_t)tl;
+  add_node(b, r);
+  node_rec raw; memset(&raw, 0, sizeof raw);
+  raw.codec = C_RAW; raw.stream = (uint16_t)add_stream(b, (uint8_t *)words, wpos * 2); raw.n = wpos; raw.u32a = 2;
+  add_node(b, raw);
+  memset(&raw, 0, sizeof raw);
+  raw.codec = C_RAW; raw.stream = (uint16_t)add_stream(b, tab, tbytes); raw.n = tbytes; raw.u32a = 1;
+  add_node(b, raw);
+  return 0;
+}
+
 /* Str: VARBYTES rows -> [concatenated bytes, per-row lengths]. */
 static int enc_str(builder *b, const tnode *t, col_t in) {
   if (!in.offs) return fail(E_UNSUPPORTED, "Str needs a VARBYTES column");
@@ -492,6 +587,7 @@ static int encode_node(builder *b, const tnode *t, col_t in) {
     case C_RLE: return enc_rle(b, t, in);
     case C_LZ4: return enc_lz4(b, t, in);
     case C_STR: return enc_str(b, t, in);
+    case C_ANS: return enc_ans(b, t, in);
   }
   return fail(E_UNSUPPORTED, "unknown codec");
 }

@@ -10,7 +10,7 @@ import struct
 
 import numpy as np
 
-RAW, BITPACK, DICT, FLOAT2INT, DELTA, RLE, LZ4, STR = range(8)
+RAW, BITPACK, DICT, FLOAT2INT, DELTA, RLE, LZ4, STR, ANS = range(9)
 I32, I64, F64, FIXED, VARBYTES = range(5)
 
 
@@ -26,10 +26,11 @@ def pack_bits(fields, w: int) -> bytes:
 
 class Node:
     def __init__(self, codec, n, children=(), stream=None, eb=0, w=0, base=0, entries=0, E=0, d=0, nruns=0,
-                 maxrun=0, nsub=0, sub=0):
+                 maxrun=0, nsub=0, sub=0, tl=0):
         self.codec, self.n, self.children, self.stream, self.eb = codec, n, list(children), stream, eb
         self.w, self.base, self.entries, self.E, self.d = w, base, entries, E, d
         self.nruns, self.maxrun, self.nsub, self.sub = nruns, maxrun, nsub, sub
+        self.tl = tl
 
     def params(self) -> bytes:
         p = bytearray(16)
@@ -44,8 +45,10 @@ class Node:
             p[8:16] = struct.pack("<Q", self.base & ((1 << 64) - 1))
         elif self.codec == RLE:
             p[0:8] = struct.pack("<II", self.nruns, self.maxrun)
-        elif self.codec == LZ4:
+        elif self.codec in (LZ4, ANS):
             p[0:8] = struct.pack("<II", self.nsub, self.sub)
+            if self.codec == ANS:
+                p[8] = self.tl
         return bytes(p)
 
 

@@ -43,12 +43,14 @@ def test_kernels_are_sm100a_sass():
     ("Float2Int|BitPack", cdm.F64, "fp(unpack+FOR+float2int)"),
     ("Delta|BitPack", cdm.I64, "scan("),
     ("RLE|[BitPack,BitPack]", cdm.I32, "rle("),
-    ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "inner_scan"),
+    ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 0"),
     ("Delta|RLE|[BitPack,BitPack]", cdm.I64, "arithmetic runs"),
-    ("Str|[LZ4,BitPack]", cdm.VARBYTES, "lz4_warp_decode"),
+    ("Str|[LZ4,BitPack]", cdm.VARBYTES, "lz4_group_decode"),
+    ("Str|[ANS,BitPack]", cdm.VARBYTES, "ans_chunk_decode"),
+    ("ANS", cdm.FIXED, "ans_chunk_decode"),
 ])
 def test_cascade_plans(spec, dtype, plan):
-    c = cdm.Cascade(spec, dtype)
+    c = cdm.Cascade(spec, dtype, 1 if dtype == cdm.FIXED else 0)
     d = c.describe()
     assert plan in d
     assert d.split(" => ")[0] == encoder.canonical(spec)
