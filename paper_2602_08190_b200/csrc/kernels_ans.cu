@@ -73,35 +73,29 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
   uint32_t pos = 0;
   uint8_t* out = D.out + i0;
   const uint32_t mask = M - 1u;
+  // the next renormalisation word is loaded as soon as the previous one is consumed, so its global-memory
+  // latency overlaps the symbols decoded in between
+  uint32_t wnext = nw ? uint32_t(__ldg(wp)) : 0u;
+  auto step = [&](uint32_t& x) -> uint32_t {
+    const uint32_t e = tab_s[x & mask];
+    x = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+    if (x < (1u << 16)) {  // one step suffices: x >= 2^(16 - tl) here, tl <= 12
+      bad |= pos >= nw;
+      x = (x << 16) | wnext;
+      pos++;
+      wnext = pos < nw ? uint32_t(__ldg(wp + pos)) : 0u;
+    }
+    return e & 0xFFu;
+  };
   if (!bad) {
     uint32_t i = 0;
     for (; i + 4 <= len; i += 4) {  // 4 symbols -> one 4-byte store (chunks are 16-byte multiples)
       uint32_t word = 0;
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const uint32_t e = tab_s[x & mask];
-        word |= (e & 0xFFu) << (8 * j);
-        x = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
-        if (x < (1u << 16)) {  // one step suffices: x >= 2^(16 - tl) here, tl <= 12
-          const uint32_t v = pos < nw ? uint32_t(__ldg(wp + pos)) : 0u;
-          bad |= pos >= nw;
-          pos++;
-          x = (x << 16) | v;
-        }
-      }
+      for (int j = 0; j < 4; j++) word |= step(x) << (8 * j);
       *reinterpret_cast<uint32_t*>(out + i) = word;
     }
-    for (; i < len; i++) {  // the column chunk's ragged tail
-      const uint32_t e = tab_s[x & mask];
-      out[i] = uint8_t(e & 0xFFu);
-      x = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
-      if (x < (1u << 16)) {
-        const uint32_t v = pos < nw ? uint32_t(__ldg(wp + pos)) : 0u;
-        bad |= pos >= nw;
-        pos++;
-        x = (x << 16) | v;
-      }
-    }
+    for (; i < len; i++) out[i] = uint8_t(step(x));  // the column chunk's ragged tail
     if (x != (1u << 16) || pos != nw) bad = true;
   }
   if (bad) atomicOr(B.err + D.err_idx, 0x20u);
