@@ -11,7 +11,7 @@
 namespace cdm {
 
 constexpr int kMaxBatch = 32;      // descriptors per launch (more chunks -> more launches)
-constexpr int kFpTile = 4096;      // H5 values per tile = 256 threads x 16
+constexpr int kFpTile = 8192;      // H5 values per tile = 256 threads x 32
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
 constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
 constexpr uint32_t kRleSegRows = 32768;  // rle_kernel: output rows per run-start bitmap segment

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     const uint32_t base32 = uint32_t(base);
 
 #pragma unroll 1
-    for (uint32_t k = 0; k < 4 && !bytes_path; k++) {
+    for (uint32_t k = 0; k < kFpTile / 1024 && !bytes_path; k++) {
       const uint32_t i0 = k * 1024 + tid * 4;  // 4 consecutive values
       if (i0 >= valid) break;
       uint64_t v[4];
@@ -214,7 +214,6 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
       // one unaligned 4-byte funnel read from the dictionary (shared memory when it fits, else L1/L2); a
       // row's index is extracted only when the row changes.
       const uint32_t E = ob;
-      const uint64_t inv = (0x100000000ull + E - 1) / E;  // ceil(2^32 / E): exact for positions < 2^17
       const uint32_t total = valid * E;
       uint8_t* obase = out8 + tile_start * E;
       auto fetch = [&](uint32_t row) -> uint32_t {
@@ -231,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
       };
       for (uint32_t c = tid; c * 16 < total; c += kThreads) {
         const uint32_t p0 = c * 16;
-        uint32_t row = uint32_t((uint64_t(p0) * inv) >> 32), col = p0 - row * E;
+        uint32_t row = p0 / E, col = p0 - row * E;
         uint32_t idx = fetch(row);
         uint32_t word[4];
 #pragma unroll
