@@ -15,7 +15,8 @@ constexpr int kFpTile = 8192;      // H5 values per tile = 256 threads x 32
 constexpr int kScanTile = 4096;    // H6 values per tile = 256 threads x 16
 constexpr int kRleTile = 1024;     // H7 runs per tile = 256 threads x 4
 constexpr uint32_t kRleSegRows = 32768;  // rle_kernel: output rows per run-start bitmap segment
-constexpr uint32_t kRleBigLimit = 1u << 15;  // a tile with more output rows is expanded by rle_big
+constexpr uint32_t kRleBigLimit = 1u << 18;  // a tile with more output rows is expanded by rle_big (a CTA
+                                              // expands up to 8 bitmap segments itself)
 constexpr uint32_t kRleBigPiece = 8192;       // rows per rle_big work item
 constexpr int kThreads = 256;
 
