@@ -294,11 +294,13 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  // the persistent grid is capped at 2 CTAs per SM (CDM_FP_CTAS_PER_SM overrides): each CTA then walks ~5+
-  // tiles with its TMA double buffer full (measured faster than 4 CTAs/SM even alone), and SM slots stay
-  // free for a concurrent RLE chain
-  static const int cap = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 2;
-  if (cap > 0 && cap < per_sm) per_sm = cap;
+  // persistent CTAs per SM: 2 for short batches (each CTA still walks ~5 tiles with its TMA double buffer
+  // full, and SM slots stay free for a concurrent RLE chain: config 2), up to 4 for long ones (more tiles in
+  // flight per SM: E2 widths at 268 MB, +20 %); CDM_FP_CTAS_PER_SM overrides
+  static const int cap_env = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 0;
+  const uint32_t tiles_per_sm = b.total_tiles / uint32_t(device_sms());
+  const int cap = cap_env > 0 ? cap_env : tiles_per_sm >= 32 ? 4 : tiles_per_sm >= 20 ? 3 : 2;
+  if (cap < per_sm) per_sm = cap;
   uint32_t grid = uint32_t(device_sms() * per_sm);
   if (!tma) grid = b.total_tiles;  // one tile per CTA, read in place
   // CDM_FP_GRID=tiles: one CTA per tile (no persistence), so CTAs of a concurrent higher-priority family

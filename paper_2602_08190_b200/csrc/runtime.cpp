@@ -1241,12 +1241,16 @@ extern "C" CDM_API cdm_status cdm_submit(cdm_engine* e, const cdm_job* job, uint
 // Johnson cost d_i must rank a Delta|RLE chunk (latency-bound expansion) above a Dict|BitPack chunk of
 // the same decoded size, or the slowest decode lands at the end of the pipeline.
 static double family_rate(const Bound& b) {
+  // relative single-chunk decode rates (measured on B200): a chunk-sequential LZ4 / ANS chunk decodes as one
+  // chain per sub-chunk, so ONE column chunk is latency bound (~40 GB/s for 16 KiB LZ4 sub-chunks, ~8 GB/s
+  // for 4 KiB ANS chunks) -- Johnson's rule then issues those decode-heavy chunks first, and the pipeline
+  // ends on short element-parallel decodes instead of a long chain
   switch (b.kind) {
     case PlanKind::Fp: return 1.0;
     case PlanKind::Scan: return 0.5;
     case PlanKind::Rle: return 0.125;
-    case PlanKind::Str: return b.lz4 ? 0.025 : b.ans ? 0.02 : 0.5;
-    case PlanKind::Ans: return 0.02;
+    case PlanKind::Str: return b.lz4 ? 0.008 : b.ans ? 0.002 : 0.5;
+    case PlanKind::Ans: return 0.002;
     case PlanKind::RawCopy: return 1.0;
   }
   return 1.0;
