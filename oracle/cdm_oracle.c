@@ -290,15 +290,18 @@ static int decode_node(ochunk *c, uint32_t *idx, ostream *out) {
     return OK;
   }
   case OC_ANS: {
+    /* il interleaved states per chunk (1 or 32): symbol i of a chunk uses state i mod il, and the words are
+     * consumed in symbol order (reading R32) */
     if (nch != 2) return bad(c, "node %llu: ANS needs 2 children, has %llu", me, nch);
-    uint32_t nchunks = rd32(pr), chunk = rd32(pr + 4), tl = pr[8];
-    if (tl < 8 || tl > 15 || chunk == 0) return bad(c, "node %llu: ANS params (table log %llu)", me, tl);
+    uint32_t nchunks = rd32(pr), chunk = rd32(pr + 4), tl = pr[8], il = pr[9] ? pr[9] : 1;
+    if (tl < 8 || tl > 15 || chunk == 0 || (il != 1 && il != 32)) return bad(c, "node %llu: ANS params (table log %llu)", me, tl);
+    const uint64_t rec = 8 + 4ull * il;
     ostream wds, tab;
     int rc = decode_node(c, idx, &wds);
     if (rc) return rc;
     rc = decode_node(c, idx, &tab);
     if (rc) { free(wds.data); return rc; }
-    if (wds.eb != 2 || tab.eb != 1 || tab.n != 512 + 12ull * nchunks || (uint64_t)nchunks * chunk < n ||
+    if (wds.eb != 2 || tab.eb != 1 || tab.n != 512 + rec * nchunks || (uint64_t)nchunks * chunk < n ||
         (n && (uint64_t)(nchunks - 1) * chunk >= n) || (!n && nchunks)) {
       free(wds.data); free(tab.data); return bad(c, "node %llu: ANS streams malformed (%llu)", me, tab.n);
     }
@@ -309,25 +312,29 @@ static int decode_node(ochunk *c, uint32_t *idx, ostream *out) {
     uint8_t *o = (uint8_t *)alloc_n(n, 1);
     if (!o) { free(wds.data); free(tab.data); return bad(c, "node %llu: cannot hold %llu bytes", me, n); }
     for (uint32_t k = 0; k < nchunks; k++) {
-      const uint8_t *ce = tab.data + 512 + 12ull * k;
-      uint64_t w0 = rd32(ce), nw = rd32(ce + 4), x = rd32(ce + 8);
+      const uint8_t *ce = tab.data + 512 + rec * k;
+      uint64_t w0 = rd32(ce), nw = rd32(ce + 4), x[32];
+      for (uint32_t l = 0; l < il; l++) x[l] = rd32(ce + 8 + 4 * l);
       if (w0 + nw > wds.n) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: words beyond the stream (%llu)", k, w0 + nw); }
       uint64_t pos = 0;
       const uint64_t i0 = (uint64_t)k * chunk, i1 = i0 + chunk < n ? i0 + chunk : n;
       for (uint64_t i = i0; i < i1; i++) {
-        const uint64_t slot = x % M;
+        uint64_t *xs = &x[(i - i0) % il];
+        const uint64_t slot = *xs % M;
         int sy = 0;
         while (sy < 256 && !(cum[sy] <= slot && slot < cum[sy] + f[sy])) sy++;
         if (sy == 256) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: no symbol for slot %llu", k, slot); }
         o[i] = (uint8_t)sy;
-        x = f[sy] * (x / M) + slot - cum[sy];
-        while (x < L) {
+        *xs = f[sy] * (*xs / M) + slot - cum[sy];
+        while (*xs < L) {
           if (pos >= nw) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: words exhausted at byte %llu", k, i); }
-          x = (x << 16) | rd16(wds.data + 2 * (w0 + pos));
+          *xs = (*xs << 16) | rd16(wds.data + 2 * (w0 + pos));
           pos++;
         }
       }
-      if (x != L || pos != nw) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: final state %llu", k, x); }
+      for (uint32_t l = 0; l < il; l++)
+        if (x[l] != L) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: final state %llu", k, x[l]); }
+      if (pos != nw) { free(wds.data); free(tab.data); free(o); return bad(c, "ANS chunk %llu: %llu words unread", k, nw - pos); }
     }
     free(wds.data); free(tab.data);
     out->n = n; out->eb = 1; out->is_int = 0; out->data = o;

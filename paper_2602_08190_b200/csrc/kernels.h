@@ -194,13 +194,13 @@ struct AnsDesc {
   uint64_t n_words;
   uint32_t nchunks;
   uint32_t chunk;          // bytes per ANS chunk (multiple of 16)
-  uint32_t tile0;          // first global tile (kThreads chunks per tile)
+  uint32_t tile0;          // first global tile (kThreads chunks per tile; kThreads/32 when il = 32)
   uint32_t err_idx;
   uint32_t tl;             // table log (8..12)
-  uint32_t pad;
+  uint32_t il;             // interleaved states per chunk: 1 (thread per chunk) or 32 (warp per chunk)
 };
 
-struct AnsBatch {
+struct AnsBatch {  // one batch holds chunks of one interleave (il) only
   uint32_t n;
   uint32_t total_tiles;
   uint32_t* err;
@@ -214,7 +214,7 @@ cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);
-cudaError_t launch_ans(const AnsBatch& b, cudaStream_t s);
+cudaError_t launch_ans(const AnsBatch& b, bool interleaved, cudaStream_t s);
 // engine bookkeeping: zero a 16-byte-aligned scratch prefix; move error words into mapped pinned memory
 // (copy, then zero them for the next launch)
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);

@@ -8,7 +8,7 @@
 // 2^tl shared by the chunks of a CDM1 chunk; each ANS chunk stores its initial decoder state, its words in
 // decode order, and must end at state 2^16 with every word consumed (else CDM_ERR_ANS = 0x20).
 //
-// B200 shape: a CTA takes 256 consecutive chunks of one column chunk; it first expands the shared table
+// il = 1 (one state per chunk): a CTA takes 256 consecutive chunks of one column chunk; it first expands the shared table
 // into a shared-memory slot table (2^tl packed entries {symbol, f - 1, slot - cum}, tl <= 12), so the
 // per-symbol step is one shared load + a multiply-add; every thread gathers 4 decoded bytes into a
 // register and writes them with one 4-byte store.
@@ -31,15 +31,11 @@ __device__ __forceinline__ int find_desc_ans(const AnsBatch& B, uint32_t tile) {
   return lo;
 }
 
-__global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ AnsBatch B) {
-  __shared__ uint32_t tab_s[1u << kAnsMaxTl];  // slot -> sym | (f - 1) << 8 | (slot - cum) << 20
-  __shared__ uint32_t cum_s[257];
-  __shared__ uint64_t warp_s[kThreads / 32];
+// The CTA's slot table from the 256 frequencies: cum_s = exclusive scan, tab_s[slot] = packed {symbol, f - 1,
+// slot - cum}; returns whether the frequencies sum to M (else every chunk reports CDM_ERR_ANS).
+__device__ __forceinline__ bool build_slot_table(const uint8_t* table, uint32_t M, uint32_t* tab_s, uint32_t* cum_s,
+                                                 uint64_t* warp_s) {
   const uint32_t tid = threadIdx.x;
-  const AnsDesc& D = B.d[find_desc_ans(B, blockIdx.x)];
-  const uint32_t tl = D.tl, M = 1u << tl;
-  const uint8_t* const table = D.table;
-  // cumulative frequencies (block scan of the 256 u16 frequencies)
   {
     const uint32_t f = tid < 256 ? uint32_t(__ldg(reinterpret_cast<const uint16_t*>(table) + tid)) : 0u;
     uint64_t tot;
@@ -48,8 +44,7 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
     if (tid == 0) cum_s[256] = uint32_t(tot);
   }
   __syncthreads();
-  const bool table_ok = cum_s[256] == M;
-  // slot table: the symbol of each slot (binary search over cum), its frequency and its offset in the range
+  const bool ok = cum_s[256] == M;
   for (uint32_t slot = tid; slot < M; slot += kThreads) {
     uint32_t lo = 0, hi = 255;
     while (lo < hi) {  // last symbol with cum <= slot
@@ -60,6 +55,18 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
     tab_s[slot] = lo | ((f - 1u) & 0xFFFu) << 8 | (slot - cum_s[lo]) << 20;
   }
   __syncthreads();
+  return ok;
+}
+
+__global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ AnsBatch B) {
+  __shared__ uint32_t tab_s[1u << kAnsMaxTl];  // slot -> sym | (f - 1) << 8 | (slot - cum) << 20
+  __shared__ uint32_t cum_s[257];
+  __shared__ uint64_t warp_s[kThreads / 32];
+  const uint32_t tid = threadIdx.x;
+  const AnsDesc& D = B.d[find_desc_ans(B, blockIdx.x)];
+  const uint32_t tl = D.tl, M = 1u << tl;
+  const uint8_t* const table = D.table;
+  const bool table_ok = build_slot_table(table, M, tab_s, cum_s, warp_s);
   const uint32_t c = (blockIdx.x - D.tile0) * kThreads + tid;  // this thread's chunk
   if (c >= D.nchunks) return;
   bool bad = !table_ok;
@@ -101,11 +108,67 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
   if (bad) atomicOr(B.err + D.err_idx, 0x20u);
 }
 
+
+// il = 32 (the default format, SURVEY Sec. 8f NEXT-1 "interleaved rANS, warp-per-chunk"): one WARP per ANS
+// chunk, lane l owns state l and decodes symbols 32s + l, so a warp emits 32 consecutive bytes per step and a
+// chunk's dependency chain is chunk/32 steps long.  The states that renormalise at a step take consecutive
+// words in lane order (ballot + popcount rank); the chunk's next 64 words sit in two registers per lane
+// (one word per lane each) and reach the renormalising lanes by shuffle, refilled 32 words at a time with a
+// coalesced load.
+__global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constant__ AnsBatch B) {
+  __shared__ uint32_t tab_s[1u << kAnsMaxTl];
+  __shared__ uint32_t cum_s[257];
+  __shared__ uint64_t warp_s[kThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const AnsDesc& D = B.d[find_desc_ans(B, blockIdx.x)];
+  const uint32_t tl = D.tl, M = 1u << tl;
+  const uint8_t* const table = D.table;
+  const bool table_ok = build_slot_table(table, M, tab_s, cum_s, warp_s);
+  const uint32_t c = (blockIdx.x - D.tile0) * (kThreads / 32) + warp;  // this warp's chunk
+  if (c >= D.nchunks) return;  // warp-uniform
+  const uint8_t* ce = table + 512 + 136ull * c;
+  const uint32_t w0 = __ldg(reinterpret_cast<const uint32_t*>(ce)), nw = __ldg(reinterpret_cast<const uint32_t*>(ce + 4));
+  uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(ce + 8) + lane);
+  bool bad = !table_ok || uint64_t(w0) + nw > D.n_words;
+  const uint64_t i0 = uint64_t(c) * D.chunk;
+  const uint32_t len = uint32_t(min(uint64_t(D.chunk), D.n - i0));
+  const uint16_t* __restrict__ wp = D.words + w0;
+  uint8_t* out = D.out + i0;
+  const uint32_t mask = M - 1u, lt_mask = (1u << lane) - 1u;
+  auto ldw = [&](uint32_t q) -> uint32_t { return q < nw ? uint32_t(__ldg(wp + q)) : 0u; };
+  uint32_t wbase = 0, cur = 0, nxt = 0, pos = 0;
+  if (!bad) { cur = ldw(lane); nxt = ldw(32 + lane); }
+  const uint32_t steps = bad ? 0u : (len + 31) / 32;
+  for (uint32_t s = 0; s < steps; s++) {
+    const uint32_t i = 32 * s + lane;
+    const bool act = i < len;
+    const uint32_t e = tab_s[x & mask];
+    const uint32_t xn = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+    const bool need = act && xn < (1u << 16);  // one step suffices for tl <= 12
+    const uint32_t m = __ballot_sync(FULL, need);
+    const uint32_t q = pos + __popc(m & lt_mask) - wbase;  // word index relative to the window (< 64)
+    const uint32_t a = __shfl_sync(FULL, cur, q & 31), b = __shfl_sync(FULL, nxt, q & 31);
+    const uint32_t w = q < 32 ? a : b;
+    bad |= need && pos + __popc(m & lt_mask) >= nw;
+    x = need ? (xn << 16) | w : (act ? xn : x);
+    if (act) out[i] = uint8_t(e & 0xFFu);
+    pos += __popc(m);
+    if (pos >= wbase + 32) {  // warp-uniform: slide the window by 32 words
+      wbase += 32;
+      cur = nxt;
+      nxt = ldw(wbase + 32 + lane);
+    }
+  }
+  bad |= !__all_sync(FULL, x == (1u << 16)) || pos != nw;
+  if (bad && lane == 0) atomicOr(B.err + D.err_idx, 0x20u);
+}
+
 }  // namespace
 
-cudaError_t launch_ans(const AnsBatch& b, cudaStream_t s) {
+cudaError_t launch_ans(const AnsBatch& b, bool interleaved, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  ans_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
+  if (interleaved) ans_warp_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
+  else ans_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
   return cudaGetLastError();
 }
 

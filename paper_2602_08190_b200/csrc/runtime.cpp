@@ -138,7 +138,7 @@ struct Bound {
   uint32_t n_sub = 0, lz_sub_bytes = 0, lz_uniform = 0;
   bool ans = false;  // NEXT-1: the bytes come from a range-ANS node (Str child or FIXED root)
   uint64_t ans_w_off = 0, ans_w_n = 0, ans_tab_off = 0, ans_n = 0;
-  uint32_t ans_nchunks = 0, ans_chunk = 0, ans_tl = 0;
+  uint32_t ans_nchunks = 0, ans_chunk = 0, ans_tl = 0, ans_il = 1;
   const uint8_t* dev_chunk = nullptr;
   void* out = nullptr;
   void* offs = nullptr;
@@ -252,10 +252,12 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
     b->ans_nchunks = an.u32_at0();
     b->ans_chunk = an.u32_at4();
     b->ans_tl = an.params[8];
+    b->ans_il = an.params[9] ? an.params[9] : 1;
+    if (b->ans_il != 1 && b->ans_il != 32) return bad("ANS interleave must be 1 or 32");
     if (b->ans_tl < 8 || b->ans_tl > 15) return bad("ANS table log out of range");
     if (b->ans_tl > 12) return fail(CDM_E_UNSUPPORTED, "ANS table log > 12 (device slot table)");
     if (!b->ans_chunk || b->ans_chunk % 16) return bad("ANS chunk size not a positive multiple of 16");
-    if (tn != 512 + 12ull * b->ans_nchunks) return bad("ANS table size");
+    if (tn != 512 + (8ull + 4ull * b->ans_il) * b->ans_nchunks) return bad("ANS table size");
     const uint64_t cap = uint64_t(b->ans_nchunks) * b->ans_chunk;
     if (cap < an.n || (an.n && cap - b->ans_chunk >= an.n) || (!an.n && b->ans_nchunks)) return bad("ANS chunk count");
     return CDM_OK;
@@ -714,28 +716,33 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     rb.big.vals = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
     rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
   }
-  // ANS (kThreads chunks per tile)
-  for (auto& g : groups(anj)) {
-    AnsBatch ab{};
-    ab.err = B->err_dev;
-    uint32_t tiles = 0;
-    for (int j : g) {
-      const Bound& b = B->jobs[j];
-      AnsDesc& d = ab.d[ab.n++];
-      d.words = reinterpret_cast<const uint16_t*>(b.dev_chunk + b.ans_w_off);
-      d.table = b.dev_chunk + b.ans_tab_off;
-      d.out = static_cast<uint8_t*>(b.out);
-      d.n = b.ans_n;
-      d.n_words = b.ans_w_n;
-      d.nchunks = b.ans_nchunks;
-      d.chunk = b.ans_chunk;
-      d.tl = b.ans_tl;
-      d.tile0 = tiles;
-      d.err_idx = uint32_t(j);
-      tiles += uint32_t(div_up(b.ans_nchunks, kThreads));
+  // ANS: batches of one interleave each; a tile = kThreads chunks (il = 1) or kThreads/32 chunks (il = 32)
+  for (int il : {1, 32}) {
+    std::vector<int> sel;
+    for (int j : anj) if (B->jobs[j].ans_il == uint32_t(il)) sel.push_back(j);
+    for (auto& g : groups(sel)) {
+      AnsBatch ab{};
+      ab.err = B->err_dev;
+      uint32_t tiles = 0;
+      for (int j : g) {
+        const Bound& b = B->jobs[j];
+        AnsDesc& d = ab.d[ab.n++];
+        d.words = reinterpret_cast<const uint16_t*>(b.dev_chunk + b.ans_w_off);
+        d.table = b.dev_chunk + b.ans_tab_off;
+        d.out = static_cast<uint8_t*>(b.out);
+        d.n = b.ans_n;
+        d.n_words = b.ans_w_n;
+        d.nchunks = b.ans_nchunks;
+        d.chunk = b.ans_chunk;
+        d.tl = b.ans_tl;
+        d.il = b.ans_il;
+        d.tile0 = tiles;
+        d.err_idx = uint32_t(j);
+        tiles += uint32_t(div_up(b.ans_nchunks, il == 32 ? kThreads / 32 : kThreads));
+      }
+      ab.total_tiles = tiles;
+      B->ans.push_back(ab);
     }
-    ab.total_tiles = tiles;
-    B->ans.push_back(ab);
   }
   // LZ4
   for (auto& g : groups(lzj)) {
@@ -874,7 +881,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
           n++; B->fam_launches[F_LZ4]++;
         }
         for (size_t i = 0; i < B->ans.size() && !st; i++) {
-          st = timed(K_ANS, [&] { return launch_ans(B->ans[i], fs); });
+          st = timed(K_ANS, [&] { return launch_ans(B->ans[i], B->ans[i].n && B->ans[i].d[0].il == 32, fs); });
           n++; B->fam_launches[F_LZ4]++;
         }
         break;
@@ -1249,8 +1256,8 @@ static double family_rate(const Bound& b) {
     case PlanKind::Fp: return 1.0;
     case PlanKind::Scan: return 0.5;
     case PlanKind::Rle: return 0.125;
-    case PlanKind::Str: return b.lz4 ? 0.008 : b.ans ? 0.002 : 0.5;
-    case PlanKind::Ans: return 0.002;
+    case PlanKind::Str: return b.lz4 ? 0.008 : b.ans ? (b.ans_il == 32 ? 0.05 : 0.002) : 0.5;
+    case PlanKind::Ans: return b.ans_il == 32 ? 0.05 : 0.002;
     case PlanKind::RawCopy: return 1.0;
   }
   return 1.0;

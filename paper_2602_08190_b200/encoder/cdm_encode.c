@@ -52,6 +52,7 @@ typedef struct tnode {
   int lz4_hc;         /* LZ4(hc=level) */
   uint32_t ans_chunk; /* ANS(chunk=...) bytes per independently coded chunk */
   uint32_t ans_tl;    /* ANS(tl=...) table log */
+  uint32_t ans_il;    /* ANS(il=1|32) interleaved states per chunk (0 = default 32) */
 } tnode;
 
 typedef struct { const char *s; size_t pos; int err; } parser;
@@ -98,8 +99,9 @@ static tnode *parse_node(parser *p) {
   tnode *t = (tnode *)calloc(1, sizeof(tnode));
   t->codec = c;
   t->lz4_sub = 65536;
-  t->ans_chunk = 4096;
+  t->ans_chunk = 0;   /* default: 16384 with 32 interleaved states, 4096 with one */
   t->ans_tl = 12;
+  t->ans_il = 32;
   skip_ws(p);
   if (p->s[p->pos] == '(') { /* options k=v,... */
     p->pos++;
@@ -120,6 +122,7 @@ static tnode *parse_node(parser *p) {
       else if (!strcmp(key, "hc")) t->lz4_hc = (int)v;
       else if (!strcmp(key, "chunk")) t->ans_chunk = (uint32_t)v;
       else if (!strcmp(key, "tl")) t->ans_tl = (uint32_t)v;
+      else if (!strcmp(key, "il")) t->ans_il = (uint32_t)v;
       skip_ws(p);
       if (p->s[p->pos] == ',') { p->pos++; continue; }
       if (p->s[p->pos] == ')') { p->pos++; break; }
@@ -153,7 +156,7 @@ static tnode *parse_node(parser *p) {
 
 static tnode *mk(int codec) {
   tnode *t = (tnode *)calloc(1, sizeof(tnode));
-  t->codec = codec; t->lz4_sub = 65536; t->ans_chunk = 4096; t->ans_tl = 12;
+  t->codec = codec; t->lz4_sub = 65536; t->ans_chunk = 0; t->ans_tl = 12; t->ans_il = 32;
   return t;
 }
 
@@ -482,16 +485,24 @@ static int enc_lz4(builder *b, const tnode *t, col_t in) {
 }
 
 /* ANS (reading R32): range-ANS over a byte stream, cut
- * into independently coded chunks of `chunk` bytes that share one table normalised to 2^tl.  32-bit state
- * in [L, 2^32), L = 2^16, 16-bit renormalisation words.  Each chunk is encoded back to front starting from
- * state L; its words are stored in decode order together with its final state, so a decoder starts from
- * that state, reads the words forward and must end at state L having consumed every word.
+ * into independently coded chunks of `chunk` bytes that share one table normalised to 2^tl.  32-bit states
+ * in [L, 2^32), L = 2^16, 16-bit renormalisation words (at most one per symbol for tl <= 16).
+ * il = 1: one state per chunk; symbols are coded back to front from state L.
+ * il = 32 (default): 32 interleaved states per chunk, symbol i belongs to state i mod 32 at step i div 32.
+ *   Decode order = step-major, state-minor; the encoder runs exactly the reverse order (steps descending,
+ *   states descending) pushing its words, and the chunk's word list is that push order reversed -- so at
+ *   every decode step the states that renormalise take consecutive words in state order.
+ * Every chunk stores its initial decoder state(s) and its words in decode order; a decoder must end with
+ * every state at L and every word read.
  * Streams: [0] u16 words of all chunks; [1] table = 256 x u16 frequencies, then per chunk
- * {u32 first word, u32 words, u32 initial decoder state}.  Node params: u32 chunks, u32 chunk bytes, u8 tl. */
+ * {u32 first word, u32 words, il x u32 initial decoder states}.  Node params: u32 chunks @0,
+ * u32 chunk bytes @4, u8 tl @8, u8 il @9. */
 static int enc_ans(builder *b, const tnode *t, col_t in) {
   if (in.is_int) return fail(E_UNSUPPORTED, "ANS needs a byte stream");
-  const uint32_t tl = t->ans_tl, chunk = t->ans_chunk;
+  const uint32_t tl = t->ans_tl, il = t->ans_il;
+  const uint32_t chunk = t->ans_chunk ? t->ans_chunk : (il == 32 ? 16384 : 4096);
   if (tl < 8 || tl > 15) return fail(E_INVALID_ARG, "ANS table log out of range [8, 15]");
+  if (il != 1 && il != 32) return fail(E_INVALID_ARG, "ANS interleave must be 1 or 32");
   if (chunk < 16 || chunk > (1u << 24) || (chunk & 15)) return fail(E_INVALID_ARG, "ANS chunk size: multiple of 16 in [16, 2^24]");
   const uint64_t n = in.n * in.eb;
   const uint8_t *src = in.data;
@@ -501,13 +512,11 @@ static int enc_ans(builder *b, const tnode *t, col_t in) {
   uint32_t f[256] = {0}, cum[257];
   if (n) {  /* normalise: floor(cnt*M/n), at least 1 for present symbols, then fix the sum on the largest */
     int64_t sum = 0;
-    int big = 0;
     for (int s = 0; s < 256; s++) {
       if (!cnt[s]) continue;
       uint64_t v = cnt[s] * M / n;
       f[s] = (uint32_t)(v ? v : 1);
       sum += f[s];
-      if (cnt[s] > cnt[big]) big = s;
     }
     while (sum != (int64_t)M) {
       int s_adj = -1;  /* the largest frequency that can still move */
@@ -517,40 +526,42 @@ static int enc_ans(builder *b, const tnode *t, col_t in) {
       if (sum < (int64_t)M) { f[s_adj] += (uint32_t)((int64_t)M - sum); sum = M; }
       else { f[s_adj]--; sum--; }
     }
-    (void)big;
   }
   cum[0] = 0;
   for (int s = 0; s < 256; s++) cum[s + 1] = cum[s] + f[s];
   const uint64_t nch = (n + chunk - 1) / chunk;
   const uint32_t L = 1u << 16;
-  /* worst case < 2 words per symbol */
-  uint16_t *words = (uint16_t *)malloc((2 * n + 16) * sizeof(uint16_t));
-  uint16_t *tmp = (uint16_t *)malloc((2 * (uint64_t)chunk + 16) * sizeof(uint16_t));
-  uint64_t tbytes = 512 + 12 * nch;
+  const uint64_t rec = 8 + 4ull * il;
+  uint16_t *words = (uint16_t *)malloc((n + 16) * sizeof(uint16_t));  /* <= 1 word per symbol */
+  uint16_t *tmp = (uint16_t *)malloc(((uint64_t)chunk + 16) * sizeof(uint16_t));
+  uint64_t tbytes = 512 + rec * nch;
   uint8_t *tab = (uint8_t *)calloc(tbytes + 16, 1);
   if (!words || !tmp || !tab) { free(words); free(tmp); free(tab); return fail(E_OOM, "out of memory"); }
   for (int s = 0; s < 256; s++) { uint16_t v = (uint16_t)f[s]; memcpy(tab + 2 * s, &v, 2); }
   uint64_t wpos = 0;
   for (uint64_t c = 0; c < nch; c++) {
     const uint64_t c0 = c * chunk, c1 = (c0 + chunk < n) ? c0 + chunk : n;
-    uint32_t x = L;
+    uint32_t x[32];
+    for (uint32_t l = 0; l < il; l++) x[l] = L;
     uint64_t k = 0;
-    for (uint64_t i = c1; i-- > c0;) {
+    for (uint64_t i = c1; i-- > c0;) {  /* reverse decode order: steps descending, states descending */
+      const uint32_t l = il == 1 ? 0 : (uint32_t)((i - c0) & 31);
       const uint32_t s = src[i], fs = f[s];
       const uint64_t x_max = ((uint64_t)(L >> tl) << 16) * fs;
-      while ((uint64_t)x >= x_max) { tmp[k++] = (uint16_t)(x & 0xFFFF); x >>= 16; }
-      x = ((x / fs) << tl) + (x % fs) + cum[s];
+      while ((uint64_t)x[l] >= x_max) { tmp[k++] = (uint16_t)(x[l] & 0xFFFF); x[l] >>= 16; }
+      x[l] = ((x[l] / fs) << tl) + (x[l] % fs) + cum[s];
     }
     const uint32_t first = (uint32_t)wpos, nw = (uint32_t)k;
     for (uint64_t j = 0; j < k; j++) words[wpos++] = tmp[k - 1 - j];  /* decode order */
-    memcpy(tab + 512 + 12 * c, &first, 4); memcpy(tab + 512 + 12 * c + 4, &nw, 4); memcpy(tab + 512 + 12 * c + 8, &x, 4);
+    memcpy(tab + 512 + rec * c, &first, 4); memcpy(tab + 512 + rec * c + 4, &nw, 4);
+    for (uint32_t l = 0; l < il; l++) memcpy(tab + 512 + rec * c + 8 + 4 * l, &x[l], 4);
     if (wpos > 0xFFFFFFFFull) { free(words); free(tmp); free(tab); return fail(E_UNSUPPORTED, "ANS payload too large"); }
   }
   free(tmp);
   node_rec r; memset(&r, 0, sizeof r);
   r.codec = C_ANS; r.nchild = 2; r.stream = 0xFFFF; r.n = n;
   uint32_t nch32 = (uint32_t)nch;
-  memcpy(r.p, &nch32, 4); memcpy(r.p + 4, &chunk, 4); r.p[8] = (uint8_t)tl;
+  memcpy(r.p, &nch32, 4); memcpy(r.p + 4, &chunk, 4); r.p[8] = (uint8_t)tl; r.p[9] = (uint8_t)il;
   add_node(b, r);
   node_rec raw; memset(&raw, 0, sizeof raw);
   raw.codec = C_RAW; raw.stream = (uint16_t)add_stream(b, (uint8_t *)words, wpos * 2); raw.n = wpos; raw.u32a = 2;

@@ -26,11 +26,11 @@ def pack_bits(fields, w: int) -> bytes:
 
 class Node:
     def __init__(self, codec, n, children=(), stream=None, eb=0, w=0, base=0, entries=0, E=0, d=0, nruns=0,
-                 maxrun=0, nsub=0, sub=0, tl=0):
+                 maxrun=0, nsub=0, sub=0, tl=0, il=0):
         self.codec, self.n, self.children, self.stream, self.eb = codec, n, list(children), stream, eb
         self.w, self.base, self.entries, self.E, self.d = w, base, entries, E, d
         self.nruns, self.maxrun, self.nsub, self.sub = nruns, maxrun, nsub, sub
-        self.tl = tl
+        self.tl, self.il = tl, il
 
     def params(self) -> bytes:
         p = bytearray(16)
@@ -49,6 +49,7 @@ class Node:
             p[0:8] = struct.pack("<II", self.nsub, self.sub)
             if self.codec == ANS:
                 p[8] = self.tl
+                p[9] = self.il
         return bytes(p)
 
 

@@ -151,11 +151,13 @@ TPCH_CASES = [
     ("o_comment", "Str|[LZ4,BitPack]"),
     ("o_totalprice", "RLE|[Float2Int|BitPack,BitPack]"),
     ("l_orderkey", "Raw"),
-    ("l_returnflag", "ANS"),                      # Table 2 L_RETURNFLAG (NEXT-1: chunk-sequential range ANS)
+    ("l_returnflag", "ANS"),                      # Table 2 L_RETURNFLAG (NEXT-1: range ANS, 32 interleaved states)
+    ("l_returnflag", "ANS(il=1,chunk=4096)"),     # one state per chunk (thread per chunk)
     ("l_linestatus", "ANS(chunk=1024)"),
     ("l_shipmode", "ANS(tl=10)"),
     ("o_orderstatus", "ANS(chunk=65536)"),
     ("l_comment", "Str|[ANS(chunk=2048),BitPack]"),
+    ("l_comment", "Str|[ANS(il=1,chunk=2048),BitPack]"),
 ]
 
 
@@ -342,17 +344,18 @@ def test_corrupt_run_sum_sets_error(engine):
         assert r["error_bits"] & cdm.ERR_RUN_SUM
 
 
-def test_corrupt_ans_sets_error(engine):
+@pytest.mark.parametrize("il", [1, 32])
+def test_corrupt_ans_sets_error(engine, il):
     import test_ans_cpu as A
     data = np.random.default_rng(11).choice(np.array([65, 78, 82], np.uint8), 30000, p=[.25, .5, .25]).tobytes()
-    good, _ = A.ans_chunk(data, 12, 4096)
+    good, _ = A.ans_chunk(data, 12, 4096, il=il)
     assert oracle.decode_chunk(good)[0].tobytes() == data
     casc = cdm.Cascade("ANS", cdm1.FIXED, 1)
     good[48:56] = np.frombuffer(struct.pack("<Q", _hash("ANS")), dtype=np.uint8)
     (payload, _, r), = gpu_decode(engine, casc, [good], resident=True)
     assert r["error_bits"] == 0 and payload.tobytes() == data
     for corrupt in ("word", "state", "truncate"):
-        ch, _ = A.ans_chunk(data, 12, 4096, corrupt=corrupt)
+        ch, _ = A.ans_chunk(data, 12, 4096, corrupt=corrupt, il=il)
         ch[48:56] = np.frombuffer(struct.pack("<Q", _hash("ANS")), dtype=np.uint8)
         (payload, _, r), = gpu_decode(engine, casc, [ch], resident=True, expect_error=True)
         assert r["error_bits"] & 0x20, corrupt
