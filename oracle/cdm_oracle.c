@@ -22,6 +22,9 @@
  *                  cum_s <= slot < cum_s + f_s (found by a linear scan), x = f_s (x div 2^tl) + slot - cum_s,
  *                  then while x < 2^16: x = x*2^16 + next word; a chunk must end at x = 2^16 with every word
  *                  read.
+ *   DeltaStride    PAPER.md:481 (Sec. 5.3, "(start, stride, count) triples", an RLE variant), DESIGN.md reading
+ *                  R9: children [starts, counts], one stride per node; run g fills [presum_{g-1}, presum_g)
+ *                  with start_g + j*stride, j = 0, 1, ... (mod 2^64); presum must end at n.
  *   Str            DESIGN.md reading R17: offsets_0 = 0, offsets_{i+1} = offsets_i + len_i.
  *   Nesting        PAPER.md:509 (Table 2 notation), decoded depth-first: children first, then parent
  *                  (no fusion exists in the oracle).
@@ -40,7 +43,7 @@
 
 /* oracle's own constants (the format spec is DESIGN.md's, restated here independently) */
 #define O_MAGIC 0x314D4443u
-enum { OC_RAW = 0, OC_BITPACK = 1, OC_DICT = 2, OC_FLOAT2INT = 3, OC_DELTA = 4, OC_RLE = 5, OC_LZ4 = 6, OC_STR = 7, OC_ANS = 8 };
+enum { OC_RAW = 0, OC_BITPACK = 1, OC_DICT = 2, OC_FLOAT2INT = 3, OC_DELTA = 4, OC_RLE = 5, OC_LZ4 = 6, OC_STR = 7, OC_ANS = 8, OC_DSTRIDE = 9 };
 enum { OT_I32 = 0, OT_I64 = 1, OT_F64 = 2, OT_FIXED = 3, OT_VARBYTES = 4 };
 enum { OK = 0, ERR_ARG = 1, ERR_UNSUPPORTED = 3, ERR_CORRUPT = 4, ERR_CAPACITY = 5, ERR_OOM = 7 };
 
@@ -229,6 +232,31 @@ static int decode_node(ochunk *c, uint32_t *idx, ostream *out) {
     int is_int = vals.is_int;
     free(vals.data); free(cnt.data);
     out->n = n; out->eb = (uint32_t)eb; out->is_int = is_int; out->data = o;
+    return OK;
+  }
+  case OC_DSTRIDE: {
+    /* "(start, stride, count) triples"; run g = start_g, start_g + stride, ... (count_g terms). */
+    if (nch != 2) return bad(c, "node %llu: DeltaStride needs 2 children, has %llu", me, nch);
+    uint32_t nruns = rd32(pr);
+    uint64_t stride = rd64(pr + 8);
+    ostream st, cnt;
+    int rc = decode_int_child(c, idx, &st);
+    if (rc) return rc;
+    rc = decode_int_child(c, idx, &cnt);
+    if (rc) { free(st.data); return rc; }
+    if (st.n != nruns || cnt.n != nruns) { free(st.data); free(cnt.data); return bad(c, "node %llu: run arrays %llu", me, st.n); }
+    uint64_t *o = (uint64_t *)alloc_n(n, 8);
+    if (!o) { free(st.data); free(cnt.data); return bad(c, "node %llu: cannot hold %llu elements", me, n); }
+    uint64_t pos = 0;
+    for (uint64_t g = 0; g < nruns; g++) {
+      uint64_t k = rd64(cnt.data + 8 * g), start = rd64(st.data + 8 * g);
+      if (k > n - pos) { free(st.data); free(cnt.data); free(o); return bad(c, "run %llu: count overflows the %llu rows", g, n); }
+      for (uint64_t j = 0; j < k; j++) o[pos + j] = start + j * stride;
+      pos += k;
+    }
+    free(st.data); free(cnt.data);
+    if (pos != n) { free(o); return bad(c, "run sum %llu != %llu rows", pos, n); }
+    out->n = n; out->eb = 8; out->is_int = 1; out->data = (uint8_t *)o;
     return OK;
   }
   case OC_LZ4: {

@@ -222,6 +222,77 @@ def test_rle_count_sum_mismatch():
             dec(cdm1.build(root, cdm1.I64, 8, 5))
 
 
+# ----------------------------------------------------------------------------- DeltaStride (closed forms)
+# PAPER.md:481 "(start, stride, count) triples"; reading R9 (children [starts, counts], one stride).
+
+def _dstride(starts, counts, stride, wst=20, wc=8, rows=None):
+    n = int(np.sum(counts)) if rows is None else rows
+    return cdm1.Node(cdm1.DSTRIDE, n, [cdm1.bitpack(starts, wst, int(min(starts)) if len(starts) else 0),
+                                       cdm1.bitpack(counts, wc, 0)],
+                     nruns=len(starts), maxrun=int(max(counts)) if len(counts) else 0, stride=stride)
+
+
+def test_dstride_spec_example():
+    # SPEC.md:279's column [10,11,12,20,22,24]: with stride 1 the greedy runs are (10,3),(20,1),(22,1),(24,1);
+    # with stride 2, (10,1),(11,1),(12,1),(20,3)
+    for starts, counts, stride in (([10, 20, 22, 24], [3, 1, 1, 1], 1), ([10, 11, 12, 20], [1, 1, 1, 3], 2)):
+        out, _ = dec(cdm1.build(_dstride(starts, counts, stride), cdm1.I64, 8, 6))
+        assert as_i64(out).tolist() == [10, 11, 12, 20, 22, 24]
+
+
+def test_dstride_tpch_orderkeys_closed_form():
+    # TPC-H sparse order keys (first 8 of every 32): key(o) = 32*(o div 8) + (o mod 8) + 1 -- triples
+    # (32q + 1, 1, 8); a chunk starting mid-group has a short first run
+    o0, n = 5, 8 * 40 + 3
+    o = np.arange(o0, o0 + n)
+    keys = 32 * (o // 8) + (o % 8) + 1
+    starts, counts, g = [], [], o0
+    while g < o0 + n:
+        k = min(8 - g % 8, o0 + n - g)
+        starts.append(int(32 * (g // 8) + g % 8 + 1)); counts.append(k); g += k
+    out, _ = dec(cdm1.build(_dstride(starts, counts, 1, wst=14, wc=4), cdm1.I64, 8, n))
+    assert np.array_equal(as_i64(out), keys)
+
+
+@pytest.mark.parametrize("stride", [0, 3, -7, (1 << 63) + 5])
+def test_dstride_arithmetic_runs(stride):
+    rng = np.random.default_rng(11)
+    nr = 200
+    counts = rng.integers(0, 40, size=nr)
+    starts = rng.integers(0, 1 << 40, size=nr)
+    n = int(counts.sum())
+    out, _ = dec(cdm1.build(_dstride(list(starts), list(counts), stride, wst=41, wc=6), cdm1.I64, 8, n))
+    exp = [(int(s) + j * stride) & MASK64 for s, c in zip(starts, counts) for j in range(int(c))]
+    assert [int(x) & MASK64 for x in as_i64(out)] == exp
+    # stride 0 is plain RLE (np.repeat)
+    if stride == 0:
+        assert np.array_equal(as_i64(out), np.repeat(starts, counts))
+
+
+def test_dstride_under_rle_and_delta():
+    # Table 2 L_ORDERKEY shape: RLE | [DeltaStride | [Delta | RLE | [BP, BP], BP], BP]
+    # starts 1, 33, 65, 97 = Delta(base 1) of RLE(value 32 x 3 after a leading 0); counts 8 each
+    inner = cdm1.Node(cdm1.RLE, 4, [cdm1.bitpack([0, 32], 6, 0), cdm1.bitpack([1, 3], 2, 0)], nruns=2, maxrun=3)
+    starts = cdm1.Node(cdm1.DELTA, 4, [inner], base=1)
+    ds = cdm1.Node(cdm1.DSTRIDE, 32, [starts, cdm1.bitpack([8, 8, 8, 8], 0, 8)], nruns=4, maxrun=8, stride=1)
+    lines = [1 + (k % 7) for k in range(32)]
+    root = cdm1.Node(cdm1.RLE, sum(lines), [ds, cdm1.bitpack(lines, 3, 0)], nruns=32, maxrun=7)
+    out, _ = dec(cdm1.build(root, cdm1.I64, 8, sum(lines)))
+    keys = [32 * (o // 8) + (o % 8) + 1 for o in range(32)]
+    assert as_i64(out).tolist() == np.repeat(keys, lines).tolist()
+
+
+def test_dstride_count_mismatch_and_arity():
+    for counts in ([3, 1], [3, 3]):
+        root = cdm1.Node(cdm1.DSTRIDE, 5, [cdm1.bitpack([7, 9], 2, 7), cdm1.bitpack(counts, 2, 1)], nruns=2, maxrun=3,
+                         stride=1)
+        with pytest.raises(OracleError, match="run"):
+            dec(cdm1.build(root, cdm1.I64, 8, 5))
+    root = cdm1.Node(cdm1.DSTRIDE, 2, [cdm1.bitpack([7, 9], 2, 7)], nruns=2, maxrun=1, stride=1)
+    with pytest.raises(OracleError, match="2 children"):
+        dec(cdm1.build(root, cdm1.I64, 8, 2))
+
+
 # ----------------------------------------------------------------------------- LZ4 (liblz4 + hand sequences)
 
 _lz4 = ctypes.CDLL("liblz4.so.1")
