@@ -57,18 +57,18 @@ WORKLOADS = {
     # BASELINE configs[3]: every lineitem + orders column with the SURVEY Sec. 8d config-4 cascade map (Table 2
     # mapped onto the hot-path codecs), at --sf (default 10; the paper's SF=100 needs ~24 GB of pinned host)
     "config4": dict(sf=10.0, dtype="mixed", cols=[
-        ("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("l_partkey", "BitPack"),
+        ("l_orderkey", "RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]"), ("l_partkey", "BitPack"),
         ("l_suppkey", "BitPack"), ("l_linenumber", "BitPack"), ("l_quantity", "Dict|BitPack"),
         ("l_extendedprice", "Float2Int|BitPack"), ("l_discount", "Dict|BitPack"), ("l_tax", "Dict|BitPack"),
         ("l_returnflag", "ANS"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
         ("l_commitdate", "Dict|BitPack"), ("l_receiptdate", "Dict|BitPack"), ("l_shipinstruct", "Dict|BitPack"),
         ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384),BitPack]"),
-        ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"), ("o_custkey", "BitPack"), ("o_orderstatus", "Dict|BitPack"),
+        ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("o_custkey", "BitPack"), ("o_orderstatus", "Dict|BitPack"),
         ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"), ("o_orderpriority", "Dict|BitPack"),
         ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
         ("o_comment", "Str|[LZ4(sub=16384),BitPack]")],
                     desc="config 4: TPC-H lineitem + orders, all 25 columns (SURVEY Sec. 8d cascade map, "
-                         "l_returnflag ANS per Table 2: FP / scan / RLE / LZ4 / ANS kernels concurrently)"),
+                         "l_returnflag ANS and l_/o_orderkey DeltaStride per Table 2: FP / RLE / LZ4 / ANS kernels concurrently)"),
     # NEXT-1 microbenchmark: the paper's ANS instance -- an L_RETURNFLAG-distributed byte
     # column under chunk-sequential range ANS (4 KiB chunks, one thread per chunk)
     "ans": dict(sf=10.0, dtype="u8", cols=[("l_returnflag", "ANS(chunk=4096)"), ("l_linestatus", "ANS(chunk=4096)")],

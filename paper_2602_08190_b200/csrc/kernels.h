@@ -95,6 +95,7 @@ struct RleDesc {
   uint64_t cnt_base;
   uint64_t val_base;
   uint64_t delta_base;        // V_LINEAR: Delta base
+  uint64_t stride;            // strided (DeltaStride): row j of run g = value_g + j * stride
   uint32_t n;                 // output rows
   uint32_t nruns;
   uint32_t tile0;
@@ -106,7 +107,7 @@ struct RleDesc {
   uint8_t vmode;
   uint8_t out_bytes;          // 4 or 8
   uint8_t d;
-  uint8_t pad[1];
+  uint8_t strided;
 };
 
 struct RleBig {  // queue of oversize tiles, expanded by rle_big

@@ -332,7 +332,7 @@ __device__ __forceinline__ void stg_u32(void* p, uint32_t v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// LIN: the batch has arithmetic-run (V_LINEAR) descriptors; their slope table lives in dynamic shared memory
+// LIN: the batch has arithmetic-run (V_LINEAR or strided) descriptors; their slope table lives in dynamic shared memory
 template <bool TR, bool LIN>
 __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ RleDesc D;
@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
   const uint32_t nr = min(uint32_t(K), D.nruns - g0);
   const uint32_t vmode = D.vmode;
   const bool linear = LIN && vmode == V_LINEAR;
+  const bool strided = LIN && D.strided;  // DeltaStride: arithmetic runs with a per-node stride
+  const bool arith = linear || strided;
+  const uint64_t stride = D.stride;
   const uint32_t ob = D.out_bytes;
   const uint32_t n = D.n;
   const uint32_t cw = D.cnt_w, vw = D.val_w;
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
         en.slot = e;
         en.piece0 = old & ((1ull << 44) - 1);
         en.out_bytes = ob;
-        en.linear = linear;
+        en.linear = arith;
       } else {
         atomicOr(B.err + D.err_idx, 0x2u);
       }
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
         if (k < nr) {
           so[k] = row;
           va[k] = linear ? D.delta_base + wv + val[r] : val[r];
-          sl[k] = linear ? val[r] : 0ull;
+          sl[k] = linear ? val[r] : stride;
         }
         if (linear) wv += val[r] * cnt[r];
         row += cnt[r];
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       if (cnt[r]) {
         cstart_s[c] = row;
         aux_s[c] = linear ? dbase + wv + val[r] : val[r];
-        if (linear) cslope_s[c] = val[r];
+        if (arith) cslope_s[c] = linear ? val[r] : stride;
         c++;
       }
       if (linear) wv += val[r] * cnt[r];
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
       cb += __popcll(wv);
       const int32_t p0 = int32_t(64 * k + b0) - int32_t(a);  // segment row of bit 2l
       uint64_t v0 = aux_s[c0 == 0xFFFFFFFFu ? 0u : c0], v1 = aux_s[c1];
-      if (linear) {
+      if (arith) {
         v0 += uint64_t(int64_t(s0) + p0 - cstart_s[c0 == 0xFFFFFFFFu ? 0u : c0]) * cslope_s[c0 == 0xFFFFFFFFu ? 0u : c0];
         v1 += uint64_t(int64_t(s0) + p0 + 1 - cstart_s[c1]) * cslope_s[c1];
       }

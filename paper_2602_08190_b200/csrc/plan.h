@@ -12,6 +12,7 @@
 #pragma once
 #include <cctype>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -35,6 +36,7 @@ inline int codec_from_name(const std::string& raw) {
   if (b == "float2int") return FLOAT2INT;
   if (b == "delta" || b == "deltaencoding") return DELTA;
   if (b == "rle") return RLE;
+  if (b == "deltastride") return DSTRIDE;
   if (b == "lz4") return LZ4;
   if (b == "str" || b == "string" || b == "varchar") return STR;
   if (b == "ans" || b == "rans") return ANS;
@@ -125,6 +127,7 @@ inline bool complete_tree(TNode* t, std::string* err) {
       break;
     case RLE:
     case STR:
+    case DSTRIDE:
       if (k.empty()) { k.push_back(mk_raw()); k.push_back(mk_raw()); }
       else if (k.size() == 1) k.push_back(mk_raw());
       break;
@@ -138,8 +141,8 @@ inline bool complete_tree(TNode* t, std::string* err) {
 }
 
 inline const char* codec_name(uint8_t c) {
-  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS"};
-  return c < 9 ? N[c] : "?";
+  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS", "DELTASTRIDE"};
+  return c < 10 ? N[c] : "?";
 }
 
 inline void render_tree(const TNode* t, std::string* out) {
@@ -211,17 +214,36 @@ inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* er
     p->text = "rle(arithmetic runs: unpack dv,dc + 2-component look-back + expand)";
     return true;
   }
-  if (is(r, RLE) && bp(kid(r, 1))) {
+  // RLE-family lineages (H7; DeltaStride = RLE with arithmetic runs): an RLE / DeltaStride node
+  // with BitPack counts whose values are BitPack, (top-level RLE only) Dict|BitPack or Float2Int|BitPack, or a
+  // lower level -- Delta|RLE arithmetic runs or another RLE / DeltaStride node -- up to 3 levels (Table 2's
+  // L_ORDERKEY).  Each non-final level expands into an L2-resident array the next level reads.
+  std::function<int(const TNode*, bool)> levels = [&](const TNode* t, bool top) -> int {
+    if (is_delta_rle(t)) return 1;
+    if (!(is(t, RLE) || is(t, DSTRIDE)) || !bp(kid(t, 1))) return 0;
+    const TNode* v = kid(t, 0);
+    if (bp(v)) return 1;
+    if (top && is(t, RLE) && ((is(v, DICT) && bp(kid(v, 1))) || (is(v, FLOAT2INT) && bp(kid(v, 0))))) return 1;
+    const int below = levels(v, false);
+    return below && below < 3 ? below + 1 : 0;
+  };
+  if (const int nl = levels(r, true)) {
     const TNode* v = kid(r, 0);
     p->kind = PlanKind::Rle;
-    if (bp(v)) { p->vmode = 0; p->text = "rle(unpack counts+values, look-back, expand)"; return true; }
-    if (is(v, DICT) && bp(kid(v, 1))) { p->vmode = 1; p->text = "rle(values = dict gather fused, look-back, expand)"; return true; }
-    if (is(v, FLOAT2INT) && bp(kid(v, 0))) { p->vmode = 2; p->text = "rle(values = float2int fused, look-back, expand)"; return true; }
-    if (is_delta_rle(v)) {
+    const char* what = is(r, DSTRIDE) ? "arithmetic runs start + j*stride" : "expand";
+    if (nl > 1) {
       p->vmode = 3;
-      p->text = "rle level 0 (inner Delta|RLE -> run values in L2) + rle level 1 (expand, values = level-0 array)";
-      return true;
+      p->text = std::string(nl == 3 ? "rle level 0 + rle level 1" : "rle level 0") +
+                " (value lineage -> run values in L2) + rle level " + std::to_string(nl - 1) + " (" + what +
+                ", values = previous level's array)";
+    } else if (bp(v)) {
+      p->vmode = 0; p->text = std::string("rle(unpack counts+values, ") + what + ")";
+    } else if (is(v, DICT)) {
+      p->vmode = 1; p->text = "rle(values = dict gather fused, look-back, expand)";
+    } else {
+      p->vmode = 2; p->text = "rle(values = float2int fused, look-back, expand)";
     }
+    return true;
   }
   *err = "no fused device plan for this cascade";
   return false;

@@ -121,18 +121,27 @@ struct BPB {  // a bound BitPack node
   uint64_t base = 0;
 };
 
+// one expansion level of an RLE-family job (deepest first; the last one writes the column)
+struct RleLevel {
+  BPB cnt, val;           // counts; values (V_BP / V_DICT / V_F2I) or slopes dv (V_LINEAR); V_RAW: unused
+  uint8_t vmode = 0;      // RleValueMode; V_RAW = the previous level's array
+  bool strided = false;   // DeltaStride node: row j of run g = value_g + j * stride
+  uint64_t delta_base = 0, stride = 0;
+  uint32_t n = 0, nruns = 0, max_run = 0;
+};
+
 struct Bound {
   const cdm_cascade* casc = nullptr;
   PlanKind kind = PlanKind::RawCopy;
   uint8_t fp_mode = 0, vmode = 0;
   uint64_t rows = 0, payload = 0, offsets_bytes = 0, total = 0, chunk_id = 0;
   uint32_t W = 0;
-  BPB main, counts, inner_dv, inner_dc;
+  BPB main;
+  std::vector<RleLevel> lv;  // PlanKind::Rle
   uint64_t dict_off = 0;
   uint32_t entries = 0;
   uint8_t d = 0;
-  uint64_t delta_base = 0, inner_base = 0;
-  uint32_t nruns = 0, n_inner = 0, max_run = 0, inner_max_run = 0;
+  uint64_t delta_base = 0;
   bool lz4 = false;
   uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
   uint32_t n_sub = 0, lz_sub_bytes = 0, lz_uniform = 0;
@@ -215,8 +224,8 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
   size_t idx = 0;
   if (c.nodes.empty() || t.walk(&idx) != 0 || idx != c.nodes.size()) return fail(CDM_E_CORRUPT, t.err.empty() ? "node table: unused nodes" : t.err);
   for (size_t i = 0; i < c.nodes.size(); i++) {
-    static const int arity[9] = {0, 1, 2, 1, 1, 2, 2, 2, 2};
-    if (c.nodes[i].codec > ANS || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
+    static const int arity[10] = {0, 1, 2, 1, 1, 2, 2, 2, 2, 2};
+    if (c.nodes[i].codec > DSTRIDE || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
       return fail(CDM_E_CORRUPT, "node " + std::to_string(i) + ": bad codec or arity");
   }
   std::string canon;
@@ -296,49 +305,62 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
     }
     case PlanKind::Rle: {
       if (!need_w48()) return fail(CDM_E_UNSUPPORTED, "RLE output width must be 4 or 8");
-      if (b->vmode == V_LINEAR) {  // Delta | RLE | [BitPack dv, BitPack dc]
-        b->delta_base = r.u64_at8();
-        int ri = t.kids[0][0];
-        const Node& rl = c.nodes[ri];
-        if (rl.n != c.rows) return bad("Delta child count mismatch");
-        b->nruns = rl.u32_at0();
-        b->max_run = rl.u32_at4();
-        if (!(e = bind_bp(c, t, t.kids[ri][0], b->nruns, 64, &b->main)).empty()) return bad(e);
-        if (!(e = bind_bp(c, t, t.kids[ri][1], b->nruns, 32, &b->counts)).empty()) return bad(e);
-        break;
+      // the value lineage, deepest level first (compile_plan fixed the shape; here: counts and streams)
+      std::function<std::string(int, uint64_t, bool)> level = [&](int ni, uint64_t rows, bool top) -> std::string {
+        const Node& nd = c.nodes[ni];
+        RleLevel L;
+        L.n = uint32_t(rows);
+        std::string er;
+        int vi = -1;
+        if (nd.codec == DELTA) {  // Delta | RLE | [BitPack dv, BitPack dc]: arithmetic runs
+          L.vmode = V_LINEAR;
+          L.delta_base = nd.u64_at8();
+          const int ri = t.kids[ni][0];
+          const Node& rl = c.nodes[ri];
+          if (rl.n != rows) return "Delta child count mismatch";
+          L.nruns = rl.u32_at0();
+          L.max_run = rl.u32_at4();
+          if (!(er = bind_bp(c, t, t.kids[ri][0], L.nruns, 64, &L.val)).empty()) return er;
+          if (!(er = bind_bp(c, t, t.kids[ri][1], L.nruns, 32, &L.cnt)).empty()) return er;
+        } else {  // RLE or DeltaStride: [values, BitPack counts]
+          L.nruns = nd.u32_at0();
+          L.max_run = nd.u32_at4();
+          if (nd.codec == DSTRIDE) { L.strided = true; L.stride = nd.u64_at8(); }
+          vi = t.kids[ni][0];
+          if (!(er = bind_bp(c, t, t.kids[ni][1], L.nruns, 32, &L.cnt)).empty()) return er;
+          const Node& v = c.nodes[vi];
+          if (v.n != L.nruns) return "RLE values count mismatch";
+          if (v.codec == BITPACK) {
+            L.vmode = V_BP;
+            if (!(er = bind_bp(c, t, vi, L.nruns, 64, &L.val)).empty()) return er;
+          } else if (v.codec == DICT && top) {
+            uint64_t dn;
+            L.vmode = V_DICT;
+            if (!(er = raw_stream(c, t, t.kids[vi][0], W, &b->dict_off, &dn)).empty()) return er;
+            b->entries = v.u32_at0();
+            if (v.u32_at4() != W || dn != b->entries) return "dictionary shape mismatch";
+            if (!(er = bind_bp(c, t, t.kids[vi][1], L.nruns, 64, &L.val)).empty()) return er;
+          } else if (v.codec == FLOAT2INT && top) {
+            if (c.dtype != T_F64) return "!Float2Int needs F64 output";
+            L.vmode = V_F2I;
+            b->d = v.params[0];
+            if (b->d > 22) return "Float2Int exponent > 22";
+            if (!(er = bind_bp(c, t, t.kids[vi][0], L.nruns, 64, &L.val)).empty()) return er;
+          } else {  // a lower level produces this level's run values
+            L.vmode = V_RAW;
+            if (!(er = level(vi, L.nruns, false)).empty()) return er;
+          }
+        }
+        // rows without runs would leave the level's output unwritten with no tile to notice
+        if (L.n && !L.nruns) return "RLE has rows but no runs";
+        b->lv.push_back(L);
+        return "";
+      };
+      if (!(e = level(0, c.rows, true)).empty()) {
+        if (e[0] == '!') return fail(CDM_E_UNSUPPORTED, e.substr(1));
+        return bad(e);
       }
-      b->nruns = r.u32_at0();
-      b->max_run = r.u32_at4();
-      int vi = t.kids[0][0], ci = t.kids[0][1];
-      if (!(e = bind_bp(c, t, ci, b->nruns, 32, &b->counts)).empty()) return bad(e);
-      const Node& v = c.nodes[vi];
-      if (b->vmode == V_BP) {
-        if (!(e = bind_bp(c, t, vi, b->nruns, 64, &b->main)).empty()) return bad(e);
-      } else if (b->vmode == V_DICT) {
-        uint64_t dn;
-        if (v.n != b->nruns) return bad("RLE values count mismatch");
-        if (!(e = raw_stream(c, t, t.kids[vi][0], W, &b->dict_off, &dn)).empty()) return bad(e);
-        b->entries = v.u32_at0();
-        if (v.u32_at4() != W || dn != b->entries) return bad("dictionary shape mismatch");
-        if (!(e = bind_bp(c, t, t.kids[vi][1], b->nruns, 64, &b->main)).empty()) return bad(e);
-      } else if (b->vmode == V_F2I) {
-        if (c.dtype != T_F64) return fail(CDM_E_UNSUPPORTED, "Float2Int needs F64 output");
-        if (v.n != b->nruns) return bad("RLE values count mismatch");
-        b->d = v.params[0];
-        if (b->d > 22) return bad("Float2Int exponent > 22");
-        if (!(e = bind_bp(c, t, t.kids[vi][0], b->nruns, 64, &b->main)).empty()) return bad(e);
-      } else {  // V_DRLE: values = Delta | RLE | [BitPack dv, BitPack dc]
-        if (v.n != b->nruns) return bad("RLE values count mismatch");
-        b->inner_base = v.u64_at8();
-        int ri = t.kids[vi][0];
-        const Node& rl = c.nodes[ri];
-        if (rl.n != b->nruns) return bad("inner RLE count mismatch");
-        b->n_inner = rl.u32_at0();
-        b->inner_max_run = rl.u32_at4();
-        if (b->nruns && !b->n_inner) return bad("inner RLE has no runs");
-        if (!(e = bind_bp(c, t, t.kids[ri][0], b->n_inner, 64, &b->inner_dv)).empty()) return bad(e);
-        if (!(e = bind_bp(c, t, t.kids[ri][1], b->n_inner, 32, &b->inner_dc)).empty()) return bad(e);
-      }
+      if (b->lv.size() > 3) return bad("RLE lineage deeper than 3 levels");
       break;
     }
     case PlanKind::Ans: {
@@ -589,24 +611,28 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     sb.lb = A.take<uint4>(tiles);
     B->scan.push_back(sb);
   }
-  // RLE units: one per RLE job; a Delta|RLE value lineage (V_DRLE) adds a level-0 unit that expands the
-  // inner arithmetic runs into the outer run values V (an L2-resident u64 array), read by the job's level-1
-  // unit as V_RAW.  Every unit has its own tile sums / prefixes; level-0 launches precede level-1 ones.
-  struct RleUnit { int job; bool level0; };
+  // RLE units: one per expansion level of each RLE job (deepest first).  A non-final level (the value lineage
+  // of Delta|RLE or DeltaStride nodes) expands into an L2-resident u64 array that the job's next level reads as
+  // V_RAW.  Units run in rounds aligned at the end (every job's final level in the last round); every unit has
+  // its own tile sums / prefixes, and each round's launches follow the previous round's (PDL-chained).
+  struct RleUnit { int job; int level; int round; bool final; };
   std::vector<RleUnit> units;
+  int rounds = 0;
+  for (int j : rlj) rounds = std::max(rounds, int(B->jobs[j].lv.size()));
   for (int j : rlj) {
-    if (B->jobs[j].vmode == V_DRLE) units.push_back({j, true});
-    units.push_back({j, false});
+    const int nl = int(B->jobs[j].lv.size());
+    for (int l = 0; l < nl; l++) units.push_back({j, l, rounds - nl + l, l == nl - 1});
   }
-  auto unit_groups = [&](int level) {  // unit indices (level -1: all), <= kMaxBatch per group
+  auto unit_groups = [&](int round) {  // unit indices (round -1: all), <= kMaxBatch per group
     std::vector<std::vector<int>> g;
     for (int u = 0; u < int(units.size()); u++) {
-      if (level >= 0 && units[u].level0 != (level == 0)) continue;
+      if (round >= 0 && units[u].round != round) continue;
       if (g.empty() || g.back().size() == size_t(kMaxBatch)) g.emplace_back();
       g.back().push_back(u);
     }
     return g;
   };
+  auto lvl = [&](int u) -> const RleLevel& { return B->jobs[units[u].job].lv[units[u].level]; };
   std::vector<std::pair<int, int>> sums_at(units.size()), rle_at(units.size());  // (batch, desc) per unit
   for (auto& g : unit_groups(-1)) {
     SumsBatch sb{};
@@ -614,21 +640,14 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     uint32_t nunits = 0;
     for (int u : g) {
       const Bound& b = B->jobs[units[u].job];
+      const RleLevel& L = lvl(u);
       sums_at[u] = {int(B->sums.size()), int(sb.n)};
       SumsChunk& d = sb.d[sb.n++];
-      if (units[u].level0) {  // inner RLE: counts dc, slopes dv over the outer runs
-        d.cnt_packed = b.dev_chunk + b.inner_dc.off; d.cnt_base = b.inner_dc.base; d.cnt_w = uint16_t(b.inner_dc.w);
-        d.dv_packed = b.dev_chunk + b.inner_dv.off; d.dv_base = b.inner_dv.base; d.dv_w = uint16_t(b.inner_dv.w);
-        d.linear = 1;
-        d.nruns = b.n_inner;
-        d.rows = b.nruns;
-      } else {
-        d.cnt_packed = b.dev_chunk + b.counts.off; d.cnt_base = b.counts.base; d.cnt_w = uint16_t(b.counts.w);
-        d.linear = b.vmode == V_LINEAR;
-        if (d.linear) { d.dv_packed = b.dev_chunk + b.main.off; d.dv_base = b.main.base; d.dv_w = uint16_t(b.main.w); }
-        d.nruns = b.nruns;
-        d.rows = uint32_t(b.rows);
-      }
+      d.cnt_packed = b.dev_chunk + L.cnt.off; d.cnt_base = L.cnt.base; d.cnt_w = uint16_t(L.cnt.w);
+      d.linear = L.vmode == V_LINEAR;
+      if (d.linear) { d.dv_packed = b.dev_chunk + L.val.off; d.dv_base = L.val.base; d.dv_w = uint16_t(L.val.w); }
+      d.nruns = L.nruns;
+      d.rows = L.n;
       d.tiles = uint32_t(div_up(d.nruns, kRleTile));
       d.units = uint32_t(div_up(uint64_t(d.tiles) * kRleTile, 8192));  // rle_sums CTA: 8 warps x 1024 runs
       d.unit0 = nunits;
@@ -638,51 +657,41 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     sb.total_units = nunits;
     B->sums.push_back(sb);
   }
-  for (int level = 0; level < 2; level++) {
-    if (level == 1) B->rle_level0 = B->rle.size();
-    for (auto& g : unit_groups(level)) {
+  for (int round = 0; round < rounds; round++) {
+    if (round == rounds - 1) B->rle_level0 = B->rle.size();
+    for (auto& g : unit_groups(round)) {
       RleBatch rb{};
       rb.err = B->err_dev;
       uint32_t tiles = 0, slots = 0;
       for (int u : g) {
         const Bound& b = B->jobs[units[u].job];
+        const RleLevel& L = lvl(u);
         rle_at[u] = {int(B->rle.size()), int(rb.n)};
         RleDesc& d = rb.d[rb.n++];
-        uint32_t max_run;
-        if (units[u].level0) {
-          d.cnt_packed = b.dev_chunk + b.inner_dc.off; d.cnt_base = b.inner_dc.base; d.cnt_w = uint16_t(b.inner_dc.w);
-          d.val_packed = b.dev_chunk + b.inner_dv.off; d.val_base = b.inner_dv.base; d.val_w = uint16_t(b.inner_dv.w);
-          d.vmode = V_LINEAR;
-          d.delta_base = b.inner_base;
-          d.out_bytes = 8;
-          d.n = b.nruns;
-          d.nruns = b.n_inner;
-          max_run = b.inner_max_run;  // d.out: the V array, assigned below
-        } else {
-          d.cnt_packed = b.dev_chunk + b.counts.off; d.cnt_base = b.counts.base; d.cnt_w = uint16_t(b.counts.w);
-          d.val_packed = b.vmode == V_DRLE ? nullptr : b.dev_chunk + b.main.off;  // V_RAW: assigned below
-          d.val_base = b.main.base;
-          d.val_w = uint16_t(b.main.w);
-          d.dict = b.vmode == V_DICT ? b.dev_chunk + b.dict_off : nullptr;
-          d.entries = b.entries;
-          d.d = b.d;
-          d.vmode = b.vmode == V_DRLE ? uint8_t(V_RAW) : b.vmode;
-          d.out = b.out;
-          d.out_bytes = uint8_t(b.W);
-          d.delta_base = b.delta_base;
-          d.n = uint32_t(b.rows);
-          d.nruns = b.nruns;
-          max_run = b.max_run;
-        }
+        d.cnt_packed = b.dev_chunk + L.cnt.off; d.cnt_base = L.cnt.base; d.cnt_w = uint16_t(L.cnt.w);
+        d.val_packed = L.vmode == V_RAW ? nullptr : b.dev_chunk + L.val.off;  // V_RAW: assigned below
+        d.val_base = L.val.base;
+        d.val_w = uint16_t(L.val.w);
+        d.dict = L.vmode == V_DICT ? b.dev_chunk + b.dict_off : nullptr;
+        d.entries = b.entries;
+        d.d = b.d;
+        d.vmode = L.vmode;
+        d.strided = L.strided;
+        d.stride = L.stride;
+        d.delta_base = L.delta_base;
+        d.out = units[u].final ? b.out : nullptr;  // non-final: the level's array, assigned below
+        d.out_bytes = units[u].final ? uint8_t(b.W) : uint8_t(8);
+        d.n = L.n;
+        d.nruns = L.nruns;
         d.tile0 = tiles;
         d.ntiles = uint32_t(div_up(d.nruns, kRleTile));
         d.err_idx = uint32_t(units[u].job);
-        if (d.vmode == V_LINEAR) rb.any_linear = 1;
+        if (d.vmode == V_LINEAR || d.strided) rb.any_linear = 1;
         tiles += d.ntiles;
         slots += d.n / kRleBigLimit + 1;
         // the header's max run bounds a tile's output; only then can rle_big be skipped (a lying header
         // only costs speed: oversize tiles are then expanded in place)
-        if (uint64_t(kRleTile) * max_run > kRleBigLimit) rb.big_enabled = 1;
+        if (uint64_t(kRleTile) * L.max_run > kRleBigLimit) rb.big_enabled = 1;
       }
       rb.total_tiles = tiles;
       rb.big.counter = A.take<unsigned long long>(1);
@@ -698,15 +707,15 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     for (auto& pb : B->sums) pb.trace = A.take<uint64_t>(size_t(pb.total_units) * 8);
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
-  // ---- non-zeroed region: tile sums + prefixes per RLE unit, big-tile slots, level-0 run values
+  // ---- non-zeroed region: tile sums + prefixes per RLE unit, big-tile slots, lineage arrays
   for (size_t u = 0; u < units.size(); u++) {
     SumsChunk& d = B->sums[sums_at[u].first].d[sums_at[u].second];
     d.tsum = A.take<uint64_t>(size_t(d.tiles) * 2);
     B->rle[rle_at[u].first].d[rle_at[u].second].tsum = d.tsum;
   }
   for (size_t u = 0; u < units.size(); u++) {
-    if (!units[u].level0) continue;
-    uint64_t* V = A.take<uint64_t>(B->jobs[units[u].job].nruns + 4);
+    if (units[u].final) continue;  // units u, u + 1 are consecutive levels of one job
+    uint64_t* V = A.take<uint64_t>(size_t(lvl(int(u)).n) + 4);
     B->rle[rle_at[u].first].d[rle_at[u].second].out = V;
     B->rle[rle_at[u + 1].first].d[rle_at[u + 1].second].val_packed = reinterpret_cast<const uint8_t*>(V);
   }

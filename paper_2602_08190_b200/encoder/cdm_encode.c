@@ -32,7 +32,7 @@ extern int LZ4_compress_default(const char *src, char *dst, int srcSize, int dst
 extern int LZ4_compress_HC(const char *src, char *dst, int srcSize, int dstCapacity, int level);
 extern int LZ4_compressBound(int inputSize);
 
-enum { C_RAW = 0, C_BITPACK = 1, C_DICT = 2, C_FLOAT2INT = 3, C_DELTA = 4, C_RLE = 5, C_LZ4 = 6, C_STR = 7, C_ANS = 8 };
+enum { C_RAW = 0, C_BITPACK = 1, C_DICT = 2, C_FLOAT2INT = 3, C_DELTA = 4, C_RLE = 5, C_LZ4 = 6, C_STR = 7, C_ANS = 8, C_DSTRIDE = 9 };
 enum { D_I32 = 0, D_I64 = 1, D_F64 = 2, D_FIXED = 3, D_VARBYTES = 4 };
 enum { E_OK = 0, E_INVALID_ARG = 1, E_PARSE = 2, E_UNSUPPORTED = 3, E_CORRUPT = 4, E_CAPACITY = 5, E_OOM = 7 };
 
@@ -53,6 +53,7 @@ typedef struct tnode {
   uint32_t ans_chunk; /* ANS(chunk=...) bytes per independently coded chunk */
   uint32_t ans_tl;    /* ANS(tl=...) table log */
   uint32_t ans_il;    /* ANS(il=1|32) interleaved states per chunk (0 = default 32) */
+  int64_t stride;     /* DeltaStride(stride=k), default 1 */
 } tnode;
 
 typedef struct { const char *s; size_t pos; int err; } parser;
@@ -69,6 +70,7 @@ static int codec_of(const char *name) {
   if (!strcmp(b, "float2int")) return C_FLOAT2INT;
   if (!strcmp(b, "delta") || !strcmp(b, "deltaencoding")) return C_DELTA;
   if (!strcmp(b, "rle")) return C_RLE;
+  if (!strcmp(b, "deltastride")) return C_DSTRIDE;
   if (!strcmp(b, "lz4")) return C_LZ4;
   if (!strcmp(b, "str") || !strcmp(b, "string") || !strcmp(b, "varchar")) return C_STR;
   if (!strcmp(b, "ans") || !strcmp(b, "rans")) return C_ANS;
@@ -102,6 +104,7 @@ static tnode *parse_node(parser *p) {
   t->ans_chunk = 0;   /* default: 16384 with 32 interleaved states, 4096 with one */
   t->ans_tl = 12;
   t->ans_il = 32;
+  t->stride = 1;
   skip_ws(p);
   if (p->s[p->pos] == '(') { /* options k=v,... */
     p->pos++;
@@ -123,6 +126,7 @@ static tnode *parse_node(parser *p) {
       else if (!strcmp(key, "chunk")) t->ans_chunk = (uint32_t)v;
       else if (!strcmp(key, "tl")) t->ans_tl = (uint32_t)v;
       else if (!strcmp(key, "il")) t->ans_il = (uint32_t)v;
+      else if (!strcmp(key, "stride")) t->stride = (int64_t)v;
       skip_ws(p);
       if (p->s[p->pos] == ',') { p->pos++; continue; }
       if (p->s[p->pos] == ')') { p->pos++; break; }
@@ -156,7 +160,7 @@ static tnode *parse_node(parser *p) {
 
 static tnode *mk(int codec) {
   tnode *t = (tnode *)calloc(1, sizeof(tnode));
-  t->codec = codec; t->lz4_sub = 65536; t->ans_chunk = 0; t->ans_tl = 12; t->ans_il = 32;
+  t->codec = codec; t->lz4_sub = 65536; t->ans_chunk = 0; t->ans_tl = 12; t->ans_il = 32; t->stride = 1;
   return t;
 }
 
@@ -184,7 +188,7 @@ static int complete(tnode *t) {
       if (t->nchild == 0) { t->child[t->nchild++] = mk(C_RAW); }
       if (t->nchild != 1) return fail(E_PARSE, "arity error: Float2Int/Delta take one child");
       break;
-    case C_RLE: case C_STR:
+    case C_RLE: case C_STR: case C_DSTRIDE:
       if (t->nchild == 0) { t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; }
       else if (t->nchild == 1) { t->child[1] = mk(C_RAW); t->nchild = 2; }
       break;
@@ -194,7 +198,7 @@ static int complete(tnode *t) {
   return 0;
 }
 
-static const char *NAMES[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS"};
+static const char *NAMES[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS", "DELTASTRIDE"};
 static void render(const tnode *t, char *buf, size_t cap) {
   strncat(buf, NAMES[t->codec], cap - strlen(buf) - 1);
   if (!t->nchild) return;
@@ -450,6 +454,31 @@ static int enc_rle(builder *b, const tnode *t, col_t in) {
   return enc_int_child(b, t->child[1], cnt, nr);
 }
 
+/* DeltaStride (reading R9): greedy maximal arithmetic runs x, x+k, x+2k, ... for the node's stride
+ * k (mod 2^64) -> starts, counts. */
+static int enc_dstride(builder *b, const tnode *t, col_t in) {
+  int64_t *v = to_int(&in);
+  if (!v) return fail(E_UNSUPPORTED, "DeltaStride needs an integer stream");
+  const uint64_t k = (uint64_t)t->stride;
+  int64_t *st = (int64_t *)malloc((in.n ? in.n : 1) * sizeof(int64_t));
+  int64_t *cnt = (int64_t *)malloc((in.n ? in.n : 1) * sizeof(int64_t));
+  uint64_t nr = 0, maxrun = 0;
+  for (uint64_t i = 0; i < in.n; i++) {
+    if (nr && (uint64_t)v[i] - (uint64_t)v[i - 1] == k) cnt[nr - 1]++;
+    else { st[nr] = v[i]; cnt[nr] = 1; nr++; }
+  }
+  free(v);
+  for (uint64_t g = 0; g < nr; g++) if ((uint64_t)cnt[g] > maxrun) maxrun = (uint64_t)cnt[g];
+  node_rec r; memset(&r, 0, sizeof r);
+  r.codec = C_DSTRIDE; r.nchild = 2; r.stream = 0xFFFF; r.n = in.n;
+  uint32_t nr32 = (uint32_t)nr, mr32 = (uint32_t)(maxrun > 0xFFFFFFFFull ? 0xFFFFFFFFull : maxrun);
+  memcpy(r.p, &nr32, 4); memcpy(r.p + 4, &mr32, 4); memcpy(r.p + 8, &k, 8);
+  add_node(b, r);
+  int rc = enc_int_child(b, t->child[0], st, nr);
+  if (rc) { free(cnt); return rc; }
+  return enc_int_child(b, t->child[1], cnt, nr);
+}
+
 /* LZ4 block format per independent sub-chunk of `sub` decompressed bytes. */
 static int enc_lz4(builder *b, const tnode *t, col_t in) {
   if (in.is_int || in.eb != 1) return fail(E_UNSUPPORTED, "LZ4 needs a byte stream");
@@ -599,6 +628,7 @@ static int encode_node(builder *b, const tnode *t, col_t in) {
     case C_LZ4: return enc_lz4(b, t, in);
     case C_STR: return enc_str(b, t, in);
     case C_ANS: return enc_ans(b, t, in);
+    case C_DSTRIDE: return enc_dstride(b, t, in);
   }
   return fail(E_UNSUPPORTED, "unknown codec");
 }

@@ -45,6 +45,10 @@ def test_kernels_are_sm100a_sass():
     ("RLE|[BitPack,BitPack]", cdm.I32, "rle("),
     ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 0"),
     ("Delta|RLE|[BitPack,BitPack]", cdm.I64, "arithmetic runs"),
+    ("DeltaStride|[BitPack,BitPack]", cdm.I64, "start + j*stride"),
+    ("DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 1 (arithmetic runs"),
+    ("RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]", cdm.I64, "rle level 2"),
+    ("RLE|[RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 1 (expand"),
     ("Str|[LZ4,BitPack]", cdm.VARBYTES, "lz4_group_decode"),
     ("Str|[ANS,BitPack]", cdm.VARBYTES, "ans_chunk_decode"),
     ("ANS", cdm.FIXED, "ans_chunk_decode"),
@@ -57,7 +61,7 @@ def test_cascade_plans(spec, dtype, plan):
 
 
 @pytest.mark.parametrize("spec,code", [("RLE|[BitPack", 2), ("Nope", 2), ("BitPack|[Raw,Raw]", 2),
-                                       ("RLE|[RLE|[BitPack,BitPack],BitPack]", 3), ("Str|[LZ4,BitPack]", 3)])
+                                       ("Delta|Delta|BitPack", 3), ("Str|[LZ4,BitPack]", 3)])
 def test_cascade_errors(spec, code):
     with pytest.raises(cdm.CdmError) as e:
         cdm.Cascade(spec, cdm.I64)

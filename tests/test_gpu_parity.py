@@ -141,6 +141,12 @@ TPCH_CASES = [
     ("l_comment", "Str|[LZ4,BitPack]"),
     ("l_comment", "Str|[Raw,BitPack]"),
     ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"),
+    ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"),                 # Table 2 O_ORDERKEY
+    ("l_orderkey", "RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]"),  # Table 2 L_ORDERKEY
+    ("o_orderkey", "DeltaStride|[BitPack,BitPack]"),
+    ("l_orderkey", "DeltaStride(stride=0)|[BitPack,BitPack]"),
+    ("l_orderkey", "RLE|[RLE|[BitPack,BitPack],BitPack]"),
+    ("l_orderkey", "RLE|[DeltaStride|[BitPack,BitPack],BitPack]"),
     ("o_custkey", "BitPack"),
     ("o_orderstatus", "Dict|BitPack"),
     ("o_totalprice", "Float2Int|BitPack"),
@@ -251,6 +257,47 @@ def test_giant_runs(engine):
     col = Column("big", I64, 8, int(counts.sum()), np.repeat(vals, counts))
     check_parity(engine, "RLE|[BitPack,BitPack]", col, both=False)
     check_parity(engine, "Delta|RLE|[BitPack,BitPack]", col, both=False)
+
+
+@pytest.mark.parametrize("stride", [1, 3, -7, 0])
+def test_dstride_random_runs(engine, stride):
+    """DeltaStride over random arithmetic runs: many tiles, int64 and int32 (wrapping) output."""
+    rng = np.random.default_rng(20 + stride)
+    nr = 300_000
+    counts = rng.integers(1, 9, size=nr)
+    counts[rng.integers(0, nr, size=200)] = rng.integers(100, 5000, size=200)
+    starts = rng.integers(-(1 << 40), 1 << 40, size=nr)
+    n = int(counts.sum())
+    idx = np.arange(n) - np.repeat(np.cumsum(counts) - counts, counts)
+    v = np.repeat(starts, counts) + idx * stride
+    spec = f"DeltaStride(stride={stride & ((1 << 64) - 1)})|[BitPack,BitPack]"
+    check_parity(engine, spec, Column("ds", I64, 8, n, v.astype(np.int64)), rows_per_chunk=1_000_003)
+    v32 = (np.repeat(starts % 1000, counts) + idx * stride).astype(np.int32)[:700_001]
+    check_parity(engine, spec, Column("ds32", I32, 4, v32.size, v32), both=False)
+
+
+def test_dstride_giant_runs(engine):
+    """Arithmetic runs far above the big-tile limit (rle_big with a stride), at every lineage depth."""
+    n = 5_000_000
+    keys = np.arange(n, dtype=np.int64) * 3 + 11
+    keys[2_000_000:] += 1000
+    col = Column("seq", I64, 8, n, keys)
+    check_parity(engine, "DeltaStride(stride=3)|[BitPack,BitPack]", col, rows_per_chunk=4_194_304, both=False)
+    check_parity(engine, "DeltaStride(stride=3)|[Delta|RLE|[BitPack,BitPack],BitPack]", col, both=False)
+    lines = np.repeat(keys[:1_000_000], np.tile([1, 2, 7], 333_334)[:1_000_000])
+    check_parity(engine, "RLE|[DeltaStride(stride=3)|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]",
+                 Column("lk", I64, 8, lines.size, lines), both=False)
+
+
+def test_corrupt_dstride_counts_set_error(engine):
+    spec = "RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]"
+    inner = cdm1.Node(cdm1.RLE, 4, [cdm1.bitpack([0, 32], 6, 0), cdm1.bitpack([1, 3], 2, 0)], nruns=2, maxrun=3)
+    ds = cdm1.Node(cdm1.DSTRIDE, 32, [cdm1.Node(cdm1.DELTA, 4, [inner], base=1), cdm1.bitpack([8, 8, 8, 9], 4, 0)],
+                   nruns=4, maxrun=9, stride=1)  # level-1 counts sum to 33 != 32
+    root = cdm1.Node(cdm1.RLE, 64, [ds, cdm1.bitpack([2] * 32, 2, 0)], nruns=32, maxrun=2)
+    ch = cdm1.build(root, cdm1.I64, 8, 64, cascade_hash=_hash(spec))
+    (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.I64), [ch], resident=True, expect_error=True)
+    assert r["error_bits"] & cdm.ERR_RUN_SUM
 
 
 def test_rle_zero_length_runs(engine):
