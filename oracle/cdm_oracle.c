@@ -25,6 +25,10 @@
  *   DeltaStride    PAPER.md:481 (Sec. 5.3, "(start, stride, count) triples", an RLE variant), DESIGN.md reading
  *                  R9: children [starts, counts], one stride per node; run g fills [presum_{g-1}, presum_g)
  *                  with start_g + j*stride, j = 0, 1, ... (mod 2^64); presum must end at n.
+ *   StrDict        PAPER.md:163 (Sec. 2.1 String-dictionary: "substituting them with dictionary indices"), :498
+ *                  (each unique word a group expanded from the dictionary), reading R34: children
+ *                  [dictionary = u32 offsets[E+1] + token bytes, token ids]; out = concatenation of the
+ *                  ids' tokens, which must total the node's n bytes.
  *   Str            DESIGN.md reading R17: offsets_0 = 0, offsets_{i+1} = offsets_i + len_i.
  *   Nesting        PAPER.md:509 (Table 2 notation), decoded depth-first: children first, then parent
  *                  (no fusion exists in the oracle).
@@ -43,7 +47,7 @@
 
 /* oracle's own constants (the format spec is DESIGN.md's, restated here independently) */
 #define O_MAGIC 0x314D4443u
-enum { OC_RAW = 0, OC_BITPACK = 1, OC_DICT = 2, OC_FLOAT2INT = 3, OC_DELTA = 4, OC_RLE = 5, OC_LZ4 = 6, OC_STR = 7, OC_ANS = 8, OC_DSTRIDE = 9 };
+enum { OC_RAW = 0, OC_BITPACK = 1, OC_DICT = 2, OC_FLOAT2INT = 3, OC_DELTA = 4, OC_RLE = 5, OC_LZ4 = 6, OC_STR = 7, OC_ANS = 8, OC_DSTRIDE = 9, OC_STRDICT = 10 };
 enum { OT_I32 = 0, OT_I64 = 1, OT_F64 = 2, OT_FIXED = 3, OT_VARBYTES = 4 };
 enum { OK = 0, ERR_ARG = 1, ERR_UNSUPPORTED = 3, ERR_CORRUPT = 4, ERR_CAPACITY = 5, ERR_OOM = 7 };
 
@@ -257,6 +261,36 @@ static int decode_node(ochunk *c, uint32_t *idx, ostream *out) {
     free(st.data); free(cnt.data);
     if (pos != n) { free(o); return bad(c, "run sum %llu != %llu rows", pos, n); }
     out->n = n; out->eb = 8; out->is_int = 1; out->data = (uint8_t *)o;
+    return OK;
+  }
+  case OC_STRDICT: {
+    /* "each unique word serve as a group ... and expands according to the lookup dictionary". */
+    if (nch != 2) return bad(c, "node %llu: StrDict needs 2 children, has %llu", me, nch);
+    uint32_t E = rd32(pr), dbytes = rd32(pr + 4);
+    ostream dict, ix;
+    int rc = decode_node(c, idx, &dict);
+    if (rc) return rc;
+    if (dict.eb != 1 || dict.is_int || dict.n != 4ull * (E + 1ull) + dbytes) { free(dict.data); return bad(c, "node %llu: dictionary stream of %llu bytes", me, dict.n); }
+    const uint8_t *tok = dict.data + 4ull * (E + 1ull);
+    for (uint32_t e = 0; e < E; e++)
+      if (rd32(dict.data + 4ull * e) > rd32(dict.data + 4ull * e + 4)) { free(dict.data); return bad(c, "token %llu: offsets decrease (%llu)", e, 0); }
+    if (rd32(dict.data) != 0 || rd32(dict.data + 4ull * E) != dbytes) { free(dict.data); return bad(c, "node %llu: dictionary offsets end at %llu", me, rd32(dict.data + 4ull * E)); }
+    rc = decode_int_child(c, idx, &ix);
+    if (rc) { free(dict.data); return rc; }
+    uint8_t *o = (uint8_t *)alloc_n(n, 1);
+    if (!o) { free(dict.data); free(ix.data); return bad(c, "node %llu: cannot hold %llu bytes", me, n); }
+    uint64_t pos = 0;
+    for (uint64_t k = 0; k < ix.n; k++) {
+      uint64_t id = rd64(ix.data + 8 * k);
+      if (id >= E) { free(dict.data); free(ix.data); free(o); return bad(c, "token %llu: dictionary index %llu out of range", k, id); }
+      uint32_t a = rd32(dict.data + 4 * id), l = rd32(dict.data + 4 * id + 4) - a;
+      if (l > n - pos) { free(dict.data); free(ix.data); free(o); return bad(c, "token %llu: bytes overflow the %llu output bytes", k, n); }
+      memcpy(o + pos, tok + a, l);
+      pos += l;
+    }
+    free(dict.data); free(ix.data);
+    if (pos != n) { free(o); return bad(c, "token bytes %llu != %llu", pos, n); }
+    out->n = n; out->eb = 1; out->is_int = 0; out->data = o;
     return OK;
   }
   case OC_LZ4: {

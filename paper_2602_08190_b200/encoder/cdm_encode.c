@@ -32,7 +32,7 @@ extern int LZ4_compress_default(const char *src, char *dst, int srcSize, int dst
 extern int LZ4_compress_HC(const char *src, char *dst, int srcSize, int dstCapacity, int level);
 extern int LZ4_compressBound(int inputSize);
 
-enum { C_RAW = 0, C_BITPACK = 1, C_DICT = 2, C_FLOAT2INT = 3, C_DELTA = 4, C_RLE = 5, C_LZ4 = 6, C_STR = 7, C_ANS = 8, C_DSTRIDE = 9 };
+enum { C_RAW = 0, C_BITPACK = 1, C_DICT = 2, C_FLOAT2INT = 3, C_DELTA = 4, C_RLE = 5, C_LZ4 = 6, C_STR = 7, C_ANS = 8, C_DSTRIDE = 9, C_STRDICT = 10 };
 enum { D_I32 = 0, D_I64 = 1, D_F64 = 2, D_FIXED = 3, D_VARBYTES = 4 };
 enum { E_OK = 0, E_INVALID_ARG = 1, E_PARSE = 2, E_UNSUPPORTED = 3, E_CORRUPT = 4, E_CAPACITY = 5, E_OOM = 7 };
 
@@ -71,6 +71,7 @@ static int codec_of(const char *name) {
   if (!strcmp(b, "delta") || !strcmp(b, "deltaencoding")) return C_DELTA;
   if (!strcmp(b, "rle")) return C_RLE;
   if (!strcmp(b, "deltastride")) return C_DSTRIDE;
+  if (!strcmp(b, "strdict") || !strcmp(b, "stringdictionary")) return C_STRDICT;
   if (!strcmp(b, "lz4")) return C_LZ4;
   if (!strcmp(b, "str") || !strcmp(b, "string") || !strcmp(b, "varchar")) return C_STR;
   if (!strcmp(b, "ans") || !strcmp(b, "rans")) return C_ANS;
@@ -172,14 +173,15 @@ static int complete(tnode *t) {
     case C_BITPACK:
       if (t->nchild == 0) { t->child[t->nchild++] = mk(C_RAW); return 0; }
       if (t->nchild == 1 && t->child[0]->codec == C_RAW) return 0;
-      return fail(E_PARSE, "arity error: BitPack's only child is Raw");
+      if (t->nchild == 1 && t->child[0]->codec == C_ANS) break;  /* packed bytes entropy coded (Table 2 O_COMMENT) */
+      return fail(E_PARSE, "arity error: BitPack's only child is Raw or ANS");
     case C_LZ4:
       if (t->nchild != 0) return fail(E_PARSE, "arity error: LZ4 takes no children");
       t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; return 0;
     case C_ANS:
       if (t->nchild != 0) return fail(E_PARSE, "arity error: ANS takes no children");
       t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; return 0;
-    case C_DICT:
+    case C_DICT: case C_STRDICT:
       if (t->nchild == 0) { t->child[0] = mk(C_RAW); t->child[1] = mk(C_RAW); t->nchild = 2; }
       else if (t->nchild == 1) { t->child[1] = t->child[0]; t->child[0] = mk(C_RAW); t->nchild = 2; }
       if (t->child[0]->codec != C_RAW) return fail(E_PARSE, "arity error: Dict's dictionary stream is Raw");
@@ -198,7 +200,7 @@ static int complete(tnode *t) {
   return 0;
 }
 
-static const char *NAMES[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS", "DELTASTRIDE"};
+static const char *NAMES[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS", "DELTASTRIDE", "STRDICT"};
 static void render(const tnode *t, char *buf, size_t cap) {
   strncat(buf, NAMES[t->codec], cap - strlen(buf) - 1);
   if (!t->nchild) return;
@@ -300,7 +302,7 @@ static int enc_raw(builder *b, col_t in) {
 }
 
 /* BitPack + FOR: base = min, w = ceil(log2(max-min+1)), LSB-first contiguous bits. */
-static int enc_bitpack(builder *b, col_t in) {
+static int enc_bitpack(builder *b, const tnode *t, col_t in) {
   int64_t *v = to_int(&in);
   if (!v) return fail(E_UNSUPPORTED, "BitPack needs an integer stream");
   int64_t mn = 0, mx = 0;
@@ -322,6 +324,12 @@ static int enc_bitpack(builder *b, col_t in) {
   r.codec = C_BITPACK; r.nchild = 1; r.stream = 0xFFFF; r.n = in.n;
   r.p[0] = (uint8_t)w; memcpy(r.p + 8, &mn, 8);
   add_node(b, r);
+  if (t && t->nchild == 1 && t->child[0]->codec == C_ANS) {  /* the packed bytes go through ANS */
+    col_t pc = {nbytes, 1, 0, pk, NULL};
+    int rc = encode_node(b, t->child[0], pc);
+    free(pk);
+    return rc;
+  }
   node_rec raw; memset(&raw, 0, sizeof raw);
   raw.codec = C_RAW; raw.stream = (uint16_t)add_stream(b, pk, nbytes); raw.n = nbytes; raw.u32a = 1;
   add_node(b, raw);
@@ -602,6 +610,76 @@ static int enc_ans(builder *b, const tnode *t, col_t in) {
 }
 
 /* Str: VARBYTES rows -> [concatenated bytes, per-row lengths]. */
+/* String-dictionary ("tokenizing on spaces and periods"; reading R34): a token
+ * is a maximal run of non-delimiter bytes followed by its trailing delimiters (space, period), cut at string
+ * boundaries and at kStrDictMaxTok bytes; the dictionary holds the unique tokens in first-appearance order.
+ * Children: [Raw dictionary = u32 offsets[E+1] (from the token bytes' start) + token bytes, token ids]. */
+static __thread const int64_t *g_str_offs;
+static __thread uint64_t g_str_rows;
+#define kStrDictMaxTok 32u
+static int sd_delim(uint8_t c) { return c == ' ' || c == '.'; }
+static int enc_strdict(builder *b, const tnode *t, col_t in) {
+  if (in.is_int || in.eb != 1) return fail(E_UNSUPPORTED, "StrDict needs a byte stream");
+  const uint8_t *d = in.data;
+  uint64_t *ts = (uint64_t *)malloc((in.n + 1) * sizeof(uint64_t)); /* token starts; ts[ntok] = n */
+  uint64_t ntok = 0;
+  const int64_t *so = g_str_offs;
+  uint64_t srow = 0, next_bound = so ? (uint64_t)(so[1] - so[0]) : in.n;
+  for (uint64_t i = 0; i < in.n; i++) {
+    int start = ntok == 0;
+    while (so && srow < g_str_rows && i >= next_bound) { /* string boundary (skips empty strings) */
+      start = 1; srow++;
+      next_bound = srow < g_str_rows ? (uint64_t)(so[srow + 1] - so[0]) : in.n;
+    }
+    if (!start && !sd_delim(d[i]) && sd_delim(d[i - 1])) start = 1;
+    if (!start && i - ts[ntok - 1] >= kStrDictMaxTok) start = 1;
+    if (start) ts[ntok++] = i;
+  }
+  ts[ntok] = in.n;
+  uint64_t cap = 16;
+  while (cap < 2 * (ntok ? ntok : 1)) cap <<= 1;
+  uint64_t *tab = (uint64_t *)calloc(cap, sizeof(uint64_t)); /* slot -> 1 + first token index */
+  int64_t *ids = (int64_t *)malloc((ntok ? ntok : 1) * sizeof(int64_t));
+  uint64_t *first = (uint64_t *)malloc((ntok ? ntok : 1) * sizeof(uint64_t)); /* id -> a token index */
+  uint32_t *id_of_slot = (uint32_t *)malloc(cap * sizeof(uint32_t));
+  if (!ts || !tab || !ids || !first || !id_of_slot) { free(ts); free(tab); free(ids); free(first); free(id_of_slot); return fail(E_OOM, "out of memory"); }
+  uint64_t E = 0, dbytes = 0;
+  for (uint64_t k = 0; k < ntok; k++) {
+    const uint8_t *tk = d + ts[k];
+    const uint32_t tn = (uint32_t)(ts[k + 1] - ts[k]);
+    uint64_t h = hash_bytes(tk, tn) & (cap - 1);
+    for (;;) {
+      if (!tab[h]) { tab[h] = k + 1; id_of_slot[h] = (uint32_t)E; first[E++] = k; dbytes += tn; break; }
+      const uint64_t o = tab[h] - 1;
+      if (ts[o + 1] - ts[o] == tn && !memcmp(d + ts[o], tk, tn)) break;
+      h = (h + 1) & (cap - 1);
+    }
+    ids[k] = id_of_slot[h];
+  }
+  uint64_t dlen = 4 * (E + 1) + dbytes;
+  uint8_t *dict = (uint8_t *)malloc(dlen ? dlen : 1);
+  uint32_t off = 0;
+  for (uint64_t e = 0; e < E; e++) {
+    const uint32_t tn = (uint32_t)(ts[first[e] + 1] - ts[first[e]]);
+    memcpy(dict + 4 * e, &off, 4);
+    memcpy(dict + 4 * (E + 1) + off, d + ts[first[e]], tn);
+    off += tn;
+  }
+  memcpy(dict + 4 * E, &off, 4);
+  free(ts); free(tab); free(first); free(id_of_slot);
+  if (E > 0xFFFFFFFFull || dbytes > 0xFFFFFFFFull) { free(dict); free(ids); return fail(E_CAPACITY, "StrDict dictionary too large"); }
+  node_rec r; memset(&r, 0, sizeof r);
+  r.codec = C_STRDICT; r.nchild = 2; r.stream = 0xFFFF; r.n = in.n;
+  uint32_t e32 = (uint32_t)E, db32 = (uint32_t)dbytes, mt = kStrDictMaxTok;
+  memcpy(r.p, &e32, 4); memcpy(r.p + 4, &db32, 4); memcpy(r.p + 8, &mt, 4);
+  add_node(b, r);
+  col_t dc = {dlen, 1, 0, dict, NULL};
+  int rc = enc_raw(b, dc);
+  free(dict);
+  if (rc) { free(ids); return rc; }
+  return enc_int_child(b, t->child[1], ids, ntok);
+}
+
 static int enc_str(builder *b, const tnode *t, col_t in) {
   if (!in.offs) return fail(E_UNSUPPORTED, "Str needs a VARBYTES column");
   int64_t *len = (int64_t *)malloc((in.n ? in.n : 1) * sizeof(int64_t));
@@ -611,7 +689,9 @@ static int enc_str(builder *b, const tnode *t, col_t in) {
   r.codec = C_STR; r.nchild = 2; r.stream = 0xFFFF; r.n = in.n;
   add_node(b, r);
   col_t bc = {nbytes, 1, 0, in.data + in.offs[0], NULL};
+  g_str_offs = in.offs; g_str_rows = in.n;  /* string boundaries for a String-dictionary bytes child */
   int rc = encode_node(b, t->child[0], bc);
+  g_str_offs = NULL; g_str_rows = 0;
   if (rc) { free(len); return rc; }
   return enc_int_child(b, t->child[1], len, in.n);
 }
@@ -620,7 +700,8 @@ static int encode_node(builder *b, const tnode *t, col_t in) {
   if (in.offs && t->codec != C_STR) return fail(E_UNSUPPORTED, "VARBYTES columns need a Str root");
   switch (t->codec) {
     case C_RAW: return enc_raw(b, in);
-    case C_BITPACK: return enc_bitpack(b, in);
+    case C_BITPACK: return enc_bitpack(b, t, in);
+    case C_STRDICT: return enc_strdict(b, t, in);
     case C_DICT: return enc_dict(b, t, in);
     case C_FLOAT2INT: return enc_float2int(b, t, in);
     case C_DELTA: return enc_delta(b, t, in);

@@ -10,7 +10,7 @@ import struct
 
 import numpy as np
 
-RAW, BITPACK, DICT, FLOAT2INT, DELTA, RLE, LZ4, STR, ANS, DSTRIDE = range(10)
+RAW, BITPACK, DICT, FLOAT2INT, DELTA, RLE, LZ4, STR, ANS, DSTRIDE, STRDICT = range(11)
 I32, I64, F64, FIXED, VARBYTES = range(5)
 
 
@@ -39,6 +39,8 @@ class Node:
             p[8:16] = struct.pack("<Q", self.base & ((1 << 64) - 1))
         elif self.codec == DICT:
             p[0:8] = struct.pack("<II", self.entries, self.E)
+        elif self.codec == STRDICT:
+            p[0:12] = struct.pack("<III", self.entries, self.E, 32)  # entries, token bytes, max token
         elif self.codec == FLOAT2INT:
             p[0] = self.d
         elif self.codec == DELTA:

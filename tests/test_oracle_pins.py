@@ -293,6 +293,83 @@ def test_dstride_count_mismatch_and_arity():
         dec(cdm1.build(root, cdm1.I64, 8, 2))
 
 
+# ----------------------------------------------------------------------------- String-dictionary
+# PAPER.md:163 / 498 (tokens on spaces and periods, each token a group expanded from the dictionary);
+# DESIGN.md reading R34 (dictionary = u32 offsets[E+1] + token bytes).  The tokenizer below is test-local.
+
+def _tokens(s: bytes):
+    out, k = [], 0
+    for i in range(1, len(s) + 1):
+        if i == len(s) or (s[i] not in b" ." and s[i - 1] in b" ."):
+            out.append(s[k:i]); k = i
+    return out
+
+
+def _strdict_chunk(strings, ids_w=None, order=None):
+    toks = [t for s in strings for t in _tokens(s)]
+    vocab = order or list(dict.fromkeys(toks))
+    ids = [vocab.index(t) for t in toks]
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in vocab])]).astype(np.uint32)
+    blob = offs.tobytes() + b"".join(vocab)
+    n = sum(len(s) for s in strings)
+    w = ids_w if ids_w is not None else max(1, (len(vocab) - 1).bit_length())
+    sd = cdm1.Node(cdm1.STRDICT, n, [cdm1.raw(blob), cdm1.bitpack(ids, w, 0)], entries=len(vocab),
+                   E=int(offs[-1]))
+    lens = [len(s) for s in strings]
+    root = cdm1.Node(cdm1.STR, len(strings), [sd, cdm1.bitpack(lens, max(1, max(lens).bit_length()), 0)])
+    return cdm1.build(root, cdm1.VARBYTES, 0, len(strings), payload=n), vocab, ids
+
+
+def test_strdict_spec_example():
+    # "a b. a " -> tokens "a ", "b. ", "a " (dictionary of 2 unique tokens, ids 0 1 0)
+    ch, vocab, ids = _strdict_chunk([b"a b. a "])
+    assert vocab == [b"a ", b"b. "] and ids == [0, 1, 0]
+    out, offs = dec(ch)
+    assert bytes(out) == b"a b. a " and offs.tolist() == [0, 7]
+
+
+def test_strdict_reconstructs_strings():
+    rng = np.random.default_rng(3)
+    words = [b"furiously", b"slyly", b"ironic", b"deposits", b"packages", b"", b"x"]
+    strings = []
+    for _ in range(400):
+        k = int(rng.integers(0, 9))
+        s = b"".join(words[int(rng.integers(len(words)))] + (b". " if rng.random() < 0.2 else b" ") for _ in range(k))
+        strings.append(s[: int(rng.integers(0, len(s) + 1))] if rng.random() < 0.3 else s)
+    strings.append(b"")
+    ch, vocab, _ = _strdict_chunk([s for s in strings] + [b"trailing"])
+    out, offs = dec(ch)
+    allb = b"".join(strings) + b"trailing"
+    assert bytes(out) == allb
+    assert offs.tolist() == np.concatenate([[0], np.cumsum([len(s) for s in strings] + [8])]).tolist()
+    # a permuted dictionary with the ids remapped decodes to the same bytes (ids index, not order)
+    perm = vocab[::-1]
+    ch2, _, _ = _strdict_chunk([s for s in strings] + [b"trailing"], order=perm)
+    assert bytes(dec(ch2)[0]) == allb
+
+
+def test_strdict_errors():
+    ch, vocab, ids = _strdict_chunk([b"a b. a "], ids_w=2)
+    # id 3 >= 2 entries
+    sd = cdm1.Node(cdm1.STRDICT, 7, [cdm1.raw(np.array([0, 2, 5], np.uint32).tobytes() + b"a b. "),
+                                     cdm1.bitpack([0, 3, 0], 2, 0)], entries=2, E=5)
+    root = cdm1.Node(cdm1.STR, 1, [sd, cdm1.bitpack([7], 3, 0)])
+    with pytest.raises(OracleError, match="out of range"):
+        dec(cdm1.build(root, cdm1.VARBYTES, 0, 1, payload=7))
+    # tokens total 5 bytes != 7
+    sd = cdm1.Node(cdm1.STRDICT, 7, [cdm1.raw(np.array([0, 2, 5], np.uint32).tobytes() + b"a b. "),
+                                     cdm1.bitpack([0, 1], 1, 0)], entries=2, E=5)
+    root = cdm1.Node(cdm1.STR, 1, [sd, cdm1.bitpack([7], 3, 0)])
+    with pytest.raises(OracleError, match="token bytes"):
+        dec(cdm1.build(root, cdm1.VARBYTES, 0, 1, payload=7))
+    # decreasing dictionary offsets
+    sd = cdm1.Node(cdm1.STRDICT, 7, [cdm1.raw(np.array([0, 4, 2], np.uint32).tobytes() + b"a b"),
+                                     cdm1.bitpack([0, 1], 1, 0)], entries=2, E=3)
+    root = cdm1.Node(cdm1.STR, 1, [sd, cdm1.bitpack([7], 3, 0)])
+    with pytest.raises(OracleError, match="offsets"):
+        dec(cdm1.build(root, cdm1.VARBYTES, 0, 1, payload=7))
+
+
 # ----------------------------------------------------------------------------- LZ4 (liblz4 + hand sequences)
 
 _lz4 = ctypes.CDLL("liblz4.so.1")
