@@ -193,10 +193,11 @@ CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
  *   2 RLE (H7), 3 LZ4 (H8), 4 raw copies;
  * cdm_batch_kernel_times() -> per-kernel milliseconds and launches (mode 2): index 0 fp_kernel,
  *   1 scan_kernel, 2 rle_sums_kernel, 3 rle_kernel level 0 (value lineage), 4 rle_kernel, 5 rle_big_kernel,
- *   6 lz4_kernel, 7 device copies, 8 ans_kernel (arrays of 9). */
+ *   6 lz4_kernel, 7 device copies, 8 ans_kernel, 9 String-dictionary (sd_sums + sd_scan + sd_expand)
+ *   (arrays of 10). */
 CDM_API cdm_status cdm_batch_set_timing(cdm_batch *b, int enable);
 CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch *b, double *ms5, uint64_t *launches5);
-CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms9, uint64_t *launches9);
+CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms10, uint64_t *launches10);
 /* Graph mode + timing: every replay re-records the same events, so call this after each launch (it
  * waits for that replay) to accumulate its per-family times; a replay not collected is not counted. */
 CDM_API cdm_status cdm_batch_collect_timing(cdm_batch *b);

@@ -16,7 +16,7 @@
 
 namespace cdm {
 
-enum Codec : uint8_t { RAW = 0, BITPACK = 1, DICT = 2, FLOAT2INT = 3, DELTA = 4, RLE = 5, LZ4 = 6, STR = 7, ANS = 8, DSTRIDE = 9 };
+enum Codec : uint8_t { RAW = 0, BITPACK = 1, DICT = 2, FLOAT2INT = 3, DELTA = 4, RLE = 5, LZ4 = 6, STR = 7, ANS = 8, DSTRIDE = 9, STRDICT = 10 };
 enum DType : uint8_t { T_I32 = 0, T_I64 = 1, T_F64 = 2, T_FIXED = 3, T_VARBYTES = 4 };
 
 constexpr uint32_t kMagic = 0x314D4443u;  // "CDM1"

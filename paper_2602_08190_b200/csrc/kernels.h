@@ -208,6 +208,34 @@ struct AnsBatch {  // one batch holds chunks of one interleave (il) only
   AnsDesc d[kMaxBatch];
 };
 
+// ---------------------------------------------------------------- NEXT-2: String-dictionary expansion
+// PAPER.md:498 ("each unique word serve as a group in [the Group-Parallel pattern] and expands according to the
+// lookup dictionary"): token ids -> token bytes at positions = exclusive scan of the tokens' lengths.
+constexpr int kSdTile = 2048;         // tokens per tile = 256 threads x 8
+constexpr int kSdStage = 32768;       // staged output bytes per tile (larger tiles store directly)
+struct SdDesc {
+  const uint8_t* ids_packed;   // w-bit token ids, LSB-first (a chunk stream or the ANS output in the arena)
+  const uint8_t* dict;         // u32 offsets[entries + 1] (validated on the host), then the token bytes
+  uint8_t* out;                // decoded bytes (the Str payload)
+  uint64_t* tsum;              // [ntiles] token bytes per tile (sd_sums); exclusive prefix after sd_scan
+  uint64_t id_base;            // FOR base of the ids
+  uint32_t ntok;
+  uint32_t n_out;              // bytes the tokens must total
+  uint32_t entries;
+  uint32_t tile0;
+  uint32_t ntiles;
+  uint32_t err_idx;
+  uint32_t w;
+  uint32_t pad;
+};
+
+struct SdBatch {
+  uint32_t n;
+  uint32_t total_tiles;
+  uint32_t* err;
+  SdDesc d[kMaxBatch];
+};
+
 // ---------------------------------------------------------------- launchers (return cudaGetLastError)
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
@@ -216,6 +244,8 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);
 cudaError_t launch_ans(const AnsBatch& b, bool interleaved, cudaStream_t s);
+// String-dictionary: tile sums -> per-descriptor exclusive scan of the sums -> expansion
+cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s);
 // engine bookkeeping: zero a 16-byte-aligned scratch prefix; move error words into mapped pinned memory
 // (copy, then zero them for the next launch)
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);

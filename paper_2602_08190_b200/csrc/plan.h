@@ -37,6 +37,7 @@ inline int codec_from_name(const std::string& raw) {
   if (b == "delta" || b == "deltaencoding") return DELTA;
   if (b == "rle") return RLE;
   if (b == "deltastride") return DSTRIDE;
+  if (b == "strdict" || b == "stringdictionary") return STRDICT;
   if (b == "lz4") return LZ4;
   if (b == "str" || b == "string" || b == "varchar") return STR;
   if (b == "ans" || b == "rans") return ANS;
@@ -107,8 +108,11 @@ inline bool complete_tree(TNode* t, std::string* err) {
       return true;
     case BITPACK:
       if (k.empty()) k.push_back(mk_raw());
-      if (k.size() != 1 || k[0]->codec != RAW) { *err = "arity error: BitPack's only child is Raw"; return false; }
-      return true;
+      if (k.size() != 1 || (k[0]->codec != RAW && k[0]->codec != ANS)) {
+        *err = "arity error: BitPack's only child is Raw or ANS";
+        return false;
+      }
+      break;
     case LZ4:
     case ANS:
       if (!k.empty()) { *err = "arity error: LZ4/ANS take no children"; return false; }
@@ -116,9 +120,10 @@ inline bool complete_tree(TNode* t, std::string* err) {
       k.push_back(mk_raw());
       return true;
     case DICT:
+    case STRDICT:
       if (k.empty()) { k.push_back(mk_raw()); k.push_back(mk_raw()); }
       else if (k.size() == 1) k.insert(k.begin(), mk_raw());
-      if (k[0]->codec != RAW) { *err = "arity error: Dict's dictionary stream is Raw"; return false; }
+      if (k[0]->codec != RAW) { *err = "arity error: a dictionary stream is Raw"; return false; }
       break;
     case FLOAT2INT:
     case DELTA:
@@ -141,8 +146,8 @@ inline bool complete_tree(TNode* t, std::string* err) {
 }
 
 inline const char* codec_name(uint8_t c) {
-  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS", "DELTASTRIDE"};
-  return c < 10 ? N[c] : "?";
+  static const char* N[] = {"RAW", "BITPACK", "DICT", "FLOAT2INT", "DELTA", "RLE", "LZ4", "STR", "ANS", "DELTASTRIDE", "STRDICT"};
+  return c < 11 ? N[c] : "?";
 }
 
 inline void render_tree(const TNode* t, std::string* out) {
@@ -179,19 +184,27 @@ struct Plan {
 // Recognise the fused shapes; anything else is a valid cascade without a device plan.
 inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* err) {
   auto is = [](const TNode* t, uint8_t c) { return t && t->codec == c; };
-  auto bp = [&](const TNode* t) { return is(t, BITPACK); };
+  auto bp = [&](const TNode* t) { return is(t, BITPACK) && is(t->kids[0].get(), RAW); };
   auto kid = [](const TNode* t, size_t i) -> const TNode* { return i < t->kids.size() ? t->kids[i].get() : nullptr; };
   if (dtype == T_VARBYTES) {
-    if (is(r, STR) && bp(kid(r, 1)) && (is(kid(r, 0), LZ4) || is(kid(r, 0), RAW) || is(kid(r, 0), ANS))) {
+    // String-dictionary bytes (NEXT-2, Table 2 O_COMMENT P:540): token ids BitPack'd, the packed bytes
+    // optionally ANS-coded
+    const TNode* sd = kid(r, 0);
+    const bool strdict = is(sd, STRDICT) && is(kid(sd, 1), BITPACK) &&
+                         (is(kid(kid(sd, 1), 0), RAW) || is(kid(kid(sd, 1), 0), ANS));
+    if (is(r, STR) && bp(kid(r, 1)) && (is(sd, LZ4) || is(sd, RAW) || is(sd, ANS) || strdict)) {
       p->kind = PlanKind::Str;
-      p->str_lz4 = is(kid(r, 0), LZ4);
-      p->str_ans = is(kid(r, 0), ANS);
+      p->str_lz4 = is(sd, LZ4);
+      p->str_ans = is(sd, ANS);
       p->text = p->str_lz4 ? "scan_offsets(unpack lengths) + lz4_group_decode"
               : p->str_ans ? "scan_offsets(unpack lengths) + ans_chunk_decode"
+              : strdict    ? (is(kid(kid(sd, 1), 0), ANS)
+                                  ? "scan_offsets(unpack lengths) + ans_chunk_decode(ids) + strdict_expand"
+                                  : "scan_offsets(unpack lengths) + strdict_expand")
                            : "scan_offsets(unpack lengths) + copy";
       return true;
     }
-    *err = "VARBYTES needs Str|[LZ4,BitPack], Str|[ANS,BitPack] or Str|[Raw,BitPack]";
+    *err = "VARBYTES needs Str|[LZ4,BitPack], Str|[ANS,BitPack], Str|[StrDict|BitPack(|ANS),BitPack] or Str|[Raw,BitPack]";
     return false;
   }
   if (is(r, ANS)) {

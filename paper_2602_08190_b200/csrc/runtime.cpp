@@ -148,6 +148,9 @@ struct Bound {
   bool ans = false;  // NEXT-1: the bytes come from a range-ANS node (Str child or FIXED root)
   uint64_t ans_w_off = 0, ans_w_n = 0, ans_tab_off = 0, ans_n = 0;
   uint32_t ans_nchunks = 0, ans_chunk = 0, ans_tl = 0, ans_il = 1;
+  bool strdict = false;  // NEXT-2: the bytes come from a String-dictionary node (ids BitPack'd, maybe |ANS)
+  uint64_t sd_dict_off = 0, sd_ids_off = 0, sd_id_base = 0;
+  uint32_t sd_entries = 0, sd_ntok = 0, sd_w = 0;
   const uint8_t* dev_chunk = nullptr;
   void* out = nullptr;
   void* offs = nullptr;
@@ -224,8 +227,8 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
   size_t idx = 0;
   if (c.nodes.empty() || t.walk(&idx) != 0 || idx != c.nodes.size()) return fail(CDM_E_CORRUPT, t.err.empty() ? "node table: unused nodes" : t.err);
   for (size_t i = 0; i < c.nodes.size(); i++) {
-    static const int arity[10] = {0, 1, 2, 1, 1, 2, 2, 2, 2, 2};
-    if (c.nodes[i].codec > DSTRIDE || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
+    static const int arity[11] = {0, 1, 2, 1, 1, 2, 2, 2, 2, 2, 2};
+    if (c.nodes[i].codec > STRDICT || t.kids[i].size() != size_t(arity[c.nodes[i].codec]))
       return fail(CDM_E_CORRUPT, "node " + std::to_string(i) + ": bad codec or arity");
   }
   std::string canon;
@@ -378,6 +381,36 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
       if (bn.codec == ANS) {
         cdm_status st = bind_ans(bi);
         if (st) return st;
+      } else if (bn.codec == STRDICT) {  // [Raw dictionary, BitPack ids (|ANS)]
+        b->strdict = true;
+        uint64_t dn;
+        if (!(e = raw_stream(c, t, t.kids[bi][0], 1, &b->sd_dict_off, &dn)).empty()) return bad(e);
+        b->sd_entries = bn.u32_at0();
+        const uint32_t dbytes = bn.u32_at4();
+        if (dn != 4ull * (b->sd_entries + 1ull) + dbytes) return bad("StrDict dictionary stream size");
+        // the kernels trust the offsets: 0, non-decreasing, ending at the token bytes (checked here once)
+        const uint8_t* dh = static_cast<const uint8_t*>(job.host_chunk) + b->sd_dict_off;
+        if (rd32(dh) != 0 || rd32(dh + 4ull * b->sd_entries) != dbytes) return bad("StrDict dictionary offsets");
+        for (uint32_t k = 0; k < b->sd_entries; k++)
+          if (rd32(dh + 4ull * k) > rd32(dh + 4ull * k + 4)) return bad("StrDict dictionary offsets decrease");
+        const int ii = t.kids[bi][1];
+        const Node& in = c.nodes[ii];
+        if (in.n >= (1ull << 31)) return fail(CDM_E_UNSUPPORTED, "StrDict tokens >= 2^31 per chunk");
+        b->sd_ntok = uint32_t(in.n);
+        if (c.payload_bytes && !b->sd_ntok) return bad("StrDict without tokens");
+        const int pi = t.kids[ii][0];
+        if (c.nodes[pi].codec == ANS) {  // BitPack | ANS: the packed id bytes are entropy coded
+          b->sd_w = in.w();
+          b->sd_id_base = in.u64_at8();
+          if (b->sd_w > 32) return bad("StrDict id width > 32");
+          if (c.nodes[pi].n < (uint64_t(b->sd_ntok) * b->sd_w + 7) / 8) return bad("StrDict packed ids too short");
+          cdm_status st = bind_ans(pi);
+          if (st) return st;
+        } else {
+          BPB ids;
+          if (!(e = bind_bp(c, t, ii, in.n, 32, &ids)).empty()) return bad(e);
+          b->sd_ids_off = ids.off; b->sd_w = ids.w; b->sd_id_base = ids.base;
+        }
       } else if (bn.codec == LZ4) {
         b->lz4 = true;
         uint64_t pn, tn;
@@ -448,7 +481,7 @@ static int fam_priority(int f, int lo, int hi) {
 }
 
 // kernel kinds of cdm_batch_kernel_times (include/cdm.h)
-enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, K_ANS, kKernelKinds };
+enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, K_ANS, K_SD, kKernelKinds };
 
 struct cdm_batch {
   cdm_engine* e = nullptr;
@@ -463,6 +496,7 @@ struct cdm_batch {
   std::vector<Lz4Batch> lz4;
   std::vector<uint32_t> lz4_max_sub;
   std::vector<AnsBatch> ans;  // runs on the chunk-sequential (LZ4) family stream
+  std::vector<SdBatch> sd;    // String-dictionary expansions, after the ANS launches on the same stream
   struct Copy { void* dst; const void* src; size_t bytes; };
   std::vector<Copy> copies;
   std::vector<void*> zero_offsets;  // VARBYTES with rows == 0: offsets[0] = 0
@@ -524,11 +558,11 @@ namespace {
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
   B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
-  B->ans.clear();
+  B->ans.clear(); B->sd.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
   B->err_dev = B->err_external ? B->err_external : A.take<uint32_t>(nj ? nj : 1);
-  std::vector<int> fpj, scj, rlj, lzj, anj;
+  std::vector<int> fpj, scj, rlj, lzj, anj, sdj;
   for (size_t i = 0; i < nj; i++) {
     const Bound& b = B->jobs[i];
     switch (b.kind) {
@@ -541,7 +575,8 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         if (b.rows) scj.push_back(int(i)); else B->zero_offsets.push_back(b.offs);
         if (b.lz4 && b.payload) lzj.push_back(int(i));
         if (b.ans && b.payload) anj.push_back(int(i));
-        if (!b.lz4 && !b.ans && b.payload) B->copies.push_back({b.out, b.dev_chunk + b.bytes_off, size_t(b.payload)});
+        if (b.strdict && b.payload) sdj.push_back(int(i));
+        if (!b.lz4 && !b.ans && !b.strdict && b.payload) B->copies.push_back({b.out, b.dev_chunk + b.bytes_off, size_t(b.payload)});
         break;
       case PlanKind::Ans:
         if (b.payload) anj.push_back(int(i));
@@ -725,6 +760,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     rb.big.vals = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
     rb.big.slopes = A.take<uint64_t>(size_t(rb.big.max_slots) * kRleTile);
   }
+  std::vector<const uint8_t*> sd_ids(nj, nullptr);
   // ANS: batches of one interleave each; a tile = kThreads chunks (il = 1) or kThreads/32 chunks (il = 32)
   for (int il : {1, 32}) {
     std::vector<int> sel;
@@ -738,7 +774,14 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         AnsDesc& d = ab.d[ab.n++];
         d.words = reinterpret_cast<const uint16_t*>(b.dev_chunk + b.ans_w_off);
         d.table = b.dev_chunk + b.ans_tab_off;
-        d.out = static_cast<uint8_t*>(b.out);
+        // a String-dictionary job's ANS node decodes its packed ids into the arena
+        if (b.strdict) {
+          uint8_t* ids = A.take<uint8_t>(size_t(b.ans_n) + 32);
+          sd_ids[j] = ids;
+          d.out = ids;
+        } else {
+          d.out = static_cast<uint8_t*>(b.out);
+        }
         d.n = b.ans_n;
         d.n_words = b.ans_w_n;
         d.nchunks = b.ans_nchunks;
@@ -752,6 +795,31 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       ab.total_tiles = tiles;
       B->ans.push_back(ab);
     }
+  }
+  // String-dictionary: one tile per kSdTile tokens; the tile sums (then their prefix) live in the arena
+  for (auto& g : groups(sdj)) {
+    SdBatch sb{};
+    sb.err = B->err_dev;
+    uint32_t tiles = 0;
+    for (int j : g) {
+      const Bound& b = B->jobs[j];
+      SdDesc& d = sb.d[sb.n++];
+      d.ids_packed = b.ans ? sd_ids[j] : b.dev_chunk + b.sd_ids_off;
+      d.dict = b.dev_chunk + b.sd_dict_off;
+      d.out = static_cast<uint8_t*>(b.out);
+      d.id_base = b.sd_id_base;
+      d.ntok = b.sd_ntok;
+      d.n_out = uint32_t(b.payload);
+      d.entries = b.sd_entries;
+      d.w = b.sd_w;
+      d.tile0 = tiles;
+      d.ntiles = uint32_t(div_up(b.sd_ntok, kSdTile));
+      d.tsum = A.take<uint64_t>(d.ntiles + 1);
+      d.err_idx = uint32_t(j);
+      tiles += d.ntiles;
+    }
+    sb.total_tiles = tiles;
+    B->sd.push_back(sb);
   }
   // LZ4
   for (auto& g : groups(lzj)) {
@@ -813,7 +881,7 @@ cudaEvent_t ev_get(cdm_batch* B, size_t k) {
 cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   uint32_t n = 0;
   size_t evk = B->pending.size() * 2;
-  const bool has[5] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty() || !B->ans.empty(),
+  const bool has[5] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty() || !B->ans.empty() || !B->sd.empty(),
                        !B->copies.empty() || !B->zero_offsets.empty()};
   int nfam = 0;
   for (bool h : has) nfam += h;
@@ -892,6 +960,10 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         for (size_t i = 0; i < B->ans.size() && !st; i++) {
           st = timed(K_ANS, [&] { return launch_ans(B->ans[i], B->ans[i].n && B->ans[i].d[0].il == 32, fs); });
           n++; B->fam_launches[F_LZ4]++;
+        }
+        for (size_t i = 0; i < B->sd.size() && !st; i++) {  // after the ANS launches that feed them
+          st = timed(K_SD, [&] { return launch_strdict(B->sd[i], fs); });
+          n += 3; B->fam_launches[F_LZ4] += 3;
         }
         break;
       case F_COPY:
@@ -1265,7 +1337,7 @@ static double family_rate(const Bound& b) {
     case PlanKind::Fp: return 1.0;
     case PlanKind::Scan: return 0.5;
     case PlanKind::Rle: return 0.125;
-    case PlanKind::Str: return b.lz4 ? 0.008 : b.ans ? (b.ans_il == 32 ? 0.05 : 0.002) : 0.5;
+    case PlanKind::Str: return b.lz4 ? 0.008 : b.ans ? (b.ans_il == 32 ? 0.05 : 0.002) : b.strdict ? 0.25 : 0.5;
     case PlanKind::Ans: return b.ans_il == 32 ? 0.05 : 0.002;
     case PlanKind::RawCopy: return 1.0;
   }
@@ -1785,11 +1857,11 @@ extern "C" CDM_API cdm_status cdm_batch_set_timing(cdm_batch* b, int enable) {
   return CDM_OK;
 }
 
-extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms9, uint64_t* launches9) {
+extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms10, uint64_t* launches10) {
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   for (int i = 0; i < kKernelKinds; i++) {
-    if (ms9) ms9[i] = b->k_ms[i];
-    if (launches9) launches9[i] = b->k_n[i];
+    if (ms10) ms10[i] = b->k_ms[i];
+    if (launches10) launches10[i] = b->k_n[i];
   }
   return CDM_OK;
 }

@@ -51,6 +51,8 @@ def test_kernels_are_sm100a_sass():
     ("RLE|[RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 1 (expand"),
     ("Str|[LZ4,BitPack]", cdm.VARBYTES, "lz4_group_decode"),
     ("Str|[ANS,BitPack]", cdm.VARBYTES, "ans_chunk_decode"),
+    ("Str|[StrDict|BitPack|ANS,BitPack]", cdm.VARBYTES, "ans_chunk_decode(ids) + strdict_expand"),
+    ("Str|[StrDict|BitPack,BitPack]", cdm.VARBYTES, "strdict_expand"),
     ("ANS", cdm.FIXED, "ans_chunk_decode"),
 ])
 def test_cascade_plans(spec, dtype, plan):
@@ -61,7 +63,7 @@ def test_cascade_plans(spec, dtype, plan):
 
 
 @pytest.mark.parametrize("spec,code", [("RLE|[BitPack", 2), ("Nope", 2), ("BitPack|[Raw,Raw]", 2),
-                                       ("Delta|Delta|BitPack", 3), ("Str|[LZ4,BitPack]", 3)])
+                                       ("Delta|Delta|BitPack", 3), ("BitPack|ANS", 3), ("Str|[LZ4,BitPack]", 3)])
 def test_cascade_errors(spec, code):
     with pytest.raises(cdm.CdmError) as e:
         cdm.Cascade(spec, cdm.I64)

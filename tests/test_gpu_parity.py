@@ -17,7 +17,7 @@ torch = pytest.importorskip("torch")
 import cdm1
 import oracle
 from paper_2602_08190_b200 import cdm, encoder
-from paper_2602_08190_b200.inputs import (TPCH, Column, I32, I64, config1_column, rle_column,
+from paper_2602_08190_b200.inputs import (TPCH, VARBYTES, Column, I32, I64, config1_column, rle_column,
                                           uniform_bits_column)
 
 pytestmark = pytest.mark.gpu
@@ -164,6 +164,9 @@ TPCH_CASES = [
     ("o_orderstatus", "ANS(chunk=65536)"),
     ("l_comment", "Str|[ANS(chunk=2048),BitPack]"),
     ("l_comment", "Str|[ANS(il=1,chunk=2048),BitPack]"),
+    ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]"),      # Table 2 O_COMMENT (NEXT-2 String-dictionary)
+    ("o_comment", "Str|[StrDict|BitPack|ANS(il=1),BitPack]"),
+    ("l_comment", "Str|[StrDict|BitPack,BitPack]"),
 ]
 
 
@@ -298,6 +301,33 @@ def test_corrupt_dstride_counts_set_error(engine):
     ch = cdm1.build(root, cdm1.I64, 8, 64, cascade_hash=_hash(spec))
     (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.I64), [ch], resident=True, expect_error=True)
     assert r["error_bits"] & cdm.ERR_RUN_SUM
+
+
+def test_strdict_long_tokens_and_empty_strings(engine):
+    """String-dictionary tiles past the staging size (32-byte tokens: direct stores), empty strings, one token."""
+    rng = np.random.default_rng(9)
+    alpha = np.frombuffer(b"abcdefghij", dtype=np.uint8)
+    lens = rng.integers(0, 400, size=20_000)
+    lens[rng.random(lens.size) < 0.1] = 0
+    data = alpha[rng.integers(0, 3, size=int(lens.sum()))]  # few letters, no delimiters: long 32-byte tokens
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = Column("long", VARBYTES, 0, lens.size, data, offs)
+    for spec in ("Str|[StrDict|BitPack,BitPack]", "Str|[StrDict|BitPack|ANS,BitPack]"):
+        check_parity(engine, spec, col, rows_per_chunk=7_001, both=False)
+    one = Column("one", VARBYTES, 0, 3, np.frombuffer(b"hello ", dtype=np.uint8).copy(),
+                 np.array([0, 0, 6, 6], dtype=np.int64))
+    check_parity(engine, "Str|[StrDict|BitPack,BitPack]", one, both=False)
+
+
+def test_corrupt_strdict_sets_error(engine):
+    spec = "Str|[StrDict|BitPack,BitPack]"
+    blob = np.array([0, 2, 5], np.uint32).tobytes() + b"a b. "
+    for ids, bit in (([0, 3, 0], cdm.ERR_DICT_INDEX), ([0, 1], cdm.ERR_LENGTHS)):
+        sd = cdm1.Node(cdm1.STRDICT, 7, [cdm1.raw(blob), cdm1.bitpack(ids, 2, 0)], entries=2, E=5)
+        root = cdm1.Node(cdm1.STR, 1, [sd, cdm1.bitpack([7], 3, 0)])
+        ch = cdm1.build(root, cdm1.VARBYTES, 0, 1, payload=7, cascade_hash=_hash(spec))
+        (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.VARBYTES), [ch], resident=True, expect_error=True)
+        assert r["error_bits"] & bit
 
 
 def test_rle_zero_length_runs(engine):
