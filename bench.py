@@ -66,13 +66,16 @@ WORKLOADS = {
         ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("o_custkey", "BitPack"), ("o_orderstatus", "Dict|BitPack"),
         ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"), ("o_orderpriority", "Dict|BitPack"),
         ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
-        ("o_comment", "Str|[LZ4(sub=16384),BitPack]")],
+        ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]")],
                     desc="config 4: TPC-H lineitem + orders, all 25 columns (SURVEY Sec. 8d cascade map, "
-                         "l_returnflag ANS and l_/o_orderkey DeltaStride per Table 2: FP / RLE / LZ4 / ANS kernels concurrently)"),
+                         "l_returnflag ANS, l_/o_orderkey DeltaStride, o_comment String-dictionary|BitPack|ANS per Table 2: FP / RLE / LZ4 / ANS kernels concurrently)"),
     # NEXT-1 microbenchmark: the paper's ANS instance -- an L_RETURNFLAG-distributed byte
     # column under chunk-sequential range ANS (4 KiB chunks, one thread per chunk)
     "ans": dict(sf=10.0, dtype="u8", cols=[("l_returnflag", "ANS(chunk=4096)"), ("l_linestatus", "ANS(chunk=4096)")],
                 desc="ANS: TPC-H lineitem l_returnflag + l_linestatus CHAR(1) under range ANS (4 KiB chunks)"),
+    # NEXT-2 microbenchmark: Table 2's O_COMMENT cascade (String-dictionary | Bit-packing | ANS)
+    "strdict": dict(sf=10.0, dtype="u8", cols=[("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]")],
+                    desc="String-dictionary: TPC-H orders o_comment under Str|[StrDict|BitPack|ANS,BitPack] (Table 2)"),
     # BASELINE configs[0]: the oracle-sized parity case (launch-bound: 4 MB decoded)
     "config1": dict(sf=None, dtype="int32", cols=[("config1", "BitPack")],
                     desc="config 1: 1M int32, FOR + 8-bit bit-packing, one chunk"),
@@ -446,6 +449,10 @@ def main():
                 fam_bytes["rle"] += info["compressed_bytes"] + info["payload_bytes"]
             elif plan.startswith("fp"):
                 fam_bytes["fp"] += info["compressed_bytes"] + info["payload_bytes"]
+            elif "strdict" in plan:  # Str: the scan writes the offsets, the String-dictionary expansion the bytes
+                fam_bytes["scan"] += info["offsets_bytes"]
+                fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
+                fam_bytes["sd"] = fam_bytes.get("sd", 0) + info["compressed_bytes"] + info["payload_bytes"]
             elif "lz4" in plan or "ans" in plan:  # Str: the scan writes the offsets, LZ4/ANS the bytes
                 fam_bytes["scan"] += info["offsets_bytes"]
                 fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
@@ -455,6 +462,7 @@ def main():
                 fam_bytes["copy"] += info["compressed_bytes"] + info["payload_bytes"]
         kbytes = {"fp_kernel": fam_bytes["fp"], "scan_kernel": fam_bytes["scan"], "rle_kernel": fam_bytes["rle"],
                   "lz4_kernel": fam_bytes.get("lz4x", 0), "ans_kernel": fam_bytes.get("ans", 0),
+                  "strdict_kernel": fam_bytes.get("sd", 0),
                   "device_copy": fam_bytes["copy"]}
         dom = max(ktimes, key=lambda k: ktimes[k][0])
         dom_ms, dom_n = ktimes[dom]

@@ -29,6 +29,18 @@ __device__ __forceinline__ uint64_t extract_bits(const uint32_t* wd, uint64_t bi
 }
 
 // Same, through the read-only path from global memory (small streams: RLE counts/values).
+// Cooperative, coalesced copy of the packed bits of items [i0, i0 + cnt) of a w-bit stream into shared
+// words.  i0 is a multiple of 2048, so i0 * w is word aligned.  Copies two words past the last field
+// (extraction reads up to word k+2); the stream's 16-byte slack keeps that in bounds.
+template <int NT>
+__device__ __forceinline__ void stage_bits(uint32_t* dst, const uint8_t* packed, uint64_t i0, uint32_t cnt,
+                                           uint32_t w) {
+  if (w == 0) return;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(packed) + (i0 * w >> 5);
+  const uint32_t nw = uint32_t((uint64_t(cnt) * w + 31) / 32) + 2;
+  for (uint32_t k = threadIdx.x; k < nw; k += NT) dst[k] = __ldg(src + k);
+}
+
 __device__ __forceinline__ uint64_t extract_bits_global(const uint32_t* __restrict__ wd, uint64_t bitoff,
                                                         uint32_t w) {
   if (w == 0) return 0;

@@ -212,7 +212,8 @@ struct AnsBatch {  // one batch holds chunks of one interleave (il) only
 // PAPER.md:498 ("each unique word serve as a group in [the Group-Parallel pattern] and expands according to the
 // lookup dictionary"): token ids -> token bytes at positions = exclusive scan of the tokens' lengths.
 constexpr int kSdTile = 2048;         // tokens per tile = 256 threads x 8
-constexpr int kSdStage = 32768;       // staged output bytes per tile (larger tiles store directly)
+constexpr int kSdStage = 24576;       // staged output bytes per tile (larger tiles store directly)
+constexpr int kSdDictSmem = 49152;    // dictionaries up to this size are copied into shared memory
 struct SdDesc {
   const uint8_t* ids_packed;   // w-bit token ids, LSB-first (a chunk stream or the ANS output in the arena)
   const uint8_t* dict;         // u32 offsets[entries + 1] (validated on the host), then the token bytes
@@ -232,6 +233,7 @@ struct SdDesc {
 struct SdBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint32_t dict_smem;          // largest dictionary stream rounded to 16 B + 16 if all fit kSdDictSmem, else 0 (L1)
   uint32_t* err;
   SdDesc d[kMaxBatch];
 };

@@ -54,17 +54,6 @@ __device__ __forceinline__ void stage_desc(T* dst, const T* src) {
     reinterpret_cast<uint32_t*>(dst)[threadIdx.x] = reinterpret_cast<const uint32_t*>(src)[threadIdx.x];
 }
 
-// Cooperative, coalesced copy of the packed bits of items [i0, i0 + cnt) of a w-bit stream into shared
-// words.  i0 is a multiple of 2048, so i0 * w is word aligned.  Copies two words past the last field
-// (extraction reads up to word k+2); the stream's 16-byte slack keeps that in bounds.
-__device__ __forceinline__ void stage_bits(uint32_t* dst, const uint8_t* packed, uint64_t i0, uint32_t cnt,
-                                           uint32_t w) {
-  if (w == 0) return;
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(packed) + (i0 * w >> 5);
-  const uint32_t nw = uint32_t((uint64_t(cnt) * w + 31) / 32) + 2;
-  for (uint32_t k = threadIdx.x; k < nw; k += kThreads) dst[k] = __ldg(src + k);
-}
-
 // ------------------------------------------------------------------------------------------ expansion
 __device__ __forceinline__ uint32_t run_search(const uint32_t* soffs, uint32_t lo, uint32_t hi, uint32_t p) {
   while (lo < hi) {  // last run in [lo, hi] with soffs[run] <= p
@@ -369,8 +358,8 @@ __global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant_
   uint32_t errbits = 0;
   const bool cnt_staged = cw <= 16;
   const bool val_staged = vmode == V_BP || vmode == V_DICT || vmode == V_F2I;
-  if (cnt_staged) stage_bits(cnt_s, cpk, g0, nr, cw);
-  if (val_staged) stage_bits(reinterpret_cast<uint32_t*>(aux_s), vpk, g0, nr, vw);
+  if (cnt_staged) stage_bits<kThreads>(cnt_s, cpk, g0, nr, cw);
+  if (val_staged) stage_bits<kThreads>(reinterpret_cast<uint32_t*>(aux_s), vpk, g0, nr, vw);
   grid_launch_dependents();  // a following level-1 launch may start its own staging
   grid_dependency_wait();    // rle_sums (and a level-0 launch) complete: tile sums / V are valid
 

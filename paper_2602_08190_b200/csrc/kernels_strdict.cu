@@ -3,11 +3,12 @@
 // The paper puts String-dictionary in the Group-Parallel (RLE) family: every token occurrence is a
 // group whose items are the bytes of its dictionary entry, and the group offsets are the prefix sum of the
 // token lengths (P:276's presum).  Three launches per batch, all on the chunk-sequential family's stream:
-//   sd_sums   one CTA per 2048-token tile: unpack the w-bit ids, look up the lengths, tile byte sum;
+//   sd_sums   one CTA per 2048-token tile: stage the w-bit ids (coalesced), look up the lengths, tile sum;
 //   sd_scan   one CTA per descriptor: exclusive scan of its tile sums in place (a few thousand values);
 //   sd_expand one CTA per tile: ids -> (dictionary offset, length), block scan of the lengths gives every
-//             token's byte position in the tile; the bytes are assembled in shared memory at the tile's
-//             global alignment (the staged image and the output agree mod 16) and leave as aligned 16-byte
+//             token's byte position in the tile; each thread assembles its tokens' bytes into 32-bit words
+//             in registers (4 dictionary bytes per step) and stores them into a shared image at the tile's
+//             global alignment (the image and the output agree mod 16), which leaves as aligned 16-byte
 //             stores, the two partial edge words byte by byte; tiles of more than 32 KB store directly.
 // The dictionary offsets were checked on the host (0, non-decreasing, ending at the token bytes), so a
 // token id < entries always names bytes inside the dictionary; an id >= entries sets CDM_ERR_DICT_INDEX and
@@ -15,6 +16,9 @@
 // end past them writes nothing.
 #include "device_util.cuh"
 #include "kernels.h"
+
+#include <algorithm>
+#include <cstdlib>
 
 namespace cdm {
 namespace {
@@ -32,11 +36,29 @@ __device__ __forceinline__ int find_desc_sd(const SdBatch& B, uint32_t tile) {
   return lo;
 }
 
-// this thread's tokens kb .. kb + 7 of the tile: dictionary offsets and lengths (0 for a bad id)
-__device__ __forceinline__ uint32_t load_tokens(const SdDesc& D, uint32_t g0, uint32_t nt, uint32_t kb,
-                                                uint32_t (&a)[kSdPer], uint32_t (&len)[kSdPer], bool& bad) {
-  const uint32_t* offs = reinterpret_cast<const uint32_t*>(D.dict);
-  const uint32_t* pk = reinterpret_cast<const uint32_t*>(D.ids_packed);
+constexpr uint32_t kIdsWords = kSdTile * 32 / 32 + 4;  // packed ids of one tile (w <= 32) + extraction slack
+
+// sd_sums is written for a grid of G <= tiles CTAs: CTA c takes the contiguous tiles [c*T/G, (c+1)*T/G) and
+// (B.dict_smem) copies each descriptor's offsets into shared memory once.  It is launched with G = tiles and
+// the offsets read through L1, which measured faster (0.25 vs 0.30 ms, o_comment SF 10).
+struct TileRange {
+  uint32_t t0, t1;
+};
+__device__ __forceinline__ TileRange my_tiles(uint32_t total) {
+  return {uint32_t(uint64_t(total) * blockIdx.x / gridDim.x), uint32_t(uint64_t(total) * (blockIdx.x + 1) / gridDim.x)};
+}
+
+// dictionary stream (offsets + token bytes) of descriptor D -> shared memory (16-byte copies)
+__device__ __forceinline__ void load_dict(const SdDesc& D, uint32_t bytes, uint32_t* dict_s) {
+  const uint4* src = reinterpret_cast<const uint4*>(D.dict);
+  for (uint32_t i = threadIdx.x; i < (bytes + 15) / 16; i += kThreads) reinterpret_cast<uint4*>(dict_s)[i] = __ldg(src + i);
+}
+
+// this thread's tokens kb .. kb + 7 of a tile (ids staged in shared words): dictionary offsets and lengths
+// (0 for a bad id).  `offs` is the dictionary in shared memory or global memory (generic loads).
+__device__ __forceinline__ uint32_t load_tokens(const SdDesc& D, const uint32_t* offs, const uint32_t* ids_s, uint32_t nt,
+                                                uint32_t kb, uint32_t (&a)[kSdPer], uint32_t (&len)[kSdPer], bool& bad) {
+  const uint32_t w = D.w;
   uint32_t sum = 0;
 #pragma unroll
   for (int r = 0; r < kSdPer; r++) {
@@ -44,10 +66,10 @@ __device__ __forceinline__ uint32_t load_tokens(const SdDesc& D, uint32_t g0, ui
     len[r] = 0;
     const uint32_t k = kb + r;
     if (k < nt) {
-      const uint64_t id = D.id_base + extract_bits_global(pk, uint64_t(g0 + k) * D.w, D.w);
+      const uint64_t id = D.id_base + extract_bits(ids_s, uint64_t(k) * w, w);
       if (id < D.entries) {
-        a[r] = __ldg(offs + id);
-        len[r] = __ldg(offs + id + 1) - a[r];
+        a[r] = offs[id];
+        len[r] = offs[id + 1] - a[r];
       } else {
         bad = true;
       }
@@ -58,82 +80,142 @@ __device__ __forceinline__ uint32_t load_tokens(const SdDesc& D, uint32_t g0, ui
 }
 
 __global__ void __launch_bounds__(kThreads) sd_sums_kernel(const __grid_constant__ SdBatch B) {
+  extern __shared__ __align__(16) uint32_t dict_s[];
+  __shared__ uint32_t ids_s[kIdsWords];
   __shared__ uint64_t warp_s[kThreads / 32];
-  const SdDesc& D = B.d[find_desc_sd(B, blockIdx.x)];
-  const uint32_t lt = blockIdx.x - D.tile0, g0 = lt * kSdTile;
-  const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
-  uint32_t a[kSdPer], len[kSdPer];
-  bool bad = false;
-  const uint64_t s = load_tokens(D, g0, nt, threadIdx.x * kSdPer, a, len, bad);
-  uint64_t tot;
-  block_excl_scan_u64<kThreads>(s, warp_s, &tot);
-  if (threadIdx.x == 0) D.tsum[lt] = tot;
-  if (bad) atomicOr(B.err + D.err_idx, 0x1u);
+  const TileRange tr = my_tiles(B.total_tiles);
+  int cur = -1;
+  for (uint32_t tile = tr.t0; tile < tr.t1; tile++) {
+    const int di = find_desc_sd(B, tile);
+    const SdDesc& D = B.d[di];
+    __syncthreads();  // the previous tile's ids / dictionary are dead
+    if (di != cur && B.dict_smem) load_dict(D, 4u * (D.entries + 1u), dict_s);  // offsets only
+    cur = di;
+    const uint32_t lt = tile - D.tile0, g0 = lt * kSdTile;
+    const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
+    stage_bits<kThreads>(ids_s, D.ids_packed, g0, nt, D.w);
+    __syncthreads();
+    uint32_t a[kSdPer], len[kSdPer];
+    bool bad = false;
+    const uint32_t* offs = B.dict_smem ? dict_s : reinterpret_cast<const uint32_t*>(D.dict);
+    const uint64_t s = load_tokens(D, offs, ids_s, nt, threadIdx.x * kSdPer, a, len, bad);
+    uint64_t tot;
+    block_excl_scan_u64<kThreads>(s, warp_s, &tot);
+    if (threadIdx.x == 0) D.tsum[lt] = tot;
+    if (bad) atomicOr(B.err + D.err_idx, 0x1u);
+  }
 }
 
-// one CTA per descriptor: tsum <- exclusive prefix of tsum (the tile's output offset)
+// one CTA per descriptor: tsum <- exclusive prefix of tsum (the tile's output offset); thread t scans a
+// contiguous segment, so the loads of a segment are independent
 __global__ void __launch_bounds__(kThreads) sd_scan_kernel(const __grid_constant__ SdBatch B) {
   __shared__ uint64_t warp_s[kThreads / 32];
   const SdDesc& D = B.d[blockIdx.x];
-  uint64_t carry = 0;
-  for (uint32_t i0 = 0; i0 < D.ntiles; i0 += kThreads) {
-    const uint32_t i = i0 + threadIdx.x;
-    const uint64_t v = i < D.ntiles ? D.tsum[i] : 0ull;
-    uint64_t tot;
-    const uint64_t ex = block_excl_scan_u64<kThreads>(v, warp_s, &tot);
-    if (i < D.ntiles) D.tsum[i] = carry + ex;
-    carry += tot;
-    __syncthreads();
+  const uint32_t per = (D.ntiles + kThreads - 1) / kThreads;
+  const uint32_t i0 = min(D.ntiles, threadIdx.x * per), i1 = min(D.ntiles, i0 + per);
+  uint64_t s = 0;
+  for (uint32_t i = i0; i < i1; i++) s += __ldcg(D.tsum + i);
+  uint64_t tot;
+  uint64_t run = block_excl_scan_u64<kThreads>(s, warp_s, &tot);
+  for (uint32_t i = i0; i < i1; i++) {
+    const uint64_t v = __ldcg(D.tsum + i);
+    D.tsum[i] = run;
+    run += v;
   }
-  if (threadIdx.x == 0 && carry != D.n_out) atomicOr(B.err + D.err_idx, 0x8u);
+  if (threadIdx.x == 0 && tot != D.n_out) atomicOr(B.err + D.err_idx, 0x8u);
 }
 
+// sd_expand (one CTA per tile; the dictionary is read through L1): a thread's 8 tokens are contiguous in the
+// output, so it builds the 32-bit words of its byte range one at a time (4 dictionary bytes per token piece:
+// two aligned dictionary words + a funnel shift) and stores them into the zeroed shared image; only its
+// first and last words, shared with the neighbouring threads, are merged with shared-memory atomicOr.
 __global__ void __launch_bounds__(kThreads) sd_expand_kernel(const __grid_constant__ SdBatch B) {
-  __shared__ __align__(16) uint8_t stage_s[kSdStage + 32];
+  extern __shared__ __align__(16) uint32_t dict_s[];  // B.dict_smem > 0: this tile's dictionary
+  __shared__ __align__(16) uint32_t stage_s[(kSdStage + 32) / 4];
+  __shared__ uint32_t ids_s[kIdsWords];
   __shared__ uint64_t warp_s[kThreads / 32];
   const SdDesc& D = B.d[find_desc_sd(B, blockIdx.x)];
   const uint32_t lt = blockIdx.x - D.tile0, g0 = lt * kSdTile;
   const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
   const uint32_t kb = threadIdx.x * kSdPer;
+  stage_bits<kThreads>(ids_s, D.ids_packed, g0, nt, D.w);
+  const uint64_t O64 = __ldcg(D.tsum + lt);
+  const uint32_t sh = uint32_t(O64) & 15u;
+  for (uint32_t i = threadIdx.x; i < (kSdStage + 32) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(stage_s)[i] = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t* offs = reinterpret_cast<const uint32_t*>(D.dict);
+  if (B.dict_smem) {
+    load_dict(D, 4u * (D.entries + 1u) + __ldg(offs + D.entries), dict_s);
+    offs = dict_s;
+  }
+  __syncthreads();
   uint32_t a[kSdPer], len[kSdPer];
   bool bad = false;
-  const uint64_t s = load_tokens(D, g0, nt, kb, a, len, bad);
+  const uint32_t s = load_tokens(D, offs, ids_s, nt, kb, a, len, bad);
   uint64_t T;
   const uint32_t ex = uint32_t(block_excl_scan_u64<kThreads>(s, warp_s, &T));
-  const uint64_t O64 = __ldcg(D.tsum + lt);
   if (O64 + T > D.n_out) return;  // inconsistent lengths (sd_scan reports them): never write outside
   const uint32_t O = uint32_t(O64), Tt = uint32_t(T);
-  const uint8_t* tok = D.dict + 4ull * (D.entries + 1ull);
+  const uint32_t* tw = offs + D.entries + 1u;  // token bytes, 4-byte aligned
   uint8_t* const out = D.out;
   if (Tt > kSdStage) {  // long tokens: direct byte stores
+    const uint8_t* tb = reinterpret_cast<const uint8_t*>(tw);
     uint32_t p = O + ex;
 #pragma unroll
     for (int r = 0; r < kSdPer; r++) {
-      for (uint32_t j = 0; j < len[r]; j++) out[p + j] = __ldg(tok + a[r] + j);
+      for (uint32_t j = 0; j < len[r]; j++) out[p + j] = tb[a[r] + j];
       p += len[r];
     }
     return;
   }
-  // staged image: stage_s[sh + q] = tile byte q, sh = O mod 16, so stage word i is output word (O - sh)/16 + i
-  const uint32_t sh = O & 15u;
-  uint32_t p = sh + ex;
+  // staged image: stage byte sh + q = tile byte q, so stage word i (16 B) is output word (O - sh)/16 + i.
+  // Word-driven: the thread walks the 4-byte words of its range [P, P + s); each word takes 4 dictionary
+  // bytes from each token it overlaps (usually one or two); consumed tokens shift out of the register arrays.
+  if (s) {
+    const uint32_t P = sh + ex, Pe = P + s;
+    uint32_t tpos = P;
+    auto shift = [&]() {
 #pragma unroll
-  for (int r = 0; r < kSdPer; r++) {
-    const uint8_t* src = tok + a[r];
-    for (uint32_t j = 0; j < len[r]; j++) stage_s[p + j] = __ldg(src + j);
-    p += len[r];
+      for (int r = 0; r + 1 < kSdPer; r++) { a[r] = a[r + 1]; len[r] = len[r + 1]; }
+      len[kSdPer - 1] = 0;
+    };
+#pragma unroll 1
+    for (int g = 0; g < kSdPer && len[0] == 0; g++) shift();
+#pragma unroll 1
+    for (uint32_t wpos = P & ~3u; wpos < Pe; wpos += 4) {
+      uint32_t word = 0;
+      uint32_t b = max(wpos, P);
+      const uint32_t be = min(wpos + 4u, Pe);
+#pragma unroll 1
+      while (b < be) {
+        const uint32_t off = a[0] + (b - tpos);
+        const uint32_t piece = __funnelshift_r(tw[off >> 2], tw[(off >> 2) + 1], (off & 3u) * 8u);
+        const uint32_t m = min(be - b, tpos + len[0] - b);
+        word |= (m >= 4u ? piece : piece & ((1u << (8u * m)) - 1u)) << (8u * (b - wpos));
+        b += m;
+        if (b == tpos + len[0]) {  // next non-empty token of this thread
+          tpos += len[0];
+          shift();
+#pragma unroll 1
+          for (int g = 0; g < kSdPer && len[0] == 0 && b < Pe; g++) shift();
+        }
+      }
+      if (wpos < P || wpos + 4u > Pe) atomicOr(stage_s + (wpos >> 2), word);  // shared with a neighbour
+      else stage_s[wpos >> 2] = word;
+    }
   }
   __syncthreads();
   const uint32_t nw = (sh + Tt + 15) / 16;
   uint4* const ow = reinterpret_cast<uint4*>(out + (O - sh));
   const uint4* const sw = reinterpret_cast<const uint4*>(stage_s);
+  const uint8_t* const sb = reinterpret_cast<const uint8_t*>(stage_s);
   for (uint32_t i = threadIdx.x; i < nw; i += kThreads) {
     const uint32_t lo = 16 * i, hi = lo + 16;
     if (lo >= sh && hi <= sh + Tt) {
       ow[i] = sw[i];
     } else {  // an edge word shared with the neighbouring tiles: only this tile's bytes
       uint8_t* const ob = reinterpret_cast<uint8_t*>(ow + i);
-      for (uint32_t q = max(lo, sh); q < min(hi, sh + Tt); q++) ob[q - lo] = stage_s[q];
+      for (uint32_t q = max(lo, sh); q < min(hi, sh + Tt); q++) ob[q - lo] = sb[q];
     }
   }
 }
@@ -142,9 +224,23 @@ __global__ void __launch_bounds__(kThreads) sd_expand_kernel(const __grid_consta
 
 cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  sd_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(sd_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
+    cudaFuncSetAttribute(sd_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
+    configured = true;
+  }
+  // default: every kernel reads the dictionary through L1 (random tokens cost one wavefront per distinct line:
+  // the expansion is L1-wavefront bound).  CDM_SD_SMEM=1: sd_expand copies the dictionary into shared memory
+  // per tile -- measured slower (2.4 vs 1.6 ms for o_comment SF 10: the copy is 3.6x the tile's output), and
+  // persistent CTAs that copy it once lose the latency hiding of 6 resident CTAs per SM (2.3 ms).
+  static const bool smem = std::getenv("CDM_SD_SMEM") && std::getenv("CDM_SD_SMEM")[0] == '1';
+  SdBatch l1 = b;
+  l1.dict_smem = 0;
+  sd_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   sd_scan_kernel<<<b.n, kThreads, 0, s>>>(b);
-  sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
+  if (smem && b.dict_smem) sd_expand_kernel<<<b.total_tiles, kThreads, b.dict_smem, s>>>(b);
+  else sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   return cudaGetLastError();
 }
 

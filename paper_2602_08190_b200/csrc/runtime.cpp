@@ -150,7 +150,7 @@ struct Bound {
   uint32_t ans_nchunks = 0, ans_chunk = 0, ans_tl = 0, ans_il = 1;
   bool strdict = false;  // NEXT-2: the bytes come from a String-dictionary node (ids BitPack'd, maybe |ANS)
   uint64_t sd_dict_off = 0, sd_ids_off = 0, sd_id_base = 0;
-  uint32_t sd_entries = 0, sd_ntok = 0, sd_w = 0;
+  uint32_t sd_entries = 0, sd_ntok = 0, sd_w = 0, sd_dict_bytes = 0;
   const uint8_t* dev_chunk = nullptr;
   void* out = nullptr;
   void* offs = nullptr;
@@ -388,6 +388,8 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
         b->sd_entries = bn.u32_at0();
         const uint32_t dbytes = bn.u32_at4();
         if (dn != 4ull * (b->sd_entries + 1ull) + dbytes) return bad("StrDict dictionary stream size");
+        if (dn >= (1ull << 31)) return fail(CDM_E_UNSUPPORTED, "StrDict dictionary >= 2 GiB");
+        b->sd_dict_bytes = uint32_t(dn);
         // the kernels trust the offsets: 0, non-decreasing, ending at the token bytes (checked here once)
         const uint8_t* dh = static_cast<const uint8_t*>(job.host_chunk) + b->sd_dict_off;
         if (rd32(dh) != 0 || rd32(dh + 4ull * b->sd_entries) != dbytes) return bad("StrDict dictionary offsets");
@@ -800,7 +802,8 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (auto& g : groups(sdj)) {
     SdBatch sb{};
     sb.err = B->err_dev;
-    uint32_t tiles = 0;
+    uint32_t tiles = 0, dmax = 0;
+    bool fits = true;
     for (int j : g) {
       const Bound& b = B->jobs[j];
       SdDesc& d = sb.d[sb.n++];
@@ -817,8 +820,12 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.tsum = A.take<uint64_t>(d.ntiles + 1);
       d.err_idx = uint32_t(j);
       tiles += d.ntiles;
+      const uint32_t db = uint32_t((b.sd_dict_bytes + 15u) & ~15u) + 16u;  // + the word past the last token byte
+      dmax = std::max(dmax, db);
+      fits = fits && db <= uint32_t(kSdDictSmem);
     }
     sb.total_tiles = tiles;
+    sb.dict_smem = fits ? dmax : 0u;  // else the kernels read the dictionaries through L1
     B->sd.push_back(sb);
   }
   // LZ4
