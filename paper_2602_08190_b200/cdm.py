@@ -26,7 +26,8 @@ SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_creat
            "cdm_submit_batch", "cdm_wait", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
            "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times",
-           "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy"]
+           "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy",
+           "cdm_tune_set", "cdm_tune_get"]
 
 
 class EngineOpts(ctypes.Structure):
@@ -97,6 +98,8 @@ def lib():
         "cdm_pipeline_launch": [vp, vp],
         "cdm_pipeline_results": [vp, ctypes.POINTER(Result)],
         "cdm_pipeline_destroy": [vp],
+        "cdm_tune_set": [ctypes.c_char_p, ctypes.c_int],
+        "cdm_tune_get": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -150,6 +153,17 @@ class Cascade:
         if getattr(self, "h", None) and _lib is not None:
             _lib.cdm_cascade_destroy(self.h)
             self.h = None
+
+
+def tune_set(knob: str, value: int) -> None:
+    """NEXT-3 launch-parameter knob (include/cdm.h: "fp_ctas_per_sm", "lz4_lanes")."""
+    _check(lib().cdm_tune_set(knob.encode(), int(value)))
+
+
+def tune_get(knob: str) -> int:
+    v = ctypes.c_int()
+    _check(lib().cdm_tune_get(knob.encode(), ctypes.byref(v)))
+    return v.value
 
 
 def chunk_info(host_chunk) -> dict:

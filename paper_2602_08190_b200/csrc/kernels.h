@@ -254,4 +254,14 @@ cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);
 cudaError_t launch_harvest(uint32_t* err, uint32_t* host_mapped, uint32_t n, cudaStream_t s);
 int device_sms();
 
+// NEXT-3: launch parameters the offline tuner explores (Table 3's per-pattern spaces).
+// Process-wide; read by the launchers at enqueue time (a captured graph keeps the values it was built with).
+enum TuneKnob : int {
+  TUNE_FP_CTAS_PER_SM = 0,  // F.P. "L": persistent fp_kernel CTAs per SM (0 = adaptive 2/3/4)
+  TUNE_LZ4_LANES = 1,       // N.P. "C": lanes per LZ4 sub-chunk: 4, 8, 16 (lane groups) or 32 (one warp)
+  kTuneKnobs
+};
+int tune_get(int knob);
+void tune_set(int knob, int value);
+
 }  // namespace cdm

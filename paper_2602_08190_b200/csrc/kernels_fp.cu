@@ -267,6 +267,27 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
 
 }  // namespace
 
+namespace {
+int g_tune[kTuneKnobs];
+bool g_tune_init = false;
+void tune_init() {
+  if (g_tune_init) return;
+  g_tune[TUNE_FP_CTAS_PER_SM] = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 0;
+  g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_WARP") ? 32 : std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 4;
+  g_tune_init = true;
+}
+}  // namespace
+
+int tune_get(int knob) {
+  tune_init();
+  return knob >= 0 && knob < kTuneKnobs ? g_tune[knob] : 0;
+}
+
+void tune_set(int knob, int value) {
+  tune_init();
+  if (knob >= 0 && knob < kTuneKnobs) g_tune[knob] = value;
+}
+
 int device_sms() {
   static int sms = 0;
   if (!sms) {
@@ -296,8 +317,8 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   // persistent CTAs per SM: 2 for short batches (each CTA still walks ~5 tiles with its TMA double buffer
   // full, and SM slots stay free for a concurrent RLE chain: config 2), up to 4 for long ones (more tiles in
-  // flight per SM: E2 widths at 268 MB, +20 %); CDM_FP_CTAS_PER_SM overrides
-  static const int cap_env = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 0;
+  // flight per SM: E2 widths at 268 MB, +20 %); the tuning knob (env CDM_FP_CTAS_PER_SM) overrides
+  const int cap_env = tune_get(TUNE_FP_CTAS_PER_SM);
   const uint32_t tiles_per_sm = b.total_tiles / uint32_t(device_sms());
   const int cap = cap_env > 0 ? cap_env : tiles_per_sm >= 32 ? 4 : tiles_per_sm >= 20 ? 3 : 2;
   if (cap < per_sm) per_sm = cap;

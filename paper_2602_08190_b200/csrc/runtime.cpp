@@ -1864,6 +1864,30 @@ extern "C" CDM_API cdm_status cdm_batch_set_timing(cdm_batch* b, int enable) {
   return CDM_OK;
 }
 
+extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
+  if (!knob) return fail(CDM_E_INVALID_ARG, "null knob");
+  const std::string k(knob);
+  if (k == "fp_ctas_per_sm") {
+    if (value < 0 || value > 16) return fail(CDM_E_INVALID_ARG, "fp_ctas_per_sm must be 0..16");
+    cdm::tune_set(cdm::TUNE_FP_CTAS_PER_SM, value);
+  } else if (k == "lz4_lanes") {
+    if (value != 4 && value != 8 && value != 16 && value != 32) return fail(CDM_E_INVALID_ARG, "lz4_lanes must be 4, 8, 16 or 32");
+    cdm::tune_set(cdm::TUNE_LZ4_LANES, value);
+  } else {
+    return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
+  }
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_tune_get(const char* knob, int* value) {
+  if (!knob || !value) return fail(CDM_E_INVALID_ARG, "null argument");
+  const std::string k(knob);
+  if (k == "fp_ctas_per_sm") *value = cdm::tune_get(cdm::TUNE_FP_CTAS_PER_SM);
+  else if (k == "lz4_lanes") *value = cdm::tune_get(cdm::TUNE_LZ4_LANES);
+  else return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
+  return CDM_OK;
+}
+
 extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms10, uint64_t* launches10) {
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   for (int i = 0; i < kKernelKinds; i++) {
