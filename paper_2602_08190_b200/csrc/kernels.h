@@ -204,6 +204,7 @@ struct AnsDesc {
 struct AnsBatch {  // one batch holds chunks of one interleave (il) only
   uint32_t n;
   uint32_t total_tiles;
+  uint32_t cpw;      // il = 32: chunks per warp (a CTA's slot table serves kThreads/32 * cpw chunks)
   uint32_t* err;
   AnsDesc d[kMaxBatch];
 };

@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
 // chunk's dependency chain is chunk/32 steps long.  The states that renormalise at a step take consecutive
 // words in lane order (ballot + popcount rank); the chunk's next 64 words sit in two registers per lane
 // (one word per lane each) and reach the renormalising lanes by shuffle, refilled 32 words at a time with a
-// coalesced load.
+// coalesced load.  A CTA's 8 warps take B.cpw rounds of 8 chunks, so the slot table is built once per
+// 8 * cpw chunks.
 __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constant__ AnsBatch B) {
   __shared__ uint32_t tab_s[1u << kAnsMaxTl];
   __shared__ uint32_t cum_s[257];
@@ -124,43 +125,45 @@ __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constan
   const uint32_t tl = D.tl, M = 1u << tl;
   const uint8_t* const table = D.table;
   const bool table_ok = build_slot_table(table, M, tab_s, cum_s, warp_s);
-  const uint32_t c = (blockIdx.x - D.tile0) * (kThreads / 32) + warp;  // this warp's chunk
-  if (c >= D.nchunks) return;  // warp-uniform
-  const uint8_t* ce = table + 512 + 136ull * c;
-  const uint32_t w0 = __ldg(reinterpret_cast<const uint32_t*>(ce)), nw = __ldg(reinterpret_cast<const uint32_t*>(ce + 4));
-  uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(ce + 8) + lane);
-  bool bad = !table_ok || uint64_t(w0) + nw > D.n_words;
-  const uint64_t i0 = uint64_t(c) * D.chunk;
-  const uint32_t len = uint32_t(min(uint64_t(D.chunk), D.n - i0));
-  const uint16_t* __restrict__ wp = D.words + w0;
-  uint8_t* out = D.out + i0;
   const uint32_t mask = M - 1u, lt_mask = (1u << lane) - 1u;
-  auto ldw = [&](uint32_t q) -> uint32_t { return q < nw ? uint32_t(__ldg(wp + q)) : 0u; };
-  uint32_t wbase = 0, cur = 0, nxt = 0, pos = 0;
-  if (!bad) { cur = ldw(lane); nxt = ldw(32 + lane); }
-  const uint32_t steps = bad ? 0u : (len + 31) / 32;
-  for (uint32_t s = 0; s < steps; s++) {
-    const uint32_t i = 32 * s + lane;
-    const bool act = i < len;
-    const uint32_t e = tab_s[x & mask];
-    const uint32_t xn = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
-    const bool need = act && xn < (1u << 16);  // one step suffices for tl <= 12
-    const uint32_t m = __ballot_sync(FULL, need);
-    const uint32_t q = pos + __popc(m & lt_mask) - wbase;  // word index relative to the window (< 64)
-    const uint32_t a = __shfl_sync(FULL, cur, q & 31), b = __shfl_sync(FULL, nxt, q & 31);
-    const uint32_t w = q < 32 ? a : b;
-    bad |= need && pos + __popc(m & lt_mask) >= nw;
-    x = need ? (xn << 16) | w : (act ? xn : x);
-    if (act) out[i] = uint8_t(e & 0xFFu);
-    pos += __popc(m);
-    if (pos >= wbase + 32) {  // warp-uniform: slide the window by 32 words
-      wbase += 32;
-      cur = nxt;
-      nxt = ldw(wbase + 32 + lane);
+  for (uint32_t rnd = 0; rnd < B.cpw; rnd++) {
+    const uint32_t c = ((blockIdx.x - D.tile0) * B.cpw + rnd) * (kThreads / 32) + warp;  // this warp's chunk
+    if (c >= D.nchunks) break;  // warp-uniform
+    const uint8_t* ce = table + 512 + 136ull * c;
+    const uint32_t w0 = __ldg(reinterpret_cast<const uint32_t*>(ce)), nw = __ldg(reinterpret_cast<const uint32_t*>(ce + 4));
+    uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(ce + 8) + lane);
+    bool bad = !table_ok || uint64_t(w0) + nw > D.n_words;
+    const uint64_t i0 = uint64_t(c) * D.chunk;
+    const uint32_t len = uint32_t(min(uint64_t(D.chunk), D.n - i0));
+    const uint16_t* __restrict__ wp = D.words + w0;
+    uint8_t* out = D.out + i0;
+    auto ldw = [&](uint32_t q) -> uint32_t { return q < nw ? uint32_t(__ldg(wp + q)) : 0u; };
+    uint32_t wbase = 0, cur = 0, nxt = 0, pos = 0;
+    if (!bad) { cur = ldw(lane); nxt = ldw(32 + lane); }
+    const uint32_t steps = bad ? 0u : (len + 31) / 32;
+    for (uint32_t s = 0; s < steps; s++) {
+      const uint32_t i = 32 * s + lane;
+      const bool act = i < len;
+      const uint32_t e = tab_s[x & mask];
+      const uint32_t xn = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+      const bool need = act && xn < (1u << 16);  // one step suffices for tl <= 12
+      const uint32_t m = __ballot_sync(FULL, need);
+      const uint32_t q = pos + __popc(m & lt_mask) - wbase;  // word index relative to the window (< 64)
+      const uint32_t a = __shfl_sync(FULL, cur, q & 31), b = __shfl_sync(FULL, nxt, q & 31);
+      const uint32_t w = q < 32 ? a : b;
+      bad |= need && pos + __popc(m & lt_mask) >= nw;
+      x = need ? (xn << 16) | w : (act ? xn : x);
+      if (act) out[i] = uint8_t(e & 0xFFu);
+      pos += __popc(m);
+      if (pos >= wbase + 32) {  // warp-uniform: slide the window by 32 words
+        wbase += 32;
+        cur = nxt;
+        nxt = ldw(wbase + 32 + lane);
+      }
     }
+    bad |= !__all_sync(FULL, x == (1u << 16)) || pos != nw;
+    if (bad && lane == 0) atomicOr(B.err + D.err_idx, 0x20u);
   }
-  bad |= !__all_sync(FULL, x == (1u << 16)) || pos != nw;
-  if (bad && lane == 0) atomicOr(B.err + D.err_idx, 0x20u);
 }
 
 }  // namespace

@@ -771,6 +771,12 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       AnsBatch ab{};
       ab.err = B->err_dev;
       uint32_t tiles = 0;
+      // il = 32: every CTA builds the slot table once for kThreads/32 * cpw chunks; cpw grows with the batch
+      // while the grid still fills the GPU (~64 resident warps per SM)
+      uint64_t nch = 0;
+      for (int j : g) nch += B->jobs[j].ans_nchunks;
+      ab.cpw = il == 32 ? uint32_t(std::min<uint64_t>(8, std::max<uint64_t>(1, nch / (uint64_t(device_sms()) * 64)))) : 1;
+      const uint32_t per_tile = il == 32 ? uint32_t(kThreads / 32) * ab.cpw : uint32_t(kThreads);
       for (int j : g) {
         const Bound& b = B->jobs[j];
         AnsDesc& d = ab.d[ab.n++];
@@ -792,7 +798,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         d.il = b.ans_il;
         d.tile0 = tiles;
         d.err_idx = uint32_t(j);
-        tiles += uint32_t(div_up(b.ans_nchunks, il == 32 ? kThreads / 32 : kThreads));
+        tiles += uint32_t(div_up(b.ans_nchunks, per_tile));
       }
       ab.total_tiles = tiles;
       B->ans.push_back(ab);
