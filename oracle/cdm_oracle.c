@@ -30,6 +30,10 @@
  *                  [dictionary = u32 offsets[E+1] + token bytes, token ids]; out = concatenation of the
  *                  ids' tokens, which must total the node's n bytes.
  *   Str            DESIGN.md reading R17: offsets_0 = 0, offsets_{i+1} = offsets_i + len_i.
+ *   Checksum       SURVEY Sec. 8a H9 (optional positional checksum): h = sum over the 8-byte little-endian
+ *                  words w_i of the decoded buffer (last one zero padded) of splitmix64(chunk_id ^ i ^ w_i),
+ *                  mod 2^64; splitmix64 = the SplitMix64 output function (golden-gamma add, two xor-shift
+ *                  multiplies, final xor-shift).
  *   Nesting        PAPER.md:509 (Table 2 notation), decoded depth-first: children first, then parent
  *                  (no fusion exists in the oracle).
  *
@@ -412,6 +416,24 @@ static int decode_node(ochunk *c, uint32_t *idx, ostream *out) {
  * VARBYTES, offsets receives rows+1 int32 (chunk-relative, exclusive end).  Returns 0 or an error
  * code; res->detail names the first violated field or the failing row.
  */
+static uint64_t o_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+EXPORT uint64_t oracle_checksum(const void *data, uint64_t bytes, uint64_t chunk_id) {
+  const uint8_t *p = (const uint8_t *)data;
+  uint64_t h = 0;
+  for (uint64_t i = 0; i * 8 < bytes; i++) {
+    uint64_t w = 0;
+    for (uint64_t k = 0; k < 8 && i * 8 + k < bytes; k++) w |= (uint64_t)p[i * 8 + k] << (8 * k);
+    h += o_splitmix64(chunk_id ^ i ^ w);
+  }
+  return h;
+}
+
 EXPORT int oracle_decode_chunk(const void *chunk, size_t bytes, void *out, size_t out_cap, int32_t *offsets,
                                size_t offsets_cap, oracle_result *res) {
   oracle_result dummy;

@@ -51,6 +51,8 @@ def _load():
             lib.oracle_decode_chunk.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
                                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(OracleResult)]
             lib.oracle_decode_many.argtypes = [ctypes.c_void_p] * 7 + [ctypes.c_size_t, ctypes.c_int]
+            lib.oracle_checksum.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]
+            lib.oracle_checksum.restype = ctypes.c_uint64
             _lib = lib
         return _lib
 
@@ -109,3 +111,10 @@ def decode_many(chunks: list[np.ndarray], nthreads: int = 1):
         dtype, width, rows, payload = _header(c)
         result.append((outs[i][:payload], offs[i] if dtype == 4 else None))
     return result
+
+
+def checksum(data: np.ndarray, chunk_id: int) -> int:
+    """SURVEY Sec. 8a H9 positional checksum of a decoded buffer (see cdm_oracle.c)."""
+    lib = _load()
+    data = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    return int(lib.oracle_checksum(data.ctypes.data if data.size else None, data.size, chunk_id))

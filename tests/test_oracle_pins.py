@@ -520,3 +520,32 @@ def test_flipped_bytes_never_crash():
                 dec(bad)
             except OracleError:
                 pass
+
+
+# ----------------------------------------------------------------------------- H9 positional checksum
+# h = sum_i splitmix64(chunk_id ^ i ^ w_i) mod 2^64 over little-endian 8-byte words.
+
+def test_checksum_splitmix64_reference_value():
+    # SplitMix64 seeded with 0: first output 0xE220A8397B1DCDAF (the generator's published first value);
+    # one zero word at index 0 of chunk 0 hashes exactly that
+    assert oracle.checksum(np.zeros(8, np.uint8), 0) == 0xE220A8397B1DCDAF
+    # an empty buffer sums nothing
+    assert oracle.checksum(np.zeros(0, np.uint8), 123) == 0
+
+
+def test_checksum_invariants():
+    rng = np.random.default_rng(4)
+    a = rng.integers(0, 256, size=8 * 1000 + 5, dtype=np.uint8)
+    h = oracle.checksum(a, 77)
+    # additive over word-aligned pieces: the words keep their positions only if the pieces are placed at
+    # their offsets -- a prefix plus the zero-extended rest equals the whole minus zero-word terms
+    pre = a.copy(); pre[4000:] = 0
+    post = a.copy(); post[:4000] = 0
+    zero_terms = oracle.checksum(np.zeros_like(a), 77)
+    assert (oracle.checksum(pre, 77) + oracle.checksum(post, 77) - zero_terms) % (1 << 64) == h
+    # position-sensitive: swapping two different words changes it; so do the chunk id and one flipped bit
+    sw = a.copy(); sw[0:8], sw[8:16] = a[8:16], a[0:8]
+    assert oracle.checksum(sw, 77) != h
+    assert oracle.checksum(a, 78) != h
+    b = a.copy(); b[8 * 1000 + 4] ^= 1  # the zero-padded tail word counts
+    assert oracle.checksum(b, 77) != h
