@@ -202,6 +202,13 @@ CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms10, uint64_t *
  * waits for that replay) to accumulate its per-family times; a replay not collected is not counted. */
 CDM_API cdm_status cdm_batch_collect_timing(cdm_batch *b);
 
+/* ---- H9: optional positional checksum of a decoded device buffer:
+ *   h = sum_i splitmix64(chunk_id ^ i ^ w_i) mod 2^64 over its little-endian 8-byte words w_i (the last one
+ *   zero padded), computed by a kernel on `stream` (a cudaStream_t, NULL = legacy default stream); the call
+ *   waits for it and writes h to *out (host).  dev_data: device pointer, 8-byte aligned (16 reads faster).
+ *   Errors: CDM_E_INVALID_ARG (null / misaligned), CDM_E_CUDA. */
+CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t chunk_id, void *stream, uint64_t *out);
+
 /* ---- NEXT-3: launch-parameter knobs for the offline tuner ("Native Config", Table 3).
  * Process-wide, read when a batch / pipeline is enqueued or captured (a captured graph keeps its values).
  *   "fp_ctas_per_sm"  F.P. pattern's L: persistent fp_kernel CTAs per SM, 0 = adaptive (2/3/4 by batch

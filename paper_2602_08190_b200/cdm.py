@@ -27,7 +27,7 @@ SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_creat
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
            "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times",
            "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy",
-           "cdm_tune_set", "cdm_tune_get"]
+           "cdm_tune_set", "cdm_tune_get", "cdm_checksum"]
 
 
 class EngineOpts(ctypes.Structure):
@@ -100,6 +100,7 @@ def lib():
         "cdm_pipeline_destroy": [vp],
         "cdm_tune_set": [ctypes.c_char_p, ctypes.c_int],
         "cdm_tune_get": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)],
+        "cdm_checksum": [vp, ctypes.c_uint64, ctypes.c_uint64, vp, ctypes.POINTER(ctypes.c_uint64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -153,6 +154,13 @@ class Cascade:
         if getattr(self, "h", None) and _lib is not None:
             _lib.cdm_cascade_destroy(self.h)
             self.h = None
+
+
+def checksum(dev_buf, chunk_id: int, stream=None) -> int:
+    """H9 positional checksum of a decoded device buffer (include/cdm.h cdm_checksum)."""
+    v = ctypes.c_uint64()
+    _check(lib().cdm_checksum(_ptr(dev_buf), _nbytes(dev_buf), int(chunk_id), _stream_ptr(stream), ctypes.byref(v)))
+    return v.value
 
 
 def tune_set(knob: str, value: int) -> None:

@@ -254,6 +254,8 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s);
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);
 cudaError_t launch_harvest(uint32_t* err, uint32_t* host_mapped, uint32_t n, cudaStream_t s);
 int device_sms();
+// H9 positional checksum of a device buffer, ADDED into *dev_out (zero it first)
+cudaError_t launch_checksum(const void* p, uint64_t bytes, uint64_t chunk_id, uint64_t* dev_out, cudaStream_t s);
 
 // NEXT-3: launch parameters the offline tuner explores (Table 3's per-pattern spaces).
 // Process-wide; read by the launchers at enqueue time (a captured graph keeps the values it was built with).

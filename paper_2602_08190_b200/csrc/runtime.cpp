@@ -1870,6 +1870,22 @@ extern "C" CDM_API cdm_status cdm_batch_set_timing(cdm_batch* b, int enable) {
   return CDM_OK;
 }
 
+extern "C" CDM_API cdm_status cdm_checksum(const void* dev_data, uint64_t bytes, uint64_t chunk_id, void* stream,
+                                           uint64_t* out) {
+  if (!out || (bytes && !dev_data)) return fail(CDM_E_INVALID_ARG, "null argument");
+  if (reinterpret_cast<uintptr_t>(dev_data) % 8) return fail(CDM_E_INVALID_ARG, "dev_data must be 8-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint64_t* d = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), 8, s));
+  cudaError_t e = cudaMemsetAsync(d, 0, 8, s);
+  if (e == cudaSuccess) e = cdm::launch_checksum(dev_data, bytes, chunk_id, d, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, 8, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(CDM_E_CUDA, std::string("checksum: ") + cudaGetErrorString(e));
+  return CDM_OK;
+}
+
 extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
   if (!knob) return fail(CDM_E_INVALID_ARG, "null knob");
   const std::string k(knob);

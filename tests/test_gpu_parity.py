@@ -601,3 +601,29 @@ def test_all_families_one_batch_graph_and_timing(engine):
             km = b.kernel_ms()
             assert all(km[f][0] > 0 for f in ("fp", "scan", "rle", "lz4"))
     b.close()
+
+
+# ------------------------------------------------------------------------------ H9 positional checksum
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,spec", [("l_orderkey", "RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]"),
+                                       ("l_extendedprice", "Float2Int|BitPack"), ("l_shipmode", "Dict|BitPack"),
+                                       ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]")])
+def test_checksum_matches_oracle(engine, name, spec):
+    """cdm_checksum of the device-decoded buffers == the oracle's checksum of its own decode."""
+    col = TPCH(0.02).column(name)
+    chunks = encoder.encode_chunks(spec, col, 50_001)
+    casc = cdm.Cascade(spec, col.dtype, col.width)
+    for ch in chunks:
+        out, offs = cdm.output_buffers(ch)
+        b = cdm.Batch(engine, [cdm.Decode(casc, ch, out, offs, dev_chunk=torch.from_numpy(ch).cuda())])
+        b.launch()
+        (r,) = b.results()
+        b.close()
+        cid = cdm.chunk_info(ch)["chunk_id"]
+        exp, exp_offs = oracle.decode_chunk(ch)
+        assert cdm.checksum(out[: exp.size], cid) == oracle.checksum(exp, cid)
+        if exp_offs is not None:
+            assert cdm.checksum(offs[: exp_offs.size], cid) == oracle.checksum(exp_offs, cid)
+    # a misaligned pointer is rejected, not read
+    with pytest.raises(cdm.CdmError):
+        cdm.checksum(out[1:9], 0)
