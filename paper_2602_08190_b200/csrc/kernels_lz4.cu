@@ -424,13 +424,16 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
     lz4_smem_kernel<<<grid, wpc * 32, smem, s>>>(b, cap);
     return cudaGetLastError();
   }
-  // lane groups of G lanes per sub-chunk (default 4: 8 sub-chunks per warp); G = 32 is one warp per
+  // lane groups of G lanes per sub-chunk (default 4: 8 sub-chunks per warp; G = 1 is the paper's thread per
+  // chunk); G = 32 is one warp per
   // sub-chunk (tuning knob TUNE_LZ4_LANES; env CDM_LZ4_G / CDM_LZ4_WARP)
   const int G = tune_get(TUNE_LZ4_LANES);
   if (G != 32) {
     const uint32_t per_cta = kWarpsPerCta * 32 / G;
     const uint32_t grid = (b.total_subs + per_cta - 1) / per_cta;
     if (G == 4) lz4_group_kernel<4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else if (G == 1) lz4_group_kernel<1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else if (G == 2) lz4_group_kernel<2><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     else if (G == 16) lz4_group_kernel<16><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     else lz4_group_kernel<8><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();

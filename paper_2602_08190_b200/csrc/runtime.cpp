@@ -1893,7 +1893,8 @@ extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
     if (value < 0 || value > 16) return fail(CDM_E_INVALID_ARG, "fp_ctas_per_sm must be 0..16");
     cdm::tune_set(cdm::TUNE_FP_CTAS_PER_SM, value);
   } else if (k == "lz4_lanes") {
-    if (value != 4 && value != 8 && value != 16 && value != 32) return fail(CDM_E_INVALID_ARG, "lz4_lanes must be 4, 8, 16 or 32");
+    if (value != 1 && value != 2 && value != 4 && value != 8 && value != 16 && value != 32)
+      return fail(CDM_E_INVALID_ARG, "lz4_lanes must be 1, 2, 4, 8, 16 or 32");
     cdm::tune_set(cdm::TUNE_LZ4_LANES, value);
   } else {
     return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");

@@ -363,7 +363,20 @@ def test_lz4_subchunk_sizes(engine, sub):
     check_parity(engine, f"Str|[LZ4(sub={sub}),BitPack]", col, rows_per_chunk=40_000, both=False)
 
 
-def test_lz4_overlapping_matches(engine):
+@pytest.fixture(params=[4, 1, 2, 8, 16, 32])
+def lz4_lanes(request):
+    """every LZ4 lane-group width the tuner may select (NEXT-3 knob lz4_lanes)"""
+    cdm.tune_set("lz4_lanes", request.param)
+    yield request.param
+    cdm.tune_set("lz4_lanes", 4)
+
+
+def test_lz4_lane_widths(engine, lz4_lanes):
+    col = TPCH(0.01).column("l_comment")
+    check_parity(engine, "Str|[LZ4(sub=4096),BitPack]", col, rows_per_chunk=30_001, both=False)
+
+
+def test_lz4_overlapping_matches(engine, lz4_lanes):
     from test_oracle_pins import _seq
     blocks, sizes = [], []
     for off, mlen in [(1, 4), (1, 300), (2, 19), (3, 1000), (5, 5), (7, 270), (31, 100), (32, 100), (33, 700)]:

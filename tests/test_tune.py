@@ -69,6 +69,9 @@ def test_cabi_tuning_knobs():
     cdm.tune_set("fp_ctas_per_sm", 3)
     assert cdm.tune_get("fp_ctas_per_sm") == 3
     cdm.tune_set("fp_ctas_per_sm", old)
+    cdm.tune_set("lz4_lanes", 1)
+    assert cdm.tune_get("lz4_lanes") == 1
+    cdm.tune_set("lz4_lanes", 4)
     for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("nope", 1)):
         with pytest.raises(cdm.CdmError):
             cdm.tune_set(knob, v)

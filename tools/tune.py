@@ -2,7 +2,7 @@
 
 The B200 build fixes S (256 threads per CTA) and the tile shapes at compile time, so the runtime spaces are:
   F.P.  L = persistent fp_kernel CTAs per SM (knob fp_ctas_per_sm) in 2^0..2^4     (Table 3: L 2^0..2^4)
-  N.P.  C = lanes per LZ4 sub-chunk (knob lz4_lanes) in {4, 8, 16, 32}             (Table 3: C 2^0..2^10)
+  N.P.  C = lanes per LZ4 sub-chunk (knob lz4_lanes) in {1, 2, 4, 8, 16, 32}       (Table 3: C 2^0..2^10)
 Each evaluation builds a fresh graph-mode batch over the workload (so the knob is captured), times K replays
 with CUDA events after a 256 MiB L2-flush write each, and returns decoded GB/s.
 usage: python tools/tune.py [--sf 10] [--steps 5] -> JSON lines + a summary table
@@ -68,7 +68,7 @@ def main():
     cases = {
         "FP": ({"fp_ctas_per_sm": [1, 2, 4, 8, 16]},
                [("Dict|BitPack", g.column("l_quantity")), ("Float2Int|BitPack", g.column("l_extendedprice"))]),
-        "NP": ({"lz4_lanes": [4, 8, 16, 32]}, [("Str|[LZ4(sub=16384),BitPack]", g.column("l_comment"))]),
+        "NP": ({"lz4_lanes": [1, 2, 4, 8, 16, 32]}, [("Str|[LZ4(sub=16384),BitPack]", g.column("l_comment"))]),
     }
     rows = []
     for pat, (space, cols) in cases.items():
