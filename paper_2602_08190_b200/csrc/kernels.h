@@ -228,12 +228,15 @@ struct SdDesc {
   uint32_t ntiles;
   uint32_t err_idx;
   uint32_t w;
-  uint32_t pad;
+  uint32_t cta0;               // first sd_expand CTA (kSdCtaTiles tiles per CTA)
 };
+
+constexpr int kSdCtaTiles = 4;        // sd_expand: tiles per CTA (the dictionary is copied once per CTA)
 
 struct SdBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint32_t total_ctas;         // sd_expand grid
   uint32_t dict_smem;          // largest dictionary stream rounded to 16 B + 16 if all fit kSdDictSmem, else 0 (L1)
   uint32_t* err;
   SdDesc d[kMaxBatch];

@@ -51,7 +51,7 @@ __device__ __forceinline__ TileRange my_tiles(uint32_t total) {
 // dictionary stream (offsets + token bytes) of descriptor D -> shared memory (16-byte copies)
 __device__ __forceinline__ void load_dict(const SdDesc& D, uint32_t bytes, uint32_t* dict_s) {
   const uint4* src = reinterpret_cast<const uint4*>(D.dict);
-  for (uint32_t i = threadIdx.x; i < (bytes + 15) / 16; i += kThreads) reinterpret_cast<uint4*>(dict_s)[i] = __ldg(src + i);
+  for (uint32_t i = threadIdx.x; i < (bytes + 15) / 16; i += blockDim.x) reinterpret_cast<uint4*>(dict_s)[i] = __ldg(src + i);
 }
 
 // this thread's tokens kb .. kb + 7 of a tile (ids staged in shared words): dictionary offsets and lengths
@@ -220,6 +220,144 @@ __global__ void __launch_bounds__(kThreads) sd_expand_kernel(const __grid_consta
   }
 }
 
+// sd_expand2 (default): word-parallel, the paper's Group-Parallel item loop turned around -- every output
+// word is an item, found in its group (token) by rank.  Per tile: the block scan of (non-empty tokens << 32 |
+// bytes) places every non-empty token (start position, dictionary offset; a sentinel end) in shared arrays and
+// marks its start in a bitmap; per-bitmap-word prefix counts make rank(p) = #starts <= p one popcount away.
+// Thread i then builds staged 32-bit word i: the token holding its first byte by rank, 4 dictionary bytes
+// per piece (two aligned words + a funnel shift), the next token when this one ends -- consecutive lanes take
+// consecutive words (no divergence beyond the 1-2 pieces a word needs, no atomics: a word has one owner).
+// The dictionary (offsets + token bytes) is copied into shared memory once per CTA of kSdCtaTiles tiles
+// (bank conflicts instead of one L1 wavefront per distinct line); larger ones are read through L1.
+constexpr int kSdT2 = 512;                      // threads per CTA
+constexpr int kSdPer2 = kSdTile / kSdT2;        // 4 tokens per thread
+constexpr uint32_t kSdBmWords = kSdStage / 32 + 2;
+
+__global__ void __launch_bounds__(kSdT2) sd_expand2_kernel(const __grid_constant__ SdBatch B) {
+  extern __shared__ __align__(16) uint32_t dyn_s[];  // stage image, then (B.dict_smem) the dictionary
+  uint32_t* const stage_s = dyn_s;
+  uint32_t* const dict_s = dyn_s + (kSdStage + 32) / 4;
+  __shared__ uint32_t ids_s[kIdsWords];
+  __shared__ uint32_t pos_s[kSdTile + 1], a_s[kSdTile];
+  __shared__ uint32_t bm_s[kSdBmWords], cnt_s[kSdBmWords];
+  __shared__ uint64_t warp_s[kSdT2 / 32];
+  const uint32_t tid = threadIdx.x;
+  // this CTA's descriptor and tiles
+  int lo = 0, hi = int(B.n) - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (B.d[mid].cta0 <= blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const SdDesc& D = B.d[lo];
+  const uint32_t t0 = (blockIdx.x - D.cta0) * kSdCtaTiles, t1 = min(D.ntiles, t0 + kSdCtaTiles);
+  const uint32_t* offs = reinterpret_cast<const uint32_t*>(D.dict);
+  if (B.dict_smem) {
+    load_dict(D, 4u * (D.entries + 1u) + __ldg(offs + D.entries), dict_s);
+    offs = dict_s;
+  }
+  const uint32_t* tw = offs + D.entries + 1u;  // token bytes, 4-byte aligned
+  const uint32_t kb = tid * kSdPer2;
+  for (uint32_t lt = t0; lt < t1; lt++) {
+    const uint32_t g0 = lt * kSdTile;
+    const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
+    __syncthreads();  // previous tile's arrays are dead (and the dictionary copy is complete)
+    stage_bits<kSdT2>(ids_s, D.ids_packed, g0, nt, D.w);
+    for (uint32_t i = tid; i < kSdBmWords; i += kSdT2) bm_s[i] = 0u;
+    __syncthreads();
+    uint32_t a[kSdPer2], len[kSdPer2];
+    uint32_t s = 0, ne = 0;
+#pragma unroll
+    for (int r = 0; r < kSdPer2; r++) {
+      a[r] = 0;
+      len[r] = 0;
+      const uint32_t k = kb + r;
+      if (k < nt) {
+        const uint64_t id = D.id_base + extract_bits(ids_s, uint64_t(k) * D.w, D.w);
+        if (id < D.entries) {
+          a[r] = offs[id];
+          len[r] = offs[id + 1] - a[r];
+        }
+      }
+      s += len[r];
+      ne += len[r] != 0u;
+    }
+    uint64_t T;
+    const uint64_t ex = block_excl_scan_u64<kSdT2>((uint64_t(ne) << 32) | s, warp_s, &T);
+    const uint64_t O64 = __ldcg(D.tsum + lt);
+    const uint32_t Tt = uint32_t(T), NE = uint32_t(T >> 32);
+    if (O64 + Tt > D.n_out) continue;  // inconsistent lengths (sd_scan reports them): never write outside
+    const uint32_t O = uint32_t(O64), sh = O & 15u;
+    uint8_t* const out = D.out;
+    if (Tt > kSdStage) {  // long tokens: direct byte stores
+      const uint8_t* tb = reinterpret_cast<const uint8_t*>(tw);
+      uint32_t p = O + uint32_t(ex);
+#pragma unroll
+      for (int r = 0; r < kSdPer2; r++) {
+        for (uint32_t j = 0; j < len[r]; j++) out[p + j] = tb[a[r] + j];
+        p += len[r];
+      }
+      continue;
+    }
+    {  // non-empty tokens: start position (stage coordinates), dictionary offset, start bit
+      uint32_t p = sh + uint32_t(ex), k = uint32_t(ex >> 32);
+#pragma unroll
+      for (int r = 0; r < kSdPer2; r++) {
+        if (len[r]) {
+          pos_s[k] = p;
+          a_s[k] = a[r];
+          atomicOr(bm_s + (p >> 5), 1u << (p & 31));
+          k++;
+        }
+        p += len[r];
+      }
+      if (tid == 0) pos_s[NE] = sh + Tt;  // sentinel: the end of the last token
+    }
+    __syncthreads();
+    const uint32_t nbw = (sh + Tt + 31) / 32;
+    {  // cnt_s[j] = number of token starts in bitmap words < j (two words per thread)
+      const uint32_t j0 = 2 * tid;
+      const uint32_t c0 = j0 < nbw ? __popc(bm_s[j0]) : 0u, c1 = j0 + 1 < nbw ? __popc(bm_s[j0 + 1]) : 0u;
+      uint64_t tot;
+      const uint32_t e = uint32_t(block_excl_scan_u64<kSdT2>(c0 + c1, warp_s, &tot));
+      if (j0 < nbw) cnt_s[j0] = e;
+      if (j0 + 1 < nbw) cnt_s[j0 + 1] = e + c0;
+    }
+    __syncthreads();
+    const uint32_t end = sh + Tt, nw4 = (end + 3) / 4;
+    for (uint32_t i = (sh >> 2) + tid; i < nw4; i += kSdT2) {
+      uint32_t b = max(4 * i, sh);
+      const uint32_t be = min(4 * i + 4, end);
+      const uint32_t wj = b >> 5;
+      uint32_t k = cnt_s[wj] + __popc(bm_s[wj] & uint32_t((2ull << (b & 31)) - 1ull)) - 1u;
+      uint32_t word = 0;
+      while (b < be) {
+        const uint32_t ts = pos_s[k], te = pos_s[k + 1];
+        const uint32_t off = a_s[k] + (b - ts);
+        const uint32_t piece = __funnelshift_r(tw[off >> 2], tw[(off >> 2) + 1], (off & 3u) * 8u);
+        const uint32_t m = min(be, te) - b;
+        word |= (m >= 4u ? piece : piece & ((1u << (8u * m)) - 1u)) << (8u * (b - 4 * i));
+        b += m;
+        k++;
+      }
+      stage_s[i] = word;
+    }
+    __syncthreads();
+    const uint32_t nw = (end + 15) / 16;
+    uint4* const ow = reinterpret_cast<uint4*>(out + (O - sh));
+    const uint4* const sw = reinterpret_cast<const uint4*>(stage_s);
+    const uint8_t* const sb = reinterpret_cast<const uint8_t*>(stage_s);
+    for (uint32_t i = tid; i < nw; i += kSdT2) {
+      const uint32_t lo16 = 16 * i, hi16 = lo16 + 16;
+      if (lo16 >= sh && hi16 <= end) {
+        ow[i] = sw[i];
+      } else {  // an edge word shared with the neighbouring tiles: only this tile's bytes
+        uint8_t* const ob = reinterpret_cast<uint8_t*>(ow + i);
+        for (uint32_t q = max(lo16, sh); q < min(hi16, end); q++) ob[q - lo16] = sb[q];
+      }
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
@@ -228,6 +366,7 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
   if (!configured) {
     cudaFuncSetAttribute(sd_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
     cudaFuncSetAttribute(sd_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
+    cudaFuncSetAttribute(sd_expand2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 32 + kSdDictSmem);
     configured = true;
   }
   // default: every kernel reads the dictionary through L1 (random tokens cost one wavefront per distinct line:
@@ -239,8 +378,16 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
   l1.dict_smem = 0;
   sd_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   sd_scan_kernel<<<b.n, kThreads, 0, s>>>(b);
-  if (smem && b.dict_smem) sd_expand_kernel<<<b.total_tiles, kThreads, b.dict_smem, s>>>(b);
-  else sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
+  // CDM_SD_EXPAND=1: the per-thread-token expansion (sd_expand_kernel, CDM_SD_SMEM=1 with a per-tile
+  // shared dictionary); default: the word-parallel sd_expand2_kernel
+  static const int variant = std::getenv("CDM_SD_EXPAND") ? std::atoi(std::getenv("CDM_SD_EXPAND")) : 2;
+  if (variant == 1) {
+    if (smem && b.dict_smem) sd_expand_kernel<<<b.total_tiles, kThreads, b.dict_smem, s>>>(b);
+    else sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
+  } else {
+    const uint32_t dyn = kSdStage + 32 + b.dict_smem;
+    sd_expand2_kernel<<<b.total_ctas, kSdT2, dyn, s>>>(b);
+  }
   return cudaGetLastError();
 }
 

@@ -808,7 +808,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (auto& g : groups(sdj)) {
     SdBatch sb{};
     sb.err = B->err_dev;
-    uint32_t tiles = 0, dmax = 0;
+    uint32_t tiles = 0, dmax = 0, ctas = 0;
     bool fits = true;
     for (int j : g) {
       const Bound& b = B->jobs[j];
@@ -823,6 +823,8 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       d.w = b.sd_w;
       d.tile0 = tiles;
       d.ntiles = uint32_t(div_up(b.sd_ntok, kSdTile));
+      d.cta0 = ctas;
+      ctas += uint32_t(div_up(d.ntiles, kSdCtaTiles));
       d.tsum = A.take<uint64_t>(d.ntiles + 1);
       d.err_idx = uint32_t(j);
       tiles += d.ntiles;
@@ -831,6 +833,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       fits = fits && db <= uint32_t(kSdDictSmem);
     }
     sb.total_tiles = tiles;
+    sb.total_ctas = ctas;
     sb.dict_smem = fits ? dmax : 0u;  // else the kernels read the dictionaries through L1
     B->sd.push_back(sb);
   }
