@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) sd_expand_kernel(const __grid_consta
   }
 }
 
-// sd_expand2 (default): word-parallel, the paper's Group-Parallel item loop turned around -- every output
+// sd_expand2 (opt-in, CDM_SD_EXPAND=2; measured slower, see launch_strdict): word-parallel, the paper's Group-Parallel item loop turned around -- every output
 // word is an item, found in its group (token) by rank.  Per tile: the block scan of (non-empty tokens << 32 |
 // bytes) places every non-empty token (start position, dictionary offset; a sentinel end) in shared arrays and
 // marks its start in a bitmap; per-bitmap-word prefix counts make rank(p) = #starts <= p one popcount away.
@@ -378,10 +378,11 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
   l1.dict_smem = 0;
   sd_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   sd_scan_kernel<<<b.n, kThreads, 0, s>>>(b);
-  // CDM_SD_EXPAND=1: the per-thread-token expansion (sd_expand_kernel, CDM_SD_SMEM=1 with a per-tile
-  // shared dictionary); default: the word-parallel sd_expand2_kernel
-  static const int variant = std::getenv("CDM_SD_EXPAND") ? std::atoi(std::getenv("CDM_SD_EXPAND")) : 2;
-  if (variant == 1) {
+  // default: the per-thread-token expansion (sd_expand_kernel, 1.35 ms for o_comment SF 10; CDM_SD_SMEM=1
+  // with a per-tile shared dictionary); CDM_SD_EXPAND=2: the word-parallel sd_expand2_kernel (1.68 ms:
+  // ~100 instructions per output word, issue-bound at IPC 2.7 with 2 CTAs of 512 threads per SM)
+  static const int variant = std::getenv("CDM_SD_EXPAND") ? std::atoi(std::getenv("CDM_SD_EXPAND")) : 1;
+  if (variant != 2) {
     if (smem && b.dict_smem) sd_expand_kernel<<<b.total_tiles, kThreads, b.dict_smem, s>>>(b);
     else sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   } else {

@@ -7,6 +7,7 @@ with oracle/ on the same seeded inputs.  Integer/byte work must be bit-exact and
 division on both sides, so the tolerance is zero everywhere.  Outputs are pre-filled
 with a sentinel so an element that is never written, or written outside [0, n), is caught.
 """
+import os
 import struct
 
 import numpy as np
@@ -317,6 +318,19 @@ def test_strdict_long_tokens_and_empty_strings(engine):
     one = Column("one", VARBYTES, 0, 3, np.frombuffer(b"hello ", dtype=np.uint8).copy(),
                  np.array([0, 0, 6, 6], dtype=np.int64))
     check_parity(engine, "Str|[StrDict|BitPack,BitPack]", one, both=False)
+
+
+def test_strdict_word_parallel_variant():
+    """the opt-in sd_expand2 kernel (CDM_SD_EXPAND=2) decodes the same bytes (fresh process: env read once)"""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
+            "from paper_2602_08190_b200.inputs import TPCH; e = cdm.Engine(0); "
+            "t.check_parity(e, 'Str|[StrDict|BitPack|ANS,BitPack]', TPCH(0.02).column('o_comment'), rows_per_chunk=50_001, both=False); "
+            "t.test_strdict_long_tokens_and_empty_strings(e); print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_SD_EXPAND": "2"}, capture_output=True,
+                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_corrupt_strdict_sets_error(engine):
