@@ -117,8 +117,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_kernel(const __grid_con
 // the offset (shuffled out within the group); literal and match bytes are copied 8 per step with
 // out[p + k] = out[p - o + (k mod o)] for overlapping short periods; __syncwarp(group mask) orders a
 // group's stores before its match reads.  Same bounds checks and error bit as lz4_kernel.
-template <uint32_t kLzG>  // lanes per sub-chunk
+// kWB = window bytes per lane: 1 (one compressed byte per lane), or 4 (each lane holds 4 bytes -- two
+// aligned words + a funnel shift -- so a 4-lane group sees 16 bytes: token, literals and offset of most
+// sequences in one load round).
+template <uint32_t kLzG, uint32_t kWB>  // lanes per sub-chunk, window bytes per lane
 __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __grid_constant__ Lz4Batch B) {
+  constexpr uint32_t kWS = kLzG * kWB;  // window bytes per group
   const uint32_t lane = threadIdx.x & 31, gl = lane & (kLzG - 1);
   const uint32_t gmask = (kLzG == 32 ? FULL : ((1u << kLzG) - 1u)) << (lane & ~(kLzG - 1));
   const uint32_t gs = (blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x) / kLzG;
@@ -146,9 +150,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __gr
   uint32_t ip = 0, op = 0;
   for (;;) {
     if (ip >= cl) { bad = true; break; }
-    // window: compressed bytes [ip, ip + 8), one per lane
-    const uint32_t wb = ip + gl < cl ? uint32_t(__ldg(in + ip + gl)) : 0u;
-    const uint32_t token = __shfl_sync(gmask, wb, 0, kLzG);
+    // window: compressed bytes [ip, ip + kWS), kWB per lane (bytes past cl are never used: every use below
+    // is bounds-checked against cl; the stream's 16 slack bytes keep the aligned word reads in bounds)
+    uint32_t wb;
+    if (kWB == 1) {
+      wb = ip + gl < cl ? uint32_t(__ldg(in + ip + gl)) : 0u;
+    } else {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(in + ip + kWB * gl);
+      const uint32_t* pw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+      wb = ip + kWB * gl < cl ? __funnelshift_r(__ldg(pw), __ldg(pw + 1), uint32_t(a & 3u) * 8u) : 0u;
+    }
+    // window byte j (j < kWS for a meaningful value; the lane index wraps modulo the group otherwise)
+    auto wbyte = [&](uint32_t j) -> uint32_t {
+      const uint32_t v = __shfl_sync(gmask, wb, j / kWB, kLzG);
+      return kWB == 1 ? v : (v >> ((j % kWB) * 8u)) & 0xFFu;
+    };
+    const uint32_t token = wbyte(0);
     uint32_t lit = token >> 4;
     uint32_t q = ip + 1;
     if (lit == 15) {
@@ -161,9 +178,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __gr
       if (bad) break;
     }
     if (lit > cl - q || lit > dl - op) { bad = true; break; }
-    if (q + lit <= ip + kLzG) {  // literals inside the window: lane gl takes window byte (q - ip) + gl
-      const uint32_t v = __shfl_sync(gmask, wb, (q - ip + gl) & (kLzG - 1), kLzG);
-      if (gl < lit) out[op + gl] = uint8_t(v);
+    if (q + lit <= ip + kWS) {  // literals inside the window: lane gl takes window bytes (q - ip) + gl + kLzG*t
+      for (uint32_t base = 0; base < lit; base += kLzG) {  // group-uniform trip count (shuffles inside)
+        const uint32_t v = wbyte(q - ip + base + gl);
+        if (base + gl < lit) out[op + base + gl] = uint8_t(v);
+      }
     } else {
       for (uint32_t k = gl; k < lit; k += kLzG) out[op + k] = __ldg(in + q + k);
     }
@@ -172,10 +191,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __gr
     if (q == cl) break;  // the last sequence carries literals only
     if (cl - q < 2) { bad = true; break; }
     uint32_t moff;
-    if (q + 2 <= ip + kLzG) {
-      const uint32_t lo = __shfl_sync(gmask, wb, (q - ip) & (kLzG - 1), kLzG);
-      const uint32_t hi = __shfl_sync(gmask, wb, (q - ip + 1) & (kLzG - 1), kLzG);
-      moff = lo | (hi << 8);
+    if (q + 2 <= ip + kWS) {
+      moff = wbyte(q - ip) | (wbyte(q - ip + 1) << 8);
     } else {
       moff = uint32_t(__ldg(in + q)) | (uint32_t(__ldg(in + q + 1)) << 8);
     }
@@ -431,11 +448,22 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
   if (G != 32) {
     const uint32_t per_cta = kWarpsPerCta * 32 / G;
     const uint32_t grid = (b.total_subs + per_cta - 1) / per_cta;
-    if (G == 4) lz4_group_kernel<4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    else if (G == 1) lz4_group_kernel<1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    else if (G == 2) lz4_group_kernel<2><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    else if (G == 16) lz4_group_kernel<16><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    else lz4_group_kernel<8><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    // window bytes per lane: 1 (default) or 4 (CDM_LZ4_WIN=4: a 16-byte window per 4-lane group -- measured
+    // 10.0 vs 9.5 ms on config 3's l_comment: the sequence chain is not bound by its compressed-byte loads)
+    static const bool win1 = !(std::getenv("CDM_LZ4_WIN") && std::getenv("CDM_LZ4_WIN")[0] == '4');
+    if (win1) {
+      if (G == 4) lz4_group_kernel<4, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else if (G == 1) lz4_group_kernel<1, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else if (G == 2) lz4_group_kernel<2, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else if (G == 16) lz4_group_kernel<16, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else lz4_group_kernel<8, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    } else {
+      if (G == 4) lz4_group_kernel<4, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else if (G == 1) lz4_group_kernel<1, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else if (G == 2) lz4_group_kernel<2, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else if (G == 16) lz4_group_kernel<16, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+      else lz4_group_kernel<8, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    }
     return cudaGetLastError();
   }
   const uint32_t grid = (b.total_subs + kWarpsPerCta - 1) / kWarpsPerCta;
