@@ -138,17 +138,28 @@ __device__ __forceinline__ void take_ticket(unsigned long long* ctr, uint32_t la
   if (*ticket == last) atomicExch(ctr, (unsigned long long)(*epoch + 1) << 32);
 }
 
-// Look-back word: 16 bytes {flag = (epoch << 2) | state, c (u32, saturating count), w (u64, wrapping)},
-// published with ONE 128-bit relaxed store and probed with ONE 128-bit load, so a reader never sees a flag
-// without its values and no fence is needed (the CUB ScanTileState 16-byte TxnWord idiom).
+// Look-back record of tile t: three 16-byte words -- [3t] the flag word {flag = (epoch << 2) | state}, [3t+1]
+// the AGG values {c (u32, saturating count), w (u64, wrapping)}, [3t+2] the INC values.  A publisher writes
+// the state's value word, then the flag with a release store; a reader acquires the flag, then reads the
+// value word of the state it saw.  Each value word is written once per epoch, before its flag, so a reader
+// never combines a flag with values it does not belong to -- without relying on 16-byte store atomicity
+// (the PTX memory model promises single-copy atomicity only up to 8 bytes).
 constexpr uint32_t LB_AGG = 1, LB_INC = 2;
 
-__device__ __forceinline__ void lb_store(uint4* p, uint32_t flag, uint32_t c, uint64_t w) {
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(flag), "r"(c),
-               "r"(uint32_t(w)), "r"(uint32_t(w >> 32))
+__device__ __forceinline__ void lb_store_vals(uint4* p, uint32_t c, uint64_t w) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(0u), "r"(c), "r"(uint32_t(w)),
+               "r"(uint32_t(w >> 32))
                : "memory");
 }
-__device__ __forceinline__ uint4 lb_load(const uint4* p) {
+__device__ __forceinline__ void lb_store_flag(uint4* p, uint32_t flag) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(flag) : "memory");
+}
+__device__ __forceinline__ uint32_t lb_load_flag(const uint4* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 lb_load_vals(const uint4* p) {
   uint4 v;
   asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -161,7 +172,8 @@ __device__ __forceinline__ uint32_t sat32(uint64_t x) { return x > 0xFFFFFFFFull
 
 __device__ __forceinline__ void lb_publish(uint4* words, uint32_t gt, uint32_t epoch, uint32_t state, uint64_t c,
                                            uint64_t w) {
-  lb_store(words + gt, (epoch << 2) | state, sat32(c), w);
+  lb_store_vals(words + 3ull * gt + state, sat32(c), w);
+  lb_store_flag(words + 3ull * gt, (epoch << 2) | state);
 }
 
 // Single-warp decoupled look-back: lanes probe 32 predecessors at a time (gt-1-lane) and fold the AGG
@@ -177,11 +189,12 @@ __device__ __forceinline__ void lb_lookback(const uint4* words, uint32_t gt, uin
     uint32_t st = LB_INC;  // lanes below the chunk start act as a terminating INC with value 0
     uint64_t c = 0, w = 0;
     if (me >= int64_t(first_gt)) {
-      uint4 v;
+      uint32_t f;
       do {
-        v = lb_load(words + me);
-      } while ((v.x >> 2) != epoch || (v.x & 3u) == 0);
-      st = v.x & 3u;
+        f = lb_load_flag(words + 3ull * me);
+      } while ((f >> 2) != epoch || (f & 3u) == 0);
+      st = f & 3u;
+      const uint4 v = lb_load_vals(words + 3ull * me + st);
       c = v.y;
       w = (uint64_t(v.w) << 32) | v.z;
     }

@@ -70,7 +70,7 @@ struct ScanBatch {
   uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   unsigned long long* ticket;  // epoch|ticket counter
-  uint4* lb;                   // [total_tiles] 16-byte look-back words
+  uint4* lb;                   // [total_tiles][3] look-back records: flag word, AGG values, INC values
   ScanDesc d[kMaxBatch];
 };
 

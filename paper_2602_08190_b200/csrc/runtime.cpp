@@ -645,7 +645,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     }
     sb.total_tiles = tiles;
     sb.ticket = A.take<unsigned long long>(1);
-    sb.lb = A.take<uint4>(tiles);
+    sb.lb = A.take<uint4>(size_t(tiles) * 3);  // per tile: flag word, AGG values, INC values
     B->scan.push_back(sb);
   }
   // RLE units: one per expansion level of each RLE job (deepest first).  A non-final level (the value lineage
