@@ -42,6 +42,7 @@ struct FpDesc {
 struct FpBatch {
   uint32_t n;
   uint32_t total_tiles;
+  uint32_t pair_map;      // 8-byte rows: pair-interleaved lane mapping (set by launch_fp)
   uint32_t* err;          // per-chunk error words
   FpDesc d[kMaxBatch];
 };

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     const uint64_t tile_start = uint64_t(lt) * kFpTile;
     const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
     bool bad_index = false;
+    const bool pair_map = B.pair_map;
     const bool bytes_path = mode == FP_DICT && ob != 4 && ob != 8;  // CHAR(n) rows
     const bool dsm = DM == 1 && mode == FP_DICT && !bytes_path && entries * ob <= kDictSmemBytes;
     const bool dsmb = DM == 1 && bytes_path && uint64_t(entries) * ob + 8 <= kDictSmemBytes;
@@ -117,6 +118,46 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
 
 #pragma unroll 1
     for (uint32_t k = 0; k < kFpTile / 1024 && !bytes_path; k++) {
+      if (ob == 8 && pair_map) {
+        // 8-byte rows: lane l of warp u takes the pairs (pa, pa+1) and (pa+64, pa+65), pa = 128u + 2l, so each
+        // 16-byte store instruction of a warp covers 512 contiguous bytes (whole sectors)
+        if (k * 1024 >= valid) break;
+        const uint32_t pa = k * 1024 + (tid >> 5) * 128 + 2 * (tid & 31);
+        const uint32_t q[4] = {pa, pa + 1, pa + 64, pa + 65};
+        uint64_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t bj = q[j] * w;
+          v[j] = w <= 32 ? base + (__funnelshift_r(wd[bj >> 5], wd[(bj >> 5) + 1], bj & 31) & m32)
+                         : base + extract_bits(wd, uint64_t(q[j]) * w, w);
+        }
+        uint64_t r[4];
+        if (mode == FP_INT) {
+#pragma unroll
+          for (int j = 0; j < 4; j++) r[j] = v[j];
+        } else if (mode == FP_DICT) {
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const uint64_t f = v[j] - base;
+            const bool ok = f < lim;
+            bad_index |= !ok && q[j] < valid;
+            const uint32_t idx = ok ? base32 + uint32_t(f) : 0u;
+            r[j] = dsm ? dict_s[idx] : __ldg(reinterpret_cast<const uint64_t*>(dict8) + idx);
+          }
+        } else {
+          const double p = kPow10[D.d];
+#pragma unroll
+          for (int j = 0; j < 4; j++) r[j] = __double_as_longlong(double(int64_t(v[j])) / p);
+        }
+        uint64_t* o = reinterpret_cast<uint64_t*>(out8) + tile_start;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint32_t e = q[2 * h];
+          if (e + 1 < valid) st_v2_u64(o + e, r[2 * h], r[2 * h + 1]);
+          else if (e < valid) o[e] = r[2 * h];
+        }
+        continue;
+      }
       const uint32_t i0 = k * 1024 + tid * 4;  // 4 consecutive values
       if (i0 >= valid) break;
       uint64_t v[4];
@@ -328,7 +369,17 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   // are scheduled as soon as any FP CTA retires
   static const bool per_tile = std::getenv("CDM_FP_GRID") && std::getenv("CDM_FP_GRID")[0] == 't';
   if (per_tile || grid > b.total_tiles) grid = b.total_tiles;
-  kern<<<grid, kThreads, tma ? smem : 0, s>>>(b, stage);
+  // default: 4 consecutive values per thread (8-byte rows: two 16-byte stores 32 bytes apart per lane);
+  // CDM_FP_PAIR=1: pair-interleaved lanes (whole-sector store instructions) -- measured: E7 l_quantity
+  // 0.127 -> 0.104 ms but l_extendedprice 0.118 -> 0.125 ms and config 2 2695 -> 2601 GB/s, so off
+  static const bool pair = std::getenv("CDM_FP_PAIR") && std::getenv("CDM_FP_PAIR")[0] == '1';
+  if (b.pair_map != uint32_t(pair)) {
+    FpBatch c = b;
+    c.pair_map = pair;
+    kern<<<grid, kThreads, tma ? smem : 0, s>>>(c, stage);
+  } else {
+    kern<<<grid, kThreads, tma ? smem : 0, s>>>(b, stage);
+  }
   return cudaGetLastError();
 }
 

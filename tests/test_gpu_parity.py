@@ -390,6 +390,20 @@ def test_lz4_lane_widths(engine, lz4_lanes):
     check_parity(engine, "Str|[LZ4(sub=4096),BitPack]", col, rows_per_chunk=30_001, both=False)
 
 
+def test_fp_pair_mapping_variant():
+    """the opt-in pair-interleaved FP lane mapping (CDM_FP_PAIR=1) decodes the same rows (fresh process)"""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
+            "from paper_2602_08190_b200.inputs import TPCH; e = cdm.Engine(0); g = TPCH(0.02); "
+            "[t.check_parity(e, s, g.column(n), rows_per_chunk=50_001, both=False) for n, s in "
+            "(('l_quantity', 'Dict|BitPack'), ('l_extendedprice', 'Float2Int|BitPack'), ('l_orderkey', 'BitPack'), "
+            "('o_totalprice', 'Float2Int|BitPack'))]; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_FP_PAIR": "1"}, capture_output=True,
+                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_lz4_wide_window_variant():
     """the opt-in 4-bytes-per-lane window (CDM_LZ4_WIN=4) decodes the same bytes (fresh process: env read once)"""
     import subprocess
