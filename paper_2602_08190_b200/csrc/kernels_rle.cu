@@ -676,7 +676,14 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
 
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  rle_big_kernel<<<device_sms() * 2, kThreads, 0, s>>>(b);
+  // every resident CTA slot: a piece's windows are latency-bound (dependent run-table loads), so occupancy
+  // hides them (2 CTAs/SM measured 1.58 TB/s on E3 even-1024)
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rle_big_kernel, kThreads, 0);
+    if (occ < 1) occ = 1;
+  }
+  rle_big_kernel<<<device_sms() * occ, kThreads, 0, s>>>(b);
   return cudaGetLastError();
 }
 
