@@ -9,7 +9,8 @@
 //             token's byte position in the tile; each thread assembles its tokens' bytes into 32-bit words
 //             in registers (4 dictionary bytes per step) and stores them into a shared image at the tile's
 //             global alignment (the image and the output agree mod 16), which leaves as aligned 16-byte
-//             stores, the two partial edge words byte by byte; tiles of more than 32 KB store directly.
+//             stores, the two partial edge words byte by byte; tiles of more than kSdStage bytes store
+//             directly.  (Opt-in variants, measured slower: CDM_SD_SMEM=1, CDM_SD_EXPAND=2; see launch_strdict.)
 // The dictionary offsets were checked on the host (0, non-decreasing, ending at the token bytes), so a
 // token id < entries always names bytes inside the dictionary; an id >= entries sets CDM_ERR_DICT_INDEX and
 // expands to nothing; tokens that do not total the node's bytes set CDM_ERR_LENGTHS and a tile that would
@@ -37,16 +38,6 @@ __device__ __forceinline__ int find_desc_sd(const SdBatch& B, uint32_t tile) {
 }
 
 constexpr uint32_t kIdsWords = kSdTile * 32 / 32 + 4;  // packed ids of one tile (w <= 32) + extraction slack
-
-// sd_sums is written for a grid of G <= tiles CTAs: CTA c takes the contiguous tiles [c*T/G, (c+1)*T/G) and
-// (B.dict_smem) copies each descriptor's offsets into shared memory once.  It is launched with G = tiles and
-// the offsets read through L1, which measured faster (0.25 vs 0.30 ms, o_comment SF 10).
-struct TileRange {
-  uint32_t t0, t1;
-};
-__device__ __forceinline__ TileRange my_tiles(uint32_t total) {
-  return {uint32_t(uint64_t(total) * blockIdx.x / gridDim.x), uint32_t(uint64_t(total) * (blockIdx.x + 1) / gridDim.x)};
-}
 
 // dictionary stream (offsets + token bytes) of descriptor D -> shared memory (16-byte copies)
 __device__ __forceinline__ void load_dict(const SdDesc& D, uint32_t bytes, uint32_t* dict_s) {
@@ -79,31 +70,24 @@ __device__ __forceinline__ uint32_t load_tokens(const SdDesc& D, const uint32_t*
   return sum;
 }
 
+// one CTA per tile; the dictionary offsets are read through L1 (a shared copy per CTA or persistent CTAs
+// with one copy measured slower: 0.30 vs 0.25 ms, o_comment SF 10)
 __global__ void __launch_bounds__(kThreads) sd_sums_kernel(const __grid_constant__ SdBatch B) {
-  extern __shared__ __align__(16) uint32_t dict_s[];
   __shared__ uint32_t ids_s[kIdsWords];
   __shared__ uint64_t warp_s[kThreads / 32];
-  const TileRange tr = my_tiles(B.total_tiles);
-  int cur = -1;
-  for (uint32_t tile = tr.t0; tile < tr.t1; tile++) {
-    const int di = find_desc_sd(B, tile);
-    const SdDesc& D = B.d[di];
-    __syncthreads();  // the previous tile's ids / dictionary are dead
-    if (di != cur && B.dict_smem) load_dict(D, 4u * (D.entries + 1u), dict_s);  // offsets only
-    cur = di;
-    const uint32_t lt = tile - D.tile0, g0 = lt * kSdTile;
-    const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
-    stage_bits<kThreads>(ids_s, D.ids_packed, g0, nt, D.w);
-    __syncthreads();
-    uint32_t a[kSdPer], len[kSdPer];
-    bool bad = false;
-    const uint32_t* offs = B.dict_smem ? dict_s : reinterpret_cast<const uint32_t*>(D.dict);
-    const uint64_t s = load_tokens(D, offs, ids_s, nt, threadIdx.x * kSdPer, a, len, bad);
-    uint64_t tot;
-    block_excl_scan_u64<kThreads>(s, warp_s, &tot);
-    if (threadIdx.x == 0) D.tsum[lt] = tot;
-    if (bad) atomicOr(B.err + D.err_idx, 0x1u);
-  }
+  const SdDesc& D = B.d[find_desc_sd(B, blockIdx.x)];
+  const uint32_t lt = blockIdx.x - D.tile0, g0 = lt * kSdTile;
+  const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
+  stage_bits<kThreads>(ids_s, D.ids_packed, g0, nt, D.w);
+  __syncthreads();
+  uint32_t a[kSdPer], len[kSdPer];
+  bool bad = false;
+  const uint64_t s = load_tokens(D, reinterpret_cast<const uint32_t*>(D.dict), ids_s, nt, threadIdx.x * kSdPer, a,
+                                 len, bad);
+  uint64_t tot;
+  block_excl_scan_u64<kThreads>(s, warp_s, &tot);
+  if (threadIdx.x == 0) D.tsum[lt] = tot;
+  if (bad) atomicOr(B.err + D.err_idx, 0x1u);
 }
 
 // one CTA per descriptor: tsum <- exclusive prefix of tsum (the tile's output offset); thread t scans a
@@ -364,15 +348,14 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(sd_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
     cudaFuncSetAttribute(sd_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
     cudaFuncSetAttribute(sd_expand2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 32 + kSdDictSmem);
     configured = true;
   }
-  // default: every kernel reads the dictionary through L1 (random tokens cost one wavefront per distinct line:
-  // the expansion is L1-wavefront bound).  CDM_SD_SMEM=1: sd_expand copies the dictionary into shared memory
-  // per tile -- measured slower (2.4 vs 1.6 ms for o_comment SF 10: the copy is 3.6x the tile's output), and
-  // persistent CTAs that copy it once lose the latency hiding of 6 resident CTAs per SM (2.3 ms).
+  // default: every kernel reads the dictionary through L1 (random tokens cost one wavefront per distinct
+  // line).  CDM_SD_SMEM=1: sd_expand copies the dictionary into shared memory per tile -- measured slower
+  // (2.4 vs 1.6 ms for o_comment SF 10: the copy is 3.6x the tile's output); persistent CTAs that copy it
+  // once lost the latency hiding of 6 resident CTAs per SM (2.3 ms).
   static const bool smem = std::getenv("CDM_SD_SMEM") && std::getenv("CDM_SD_SMEM")[0] == '1';
   SdBatch l1 = b;
   l1.dict_smem = 0;
