@@ -555,6 +555,11 @@ struct cdm_batch {
 
 namespace {
 
+bool getenv_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && v[0] == '1';
+}
+
 // Build all launch descriptors for `jobs` over an arena laid out by `A` (pass 1: A.base == nullptr).
 // Returns the arena bytes; `zero_bytes` = prefix of the arena that must start zeroed.
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
@@ -1509,20 +1514,66 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
   std::vector<size_t> order, first_job;
   cdm_status st = plan_groups(e, jobs, n, e->opts.slot_bytes, &groups, &order, &first_job);
   if (st) return st;
-  // staging layout: group after group, chunks 256-aligned (one copy per chunk)
-  std::vector<size_t> stage_off;
+  // staging layout: group after group; inside a group the chunks in host-address order, exactly contiguous
+  // host neighbours (16-byte multiples) keep their relative offsets and share ONE H2D copy (pinned H2D runs
+  // at ~41 GB/s for 1 MB copies vs ~55 GB/s from 8 MB up); other chunks start 256-aligned
+  struct CopyRun { size_t off, bytes; const void* src; };
+  std::vector<std::vector<CopyRun>> runs(groups.size());
+  std::vector<std::vector<size_t>> stage_off(groups.size());
   size_t stage_bytes = 0;
-  for (auto& g : groups)
-    for (auto& b : g.bs) {
-      stage_off.push_back(stage_bytes);
-      stage_bytes += (b.total + 255) & ~size_t(255);
+  for (size_t g = 0; g < groups.size(); g++) {
+    auto& G = groups[g];
+    std::vector<size_t> by_addr(G.bs.size());
+    std::iota(by_addr.begin(), by_addr.end(), size_t(0));
+    std::sort(by_addr.begin(), by_addr.end(),
+              [&](size_t a, size_t b) { return G.js[a]->host_chunk < G.js[b]->host_chunk; });
+    stage_off[g].resize(G.bs.size());
+    for (size_t k = 0; k < by_addr.size(); k++) {
+      const size_t j = by_addr[k];
+      const uint8_t* h = static_cast<const uint8_t*>(G.js[j]->host_chunk);
+      CopyRun* last = runs[g].empty() ? nullptr : &runs[g].back();
+      if (last && static_cast<const uint8_t*>(last->src) + last->bytes == h && last->bytes % 16 == 0 &&
+          !getenv_flag("CDM_PIPE_NOMERGE")) {
+        stage_off[g][j] = last->off + last->bytes;  // == stage_bytes
+        last->bytes += G.bs[j].total;
+      } else {
+        stage_bytes = (stage_bytes + 255) & ~size_t(255);
+        stage_off[g][j] = stage_bytes;
+        runs[g].push_back({stage_bytes, size_t(G.bs[j].total), h});
+      }
+      stage_bytes = stage_off[g][j] + G.bs[j].total;
     }
+  }
   if (cudaMalloc(&P->staging, std::max<size_t>(stage_bytes, 256)) != cudaSuccess)
     return fail(CDM_E_OOM, "pipeline staging cudaMalloc failed");
+  for (size_t g = 0; g < groups.size(); g++)
+    for (size_t j = 0; j < groups[g].bs.size(); j++) groups[g].bs[j].dev_chunk = P->staging + stage_off[g][j];
   {
-    size_t q = 0;
-    for (auto& g : groups)
-      for (auto& b : g.bs) b.dev_chunk = P->staging + stage_off[q++];
+    // a copy may not span two host allocations that merely touch: try every merged run once, outside the
+    // capture; the driver rejects such a copy at the call (cudaErrorInvalidValue) -> split it per chunk
+    cudaStream_t probe = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&probe, cudaStreamNonBlocking));
+    for (size_t g = 0; g < groups.size(); g++) {
+      std::vector<CopyRun> fixed;
+      for (const CopyRun& r : runs[g]) {
+        bool whole = true;
+        if (r.bytes > 0) {
+          const cudaError_t ce = cudaMemcpyAsync(P->staging + r.off, r.src, r.bytes, cudaMemcpyHostToDevice, probe);
+          if (ce == cudaErrorInvalidValue) { cudaGetLastError(); whole = false; }
+          else if (ce != cudaSuccess) { cudaStreamDestroy(probe); return fail(CDM_E_CUDA, std::string("H2D probe: ") + cudaGetErrorString(ce)); }
+        }
+        if (whole) { fixed.push_back(r); continue; }
+        for (size_t j = 0; j < groups[g].bs.size(); j++) {  // the run's chunks, one copy each
+          const size_t o = stage_off[g][j];
+          if (o >= r.off && o < r.off + r.bytes)
+            fixed.push_back({o, size_t(groups[g].bs[j].total), groups[g].js[j]->host_chunk});
+        }
+      }
+      runs[g].swap(fixed);
+    }
+    const cudaError_t se = cudaStreamSynchronize(probe);
+    cudaStreamDestroy(probe);
+    if (se != cudaSuccess) return fail(CDM_E_CUDA, std::string("H2D probe: ") + cudaGetErrorString(se));
   }
   // one batch per group over its own arena slice; error words in one array (issue order)
   if (cudaMalloc(&P->err_dev, sizeof(uint32_t) * std::max<size_t>(1, n)) != cudaSuccess)
@@ -1613,11 +1664,10 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
   CAP_TRY(cudaEventRecord(start, origin));
   CAP_TRY(cudaStreamWaitEvent(copy, start, 0));
   for (size_t l = 0; l < lanes; l++) CAP_TRY(cudaStreamWaitEvent(ds[l], start, 0));
-  // copy branch: Johnson order, one copy per chunk
+  // copy branch: Johnson order of groups, one copy per run of host-contiguous chunks
   for (size_t g = 0; g < groups.size(); g++) {
-    for (size_t j = 0; j < groups[g].bs.size(); j++)
-      CAP_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(groups[g].bs[j].dev_chunk), groups[g].js[j]->host_chunk,
-                              groups[g].bs[j].total, cudaMemcpyHostToDevice, copy));
+    for (const CopyRun& r : runs[g])
+      CAP_TRY(cudaMemcpyAsync(P->staging + r.off, r.src, r.bytes, cudaMemcpyHostToDevice, copy));
     CAP_TRY(cudaEventRecord(copied[g], copy));
   }
   CAP_TRY(cudaEventRecord(copy_end, copy));
