@@ -321,9 +321,11 @@ __device__ __forceinline__ void stg_u32(void* p, uint32_t v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// LIN: the batch has arithmetic-run (V_LINEAR or strided) descriptors; their slope table lives in dynamic shared memory
+// LIN: the batch has arithmetic-run (V_LINEAR or strided) descriptors; their slope table lives in dynamic shared memory.
+// Occupancy: 4 CTAs/SM for LIN (64 registers; 5 measured slower: config 2 level 0 13 -> 15 us), 5 for the
+// rest (48 registers; config 2 2700 -> 2820 GB/s, level 1 23.1 -> 21.8 us; 6 / 40 registers measured slower)
 template <bool TR, bool LIN>
-__global__ void __launch_bounds__(kThreads, 4) rle_kernel(const __grid_constant__ RleBatch B) {
+__global__ void __launch_bounds__(kThreads, LIN ? 4 : 5) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ RleDesc D;
   __shared__ uint32_t cnt_s[K / 2 + 8];             // staged packed counts when w <= 16 (else read via L1)
   __shared__ __align__(16) uint64_t aux_s[K + 8];   // staged packed values (V_BP/DICT/F2I); then compact values
