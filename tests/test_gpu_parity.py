@@ -681,3 +681,46 @@ def test_checksum_matches_oracle(engine, name, spec):
     # a misaligned pointer is rejected, not read
     with pytest.raises(cdm.CdmError):
         cdm.checksum(out[1:9], 0)
+
+
+# ------------------------------------------------------------------------------ BASELINE full sizes
+@pytest.mark.parametrize("workload", ["config3", "config4"])
+def test_full_size_workload_sampled(engine, workload):
+    """BASELINE configs 3 / 4 at full size (SF 10) in bench.py's launch configuration -- every chunk of the
+    workload in ONE graph-mode device batch -- with no device error bit, and sampled chunks (first, last and
+    two random per column) equal to the oracle byte for byte."""
+    import random
+    sys_path = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import sys
+    if sys_path not in sys.path:
+        sys.path.insert(0, sys_path)
+    import bench
+    cols = bench.build_workload(0, workload)
+    decs, keep = [], []
+    for name, spec, dtype, width, chunks, _ in cols:
+        casc = cdm.Cascade(spec, dtype, width)
+        for i, ch in enumerate(chunks):
+            out, offs = cdm.output_buffers(ch)
+            decs.append(cdm.Decode(casc, ch, out, offs, dev_chunk=torch.from_numpy(ch).cuda()))
+            keep.append((name, i, len(chunks), ch, out, offs))
+    b = cdm.Batch(engine, decs)
+    b.set_graph(True)
+    b.launch()
+    res = b.results()
+    b.launch()  # the replay bench.py times
+    res = b.results()
+    assert all(r["error_bits"] == 0 for r in res)
+    rng = random.Random(7)
+    by_col = {}
+    for k in keep:
+        by_col.setdefault(k[0], []).append(k)
+    for name, ks in by_col.items():
+        pick = {0, len(ks) - 1} | {rng.randrange(len(ks)) for _ in range(2)}
+        for j in sorted(pick):
+            _, i, _, ch, out, offs = ks[j]
+            exp, exp_offs = oracle.decode_chunk(ch)
+            got = out[: exp.size].cpu().numpy()
+            assert np.array_equal(got, exp), f"{workload} {name} chunk {i}: payload differs"
+            if exp_offs is not None:
+                assert np.array_equal(offs[: exp_offs.size].cpu().numpy(), exp_offs), f"{name} chunk {i}: offsets"
+    b.close()
