@@ -137,6 +137,7 @@ struct RleBatch {
   uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
   uint32_t big_enabled;          // 0: rle_big is not launched -> oversize tiles are expanded in place
+  uint32_t short_runs;           // <= 16 rows per run on average: the 5-CTAs/SM variant (non-arithmetic)
   RleBig big;
   RleDesc d[kMaxBatch];
 };

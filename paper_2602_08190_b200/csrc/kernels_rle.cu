@@ -322,10 +322,12 @@ __device__ __forceinline__ void stg_u32(void* p, uint32_t v) {
 }
 
 // LIN: the batch has arithmetic-run (V_LINEAR or strided) descriptors; their slope table lives in dynamic shared memory.
-// Occupancy: 4 CTAs/SM for LIN (64 registers; 5 measured slower: config 2 level 0 13 -> 15 us), 5 for the
-// rest (48 registers; config 2 2700 -> 2820 GB/s, level 1 23.1 -> 21.8 us; 6 / 40 registers measured slower)
-template <bool TR, bool LIN>
-__global__ void __launch_bounds__(kThreads, LIN ? 4 : 5) rle_kernel(const __grid_constant__ RleBatch B) {
+// Occupancy OCC: 4 CTAs/SM (64 registers) for LIN (5 measured slower: config 2 level 0 13 -> 15 us) and for
+// long runs; 5 (48 registers) for short-run batches (<= 16 rows per run: config 2 level 1 23.1 -> 21.8 us,
+// 2700 -> 2820 GB/s; E3 even-1/even-4/random-1-8 +9-12 %; but even-32 / random-1-64 -6 %, hence the split;
+// 6 / 40 registers measured slower)
+template <bool TR, bool LIN, int OCC = 4>
+__global__ void __launch_bounds__(kThreads, OCC) rle_kernel(const __grid_constant__ RleBatch B) {
   __shared__ RleDesc D;
   __shared__ uint32_t cnt_s[K / 2 + 8];             // staged packed counts when w <= 16 (else read via L1)
   __shared__ __align__(16) uint64_t aux_s[K + 8];   // staged packed values (V_BP/DICT/F2I); then compact values
@@ -672,6 +674,8 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   }
   cudaError_t e;
   if (b.any_linear) e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, true>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, true>, b);
+  else if (b.short_runs)
+    e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, false, 5>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, false, 5>, b);
   else e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, false>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, false>, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

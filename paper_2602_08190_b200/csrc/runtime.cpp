@@ -736,6 +736,11 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         if (uint64_t(kRleTile) * L.max_run > kRleBigLimit) rb.big_enabled = 1;
       }
       rb.total_tiles = tiles;
+      {
+        uint64_t rows = 0, runs = 0;
+        for (int u : g) { rows += lvl(u).n; runs += lvl(u).nruns; }
+        rb.short_runs = runs && rows <= 16 * runs;
+      }
       rb.big.counter = A.take<unsigned long long>(1);
       rb.big.done = A.take<uint32_t>(1);
       rb.big.max_slots = slots;
