@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
 // chunk, lane l owns state l and decodes symbols 32s + l, so a warp emits 32 consecutive bytes per step and a
 // chunk's dependency chain is chunk/32 steps long.  The states that renormalise at a step take consecutive
 // words in lane order (ballot + popcount rank); the chunk's next 64 words sit in two registers per lane
-// (one word per lane each) and reach the renormalising lanes by shuffle, refilled 32 words at a time with a
-// coalesced load.  A CTA's 8 warps take B.cpw rounds of 8 chunks, so the slot table is built once per
+// (one word per lane each) and reach the renormalising lanes by shuffle, refilled 32 words at a time from a
+// third register whose coalesced load was issued one slide earlier.  A CTA's 8 warps take B.cpw rounds of 8 chunks, so the slot table is built once per
 // 8 * cpw chunks.
 __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constant__ AnsBatch B) {
   __shared__ uint32_t tab_s[1u << kAnsMaxTl];
@@ -138,12 +138,13 @@ __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constan
     const uint16_t* __restrict__ wp = D.words + w0;
     uint8_t* out = D.out + i0;
     auto ldw = [&](uint32_t q) -> uint32_t { return q < nw ? uint32_t(__ldg(wp + q)) : 0u; };
-    uint32_t wbase = 0, cur = 0, nxt = 0, pos = 0;
-    if (!bad) { cur = ldw(lane); nxt = ldw(32 + lane); }
-    const uint32_t steps = bad ? 0u : (len + 31) / 32;
-    for (uint32_t s = 0; s < steps; s++) {
-      const uint32_t i = 32 * s + lane;
-      const bool act = i < len;
+    // words [wbase, wbase + 64) are resident in (cur, nxt); pre holds [wbase + 64, wbase + 96), loaded one slide
+    // ahead so its latency overlaps the ~10 steps that consume a 32-word slice (the shuffles never read it)
+    uint32_t wbase = 0, cur = 0, nxt = 0, pre = 0, pos = 0;
+    if (!bad) { cur = ldw(lane); nxt = ldw(32 + lane); pre = ldw(64 + lane); }
+    // one decode step of the warp (32 symbols); words past nw read as 0 (ldw) and over-consumption shows in
+    // the final pos == nw check, so the step itself carries no bounds test
+    auto step = [&](uint32_t i0, bool act) {
       const uint32_t e = tab_s[x & mask];
       const uint32_t xn = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
       const bool need = act && xn < (1u << 16);  // one step suffices for tl <= 12
@@ -151,16 +152,20 @@ __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constan
       const uint32_t q = pos + __popc(m & lt_mask) - wbase;  // word index relative to the window (< 64)
       const uint32_t a = __shfl_sync(FULL, cur, q & 31), b = __shfl_sync(FULL, nxt, q & 31);
       const uint32_t w = q < 32 ? a : b;
-      bad |= need && pos + __popc(m & lt_mask) >= nw;
       x = need ? (xn << 16) | w : (act ? xn : x);
-      if (act) out[i] = uint8_t(e & 0xFFu);
+      if (act) out[i0 + lane] = uint8_t(e & 0xFFu);
       pos += __popc(m);
       if (pos >= wbase + 32) {  // warp-uniform: slide the window by 32 words
         wbase += 32;
         cur = nxt;
-        nxt = ldw(wbase + 32 + lane);
+        nxt = pre;
+        pre = ldw(wbase + 64 + lane);
       }
-    }
+    };
+    const uint32_t full = bad ? 0u : len / 32, tail = bad ? 0u : len % 32;
+#pragma unroll 2
+    for (uint32_t st = 0; st < full; st++) step(32 * st, true);
+    if (tail) step(32 * full, lane < tail);
     bad |= !__all_sync(FULL, x == (1u << 16)) || pos != nw;
     if (bad && lane == 0) atomicOr(B.err + D.err_idx, 0x20u);
   }
