@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constan
       }
     };
     const uint32_t full = bad ? 0u : len / 32, tail = bad ? 0u : len % 32;
-#pragma unroll 8  // measured: unroll 2 / 4 / 8 -> 554 / 613 / 628 GB/s (ans workload)
+#pragma unroll 8  // measured: unroll 2 / 4 / 8 / 16 -> 554 / 613 / 628-644 / 640-644 GB/s (ans workload)
     for (uint32_t st = 0; st < full; st++) step(32 * st, true);
     if (tail) step(32 * full, lane < tail);
     bad |= !__all_sync(FULL, x == (1u << 16)) || pos != nw;
