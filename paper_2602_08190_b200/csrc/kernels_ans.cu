@@ -9,7 +9,7 @@
 // decode order, and must end at state 2^16 with every word consumed (else CDM_ERR_ANS = 0x20).
 //
 // il = 1 (one state per chunk): a CTA takes 256 consecutive chunks of one column chunk; it first expands the shared table
-// into a shared-memory slot table (2^tl packed entries {symbol, f - 1, slot - cum}, tl <= 12), so the
+// into a shared-memory slot table (2^tl packed entries {symbol, slot - cum, f}, tl <= 12), so the
 // per-symbol step is one shared load + a multiply-add; every thread gathers 4 decoded bytes into a
 // register and writes them with one 4-byte store.
 #include "device_util.cuh"
@@ -31,10 +31,11 @@ __device__ __forceinline__ int find_desc_ans(const AnsBatch& B, uint32_t tile) {
   return lo;
 }
 
-// The CTA's slot table from the 256 frequencies: cum_s = exclusive scan, tab_s[slot] = packed {symbol, f - 1,
-// slot - cum}; returns whether the frequencies sum to M (else every chunk reports CDM_ERR_ANS).
-__device__ __forceinline__ bool build_slot_table(const uint8_t* table, uint32_t M, uint32_t* tab_s, uint32_t* cum_s,
+// The CTA's slot table from the 256 frequencies: cum_s = exclusive scan, tab_s[slot] = packed {symbol, slot - cum,
+// f}; returns whether the frequencies sum to M (else every chunk reports CDM_ERR_ANS).
+__device__ __forceinline__ bool build_slot_table(const uint8_t* table, uint32_t& tl, uint32_t* tab_s, uint32_t* cum_s,
                                                  uint64_t* warp_s) {
+  uint32_t M = 1u << tl;
   const uint32_t tid = threadIdx.x;
   {
     const uint32_t f = tid < 256 ? uint32_t(__ldg(reinterpret_cast<const uint16_t*>(table) + tid)) : 0u;
@@ -45,28 +46,32 @@ __device__ __forceinline__ bool build_slot_table(const uint8_t* table, uint32_t 
   }
   __syncthreads();
   const bool ok = cum_s[256] == M;
+  // f = 2^12 (one symbol owns the whole table) does not fit the 12-bit f field; such a step is the identity
+  // x' = M (x >> tl) + (x & (M - 1)) = x for every table log, so that table decodes with tl = 11 and f = 2^11
+  if (__syncthreads_or(M == 4096u && tid < 256 && cum_s[tid + 1] - cum_s[tid] == M)) { tl = 11; M = 2048; }
   for (uint32_t slot = tid; slot < M; slot += kThreads) {
     uint32_t lo = 0, hi = 255;
     while (lo < hi) {  // last symbol with cum <= slot
       const uint32_t mid = (lo + hi + 1) >> 1;
       if (cum_s[mid] <= slot) lo = mid; else hi = mid - 1;
     }
-    const uint32_t f = cum_s[lo + 1] - cum_s[lo];
-    tab_s[slot] = lo | ((f - 1u) & 0xFFFu) << 8 | (slot - cum_s[lo]) << 20;
+    const uint32_t f = min(cum_s[lo + 1] - cum_s[lo], M);
+    tab_s[slot] = lo | (slot - cum_s[lo]) << 8 | f << 20;
   }
   __syncthreads();
   return ok;
 }
 
 __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ AnsBatch B) {
-  __shared__ uint32_t tab_s[1u << kAnsMaxTl];  // slot -> sym | (f - 1) << 8 | (slot - cum) << 20
+  __shared__ uint32_t tab_s[1u << kAnsMaxTl];  // slot -> sym | (slot - cum) << 8 | f << 20
   __shared__ uint32_t cum_s[257];
   __shared__ uint64_t warp_s[kThreads / 32];
   const uint32_t tid = threadIdx.x;
   const AnsDesc& D = B.d[find_desc_ans(B, blockIdx.x)];
-  const uint32_t tl = D.tl, M = 1u << tl;
+  uint32_t tl = D.tl;
   const uint8_t* const table = D.table;
-  const bool table_ok = build_slot_table(table, M, tab_s, cum_s, warp_s);
+  const bool table_ok = build_slot_table(table, tl, tab_s, cum_s, warp_s);
+  const uint32_t M = 1u << tl;
   const uint32_t c = (blockIdx.x - D.tile0) * kThreads + tid;  // this thread's chunk
   if (c >= D.nchunks) return;
   bool bad = !table_ok;
@@ -85,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) ans_kernel(const __grid_constant__ A
   uint32_t wnext = nw ? uint32_t(__ldg(wp)) : 0u;
   auto step = [&](uint32_t& x) -> uint32_t {
     const uint32_t e = tab_s[x & mask];
-    x = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+    x = (e >> 20) * (x >> tl) + ((e >> 8) & 0xFFFu);
     if (x < (1u << 16)) {  // one step suffices: x >= 2^(16 - tl) here, tl <= 12
       bad |= pos >= nw;
       x = (x << 16) | wnext;
@@ -122,9 +127,10 @@ __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constan
   __shared__ uint64_t warp_s[kThreads / 32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const AnsDesc& D = B.d[find_desc_ans(B, blockIdx.x)];
-  const uint32_t tl = D.tl, M = 1u << tl;
+  uint32_t tl = D.tl;
   const uint8_t* const table = D.table;
-  const bool table_ok = build_slot_table(table, M, tab_s, cum_s, warp_s);
+  const bool table_ok = build_slot_table(table, tl, tab_s, cum_s, warp_s);
+  const uint32_t M = 1u << tl;
   const uint32_t mask = M - 1u, lt_mask = (1u << lane) - 1u;
   for (uint32_t rnd = 0; rnd < B.cpw; rnd++) {
     const uint32_t c = ((blockIdx.x - D.tile0) * B.cpw + rnd) * (kThreads / 32) + warp;  // this warp's chunk
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) ans_warp_kernel(const __grid_constan
     // the final pos == nw check, so the step itself carries no bounds test
     auto step = [&](uint32_t i0, bool act) {
       const uint32_t e = tab_s[x & mask];
-      const uint32_t xn = (((e >> 8) & 0xFFFu) + 1u) * (x >> tl) + (e >> 20);
+      const uint32_t xn = (e >> 20) * (x >> tl) + ((e >> 8) & 0xFFFu);
       const bool need = act && xn < (1u << 16);  // one step suffices for tl <= 12
       const uint32_t m = __ballot_sync(FULL, need);
       const uint32_t q = pos + __popc(m & lt_mask) - wbase;  // word index relative to the window (< 64)

@@ -475,6 +475,20 @@ def test_corrupt_run_sum_sets_error(engine):
         assert r["error_bits"] & cdm.ERR_RUN_SUM
 
 
+
+# A single symbol owns the whole ANS table (f = 2^tl): each decode step is the identity, no renormalisation
+# word is read, and at tl = 12 the kernels decode it with tl = 11 (f = 2^12 does not fit their 12-bit f field).
+# Also a near-degenerate two-symbol mix (f = 2^tl - 1 and 1) that exercises the widest f the field holds.
+@pytest.mark.parametrize("spec", ["ANS", "ANS(il=1,chunk=4096)", "ANS(tl=10)", "ANS(il=1,tl=10,chunk=1024)"])
+def test_ans_degenerate_tables(engine, spec):
+    n = 100_003
+    one = np.full((n, 1), 82, dtype=np.uint8)
+    check_parity(engine, spec, Column("one", cdm1.FIXED, 1, n, one), rows_per_chunk=50_001)
+    two = one.copy()
+    two[np.random.default_rng(7).integers(0, n, 40), 0] = 65
+    check_parity(engine, spec, Column("two", cdm1.FIXED, 1, n, two), rows_per_chunk=50_001)
+
+
 @pytest.mark.parametrize("il", [1, 32])
 def test_corrupt_ans_sets_error(engine, il):
     import test_ans_cpu as A
