@@ -461,7 +461,7 @@ def main():
             else:
                 fam_bytes["copy"] += info["compressed_bytes"] + info["payload_bytes"]
         kbytes = {"fp_kernel": fam_bytes["fp"], "scan_kernel": fam_bytes["scan"], "rle_kernel": fam_bytes["rle"],
-                  "lz4_kernel": fam_bytes.get("lz4x", 0), "ans_kernel": fam_bytes.get("ans", 0),
+                  "lz4_kernel": fam_bytes.get("lz4x", 0), "ans_warp_kernel": fam_bytes.get("ans", 0),
                   "strdict_kernel": fam_bytes.get("sd", 0),
                   "device_copy": fam_bytes["copy"]}
         dom = max(ktimes, key=lambda k: ktimes[k][0])

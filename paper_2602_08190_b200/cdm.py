@@ -19,7 +19,7 @@ STATUS = {0: "CDM_OK", 1: "CDM_E_INVALID_ARG", 2: "CDM_E_PARSE", 3: "CDM_E_UNSUP
 ERR_DICT_INDEX, ERR_RUN_SUM, ERR_LZ4, ERR_LENGTHS, ERR_WIDTH = 0x1, 0x2, 0x4, 0x8, 0x10
 FAMILIES = ["fp", "scan", "rle", "lz4", "copy"]
 KERNELS = ["fp_kernel", "scan_kernel", "rle_sums_kernel", "rle_kernel(level0)", "rle_kernel", "rle_big_kernel",
-           "lz4_kernel", "device_copy", "ans_kernel", "strdict_kernel"]
+           "lz4_kernel", "device_copy", "ans_warp_kernel", "strdict_kernel"]  # ANS slot: ans_warp_kernel (il = 32) or ans_kernel (il = 1)
 
 SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_create", "cdm_cascade_destroy",
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
