@@ -4,7 +4,7 @@ Everything is compiled IN-TREE (the .so files travel to the GPU box with the gpu
   paper_2602_08190_b200/_lib/libcdm.so       CUDA decode runtime + kernels, C-ABI in include/cdm.h
   paper_2602_08190_b200/_lib/libcdm_gen.so   seeded TPC-H-shaped input generator (inputs/)
   paper_2602_08190_b200/_lib/libcdm_enc.so   CPU cascade encoder (encoder/), links liblz4
-The CPU oracle (oracle/) is built by oracle/_build.py, never from here.
+The CPU oracle (oracle/, test infrastructure) is built by oracle.build() (oracle/oracle.py), never from here.
 """
 from __future__ import annotations
 

@@ -259,6 +259,14 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s);
 cudaError_t launch_zero(void* p, size_t bytes, cudaStream_t s);
 cudaError_t launch_harvest(uint32_t* err, uint32_t* host_mapped, uint32_t n, cudaStream_t s);
 int device_sms();
+// per-device launch state (function attributes, occupancy) is cached per device ordinal: an engine on a
+// second device of the process configures its own context
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d >= 0 && d < kMaxDevices ? d : 0;
+}
 // H9 positional checksum of a device buffer, ADDED into *dev_out (zero it first)
 cudaError_t launch_checksum(const void* p, uint64_t bytes, uint64_t chunk_id, uint64_t* dev_out, cudaStream_t s);
 

@@ -330,14 +330,14 @@ void tune_set(int knob, int value) {
 }
 
 int device_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static int sms[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
   }
-  return sms;
+  return sms[dev];
 }
 
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
@@ -347,11 +347,12 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   static const int dm = std::getenv("CDM_FP_DICT") && std::getenv("CDM_FP_DICT")[0] == 'l' ? 0 : 1;
   static const bool tma = !(std::getenv("CDM_FP_TMA") && std::getenv("CDM_FP_TMA")[0] == '0');
   auto kern = tma ? (dm ? fp_kernel<1, true> : fp_kernel<0, true>) : (dm ? fp_kernel<1, false> : fp_kernel<0, false>);
-  static uint32_t configured[4] = {0, 0, 0, 0};
+  static uint32_t configured[kMaxDevices][4] = {};
   const int ci = dm + 2 * tma;
-  if (tma && smem > 40 * 1024 && smem > configured[ci]) {
+  uint32_t& conf = configured[current_device()][ci];
+  if (tma && smem > 40 * 1024 && smem > conf) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured[ci] = smem;
+    conf = smem;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);

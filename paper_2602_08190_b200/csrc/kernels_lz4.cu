@@ -432,10 +432,11 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
     uint32_t wpc = 8;
     while (wpc > 1 && 3ull * wpc * (cap + 16) > 220 * 1024) wpc >>= 1;
     const uint32_t smem = wpc * (cap + 16);
-    static uint32_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    static uint32_t configured[kMaxDevices] = {};
+    uint32_t& conf = configured[current_device()];
+    if (smem > 48 * 1024 && smem > conf) {
       cudaFuncSetAttribute(lz4_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      configured = smem;
+      conf = smem;
     }
     const uint32_t grid = (b.total_subs + wpc - 1) / wpc;
     lz4_smem_kernel<<<grid, wpc * 32, smem, s>>>(b, cap);

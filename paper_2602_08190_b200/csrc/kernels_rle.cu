@@ -666,11 +666,12 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static bool configured = false;
-  if (!configured) {  // the slope table takes the linear variants past the 48 KB default
+  static bool configured[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {  // the slope table takes the linear variants past the 48 KB default
     cudaFuncSetAttribute(rle_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * sizeof(uint64_t));
     cudaFuncSetAttribute(rle_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * sizeof(uint64_t));
-    configured = true;
+    configured[dev] = true;
   }
   cudaError_t e;
   if (b.any_linear) e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, true>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, true>, b);
@@ -684,12 +685,13 @@ cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
   // every resident CTA slot: a piece's windows are latency-bound (dependent run-table loads), so occupancy
   // hides them (2 CTAs/SM measured 1.58 TB/s on E3 even-1024)
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rle_big_kernel, kThreads, 0);
-    if (occ < 1) occ = 1;
+  static int occ[kMaxDevices] = {};
+  int& o = occ[current_device()];
+  if (!o) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, rle_big_kernel, kThreads, 0);
+    if (o < 1) o = 1;
   }
-  rle_big_kernel<<<device_sms() * occ, kThreads, 0, s>>>(b);
+  rle_big_kernel<<<device_sms() * o, kThreads, 0, s>>>(b);
   return cudaGetLastError();
 }
 

@@ -346,11 +346,12 @@ __global__ void __launch_bounds__(kSdT2) sd_expand2_kernel(const __grid_constant
 
 cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {
     cudaFuncSetAttribute(sd_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdDictSmem);
     cudaFuncSetAttribute(sd_expand2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 32 + kSdDictSmem);
-    configured = true;
+    configured[dev] = true;
   }
   // default: every kernel reads the dictionary through L1 (random tokens cost one wavefront per distinct
   // line).  CDM_SD_SMEM=1: sd_expand copies the dictionary into shared memory per tile -- measured slower

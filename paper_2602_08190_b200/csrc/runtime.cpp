@@ -1233,7 +1233,9 @@ static cdm_status group_copy(cdm_engine* e, PendingGroup& pg) {
     size_t m = k + 1;
     while (m < by_addr.size()) {
       const size_t j = by_addr[m];
-      if (static_cast<const uint8_t*>(js[j]->host_chunk) != h0 + end || bs[j].total % 16 ||
+      // the appended chunk lands at pos + end: only a run whose running length is a 16-byte multiple keeps
+      // it 16-byte aligned (TMA bulk copies and vector loads read its streams in place)
+      if (static_cast<const uint8_t*>(js[j]->host_chunk) != h0 + end || end % 16 ||
           pos + end + bs[j].total > e->opts.slot_bytes)
         break;
       bs[j].dev_chunk = s.dev + pos + end;

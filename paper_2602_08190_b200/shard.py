@@ -10,14 +10,18 @@ def shard_ranges(sizes: list[int], world: int) -> list[tuple[int, int]]:
     """Split one column's chunk list (compressed sizes, in row order) into `world` contiguous ranges
     [a, b) with near-equal byte totals.  Ranks may get an empty range when chunks < world."""
     n = len(sizes)
+    if n <= world:  # one chunk per rank, the rest empty
+        return [(min(r, n), min(r + 1, n)) for r in range(world)]
     total = sum(sizes)
     bounds = [0]
     acc = 0
     k = 1
     for i, s in enumerate(sizes):
         acc += s
-        # close range k-1 once it holds at least its share, leaving a chunk for each later rank if possible
-        while k < world and acc >= total * k / world and (n - (i + 1)) >= 0:
+        rest = n - (i + 1)  # chunks after this one
+        # close range k-1 (never empty) once it holds its share of the bytes, as long as every later rank
+        # still gets a chunk; close it anyway when exactly one chunk per later rank remains
+        if k < world and bounds[-1] < i + 1 and rest >= world - k and (acc >= total * k / world or rest == world - k):
             bounds.append(i + 1)
             k += 1
     while len(bounds) < world:

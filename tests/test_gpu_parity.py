@@ -738,3 +738,37 @@ def test_full_size_workload_sampled(engine, workload):
             if exp_offs is not None:
                 assert np.array_equal(offs[: exp_offs.size].cpu().numpy(), exp_offs), f"{name} chunk {i}: offsets"
     b.close()
+
+
+@pytest.mark.parametrize("mode", ["submit", "pipeline"])
+def test_contiguous_chunks_after_unaligned_total(engine, mode):
+    """two host-contiguous chunks whose first total_bytes is NOT a multiple of 16 (a valid
+    container: the header's total covers 8 trailing bytes) must not share one H2D copy -- the second chunk
+    would land 8 bytes off a 16-byte boundary in the staging slot, where TMA and vector loads read it."""
+    g = TPCH(0.002)
+    spec = "Str|[LZ4,BitPack]"
+    col = g.column("l_comment")
+    a, b = encoder.encode_chunks(spec, col, 4000)[:2]
+    a2 = np.concatenate([a, np.zeros(8, np.uint8)])
+    struct.pack_into("<Q", a2, 40, a2.size)              # header total_bytes = 16k + 8
+    host = cdm.pinned(np.concatenate([a2, b]))
+    casc = cdm.Cascade(spec, col.dtype, col.width)
+    parts = [host[: a2.size], host[a2.size:]]
+    decs, bufs = [], []
+    for ch in parts:
+        out, offs, info = _outputs(ch.numpy())
+        decs.append(cdm.Decode(casc, ch, out, offs))
+        bufs.append((out, offs, info))
+    if mode == "submit":
+        res = [engine.wait(t) for t in engine.submit_batch(decs)]
+    else:
+        p = cdm.Pipeline(engine, decs)
+        p.launch()
+        res = p.results()
+        p.close()
+    torch.cuda.synchronize()
+    for ch, (out, offs, info), r in zip((a2, b), bufs, res):
+        assert r["error_bits"] == 0
+        exp, exp_offs = oracle.decode_chunk(ch)
+        assert np.array_equal(out[: exp.size].cpu().numpy(), exp)
+        assert np.array_equal(offs[: exp_offs.size].cpu().numpy(), exp_offs)

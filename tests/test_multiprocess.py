@@ -23,6 +23,17 @@ def test_shard_ranges_cover_and_balance():
             assert max(per) - min(per) <= 1
 
 
+def test_shard_ranges_every_rank_gets_a_chunk():
+    # a large leading chunk must not close several ranges at once: with chunks >= ranks, no rank
+    # is left empty; with fewer chunks than ranks, each chunk goes to its own rank
+    for sizes, world in [([100, 1, 1, 1], 4), ([1, 1, 1, 100], 2), ([1000, 1, 1, 1, 1, 1], 3), ([9, 9], 4)]:
+        rs = shard_ranges(sizes, world)
+        per = [b - a for a, b in rs]
+        assert sum(per) == len(sizes)
+        assert all(p >= 1 for p in per[:min(world, len(sizes))]), (sizes, world, rs)
+    assert shard_ranges([100, 1, 1, 1], 4) == [(0, 1), (1, 2), (2, 3), (3, 4)]
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
