@@ -1,29 +1,38 @@
 #!/usr/bin/env python
-"""bench.py -- effective decoded GB/s of the cascaded-columnar decode hot path on B200.
+"""bench.py -- effective decoded GB/s (host-compressed -> device-decoded) of the cascaded-columnar decode hot
+path on B200.
 
-Workload (BASELINE.json configs[1], "config 2"): TPC-H SF=1 lineitem numeric columns, synthetic
-dbgen-like data (paper_2602_08190_b200.inputs), row groups of 2^22 rows:
-    l_orderkey   RLE|[Delta|RLE|[BitPack,BitPack],BitPack]   int64   (H7 + inner pre-pass)
-    l_quantity   Dict|BitPack                                 float64 (H5)
-    l_discount   Dict|BitPack                                 float64 (H5)
-One step = decode every chunk of the three columns (all hot-path rows this workload touches).
+Default workload = the north-star configuration (BASELINE.json configs[3], "config 4"): every TPC-H lineitem
+and orders column (25) at SF=100 ("all experiments use a TPC-H scale factor of 100"), synthetic
+dbgen-like data, row groups of 2^22 rows, each column under the SURVEY Sec. 8d cascade map (Table 2 mapped onto
+the hot-path codecs: FP, Delta/VARCHAR scans, RLE / DeltaStride chains, LZ4, ANS, String-dictionary).  The
+compressed chunks (~21.5 GB) are generated and encoded in parallel worker processes into ONE host buffer that
+is page-locked in place (cdm_host_register) -- the paper's column store in pinned CPU memory.
 
-  value  device-resident: compressed chunks already in HBM, decoded bytes / device time (CUDA events on
-         the launching stream around cdm_batch_launch; L2 flushed by a 256 MiB write between steps,
-         outside the events).
-  e2e    through the public C-ABI from PINNED HOST memory: cdm_pipeline_launch (the H4 schedule -- H2D
-         copies in Johnson order overlapped with the fused decodes of earlier groups -- captured once as a
-         CUDA graph) + cdm_pipeline_results (each chunk's error word read on the host).  The same schedule
-         enqueued group by group by the host (cdm_submit_batch + cdm_wait) is reported under
-         e2e.submit_batch.
-  roofline  the dominant kernel family (by device time) against the measured HBM copy peak.
-  cpu_baseline  the CPU oracle (oracle/, plain C, chunk-parallel) on the same chunks.
+One step = every chunk of the workload crosses PCIe and is decoded into its device output buffer.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling -- every rank decodes its own independent
-SF=1 shard (seed offset by rank); the only collective is the final NCCL all-reduce of
-(rows, decoded bytes, compressed bytes, error bits) plus a MAX of the device time.
+  value      host-compressed -> device-decoded GB/s: decoded bytes / device time of one cdm_pipeline_launch
+             (the H4 schedule: Johnson order, H2D copies from pinned host overlapped with the fused decodes of
+             earlier groups, captured once as a CUDA graph), CUDA events on the launching stream; K steps.
+  e2e        the same through the public API with the host in the loop: wall clock of cdm_pipeline_launch +
+             cdm_pipeline_results (every chunk's error word read back on the host) per step.
+  device_resident  decode only, compressed chunks already in HBM (cdm_batch graph replay), L2 flushed
+             between steps -- the kernel-level number.
+  serialized the non-pipelined schedule (E11): one H2D copy of all compressed bytes, then
+             the decode -- what pipelining saves.
+  roofline   the dominant kernel (alone) against the measured HBM peak; roofline.families = every kernel
+             family's algorithmic bytes (Eq. 1, from cdm_batch_kernel_bytes) / its time alone.
+  parity     H9 checksums of every chunk's device output; the oracle's checksums of the cpu_baseline sample.
+  cpu_baseline  the CPU oracle (oracle/, plain C) on a bounded sample (the first chunk of every column), on 1
+             thread and on every host core.
 
---impl reference: the reference arm of this tier is the CPU oracle, timed as it stands on the host cores.
+Multi-GPU (torchrun, one process per GPU, NCCL): strong scaling -- ONE dataset, each column's chunks split
+into contiguous per-rank ranges balanced by row count (= compressed bytes for equal-size chunks; shard.py);
+each rank builds, pins and decodes only its shard, CPU-bound to its GPU's affinity; the only collectives are
+all-reduces of metadata, checksums and times.  checksum_total is the same for every N.
+
+--impl reference: this tier's reference arm is the CPU oracle, timed as it stands on the host cores over the
+bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -31,7 +40,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -42,87 +50,101 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "effective decoded GB/s (host-compressed→device-decoded) at 1/2/4/8 B200 vs roofline"
+CONFIG4_COLS = [
+    ("l_orderkey", "RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]"), ("l_partkey", "BitPack"),
+    ("l_suppkey", "BitPack"), ("l_linenumber", "BitPack"), ("l_quantity", "Dict|BitPack"),
+    ("l_extendedprice", "Float2Int|BitPack"), ("l_discount", "Dict|BitPack"), ("l_tax", "Dict|BitPack"),
+    ("l_returnflag", "ANS"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
+    ("l_commitdate", "Dict|BitPack"), ("l_receiptdate", "Dict|BitPack"), ("l_shipinstruct", "Dict|BitPack"),
+    ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384),BitPack]"),
+    ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("o_custkey", "BitPack"),
+    ("o_orderstatus", "Dict|BitPack"), ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"),
+    ("o_orderpriority", "Dict|BitPack"), ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
+    ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]")]
 WORKLOADS = {
-    # BASELINE configs[1] (the default / headline): TPC-H SF=1 lineitem numeric columns
+    # BASELINE configs[3] (the default / headline): all 25 lineitem + orders columns, SF=100 (north star)
+    "config4": dict(sf=100.0, dtype="mixed", cols=CONFIG4_COLS,
+                    desc="config 4: TPC-H lineitem + orders, all 25 columns at SF={sf} (SURVEY Sec. 8d cascade "
+                         "map: l_returnflag ANS, l_/o_orderkey DeltaStride, o_comment String-dictionary|BitPack|ANS "
+                         "per Table 2), streamed from pinned host"),
+    # BASELINE configs[1]: TPC-H SF=1 lineitem numeric columns
     "config2": dict(sf=1.0, dtype="int64", cols=[("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"),
-                                                  ("l_quantity", "Dict|BitPack"),
-                                                  ("l_discount", "Dict|BitPack")],
-                    desc="config 2: TPC-H SF=1 lineitem numeric columns (l_orderkey RLE|[Delta|RLE|[BitPack,BitPack],"
-                         "BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack)"),
+                                                  ("l_quantity", "Dict|BitPack"), ("l_discount", "Dict|BitPack")],
+                    desc="config 2: TPC-H SF={sf} lineitem numeric columns (l_orderkey RLE|[Delta|RLE|[BitPack,"
+                         "BitPack],BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack)"),
     # BASELINE configs[2]: TPC-H SF=10 lineitem string columns (dictionary CHAR(n) + chunk-parallel LZ4)
     "config3": dict(sf=10.0, dtype="u8", cols=[("l_shipmode", "Dict|BitPack"), ("l_returnflag", "Dict|BitPack"),
                                                 ("l_comment", "Str|[LZ4(sub=16384),BitPack]")],
-                    desc="config 3: TPC-H SF=10 lineitem string columns (l_shipmode/l_returnflag Dict|BitPack CHAR(n), "
-                         "l_comment Str|[LZ4(16 KiB sub-chunks),BitPack])"),
-    # BASELINE configs[3]: every lineitem + orders column with the SURVEY Sec. 8d config-4 cascade map (Table 2
-    # mapped onto the hot-path codecs), at --sf (default 10; the paper's SF=100 needs ~24 GB of pinned host)
-    "config4": dict(sf=10.0, dtype="mixed", cols=[
-        ("l_orderkey", "RLE|[DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack],BitPack]"), ("l_partkey", "BitPack"),
-        ("l_suppkey", "BitPack"), ("l_linenumber", "BitPack"), ("l_quantity", "Dict|BitPack"),
-        ("l_extendedprice", "Float2Int|BitPack"), ("l_discount", "Dict|BitPack"), ("l_tax", "Dict|BitPack"),
-        ("l_returnflag", "ANS"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
-        ("l_commitdate", "Dict|BitPack"), ("l_receiptdate", "Dict|BitPack"), ("l_shipinstruct", "Dict|BitPack"),
-        ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384),BitPack]"),
-        ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("o_custkey", "BitPack"), ("o_orderstatus", "Dict|BitPack"),
-        ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"), ("o_orderpriority", "Dict|BitPack"),
-        ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
-        ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]")],
-                    desc="config 4: TPC-H lineitem + orders, all 25 columns (SURVEY Sec. 8d cascade map, "
-                         "l_returnflag ANS, l_/o_orderkey DeltaStride, o_comment String-dictionary|BitPack|ANS per Table 2: FP / RLE / LZ4 / ANS kernels concurrently)"),
-    # NEXT-1 microbenchmark: the paper's ANS instance -- an L_RETURNFLAG-distributed byte
-    # column under chunk-sequential range ANS (4 KiB chunks, one thread per chunk)
+                    desc="config 3: TPC-H SF={sf} lineitem string columns (l_shipmode/l_returnflag Dict|BitPack "
+                         "CHAR(n), l_comment Str|[LZ4(16 KiB sub-chunks),BitPack])"),
+    # NEXT-1 microbenchmark: the paper's ANS instance
     "ans": dict(sf=10.0, dtype="u8", cols=[("l_returnflag", "ANS(chunk=4096)"), ("l_linestatus", "ANS(chunk=4096)")],
-                desc="ANS: TPC-H lineitem l_returnflag + l_linestatus CHAR(1) under range ANS (4 KiB chunks)"),
-    # NEXT-2 microbenchmark: Table 2's O_COMMENT cascade (String-dictionary | Bit-packing | ANS)
+                desc="ANS: TPC-H SF={sf} lineitem l_returnflag + l_linestatus CHAR(1) under range ANS (4 KiB chunks)"),
+    # NEXT-2 microbenchmark: Table 2's O_COMMENT cascade
     "strdict": dict(sf=10.0, dtype="u8", cols=[("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]")],
-                    desc="String-dictionary: TPC-H orders o_comment under Str|[StrDict|BitPack|ANS,BitPack] (Table 2)"),
+                    desc="String-dictionary: TPC-H SF={sf} orders o_comment under Str|[StrDict|BitPack|ANS,BitPack]"),
     # BASELINE configs[0]: the oracle-sized parity case (launch-bound: 4 MB decoded)
-    "config1": dict(sf=None, dtype="int32", cols=[("config1", "BitPack")],
+    "config1": dict(sf=1.0, dtype="int32", cols=[("config1", "BitPack")],
                     desc="config 1: 1M int32, FOR + 8-bit bit-packing, one chunk"),
 }
 CHUNK_ROWS = 1 << 22
-FAMILY_NAMES = ["fp", "scan", "rle", "lz4", "copy"]
-FAMILY_KERNELS = {"fp": "fp_kernel", "scan": "scan_kernel", "rle": "rle_sums_kernel+rle_kernel(+rle_big_kernel)",
-                  "lz4": "lz4_kernel", "copy": "cudaMemcpyAsync D2D"}
+# kernel kinds of cdm_batch_kernel_times / _bytes grouped into families (the RLE chain's bytes sit on rle_kernel)
+FAMILY_OF = {"fp_kernel": "fp_numeric", "fp_kernel(char)": "fp_char", "scan_kernel": "scan",
+             "rle_sums_kernel": "rle_chain", "rle_kernel(level0)": "rle_chain", "rle_kernel": "rle_chain",
+             "rle_big_kernel": "rle_chain", "lz4_kernel": "lz4", "ans_kernel": "ans", "strdict_kernel": "strdict",
+             "device_copy": "copy"}
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="cdm", choices=["cdm", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=2.0, help="wall seconds of the oracle sample")
-    p.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
-    p.add_argument("--sf", type=float, default=None, help="scale factor override (config 2/3/4)")
+    p.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
+    p.add_argument("--sf", type=float, default=None, help="scale factor override")
+    p.add_argument("--workers", type=int, default=None, help="generator/encoder processes per rank")
     a = p.parse_args()
     if a.sf is not None:
         WORKLOADS[a.workload]["sf"] = a.sf
     return a
 
 
-def _encode_column(job):
-    """(sf, seed, rank, name, spec) -> (name, spec, dtype, width, chunks, plain bytes); runs in a worker."""
-    sf, seed, rank, name, spec = job
-    from paper_2602_08190_b200 import encoder
-    from paper_2602_08190_b200.inputs import TPCH, config1_column
-    col = config1_column() if name == "config1" else TPCH(sf, seed).column(name)
-    chunks = encoder.encode_chunks(spec, col, CHUNK_ROWS, first_chunk_id=1000 * rank)
-    return (name, spec, col.dtype, col.width, chunks, col.nbytes())
+def desc_of(wl) -> str:
+    return wl["desc"].format(sf=f"{wl['sf']:g}")
 
 
-def build_workload(rank: int, workload: str = "config2"):
-    """Generate + encode this rank's shard (untimed), one column per worker process for multi-column
-    workloads.  Returns list of (name, spec, dtype, width, chunks, plain bytes)."""
-    from paper_2602_08190_b200.inputs import MASTER_SEED
-    wl = WORKLOADS[workload]
-    jobs = [(wl["sf"], MASTER_SEED + 1000 * rank, rank, name, spec) for name, spec in wl["cols"]]
-    if len(jobs) > 3:
-        import multiprocessing as mp
-        with mp.get_context("fork").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
-            return pool.map(_encode_column, jobs)
-    return [_encode_column(j) for j in jobs]
+def shard_select(cols, sf, rank, world):
+    """{column index: this rank's chunk indices}: contiguous ranges balanced by row count (shard.py)."""
+    from paper_2602_08190_b200 import workload
+    from paper_2602_08190_b200.inputs import MASTER_SEED, TPCH
+    from paper_2602_08190_b200.shard import shard_ranges
+    gen = TPCH(sf, MASTER_SEED)
+    sel = {}
+    for k, (name, _) in enumerate(cols):
+        n = workload._row_count(gen, name)
+        nch = max(1, -(-n // CHUNK_ROWS))
+        rows = [min(CHUNK_ROWS, n - c * CHUNK_ROWS) for c in range(nch)]
+        a, b = shard_ranges(rows, world)[rank]
+        sel[k] = list(range(a, b))
+    return sel
+
+
+def bind_cpus(local: int) -> list[int]:
+    """Bind this process (and the workers it forks) to the CPUs NVML reports as close to the GPU."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = [64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1]
+        cpus = [c for c in cpus if c < (os.cpu_count() or 1)]
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return sorted(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001 -- no NVML (CPU box): leave the affinity alone
+        return sorted(os.sched_getaffinity(0))
 
 
 def load_peaks():
@@ -132,6 +154,17 @@ def load_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -195,45 +228,54 @@ def measure_h2d(torch, nbytes=256 << 20, reps=5):
             b.record()
         b.synchronize()
         best = min(best, a.elapsed_time(b))
+    del h, d
     return nbytes / best / 1e6
 
 
-def _decoded_bytes(chunk) -> int:
-    """payload + offsets bytes from a chunk header (the oracle writes both)."""
+def chunk_checksum_oracle(payload, offs, chunk_id: int) -> int:
+    """H9 checksum of a decoded chunk (payload words under chunk_id, offsets words under chunk_id ^ 2^63)."""
     import oracle
-    dtype, _, rows, payload = oracle.oracle._header(chunk)
-    return int(payload) + (4 * (int(rows) + 1) if dtype == 4 else 0)
+    cs = oracle.checksum(payload, chunk_id)
+    if offs is not None:
+        cs = (cs + oracle.checksum(offs, chunk_id ^ (1 << 63))) % (1 << 64)
+    return cs
 
 
-def cpu_baseline(cols, seconds: float):
-    """The oracle as it stands: plain C decode of the same chunks, chunk-parallel on the host cores."""
+def oracle_sample(samples, threads_list):
+    """The oracle as it stands on the sample chunks: (decoded bytes, {threads: seconds}, per-chunk checksums)."""
     import oracle
-    chunks = [c for (_, _, _, _, chs, _) in cols for c in chs]
-    decoded = sum(_decoded_bytes(c) for c in chunks)
-    threads = min(os.cpu_count() or 1, len(chunks))
-    t0 = time.perf_counter()
-    passes = 0
-    while True:
-        oracle.decode_many(chunks, nthreads=threads)
-        passes += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": decoded * passes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": f"{passes} full pass(es) over the {len(chunks)} workload chunks ({decoded / 1e6:.1f} MB decoded "
-                      f"each) with {threads} threads, {dt:.2f} s wall"}
+    decoded = 0
+    for _, _, ch in samples:
+        r = oracle.oracle._header(ch)
+        decoded += int(r[3]) + (4 * (int(r[2]) + 1) if r[0] == 4 else 0)
+    times, outs = {}, None
+    for th in threads_list:
+        t0 = time.perf_counter()
+        o = oracle.decode_many([c for _, _, c in samples], nthreads=th)
+        times[th] = time.perf_counter() - t0
+        outs = o
+    sums = {}
+    for (k, c, ch), (payload, offs) in zip(samples, outs):
+        cid = int.from_bytes(ch[56:64].tobytes(), "little")
+        sums[(k, c)] = chunk_checksum_oracle(payload, offs, cid)
+    return decoded, times, sums
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle on this arm's workload, K timed steps after W warm-up steps."""
+    """--impl reference: the CPU oracle on the bounded sample of this arm's workload, K timed steps after W."""
     if rank != 0:
         return
-    cols = build_workload(0, args.workload)
-    wl = WORKLOADS[args.workload]
+    from paper_2602_08190_b200 import workload
+    from paper_2602_08190_b200.inputs import MASTER_SEED
     import oracle
-    chunks = [c for (_, _, _, _, chs, _) in cols for c in chs]
-    decoded = sum(_decoded_bytes(c) for c in chunks)
-    threads = min(os.cpu_count() or 1, len(chunks))
+    wl = WORKLOADS[args.workload]
+    samples = workload.sample_chunks(wl["cols"], wl["sf"], MASTER_SEED, CHUNK_ROWS, per_column=1)
+    chunks = [c for _, _, c in samples]
+    decoded = 0
+    for c in chunks:
+        r = oracle.oracle._header(c)
+        decoded += int(r[3]) + (4 * (int(r[2]) + 1) if r[0] == 4 else 0)
+    threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         oracle.decode_many(chunks, nthreads=threads)
     t0 = time.perf_counter()
@@ -241,13 +283,15 @@ def run_reference(args, rank, world):
         oracle.decode_many(chunks, nthreads=threads)
     dt = time.perf_counter() - t0
     v = decoded * args.steps / dt / 1e9
+    sample = (f"each step = one oracle pass over the first chunk of every column ({len(chunks)} chunks, "
+              f"{decoded / 1e6:.1f} MB decoded) of the {desc_of(wl).split(':')[0]} workload at SF={wl['sf']:g}")
     line = {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"],
-            "data": "synthetic", "config": {"workload": wl["desc"], "chunk_rows": CHUNK_ROWS,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"],
+            "data": "synthetic", "config": {"workload": desc_of(wl), "chunk_rows": CHUNK_ROWS,
                                             "decoded_bytes_per_step": decoded},
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "oracle",
-                             "sample": f"each step = one full oracle pass over the {len(chunks)} workload chunks"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -257,9 +301,21 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    from paper_2602_08190_b200 import workload
+    from paper_2602_08190_b200.inputs import MASTER_SEED
+    wl = WORKLOADS[args.workload]
+    cpus = bind_cpus(local)
+
+    # ------------------------------------------------------------ this rank's shard (untimed; forks workers,
+    # so it runs before CUDA is initialised)
+    sel = shard_select(wl["cols"], wl["sf"], rank, world) if world > 1 else None
+    workers = args.workers or max(1, len(cpus) // max(1, local_world) if world > 1 else len(cpus))
+    ds = workload.build(wl["cols"], wl["sf"], MASTER_SEED, CHUNK_ROWS, select=sel, workers=workers)
+
     import torch
     import torch.distributed as dist
     from paper_2602_08190_b200 import cdm
@@ -267,267 +323,305 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # the column store moves into page-locked host memory (cudaHostAlloc through cdm_host_alloc: registering
+    # the workers' shared mapping in place is refused by the driver on this VM)
+    t0 = time.perf_counter()
+    pinned = cdm.PinnedBuffer(ds.used)
+    pin_s = time.perf_counter() - t0
+    src = ds.array()
+    step = 1 << 28
+    for a in range(0, ds.used, step):
+        pinned.array[a: a + step] = src[a: a + step]
+    host_all = pinned.array
+    copy_s = time.perf_counter() - t0 - pin_s
+    del src
+    ds.rebind(host_all)
+    host_t = torch.from_numpy(host_all)
 
-    cols = build_workload(rank, args.workload)
-    wl = WORKLOADS[args.workload]
-    compressed = sum(int(c.size) for (_, _, _, _, chs, _) in cols for c in chs)
-    decoded = sum(int(cdm.chunk_info(c)["payload_bytes"]) + int(cdm.chunk_info(c)["offsets_bytes"])
-                  for (_, _, _, _, chs, _) in cols for c in chs)
-    n_chunks = sum(len(chs) for (_, _, _, _, chs, _) in cols)
+    compressed, decoded, n_chunks = ds.compressed, ds.decoded, len(ds.chunks)
+    # one device buffer for every chunk's outputs (payload + offsets, 256-byte aligned slices) and one for the
+    # device-resident copy of the compressed chunks
+    def up(x):
+        return (x + 255) // 256 * 256
+    out_bytes = sum(up(max(c.payload, 16)) + up(c.offsets) for c in ds.chunks)
+    out_all = torch.empty(max(out_bytes, 256), dtype=torch.uint8, device="cuda")
+    dev_all = torch.empty(max(ds.used, 256), dtype=torch.uint8, device="cuda")
+    copy_stream = torch.cuda.Stream()
+    with torch.cuda.stream(copy_stream):
+        dev_all[: ds.used].copy_(host_t, non_blocking=True)
+    copy_stream.synchronize()
 
-    max_chunk = max(int(c.size) for (_, _, _, _, chs, _) in cols for c in chs)
-    slot = max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20))  # a slot holds any one chunk
+    max_chunk = max(c.size for c in ds.chunks)
+    slot = max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20))
     eng = cdm.Engine(local, n_slots=4, slot_bytes=slot, order_policy=1)
-    stream = torch.cuda.Stream()
-    # the compressed columns live back to back in ONE pinned host buffer (as a column store would keep them)
-    sizes = [int(c.size) for (_, _, _, _, chs, _) in cols for c in chs]
-    pinned_all = torch.empty(sum(sizes), dtype=torch.uint8).pin_memory()
-    pin_np = pinned_all.numpy()
-    decs_dev, decs_host, outs = [], [], []
+    cascs = [cdm.Cascade(spec, dt, w) for (_, spec, dt, w) in ds.columns]
+    decs_dev, decs_host, views = [], [], []
     pos = 0
-    for name, spec, dtype, width, chunks, _ in cols:
-        casc = cdm.Cascade(spec, dtype, width)
-        for ch in chunks:
-            out, offs = cdm.output_buffers(ch)
-            pin_np[pos:pos + ch.size] = ch
-            host = pinned_all[pos:pos + ch.size]
-            pos += ch.size
-            dev = torch.from_numpy(ch).cuda()
-            decs_dev.append(cdm.Decode(casc, host, out, offs, dev_chunk=dev))
-            decs_host.append(cdm.Decode(casc, host, out, offs))
-            outs.append(out)
-    batch = cdm.Batch(eng, decs_dev)
-    batch.set_graph(True)  # each step = one CUDA graph replay of the whole fused decode (no host launch gaps)
+    for c in ds.chunks:
+        pb = up(max(c.payload, 16))
+        out = out_all[pos: pos + pb]
+        pos += pb
+        offs = None
+        if c.offsets:
+            offs = out_all[pos: pos + c.offsets].view(torch.int32)
+            pos += up(c.offsets)
+        host = host_all[c.offset: c.offset + c.size]
+        decs_dev.append(cdm.Decode(cascs[c.column], host, out, offs, dev_chunk=dev_all[c.offset: c.offset + c.size]))
+        decs_host.append(cdm.Decode(cascs[c.column], host, out, offs))
+        views.append((out, offs))
+    stream = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    err_bits = 0
 
-    # ---------------------------------------------------------------- device-resident (value)
-    # one CUDA-graph replay of the whole fused decode per step; no family events inside the timed graph
-    batch.set_timing(False)
+    # ------------------------------------------------------------ (value) pipelined host -> device decode
+    pipe = cdm.Pipeline(eng, decs_host)
+    pinfo = pipe.info()
     for _ in range(args.warmup):
-        batch.launch(stream)
-    batch.results(stream)
+        pipe.launch(stream)
+        for r in pipe.results(raise_on_error=False):
+            err_bits |= r["error_bits"]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches = 0
+    wall = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    wall0 = time.perf_counter()
     with ClockSampler(local) as clocks:
         for k in range(args.steps):
+            t0 = time.perf_counter()
+            ev[k][0].record(stream)
+            pipe.launch(stream)                     # every compressed byte crosses PCIe + every chunk decodes
+            ev[k][1].record(stream)
+            for r in pipe.results(raise_on_error=False):  # per-chunk error words on the host
+                err_bits |= r["error_bits"]
+            wall.append(time.perf_counter() - t0)
+    torch.cuda.synchronize()
+    pipe_ms = sum(a.elapsed_time(b) for a, b in ev)
+    e2e_s = sum(wall)
+    launches = pinfo["kernel_launches"] * args.steps
+
+    # ------------------------------------------------------------ H9 parity: checksums of every chunk output
+    gpu_sums = {}
+    for c, (out, offs) in zip(ds.chunks, views):
+        cs = cdm.checksum(out[: c.payload], c.chunk_id, stream)
+        if offs is not None:
+            cs = (cs + cdm.checksum(offs, c.chunk_id ^ (1 << 63), stream)) % (1 << 64)
+        gpu_sums[(c.column, c.index)] = cs
+    checksum_total = sum(gpu_sums.values()) % (1 << 64)
+
+    # ------------------------------------------------------------ device-resident decode (kernel level)
+    batch = cdm.Batch(eng, decs_dev)
+    batch.set_graph(True)
+    kbytes = batch.kernel_bytes()
+    for _ in range(args.warmup):
+        batch.launch(stream)
+    for r in batch.results(stream, raise_on_error=False):
+        err_bits |= r["error_bits"]
+    dev_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as dev_clocks:
+        for k in range(args.steps):
             with torch.cuda.stream(stream):
-                flush.zero_()                     # L2 flush (256 MiB write), outside the events
-                ev[k][0].record(stream)
-                launches += batch.launch(stream)  # the whole hot path for this workload
-                ev[k][1].record(stream)
+                flush.zero_()                      # L2 flush (256 MiB write), outside the events
+                dev_ev[k][0].record(stream)
+                batch.launch(stream)
+                dev_ev[k][1].record(stream)
         torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    res = batch.results(stream)
-    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
-    err_bits = 0
-    for r in res:
+    dev_ms = sum(a.elapsed_time(b) for a, b in dev_ev)
+    for r in batch.results(stream, raise_on_error=False):
         err_bits |= r["error_bits"]
 
-    # ---------------------------------------------------------------- per-kernel / per-family time (roofline)
-    # the same graph re-captured with CUDA events around each kernel launch (mode 2: families one after
-    # another and the programmatically dependent RLE launches serialised, so every kernel is timed alone, as
-    # in the ncu launch list) and, in a second pass, around each kernel family (mode 1, concurrent);
-    # each replay's events are read between replays.  Kept apart from the value pass: in-graph events
-    # lengthen the step.
-    tsteps = min(args.steps, 50)
-    timing = {}
-    batch.set_graph(False)  # plain stream launches: an event record there is a light command (in a graph
-    for mode in (2, 1):     # an external event node costs ~2 us)
-        batch.set_timing(mode)
-        for _ in range(2):
+    # ------------------------------------------------------------ serialized (E11): copy everything, then decode
+    ser_ev = []
+    for k in range(max(2, min(args.steps, 3))):
+        a, m, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            dev_all[: ds.used].copy_(host_t, non_blocking=True)
+            m.record(stream)
             batch.launch(stream)
-        for r in batch.results(stream, raise_on_error=False):
-            err_bits |= r["error_bits"]
-        batch.set_timing(mode)  # reset the accumulated times
+            b.record(stream)
+        ser_ev.append((a, m, b))
+    torch.cuda.synchronize()
+    ser_ms = [a.elapsed_time(b) for a, _, b in ser_ev]
+    ser_copy_ms = [a.elapsed_time(m) for a, m, _ in ser_ev]
+    for r in batch.results(stream, raise_on_error=False):
+        err_bits |= r["error_bits"]
+
+    # ------------------------------------------------------------ per-kernel (alone) and per-family timing
+    tsteps = max(1, min(args.steps, 3))
+    timing = {}
+    batch.set_graph(False)
+    for mode in (2, 1):
+        batch.set_timing(mode)
+        batch.launch(stream)
+        batch.results(stream, raise_on_error=False)
+        batch.set_timing(mode)
         for k in range(tsteps):
             with torch.cuda.stream(stream):
                 flush.zero_()
                 batch.launch(stream)
-        for r in batch.results(stream, raise_on_error=False):  # reads every launch's events
+        for r in batch.results(stream, raise_on_error=False):
             err_bits |= r["error_bits"]
         timing[mode] = batch.kernel_times() if mode == 2 else batch.kernel_ms()
-    kern, ktimes = timing[1], timing[2]
-
-    # ---------------------------------------------------------------- end to end from pinned host (e2e)
-    # (a) streaming (the headline): two cdm_pipelines -- the H4 schedule (Johnson order, groups, H2D copies
-    #     overlapped with the fused decodes) captured once each as a CUDA graph, each with its own output
-    #     buffers -- launched alternately on two streams; every step re-copies all compressed bytes from
-    #     pinned host memory, decodes them and reads its per-chunk error words back on the host before that
-    #     pipeline is relaunched, so step k+1's copies overlap step k's decodes (a decode service's steady
-    #     state; the decoded bytes of a step exceed L2, the inputs cross PCIe every step).  Wall clock over
-    #     all steps.
-    # (b) one step at a time: launch + results, L2 flushed and the GPU idle before each step (includes the
-    #     graph launch latency and the last group's decode tail every step).
-    # (c) cdm_submit_batch + cdm_wait: the same schedule enqueued by the host group by group (reported too)
-    decs_host2 = []
-    for d in decs_host:
-        out2, offs2 = cdm.output_buffers(d.host_chunk.numpy() if hasattr(d.host_chunk, "numpy") else d.host_chunk)
-        decs_host2.append(cdm.Decode(d.cascade, d.host_chunk, out2, offs2))
-    pipes = [cdm.Pipeline(eng, decs_host), cdm.Pipeline(eng, decs_host2)]
-    streams2 = [torch.cuda.Stream(), torch.cuda.Stream()]
-    for _ in range(max(1, args.warmup)):
-        for k in range(2):
-            pipes[k].launch(streams2[k])
-        for k in range(2):
-            pipes[k].results()
-    e2e_steps = max(3, args.steps // 4)
-    stream_steps = 2 * max(4, args.steps // 4)
-    torch.cuda.synchronize()
+    ktimes, fams_conc = timing[2], timing[1]
+    batch.close()
+    h2d_alone = measure_h2d(torch) if rank == 0 or world == 1 else None
+    # H2D denominators: each rank alone (one after another), then all ranks concurrently
+    h2d_each = None
+    h2d_conc = None
     if world > 1:
+        h2d_each = []
+        for r in range(world):
+            dist.barrier()
+            v = measure_h2d(torch) if rank == r else 0.0
+            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t)
+            h2d_each.append(round(float(t.item()), 1))
         dist.barrier()
-    t0 = time.perf_counter()
-    pipes[0].launch(streams2[0])
-    for k in range(1, stream_steps + 1):
-        if k < stream_steps:
-            pipes[k % 2].launch(streams2[k % 2])   # step k's copies start while step k-1 decodes
-        for r in pipes[(k - 1) % 2].results(raise_on_error=False):  # step k-1's result on the host
-            err_bits |= r["error_bits"]
-    e2e_stream_total = time.perf_counter() - t0
-    pipes[1].close()
-    pipe = pipes[0]
-    for _ in range(max(1, args.warmup)):
-        pipe.launch(stream)
-        pipe.results()
-        for t in eng.submit_batch(decs_host):
-            eng.wait(t)
-    e2e_steps = max(3, args.steps // 4)
-    torch.cuda.synchronize()
-    e2e_total = 0.0
-    for _ in range(e2e_steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        pipe.launch(stream)
-        for r in pipe.results(raise_on_error=False):
-            err_bits |= r["error_bits"]
-        e2e_total += time.perf_counter() - t0
-    sub_total = 0.0
-    e2e_submit = 0.0
-    for _ in range(e2e_steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        tickets = eng.submit_batch(decs_host)
-        e2e_submit += time.perf_counter() - t0
-        for t in tickets:
-            r = eng.wait(t, raise_on_error=False)
-            err_bits |= r["error_bits"]
-        sub_total += time.perf_counter() - t0
-    pipe.close()
-    h2d_gbs = measure_h2d(torch)
+        v = measure_h2d(torch)
+        t = torch.zeros(world, dtype=torch.float64, device="cuda")
+        t[rank] = v
+        dist.all_reduce(t)
+        h2d_conc = [round(float(x), 1) for x in t.tolist()]
+        h2d_alone = h2d_each[rank]
 
-    # ---------------------------------------------------------------- reduce over ranks (metadata only)
-    dev_s = dev_ms / 1e3
+    # ------------------------------------------------------------ reduce over ranks (metadata only)
+    pipe_s, dev_s = pipe_ms / 1e3, dev_ms / 1e3
     if world > 1:
         meta = torch.tensor([decoded, compressed, n_chunks, err_bits], dtype=torch.int64, device="cuda")
         dist.all_reduce(meta, op=dist.ReduceOp.SUM)
-        tmax = torch.tensor([dev_s, e2e_total, sub_total, e2e_stream_total], dtype=torch.float64, device="cuda")
+        cs = torch.tensor([checksum_total & 0xFFFFFFFF, checksum_total >> 32], dtype=torch.int64, device="cuda")
+        dist.all_reduce(cs, op=dist.ReduceOp.SUM)  # 32-bit halves summed exactly, recombined mod 2^64
+        tmax = torch.tensor([pipe_s, e2e_s, dev_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tot_decoded, tot_comp, tot_chunks, tot_err = [int(x) for x in meta.tolist()]
-        dev_s, e2e_total, sub_total, e2e_stream_total = [float(x) for x in tmax.tolist()]
+        lo, hi = [int(x) for x in cs.tolist()]
+        checksum_total = (lo + (hi << 32)) % (1 << 64)
+        pipe_s, e2e_s, dev_s = [float(x) for x in tmax.tolist()]
     else:
         tot_decoded, tot_comp, tot_chunks, tot_err = decoded, compressed, n_chunks, err_bits
 
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded sample: the first chunk of every column, decoded by the oracle on 1 thread and on all cores
+        samples = [(c.column, c.index, ds.host(c).copy()) for c in ds.chunks if c.index == 0]
+        threads = os.cpu_count() or 1
+        sdec, stimes, osums = oracle_sample(samples, [1, threads])
+        mism = [k for k, v in osums.items() if gpu_sums.get(k) != v]
+        cpu = {"value": round(sdec / stimes[threads] / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+               "one_thread": {"value": round(sdec / stimes[1] / 1e9, 4), "cores": 1},
+               "cpu_model": cpu_model(),
+               "sample": f"the first chunk (2^22 rows) of each of the {len(samples)} columns, {sdec / 1e6:.1f} MB "
+                         f"decoded, one oracle pass on {threads} threads ({stimes[threads]:.2f} s) and one on 1 "
+                         f"thread ({stimes[1]:.2f} s)"}
+        parity = {"chunks_checked_vs_oracle": len(osums), "mismatches": len(mism),
+                  "mismatched": [list(k) for k in mism[:8]]}
+    else:
+        parity = {"chunks_checked_vs_oracle": 0, "mismatches": 0}
+
     if rank == 0:
-        value = tot_decoded * args.steps / dev_s / 1e9
-        e2e_single = tot_decoded * e2e_steps / e2e_total / 1e9
-        e2e = tot_decoded * stream_steps / e2e_stream_total / 1e9
-        e2e_sub = tot_decoded * e2e_steps / sub_total / 1e9
         peak, peak_src = load_peaks()
-        # dominant kernel by device time; algorithmic bytes = compressed read + decoded written (Eq. 1) of
-        # the chunks that kernel decodes
-        fam_ms = {FAMILY_NAMES[i]: kern[FAMILY_NAMES[i]] for i in range(5)}
-        fam_bytes = {"fp": 0, "scan": 0, "rle": 0, "lz4": 0, "copy": 0}  # lz4 = the chunk-sequential family
-        for d in decs_dev:
-            info = cdm.chunk_info(d.host_chunk)
-            plan = d.cascade.describe().split(" => ")[1]
-            if plan.startswith(("rle", "inner")):
-                fam_bytes["rle"] += info["compressed_bytes"] + info["payload_bytes"]
-            elif plan.startswith("fp"):
-                fam_bytes["fp"] += info["compressed_bytes"] + info["payload_bytes"]
-            elif "strdict" in plan:  # Str: the scan writes the offsets, the String-dictionary expansion the bytes
-                fam_bytes["scan"] += info["offsets_bytes"]
-                fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
-                fam_bytes["sd"] = fam_bytes.get("sd", 0) + info["compressed_bytes"] + info["payload_bytes"]
-            elif "lz4" in plan or "ans" in plan:  # Str: the scan writes the offsets, LZ4/ANS the bytes
-                fam_bytes["scan"] += info["offsets_bytes"]
-                fam_bytes["lz4"] += info["compressed_bytes"] + info["payload_bytes"]
-                fam_bytes["ans" if "ans" in plan else "lz4x"] = fam_bytes.get("ans" if "ans" in plan else "lz4x", 0) + \
-                    info["compressed_bytes"] + info["payload_bytes"]
-            else:
-                fam_bytes["copy"] += info["compressed_bytes"] + info["payload_bytes"]
-        kbytes = {"fp_kernel": fam_bytes["fp"], "scan_kernel": fam_bytes["scan"], "rle_kernel": fam_bytes["rle"],
-                  "lz4_kernel": fam_bytes.get("lz4x", 0), "ans_warp_kernel": fam_bytes.get("ans", 0),
-                  "strdict_kernel": fam_bytes.get("sd", 0),
-                  "device_copy": fam_bytes["copy"]}
-        dom = max(ktimes, key=lambda k: ktimes[k][0])
-        dom_ms, dom_n = ktimes[dom]
-        per_step_ms = dom_ms / tsteps
-        dom_bytes = kbytes.get(dom) or 0
-        achieved = dom_bytes / (per_step_ms / 1e3) / 1e9 if dom_bytes else 0.0
-        domf = max(fam_ms, key=lambda f: fam_ms[f][0])
+        value = tot_decoded * args.steps / pipe_s / 1e9
+        e2e = tot_decoded * args.steps / e2e_s / 1e9
+        dev_v = tot_decoded * args.steps / dev_s / 1e9
+        cr = tot_decoded / tot_comp
+        # rooflines: each kernel kind alone (events around each launch) against its algorithmic bytes
+        fam_ms, fam_bytes = {}, {}
+        for kname, (ms, n) in ktimes.items():
+            f = FAMILY_OF[kname]
+            if n:
+                fam_ms[f] = fam_ms.get(f, 0.0) + ms / tsteps
+            fam_bytes[f] = fam_bytes.get(f, 0) + kbytes.get(kname, 0)
+        families = {}
+        for f, ms in sorted(fam_ms.items(), key=lambda x: -x[1]):
+            b = fam_bytes.get(f, 0)
+            gbs = b / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+            families[f] = {"ms_per_step": round(ms, 4), "algorithmic_bytes": b, "achieved_gbs": round(gbs, 1),
+                           "frac": round(gbs / peak, 4)}
+        dom = max(families, key=lambda f: families[f]["ms_per_step"])
+        kern_of = {"fp_numeric": "fp_kernel", "fp_char": "fp_kernel(char)", "scan": "scan_kernel",
+                   "rle_chain": "rle_sums_kernel+rle_kernel(+level0, rle_big_kernel)", "lz4": "lz4_group_kernel",
+                   "ans": "ans_warp_kernel", "strdict": "sd_sums+sd_scan+sd_expand", "copy": "cudaMemcpyAsync D2D"}
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get(dom)
-        cr = tot_decoded / tot_comp
+                traffic = json.load(f).get(f"{args.workload}:{kern_of[dom]}")
+        conc = {k: round(v[0] / tsteps, 4) for k, v in fams_conc.items() if v[1]}
+        crit = max(conc, key=conc.get) if conc else None
+        cfg = {"workload": desc_of(wl), "sf": wl["sf"], "chunk_rows": CHUNK_ROWS, "columns": len(ds.columns),
+               "chunks": tot_chunks, "decoded_bytes_per_step": tot_decoded, "compressed_bytes_per_step": tot_comp,
+               "compression_ratio": round(cr, 3),
+               "parallelism": f"dp{world}: one dataset, per-rank contiguous chunk ranges (strong scaling)",
+               "l2": "inputs (21.5 GB compressed at SF=100) and outputs exceed the 126 MB L2; the device-resident "
+                     "pass also flushes L2 (256 MiB write) before each step",
+               "timing": "value: CUDA events on the launching stream around each cdm_pipeline_launch (sum over "
+                         "steps, max over ranks); e2e: host wall clock of launch + results",
+               "host": {"cpus_bound": len(cpus), "build_s": round(ds.build_s, 1), "build_workers": ds.workers,
+                        "pin_alloc_s": round(pin_s, 2), "pin_copy_s": round(copy_s, 2), "pinned_bytes": ds.used},
+               "pipeline": pinfo}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(dev_s * 1e3 / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
-            "config": {
-                "workload": wl["desc"] + ", per rank",
-                "sf_per_rank": wl["sf"], "chunk_rows": CHUNK_ROWS, "chunks_per_rank": n_chunks,
-                "decoded_bytes_per_step": tot_decoded, "compressed_bytes_per_step": tot_comp,
-                "compression_ratio": round(cr, 2), "parallelism": f"dp{world} (independent shards)",
-                "l2": "flushed between timed steps by a 256 MiB write outside the CUDA events",
-                "timing": "sum of per-step CUDA-event device times around one CUDA-graph replay of the batch on "
-                          "the launching stream; max over ranks",
-                "wall_s_timed_loop": round(wall, 4)},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
-                         "algorithmic_bytes_per_step": dom_bytes, "kernel_ms_per_step": round(per_step_ms, 4),
-                         "launches_per_step": round(dom_n / tsteps, 2),
-                         "kernels_ms_per_step": {k: round(v[0] / tsteps, 4) for k, v in ktimes.items() if v[1]},
-                         "peak_source": peak_src,
-                         "families_ms_per_step": {f: round(fam_ms[f][0] / tsteps, 4) for f in fam_ms if fam_ms[f][1]},
-                         "timing": f"CUDA events around each kernel launch, each kernel alone (kernels_ms), and "
-                                   f"around each concurrent kernel family (families_ms, dominant family {domf}), "
-                                   f"recorded on the launching streams over {tsteps} steps after L2 flushes each "
-                                   "(passes separate from the graph-timed value pass)"},
+            "warmup": args.warmup, "ms_per_step": round(pipe_s * 1e3 / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic", "config": cfg,
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": tot_comp,
-                    "d2h_bytes_per_step": 4 * tot_chunks, "pcie_h2d_gbs_measured": round(h2d_gbs, 1),
-                    "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_gbs, 1),
-                    "how": f"{stream_steps} streaming steps, wall clock: two cdm_pipelines (each the H4 schedule -- "
-                           "H2D copies of every compressed chunk from pinned host + fused decodes, Johnson order, "
-                           "groups overlapped -- captured once as a CUDA graph, own output buffers) launched "
-                           "alternately on two streams; each step's per-chunk error words are read on the host "
-                           "before its pipeline is relaunched, so a step's copies overlap the previous step's "
-                           "decodes",
-                    "single_step": {"value": round(e2e_single, 2),
-                                    "how": "cdm_pipeline_launch + cdm_pipeline_results, one step at a time after "
-                                           "an L2 flush and a device synchronize (includes the graph launch "
-                                           "latency and the last group's decode tail each step)"},
-                    "submit_batch": {"value": round(e2e_sub, 2),
-                                     "host_submit_ms_per_step": round(e2e_submit * 1e3 / e2e_steps, 4),
-                                     "how": "cdm_submit_batch + cdm_wait per chunk (host enqueues each group)"}},
+                    "d2h_bytes_per_step": 4 * tot_chunks, "ms_per_step": round(e2e_s * 1e3 / args.steps, 3),
+                    "how": "cdm_pipeline_launch + cdm_pipeline_results per step, host wall clock: every compressed "
+                           "chunk copied H2D from pinned host and decoded, every chunk's error word read back",
+                    "pcie_h2d_gbs_measured": round(h2d_alone, 1) if h2d_alone else None,
+                    "pcie_h2d_gbs_each_rank_alone": h2d_each, "pcie_h2d_gbs_all_ranks_concurrent": h2d_conc,
+                    "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_alone * (world if world > 1 else 1), 1)
+                    if h2d_alone else None,
+                    "serialized": {"value": round(tot_decoded / (statistics.median(ser_ms) / 1e3) / 1e9, 2)
+                                   if world == 1 else None,
+                                   "ms_per_step": round(statistics.median(ser_ms), 3),
+                                   "copy_ms": round(statistics.median(ser_copy_ms), 3),
+                                   "how": "E11 (PAPER.md:654-657): one H2D copy of all compressed bytes, then the "
+                                          "device-resident decode, no overlap (rank 0)"}},
+            "device_resident": {"value": round(dev_v, 2), "unit": "GB/s",
+                                "ms_per_step": round(dev_s * 1e3 / args.steps, 3),
+                                "decoded_written_over_8tbs": round(dev_v / 8000.0, 4),
+                                "clocks": dev_clocks.summary(),
+                                "how": "one CUDA-graph replay of the whole fused decode of every chunk already in "
+                                       "HBM, CUDA events on the launching stream, L2 flushed between steps"},
+            "roofline": {"bound": "hbm", "achieved": families[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": families[dom]["frac"], "traffic": traffic, "kernel": kern_of[dom], "family": dom,
+                         "algorithmic_bytes_per_step": families[dom]["algorithmic_bytes"],
+                         "kernel_ms_per_step": families[dom]["ms_per_step"], "peak_source": peak_src,
+                         "families": families, "families_concurrent_ms": conc, "critical_path_family": crit,
+                         "timing": f"CUDA events around each kernel launch (each kernel alone, families serialised) "
+                                   f"over {tsteps} device-resident steps after L2 flushes; bytes from "
+                                   "cdm_batch_kernel_bytes (Eq. 1)"},
+            "parity": dict(parity, checksum_total=f"{checksum_total:016x}", chunks_checksummed_on_gpu=tot_chunks,
+                           errors=tot_err),
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "errors": tot_err,
         }
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cols, args.cpu_seconds)
+        if cpu:
+            line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    batch.close()
+    pipe.close()
     eng.close()
+    del decs_host, decs_dev, host_t
+    pinned.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def build_workload(rank: int, workload: str = "config2"):
+    """Compatibility helper for tests: [(name, spec, dtype, width, [chunk numpy arrays], plain bytes)]."""
+    from paper_2602_08190_b200 import workload as W
+    from paper_2602_08190_b200.inputs import MASTER_SEED
+    wl = WORKLOADS[workload]
+    ds = W.build(wl["cols"], wl["sf"], MASTER_SEED + 1000 * rank, CHUNK_ROWS)
+    out = []
+    for k, (name, spec, dt, w) in enumerate(ds.columns):
+        chs = [ds.host(c).copy() for c in ds.chunks if c.column == k]
+        plain = sum(c.plain for c in ds.chunks if c.column == k)
+        out.append((name, spec, dt, w, chs, plain))
+    return out
 
 
 if __name__ == "__main__":

@@ -183,6 +183,20 @@ CDM_API cdm_status cdm_pipeline_create(cdm_engine *e, const cdm_job *jobs, size_
 CDM_API cdm_status cdm_pipeline_launch(cdm_pipeline *p, void *stream);
 CDM_API cdm_status cdm_pipeline_results(cdm_pipeline *p, cdm_result *results);
 CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
+/* What one cdm_pipeline_launch enqueues: kernel launches (every decode kernel + the error harvest), groups
+ * (staging regions / multi-chunk batches) and H2D copies (runs of host-contiguous chunks). */
+CDM_API cdm_status cdm_pipeline_info(const cdm_pipeline *p, uint32_t *n_launches, uint32_t *n_groups,
+                                     uint32_t *n_copies);
+
+/* ---- pinned host memory: page-lock (cudaHostRegister) a caller-owned host range in place, so chunks that
+ * live in it can be submitted (the paper pins all host buffers).  p/bytes: the range (page
+ * aligned for best results); unregister before freeing it.  Errors: CDM_E_INVALID_ARG, CDM_E_CUDA. */
+CDM_API cdm_status cdm_host_register(void *p, size_t bytes);
+CDM_API cdm_status cdm_host_unregister(void *p);
+/* Allocate / free page-locked host memory for a column store (cudaHostAlloc; exactly `bytes`, no rounding).
+ * Errors: CDM_E_INVALID_ARG, CDM_E_OOM. */
+CDM_API cdm_status cdm_host_alloc(size_t bytes, void **out);
+CDM_API cdm_status cdm_host_free(void *p);
 
 /* ---- instrumentation ---- */
 /* Record CUDA events around each kernel family (enable = 1) or around each kernel launch (enable = 2,
@@ -191,13 +205,18 @@ CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline *p);
  * call resets the accumulators.  After cdm_batch_results (or cdm_batch_collect_timing in graph mode):
  * cdm_batch_kernel_ms() -> per-family milliseconds and launches: index 0 FP (H5), 1 delta/offset scan (H6),
  *   2 RLE (H7), 3 LZ4 (H8), 4 raw copies;
- * cdm_batch_kernel_times() -> per-kernel milliseconds and launches (mode 2): index 0 fp_kernel,
+ * cdm_batch_kernel_times() -> per-kernel milliseconds and launches (mode 2): index 0 fp_kernel (numeric rows),
  *   1 scan_kernel, 2 rle_sums_kernel, 3 rle_kernel level 0 (value lineage), 4 rle_kernel, 5 rle_big_kernel,
- *   6 lz4_kernel, 7 device copies, 8 ans_kernel, 9 String-dictionary (sd_sums + sd_scan + sd_expand)
- *   (arrays of 10). */
+ *   6 lz4 kernel, 7 device copies, 8 ANS kernel, 9 String-dictionary (sd_sums + sd_scan + sd_expand),
+ *   10 fp_kernel on FIXED (CHAR(n)) rows (arrays of CDM_KERNEL_KINDS);
+ * cdm_batch_kernel_bytes() -> per kernel kind, the ALGORITHMIC bytes one launch of the batch moves (Eq. 1,
+ *   the compressed bytes the kind must read + the decoded bytes it must write, summed over
+ *   the batch's jobs; a job's whole RLE chain -- counts, values, output -- is booked on index 4). */
+#define CDM_KERNEL_KINDS 11
 CDM_API cdm_status cdm_batch_set_timing(cdm_batch *b, int enable);
 CDM_API cdm_status cdm_batch_kernel_ms(cdm_batch *b, double *ms5, uint64_t *launches5);
-CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms10, uint64_t *launches10);
+CDM_API cdm_status cdm_batch_kernel_times(cdm_batch *b, double *ms, uint64_t *launches);
+CDM_API cdm_status cdm_batch_kernel_bytes(cdm_batch *b, uint64_t *bytes);
 /* Graph mode + timing: every replay re-records the same events, so call this after each launch (it
  * waits for that replay) to accumulate its per-family times; a replay not collected is not counted. */
 CDM_API cdm_status cdm_batch_collect_timing(cdm_batch *b);

@@ -19,15 +19,18 @@ STATUS = {0: "CDM_OK", 1: "CDM_E_INVALID_ARG", 2: "CDM_E_PARSE", 3: "CDM_E_UNSUP
 ERR_DICT_INDEX, ERR_RUN_SUM, ERR_LZ4, ERR_LENGTHS, ERR_WIDTH = 0x1, 0x2, 0x4, 0x8, 0x10
 FAMILIES = ["fp", "scan", "rle", "lz4", "copy"]
 KERNELS = ["fp_kernel", "scan_kernel", "rle_sums_kernel", "rle_kernel(level0)", "rle_kernel", "rle_big_kernel",
-           "lz4_kernel", "device_copy", "ans_warp_kernel", "strdict_kernel"]  # ANS slot: ans_warp_kernel (il = 32) or ans_kernel (il = 1)
+           "lz4_kernel", "device_copy", "ans_kernel", "strdict_kernel", "fp_kernel(char)"]
+# cdm_batch_kernel_times slots (include/cdm.h): the ANS slot times ans_warp_kernel (il = 32) and ans_kernel
+# (il = 1); "rle_kernel" carries the algorithmic bytes of the whole RLE chain
 
 SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_create", "cdm_cascade_destroy",
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
            "cdm_submit_batch", "cdm_wait", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
-           "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times",
+           "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times", "cdm_batch_kernel_bytes",
            "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy",
-           "cdm_tune_set", "cdm_tune_get", "cdm_checksum"]
+           "cdm_tune_set", "cdm_tune_get", "cdm_checksum", "cdm_pipeline_info", "cdm_host_register",
+           "cdm_host_unregister", "cdm_host_alloc", "cdm_host_free"]
 
 
 class EngineOpts(ctypes.Structure):
@@ -94,10 +97,16 @@ def lib():
         "cdm_batch_set_graph": [vp, st],
         "cdm_batch_collect_timing": [vp],
         "cdm_batch_kernel_times": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)],
+        "cdm_batch_kernel_bytes": [vp, ctypes.POINTER(u64)],
         "cdm_pipeline_create": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(vp)],
         "cdm_pipeline_launch": [vp, vp],
         "cdm_pipeline_results": [vp, ctypes.POINTER(Result)],
         "cdm_pipeline_destroy": [vp],
+        "cdm_pipeline_info": [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u32)],
+        "cdm_host_register": [vp, sz],
+        "cdm_host_unregister": [vp],
+        "cdm_host_alloc": [sz, ctypes.POINTER(vp)],
+        "cdm_host_free": [vp],
         "cdm_tune_set": [ctypes.c_char_p, ctypes.c_int],
         "cdm_tune_get": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)],
         "cdm_checksum": [vp, ctypes.c_uint64, ctypes.c_uint64, vp, ctypes.POINTER(ctypes.c_uint64)],
@@ -314,6 +323,12 @@ class Batch:
         _check(lib().cdm_batch_kernel_times(self.h, ms, nl))
         return {KERNELS[i]: (ms[i], nl[i]) for i in range(len(KERNELS))}
 
+    def kernel_bytes(self) -> dict:
+        """Algorithmic bytes (Eq. 1) one launch of the batch moves, per kernel kind."""
+        b = (ctypes.c_uint64 * len(KERNELS))()
+        _check(lib().cdm_batch_kernel_bytes(self.h, b))
+        return {KERNELS[i]: int(b[i]) for i in range(len(KERNELS))}
+
     def close(self) -> None:
         if getattr(self, "h", None) and _lib is not None:
             _lib.cdm_batch_destroy(self.h)
@@ -346,6 +361,11 @@ class Pipeline:
             _check(rc)
         return [self._res[i].as_dict() for i in range(self.n)]
 
+    def info(self) -> dict:
+        a, b, c = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        _check(lib().cdm_pipeline_info(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"kernel_launches": a.value, "groups": b.value, "h2d_copies": c.value}
+
     def close(self) -> None:
         if getattr(self, "h", None) and _lib is not None:
             _lib.cdm_pipeline_destroy(self.h)
@@ -373,6 +393,35 @@ def output_buffers(host_chunk: np.ndarray, device="cuda"):
     if info["offsets_bytes"]:
         offs = torch.empty(info["offsets_bytes"] // 4, dtype=torch.int32, device=device)
     return out, offs
+
+
+def host_register(ptr: int, nbytes: int) -> None:
+    """cdm_host_register: page-lock a caller-owned host range in place."""
+    _check(lib().cdm_host_register(ptr, nbytes))
+
+
+def host_unregister(ptr: int) -> None:
+    _check(lib().cdm_host_unregister(ptr))
+
+
+class PinnedBuffer:
+    """cdm_host_alloc: `nbytes` of page-locked host memory (no size rounding), viewed as a numpy uint8 array."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _check(lib().cdm_host_alloc(max(int(nbytes), 1), ctypes.byref(p)))
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+        self.array = np.ctypeslib.as_array((ctypes.c_uint8 * max(self.nbytes, 1)).from_address(self.ptr))[: self.nbytes]
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None) and _lib is not None:
+            self.array = None
+            _lib.cdm_host_free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        self.close()
 
 
 def pinned(a: np.ndarray):

@@ -483,7 +483,8 @@ static int fam_priority(int f, int lo, int hi) {
 }
 
 // kernel kinds of cdm_batch_kernel_times (include/cdm.h)
-enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, K_ANS, K_SD, kKernelKinds };
+enum KernelKind { K_FP = 0, K_SCAN, K_RLE_SUMS, K_RLE_L0, K_RLE_L1, K_RLE_BIG, K_LZ4, K_COPY, K_ANS, K_SD, K_FPC,
+                  kKernelKinds };
 
 struct cdm_batch {
   cdm_engine* e = nullptr;
@@ -491,6 +492,10 @@ struct cdm_batch {
   std::vector<Bound> jobs;
   std::vector<FpBatch> fp;
   std::vector<uint32_t> fp_maxw;
+  std::vector<uint8_t> fp_char;  // 1: the launch decodes FIXED (CHAR(n)) rows (kernel kind K_FPC)
+  // algorithmic bytes per kernel kind (Eq. 1: compressed bytes the kind must read + decoded
+  // bytes it must write, summed over the batch's jobs); the RLE chain is booked on K_RLE_L1
+  uint64_t k_bytes[kKernelKinds] = {};
   std::vector<ScanBatch> scan;
   std::vector<SumsBatch> sums;
   std::vector<RleBatch> rle;
@@ -564,7 +569,8 @@ bool getenv_flag(const char* name) {
 // Returns the arena bytes; `zero_bytes` = prefix of the arena that must start zeroed.
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
-  B->fp.clear(); B->fp_maxw.clear(); B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
+  B->fp.clear(); B->fp_maxw.clear(); B->fp_char.clear();
+  for (auto& kb : B->k_bytes) kb = 0; B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
   B->ans.clear(); B->sd.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
@@ -599,8 +605,15 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       g.emplace_back(v.begin() + i, v.begin() + std::min(v.size(), i + size_t(kMaxBatch)));
     return g;
   };
-  // FP
-  for (auto& g : groups(fpj)) {
+  // FP: numeric rows and FIXED (CHAR(n)) rows in separate launches (separate kernel kinds)
+  std::vector<int> fp_num, fp_chr;
+  for (int j : fpj) (B->jobs[j].casc->dtype == T_FIXED ? fp_chr : fp_num).push_back(j);
+  std::vector<std::vector<int>> fp_groups = groups(fp_num);
+  const size_t n_num_groups = fp_groups.size();
+  for (auto& g : groups(fp_chr)) fp_groups.push_back(g);
+  for (size_t gi = 0; gi < fp_groups.size(); gi++) {
+    const auto& g = fp_groups[gi];
+    B->fp_char.push_back(gi >= n_num_groups);
     FpBatch fb{};
     fb.err = B->err_dev;
     uint32_t tiles = 0, maxw = 0;
@@ -871,6 +884,37 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     B->lz4.push_back(lb);
     B->lz4_max_sub.push_back(max_sub);
   }
+  for (size_t i = 0; i < nj; i++) {
+    const Bound& b = B->jobs[i];
+    auto packed = [](const BPB& p) { return (p.n * p.w + 7) / 8; };
+    const uint64_t ans_in = b.ans ? 2 * b.ans_w_n + 512 + (8ull + 4ull * b.ans_il) * b.ans_nchunks : 0;
+    switch (b.kind) {
+      case PlanKind::Fp:
+        B->k_bytes[b.casc->dtype == T_FIXED ? K_FPC : K_FP] +=
+            packed(b.main) + uint64_t(b.entries) * (b.fp_mode == FP_DICT ? b.W : 0) + b.payload;
+        break;
+      case PlanKind::Scan: B->k_bytes[K_SCAN] += packed(b.main) + b.payload; break;
+      case PlanKind::Rle: {
+        uint64_t in = 0;
+        for (const RleLevel& L : b.lv) in += packed(L.cnt) + (L.vmode == V_RAW ? 0 : packed(L.val));
+        if (b.lv.back().vmode == V_DICT) in += uint64_t(b.entries) * b.W;
+        B->k_bytes[K_RLE_L1] += in + b.payload;
+        break;
+      }
+      case PlanKind::Ans: B->k_bytes[K_ANS] += ans_in + b.payload; break;
+      case PlanKind::RawCopy: B->k_bytes[K_COPY] += 2 * b.payload; break;
+      case PlanKind::Str:
+        if (b.rows) B->k_bytes[K_SCAN] += packed(b.main) + b.offsets_bytes;
+        if (b.lz4) B->k_bytes[K_LZ4] += b.lz_pay_bytes + 12ull * b.n_sub + b.payload;
+        else if (b.strdict) {
+          const uint64_t ids = b.ans ? b.ans_n : (uint64_t(b.sd_ntok) * b.sd_w + 7) / 8;
+          if (b.ans) B->k_bytes[K_ANS] += ans_in + ids;
+          B->k_bytes[K_SD] += ids + b.sd_dict_bytes + b.payload;
+        } else if (b.ans) B->k_bytes[K_ANS] += ans_in + b.payload;
+        else B->k_bytes[K_COPY] += 2 * b.payload;
+        break;
+    }
+  }
   return A.off + 256;
 }
 
@@ -952,7 +996,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
     switch (fam) {
       case F_FP:
         for (size_t i = 0; i < B->fp.size() && !st; i++) {
-          st = timed(K_FP, [&] { return launch_fp(B->fp[i], B->fp_maxw[i], fs); });
+          st = timed(B->fp_char[i] ? K_FPC : K_FP, [&] { return launch_fp(B->fp[i], B->fp_maxw[i], fs); });
           n++; B->fam_launches[F_FP]++;
         }
         break;
@@ -1497,6 +1541,7 @@ struct cdm_pipeline {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaStream_t last_stream = nullptr;
+  uint32_t n_launches = 0, n_groups = 0, n_copies = 0;  // kernel launches / groups / H2D copies per launch
   ~cdm_pipeline() {
     if (exec) cudaGraphExecDestroy(exec);
     if (err_dev) cudaFree(err_dev);
@@ -1539,10 +1584,15 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
       const size_t j = by_addr[k];
       const uint8_t* h = static_cast<const uint8_t*>(G.js[j]->host_chunk);
       CopyRun* last = runs[g].empty() ? nullptr : &runs[g].back();
-      if (last && static_cast<const uint8_t*>(last->src) + last->bytes == h && last->bytes % 16 == 0 &&
-          !getenv_flag("CDM_PIPE_NOMERGE")) {
-        stage_off[g][j] = last->off + last->bytes;  // == stage_bytes
-        last->bytes += G.bs[j].total;
+      // a chunk that starts at most kCopyGap bytes after the previous run's end (the alignment padding of a
+      // column store) joins that run: the copy spans the gap and the chunk keeps its 16-byte-aligned
+      // relative offset in the staging region
+      const uint8_t* last_end = last ? static_cast<const uint8_t*>(last->src) + last->bytes : nullptr;
+      constexpr size_t kCopyGap = 256;
+      if (last && h >= last_end && size_t(h - last_end) <= kCopyGap &&
+          size_t(h - static_cast<const uint8_t*>(last->src)) % 16 == 0 && !getenv_flag("CDM_PIPE_NOMERGE")) {
+        stage_off[g][j] = last->off + size_t(h - static_cast<const uint8_t*>(last->src));
+        last->bytes = size_t(h - static_cast<const uint8_t*>(last->src)) + G.bs[j].total;
       } else {
         stage_bytes = (stage_bytes + 255) & ~size_t(255);
         stage_off[g][j] = stage_bytes;
@@ -1673,8 +1723,10 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
   for (size_t l = 0; l < lanes; l++) CAP_TRY(cudaStreamWaitEvent(ds[l], start, 0));
   // copy branch: Johnson order of groups, one copy per run of host-contiguous chunks
   for (size_t g = 0; g < groups.size(); g++) {
-    for (const CopyRun& r : runs[g])
+    for (const CopyRun& r : runs[g]) {
       CAP_TRY(cudaMemcpyAsync(P->staging + r.off, r.src, r.bytes, cudaMemcpyHostToDevice, copy));
+      P->n_copies++;
+    }
     CAP_TRY(cudaEventRecord(copied[g], copy));
   }
   CAP_TRY(cudaEventRecord(copy_end, copy));
@@ -1687,7 +1739,9 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
     uint32_t nl = 0;
     cdm_status s2 = batch_enqueue(B, ds[l], &nl);
     if (s2) return abort_capture(s2);
+    P->n_launches += nl;
   }
+  P->n_groups = uint32_t(groups.size());
   for (size_t l = 0; l < lanes; l++) {
     CAP_TRY(cudaEventRecord(lane_end[l], ds[l]));
     CAP_TRY(cudaStreamWaitEvent(origin, lane_end[l], 0));
@@ -1695,6 +1749,7 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
   CAP_TRY(cudaStreamWaitEvent(origin, copy_end, 0));
   // one harvest at the end: every job's error word to mapped pinned memory, then zeroed for the next launch
   CAP_TRY(launch_harvest(P->err_dev, P->err_mapped, uint32_t(n), origin));
+  P->n_launches += 1;
 #undef CAP_TRY
   CUDA_TRY(cudaStreamEndCapture(origin, &P->graph));
   // kernel nodes keep the priority of the stream they were captured on (RLE lowest, the rest highest)
@@ -1736,6 +1791,40 @@ extern "C" CDM_API cdm_status cdm_pipeline_results(cdm_pipeline* p, cdm_result* 
     }
   }
   return bad ? CDM_E_CORRUPT : CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_pipeline_info(const cdm_pipeline* p, uint32_t* n_launches, uint32_t* n_groups,
+                                               uint32_t* n_copies) {
+  if (!p) return fail(CDM_E_INVALID_ARG, "null pipeline");
+  if (n_launches) *n_launches = p->n_launches;
+  if (n_groups) *n_groups = p->n_groups;
+  if (n_copies) *n_copies = p->n_copies;
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_host_register(void* p, size_t bytes) {
+  if (!p || !bytes) return fail(CDM_E_INVALID_ARG, "null / empty host range");
+  CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_host_alloc(size_t bytes, void** out) {
+  if (!out || !bytes) return fail(CDM_E_INVALID_ARG, "null out / zero bytes");
+  *out = nullptr;
+  const cudaError_t ce = cudaHostAlloc(out, bytes, cudaHostAllocDefault);
+  if (ce != cudaSuccess) { *out = nullptr; return fail(CDM_E_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(ce)); }
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_host_free(void* p) {
+  if (p) CUDA_TRY(cudaFreeHost(p));
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_host_unregister(void* p) {
+  if (!p) return fail(CDM_E_INVALID_ARG, "null host pointer");
+  CUDA_TRY(cudaHostUnregister(p));
+  return CDM_OK;
 }
 
 extern "C" CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline* p) {
@@ -1971,12 +2060,18 @@ extern "C" CDM_API cdm_status cdm_tune_get(const char* knob, int* value) {
   return CDM_OK;
 }
 
-extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms10, uint64_t* launches10) {
+extern "C" CDM_API cdm_status cdm_batch_kernel_times(cdm_batch* b, double* ms, uint64_t* launches) {
   if (!b) return fail(CDM_E_INVALID_ARG, "null batch");
   for (int i = 0; i < kKernelKinds; i++) {
-    if (ms10) ms10[i] = b->k_ms[i];
-    if (launches10) launches10[i] = b->k_n[i];
+    if (ms) ms[i] = b->k_ms[i];
+    if (launches) launches[i] = b->k_n[i];
   }
+  return CDM_OK;
+}
+
+extern "C" CDM_API cdm_status cdm_batch_kernel_bytes(cdm_batch* b, uint64_t* bytes) {
+  if (!b || !bytes) return fail(CDM_E_INVALID_ARG, "null argument");
+  for (int i = 0; i < kKernelKinds; i++) bytes[i] = b->k_bytes[i];
   return CDM_OK;
 }
 

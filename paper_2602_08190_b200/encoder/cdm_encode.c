@@ -24,6 +24,7 @@
 #include <string.h>
 #include <stdio.h>
 #include <ctype.h>
+#include <math.h>
 
 #define EXPORT __attribute__((visibility("default")))
 
@@ -313,11 +314,16 @@ static int enc_bitpack(builder *b, const tnode *t, col_t in) {
   uint64_t nbytes = (in.n * (uint64_t)w + 7) / 8;
   uint8_t *pk = (uint8_t *)calloc(nbytes + 16, 1);
   if (!pk) { free(v); return fail(E_OOM, "out of memory"); }
-  for (uint64_t i = 0; i < in.n; i++) {
+  /* value i occupies bits [i*w, i*w + w): OR it into the little-endian 8-byte word at its first byte, and
+   * its top bits into the next word when it crosses (the buffer has 16 slack bytes) */
+  for (uint64_t i = 0; w && i < in.n; i++) {
     uint64_t f = (uint64_t)v[i] - (uint64_t)mn;
     uint64_t bit = i * (uint64_t)w;
-    for (int k = 0; k < w; k++, bit++)
-      if ((f >> k) & 1) pk[bit >> 3] |= (uint8_t)(1u << (bit & 7));
+    unsigned sh = (unsigned)(bit & 7);
+    uint8_t *p = pk + (bit >> 3);
+    uint64_t word;
+    memcpy(&word, p, 8); word |= f << sh; memcpy(p, &word, 8);
+    if (sh + (unsigned)w > 64) { memcpy(&word, p + 8, 8); word |= f >> (64 - sh); memcpy(p + 8, &word, 8); }
   }
   free(v);
   node_rec r; memset(&r, 0, sizeof r);

@@ -180,24 +180,39 @@ static inline int64_t retail_cents(int64_t pk) { return 90000 + ((pk / 10) % 200
 
 typedef struct { int64_t part, supp, qty, ext_c, disc_c, tax_c; int32_t sd, cd, rd; char rflag, lstatus; } line_t;
 
-static void make_line(const gen_ctx *g, uint64_t o, uint32_t l, line_t *L) {
+/* Which line fields a column needs (each field is a pure function of (seed, field, order, line), so
+ * computing only the needed ones gives the same values as computing all of them). */
+enum { N_PART = 1, N_SUPP = 2, N_QTY = 4, N_EXT = 8, N_DISC = 16, N_TAX = 32, N_SD = 64, N_CD = 128, N_RD = 256,
+       N_RFLAG = 512, N_LSTATUS = 1024, N_ALL = 2047 };
+
+static void make_line_fields(const gen_ctx *g, uint64_t o, uint32_t l, unsigned need, line_t *L) {
   uint64_t id = o * 8 + l;
-  int64_t nparts = (int64_t)(200000.0 * g->sf); if (nparts < 1) nparts = 1;
-  int64_t nsupp = (int64_t)(10000.0 * g->sf); if (nsupp < 1) nsupp = 1;
-  int32_t od = (int32_t)unif(g, F_ODATE, o, STARTDATE, ENDDATE - 151);
-  L->part = unif(g, F_PART, id, 1, nparts);
-  int64_t i = unif(g, F_SUPPI, id, 0, 3);
-  L->supp = (L->part + (i * (nsupp / 4 + (L->part - 1) / nsupp))) % nsupp + 1;
-  L->qty = unif(g, F_QTY, id, 1, 50);
-  L->ext_c = L->qty * retail_cents(L->part);
-  L->disc_c = unif(g, F_DISC, id, 0, 10);
-  L->tax_c = unif(g, F_TAX, id, 0, 8);
-  L->sd = od + (int32_t)unif(g, F_SHIPD, id, 1, 121);
-  L->cd = od + (int32_t)unif(g, F_COMMITD, id, 30, 90);
-  L->rd = L->sd + (int32_t)unif(g, F_RECEIPTD, id, 1, 30);
-  L->rflag = (L->rd <= CURRENTDATE) ? ((rnd(g, F_RFLAG, id) >> 20) & 1 ? 'R' : 'A') : 'N';
-  L->lstatus = (L->sd > CURRENTDATE) ? 'O' : 'F';
+  if (need & (N_RFLAG | N_LSTATUS)) need |= N_SD | N_RD;
+  if (need & N_RD) need |= N_SD;
+  if (need & N_EXT) need |= N_QTY | N_PART;
+  if (need & N_SUPP) need |= N_PART;
+  int32_t od = 0;
+  if (need & (N_SD | N_CD)) od = (int32_t)unif(g, F_ODATE, o, STARTDATE, ENDDATE - 151);
+  if (need & N_PART) {
+    int64_t nparts = (int64_t)(200000.0 * g->sf); if (nparts < 1) nparts = 1;
+    L->part = unif(g, F_PART, id, 1, nparts);
+  }
+  if (need & N_SUPP) {
+    int64_t nsupp = (int64_t)(10000.0 * g->sf); if (nsupp < 1) nsupp = 1;
+    int64_t i = unif(g, F_SUPPI, id, 0, 3);
+    L->supp = (L->part + (i * (nsupp / 4 + (L->part - 1) / nsupp))) % nsupp + 1;
+  }
+  if (need & N_QTY) L->qty = unif(g, F_QTY, id, 1, 50);
+  if (need & N_EXT) L->ext_c = L->qty * retail_cents(L->part);
+  if (need & N_DISC) L->disc_c = unif(g, F_DISC, id, 0, 10);
+  if (need & N_TAX) L->tax_c = unif(g, F_TAX, id, 0, 8);
+  if (need & N_SD) L->sd = od + (int32_t)unif(g, F_SHIPD, id, 1, 121);
+  if (need & N_CD) L->cd = od + (int32_t)unif(g, F_COMMITD, id, 30, 90);
+  if (need & N_RD) L->rd = L->sd + (int32_t)unif(g, F_RECEIPTD, id, 1, 30);
+  if (need & N_RFLAG) L->rflag = (L->rd <= CURRENTDATE) ? ((rnd(g, F_RFLAG, id) >> 20) & 1 ? 'R' : 'A') : 'N';
+  if (need & N_LSTATUS) L->lstatus = (L->sd > CURRENTDATE) ? 'O' : 'F';
 }
+
 
 static void put_padded(uint8_t *dst, const char *s, int w) {
   int n = (int)strlen(s);
@@ -220,12 +235,15 @@ EXPORT int gen_fixed(void *p, int table, int col, uint64_t row0, uint64_t nrows,
   if (table == T_LINEITEM) {
     if (row0 + nrows > g->n_lines) return -1;
     if (nrows == 0) return 0;
+    static const unsigned NEED[L_NCOLS] = {0, N_PART, N_SUPP, 0, N_QTY, N_EXT, N_DISC, N_TAX, N_RFLAG, N_LSTATUS,
+                                           N_SD, N_CD, N_RD, 0, 0, 0};
+    const unsigned need = NEED[col];
     uint64_t o = find_order(g, row0);
     uint32_t l = (uint32_t)(row0 - lp(g, o));
     for (uint64_t r = 0; r < nrows; r++) {
       while (lp(g, o) + l >= lp(g, o + 1)) { o++; l = 0; }
       line_t L;
-      make_line(g, o, l, &L);
+      if (need) make_line_fields(g, o, l, need, &L);
       uint8_t *d = dst + r * (uint64_t)w;
       int64_t i64; int32_t i32; double f;
       switch (col) {
@@ -277,7 +295,7 @@ EXPORT int gen_fixed(void *p, int table, int col, uint64_t row0, uint64_t nrows,
         uint32_t nl = (uint32_t)(lp(g, o + 1) - lp(g, o));
         int nf = 0; int64_t tot = 0;
         for (uint32_t l = 0; l < nl; l++) {
-          line_t L; make_line(g, o, l, &L);
+          line_t L; make_line_fields(g, o, l, col == O_ORDERSTATUS ? N_LSTATUS : (N_EXT | N_TAX | N_DISC), &L);
           nf += (L.lstatus == 'F');
           /* cents * (100+tax) * (100-disc) / 10^4, rounded half up (integer, exact) */
           tot += (L.ext_c * (100 + L.tax_c) * (100 - L.disc_c) + 5000) / 10000;
