@@ -233,8 +233,11 @@ CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t c
  *   "fp_ctas_per_sm"  F.P. pattern's L: persistent fp_kernel CTAs per SM, 0 = adaptive (2/3/4 by batch
  *                     length), 1..16 (clamped to what fits an SM); env CDM_FP_CTAS_PER_SM sets the start value
  *   "lz4_lanes"       N.P. pattern's C: lanes cooperating on one LZ4 sub-chunk: 1 (the paper's thread per
- *                     chunk), 2, 4 (default), 8, 16 or 32 (one warp per sub-chunk); env CDM_LZ4_G /
- *                     CDM_LZ4_WARP set the start value
+ *                     chunk, lz4_thread_kernel), 2, 4, 8, 16 (lane groups) or 32 (one warp per sub-chunk);
+ *                     env CDM_LZ4_G sets the start value
+ *   "scan_mode"       H6 schedule (single-pass look-back vs the 2-pass baseline): 0 =
+ *                     reduce-then-scan (tile sums, then a persistent scan; default), 1 = single-pass decoupled
+ *                     look-back (one tile per CTA in ticket order); env CDM_SCAN_MODE sets the start value
  * Errors: CDM_E_INVALID_ARG for an unknown knob, a value outside its set, or a null pointer. */
 CDM_API cdm_status cdm_tune_set(const char *knob, int value);
 CDM_API cdm_status cdm_tune_get(const char *knob, int *value);

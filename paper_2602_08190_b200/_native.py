@@ -39,7 +39,7 @@ def _csrc(*names: str) -> list[str]:
     return [os.path.join(PKG, "csrc", n) for n in names]
 
 
-CUDA_SOURCES = ["runtime.cpp", "kernels_fp.cu", "kernels_scan.cu", "kernels_rle.cu", "kernels_lz4.cu", "kernels_ans.cu", "kernels_strdict.cu",
+CUDA_SOURCES = ["runtime.cpp", "kernels_fp.cu", "kernels_fpc.cu", "kernels_scan.cu", "kernels_rle.cu", "kernels_lz4.cu", "kernels_ans.cu", "kernels_strdict.cu",
                 "kernels_util.cu"]
 CUDA_HEADERS = ["format.h", "plan.h", "kernels.h", "device_util.cuh"]
 

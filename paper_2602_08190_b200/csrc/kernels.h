@@ -70,8 +70,9 @@ struct ScanBatch {
   uint32_t total_tiles;
   uint64_t* trace;               // CDM_TRACE: per-tile globaltimer stamps [tile][8], else null
   uint32_t* err;
-  unsigned long long* ticket;  // epoch|ticket counter
-  uint4* lb;                   // [total_tiles][3] look-back records: flag word, AGG values, INC values
+  unsigned long long* ticket;  // look-back mode: epoch|ticket counter
+  uint4* lb;                   // look-back mode: [total_tiles][3] records: flag word, AGG values, INC values
+  uint64_t* tsum;              // reduce-then-scan mode: [total_tiles] tile sums (scan_sums_kernel)
   ScanDesc d[kMaxBatch];
 };
 
@@ -246,6 +247,10 @@ struct SdBatch {
 
 // ---------------------------------------------------------------- launchers (return cudaGetLastError)
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);
+// CHAR(n) rows (FP_DICT, every descriptor of the batch with out_bytes == E): the row-group kernel
+// (kernels_fpc.cu) for the widths fpc_supported() names; launch_fp routes such batches there
+bool fpc_supported(uint32_t E);
+cudaError_t launch_fpc(const FpBatch& b, uint32_t E, cudaStream_t s);
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
 cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
@@ -274,7 +279,8 @@ cudaError_t launch_checksum(const void* p, uint64_t bytes, uint64_t chunk_id, ui
 // Process-wide; read by the launchers at enqueue time (a captured graph keeps the values it was built with).
 enum TuneKnob : int {
   TUNE_FP_CTAS_PER_SM = 0,  // F.P. "L": persistent fp_kernel CTAs per SM (0 = adaptive 2/3/4)
-  TUNE_LZ4_LANES = 1,       // N.P. "C": lanes per LZ4 sub-chunk: 4, 8, 16 (lane groups) or 32 (one warp)
+  TUNE_LZ4_LANES = 1,       // N.P. "C": lanes per LZ4 sub-chunk: 1 (thread per sub-chunk), 2..16 (lane groups), 32
+  TUNE_SCAN_MODE = 2,       // H6 schedule: 0 reduce-then-scan (tile sums + persistent scan), 1 decoupled look-back
   kTuneKnobs
 };
 int tune_get(int knob);

@@ -314,7 +314,8 @@ bool g_tune_init = false;
 void tune_init() {
   if (g_tune_init) return;
   g_tune[TUNE_FP_CTAS_PER_SM] = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 0;
-  g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_WARP") ? 32 : std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 4;
+  g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 4;
+  g_tune[TUNE_SCAN_MODE] = std::getenv("CDM_SCAN_MODE") ? std::atoi(std::getenv("CDM_SCAN_MODE")) : 0;
   g_tune_init = true;
 }
 }  // namespace
@@ -342,6 +343,13 @@ int device_sms() {
 
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
+  {  // CHAR(n) dictionary rows of one width: the row-group kernel
+    bool chr = b.n > 0;
+    const uint32_t E = b.n ? b.d[0].out_bytes : 0;
+    for (uint32_t i = 0; i < b.n && chr; i++) chr = b.d[i].mode == FP_DICT && b.d[i].out_bytes == E;
+    static const bool generic = std::getenv("CDM_FPC") && std::getenv("CDM_FPC")[0] == '0';
+    if (chr && E != 4 && E != 8 && fpc_supported(E) && !generic) return launch_fpc(b, E, s);
+  }
   const uint32_t stage = ((kFpTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words for extraction
   const uint32_t smem = 2 * stage;
   static const int dm = std::getenv("CDM_FP_DICT") && std::getenv("CDM_FP_DICT")[0] == 'l' ? 0 : 1;

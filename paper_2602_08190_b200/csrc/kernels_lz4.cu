@@ -262,209 +262,269 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __gr
   if (bad && gl == 0) atomicOr(B.err + D.err_idx, 0x4u);
 }
 
-// ------------------------------------------------------------------------------------------ smem decoder
-// Sub-chunks of <= kLz4SmemMax decompressed bytes are decoded into a per-warp shared-memory window: match
-// sources are then shared-memory reads instead of L2 round trips.  Each sequence is parsed from one
-// coalesced 32-byte window of the compressed stream held across the lanes (token, literals, offset
-// fetched with shuffles); long literal runs / extension bytes fall back to broadcast loads.  The finished
-// window is copied out with 16-byte stores: it is placed at byte offset (dst & 15) inside its buffer so
-// shared and global addresses share their alignment.
-constexpr uint32_t kLz4SmemMax = 32768;
+// ------------------------------------------------------------------------------------------ thread per sub-chunk
+// The paper's Non-Parallel schedule, one thread per chunk, built around the per-sub-chunk
+// latency chain: a sub-chunk's sequences decode one after another, so its decode time is
+// (sequences) x (latency per sequence), and a launch lasts as long as its slowest sub-chunk.  Per sequence this
+// kernel has at most one dependent global round trip (a far match source); everything else is shared memory:
+//  * the compressed stream is prefetched 16-byte block by block into a 64-byte per-thread input ring, two
+//    blocks ahead in registers (the loads are in flight while earlier sequences decode);
+//  * output bytes go to a 64-byte per-thread output ring indexed by global address bits; a completed 16-byte
+//    block of the global output leaves the ring with ONE 16-byte store (byte stores only at the sub-chunk's
+//    unaligned head and tail);
+//  * a literal run or match moves up to 16 bytes per step; match sources within 48 bytes come from the output
+//    ring, farther ones from global memory (three 8-byte loads in flight together), where the thread's own
+//    earlier 16-byte stores already are (same-thread program order).  An overlapping match (offset < 16)
+//    moves `offset` bytes per step, so every source byte precedes the bytes being written.
+// A warp instruction advances 32 sub-chunks (vs one per warp for lz4_kernel).
+constexpr uint32_t kLzRing = 64;   // ring bytes per thread (input and output each)
+constexpr uint32_t kLzNear = 48;   // match offsets up to this are read from the output ring
 
-__device__ __forceinline__ uint32_t ldb(const uint8_t* __restrict__ p) { return __ldg(p); }
+__device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the thread's own earlier stores)
+  uint2 v;
+  asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
 
-// A two-window reader over the compressed stream held across the warp's lanes: bytes [pos, pos+64) live in
-// (cur, nxt), one byte per lane each, and the window after them is already in flight (pre), so the next
-// sequence's bytes are usually a shuffle away.
-struct Lz4Reader {
-  const uint8_t* __restrict__ in;
-  uint32_t cl, pos;
-  uint32_t cur, nxt, pre;
-  __device__ __forceinline__ uint32_t load(uint32_t q, uint32_t lane) const {
-    return (q + lane < cl) ? uint32_t(__ldg(in + q + lane)) : 0u;
-  }
-  __device__ __forceinline__ void init(const uint8_t* p, uint32_t n, uint32_t lane) {
-    in = p; cl = n; pos = 0;
-    cur = load(0, lane); nxt = load(32, lane); pre = load(64, lane);
-  }
-  // make q < pos + 32 (q's byte and the 32 after it are resident)
-  __device__ __forceinline__ void advance(uint32_t q, uint32_t lane) {
-    while (q >= pos + 32) {
-      cur = nxt; nxt = pre; pos += 32;
-      pre = load(pos + 64, lane);
-    }
-  }
-  // byte at q (uniform across lanes), q in [pos, pos + 64)
-  __device__ __forceinline__ uint32_t at(uint32_t q) const {
-    const uint32_t d = q - pos;
-    const uint32_t a = __shfl_sync(FULL, cur, d & 31), b = __shfl_sync(FULL, nxt, d & 31);
-    return d < 32 ? a : b;
-  }
-  // per-lane byte at q + lane (q + 31 < pos + 64)
-  __device__ __forceinline__ uint32_t lane_at(uint32_t q, uint32_t lane) const {
-    const uint32_t d = q + lane - pos;
-    const uint32_t a = __shfl_sync(FULL, cur, d & 31), b = __shfl_sync(FULL, nxt, d & 31);
-    return d < 32 ? a : b;
-  }
-};
-
-__global__ void lz4_smem_kernel(const __grid_constant__ Lz4Batch B, uint32_t cap) {
-  extern __shared__ __align__(16) uint8_t lzbuf[];
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-  const uint32_t gs = blockIdx.x * wpc + wib;
-  if (gs >= B.total_subs) return;
-  const Lz4Desc& D = B.d[find_desc_lz4(B, gs)];
+__global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_thread_kernel(const __grid_constant__ Lz4Batch B) {
+  __shared__ __align__(16) uint8_t oring_s[kWarpsPerCta * 32 * kLzRing];
+  __shared__ __align__(16) uint8_t iring_s[kWarpsPerCta * 32 * kLzRing];
+  const uint32_t gs = blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31;
+  const bool live = gs < B.total_subs;
+  const Lz4Desc& D = B.d[find_desc_lz4(B, live ? gs : B.total_subs - 1)];
   const uint32_t s = gs - D.sub0;
   const uint32_t* tab = reinterpret_cast<const uint32_t*>(D.table);
   uint64_t off = 0;
   if (D.uniform) {
-    off = uint64_t(s) * D.uniform;  // host-verified uniform sub-chunk sizes
+    off = uint64_t(s) * D.uniform;
   } else {
-    for (uint32_t k = lane; k < s; k += 32) off += __ldg(tab + 3 * k + 2);
+    // sum of the preceding sub-chunks' lengths, the warp cooperating on each lane's sum in turn
+    const uint32_t act = __ballot_sync(FULL, live);
+    for (uint32_t L = 0; L < 32; L++) {
+      if (!(act >> L & 1u)) continue;
+      const uint32_t sL = __shfl_sync(FULL, s, L);
+      const uint64_t tL = __shfl_sync(FULL, reinterpret_cast<uint64_t>(tab), L);
+      const uint32_t uL = __shfl_sync(FULL, D.uniform, L);
+      uint64_t acc = 0;
+      if (!uL)
+        for (uint32_t k = lane; k < sL; k += 32) acc += __ldg(reinterpret_cast<const uint32_t*>(tL) + 3 * k + 2);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(FULL, off, o);
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+      if (lane == L && !uL) off = acc;
+    }
   }
+  if (!live) return;
   const uint32_t co = __ldg(tab + 3 * s), cl = __ldg(tab + 3 * s + 1), dl = __ldg(tab + 3 * s + 2);
-  bool bad = uint64_t(co) + cl > D.payload_bytes || off + dl > D.n || dl > cap;
+  bool bad = uint64_t(co) + cl > D.payload_bytes || off + dl > D.n;
   if (s + 1 == D.n_sub && off + dl != D.n) bad = true;
   if (bad) {
-    if (lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
+    atomicOr(B.err + D.err_idx, 0x4u);
     return;
   }
-  uint8_t* gdst = D.out + off;
-  const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(gdst) & 15);
-  uint8_t* win = lzbuf + wib * (cap + 16) + mis;
-  Lz4Reader R;
-  R.init(D.payload + co, cl, lane);
-  uint32_t ip = 0, op = 0;
-  for (;;) {
-    if (ip >= cl) { bad = true; break; }
-    R.advance(ip, lane);
-    const uint32_t token = R.at(ip);
-    uint32_t lit = token >> 4;
-    ip++;
+  uint8_t* const oring = oring_s + threadIdx.x * kLzRing;
+  uint8_t* const iring = iring_s + threadIdx.x * kLzRing;
+  const uint32_t* const orw = reinterpret_cast<const uint32_t*>(oring);
+  const uint32_t* const irw = reinterpret_cast<const uint32_t*>(iring);
+
+  // ---- compressed input: global addresses [ia0, ia0 + cl); 16-byte blocks below `ihave` are in the input
+  // ring (the last four of them), blocks ihave and ihave + 16 are in flight in nb0 / nb1
+  const uintptr_t ia0 = reinterpret_cast<uintptr_t>(D.payload + co);
+  // blocks at or past the stream's padded end (16-byte padding + 16 slack bytes) are never loaded
+  const uintptr_t istop = (reinterpret_cast<uintptr_t>(D.payload) + D.payload_bytes + 31) & ~uintptr_t(15);
+  auto ldblk = [&](uintptr_t a) -> uint4 {
+    return a < istop ? __ldg(reinterpret_cast<const uint4*>(a)) : make_uint4(0, 0, 0, 0);
+  };
+  uintptr_t ihave = ia0 & ~uintptr_t(15);
+  uint4 nb0 = ldblk(ihave), nb1 = ldblk(ihave + 16);
+  auto ensure = [&](uintptr_t end) {  // input bytes below `end` are in the ring
+    while (ihave < end) {
+      *reinterpret_cast<uint4*>(iring + (ihave & (kLzRing - 1))) = nb0;
+      nb0 = nb1;
+      nb1 = ldblk(ihave + 32);
+      ihave += 16;
+    }
+  };
+  auto in_u8 = [&](uint32_t p) -> uint32_t { return iring[(ia0 + p) & (kLzRing - 1)]; };
+  // 16 ring bytes from global address a (words q..q+4 of the ring, funnel-shifted)
+  auto ring16 = [&](const uint32_t* rw, uintptr_t a, uint32_t (&v)[4]) {
+    const uint32_t q = uint32_t(a >> 2), sh = uint32_t(a & 3u) * 8u;
+    uint32_t w[5];
+#pragma unroll
+    for (int i = 0; i < 5; i++) w[i] = rw[(q + i) & (kLzRing / 4 - 1)];
+#pragma unroll
+    for (int i = 0; i < 4; i++) v[i] = __funnelshift_r(w[i], w[i + 1], sh);
+  };
+
+  // ---- output: global addresses [ga0, ga0 + dl)
+  uint8_t* const out = D.out + off;
+  const uintptr_t ga0 = reinterpret_cast<uintptr_t>(out), ge = ga0 + dl;
+  auto flush = [&](uintptr_t blk) {  // block [blk, blk + 16) leaves the ring (bytes inside [ga0, ge) only)
+    const uint8_t* r = oring + (blk & (kLzRing - 1));
+    if (blk >= ga0 && blk + 16 <= ge) {
+      const uint4 v = *reinterpret_cast<const uint4*>(r);
+      st_v4_u32(reinterpret_cast<void*>(blk), v.x, v.y, v.z, v.w);
+    } else {
+      for (uint32_t b = 0; b < 16; b++)
+        if (blk + b >= ga0 && blk + b < ge) reinterpret_cast<uint8_t*>(blk)[b] = r[b];
+    }
+  };
+
+  // ---- one LZ4 sequence: header fields, parsed in two parts (head: token + literal length; tail: offset +
+  // match length), and a match source preloaded from global memory one sequence ahead
+  struct Seq {
+    uint32_t token, lit, lit_src, ipx, moff, ml;
+    bool last, tail, pre;
+    uint2 x0, x1, x2;
+  };
+  auto head = [&](uint32_t ip, Seq& q) -> bool {  // token + literal length at ip
+    ensure(ia0 + ip + 32);
+    if (ip >= cl) return false;
+    q.token = in_u8(ip++);
+    uint32_t lit = q.token >> 4;
     if (lit == 15) {
       uint32_t b;
       do {
-        if (ip >= cl) { bad = true; break; }
-        R.advance(ip, lane);
-        b = R.at(ip++);
+        if (ip >= cl) return false;
+        ensure(ia0 + ip + 1);
+        b = in_u8(ip++);
         lit += b;
       } while (b == 255);
-      if (bad) break;
     }
-    if (lit > cl - ip || lit > dl - op) { bad = true; break; }
-    // literals: 32 per step, from the reader's windows
-    for (uint32_t k = 0; k < lit; k += 32) {
-      R.advance(ip + k, lane);
-      const uint32_t v = R.lane_at(ip + k, lane);
-      if (k + lane < lit) win[op + k + lane] = uint8_t(v);
-    }
-    ip += lit;
-    op += lit;
-    if (ip == cl) break;  // the last sequence carries literals only
-    if (cl - ip < 2) { bad = true; break; }
-    R.advance(ip, lane);
-    const uint32_t moff = R.at(ip) | (R.at(ip + 1) << 8);
+    if (lit > cl - ip) return false;
+    q.lit = lit;
+    q.lit_src = ip;
+    q.ipx = ip + lit;
+    q.last = q.ipx == cl;  // the last sequence carries literals only
+    q.tail = q.pre = false;
+    return true;
+  };
+  auto tail = [&](Seq& q) -> bool {  // offset + match length after the literals
+    uint32_t ip = q.ipx;
+    if (cl - ip < 2) return false;
+    ensure(ia0 + ip + 2);
+    q.moff = in_u8(ip) | (in_u8(ip + 1) << 8);
     ip += 2;
-    if (moff == 0 || moff > op) { bad = true; break; }
-    uint32_t ml = token & 15;
+    if (q.moff == 0) return false;
+    uint32_t ml = q.token & 15;
     if (ml == 15) {
       uint32_t b;
       do {
-        if (ip >= cl) { bad = true; break; }
-        R.advance(ip, lane);
-        b = R.at(ip++);
+        if (ip >= cl) return false;
+        ensure(ia0 + ip + 1);
+        b = in_u8(ip++);
         ml += b;
       } while (b == 255);
-      if (bad) break;
     }
-    ml += 4;
-    if (ml > dl - op) { bad = true; break; }
-    __syncwarp();  // literal bytes written by other lanes are visible to the match copy
-    if (moff >= 32 || moff >= ml) {
-      for (uint32_t base = 0; base < ml; base += 32) {
-        const uint32_t k = base + lane;
-        if (k < ml) win[op + k] = win[op - moff + k];
-        __syncwarp();
-      }
-    } else {  // period moff < 32 and overlapping: out[op+k] = out[op - moff + (k mod moff)]
-      uint32_t m = lane % moff;
-      const uint32_t step = 32 % moff;
-      for (uint32_t base = 0; base < ml; base += 32) {
-        const uint32_t k = base + lane;
-        if (k < ml) win[op + k] = win[op - moff + m];
-        m += step;
-        if (m >= moff) m -= moff;
-      }
-      __syncwarp();
+    q.ml = ml + 4;
+    q.ipx = ip;
+    q.tail = true;
+    return true;
+  };
+  auto put16 = [&](uint32_t op, const uint32_t (&v)[4], uint32_t k) {  // k <= 16 bytes at output position op
+    const uintptr_t ga = ga0 + op;
+#pragma unroll
+    for (uint32_t b = 0; b < 16; b++)
+      if (b < k) oring[(ga + b) & (kLzRing - 1)] = uint8_t(v[b >> 2] >> (8 * (b & 3)));
+    if ((ga & 15u) + k >= 16u) flush(ga & ~uintptr_t(15));
+  };
+  auto far_load = [&](uintptr_t src, uint2& x0, uint2& x1, uint2& x2) {  // bytes [src & ~7, +24)
+    const uintptr_t a8 = src & ~uintptr_t(7);
+    x0 = ld_v2_global(reinterpret_cast<const void*>(a8));
+    x1 = ld_v2_global(reinterpret_cast<const void*>(a8 + 8));
+    x2 = ld_v2_global(reinterpret_cast<const void*>(a8 + 16));
+  };
+  auto far_words = [&](uintptr_t src, const uint2& x0, const uint2& x1, const uint2& x2, uint32_t (&v)[4]) {
+    const bool hi = (src & 4u) != 0;
+    const uint32_t sh = uint32_t(src & 3u) * 8u;
+    const uint32_t w0 = hi ? x0.y : x0.x, w1 = hi ? x1.x : x0.y, w2 = hi ? x1.y : x1.x, w3 = hi ? x2.x : x1.y,
+                   w4 = hi ? x2.y : x2.x;
+    v[0] = __funnelshift_r(w0, w1, sh);
+    v[1] = __funnelshift_r(w1, w2, sh);
+    v[2] = __funnelshift_r(w2, w3, sh);
+    v[3] = __funnelshift_r(w3, w4, sh);
+  };
+
+  uint32_t op = 0;
+  Seq T;
+  if (!head(0, T)) bad = true;
+  while (!bad) {
+    // ---- T's literals, 16 bytes per step from the input ring
+    if (T.lit > dl - op) { bad = true; break; }
+    for (uint32_t done = 0; done < T.lit;) {
+      const uint32_t k = min(16u, T.lit - done);
+      ensure(ia0 + T.lit_src + done + 16);
+      uint32_t v[4];
+      ring16(irw, ia0 + T.lit_src + done, v);
+      put16(op, v, k);
+      op += k;
+      done += k;
     }
-    op += ml;
+    if (T.last) break;
+    if (!T.tail && !tail(T)) { bad = true; break; }
+    if (T.moff > op || T.ml > dl - op) { bad = true; break; }
+    // ---- look ahead: the next sequence's header (short literal runs only, so its literal bytes stay in the
+    // input ring) and, for a far match whose first 16 source bytes are already flushed, its source loads --
+    // in flight while T's match completes
+    Seq N;
+    if (!head(T.ipx, N)) { bad = true; break; }
+    if (!N.last && N.lit <= 16 && (N.token & 15) != 15) {
+      if (!tail(N)) { bad = true; break; }
+      const uint32_t opm = op + T.ml + N.lit;  // N's match position
+      const uintptr_t flushed = (ga0 + op) & ~uintptr_t(15);
+      if (N.moff > kLzNear && N.moff <= opm && ga0 + opm - N.moff + 16 <= flushed) {
+        far_load(ga0 + opm - N.moff, N.x0, N.x1, N.x2);
+        N.pre = true;
+      }
+    }
+    // ---- T's match, up to 16 bytes (at most `moff`) per step
+    for (uint32_t done = 0; done < T.ml;) {
+      const uint32_t k = min(min(16u, T.ml - done), T.moff);
+      const uintptr_t src = ga0 + op - T.moff;
+      uint32_t v[4];
+      if (T.moff <= kLzNear) {
+        ring16(orw, src, v);
+      } else if (done == 0 && T.pre) {
+        far_words(src, T.x0, T.x1, T.x2, v);
+      } else {
+        uint2 x0, x1, x2;
+        far_load(src, x0, x1, x2);
+        far_words(src, x0, x1, x2, v);
+      }
+      put16(op, v, k);
+      op += k;
+      done += k;
+    }
+    T = N;
   }
   if (!bad && op != dl) bad = true;
   if (bad) {
-    if (lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
+    atomicOr(B.err + D.err_idx, 0x4u);
     return;
   }
-  __syncwarp();
-  // copy-out: unaligned head bytes, 16-byte body, tail bytes
-  const uint32_t head = min(dl, (16u - mis) & 15u);
-  if (lane < head) gdst[lane] = win[lane];
-  const uint32_t body = (dl - head) & ~15u;
-  for (uint32_t o = head + lane * 16; o < head + body; o += 32 * 16) {
-    const uint4 v = *reinterpret_cast<const uint4*>(win + o);
-    st_v4_u32(gdst + o, v.x, v.y, v.z, v.w);
-  }
-  const uint32_t t = head + body + lane;
-  if (t < dl) gdst[t] = win[t];
+  if (ge & 15u) flush(ge & ~uintptr_t(15));  // the partial last block
 }
 
 }  // namespace
 
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
+  (void)max_sub;
   if (!b.total_subs) return cudaSuccess;
-  // The shared-memory variant is opt-in (CDM_LZ4_SMEM=1): measured on config 3 (16 KiB sub-chunks) it is
-  // 2.5x slower than the global-memory kernel (12 vs 64 resident warps per SM; both are issue-bound).
-  static const bool use_smem = std::getenv("CDM_LZ4_SMEM") != nullptr;
-  if (max_sub <= kLz4SmemMax && use_smem) {
-    // warps per CTA such that 3 CTAs fit an SM's shared memory
-    const uint32_t cap = (max_sub + 15) & ~15u;
-    uint32_t wpc = 8;
-    while (wpc > 1 && 3ull * wpc * (cap + 16) > 220 * 1024) wpc >>= 1;
-    const uint32_t smem = wpc * (cap + 16);
-    static uint32_t configured[kMaxDevices] = {};
-    uint32_t& conf = configured[current_device()];
-    if (smem > 48 * 1024 && smem > conf) {
-      cudaFuncSetAttribute(lz4_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      conf = smem;
-    }
-    const uint32_t grid = (b.total_subs + wpc - 1) / wpc;
-    lz4_smem_kernel<<<grid, wpc * 32, smem, s>>>(b, cap);
+  // lanes per sub-chunk (NEXT-3 tuning knob TUNE_LZ4_LANES, env CDM_LZ4_G): 1 = the paper's thread per chunk
+  // (lz4_thread_kernel), 2/4/8/16 = lane groups, 32 = one warp per sub-chunk
+  const int G = tune_get(TUNE_LZ4_LANES);
+  if (G == 1) {
+    const uint32_t grid = (b.total_subs + kWarpsPerCta * 32 - 1) / (kWarpsPerCta * 32);
+    lz4_thread_kernel<<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();
   }
-  // lane groups of G lanes per sub-chunk (default 4: 8 sub-chunks per warp; G = 1 is the paper's thread per
-  // chunk); G = 32 is one warp per
-  // sub-chunk (tuning knob TUNE_LZ4_LANES; env CDM_LZ4_G / CDM_LZ4_WARP)
-  const int G = tune_get(TUNE_LZ4_LANES);
   if (G != 32) {
     const uint32_t per_cta = kWarpsPerCta * 32 / G;
     const uint32_t grid = (b.total_subs + per_cta - 1) / per_cta;
-    // window bytes per lane: 1 (default) or 4 (CDM_LZ4_WIN=4: a 16-byte window per 4-lane group -- measured
-    // 10.0 vs 9.5 ms on config 3's l_comment: the sequence chain is not bound by its compressed-byte loads)
-    static const bool win1 = !(std::getenv("CDM_LZ4_WIN") && std::getenv("CDM_LZ4_WIN")[0] == '4');
-    if (win1) {
-      if (G == 4) lz4_group_kernel<4, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else if (G == 1) lz4_group_kernel<1, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else if (G == 2) lz4_group_kernel<2, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else if (G == 16) lz4_group_kernel<16, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else lz4_group_kernel<8, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    } else {
-      if (G == 4) lz4_group_kernel<4, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else if (G == 1) lz4_group_kernel<1, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else if (G == 2) lz4_group_kernel<2, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else if (G == 16) lz4_group_kernel<16, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-      else lz4_group_kernel<8, 4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    }
+    if (G == 4) lz4_group_kernel<4, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else if (G == 2) lz4_group_kernel<2, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else if (G == 16) lz4_group_kernel<16, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else lz4_group_kernel<8, 1><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();
   }
   const uint32_t grid = (b.total_subs + kWarpsPerCta - 1) / kWarpsPerCta;

@@ -1,14 +1,25 @@
-// kernels_scan.cu -- H6: scan-dependent delta decode / VARCHAR offsets in ONE pass.
+// kernels_scan.cu -- H6: scan-dependent delta decode / VARCHAR offsets.
 //
-//   DELTA   out[i]   = base + sum_{k<=i} (FOR + bits_k)         (mod 2^bits)
-//   OFFSETS out[0] = 0, out[i+1] = sum_{k<=i} (FOR + bits_k)    (lengths -> int32 offsets, reading R17)
+//   DELTA   out[i] = base + sum_{k<=i} (FOR + bits_k)            (mod 2^bits)
+//   OFFSETS out[i] = sum_{k<i} (FOR + bits_k), out[n] = the total (lengths -> int32 offsets, reading R17)
 //
-// The paper decodes delta with PyTorch's cumsum as a separate pass.  Here the
-// unpack is fused into a single-pass decoupled look-back scan: one 4096-element tile
-// per CTA, tile order from an epoch|ticket counter (predecessors are always resident), the tile's
-// packed bytes staged by one TMA bulk copy, a blocked thread-local scan of 16 values, a CTA scan of
-// the thread totals, a warp-wide look-back over 32 predecessors at a time, then the results are
-// transposed through shared memory so every warp store is a contiguous 16-byte-per-lane write.
+// The paper decodes delta with PyTorch's cumsum as a separate pass.  Here the unpack is
+// fused into the scan, in one of two schedules (NEXT-3 knob TUNE_SCAN_MODE):
+//
+//  * reduce-then-scan (default): scan_sums_kernel writes every 4096-element tile's sum (one warp per tile,
+//    fully parallel: the packed stream is read once more, w/8 bytes per element); scan_kernel_rts is a
+//    persistent, programmatically dependent launch whose CTAs each walk a contiguous range of tiles with the
+//    next tile's packed bytes staged by the TMA engine (double buffer): the first tile's prefix is the sum of
+//    the chunk's tile sums before it, later tiles carry the running prefix.  No inter-CTA waits.
+//  * single-pass decoupled look-back: scan_kernel<true>, one tile per CTA in ticket order (epoch|ticket
+//    counter: no memset, CUDA-graph safe), warp 0 publishes the tile aggregate and looks back over 32
+//    predecessors at a time (device_util.cuh lb_tile).
+//
+// Both: a blocked thread-local scan of 16 values, a CTA scan of the thread totals, results transposed through
+// shared memory so every warp store is a contiguous 16-byte-per-lane write; offsets are the EXCLUSIVE scan,
+// aligned with the tile (16-byte stores), plus out[n] written by the chunk's last tile.
+#include <cstdlib>
+
 #include "device_util.cuh"
 #include "kernels.h"
 
@@ -28,17 +39,208 @@ __device__ __forceinline__ int find_desc_scan(const ScanBatch& B, uint32_t tile)
 
 constexpr int kPer = kScanTile / kThreads;  // 16 values per thread
 
-__global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ ScanBatch B) {
-  // one buffer: the staged packed tile, then (after the CTA scan) the transposed results
-  __shared__ __align__(128) uint64_t buf_s[(kScanTile * 8 + 32) / 8];
-  uint8_t* packed_s = reinterpret_cast<uint8_t*>(buf_s);
-  uint64_t* res_s = buf_s;
+__device__ __forceinline__ uint32_t scan_stage_bytes(const ScanDesc& D, uint64_t tile_start) {
+  const uint64_t stream_bytes = ((uint64_t(D.n) * D.w + 7) / 8 + 15) & ~15ull;
+  const uint64_t start = tile_start / 8 * D.w;
+  const uint64_t want = uint64_t(kScanTile / 8) * D.w;
+  const uint64_t have = stream_bytes > start ? stream_bytes - start : 0ull;
+  return uint32_t(want < have ? want : have);
+}
+
+// Tile sums for reduce-then-scan: one warp per tile, lane l sums the fields of elements l, l + 32, ... (adjacent
+// lanes read adjacent bits: coalesced).  Exact in u64 (the offsets check compares the chunk's total).
+__global__ void __launch_bounds__(kThreads) scan_sums_kernel(const __grid_constant__ ScanBatch B) {
+  grid_launch_dependents();  // scan_kernel's CTAs may be scheduled (they stage their first tile, then wait)
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gt = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (gt >= B.total_tiles) return;
+  const ScanDesc& D = B.d[find_desc_scan(B, gt)];
+  const uint32_t lt = gt - D.tile0, w = D.w;
+  const uint64_t tile_start = uint64_t(lt) * kScanTile;
+  const uint32_t valid = uint32_t(min(uint64_t(kScanTile), uint64_t(D.n) - tile_start));
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(D.packed + tile_start / 8 * w);
+  uint64_t acc = 0;
+  if (w && w <= 32) {
+    const uint32_t m = w == 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+    uint32_t part = 0;  // < 128 fields of < 2^25 ... summed in 64 bits below when w > 24
+#pragma unroll 8
+    for (uint32_t i = lane; i < valid; i += 32) {
+      const uint32_t b = i * w;
+      const uint32_t f = __funnelshift_r(__ldg(wd + (b >> 5)), __ldg(wd + (b >> 5) + 1), b & 31) & m;
+      if (w <= 24) part += f; else acc += f;
+    }
+    acc += part;
+  } else if (w) {
+    for (uint32_t i = lane; i < valid; i += 32) acc += extract_bits_global(wd, uint64_t(i) * w, w);
+  }
+  const uint32_t cnt = valid > lane ? (valid - lane + 31) / 32 : 0u;
+  acc += D.for_base * uint64_t(cnt);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if (lane == 0) B.tsum[gt] = acc;
+}
+
+// One tile: unpack + scan + prefix + transposed 16-byte stores.  T = uint32_t when every output of the launch is
+// 4 bytes (the values are needed mod 2^32 only: 32-bit arithmetic, the low 32 bits of each field), else
+// uint64_t.  LB: the prefix comes from the decoupled look-back (warp 0) and the chunk's LENGTHS check uses the
+// tile total; else `prefix` is the CTA's running prefix and `tsum_tile` this tile's exact sum (B.tsum).
+constexpr uint32_t kResPad = kScanTile + kScanTile / 16;  // results in shared memory, one pad slot per 16
+__device__ __forceinline__ uint32_t rpad(uint32_t i) { return i + (i >> 4); }
+
+template <bool LB, typename T>
+__device__ __forceinline__ void scan_tile(const ScanBatch& B, uint32_t gt, uint32_t epoch, const uint32_t* wd,
+                                          T* res_s, uint64_t* warp_s, uint64_t* prefix_s, uint64_t prefix,
+                                          uint64_t tsum_tile) {
+  constexpr bool W64 = sizeof(T) == 8;
+  const uint32_t tid = threadIdx.x;
+  const ScanDesc& D = B.d[find_desc_scan(B, gt)];
+  const uint32_t lt = gt - D.tile0, w = D.w;
+  const uint64_t tile_start = uint64_t(lt) * kScanTile;
+  const uint32_t valid = uint32_t(min(uint64_t(kScanTile), uint64_t(D.n) - tile_start));
+  const T fb = T(D.for_base);
+  const uint32_t m32 = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+
+  // blocked: thread t owns values [16t, 16t+16); v[j] = exclusive prefix within the thread
+  T v[kPer + 1];
+  T run = 0;
+  const uint32_t i0 = tid * kPer;
+  if (!W64 || w <= 32) {
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+      const uint32_t b = (i0 + j) * w;
+      const T f = (i0 + j < valid) ? fb + T(__funnelshift_r(wd[b >> 5], wd[(b >> 5) + 1], b & 31) & m32) : T(0);
+      v[j] = run;
+      run += f;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+      const T f = (i0 + j < valid) ? fb + T(extract_bits(wd, uint64_t(i0 + j) * w, w)) : T(0);
+      v[j] = run;
+      run += f;
+    }
+  }
+  v[kPer] = run;
+  trace_stamp(B.trace, gt, 1);
+  uint64_t tile_total;
+  const uint64_t texcl = block_excl_scan_u64<kThreads>(uint64_t(run), warp_s, &tile_total);
+  if (LB) {
+    if (tid < 32) {
+      uint64_t pc, p0;
+      lb_tile(B.lb, gt, D.tile0, epoch, 0, tile_total, &pc, &p0);
+      if (tid == 0) *prefix_s = p0;
+    }
+    __syncthreads();
+    prefix = *prefix_s;
+    tsum_tile = tile_total;
+  }
+  trace_stamp(B.trace, gt, 3);
+  if (tid == 0 && D.mode == SCAN_OFFSETS && lt + 1 == D.ntiles) {
+    if (prefix + tsum_tile != D.base) atomicOr(B.err + D.err_idx, 0x8u);  // CDM_ERR_LENGTHS
+    reinterpret_cast<int32_t*>(D.out)[D.n] = int32_t(uint32_t(prefix + tsum_tile));  // offsets[n]
+  }
+  // DELTA: out[i] = base + inclusive sum; OFFSETS: out[i] = exclusive sum
+  const bool delta = D.mode == SCAN_DELTA;
+  const T add = T((delta ? D.base : 0ull) + prefix + texcl);
+#pragma unroll
+  for (int j = 0; j < kPer; j++) res_s[rpad(i0 + j)] = add + (delta ? v[j + 1] : v[j]);
+  __syncthreads();
+  // striped: thread t stores values k*1024 + 4t .. +3 (16 or 32 contiguous bytes per lane, whole lines per warp)
+#pragma unroll
+  for (uint32_t k = 0; k < 4; k++) {
+    const uint32_t e0 = k * 1024 + tid * 4;
+    if (e0 >= valid) break;
+    const uint64_t gi = tile_start + e0;
+    const T r0 = res_s[rpad(e0)], r1 = res_s[rpad(e0 + 1)], r2 = res_s[rpad(e0 + 2)], r3 = res_s[rpad(e0 + 3)];
+    if (D.out_bytes == 8) {
+      uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
+      if (e0 + 4 <= valid) {
+        st_v2_u64(o, uint64_t(r0), uint64_t(r1));
+        st_v2_u64(o + 2, uint64_t(r2), uint64_t(r3));
+      } else {
+        const T r[4] = {r0, r1, r2, r3};
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++) if (e0 + j < valid) o[j] = uint64_t(r[j]);
+      }
+    } else {
+      uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
+      if (e0 + 4 <= valid) {
+        st_v4_u32(o, uint32_t(r0), uint32_t(r1), uint32_t(r2), uint32_t(r3));
+      } else {
+        const T r[4] = {r0, r1, r2, r3};
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++) if (e0 + j < valid) o[j] = uint32_t(r[j]);
+      }
+    }
+  }
+  __syncthreads();  // res_s and the staged tile are free
+  trace_stamp(B.trace, gt, 4);
+}
+
+// reduce-then-scan: persistent CTAs, each over a CONTIGUOUS range of tiles, the next tile's packed bytes staged by
+// the TMA engine while the current one is scanned.  A CTA needs the tile sums once for its first tile (the sum of
+// the chunk's tiles before it, block-reduced); after that the running prefix grows by each tile's sum (and
+// restarts at 0 at a chunk's first tile).
+template <typename T>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 3) scan_kernel_rts(const __grid_constant__ ScanBatch B, uint32_t stage_alloc) {
+  extern __shared__ __align__(128) uint8_t smem[];  // [2 x stage_alloc packed][kResPad x T results]
+  T* res_s = reinterpret_cast<T*>(smem + 2 * stage_alloc);
+  __shared__ uint64_t warp_s[kThreads / 32];
+  __shared__ __align__(8) uint64_t bar[2];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (B.total_tiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * per, t1 = min(B.total_tiles, t0 + per);
+  if (t0 >= t1) return;
+  auto stage = [&](uint32_t t, uint32_t s) {  // tid 0: TMA the packed bytes of tile t into stage s
+    const ScanDesc& D = B.d[find_desc_scan(B, t)];
+    const uint64_t tile_start = uint64_t(t - D.tile0) * kScanTile;
+    const uint32_t nb = scan_stage_bytes(D, tile_start);
+    fence_proxy_async();  // generic reads of this stage (two tiles ago) precede the TMA refill
+    mbar_arrive_expect_tx(&bar[s], nb);
+    if (nb) tma_load_1d(smem + s * stage_alloc, D.packed + tile_start / 8 * D.w, nb, &bar[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    stage(t0, 0);
+  }
+  __syncthreads();
+  grid_dependency_wait();  // scan_sums_kernel complete: the tile sums are valid
+  uint64_t prefix;
+  {
+    const ScanDesc& D = B.d[find_desc_scan(B, t0)];
+    uint64_t part = 0;
+    for (uint32_t k = D.tile0 + tid; k < t0; k += kThreads) part += B.tsum[k];
+    uint64_t tot;
+    block_excl_scan_u64<kThreads>(part, warp_s, &tot);
+    prefix = tot;
+  }
+  uint32_t it = 0;
+  uint64_t ts = B.tsum[t0];
+  for (uint32_t gt = t0; gt < t1; gt++, it++) {
+    const uint32_t s = it & 1;
+    if (tid == 0 && gt + 1 < t1) stage(gt + 1, s ^ 1);  // stage s^1 was freed by the previous tile
+    const uint64_t ts_next = gt + 1 < t1 ? B.tsum[gt + 1] : 0ull;  // in flight during this tile
+    trace_stamp(B.trace, gt, 0);
+    trace_stamp(B.trace, gt, 7);
+    if (gt == B.d[find_desc_scan(B, gt)].tile0) prefix = 0;  // a chunk's first tile
+    mbar_wait(&bar[s], (it >> 1) & 1);
+    scan_tile<false, T>(B, gt, 0, reinterpret_cast<const uint32_t*>(smem + s * stage_alloc), res_s, warp_s, nullptr,
+                        prefix, ts);
+    prefix += ts;
+    ts = ts_next;
+  }
+}
+
+// single-pass decoupled look-back: one tile per CTA, tiles in ticket order
+__global__ void __launch_bounds__(kThreads) scan_kernel_lb(const __grid_constant__ ScanBatch B) {
+  __shared__ __align__(128) uint64_t buf_s[kResPad + 4];  // the staged tile, then the results
   __shared__ uint64_t warp_s[kThreads / 32];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tile_s, epoch_s;
   __shared__ uint64_t prefix_s;
   const uint32_t tid = threadIdx.x;
-
   if (tid == 0) {
     uint32_t t, e;
     take_ticket(B.ticket, B.total_tiles - 1, &t, &e);
@@ -52,98 +254,67 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
   if (gt >= B.total_tiles) return;
   trace_stamp(B.trace, gt, 0);
   trace_stamp(B.trace, gt, 7);
-  const ScanDesc& D = B.d[find_desc_scan(B, gt)];
-  const uint32_t lt = gt - D.tile0;
-  const uint32_t w = D.w;
-  const uint64_t tile_start = uint64_t(lt) * kScanTile;
-  const uint32_t valid = uint32_t(min(uint64_t(kScanTile), uint64_t(D.n) - tile_start));
-
   if (tid == 0) {
-    const uint64_t stream_bytes = ((uint64_t(D.n) * w + 7) / 8 + 15) & ~15ull;
-    const uint64_t start = tile_start / 8 * w;
-    const uint64_t want = uint64_t(kScanTile / 8) * w;
-    const uint64_t have = stream_bytes > start ? stream_bytes - start : 0ull;
-    const uint32_t nb = uint32_t(want < have ? want : have);
+    const ScanDesc& D = B.d[find_desc_scan(B, gt)];
+    const uint64_t tile_start = uint64_t(gt - D.tile0) * kScanTile;
+    const uint32_t nb = scan_stage_bytes(D, tile_start);
     mbar_arrive_expect_tx(&bar, nb);
-    if (nb) tma_load_1d(packed_s, D.packed + start, nb, &bar);
+    if (nb) tma_load_1d(buf_s, D.packed + tile_start / 8 * D.w, nb, &bar);
   }
   mbar_wait(&bar, 0);
+  // the unpack reads the staged bytes into registers before the results overwrite the buffer (scan_tile's
+  // first barrier sits between the two)
+  scan_tile<true, uint64_t>(B, gt, epoch, reinterpret_cast<const uint32_t*>(buf_s), buf_s, warp_s, &prefix_s, 0, 0);
+}
 
-  // blocked: thread t owns values [16t, 16t+16)
-  const uint32_t* wd = reinterpret_cast<const uint32_t*>(packed_s);
-  uint64_t v[kPer];
-  uint64_t run = 0;
-#pragma unroll
-  for (int j = 0; j < kPer; j++) {
-    const uint32_t i = tid * kPer + j;
-    const uint64_t x = (i < valid) ? D.for_base + (w ? extract_bits(wd, uint64_t(i) * w, w) : 0ull) : 0ull;
-    run += x;
-    v[j] = run;  // inclusive within the thread
-  }
-  trace_stamp(B.trace, gt, 1);
-  uint64_t tile_total;
-  const uint64_t texcl = block_excl_scan_u64<kThreads>(run, warp_s, &tile_total);
-  trace_stamp(B.trace, gt, 2);
-
-  // decoupled look-back (warp 0)
-  if (tid < 32) {
-    uint64_t pc, p0;
-    lb_tile(B.lb, gt, D.tile0, epoch, 0, tile_total, &pc, &p0);
-    trace_stamp(B.trace, gt, 3);
-    if (tid == 0) {
-      prefix_s = p0;
-      if (D.mode == SCAN_OFFSETS && lt + 1 == D.ntiles && p0 + tile_total != D.base)
-        atomicOr(B.err + D.err_idx, 0x8u);  // lengths do not sum to the payload (CDM_ERR_LENGTHS)
-    }
-  }
-  __syncthreads();
-  const uint64_t add = (D.mode == SCAN_DELTA ? D.base : 0ull) + prefix_s + texcl;
-#pragma unroll
-  for (int j = 0; j < kPer; j++) res_s[tid * kPer + j] = add + v[j];
-  __syncthreads();
-
-  if (D.mode == SCAN_DELTA) {
-    // striped: thread t stores values k*1024 + 4t .. +3 (16 or 32 contiguous bytes per lane)
-#pragma unroll
-    for (uint32_t k = 0; k < 4; k++) {
-      const uint32_t i0 = k * 1024 + tid * 4;
-      if (i0 >= valid) break;
-      const uint64_t gi = tile_start + i0;
-      if (D.out_bytes == 8) {
-        uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + gi;
-        if (i0 + 4 <= valid) {
-          st_v2_u64(o, res_s[i0], res_s[i0 + 1]);
-          st_v2_u64(o + 2, res_s[i0 + 2], res_s[i0 + 3]);
-        } else {
-#pragma unroll
-          for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = res_s[i0 + j];
-        }
-      } else {
-        uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + gi;
-        if (i0 + 4 <= valid) {
-          st_v4_u32(o, uint32_t(res_s[i0]), uint32_t(res_s[i0 + 1]), uint32_t(res_s[i0 + 2]), uint32_t(res_s[i0 + 3]));
-        } else {
-#pragma unroll
-          for (uint32_t j = 0; j < 4; j++) if (i0 + j < valid) o[j] = uint32_t(res_s[i0 + j]);
-        }
-      }
-    }
-  } else {
-    // offsets[i+1] = inclusive sum; offsets[0] = 0 written by the chunk's first tile
-    int32_t* o = reinterpret_cast<int32_t*>(D.out) + tile_start + 1;
-    for (uint32_t i = tid; i < valid; i += kThreads) o[i] = int32_t(uint32_t(res_s[i]));
-    if (lt == 0 && tid == 0) reinterpret_cast<int32_t*>(D.out)[0] = 0;
-  }
-  __syncthreads();
-  trace_stamp(B.trace, gt, 4);
+bool pdl_on() {
+  static const bool pdl = !(std::getenv("CDM_PDL") && std::getenv("CDM_PDL")[0] == '0');
+  return pdl;
 }
 
 }  // namespace
 
 cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
-  scan_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
-  return cudaGetLastError();
+  if (tune_get(TUNE_SCAN_MODE) == 1) {
+    scan_kernel_lb<<<b.total_tiles, kThreads, 0, s>>>(b);
+    return cudaGetLastError();
+  }
+  scan_sums_kernel<<<(b.total_tiles + kThreads / 32 - 1) / (kThreads / 32), kThreads, 0, s>>>(b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  uint32_t max_w = 0;
+  bool w64 = false;  // some output of the launch is 8 bytes: 64-bit arithmetic
+  for (uint32_t i = 0; i < b.n; i++) {
+    max_w = std::max<uint32_t>(max_w, b.d[i].w);
+    w64 = w64 || b.d[i].out_bytes == 8;
+  }
+  const uint32_t stage = ((kScanTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words
+  const uint32_t smem = 2 * stage + kResPad * (w64 ? 8 : 4);
+  auto kern = w64 ? scan_kernel_rts<uint64_t> : scan_kernel_rts<uint32_t>;
+  static uint32_t configured[kMaxDevices][2] = {};
+  uint32_t& conf = configured[current_device()][w64];
+  if (smem > conf) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    conf = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint32_t grid = uint32_t(device_sms() * per_sm);
+  if (grid > b.total_tiles) grid = b.total_tiles;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, b, stage);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace cdm

@@ -610,7 +610,16 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (int j : fpj) (B->jobs[j].casc->dtype == T_FIXED ? fp_chr : fp_num).push_back(j);
   std::vector<std::vector<int>> fp_groups = groups(fp_num);
   const size_t n_num_groups = fp_groups.size();
-  for (auto& g : groups(fp_chr)) fp_groups.push_back(g);
+  {  // CHAR(n) launches hold one row width each (the row-group kernel is specialised on it)
+    std::vector<int> by_w(fp_chr);
+    std::stable_sort(by_w.begin(), by_w.end(), [&](int a, int c) { return B->jobs[a].W < B->jobs[c].W; });
+    for (size_t i = 0; i < by_w.size();) {
+      size_t k = i;
+      while (k < by_w.size() && B->jobs[by_w[k]].W == B->jobs[by_w[i]].W) k++;
+      for (auto& g : groups(std::vector<int>(by_w.begin() + i, by_w.begin() + k))) fp_groups.push_back(g);
+      i = k;
+    }
+  }
   for (size_t gi = 0; gi < fp_groups.size(); gi++) {
     const auto& g = fp_groups[gi];
     B->fp_char.push_back(gi >= n_num_groups);
@@ -640,6 +649,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     B->fp_maxw.push_back(maxw);
   }
   // scan (delta + VARBYTES offsets)
+  std::vector<uint32_t> scan_tiles;
   for (auto& g : groups(scj)) {
     ScanBatch sb{};
     sb.err = B->err_dev;
@@ -665,6 +675,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     sb.ticket = A.take<unsigned long long>(1);
     sb.lb = A.take<uint4>(size_t(tiles) * 3);  // per tile: flag word, AGG values, INC values
     B->scan.push_back(sb);
+    scan_tiles.push_back(tiles);
   }
   // RLE units: one per expansion level of each RLE job (deepest first).  A non-final level (the value lineage
   // of Delta|RLE or DeltaStride nodes) expands into an L2-resident u64 array that the job's next level reads as
@@ -767,7 +778,8 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     for (auto& pb : B->sums) pb.trace = A.take<uint64_t>(size_t(pb.total_units) * 8);
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
-  // ---- non-zeroed region: tile sums + prefixes per RLE unit, big-tile slots, lineage arrays
+  // ---- non-zeroed region: scan tile sums (reduce-then-scan), RLE tile sums + prefixes, big-tile slots, lineage
+  for (size_t i = 0; i < B->scan.size(); i++) B->scan[i].tsum = A.take<uint64_t>(scan_tiles[i]);
   for (size_t u = 0; u < units.size(); u++) {
     SumsChunk& d = B->sums[sums_at[u].first].d[sums_at[u].second];
     d.tsum = A.take<uint64_t>(size_t(d.tiles) * 2);
@@ -2045,6 +2057,9 @@ extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
     if (value != 1 && value != 2 && value != 4 && value != 8 && value != 16 && value != 32)
       return fail(CDM_E_INVALID_ARG, "lz4_lanes must be 1, 2, 4, 8, 16 or 32");
     cdm::tune_set(cdm::TUNE_LZ4_LANES, value);
+  } else if (k == "scan_mode") {
+    if (value != 0 && value != 1) return fail(CDM_E_INVALID_ARG, "scan_mode must be 0 (reduce-then-scan) or 1 (look-back)");
+    cdm::tune_set(cdm::TUNE_SCAN_MODE, value);
   } else {
     return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   }
@@ -2056,6 +2071,7 @@ extern "C" CDM_API cdm_status cdm_tune_get(const char* knob, int* value) {
   const std::string k(knob);
   if (k == "fp_ctas_per_sm") *value = cdm::tune_get(cdm::TUNE_FP_CTAS_PER_SM);
   else if (k == "lz4_lanes") *value = cdm::tune_get(cdm::TUNE_LZ4_LANES);
+  else if (k == "scan_mode") *value = cdm::tune_get(cdm::TUNE_SCAN_MODE);
   else return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   return CDM_OK;
 }

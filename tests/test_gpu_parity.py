@@ -226,8 +226,16 @@ def test_config1_parity(engine):
     check_parity(engine, "BitPack", config1_column())
 
 
+@pytest.fixture(params=[0, 1])
+def scan_mode(request):
+    """both H6 schedules (NEXT-3 knob scan_mode): 0 reduce-then-scan, 1 single-pass decoupled look-back"""
+    cdm.tune_set("scan_mode", request.param)
+    yield request.param
+    cdm.tune_set("scan_mode", 0)
+
+
 @pytest.mark.parametrize("w", [1, 3, 8, 17, 33, 64])
-def test_delta_scan_many_tiles(engine, w):
+def test_delta_scan_many_tiles(engine, w, scan_mode):
     rng = np.random.default_rng(w)
     n = 300_000
     d = rng.integers(0, 1 << min(w, 62), size=n, dtype=np.uint64).astype(np.int64)
@@ -404,19 +412,6 @@ def test_fp_pair_mapping_variant():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-def test_lz4_wide_window_variant():
-    """the opt-in 4-bytes-per-lane window (CDM_LZ4_WIN=4) decodes the same bytes (fresh process: env read once)"""
-    import subprocess
-    import sys
-    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
-            "from paper_2602_08190_b200.inputs import TPCH; e = cdm.Engine(0); "
-            "[t.check_parity(e, s, TPCH(0.01).column('l_comment'), rows_per_chunk=30_001, both=False) "
-            " for s in ('Str|[LZ4(sub=4096),BitPack]', 'Str|[LZ4,BitPack]')]; print('ok')")
-    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_LZ4_WIN": "4"}, capture_output=True,
-                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
-
-
 def test_lz4_overlapping_matches(engine, lz4_lanes):
     from test_oracle_pins import _seq
     blocks, sizes = [], []
@@ -476,6 +471,21 @@ def test_corrupt_run_sum_sets_error(engine):
 
 
 
+# CHAR(n) dictionary rows (reading R14): every row width E -- the row-group kernel's widths (1, 2, 3, 10, 15,
+# 25) and the generic byte path's (5, 7, 12, 31) -- with a tiny dictionary (shared-memory path), a large one
+# (o_clerk-like, read through L1/L2) and an out-of-range index free column; ragged tails across several tiles.
+@pytest.mark.parametrize("E", [1, 2, 3, 5, 7, 10, 12, 15, 25, 31])
+@pytest.mark.parametrize("entries", [3, 7, 2000])
+def test_char_rows_every_width(engine, E, entries):
+    rng = np.random.default_rng(E * 1000 + entries)
+    words = rng.integers(32, 127, size=(entries, E), dtype=np.uint8)
+    words = np.unique(words, axis=0)
+    n = 3 * 8192 + 777
+    data = words[rng.integers(0, words.shape[0], n)]
+    col = Column("chr", cdm1.FIXED, E, n, np.ascontiguousarray(data))
+    check_parity(engine, "Dict|BitPack", col, rows_per_chunk=20_011, both=False)
+
+
 # A single symbol owns the whole ANS table (f = 2^tl): each decode step is the identity, no renormalisation
 # word is read, and at tl = 12 the kernels decode it with tl = 11 (f = 2^12 does not fit their 12-bit f field).
 # Also a near-degenerate two-symbol mix (f = 2^tl - 1 and 1) that exercises the widest f the field holds.
@@ -506,7 +516,21 @@ def test_corrupt_ans_sets_error(engine, il):
         assert r["error_bits"] & 0x20, corrupt
 
 
-def test_corrupt_lz4_sets_error(engine):
+def test_varchar_offsets_scan_modes(engine, scan_mode):
+    """VARCHAR offsets (exclusive scan + offsets[n]) over many tiles and a ragged tail, both schedules; a chunk
+    whose lengths do not sum to its payload raises CDM_ERR_LENGTHS"""
+    col = TPCH(0.01).column("l_comment")
+    check_parity(engine, "Str|[LZ4,BitPack]", col, rows_per_chunk=40_961)
+    lens = [7] * 9000
+    n = sum(lens) + 1
+    spec = "Str|[Raw,BitPack]"
+    root = cdm1.Node(cdm1.STR, len(lens), [cdm1.raw(bytes(n)), cdm1.bitpack(lens, 3, 0)])
+    ch = cdm1.build(root, cdm1.VARBYTES, 1, len(lens), payload=n, cascade_hash=_hash(spec))
+    (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.VARBYTES), [ch], resident=True, expect_error=True)
+    assert r["error_bits"] & cdm.ERR_LENGTHS
+
+
+def test_corrupt_lz4_sets_error(engine, lz4_lanes):
     from test_oracle_pins import _seq
     spec = "Str|[LZ4,BitPack]"
     for blk, dl in [(_seq(b"ABCDEFGH", 9, 4) + _seq(b"", None, None), 12),

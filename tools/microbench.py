@@ -7,6 +7,10 @@ MEASURED_PEAKS copy peak).  Sweeps:
   E2  BitPack bit width w = 1..32, int32 output (uniform w-bit values)
   E3  RLE group-size distributions even-X / random-L-R / outlier-X-P / mixed, int64
   E7  fused vs decoded-twice: Dict|BitPack and Float2Int|BitPack (PAPER.md:565-588's fusion question)
+  CHR CHAR(n) dictionary rows: l_shipinstruct (25 B), l_shipmode (10), l_returnflag (1), o_orderpriority /
+      o_clerk (15), o_orderstatus (1)
+  SCAN H6 element-level Delta|BitPack / VARCHAR offsets: l_comment offsets, o_orderkey SF 100, config 1 sorted,
+      random walks w = 4..32 (per-kernel times reported for every case)
   NP  LZ4 sub-chunk size and ANS chunk size (PAPER.md:411-416's chunk-size trade-off)
 usage: python tools/microbench.py [sweeps] [--rows N] [--steps K]  -> JSON lines + a markdown table on stdout
 """
@@ -20,7 +24,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 from paper_2602_08190_b200 import cdm, encoder  # noqa: E402
-from paper_2602_08190_b200.inputs import I32, I64, TPCH, rle_column, uniform_bits_column  # noqa: E402
+from paper_2602_08190_b200.inputs import (I32, I64, TPCH, Column, config1_column, rle_column,  # noqa: E402
+                                          uniform_bits_column)
 
 CHUNK = 1 << 22
 
@@ -30,7 +35,12 @@ def peak():
     return float(json.load(open(p))["hbm_gbs"]) if os.path.exists(p) else 6650.0
 
 
+FILTER = None
+
+
 def run_case(eng, name, spec, col, steps, flush, stream):
+    if FILTER and FILTER not in name:
+        return None
     chunks = encoder.encode_chunks(spec, col, CHUNK)
     decs = []
     comp = dec = 0
@@ -57,12 +67,26 @@ def run_case(eng, name, spec, col, steps, flush, stream):
         e1.synchronize()
         tot += e0.elapsed_time(e1)
     res = b.results(stream, raise_on_error=False)
+    # every kernel timed alone (events around each launch, families serialised), after L2 flushes
+    b.set_timing(2)
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            b.launch(stream)
+        b.collect_timing()
+    b.results(stream, raise_on_error=False)
+    kt, kb = b.kernel_times(), b.kernel_bytes()
+    kern = {}
+    for k, (kms, n) in kt.items():
+        if n and kb.get(k):
+            per = kms / steps  # kernel_times sums over steps (a kind may launch several times per step)
+            kern[k] = {"ms": round(per, 4), "gbs": round(kb[k] / per / 1e6, 1), "frac": round(kb[k] / per / 1e6 / peak(), 3)}
     b.close()
     ms = tot / steps
     return {"case": name, "cascade": spec, "rows": col.rows, "decoded_mb": round(dec / 1e6, 1),
             "compressed_mb": round(comp / 1e6, 2), "cr": round(dec / comp, 2), "ms": round(ms, 4),
             "decoded_gbs": round(dec / ms / 1e6, 1), "eq1_frac": round((dec + comp) / ms / 1e6 / peak(), 3),
-            "errors": int(any(r["error_bits"] for r in res))}
+            "errors": int(any(r["error_bits"] for r in res)), "kernels": kern}
 
 
 def main():
@@ -70,7 +94,10 @@ def main():
     ap.add_argument("sweeps", nargs="*", default=["E2", "E3", "E7", "NP"])
     ap.add_argument("--rows", type=int, default=1 << 27)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--filter", default=None, help="only the cases whose name contains this")
     a = ap.parse_args()
+    global FILTER
+    FILTER = a.filter
     eng = cdm.Engine(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.Stream()
@@ -78,6 +105,8 @@ def main():
     rows = []
 
     def emit(r):
+        if r is None:
+            return
         rows.append(r)
         print(json.dumps(r), flush=True)
 
@@ -94,6 +123,25 @@ def main():
         for name, spec in (("l_quantity", "Dict|BitPack"), ("l_extendedprice", "Float2Int|BitPack"),
                            ("l_shipinstruct", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack")):
             emit(run_case(eng, f"E7 {name}", spec, g.column(name), a.steps, flush, stream))
+    if "CHR" in a.sweeps:  # CHAR(n) Dict|BitPack rows (reading R14), SF 10
+        g = TPCH(10.0)
+        for name in ("l_shipinstruct", "l_shipmode", "l_returnflag", "o_orderpriority", "o_clerk", "o_orderstatus"):
+            emit(run_case(eng, f"CHR {name}", "Dict|BitPack", g.column(name), a.steps, flush, stream))
+    if "SCAN" in a.sweeps:  # H6 element-level scans (SURVEY Sec. 8d "Extra sweeps")
+        g = TPCH(10.0)
+        emit(run_case(eng, "SCAN l_comment offsets", "Str|[LZ4(sub=16384),BitPack]", g.column("l_comment"), a.steps,
+                      flush, stream))
+        emit(run_case(eng, "SCAN o_orderkey SF100 Delta|BitPack", "Delta|BitPack", TPCH(100.0).column("o_orderkey"),
+                      a.steps, flush, stream))
+        c1 = config1_column(n)
+        c1s = Column("sorted", I32, 4, n, np.sort(c1.data))
+        emit(run_case(eng, "SCAN config1 sorted Delta|BitPack", "Delta|BitPack", c1s, a.steps, flush, stream))
+        rng = np.random.default_rng(5)
+        for w in (4, 8, 16, 32):
+            steps_w = rng.integers(-(1 << (w - 1)), 1 << (w - 1), size=n // 2, dtype=np.int64)
+            walk = np.cumsum(steps_w).astype(np.int64)
+            emit(run_case(eng, f"SCAN random walk w={w}", "Delta|BitPack", Column("walk", I64, 8, n // 2, walk), a.steps,
+                          flush, stream))
     if "NP" in a.sweeps:
         g = TPCH(10.0)
         com = g.column("l_comment")
