@@ -105,6 +105,10 @@ def parse():
     p.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
     p.add_argument("--sf", type=float, default=None, help="scale factor override")
     p.add_argument("--workers", type=int, default=None, help="generator/encoder processes per rank")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="torch.distributed backend for N>1 (gloo: the one-GPU multi-rank test)")
+    p.add_argument("--device-map", default="local", choices=["local", "zero"],
+                   help="local: rank -> cuda:LOCAL_RANK; zero: every rank on cuda:0 (tests on a single GPU)")
     a = p.parse_args()
     if a.sf is not None:
         WORKLOADS[a.workload]["sf"] = a.sf
@@ -320,9 +324,14 @@ def main():
     import torch.distributed as dist
     from paper_2602_08190_b200 import cdm
 
-    torch.cuda.set_device(local)
+    dev = local if args.device_map == "local" else 0
+    torch.cuda.set_device(dev)
+    coll = "cuda" if args.dist_backend == "nccl" else "cpu"  # device of the collectives' tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     # the column store moves into page-locked host memory (cudaHostAlloc through cdm_host_alloc: registering
     # the workers' shared mapping in place is refused by the driver on this VM)
     t0 = time.perf_counter()
@@ -353,7 +362,7 @@ def main():
 
     max_chunk = max(c.size for c in ds.chunks)
     slot = max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20))
-    eng = cdm.Engine(local, n_slots=4, slot_bytes=slot, order_policy=1)
+    eng = cdm.Engine(dev, n_slots=4, slot_bytes=slot, order_policy=1)
     cascs = [cdm.Cascade(spec, dt, w) for (_, spec, dt, w) in ds.columns]
     decs_dev, decs_host, views = [], [], []
     pos = 0
@@ -385,7 +394,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         for k in range(args.steps):
             t0 = time.perf_counter()
             ev[k][0].record(stream)
@@ -418,7 +427,7 @@ def main():
         err_bits |= r["error_bits"]
     dev_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
-    with ClockSampler(local) as dev_clocks:
+    with ClockSampler(dev) as dev_clocks:
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()                      # L2 flush (256 MiB write), outside the events
@@ -474,12 +483,12 @@ def main():
         for r in range(world):
             dist.barrier()
             v = measure_h2d(torch) if rank == r else 0.0
-            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            t = torch.tensor([v], dtype=torch.float64, device=coll)
             dist.all_reduce(t)
             h2d_each.append(round(float(t.item()), 1))
         dist.barrier()
         v = measure_h2d(torch)
-        t = torch.zeros(world, dtype=torch.float64, device="cuda")
+        t = torch.zeros(world, dtype=torch.float64, device=coll)
         t[rank] = v
         dist.all_reduce(t)
         h2d_conc = [round(float(x), 1) for x in t.tolist()]
@@ -488,11 +497,11 @@ def main():
     # ------------------------------------------------------------ reduce over ranks (metadata only)
     pipe_s, dev_s = pipe_ms / 1e3, dev_ms / 1e3
     if world > 1:
-        meta = torch.tensor([decoded, compressed, n_chunks, err_bits], dtype=torch.int64, device="cuda")
+        meta = torch.tensor([decoded, compressed, n_chunks, err_bits], dtype=torch.int64, device=coll)
         dist.all_reduce(meta, op=dist.ReduceOp.SUM)
-        cs = torch.tensor([checksum_total & 0xFFFFFFFF, checksum_total >> 32], dtype=torch.int64, device="cuda")
+        cs = torch.tensor([checksum_total & 0xFFFFFFFF, checksum_total >> 32], dtype=torch.int64, device=coll)
         dist.all_reduce(cs, op=dist.ReduceOp.SUM)  # 32-bit halves summed exactly, recombined mod 2^64
-        tmax = torch.tensor([pipe_s, e2e_s, dev_s], dtype=torch.float64, device="cuda")
+        tmax = torch.tensor([pipe_s, e2e_s, dev_s], dtype=torch.float64, device=coll)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tot_decoded, tot_comp, tot_chunks, tot_err = [int(x) for x in meta.tolist()]
         lo, hi = [int(x) for x in cs.tolist()]
@@ -539,8 +548,11 @@ def main():
             families[f] = {"ms_per_step": round(ms, 4), "algorithmic_bytes": b, "achieved_gbs": round(gbs, 1),
                            "frac": round(gbs / peak, 4)}
         dom = max(families, key=lambda f: families[f]["ms_per_step"])
-        kern_of = {"fp_numeric": "fp_kernel", "fp_char": "fp_kernel(char)", "scan": "scan_kernel",
-                   "rle_chain": "rle_sums_kernel+rle_kernel(+level0, rle_big_kernel)", "lz4": "lz4_group_kernel",
+        lanes = cdm.tune_get("lz4_lanes")
+        kern_of = {"fp_numeric": "fp_kernel", "fp_char": "fpc_kernel (CHAR(n) row groups)",
+                   "scan": "scan_sums_kernel+scan_kernel_rts" if cdm.tune_get("scan_mode") == 0 else "scan_kernel_lb",
+                   "rle_chain": "rle_sums_kernel+rle_kernel(+level0, rle_big_kernel)",
+                   "lz4": "lz4_thread_kernel" if lanes == 1 else "lz4_kernel" if lanes == 32 else "lz4_group_kernel",
                    "ans": "ans_warp_kernel", "strdict": "sd_sums+sd_scan+sd_expand", "copy": "cudaMemcpyAsync D2D"}
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")

@@ -21,11 +21,17 @@
  *    lengths not summing to the row count, LZ4 offsets/lengths out of bounds) are reported by
  *    cdm_wait / cdm_batch_results as CDM_E_CORRUPT with cdm_result.error_bits set.  Kernels never
  *    read or write out of bounds, even on corrupt input.
+ *  - Ordering: the engine's copy/decode streams are non-blocking with respect to the legacy default stream.
+ *    Writes the caller makes to dev_out / dev_offsets / dev_chunk (e.g. torch fills on the default stream)
+ *    must be complete, or ordered before the launch stream passed in, when a job is submitted or launched;
+ *    results are ready after cdm_wait / cdm_batch_results / cdm_pipeline_results or cdm_ticket_event.
  *  - cdm_last_error() returns a thread-local human-readable detail of the last failing call.
  *  - Chunks are CDM1 containers: self-contained row groups of
  *    < 2^31 rows, little-endian, 16-byte aligned zero-padded streams.
- *  - Threading: one engine per (process, device).  An engine is NOT thread-safe: serialise calls on
- *    one engine.  Cascades are immutable and may be shared by engines and threads.
+ *  - Threading: one engine per (process, device).  cdm_submit, cdm_submit_batch, cdm_wait, cdm_ticket_event
+ *    and cdm_synchronize are thread-safe on one engine (serialised by an engine mutex; a wait blocks with the
+ *    mutex released).  Batches and pipelines are single-threaded objects.  Cascades are immutable and may be
+ *    shared by engines and threads.
  */
 #ifndef CDM_H
 #define CDM_H
@@ -89,8 +95,13 @@ typedef struct {
                              other kernel families are costed at fixed fractions of it measured on B200
                              (scan 1/2, RLE 1/8, LZ4 1/40, raw copy 1) */
   uint32_t order_policy;  /* 0 = submission order, 1 = Johnson's rule */
-  uint32_t reserved;
+  uint32_t flags;         /* CDM_ENGINE_* */
 } cdm_engine_opts;
+
+/* cdm_engine_opts.flags: compute the H9 positional checksum of every chunk decoded through cdm_submit* on the
+ * device, after its decode (cdm_result.checksum): h = sum over the 8-byte words k of the zero-padded payload of
+ * splitmix64(chunk_id ^ k ^ word_k) mod 2^64, plus the same over the offsets under chunk_id ^ 2^63. */
+#define CDM_ENGINE_CHECKSUM 0x1u
 
 typedef struct {
   uint64_t rows;              /* rows decoded */
@@ -100,6 +111,7 @@ typedef struct {
   uint64_t chunk_id;          /* from the chunk header */
   uint32_t error_bits;        /* CDM_ERR_* found on the device, 0 if clean */
   uint32_t status;            /* cdm_status of this chunk */
+  uint64_t checksum;          /* H9 checksum of the decoded chunk (engines created with CDM_ENGINE_CHECKSUM), else 0 */
 } cdm_result;
 
 typedef struct {
@@ -145,6 +157,11 @@ CDM_API cdm_status cdm_submit(cdm_engine *e, const cdm_job *job, uint64_t *ticke
 CDM_API cdm_status cdm_submit_batch(cdm_engine *e, const cdm_job *jobs, size_t n, uint64_t *tickets);
 /* Block until the ticket's decode finished; fills *out.  CDM_E_CORRUPT if error_bits != 0. */
 CDM_API cdm_status cdm_wait(cdm_engine *e, uint64_t ticket, cdm_result *out);
+/* A CUDA event (cudaEvent_t, owned by the engine) that completes when the ticket's decode (and its checksum)
+ * has finished, so a consumer stream can cudaStreamWaitEvent on it without a host synchronisation
+ * (SURVEY Sec. 8b).  Valid until the ticket is consumed by cdm_wait; for a ticket whose group was already
+ * harvested it is an event that has completed.  Errors: CDM_E_INVALID_ARG, CDM_E_BUSY (unknown ticket). */
+CDM_API cdm_status cdm_ticket_event(cdm_engine *e, uint64_t ticket, void **cuda_event);
 /* Wait for everything submitted so far (results stay retrievable with cdm_wait). */
 CDM_API cdm_status cdm_synchronize(cdm_engine *e);
 /* H3 as a pure host function: Johnson's rule over jobs with transfer costs t[i] and
@@ -232,8 +249,8 @@ CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t c
  * Process-wide, read when a batch / pipeline is enqueued or captured (a captured graph keeps its values).
  *   "fp_ctas_per_sm"  F.P. pattern's L: persistent fp_kernel CTAs per SM, 0 = adaptive (2/3/4 by batch
  *                     length), 1..16 (clamped to what fits an SM); env CDM_FP_CTAS_PER_SM sets the start value
- *   "lz4_lanes"       N.P. pattern's C: lanes cooperating on one LZ4 sub-chunk: 1 (the paper's thread per
- *                     chunk, lz4_thread_kernel), 2, 4, 8, 16 (lane groups) or 32 (one warp per sub-chunk);
+ *   "lz4_lanes"       N.P. pattern's C: lanes cooperating on one LZ4 sub-chunk: 1 (default: the paper's thread
+ *                     per chunk, lz4_thread_kernel), 2, 4, 8, 16 (lane groups) or 32 (one warp per sub-chunk);
  *                     env CDM_LZ4_G sets the start value
  *   "scan_mode"       H6 schedule (single-pass look-back vs the 2-pass baseline): 0 =
  *                     reduce-then-scan (tile sums, then a persistent scan; default), 1 = single-pass decoupled

@@ -25,7 +25,7 @@ KERNELS = ["fp_kernel", "scan_kernel", "rle_sums_kernel", "rle_kernel(level0)", 
 
 SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_create", "cdm_cascade_destroy",
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
-           "cdm_submit_batch", "cdm_wait", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
+           "cdm_submit_batch", "cdm_wait", "cdm_ticket_event", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
            "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times", "cdm_batch_kernel_bytes",
            "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy",
@@ -36,13 +36,16 @@ SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_creat
 class EngineOpts(ctypes.Structure):
     _fields_ = [("n_slots", ctypes.c_uint32), ("slot_bytes", ctypes.c_uint64), ("copy_stream", ctypes.c_void_p),
                 ("decode_stream", ctypes.c_void_p), ("pcie_gbps", ctypes.c_double), ("decode_gbps", ctypes.c_double),
-                ("order_policy", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("order_policy", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
+
+
+ENGINE_CHECKSUM = 0x1  # cdm_engine_opts.flags: H9 checksum of every submitted chunk in cdm_result.checksum
 
 
 class Result(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_uint64), ("payload_bytes", ctypes.c_uint64), ("offsets_bytes", ctypes.c_uint64),
                 ("compressed_bytes", ctypes.c_uint64), ("chunk_id", ctypes.c_uint64), ("error_bits", ctypes.c_uint32),
-                ("status", ctypes.c_uint32)]
+                ("status", ctypes.c_uint32), ("checksum", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -86,6 +89,7 @@ def lib():
         "cdm_submit_batch": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(u64)],
         "cdm_wait": [vp, u64, ctypes.POINTER(Result)],
         "cdm_synchronize": [vp],
+        "cdm_ticket_event": [vp, u64, ctypes.POINTER(vp)],
         "cdm_johnson_order": [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), sz,
                               ctypes.POINTER(sz)],
         "cdm_batch_create": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(vp)],
@@ -229,9 +233,10 @@ class Engine:
     """cdm_engine_create: staging ring + copy/decode streams on one device."""
 
     def __init__(self, device: int = 0, n_slots: int = 4, slot_bytes: int = 64 << 20, copy_stream=None,
-                 decode_stream=None, order_policy: int = 1, pcie_gbps: float = 55.0, decode_gbps: float = 5000.0):
+                 decode_stream=None, order_policy: int = 1, pcie_gbps: float = 55.0, decode_gbps: float = 5000.0,
+                 checksum: bool = False):
         o = EngineOpts(n_slots, slot_bytes, _stream_ptr(copy_stream), _stream_ptr(decode_stream), pcie_gbps,
-                       decode_gbps, order_policy, 0)
+                       decode_gbps, order_policy, ENGINE_CHECKSUM if checksum else 0)
         h = ctypes.c_void_p()
         _check(lib().cdm_engine_create(device, ctypes.byref(o), ctypes.byref(h)))
         self.h = h
@@ -264,6 +269,12 @@ class Engine:
         if rc and (raise_on_error or rc != 4):
             _check(rc)
         return r.as_dict()
+
+    def ticket_event(self, ticket: int) -> int:
+        """cdm_ticket_event: the cudaEvent_t (as an int handle) completing with the ticket's decode."""
+        ev = ctypes.c_void_p()
+        _check(lib().cdm_ticket_event(self.h, ticket, ctypes.byref(ev)))
+        return ev.value or 0
 
     def synchronize(self) -> None:
         _check(lib().cdm_synchronize(self.h))

@@ -41,29 +41,27 @@ __device__ __forceinline__ uint32_t stage_bytes(const FpDesc& D, uint32_t lt) {
 
 constexpr uint32_t kDictSmemBytes = 8192;  // dictionaries up to this size are gathered from shared memory
 
-// DM: dictionary gathers from shared memory (1: the tile's dictionary is copied there when the tile's
-// chunk changes) or through the read-only L1 path (0).
-// TMA: the tile's packed bytes are staged in shared memory by the TMA engine, double-buffered across the
-// tiles of a persistent CTA (1), or read in place through L1 by each thread, one tile per CTA (0).
-template <int DM, bool TMA>
+// Dictionaries up to kDictSmemBytes are gathered from shared memory (copied there when the tile's chunk
+// changes), larger ones through the read-only L1 path; the tile's packed bytes are staged in shared memory by
+// the TMA engine, double-buffered across the tiles of a persistent CTA.
 __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__ FpBatch B, uint32_t stage_bytes_alloc) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ __align__(16) uint64_t dict_s[DM == 1 ? kDictSmemBytes / 8 : 2];
+  __shared__ __align__(16) uint64_t dict_s[kDictSmemBytes / 8];
   int staged_di = -1;
   const uint32_t tid = threadIdx.x;
   // stage_bytes_alloc: set by the host from the batch's largest w; dynamic smem = 2 stages
 
-  if (TMA && tid == 0) {
+  if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  if (TMA) __syncthreads();
+  __syncthreads();
 
   uint32_t tile = blockIdx.x;
   // prologue: stage the first tile
-  if (TMA && tid == 0 && tile < B.total_tiles) {
+  if (tid == 0 && tile < B.total_tiles) {
     const int di = find_desc_fp(B, tile);
     const FpDesc& D = B.d[di];
     const uint32_t lt = tile - D.tile0;
@@ -74,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
   for (uint32_t it = 0; tile < B.total_tiles; it++, tile += gridDim.x) {
     const uint32_t s = it & 1;
     const uint32_t next = tile + gridDim.x;
-    if (TMA && tid == 0 && next < B.total_tiles) {  // stage s^1 was released by the __syncthreads ending it-1
+    if (tid == 0 && next < B.total_tiles) {  // stage s^1 was released by the __syncthreads ending it-1
       const int dn = find_desc_fp(B, next);
       const FpDesc& Dn = B.d[dn];
       const uint32_t ltn = next - Dn.tile0;
@@ -92,16 +90,15 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     const uint64_t base = D.base;
     const uint8_t* const dict8 = D.dict;
     uint8_t* const out8 = reinterpret_cast<uint8_t*>(D.out);
-    if (TMA) mbar_wait(&bar[s], (it >> 1) & 1);
-    const uint32_t* wd = TMA ? reinterpret_cast<const uint32_t*>(smem + s * stage_bytes_alloc)
-                             : reinterpret_cast<const uint32_t*>(D.packed + uint64_t(lt) * (kFpTile / 8) * w);
+    mbar_wait(&bar[s], (it >> 1) & 1);
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(smem + s * stage_bytes_alloc);
     const uint64_t tile_start = uint64_t(lt) * kFpTile;
     const uint32_t valid = uint32_t(min(uint64_t(kFpTile), uint64_t(D.n) - tile_start));
     bool bad_index = false;
     const bool pair_map = B.pair_map;
     const bool bytes_path = mode == FP_DICT && ob != 4 && ob != 8;  // CHAR(n) rows
-    const bool dsm = DM == 1 && mode == FP_DICT && !bytes_path && entries * ob <= kDictSmemBytes;
-    const bool dsmb = DM == 1 && bytes_path && uint64_t(entries) * ob + 8 <= kDictSmemBytes;
+    const bool dsm = mode == FP_DICT && !bytes_path && entries * ob <= kDictSmemBytes;
+    const bool dsmb = bytes_path && uint64_t(entries) * ob + 8 <= kDictSmemBytes;
     if ((dsm || dsmb) && di != staged_di) {  // uniform: every thread passed the barrier ending the previous tile
       const uint4* src = reinterpret_cast<const uint4*>(dict8);
       for (uint32_t q = tid; q < (entries * ob + 15) / 16; q += kThreads) reinterpret_cast<uint4*>(dict_s)[q] = __ldg(src + q);
@@ -314,7 +311,7 @@ bool g_tune_init = false;
 void tune_init() {
   if (g_tune_init) return;
   g_tune[TUNE_FP_CTAS_PER_SM] = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 0;
-  g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 4;
+  g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 1;
   g_tune[TUNE_SCAN_MODE] = std::getenv("CDM_SCAN_MODE") ? std::atoi(std::getenv("CDM_SCAN_MODE")) : 0;
   g_tune_init = true;
 }
@@ -352,13 +349,10 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   }
   const uint32_t stage = ((kFpTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words for extraction
   const uint32_t smem = 2 * stage;
-  static const int dm = std::getenv("CDM_FP_DICT") && std::getenv("CDM_FP_DICT")[0] == 'l' ? 0 : 1;
-  static const bool tma = !(std::getenv("CDM_FP_TMA") && std::getenv("CDM_FP_TMA")[0] == '0');
-  auto kern = tma ? (dm ? fp_kernel<1, true> : fp_kernel<0, true>) : (dm ? fp_kernel<1, false> : fp_kernel<0, false>);
-  static uint32_t configured[kMaxDevices][4] = {};
-  const int ci = dm + 2 * tma;
-  uint32_t& conf = configured[current_device()][ci];
-  if (tma && smem > 40 * 1024 && smem > conf) {
+  auto kern = fp_kernel;
+  static uint32_t configured[kMaxDevices] = {};
+  uint32_t& conf = configured[current_device()];
+  if (smem > 40 * 1024 && smem > conf) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     conf = smem;
   }
@@ -373,7 +367,6 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   const int cap = cap_env > 0 ? cap_env : tiles_per_sm >= 32 ? 4 : tiles_per_sm >= 20 ? 3 : 2;
   if (cap < per_sm) per_sm = cap;
   uint32_t grid = uint32_t(device_sms() * per_sm);
-  if (!tma) grid = b.total_tiles;  // one tile per CTA, read in place
   // CDM_FP_GRID=tiles: one CTA per tile (no persistence), so CTAs of a concurrent higher-priority family
   // are scheduled as soon as any FP CTA retires
   static const bool per_tile = std::getenv("CDM_FP_GRID") && std::getenv("CDM_FP_GRID")[0] == 't';
@@ -385,9 +378,9 @@ cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s) {
   if (b.pair_map != uint32_t(pair)) {
     FpBatch c = b;
     c.pair_map = pair;
-    kern<<<grid, kThreads, tma ? smem : 0, s>>>(c, stage);
+    kern<<<grid, kThreads, smem, s>>>(c, stage);
   } else {
-    kern<<<grid, kThreads, tma ? smem : 0, s>>>(b, stage);
+    kern<<<grid, kThreads, smem, s>>>(b, stage);
   }
   return cudaGetLastError();
 }

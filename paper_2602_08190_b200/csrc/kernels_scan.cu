@@ -88,12 +88,11 @@ constexpr uint32_t kResPad = kScanTile + kScanTile / 16;  // results in shared m
 __device__ __forceinline__ uint32_t rpad(uint32_t i) { return i + (i >> 4); }
 
 template <bool LB, typename T>
-__device__ __forceinline__ void scan_tile(const ScanBatch& B, uint32_t gt, uint32_t epoch, const uint32_t* wd,
-                                          T* res_s, uint64_t* warp_s, uint64_t* prefix_s, uint64_t prefix,
-                                          uint64_t tsum_tile) {
+__device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D, uint32_t gt, uint32_t epoch,
+                                          const uint32_t* wd, T* res_s, uint64_t* warp_s, uint64_t* prefix_s,
+                                          uint64_t prefix, uint64_t tsum_tile) {
   constexpr bool W64 = sizeof(T) == 8;
   const uint32_t tid = threadIdx.x;
-  const ScanDesc& D = B.d[find_desc_scan(B, gt)];
   const uint32_t lt = gt - D.tile0, w = D.w;
   const uint64_t tile_start = uint64_t(lt) * kScanTile;
   const uint32_t valid = uint32_t(min(uint64_t(kScanTile), uint64_t(D.n) - tile_start));
@@ -105,12 +104,22 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, uint32_t gt, uint3
   T run = 0;
   const uint32_t i0 = tid * kPer;
   if (!W64 || w <= 32) {
+    // a two-word bit window slides over the thread's 16 fields (one shared load per 32 bits consumed)
+    uint32_t q = (i0 * w) >> 5, sh = (i0 * w) & 31;
+    uint32_t lo = wd[q], hi = wd[q + 1];
+    const bool full = valid == kScanTile;
 #pragma unroll
     for (int j = 0; j < kPer; j++) {
-      const uint32_t b = (i0 + j) * w;
-      const T f = (i0 + j < valid) ? fb + T(__funnelshift_r(wd[b >> 5], wd[(b >> 5) + 1], b & 31) & m32) : T(0);
+      const uint32_t f = __funnelshift_r(lo, hi, sh) & m32;
       v[j] = run;
-      run += f;
+      run += (full || i0 + j < valid) ? fb + T(f) : T(0);
+      sh += w;
+      if (sh >= 32) {
+        sh -= 32;
+        q++;
+        lo = hi;
+        hi = wd[q + 1];
+      }
     }
   } else {
 #pragma unroll
@@ -121,7 +130,6 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, uint32_t gt, uint3
     }
   }
   v[kPer] = run;
-  trace_stamp(B.trace, gt, 1);
   uint64_t tile_total;
   const uint64_t texcl = block_excl_scan_u64<kThreads>(uint64_t(run), warp_s, &tile_total);
   if (LB) {
@@ -134,7 +142,6 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, uint32_t gt, uint3
     prefix = *prefix_s;
     tsum_tile = tile_total;
   }
-  trace_stamp(B.trace, gt, 3);
   if (tid == 0 && D.mode == SCAN_OFFSETS && lt + 1 == D.ntiles) {
     if (prefix + tsum_tile != D.base) atomicOr(B.err + D.err_idx, 0x8u);  // CDM_ERR_LENGTHS
     reinterpret_cast<int32_t*>(D.out)[D.n] = int32_t(uint32_t(prefix + tsum_tile));  // offsets[n]
@@ -174,7 +181,6 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, uint32_t gt, uint3
     }
   }
   __syncthreads();  // res_s and the staged tile are free
-  trace_stamp(B.trace, gt, 4);
 }
 
 // reduce-then-scan: persistent CTAs, each over a CONTIGUOUS range of tiles, the next tile's packed bytes staged by
@@ -191,8 +197,12 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 3) scan_kernel_
   const uint32_t per = (B.total_tiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * per, t1 = min(B.total_tiles, t0 + per);
   if (t0 >= t1) return;
+  // the descriptor of a tile: the CTA's tiles are contiguous, so the index only moves forward
+  int di = find_desc_scan(B, t0);
+  int sdi = di;  // the staging cursor (one tile ahead)
   auto stage = [&](uint32_t t, uint32_t s) {  // tid 0: TMA the packed bytes of tile t into stage s
-    const ScanDesc& D = B.d[find_desc_scan(B, t)];
+    while (sdi + 1 < int(B.n) && B.d[sdi + 1].tile0 <= t) sdi++;
+    const ScanDesc& D = B.d[sdi];
     const uint64_t tile_start = uint64_t(t - D.tile0) * kScanTile;
     const uint32_t nb = scan_stage_bytes(D, tile_start);
     fence_proxy_async();  // generic reads of this stage (two tiles ago) precede the TMA refill
@@ -209,9 +219,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 3) scan_kernel_
   grid_dependency_wait();  // scan_sums_kernel complete: the tile sums are valid
   uint64_t prefix;
   {
-    const ScanDesc& D = B.d[find_desc_scan(B, t0)];
     uint64_t part = 0;
-    for (uint32_t k = D.tile0 + tid; k < t0; k += kThreads) part += B.tsum[k];
+    for (uint32_t k = B.d[di].tile0 + tid; k < t0; k += kThreads) part += B.tsum[k];
     uint64_t tot;
     block_excl_scan_u64<kThreads>(part, warp_s, &tot);
     prefix = tot;
@@ -222,12 +231,12 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 3) scan_kernel_
     const uint32_t s = it & 1;
     if (tid == 0 && gt + 1 < t1) stage(gt + 1, s ^ 1);  // stage s^1 was freed by the previous tile
     const uint64_t ts_next = gt + 1 < t1 ? B.tsum[gt + 1] : 0ull;  // in flight during this tile
-    trace_stamp(B.trace, gt, 0);
-    trace_stamp(B.trace, gt, 7);
-    if (gt == B.d[find_desc_scan(B, gt)].tile0) prefix = 0;  // a chunk's first tile
+    while (di + 1 < int(B.n) && B.d[di + 1].tile0 <= gt) di++;
+    const ScanDesc& D = B.d[di];
+    if (gt == D.tile0) prefix = 0;  // a chunk's first tile
     mbar_wait(&bar[s], (it >> 1) & 1);
-    scan_tile<false, T>(B, gt, 0, reinterpret_cast<const uint32_t*>(smem + s * stage_alloc), res_s, warp_s, nullptr,
-                        prefix, ts);
+    scan_tile<false, T>(B, D, gt, 0, reinterpret_cast<const uint32_t*>(smem + s * stage_alloc), res_s, warp_s,
+                                nullptr, prefix, ts);
     prefix += ts;
     ts = ts_next;
   }
@@ -252,10 +261,8 @@ __global__ void __launch_bounds__(kThreads) scan_kernel_lb(const __grid_constant
   __syncthreads();
   const uint32_t gt = tile_s, epoch = epoch_s;
   if (gt >= B.total_tiles) return;
-  trace_stamp(B.trace, gt, 0);
-  trace_stamp(B.trace, gt, 7);
+  const ScanDesc& D = B.d[find_desc_scan(B, gt)];
   if (tid == 0) {
-    const ScanDesc& D = B.d[find_desc_scan(B, gt)];
     const uint64_t tile_start = uint64_t(gt - D.tile0) * kScanTile;
     const uint32_t nb = scan_stage_bytes(D, tile_start);
     mbar_arrive_expect_tx(&bar, nb);
@@ -264,7 +271,8 @@ __global__ void __launch_bounds__(kThreads) scan_kernel_lb(const __grid_constant
   mbar_wait(&bar, 0);
   // the unpack reads the staged bytes into registers before the results overwrite the buffer (scan_tile's
   // first barrier sits between the two)
-  scan_tile<true, uint64_t>(B, gt, epoch, reinterpret_cast<const uint32_t*>(buf_s), buf_s, warp_s, &prefix_s, 0, 0);
+  scan_tile<true, uint64_t>(B, D, gt, epoch, reinterpret_cast<const uint32_t*>(buf_s), buf_s, warp_s, &prefix_s, 0,
+                                   0);
 }
 
 bool pdl_on() {

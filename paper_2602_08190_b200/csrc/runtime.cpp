@@ -1133,6 +1133,15 @@ struct cdm_engine {
   uint32_t* err_mapped = nullptr;  // its device alias: harvest_kernel stores there
   uint32_t err_ring = 0, err_next = 0;
   std::map<uint32_t, uint64_t> err_owner;  // ring start position -> group whose words live there
+  // H9 checksums (opts.flags & CDM_ENGINE_CHECKSUM): per job, accumulated on the device, copied to pinned
+  // host memory at the end of its group (same ring positions as the error words)
+  bool checksum = false;
+  uint64_t* cs_dev = nullptr;
+  uint64_t* cs_host = nullptr;
+  cudaEvent_t complete = nullptr;  // recorded once at creation: an event that has always completed
+  // submit / wait / synchronize / ticket_event are serialised by this mutex (PAPER.md:207-208's submit path
+  // may be driven by several host threads); a wait blocks on its group's event with the mutex released
+  std::mutex mu;
 };
 
 
@@ -1146,6 +1155,7 @@ static cdm_status harvest_group(cdm_engine* e, uint64_t gid) {
     if (kv.second.group == gid) {
       const uint32_t w = e->err_host[g.err_pos + kv.second.index];
       kv.second.res.error_bits = w;
+      kv.second.res.checksum = e->checksum ? e->cs_host[g.err_pos + kv.second.index] : 0ull;
       kv.second.res.status = w ? CDM_E_CORRUPT : CDM_OK;
     }
   g.harvested = true;
@@ -1200,6 +1210,15 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   e->err_ring = 4096;
   CUDA_TRY(cudaHostAlloc(&e->err_host, sizeof(uint32_t) * e->err_ring, cudaHostAllocMapped));
   CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->err_mapped), e->err_host, 0));
+  e->checksum = (o.flags & CDM_ENGINE_CHECKSUM) != 0;
+  if (e->checksum) {
+    if (cudaMalloc(&e->cs_dev, sizeof(uint64_t) * e->err_ring) != cudaSuccess)
+      return fail(CDM_E_OOM, "checksum ring cudaMalloc failed");
+    CUDA_TRY(cudaHostAlloc(&e->cs_host, sizeof(uint64_t) * e->err_ring, cudaHostAllocDefault));
+  }
+  CUDA_TRY(cudaEventCreateWithFlags(&e->complete, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(e->complete, e->copy));
+  CUDA_TRY(cudaEventSynchronize(e->complete));
   *out = e.release();
   return CDM_OK;
 }
@@ -1223,6 +1242,9 @@ extern "C" CDM_API cdm_status cdm_engine_destroy(cdm_engine* e) {
     cudaEventDestroy(s.freed);
   }
   if (e->err_host) cudaFreeHost(e->err_host);
+  if (e->cs_dev) cudaFree(e->cs_dev);
+  if (e->cs_host) cudaFreeHost(e->cs_host);
+  if (e->complete) cudaEventDestroy(e->complete);
   for (auto fs : e->fam) if (fs) { cudaStreamSynchronize(fs); cudaStreamDestroy(fs); }
   if (e->own_copy) cudaStreamDestroy(e->copy);
   if (e->own_decode) cudaStreamDestroy(e->decode);
@@ -1363,6 +1385,16 @@ static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* ticket
       ++it;
     }
   }
+  if (e->checksum) {  // H9: positional checksum of every decoded chunk (payload, then offsets under id ^ 2^63)
+    CUDA_TRY(cudaMemsetAsync(e->cs_dev + ep, 0, sizeof(uint64_t) * nj, s.ds));
+    for (uint32_t j = 0; j < nj; j++) {
+      const Bound& b = bs[j];
+      if (b.payload) CUDA_TRY(launch_checksum(b.out, b.payload, b.chunk_id, e->cs_dev + ep + j, s.ds));
+      if (b.offs && b.offsets_bytes)
+        CUDA_TRY(launch_checksum(b.offs, b.offsets_bytes, b.chunk_id ^ (1ull << 63), e->cs_dev + ep + j, s.ds));
+    }
+    CUDA_TRY(cudaMemcpyAsync(e->cs_host + ep, e->cs_dev + ep, sizeof(uint64_t) * nj, cudaMemcpyDeviceToHost, s.ds));
+  }
   CUDA_TRY(launch_harvest(batch->err_dev, e->err_mapped + ep, nj, s.ds));
   CUDA_TRY(cudaEventRecord(s.freed, s.ds));
   const uint64_t gid = e->next_group++;
@@ -1401,6 +1433,7 @@ static cdm_status submit_group(cdm_engine* e, std::vector<Bound>& bs, const std:
 
 extern "C" CDM_API cdm_status cdm_submit(cdm_engine* e, const cdm_job* job, uint64_t* ticket) {
   if (!e || !job || !ticket) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(e->mu);
   CUDA_TRY(cudaSetDevice(e->device));
   std::vector<Bound> bs(1);
   cdm_status st = bind_job(*job, &bs[0]);
@@ -1509,6 +1542,7 @@ static cdm_status plan_groups(cdm_engine* e, const cdm_job* jobs, size_t n, uint
 
 extern "C" CDM_API cdm_status cdm_submit_batch(cdm_engine* e, const cdm_job* jobs, size_t n, uint64_t* tickets) {
   if (!e || (n && (!jobs || !tickets))) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(e->mu);
   CUDA_TRY(cudaSetDevice(e->device));
   std::vector<PendingGroup> groups;
   std::vector<size_t> order, first_job;
@@ -1849,9 +1883,22 @@ extern "C" CDM_API cdm_status cdm_pipeline_destroy(cdm_pipeline* p) {
 
 extern "C" CDM_API cdm_status cdm_wait(cdm_engine* e, uint64_t ticket, cdm_result* out) {
   if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
+  std::unique_lock<std::mutex> lock(e->mu);
   auto it = e->tickets.find(ticket);
   if (it == e->tickets.end()) return fail(CDM_E_BUSY, "unknown or consumed ticket");
   const uint64_t gid = it->second.group;
+  {  // block on the group's event with the engine unlocked (other threads keep submitting / waiting)
+    auto g = e->groups.find(gid);
+    if (g != e->groups.end() && !g->second.harvested && g->second.done) {
+      cudaEvent_t ev = g->second.done;
+      lock.unlock();
+      cudaError_t ce = cudaEventSynchronize(ev);  // a recycled event only makes this wait longer
+      lock.lock();
+      if (ce != cudaSuccess) return fail(CDM_E_CUDA, std::string("wait: ") + cudaGetErrorString(ce));
+    }
+  }
+  it = e->tickets.find(ticket);  // another thread may have consumed it meanwhile
+  if (it == e->tickets.end()) return fail(CDM_E_BUSY, "unknown or consumed ticket");
   cdm_status st = harvest_group(e, gid);
   if (st) return st;
   if (out) *out = it->second.res;
@@ -1863,8 +1910,20 @@ extern "C" CDM_API cdm_status cdm_wait(cdm_engine* e, uint64_t ticket, cdm_resul
   return r;
 }
 
+extern "C" CDM_API cdm_status cdm_ticket_event(cdm_engine* e, uint64_t ticket, void** cuda_event) {
+  if (!e || !cuda_event) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(e->mu);
+  auto it = e->tickets.find(ticket);
+  if (it == e->tickets.end()) return fail(CDM_E_BUSY, "unknown or consumed ticket");
+  auto g = e->groups.find(it->second.group);
+  if (g == e->groups.end() || g->second.harvested || !g->second.done) *cuda_event = e->complete;
+  else *cuda_event = g->second.done;
+  return CDM_OK;
+}
+
 extern "C" CDM_API cdm_status cdm_synchronize(cdm_engine* e) {
   if (!e) return fail(CDM_E_INVALID_ARG, "null engine");
+  std::lock_guard<std::mutex> lock(e->mu);
   CUDA_TRY(cudaStreamSynchronize(e->copy));
   CUDA_TRY(cudaStreamSynchronize(e->decode));
   for (auto& s : e->slots) CUDA_TRY(cudaStreamSynchronize(s.ds));

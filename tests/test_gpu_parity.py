@@ -57,6 +57,9 @@ def gpu_decode(engine, casc, chunks, resident=False, expect_error=False):
             d.dev_chunk = torch.from_numpy(ch).cuda()
         decs.append(d)
         bufs.append((out, offs, info))
+    # the sentinel fills run on torch's (legacy) default stream, the engine on its own non-blocking streams:
+    # the fills must be complete before the decode is enqueued (include/cdm.h: caller-owned outputs)
+    torch.cuda.synchronize()
     if resident == "pipeline":
         p = cdm.Pipeline(engine, decs)
         p.launch()
@@ -117,7 +120,7 @@ def check_parity(engine, spec, col_or_chunks, dtype=None, width=0, rows_per_chun
                 raise AssertionError(f"{spec} resident={resident}: first mismatch at byte {bad} "
                                      f"(got {payload[bad]}, oracle {exp[bad]})")
             if exp_offs is not None:
-                assert np.array_equal(offs[: exp_offs.size], exp_offs), f"{spec}: offsets differ"
+                assert np.array_equal(offs[: exp_offs.size], exp_offs), f"{spec} resident={resident}: offsets differ"
     return chunks
 
 
@@ -229,9 +232,10 @@ def test_config1_parity(engine):
 @pytest.fixture(params=[0, 1])
 def scan_mode(request):
     """both H6 schedules (NEXT-3 knob scan_mode): 0 reduce-then-scan, 1 single-pass decoupled look-back"""
+    prev = cdm.tune_get("scan_mode")
     cdm.tune_set("scan_mode", request.param)
     yield request.param
-    cdm.tune_set("scan_mode", 0)
+    cdm.tune_set("scan_mode", prev)
 
 
 @pytest.mark.parametrize("w", [1, 3, 8, 17, 33, 64])
@@ -328,15 +332,17 @@ def test_strdict_long_tokens_and_empty_strings(engine):
     check_parity(engine, "Str|[StrDict|BitPack,BitPack]", one, both=False)
 
 
-def test_strdict_word_parallel_variant():
-    """the opt-in sd_expand2 kernel (CDM_SD_EXPAND=2) decodes the same bytes (fresh process: env read once)"""
+@pytest.mark.parametrize("env", [{"CDM_SD_EXPAND": "2"}, {"CDM_SD_SMEM": "1"}])
+def test_strdict_expand_variants(env):
+    """the opt-in String-dictionary expansions -- the word-parallel sd_expand2 kernel (CDM_SD_EXPAND=2) and the
+    per-tile shared-memory dictionary (CDM_SD_SMEM=1) -- decode the same bytes (fresh process: env read once)"""
     import subprocess
     import sys
     code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
             "from paper_2602_08190_b200.inputs import TPCH; e = cdm.Engine(0); "
             "t.check_parity(e, 'Str|[StrDict|BitPack|ANS,BitPack]', TPCH(0.02).column('o_comment'), rows_per_chunk=50_001, both=False); "
             "t.test_strdict_long_tokens_and_empty_strings(e); print('ok')")
-    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_SD_EXPAND": "2"}, capture_output=True,
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
                        text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
@@ -385,12 +391,13 @@ def test_lz4_subchunk_sizes(engine, sub):
     check_parity(engine, f"Str|[LZ4(sub={sub}),BitPack]", col, rows_per_chunk=40_000, both=False)
 
 
-@pytest.fixture(params=[4, 1, 2, 8, 16, 32])
+@pytest.fixture(params=[1, 4, 2, 8, 16, 32])
 def lz4_lanes(request):
     """every LZ4 lane-group width the tuner may select (NEXT-3 knob lz4_lanes)"""
+    prev = cdm.tune_get("lz4_lanes")
     cdm.tune_set("lz4_lanes", request.param)
     yield request.param
-    cdm.tune_set("lz4_lanes", 4)
+    cdm.tune_set("lz4_lanes", prev)
 
 
 def test_lz4_lane_widths(engine, lz4_lanes):

@@ -55,6 +55,26 @@ def test_tpch_roundtrip(name, cascade):
     _check(col, encoder.encode_chunks(cascade, col, 17_001))  # several ragged chunks
 
 
+def _config4_cols():
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    return bench.CONFIG4_COLS
+
+
+@pytest.mark.parametrize("name,cascade", _config4_cols())
+def test_config4_cascades_roundtrip(name, cascade):
+    """the north-star workload's 25 columns under the exact cascades bench.py times (Table 2 mapped onto the
+    hot-path codecs: DeltaStride order keys, ANS l_returnflag, String-dictionary|BitPack|ANS o_comment, ...):
+    generator == oracle(encoder(generator)) over several ragged chunks"""
+    g = TPCH(0.01)
+    col = g.column(name)
+    _check(col, encoder.encode_chunks(cascade, col, 23_017))
+
+
 def test_ragged_and_empty():
     col = config1_column(1000)
     for rpc in (1, 7, 999, 1000, 5000):

@@ -64,14 +64,20 @@ def test_pruned_stops_at_first_decline_even_if_not_global():
 
 
 def test_cabi_tuning_knobs():
-    assert cdm.tune_get("lz4_lanes") in (4, 8, 16, 32)
+    assert cdm.tune_get("lz4_lanes") in (1, 2, 4, 8, 16, 32)
+    assert cdm.tune_get("scan_mode") in (0, 1)
     old = cdm.tune_get("fp_ctas_per_sm")
     cdm.tune_set("fp_ctas_per_sm", 3)
     assert cdm.tune_get("fp_ctas_per_sm") == 3
     cdm.tune_set("fp_ctas_per_sm", old)
-    cdm.tune_set("lz4_lanes", 1)
-    assert cdm.tune_get("lz4_lanes") == 1
+    lanes = cdm.tune_get("lz4_lanes")
     cdm.tune_set("lz4_lanes", 4)
-    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("nope", 1)):
+    assert cdm.tune_get("lz4_lanes") == 4
+    cdm.tune_set("lz4_lanes", lanes)
+    mode = cdm.tune_get("scan_mode")
+    cdm.tune_set("scan_mode", 1)
+    assert cdm.tune_get("scan_mode") == 1
+    cdm.tune_set("scan_mode", mode)
+    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("nope", 1)):
         with pytest.raises(cdm.CdmError):
             cdm.tune_set(knob, v)

@@ -71,6 +71,7 @@ def main():
         "NP": ({"lz4_lanes": [1, 2, 4, 8, 16, 32]}, [("Str|[LZ4(sub=16384),BitPack]", g.column("l_comment"))]),
     }
     rows = []
+    defaults = {k: cdm.tune_get(k) for k in ("fp_ctas_per_sm", "lz4_lanes", "scan_mode")}
     for pat, (space, cols) in cases.items():
         ev = make_eval(eng, cols, a.steps, flush, stream, list(space))
         bf = tune.brute_force(space, ev)
@@ -82,7 +83,7 @@ def main():
         rows.append(row)
         print(json.dumps(row), flush=True)
         for k in space:  # restore the defaults
-            cdm.tune_set(k, {"fp_ctas_per_sm": 0, "lz4_lanes": 4}[k])
+            cdm.tune_set(k, defaults[k])
     print("\n| pattern | space | B.F. evals | B.F. best (GB/s) | pruned evals | pruned best (GB/s) |")
     print("|---|---|---|---|---|---|")
     for r in rows:
