@@ -162,6 +162,9 @@ CDM_API cdm_status cdm_wait(cdm_engine *e, uint64_t ticket, cdm_result *out);
  * (SURVEY Sec. 8b).  Valid until the ticket is consumed by cdm_wait; for a ticket whose group was already
  * harvested it is an event that has completed.  Errors: CDM_E_INVALID_ARG, CDM_E_BUSY (unknown ticket). */
 CDM_API cdm_status cdm_ticket_event(cdm_engine *e, uint64_t ticket, void **cuda_event);
+/* Kernels the engine has enqueued through cdm_submit* so far (fused decode kernels, scratch zeroing, error
+ * harvest, checksums): the launch count of a measured region is the difference of two reads. */
+CDM_API cdm_status cdm_engine_launches(cdm_engine *e, uint64_t *n);
 /* Wait for everything submitted so far (results stay retrievable with cdm_wait). */
 CDM_API cdm_status cdm_synchronize(cdm_engine *e);
 /* H3 as a pure host function: Johnson's rule over jobs with transfer costs t[i] and
@@ -252,6 +255,8 @@ CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t c
  *   "lz4_lanes"       N.P. pattern's C: lanes cooperating on one LZ4 sub-chunk: 1 (default: the paper's thread
  *                     per chunk, lz4_thread_kernel), 2, 4, 8, 16 (lane groups) or 32 (one warp per sub-chunk);
  *                     env CDM_LZ4_G sets the start value
+ *   "gp_ctas_per_sm"  G.P. pattern's L (Table 3 G.P. row): resident rle_kernel CTAs per SM, 0 = the kernel's own
+ *                     occupancy (default), 1..8 (enforced by padding the launch's dynamic shared memory)
  *   "scan_mode"       H6 schedule (single-pass look-back vs the 2-pass baseline): 0 =
  *                     reduce-then-scan (tile sums, then a persistent scan; default), 1 = single-pass decoupled
  *                     look-back (one tile per CTA in ticket order); env CDM_SCAN_MODE sets the start value

@@ -281,6 +281,7 @@ enum TuneKnob : int {
   TUNE_FP_CTAS_PER_SM = 0,  // F.P. "L": persistent fp_kernel CTAs per SM (0 = adaptive 2/3/4)
   TUNE_LZ4_LANES = 1,       // N.P. "C": lanes per LZ4 sub-chunk: 1 (thread per sub-chunk), 2..16 (lane groups), 32
   TUNE_SCAN_MODE = 2,       // H6 schedule: 0 reduce-then-scan (tile sums + persistent scan), 1 decoupled look-back
+  TUNE_GP_CTAS_PER_SM = 3,  // G.P. "L": resident rle_kernel CTAs per SM (0 = the kernel's occupancy), 1..8
   kTuneKnobs
 };
 int tune_get(int knob);

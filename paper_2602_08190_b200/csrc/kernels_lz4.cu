@@ -286,7 +286,8 @@ __device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the
   return v;
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_thread_kernel(const __grid_constant__ Lz4Batch B) {
+template <int MINB>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) lz4_thread_kernel(const __grid_constant__ Lz4Batch B) {
   __shared__ __align__(16) uint8_t oring_s[kWarpsPerCta * 32 * kLzRing];
   __shared__ __align__(16) uint8_t iring_s[kWarpsPerCta * 32 * kLzRing];
   const uint32_t gs = blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x;
@@ -421,11 +422,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_thread_kernel(const __g
     q.tail = true;
     return true;
   };
-  auto put16 = [&](uint32_t op, const uint32_t (&v)[4], uint32_t k) {  // k <= 16 bytes at output position op
+  // Append k <= 16 bytes (v, little-endian) at output position op: the bytes are shifted into the 8-byte word
+  // containing op (its bytes below op are kept from the ring's copy of that word) and whole 8-byte words are
+  // stored into the ring (no byte stores); bytes past op + k in the last word are scratch, overwritten by later
+  // appends before any read (they alias ring bytes more than 48 behind, which no near match reads).
+  uint64_t acc = 0;  // the ring word holding output bytes [(ga0 + op) & ~7, ga0 + op)
+  auto put16 = [&](uint32_t op, const uint32_t (&v)[4], uint32_t k) {
     const uintptr_t ga = ga0 + op;
-#pragma unroll
-    for (uint32_t b = 0; b < 16; b++)
-      if (b < k) oring[(ga + b) & (kLzRing - 1)] = uint8_t(v[b >> 2] >> (8 * (b & 3)));
+    const uint32_t fill = uint32_t(ga & 7u), sh = 8u * fill;
+    const uint64_t v01 = (uint64_t(v[1]) << 32) | v[0], v23 = (uint64_t(v[3]) << 32) | v[2];
+    const uint64_t keep = fill ? (acc & ((1ull << sh) - 1ull)) : 0ull;
+    const uint64_t w0 = keep | (v01 << sh);
+    const uint64_t w1 = (fill ? (v01 >> (64u - sh)) : 0ull) | (v23 << sh);
+    const uint64_t w2 = fill ? (v23 >> (64u - sh)) : 0ull;
+    uint64_t* rw8 = reinterpret_cast<uint64_t*>(oring);
+    const uint32_t q = uint32_t(ga >> 3), words = (fill + k + 7u) >> 3;  // words touched: 1..3
+    rw8[q & (kLzRing / 8 - 1)] = w0;
+    if (words > 1) rw8[(q + 1) & (kLzRing / 8 - 1)] = w1;
+    if (words > 2) rw8[(q + 2) & (kLzRing / 8 - 1)] = w2;
+    const uint32_t last = (fill + k) >> 3;  // index of the word holding the new end position
+    acc = last == 0 ? w0 : last == 1 ? w1 : w2;
     if ((ga & 15u) + k >= 16u) flush(ga & ~uintptr_t(15));
   };
   auto far_load = [&](uintptr_t src, uint2& x0, uint2& x1, uint2& x2) {  // bytes [src & ~7, +24)
@@ -515,7 +531,9 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
   const int G = tune_get(TUNE_LZ4_LANES);
   if (G == 1) {
     const uint32_t grid = (b.total_subs + kWarpsPerCta * 32 - 1) / (kWarpsPerCta * 32);
-    lz4_thread_kernel<<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    static const int minb = std::getenv("CDM_LZ4_MINB") ? std::atoi(std::getenv("CDM_LZ4_MINB")) : 3;
+    if (minb == 4) lz4_thread_kernel<4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    else lz4_thread_kernel<3><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();
   }
   if (G != 32) {

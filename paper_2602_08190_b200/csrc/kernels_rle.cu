@@ -666,18 +666,31 @@ cudaError_t launch_rle(const RleBatch& b, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static bool configured[kMaxDevices] = {};
+  void (*kern)(RleBatch);
+  if (b.any_linear) kern = b.trace ? rle_kernel<true, true> : rle_kernel<false, true>;
+  else if (b.short_runs) kern = b.trace ? rle_kernel<true, false, 5> : rle_kernel<false, false, 5>;
+  else kern = b.trace ? rle_kernel<true, false> : rle_kernel<false, false>;
+  // NEXT-3 G.P. knob (Table 3's G.P. row): resident rle_kernel CTAs per SM, enforced by
+  // padding the launch's dynamic shared memory (0 = the kernel's own occupancy)
+  const int cap = tune_get(TUNE_GP_CTAS_PER_SM);
   const int dev = current_device();
-  if (!configured[dev]) {  // the slope table takes the linear variants past the 48 KB default
-    cudaFuncSetAttribute(rle_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * sizeof(uint64_t));
-    cudaFuncSetAttribute(rle_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * sizeof(uint64_t));
-    configured[dev] = true;
+  if (cap > 0) {
+    static int smem_sm[kMaxDevices] = {};
+    if (!smem_sm[dev]) cudaDeviceGetAttribute(&smem_sm[dev], cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    const long want = long(smem_sm[dev]) / cap - long(fa.sharedSizeBytes) - 1024;  // 1 KB reserved per CTA
+    if (want > long(cfg.dynamicSmemBytes)) cfg.dynamicSmemBytes = size_t(want);
   }
-  cudaError_t e;
-  if (b.any_linear) e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, true>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, true>, b);
-  else if (b.short_runs)
-    e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, false, 5>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, false, 5>, b);
-  else e = b.trace ? cudaLaunchKernelEx(&cfg, rle_kernel<true, false>, b) : cudaLaunchKernelEx(&cfg, rle_kernel<false, false>, b);
+  static size_t configured[kMaxDevices][6] = {};
+  const int ki = kern == rle_kernel<true, true> ? 0 : kern == rle_kernel<false, true> ? 1
+               : kern == rle_kernel<true, false, 5> ? 2 : kern == rle_kernel<false, false, 5> ? 3
+               : kern == rle_kernel<true, false> ? 4 : 5;
+  if (cfg.dynamicSmemBytes > 48 * 1024 && cfg.dynamicSmemBytes > configured[dev][ki]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.dynamicSmemBytes));
+    configured[dev][ki] = cfg.dynamicSmemBytes;
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

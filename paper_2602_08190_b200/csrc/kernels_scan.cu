@@ -37,7 +37,7 @@ __device__ __forceinline__ int find_desc_scan(const ScanBatch& B, uint32_t tile)
   return lo;
 }
 
-constexpr int kPer = kScanTile / kThreads;  // 16 values per thread
+constexpr int kRtsThreads = 512;  // reduce-then-scan CTA: 8 values per thread (more warps in flight per SM)
 
 __device__ __forceinline__ uint32_t scan_stage_bytes(const ScanDesc& D, uint64_t tile_start) {
   const uint64_t stream_bytes = ((uint64_t(D.n) * D.w + 7) / 8 + 15) & ~15ull;
@@ -87,11 +87,12 @@ __global__ void __launch_bounds__(kThreads) scan_sums_kernel(const __grid_consta
 constexpr uint32_t kResPad = kScanTile + kScanTile / 16;  // results in shared memory, one pad slot per 16
 __device__ __forceinline__ uint32_t rpad(uint32_t i) { return i + (i >> 4); }
 
-template <bool LB, typename T>
+template <bool LB, typename T, int NT>
 __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D, uint32_t gt, uint32_t epoch,
                                           const uint32_t* wd, T* res_s, uint64_t* warp_s, uint64_t* prefix_s,
                                           uint64_t prefix, uint64_t tsum_tile) {
   constexpr bool W64 = sizeof(T) == 8;
+  constexpr int kPer = kScanTile / NT;  // values per thread
   const uint32_t tid = threadIdx.x;
   const uint32_t lt = gt - D.tile0, w = D.w;
   const uint64_t tile_start = uint64_t(lt) * kScanTile;
@@ -99,7 +100,7 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D,
   const T fb = T(D.for_base);
   const uint32_t m32 = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
 
-  // blocked: thread t owns values [16t, 16t+16); v[j] = exclusive prefix within the thread
+  // blocked: thread t owns values [kPer t, kPer (t+1)); v[j] = exclusive prefix within the thread
   T v[kPer + 1];
   T run = 0;
   const uint32_t i0 = tid * kPer;
@@ -131,7 +132,7 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D,
   }
   v[kPer] = run;
   uint64_t tile_total;
-  const uint64_t texcl = block_excl_scan_u64<kThreads>(uint64_t(run), warp_s, &tile_total);
+  const uint64_t texcl = block_excl_scan_u64<NT>(uint64_t(run), warp_s, &tile_total);
   if (LB) {
     if (tid < 32) {
       uint64_t pc, p0;
@@ -152,10 +153,10 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D,
 #pragma unroll
   for (int j = 0; j < kPer; j++) res_s[rpad(i0 + j)] = add + (delta ? v[j + 1] : v[j]);
   __syncthreads();
-  // striped: thread t stores values k*1024 + 4t .. +3 (16 or 32 contiguous bytes per lane, whole lines per warp)
+  // striped: thread t stores values k*4NT + 4t .. +3 (16 or 32 contiguous bytes per lane, whole lines per warp)
 #pragma unroll
-  for (uint32_t k = 0; k < 4; k++) {
-    const uint32_t e0 = k * 1024 + tid * 4;
+  for (uint32_t k = 0; k < kScanTile / (4 * NT); k++) {
+    const uint32_t e0 = k * 4 * NT + tid * 4;
     if (e0 >= valid) break;
     const uint64_t gi = tile_start + e0;
     const T r0 = res_s[rpad(e0)], r1 = res_s[rpad(e0 + 1)], r2 = res_s[rpad(e0 + 2)], r3 = res_s[rpad(e0 + 3)];
@@ -187,56 +188,58 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D,
 // the TMA engine while the current one is scanned.  A CTA needs the tile sums once for its first tile (the sum of
 // the chunk's tiles before it, block-reduced); after that the running prefix grows by each tile's sum (and
 // restarts at 0 at a chunk's first tile).
+constexpr uint32_t kRtsStages = 4;  // packed-tile stages: the TMA engine runs up to 3 tiles ahead
+
 template <typename T>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 3) scan_kernel_rts(const __grid_constant__ ScanBatch B, uint32_t stage_alloc) {
-  extern __shared__ __align__(128) uint8_t smem[];  // [2 x stage_alloc packed][kResPad x T results]
-  T* res_s = reinterpret_cast<T*>(smem + 2 * stage_alloc);
-  __shared__ uint64_t warp_s[kThreads / 32];
-  __shared__ __align__(8) uint64_t bar[2];
+__global__ void __launch_bounds__(kRtsThreads, sizeof(T) == 4 ? 3 : 2) scan_kernel_rts(const __grid_constant__ ScanBatch B, uint32_t stage_alloc) {
+  extern __shared__ __align__(128) uint8_t smem[];  // [kRtsStages x stage_alloc packed][kResPad x T results]
+  T* res_s = reinterpret_cast<T*>(smem + kRtsStages * stage_alloc);
+  __shared__ uint64_t warp_s[kRtsThreads / 32];
+  __shared__ __align__(8) uint64_t bar[kRtsStages];
   const uint32_t tid = threadIdx.x;
   const uint32_t per = (B.total_tiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * per, t1 = min(B.total_tiles, t0 + per);
   if (t0 >= t1) return;
   // the descriptor of a tile: the CTA's tiles are contiguous, so the index only moves forward
   int di = find_desc_scan(B, t0);
-  int sdi = di;  // the staging cursor (one tile ahead)
+  int sdi = di;  // the staging cursor (kRtsStages - 1 tiles ahead)
   auto stage = [&](uint32_t t, uint32_t s) {  // tid 0: TMA the packed bytes of tile t into stage s
     while (sdi + 1 < int(B.n) && B.d[sdi + 1].tile0 <= t) sdi++;
     const ScanDesc& D = B.d[sdi];
     const uint64_t tile_start = uint64_t(t - D.tile0) * kScanTile;
     const uint32_t nb = scan_stage_bytes(D, tile_start);
-    fence_proxy_async();  // generic reads of this stage (two tiles ago) precede the TMA refill
+    fence_proxy_async();  // generic reads of this stage (kRtsStages tiles ago) precede the TMA refill
     mbar_arrive_expect_tx(&bar[s], nb);
     if (nb) tma_load_1d(smem + s * stage_alloc, D.packed + tile_start / 8 * D.w, nb, &bar[s]);
   };
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (uint32_t k = 0; k < kRtsStages; k++) mbar_init(&bar[k], 1);
     fence_mbar_init();
-    stage(t0, 0);
+    for (uint32_t k = 0; k + 1 < kRtsStages && t0 + k < t1; k++) stage(t0 + k, k);
   }
   __syncthreads();
   grid_dependency_wait();  // scan_sums_kernel complete: the tile sums are valid
   uint64_t prefix;
   {
     uint64_t part = 0;
-    for (uint32_t k = B.d[di].tile0 + tid; k < t0; k += kThreads) part += B.tsum[k];
+    for (uint32_t k = B.d[di].tile0 + tid; k < t0; k += kRtsThreads) part += B.tsum[k];
     uint64_t tot;
-    block_excl_scan_u64<kThreads>(part, warp_s, &tot);
+    block_excl_scan_u64<kRtsThreads>(part, warp_s, &tot);
     prefix = tot;
   }
   uint32_t it = 0;
   uint64_t ts = B.tsum[t0];
   for (uint32_t gt = t0; gt < t1; gt++, it++) {
-    const uint32_t s = it & 1;
-    if (tid == 0 && gt + 1 < t1) stage(gt + 1, s ^ 1);  // stage s^1 was freed by the previous tile
+    const uint32_t s = it % kRtsStages;
+    // the stage of tile gt - 1 was freed by its barriers: refill it with tile gt + kRtsStages - 1
+    if (tid == 0 && gt + kRtsStages - 1 < t1) stage(gt + kRtsStages - 1, (it + kRtsStages - 1) % kRtsStages);
     const uint64_t ts_next = gt + 1 < t1 ? B.tsum[gt + 1] : 0ull;  // in flight during this tile
     while (di + 1 < int(B.n) && B.d[di + 1].tile0 <= gt) di++;
     const ScanDesc& D = B.d[di];
     if (gt == D.tile0) prefix = 0;  // a chunk's first tile
-    mbar_wait(&bar[s], (it >> 1) & 1);
-    scan_tile<false, T>(B, D, gt, 0, reinterpret_cast<const uint32_t*>(smem + s * stage_alloc), res_s, warp_s,
-                                nullptr, prefix, ts);
+    mbar_wait(&bar[s], (it / kRtsStages) & 1);
+    scan_tile<false, T, kRtsThreads>(B, D, gt, 0, reinterpret_cast<const uint32_t*>(smem + s * stage_alloc), res_s,
+                                     warp_s, nullptr, prefix, ts);
     prefix += ts;
     ts = ts_next;
   }
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel_lb(const __grid_constant
   mbar_wait(&bar, 0);
   // the unpack reads the staged bytes into registers before the results overwrite the buffer (scan_tile's
   // first barrier sits between the two)
-  scan_tile<true, uint64_t>(B, D, gt, epoch, reinterpret_cast<const uint32_t*>(buf_s), buf_s, warp_s, &prefix_s, 0,
+  scan_tile<true, uint64_t, kThreads>(B, D, gt, epoch, reinterpret_cast<const uint32_t*>(buf_s), buf_s, warp_s, &prefix_s, 0,
                                    0);
 }
 
@@ -298,7 +301,7 @@ cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s) {
     w64 = w64 || b.d[i].out_bytes == 8;
   }
   const uint32_t stage = ((kScanTile / 8) * (max_w ? max_w : 1) + 16 + 127) & ~127u;  // + slack words
-  const uint32_t smem = 2 * stage + kResPad * (w64 ? 8 : 4);
+  const uint32_t smem = kRtsStages * stage + kResPad * (w64 ? 8 : 4);
   auto kern = w64 ? scan_kernel_rts<uint64_t> : scan_kernel_rts<uint32_t>;
   static uint32_t configured[kMaxDevices][2] = {};
   uint32_t& conf = configured[current_device()][w64];
@@ -307,13 +310,13 @@ cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s) {
     conf = smem;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtsThreads, smem);
   if (per_sm < 1) per_sm = 1;
   uint32_t grid = uint32_t(device_sms() * per_sm);
   if (grid > b.total_tiles) grid = b.total_tiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kRtsThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -1139,6 +1139,7 @@ struct cdm_engine {
   uint64_t* cs_dev = nullptr;
   uint64_t* cs_host = nullptr;
   cudaEvent_t complete = nullptr;  // recorded once at creation: an event that has always completed
+  uint64_t kernel_launches = 0;  // kernels enqueued by cdm_submit* (decode kernels, checksums, harvests)
   // submit / wait / synchronize / ticket_event are serialised by this mutex (PAPER.md:207-208's submit path
   // may be driven by several host threads); a wait blocks on its group's event with the mutex released
   std::mutex mu;
@@ -1367,6 +1368,7 @@ static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* ticket
   uint32_t nl = 0;
   st = batch_enqueue(batch.get(), s.ds, &nl);
   if (st) return st;
+  e->kernel_launches += nl + 2;  // + zero + harvest
   // pinned error words for this group (contiguous ring slice; an old group still there is harvested)
   const uint32_t nj = uint32_t(bs.size());
   if (nj > e->err_ring) return fail(CDM_E_CAPACITY, "too many chunks in one group");
@@ -1389,9 +1391,11 @@ static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* ticket
     CUDA_TRY(cudaMemsetAsync(e->cs_dev + ep, 0, sizeof(uint64_t) * nj, s.ds));
     for (uint32_t j = 0; j < nj; j++) {
       const Bound& b = bs[j];
-      if (b.payload) CUDA_TRY(launch_checksum(b.out, b.payload, b.chunk_id, e->cs_dev + ep + j, s.ds));
-      if (b.offs && b.offsets_bytes)
+      if (b.payload) { CUDA_TRY(launch_checksum(b.out, b.payload, b.chunk_id, e->cs_dev + ep + j, s.ds)); e->kernel_launches++; }
+      if (b.offs && b.offsets_bytes) {
         CUDA_TRY(launch_checksum(b.offs, b.offsets_bytes, b.chunk_id ^ (1ull << 63), e->cs_dev + ep + j, s.ds));
+        e->kernel_launches++;
+      }
     }
     CUDA_TRY(cudaMemcpyAsync(e->cs_host + ep, e->cs_dev + ep, sizeof(uint64_t) * nj, cudaMemcpyDeviceToHost, s.ds));
   }
@@ -1910,6 +1914,13 @@ extern "C" CDM_API cdm_status cdm_wait(cdm_engine* e, uint64_t ticket, cdm_resul
   return r;
 }
 
+extern "C" CDM_API cdm_status cdm_engine_launches(cdm_engine* e, uint64_t* n) {
+  if (!e || !n) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(e->mu);
+  *n = e->kernel_launches;
+  return CDM_OK;
+}
+
 extern "C" CDM_API cdm_status cdm_ticket_event(cdm_engine* e, uint64_t ticket, void** cuda_event) {
   if (!e || !cuda_event) return fail(CDM_E_INVALID_ARG, "null argument");
   std::lock_guard<std::mutex> lock(e->mu);
@@ -2116,6 +2127,9 @@ extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
     if (value != 1 && value != 2 && value != 4 && value != 8 && value != 16 && value != 32)
       return fail(CDM_E_INVALID_ARG, "lz4_lanes must be 1, 2, 4, 8, 16 or 32");
     cdm::tune_set(cdm::TUNE_LZ4_LANES, value);
+  } else if (k == "gp_ctas_per_sm") {
+    if (value < 0 || value > 8) return fail(CDM_E_INVALID_ARG, "gp_ctas_per_sm must be 0..8");
+    cdm::tune_set(cdm::TUNE_GP_CTAS_PER_SM, value);
   } else if (k == "scan_mode") {
     if (value != 0 && value != 1) return fail(CDM_E_INVALID_ARG, "scan_mode must be 0 (reduce-then-scan) or 1 (look-back)");
     cdm::tune_set(cdm::TUNE_SCAN_MODE, value);
@@ -2131,6 +2145,7 @@ extern "C" CDM_API cdm_status cdm_tune_get(const char* knob, int* value) {
   if (k == "fp_ctas_per_sm") *value = cdm::tune_get(cdm::TUNE_FP_CTAS_PER_SM);
   else if (k == "lz4_lanes") *value = cdm::tune_get(cdm::TUNE_LZ4_LANES);
   else if (k == "scan_mode") *value = cdm::tune_get(cdm::TUNE_SCAN_MODE);
+  else if (k == "gp_ctas_per_sm") *value = cdm::tune_get(cdm::TUNE_GP_CTAS_PER_SM);
   else return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   return CDM_OK;
 }

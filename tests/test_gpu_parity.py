@@ -255,6 +255,19 @@ RLE_DISTS = ["even-1", "even-2", "even-4", "even-64", "even-1024", "random-1-8",
              "single"]
 
 
+@pytest.mark.parametrize("cap", [1, 3, 8])
+def test_gp_occupancy_knob(engine, cap):
+    """the G.P. tuner knob (resident rle_kernel CTAs per SM) changes scheduling only, never bytes"""
+    prev = cdm.tune_get("gp_ctas_per_sm")
+    cdm.tune_set("gp_ctas_per_sm", cap)
+    try:
+        check_parity(engine, "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", TPCH(0.02).column("l_orderkey"),
+                     rows_per_chunk=50_001, both=False)
+        check_parity(engine, "RLE|[BitPack,BitPack]", rle_column("random-1-8", 300_000, I64), both=False)
+    finally:
+        cdm.tune_set("gp_ctas_per_sm", prev)
+
+
 @pytest.mark.parametrize("dist", RLE_DISTS)
 def test_rle_distributions(engine, dist):
     col = rle_column(dist, 1_000_003, I64)

@@ -78,6 +78,10 @@ def test_cabi_tuning_knobs():
     cdm.tune_set("scan_mode", 1)
     assert cdm.tune_get("scan_mode") == 1
     cdm.tune_set("scan_mode", mode)
-    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("nope", 1)):
+    gp = cdm.tune_get("gp_ctas_per_sm")
+    cdm.tune_set("gp_ctas_per_sm", 2)
+    assert cdm.tune_get("gp_ctas_per_sm") == 2
+    cdm.tune_set("gp_ctas_per_sm", gp)
+    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("gp_ctas_per_sm", 9), ("nope", 1)):
         with pytest.raises(cdm.CdmError):
             cdm.tune_set(knob, v)

@@ -2,7 +2,9 @@
 
 The B200 build fixes S (256 threads per CTA) and the tile shapes at compile time, so the runtime spaces are:
   F.P.  L = persistent fp_kernel CTAs per SM (knob fp_ctas_per_sm) in 2^0..2^4     (Table 3: L 2^0..2^4)
+  G.P.  L = resident rle_kernel CTAs per SM (knob gp_ctas_per_sm) in 2^0..2^3   (Table 3: G.P. L = numCUs, S x C)
   N.P.  C = lanes per LZ4 sub-chunk (knob lz4_lanes) in {1, 2, 4, 8, 16, 32}       (Table 3: C 2^0..2^10)
+  H6    the scan schedule (knob scan_mode): reduce-then-scan vs single-pass look-back
 Each evaluation builds a fresh graph-mode batch over the workload (so the knob is captured), times K replays
 with CUDA events after a 256 MiB L2-flush write each, and returns decoded GB/s.
 usage: python tools/tune.py [--sf 10] [--steps 5] -> JSON lines + a summary table
@@ -16,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 from paper_2602_08190_b200 import cdm, encoder, tune  # noqa: E402
-from paper_2602_08190_b200.inputs import TPCH  # noqa: E402
+from paper_2602_08190_b200.inputs import I64, TPCH, rle_column  # noqa: E402
 
 
 def make_eval(eng, cols, steps, flush, stream, knob_names):
@@ -68,10 +70,15 @@ def main():
     cases = {
         "FP": ({"fp_ctas_per_sm": [1, 2, 4, 8, 16]},
                [("Dict|BitPack", g.column("l_quantity")), ("Float2Int|BitPack", g.column("l_extendedprice"))]),
+        "GP": ({"gp_ctas_per_sm": [1, 2, 4, 8]},
+               [("RLE|[BitPack,BitPack]", rle_column("even-4", 1 << 26, I64)),
+                ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", g.column("l_orderkey"))]),
         "NP": ({"lz4_lanes": [1, 2, 4, 8, 16, 32]}, [("Str|[LZ4(sub=16384),BitPack]", g.column("l_comment"))]),
+        "SCAN": ({"scan_mode": [0, 1]}, [("Delta|BitPack", g.column("o_orderkey")),
+                                         ("Str|[Raw,BitPack]", g.column("l_comment"))]),
     }
     rows = []
-    defaults = {k: cdm.tune_get(k) for k in ("fp_ctas_per_sm", "lz4_lanes", "scan_mode")}
+    defaults = {k: cdm.tune_get(k) for k in ("fp_ctas_per_sm", "lz4_lanes", "scan_mode", "gp_ctas_per_sm")}
     for pat, (space, cols) in cases.items():
         ev = make_eval(eng, cols, a.steps, flush, stream, list(space))
         bf = tune.brute_force(space, ev)
