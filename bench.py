@@ -346,14 +346,14 @@ def run_config5(args, rank, world, local, local_world):
 
     def up(x):
         return (x + 255) // 256 * 256
-    W, DEPTH = 32, 3  # chunks per window (one submit_batch); windows in flight = output ring sections
+    # chunks per window (one submit_batch); windows in flight = output ring sections.  Measured on B200 (slice 0):
+    # W 32 / DEPTH 2 / 4 staging slots 161 GB/s; DEPTH 3 with 12 slots 79 GB/s
+    W, DEPTH = 32, 2
     slot_out = max(up(max(c.payload, 16)) + up(c.offsets) for c in ds.chunks)
     ring = torch.empty(DEPTH * W * slot_out, dtype=torch.uint8, device="cuda")
     cascs = [cdm.Cascade(spec, dt, w) for (_, spec, dt, w) in ds.columns]
     max_chunk = max(c.size for c in ds.chunks)
-    # staging slots: an LZ4 chunk holds its slot for its whole decode chain (~6 ms, longer than a window's PCIe
-    # time), so the ring is deep enough for the copies of later chunks to keep the link busy meanwhile
-    eng = cdm.Engine(dev, n_slots=12, slot_bytes=max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20)),
+    eng = cdm.Engine(dev, n_slots=4, slot_bytes=max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20)),
                      order_policy=1, checksum=True)
     order = sorted(range(len(ds.chunks)), key=lambda i: (ds.chunks[i].index, ds.chunks[i].column))  # row order
     windows = [order[a: a + W] for a in range(0, len(order), W)]
@@ -701,18 +701,19 @@ def main():
         dev_v = tot_decoded * args.steps / dev_s / 1e9
         cr = tot_decoded / tot_comp
         # rooflines: each kernel kind alone (events around each launch) against its algorithmic bytes
-        fam_ms, fam_bytes = {}, {}
+        fam_ms, fam_bytes, fam_n = {}, {}, {}
         for kname, (ms, n) in ktimes.items():
             f = FAMILY_OF[kname]
             if n:
                 fam_ms[f] = fam_ms.get(f, 0.0) + ms / tsteps
+                fam_n[f] = fam_n.get(f, 0) + n / tsteps
             fam_bytes[f] = fam_bytes.get(f, 0) + kbytes.get(kname, 0)
         families = {}
         for f, ms in sorted(fam_ms.items(), key=lambda x: -x[1]):
             b = fam_bytes.get(f, 0)
             gbs = b / (ms / 1e3) / 1e9 if ms > 0 else 0.0
             families[f] = {"ms_per_step": round(ms, 4), "algorithmic_bytes": b, "achieved_gbs": round(gbs, 1),
-                           "frac": round(gbs / peak, 4)}
+                           "frac": round(gbs / peak, 4), "launches_per_step": round(fam_n.get(f, 0), 2)}
         dom = max(families, key=lambda f: families[f]["ms_per_step"])
         lanes = cdm.tune_get("lz4_lanes")
         kern_of = {"fp_numeric": "fp_kernel", "fp_char": "fpc_kernel (CHAR(n) row groups)",
@@ -764,6 +765,11 @@ def main():
                                        "HBM, CUDA events on the launching stream, L2 flushed between steps"},
             "roofline": {"bound": "hbm", "achieved": families[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
                          "frac": families[dom]["frac"], "traffic": traffic, "kernel": kern_of[dom], "family": dom,
+                         "launches_per_step": families[dom]["launches_per_step"],
+                         "algorithmic_bytes_per_launch": int(families[dom]["algorithmic_bytes"] /
+                                                             max(families[dom]["launches_per_step"], 1)),
+                         "traffic_how": "ncu --set full DRAM read + write bytes of ONE launch of this kernel in this "
+                                        "workload (profiles/ncu_traffic.json), per launch like algorithmic_bytes_per_launch",
                          "algorithmic_bytes_per_step": families[dom]["algorithmic_bytes"],
                          "kernel_ms_per_step": families[dom]["ms_per_step"], "peak_source": peak_src,
                          "families": families, "families_concurrent_ms": conc, "critical_path_family": crit,
