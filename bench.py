@@ -67,6 +67,13 @@ WORKLOADS = {
                     desc="config 4: TPC-H lineitem + orders, all 25 columns at SF={sf} (SURVEY Sec. 8d cascade "
                          "map: l_returnflag ANS, l_/o_orderkey DeltaStride, o_comment String-dictionary|BitPack|ANS "
                          "per Table 2), streamed from pinned host"),
+    # config 4 with Table 2's comment cascade (O_COMMENT's String-dictionary|Bit-packing|ANS) also on
+    # l_comment: the cascade choice the paper's per-column selection would make for a comment column (P:499-500:
+    # String-dictionary beats the LZ77 family on comments); the default config 4 keeps chunk-parallel LZ4
+    "config4sd": dict(sf=100.0, dtype="mixed",
+                      cols=[(n, "Str|[StrDict|BitPack|ANS,BitPack]" if n == "l_comment" else c) for n, c in CONFIG4_COLS],
+                      desc="config 4 with l_comment under Table 2's comment cascade Str|[StrDict|BitPack|ANS,BitPack]: "
+                           "TPC-H lineitem + orders, all 25 columns at SF={sf}, streamed from pinned host"),
     # BASELINE configs[4]: SF=1000 lineitem streamed through an output ring, 8 GPUs; one process decodes its
     # 1/8 slice (chunk ranges of every column), N processes take slices rank, rank + N, ... (see run_config5)
     "config5": dict(sf=1000.0, dtype="mixed", cols=[c for c in CONFIG4_COLS if c[0].startswith("l_")],
@@ -348,7 +355,8 @@ def run_config5(args, rank, world, local, local_world):
         return (x + 255) // 256 * 256
     # chunks per window (one submit_batch); windows in flight = output ring sections.  Measured on B200 (slice 0):
     # W 32 / DEPTH 2 / 4 staging slots 161 GB/s; DEPTH 3 with 12 slots 79 GB/s
-    W, DEPTH = 32, 2
+    W = int(os.environ.get("CDM_C5_WINDOW", "32"))
+    DEPTH = 2
     slot_out = max(up(max(c.payload, 16)) + up(c.offsets) for c in ds.chunks)
     ring = torch.empty(DEPTH * W * slot_out, dtype=torch.uint8, device="cuda")
     cascs = [cdm.Cascade(spec, dt, w) for (_, spec, dt, w) in ds.columns]
@@ -794,12 +802,12 @@ def main():
         dist.destroy_process_group()
 
 
-def build_workload(rank: int, workload: str = "config2"):
+def build_workload(rank: int, workload: str = "config2", sf: float | None = None):
     """Compatibility helper for tests: [(name, spec, dtype, width, [chunk numpy arrays], plain bytes)]."""
     from paper_2602_08190_b200 import workload as W
     from paper_2602_08190_b200.inputs import MASTER_SEED
     wl = WORKLOADS[workload]
-    ds = W.build(wl["cols"], wl["sf"], MASTER_SEED + 1000 * rank, CHUNK_ROWS)
+    ds = W.build(wl["cols"], sf if sf is not None else wl["sf"], MASTER_SEED + 1000 * rank, CHUNK_ROWS)
     out = []
     for k, (name, spec, dt, w) in enumerate(ds.columns):
         chs = [ds.host(c).copy() for c in ds.chunks if c.column == k]

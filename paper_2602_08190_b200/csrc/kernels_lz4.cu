@@ -286,8 +286,7 @@ __device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the
   return v;
 }
 
-template <int MINB>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) lz4_thread_kernel(const __grid_constant__ Lz4Batch B) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const __grid_constant__ Lz4Batch B) {
   __shared__ __align__(16) uint8_t oring_s[kWarpsPerCta * 32 * kLzRing];
   __shared__ __align__(16) uint8_t iring_s[kWarpsPerCta * 32 * kLzRing];
   const uint32_t gs = blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x;
@@ -531,9 +530,7 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
   const int G = tune_get(TUNE_LZ4_LANES);
   if (G == 1) {
     const uint32_t grid = (b.total_subs + kWarpsPerCta * 32 - 1) / (kWarpsPerCta * 32);
-    static const int minb = std::getenv("CDM_LZ4_MINB") ? std::atoi(std::getenv("CDM_LZ4_MINB")) : 3;
-    if (minb == 4) lz4_thread_kernel<4><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
-    else lz4_thread_kernel<3><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    lz4_thread_kernel<<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();
   }
   if (G != 32) {

@@ -742,18 +742,21 @@ def test_checksum_matches_oracle(engine, name, spec):
 
 
 # ------------------------------------------------------------------------------ BASELINE full sizes
+@pytest.mark.timeout(1200)
 @pytest.mark.parametrize("workload", ["config3", "config4"])
-def test_full_size_workload_sampled(engine, workload):
-    """BASELINE configs 3 / 4 at full size (SF 10) in bench.py's launch configuration -- every chunk of the
-    workload in ONE graph-mode device batch -- with no device error bit, and sampled chunks (first, last and
-    two random per column) equal to the oracle byte for byte."""
+def test_full_size_workload_every_chunk(engine, workload):
+    """BASELINE configs 3 / 4 at SF 10 (config 3's full size; config 4's 25 columns at a tenth of the headline) in
+    bench.py's launch configuration -- every chunk of the workload in ONE graph-mode device batch, decoded twice --
+    with no device error bit, the H9 checksum of EVERY chunk equal to the oracle's checksum of the same chunk
+    (oracle decodes on all host threads), and sampled chunks (first, last and two random per column) equal to the
+    oracle byte for byte."""
     import random
     sys_path = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     import sys
     if sys_path not in sys.path:
         sys.path.insert(0, sys_path)
     import bench
-    cols = bench.build_workload(0, workload)
+    cols = bench.build_workload(0, workload, sf=10.0)
     decs, keep = [], []
     for name, spec, dtype, width, chunks, _ in cols:
         casc = cdm.Cascade(spec, dtype, width)
@@ -768,6 +771,25 @@ def test_full_size_workload_sampled(engine, workload):
     b.launch()  # the replay bench.py times
     res = b.results()
     assert all(r["error_bits"] == 0 for r in res)
+    torch.cuda.synchronize()
+    # every chunk: device checksum == oracle checksum (payload under the chunk id, offsets under id ^ 2^63)
+    gpu = []
+    for name, i, _, ch, out, offs in keep:
+        info = cdm.chunk_info(ch)
+        cs = cdm.checksum(out[: info["payload_bytes"]], info["chunk_id"])
+        if offs is not None:
+            cs = (cs + cdm.checksum(offs, info["chunk_id"] ^ (1 << 63))) % (1 << 64)
+        gpu.append(cs)
+    threads = os.cpu_count() or 1
+    for a in range(0, len(keep), 64):
+        part = keep[a: a + 64]
+        dec = oracle.decode_many([k[3] for k in part], nthreads=threads)
+        for j, (k, (payload, offs)) in enumerate(zip(part, dec)):
+            cid = int.from_bytes(k[3][56:64].tobytes(), "little")
+            want = oracle.checksum(payload, cid)
+            if offs is not None:
+                want = (want + oracle.checksum(offs, cid ^ (1 << 63))) % (1 << 64)
+            assert gpu[a + j] == want, f"{workload} {k[0]} chunk {k[1]}: checksum differs from the oracle's"
     rng = random.Random(7)
     by_col = {}
     for k in keep:

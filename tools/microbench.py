@@ -147,6 +147,15 @@ def main():
         com = g.column("l_comment")
         for sub in (4096, 16384, 65536):
             emit(run_case(eng, f"NP lz4 sub={sub}", f"Str|[LZ4(sub={sub}),BitPack]", com, a.steps, flush, stream))
+        # single-sub-chunk latency: ONE sub-chunk (l_comment rows totalling ~sub bytes) per launch -- the length of
+        # the chunk-sequential chain that bounds every LZ4 launch
+        for sub in (4096, 16384, 65536):
+            lens = np.diff(com.offsets)
+            nrow = int(np.searchsorted(np.cumsum(lens), sub - 64))
+            one = Column("l_comment", com.dtype, com.width, nrow, com.data[: int(com.offsets[nrow])].copy(),
+                         com.offsets[: nrow + 1].copy())
+            emit(run_case(eng, f"NP lz4 one sub-chunk sub={sub}", f"Str|[LZ4(sub={sub}),BitPack]", one, a.steps,
+                          flush, stream))
         rf = g.column("l_returnflag")
         for chunk in (1024, 4096, 16384):
             emit(run_case(eng, f"NP ans chunk={chunk}", f"ANS(chunk={chunk})", rf, a.steps, flush, stream))
