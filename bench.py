@@ -354,8 +354,8 @@ def run_config5(args, rank, world, local, local_world):
     def up(x):
         return (x + 255) // 256 * 256
     # chunks per window (one submit_batch); windows in flight = output ring sections.  Measured on B200 (slice 0):
-    # W 32 / DEPTH 2 / 4 staging slots 161 GB/s; DEPTH 3 with 12 slots 79 GB/s
-    W = int(os.environ.get("CDM_C5_WINDOW", "32"))
+    # W 128 / DEPTH 2 / 4 staging slots 196 GB/s (bar 181); W 32 158-161 GB/s; DEPTH 3 with 12 slots 79 GB/s
+    W = int(os.environ.get("CDM_C5_WINDOW", "128"))
     DEPTH = 2
     slot_out = max(up(max(c.payload, 16)) + up(c.offsets) for c in ds.chunks)
     ring = torch.empty(DEPTH * W * slot_out, dtype=torch.uint8, device="cuda")

@@ -291,6 +291,13 @@ __global__ void __launch_bounds__(kThreads, 3) rle_sums_kernel(const __grid_cons
     D.tsum[2 * (t0 + threadIdx.x)] = a;
     D.tsum[2 * (t0 + threadIdx.x) + 1] = b;
   }
+  if (threadIdx.x == 0) {  // the group's total (its kSumsTiles tiles), after the tile sums: tsum[2 (tiles + g)]
+    uint64_t a = 0, b = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) { a += part_s[w][0]; b += part_s[w][1]; }
+    D.tsum[2 * (D.tiles + (unit - D.unit0))] = a;
+    D.tsum[2 * (D.tiles + (unit - D.unit0)) + 1] = b;
+  }
   if (bad) atomicOr(B.err + D.err_idx, 0x2u);
   trace_stamp(B.trace, unit, 4);
 }
@@ -371,10 +378,18 @@ __global__ void __launch_bounds__(kThreads, OCC) rle_kernel(const __grid_constan
   // tile sums before it (L2-resident, written by rle_sums; loaded through L2 only)
   uint64_t O64, Pw;
   {
+    // the group sums of the rle_sums groups before this tile's group, plus the tile sums of its group before it
+    // (one round of independent L2 loads however deep the tile is in its chunk)
     uint64_t pc = 0, pw = 0;
     const ulonglong2* ts = reinterpret_cast<const ulonglong2*>(D.tsum);
-    for (uint32_t i = tid; i < lt; i += kThreads) {
-      const ulonglong2 v = __ldcg(ts + i);
+    const uint32_t grp = lt / kSumsTiles, tg0 = grp * kSumsTiles;
+    for (uint32_t i = tid; i < grp; i += kThreads) {
+      const ulonglong2 v = __ldcg(ts + D.ntiles + i);
+      pc += v.x;
+      pw += v.y;
+    }
+    if (tid < lt - tg0) {
+      const ulonglong2 v = __ldcg(ts + tg0 + tid);
       pc += v.x;
       pw += v.y;
     }

@@ -782,7 +782,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (size_t i = 0; i < B->scan.size(); i++) B->scan[i].tsum = A.take<uint64_t>(scan_tiles[i]);
   for (size_t u = 0; u < units.size(); u++) {
     SumsChunk& d = B->sums[sums_at[u].first].d[sums_at[u].second];
-    d.tsum = A.take<uint64_t>(size_t(d.tiles) * 2);
+    d.tsum = A.take<uint64_t>(size_t(d.tiles + d.units) * 2);  // tile sums, then one sum per rle_sums group
     B->rle[rle_at[u].first].d[rle_at[u].second].tsum = d.tsum;
   }
   for (size_t u = 0; u < units.size(); u++) {

@@ -5,6 +5,7 @@ Each case: synthetic column -> CDM1 chunks of 2^22 rows (host, untimed) -> devic
 events) -> decoded GB/s and the Eq. 1 roofline fraction ((compressed read + decoded written) / time / the
 MEASURED_PEAKS copy peak).  Sweeps:
   E2  BitPack bit width w = 1..32, int32 output (uniform w-bit values)
+  E2L BitPack bit width w = 1..64, int64 output
   E3  RLE group-size distributions even-X / random-L-R / outlier-X-P / mixed, int64
   E7  fused vs decoded-twice: Dict|BitPack and Float2Int|BitPack (PAPER.md:565-588's fusion question)
   CHR CHAR(n) dictionary rows: l_shipinstruct (25 B), l_shipmode (10), l_returnflag (1), o_orderpriority /
@@ -113,6 +114,9 @@ def main():
     if "E2" in a.sweeps:
         for w in (1, 2, 4, 8, 12, 16, 20, 24, 28, 32):
             emit(run_case(eng, f"E2 w={w}", "BitPack", uniform_bits_column(n, w, I32), a.steps, flush, stream))
+    if "E2L" in a.sweeps:  # E2 on int64 output up to w = 64 (PAPER.md:356-371's bit-width sweep, 8-byte rows)
+        for w in (1, 4, 8, 16, 24, 32, 40, 48, 56, 64):
+            emit(run_case(eng, f"E2 i64 w={w}", "BitPack", uniform_bits_column(n // 2, w, I64), a.steps, flush, stream))
     if "E3" in a.sweeps:
         for dist in ("even-1", "even-4", "even-32", "even-1024", "random-1-8", "random-1-64", "outlier-1024-1",
                      "mixed-even-4+random-1-64"):
