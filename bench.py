@@ -119,6 +119,8 @@ def parse():
     p.add_argument("--workers", type=int, default=None, help="generator/encoder processes per rank")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="torch.distributed backend for N>1 (gloo: the one-GPU multi-rank test)")
+    p.add_argument("--ingest", default="", help="config5: comma-separated devices whose PCIe links carry the H2D "
+                   "copies (NEXT-4 multi-link ingestion, cdm_engine_set_ingest); empty = the rank's own link")
     p.add_argument("--device-map", default="local", choices=["local", "zero"],
                    help="local: rank -> cuda:LOCAL_RANK; zero: every rank on cuda:0 (tests on a single GPU)")
     a = p.parse_args()
@@ -363,6 +365,8 @@ def run_config5(args, rank, world, local, local_world):
     max_chunk = max(c.size for c in ds.chunks)
     eng = cdm.Engine(dev, n_slots=4, slot_bytes=max(64 << 20, (max_chunk + (1 << 20) - 1) // (1 << 20) * (1 << 20)),
                      order_policy=1, checksum=True)
+    if args.ingest:
+        eng.set_ingest([int(x) for x in args.ingest.split(",")])
     order = sorted(range(len(ds.chunks)), key=lambda i: (ds.chunks[i].index, ds.chunks[i].column))  # row order
     windows = [order[a: a + W] for a in range(0, len(order), W)]
     decs = []
@@ -443,6 +447,7 @@ def run_config5(args, rank, world, local, local_world):
                        "chunk_rows": CHUNK_ROWS, "columns": len(ds.columns), "chunks": n_chunks,
                        "decoded_bytes_per_step": decoded, "compressed_bytes_per_step": compressed,
                        "compression_ratio": round(cr, 3), "window_chunks": W, "windows_in_flight": DEPTH,
+                       "ingest_devices": args.ingest or None,
                        "output_ring_bytes": int(ring.numel()),
                        "parallelism": f"{world} rank(s) x their 1/8 slices of one SF=1000 dataset",
                        "l2": "inputs and outputs exceed the 126 MB L2",

@@ -162,6 +162,13 @@ CDM_API cdm_status cdm_wait(cdm_engine *e, uint64_t ticket, cdm_result *out);
  * (SURVEY Sec. 8b).  Valid until the ticket is consumed by cdm_wait; for a ticket whose group was already
  * harvested it is an event that has completed.  Errors: CDM_E_INVALID_ARG, CDM_E_BUSY (unknown ticket). */
 CDM_API cdm_status cdm_ticket_event(cdm_engine *e, uint64_t ticket, void **cuda_event);
+/* NEXT-4 multi-link ingestion (Vortex): route the H2D copies of cdm_submit* over the PCIe links of
+ * `devices` (round-robin per group): each group is copied into a staging buffer on that device and then peer-copied
+ * over NVLink into the engine device's staging slot, so one consumer GPU can draw on several hosts links.  A listed
+ * device equal to the engine's takes the same two-hop path (H2D, then a device-to-device copy).  n = 0 restores
+ * direct copies.  Drains in-flight work first; allocates slot_bytes on each listed device.
+ * Errors: CDM_E_INVALID_ARG (null / device out of range), CDM_E_OOM, CDM_E_CUDA. */
+CDM_API cdm_status cdm_engine_set_ingest(cdm_engine *e, const int *devices, size_t n);
 /* Kernels the engine has enqueued through cdm_submit* so far (fused decode kernels, scratch zeroing, error
  * harvest, checksums): the launch count of a measured region is the difference of two reads. */
 CDM_API cdm_status cdm_engine_launches(cdm_engine *e, uint64_t *n);

@@ -25,7 +25,7 @@ KERNELS = ["fp_kernel", "scan_kernel", "rle_sums_kernel", "rle_kernel(level0)", 
 
 SYMBOLS = ["cdm_status_str", "cdm_last_error", "cdm_version", "cdm_cascade_create", "cdm_cascade_destroy",
            "cdm_cascade_describe", "cdm_chunk_info", "cdm_chunk_check", "cdm_engine_create", "cdm_engine_destroy", "cdm_submit",
-           "cdm_submit_batch", "cdm_wait", "cdm_ticket_event", "cdm_engine_launches", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
+           "cdm_submit_batch", "cdm_wait", "cdm_ticket_event", "cdm_engine_launches", "cdm_engine_set_ingest", "cdm_synchronize", "cdm_johnson_order", "cdm_batch_create", "cdm_batch_launch",
            "cdm_batch_results", "cdm_batch_destroy", "cdm_batch_set_timing", "cdm_batch_kernel_ms",
            "cdm_batch_set_graph", "cdm_batch_collect_timing", "cdm_batch_kernel_times", "cdm_batch_kernel_bytes",
            "cdm_pipeline_create", "cdm_pipeline_launch", "cdm_pipeline_results", "cdm_pipeline_destroy",
@@ -91,6 +91,7 @@ def lib():
         "cdm_synchronize": [vp],
         "cdm_ticket_event": [vp, u64, ctypes.POINTER(vp)],
         "cdm_engine_launches": [vp, ctypes.POINTER(u64)],
+        "cdm_engine_set_ingest": [vp, ctypes.POINTER(ctypes.c_int), sz],
         "cdm_johnson_order": [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), sz,
                               ctypes.POINTER(sz)],
         "cdm_batch_create": [vp, ctypes.POINTER(Job), sz, ctypes.POINTER(vp)],
@@ -276,6 +277,11 @@ class Engine:
         ev = ctypes.c_void_p()
         _check(lib().cdm_ticket_event(self.h, ticket, ctypes.byref(ev)))
         return ev.value or 0
+
+    def set_ingest(self, devices: list[int]) -> None:
+        """cdm_engine_set_ingest (NEXT-4): copy over these devices' PCIe links, then NVLink into this engine."""
+        arr = (ctypes.c_int * max(len(devices), 1))(*devices)
+        _check(lib().cdm_engine_set_ingest(self.h, arr, len(devices)))
 
     def launches(self) -> int:
         """cdm_engine_launches: kernels enqueued through cdm_submit* so far."""

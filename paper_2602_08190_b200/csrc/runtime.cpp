@@ -1139,6 +1139,17 @@ struct cdm_engine {
   uint64_t* cs_dev = nullptr;
   uint64_t* cs_host = nullptr;
   cudaEvent_t complete = nullptr;  // recorded once at creation: an event that has always completed
+  // NEXT-4 multi-link ingestion (cdm_engine_set_ingest; Vortex): groups are copied H2D over the
+  // PCIe links of these devices, in turn, into a staging buffer on that device, then peer-copied (NVLink) into
+  // the engine's staging slot.  Empty: every copy goes over the engine device's own link.
+  struct Ingest {
+    int device = 0;
+    cudaStream_t stream = nullptr;       // on `device`: H2D copy, then the peer copy (ordered)
+    uint8_t* buf = nullptr;              // on `device`: one group's chunks (slot_bytes)
+    std::vector<cudaEvent_t> copied;     // on `device`, one per engine slot: the slot's data has arrived
+  };
+  std::vector<Ingest> ingest;
+  uint64_t ingest_rr = 0;
   uint64_t kernel_launches = 0;  // kernels enqueued by cdm_submit* (decode kernels, checksums, harvests)
   // submit / wait / synchronize / ticket_event are serialised by this mutex (PAPER.md:207-208's submit path
   // may be driven by several host threads); a wait blocks on its group's event with the mutex released
@@ -1246,6 +1257,13 @@ extern "C" CDM_API cdm_status cdm_engine_destroy(cdm_engine* e) {
   if (e->cs_dev) cudaFree(e->cs_dev);
   if (e->cs_host) cudaFreeHost(e->cs_host);
   if (e->complete) cudaEventDestroy(e->complete);
+  for (auto& ig : e->ingest) {
+    cudaSetDevice(ig.device);
+    if (ig.stream) { cudaStreamSynchronize(ig.stream); cudaStreamDestroy(ig.stream); }
+    if (ig.buf) cudaFree(ig.buf);
+    for (auto ev : ig.copied) if (ev) cudaEventDestroy(ev);
+  }
+  cudaSetDevice(e->device);
   for (auto fs : e->fam) if (fs) { cudaStreamSynchronize(fs); cudaStreamDestroy(fs); }
   if (e->own_copy) cudaStreamDestroy(e->copy);
   if (e->own_decode) cudaStreamDestroy(e->decode);
@@ -1285,6 +1303,7 @@ struct PendingGroup {
   uint32_t slot = 0;
   std::vector<Bound> bs;
   std::vector<const cdm_job*> js;
+  cudaEvent_t copied = nullptr;  // the event the decode waits on (the slot's, or an ingest device's)
 };
 
 // Phase 1: enqueue the group's H2D copies into its slot (copy stream) and record the slot's `copied` event.
@@ -1293,7 +1312,12 @@ static cdm_status group_copy(cdm_engine* e, PendingGroup& pg) {
   e->next_slot = (e->next_slot + 1) % uint32_t(e->slots.size());
   pg.slot = si;
   cdm_engine::Slot& s = e->slots[si];
-  if (s.used) CUDA_TRY(cudaStreamWaitEvent(e->copy, s.freed, 0));
+  // NEXT-4: the copy runs over an ingest device's PCIe link into its buffer, then over NVLink into the slot
+  cdm_engine::Ingest* ig = e->ingest.empty() ? nullptr : &e->ingest[e->ingest_rr++ % e->ingest.size()];
+  cudaStream_t cs = ig ? ig->stream : e->copy;
+  uint8_t* const base = ig ? ig->buf : s.dev;
+  if (ig) CUDA_TRY(cudaSetDevice(ig->device));
+  if (s.used) CUDA_TRY(cudaStreamWaitEvent(cs, s.freed, 0));  // (a cross-device wait for an ingest device)
   auto& bs = pg.bs;
   auto& js = pg.js;
   // Lay the chunks out in the slot in host-address order: exactly contiguous host neighbours keep their
@@ -1321,22 +1345,34 @@ static cdm_status group_copy(cdm_engine* e, PendingGroup& pg) {
       end += bs[j].total;
       m++;
     }
-    if (pos + end > e->opts.slot_bytes) return fail(CDM_E_CAPACITY, "group larger than a staging slot");
-    cudaError_t ce = cudaMemcpyAsync(s.dev + pos, h0, end, cudaMemcpyHostToDevice, e->copy);
+    if (pos + end > e->opts.slot_bytes) { if (ig) cudaSetDevice(e->device); return fail(CDM_E_CAPACITY, "group larger than a staging slot"); }
+    cudaError_t ce = cudaMemcpyAsync(base + pos, h0, end, cudaMemcpyHostToDevice, cs);
     if (ce == cudaErrorInvalidValue && m > k + 1) {
       cudaGetLastError();
       for (size_t q = k; q < m; q++) {
         const size_t j = by_addr[q];
-        CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(bs[j].dev_chunk), js[j]->host_chunk, bs[j].total,
-                                 cudaMemcpyHostToDevice, e->copy));
+        ce = cudaMemcpyAsync(base + (bs[j].dev_chunk - s.dev), js[j]->host_chunk, bs[j].total,
+                             cudaMemcpyHostToDevice, cs);
+        if (ce != cudaSuccess) break;
       }
-    } else if (ce != cudaSuccess) {
+    }
+    if (ce != cudaSuccess) {
+      if (ig) cudaSetDevice(e->device);
       return fail(CDM_E_CUDA, std::string("H2D copy: ") + cudaGetErrorString(ce));
     }
     pos += end;
     k = m;
   }
-  CUDA_TRY(cudaEventRecord(s.copied, e->copy));
+  if (ig) {  // the group's bytes: ingest device -> engine device (NVLink peer copy; a D2D copy for the device itself)
+    cudaError_t ce = cudaMemcpyPeerAsync(s.dev, e->device, ig->buf, ig->device, pos, cs);
+    if (ce == cudaSuccess) ce = cudaEventRecord(ig->copied[si], cs);
+    cudaSetDevice(e->device);
+    if (ce != cudaSuccess) return fail(CDM_E_CUDA, std::string("ingest peer copy: ") + cudaGetErrorString(ce));
+    pg.copied = ig->copied[si];
+  } else {
+    CUDA_TRY(cudaEventRecord(s.copied, e->copy));
+    pg.copied = s.copied;
+  }
   s.used = true;
   return CDM_OK;
 }
@@ -1364,7 +1400,7 @@ static cdm_status group_decode(cdm_engine* e, PendingGroup& pg, uint64_t* ticket
   // fresh error words / counters for this group, zeroed while the group's copy is still in flight
   CUDA_TRY(launch_zero(s.arena, batch->zero_bytes, s.ds));
   batch->zeroed_by_caller = true;
-  CUDA_TRY(cudaStreamWaitEvent(s.ds, s.copied, 0));
+  CUDA_TRY(cudaStreamWaitEvent(s.ds, pg.copied ? pg.copied : s.copied, 0));
   uint32_t nl = 0;
   st = batch_enqueue(batch.get(), s.ds, &nl);
   if (st) return st;
@@ -1912,6 +1948,47 @@ extern "C" CDM_API cdm_status cdm_wait(cdm_engine* e, uint64_t ticket, cdm_resul
   auto g = e->groups.find(gid);
   if (g != e->groups.end() && --g->second.pending == 0) e->groups.erase(g);
   return r;
+}
+
+extern "C" CDM_API cdm_status cdm_engine_set_ingest(cdm_engine* e, const int* devices, size_t n) {
+  if (!e || (n && !devices)) return fail(CDM_E_INVALID_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(e->mu);
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  for (size_t i = 0; i < n; i++)
+    if (devices[i] < 0 || devices[i] >= ndev) return fail(CDM_E_INVALID_ARG, "ingest device out of range");
+  // drain and drop the previous set
+  for (auto& s : e->slots) CUDA_TRY(cudaStreamSynchronize(s.ds));
+  for (auto& ig : e->ingest) {
+    CUDA_TRY(cudaSetDevice(ig.device));
+    CUDA_TRY(cudaStreamSynchronize(ig.stream));
+    cudaStreamDestroy(ig.stream);
+    cudaFree(ig.buf);
+    for (auto ev : ig.copied) cudaEventDestroy(ev);
+  }
+  e->ingest.clear();
+  e->ingest_rr = 0;
+  for (size_t i = 0; i < n; i++) {
+    cdm_engine::Ingest ig;
+    ig.device = devices[i];
+    CUDA_TRY(cudaSetDevice(ig.device));
+    if (ig.device != e->device) {  // NVLink peer access both ways where the topology allows it
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, ig.device, e->device);
+      if (can) {
+        cudaError_t pe = cudaDeviceEnablePeerAccess(e->device, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return fail(CDM_E_CUDA, "peer access");
+        cudaGetLastError();
+      }
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&ig.stream, cudaStreamNonBlocking));
+    if (cudaMalloc(&ig.buf, e->opts.slot_bytes) != cudaSuccess) { cudaSetDevice(e->device); return fail(CDM_E_OOM, "ingest buffer"); }
+    ig.copied.resize(e->slots.size());
+    for (auto& ev : ig.copied) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->ingest.push_back(ig);
+  }
+  CUDA_TRY(cudaSetDevice(e->device));
+  return CDM_OK;
 }
 
 extern "C" CDM_API cdm_status cdm_engine_launches(cdm_engine* e, uint64_t* n) {

@@ -132,3 +132,27 @@ def test_engine_checksum_matches_oracle(items):
     assert r0["checksum"] == 0
     plain.close()
     eng.close()
+
+
+def test_multi_link_ingestion_path(items):
+    """NEXT-4: cdm_engine_set_ingest routes each group's H2D copy through an ingest device's own
+    staging buffer and stream, then a peer (here device-to-device) copy into the engine's slot.  With one GPU the
+    ingest devices are the engine's own device twice (two buffers / streams, round-robin): every byte still equals
+    the oracle's, the checksum path is unchanged, and clearing the list restores direct copies."""
+    eng = cdm.Engine(0, n_slots=3, slot_bytes=64 << 20, checksum=True)
+    eng.set_ingest([0, 0])
+    for rep in range(2):
+        decs, bufs = _decodes(items)
+        res = [eng.wait(t) for t in eng.submit_batch(decs)]
+        torch.cuda.synchronize()
+        _check(bufs)
+        assert all(r["error_bits"] == 0 for r in res)
+    eng.set_ingest([])
+    decs, bufs = _decodes(items[:3])
+    for t in eng.submit_batch(decs):
+        eng.wait(t)
+    torch.cuda.synchronize()
+    _check(bufs)
+    with pytest.raises(cdm.CdmError):
+        eng.set_ingest([99])
+    eng.close()
