@@ -278,6 +278,33 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* sm
   return wp + x - v;
 }
 
+// Exclusive scan of one value per thread across the CTA in T arithmetic (uint32_t: mod 2^32) with log-step
+// scans at both levels: a shuffle scan inside each warp, then every warp scans the NT/32 warp totals with
+// shuffles (no serial loop over the warps).  Returns the exclusive prefix; *total = the CTA's sum.
+template <int NT, typename T>
+__device__ __forceinline__ T block_excl_scan_log(T v, T* smem_warp /*[NT/32]*/, T* total) {
+  constexpr int NW = NT / 32;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(FULL, x, o);
+    if (lane >= uint32_t(o)) x += y;
+  }
+  if (lane == 31) smem_warp[warp] = x;
+  __syncthreads();
+  T w = lane < uint32_t(NW) ? smem_warp[lane] : T(0);
+#pragma unroll
+  for (int o = 1; o < NW; o <<= 1) {
+    const T y = __shfl_up_sync(FULL, w, o);
+    if (lane >= uint32_t(o)) w += y;
+  }
+  const T wp = warp ? __shfl_sync(FULL, w, warp - 1) : T(0);
+  *total = __shfl_sync(FULL, w, NW - 1);
+  __syncthreads();
+  return wp + x - v;
+}
+
 // Exclusive scan of a pair (a, b) of u64 per thread across the CTA with one barrier pair; *ta, *tb = totals.
 // smem_warp holds 2 * NT/32 words.  The warp totals are scanned by every warp with one shuffle scan.
 template <int NT>

@@ -47,37 +47,46 @@ __device__ __forceinline__ uint32_t scan_stage_bytes(const ScanDesc& D, uint64_t
   return uint32_t(want < have ? want : have);
 }
 
-// Tile sums for reduce-then-scan: one warp per tile, lane l sums the fields of elements l, l + 32, ... (adjacent
-// lanes read adjacent bits: coalesced).  Exact in u64 (the offsets check compares the chunk's total).
+// Tile sums for reduce-then-scan: one 256-thread CTA per tile, thread t sums the 16 consecutive fields
+// [16t, 16t + 16) through a two-word bit window that slides over the packed words (one load per 32 bits consumed,
+// adjacent threads read adjacent words: coalesced), then a block reduction.  Exact in u64 (the offsets check
+// compares the chunk's total).
 __global__ void __launch_bounds__(kThreads) scan_sums_kernel(const __grid_constant__ ScanBatch B) {
   grid_launch_dependents();  // scan_kernel's CTAs may be scheduled (they stage their first tile, then wait)
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t gt = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  if (gt >= B.total_tiles) return;
+  __shared__ uint64_t warp_s[kThreads / 32];
+  const uint32_t gt = blockIdx.x, tid = threadIdx.x;
   const ScanDesc& D = B.d[find_desc_scan(B, gt)];
   const uint32_t lt = gt - D.tile0, w = D.w;
   const uint64_t tile_start = uint64_t(lt) * kScanTile;
   const uint32_t valid = uint32_t(min(uint64_t(kScanTile), uint64_t(D.n) - tile_start));
   const uint32_t* wd = reinterpret_cast<const uint32_t*>(D.packed + tile_start / 8 * w);
+  constexpr uint32_t kPerS = kScanTile / kThreads;  // 16 fields per thread
+  const uint32_t i0 = tid * kPerS, i1 = min(valid, i0 + kPerS);
   uint64_t acc = 0;
-  if (w && w <= 32) {
-    const uint32_t m = w == 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
-    uint32_t part = 0;  // < 128 fields of < 2^25 ... summed in 64 bits below when w > 24
-#pragma unroll 8
-    for (uint32_t i = lane; i < valid; i += 32) {
-      const uint32_t b = i * w;
-      const uint32_t f = __funnelshift_r(__ldg(wd + (b >> 5)), __ldg(wd + (b >> 5) + 1), b & 31) & m;
-      if (w <= 24) part += f; else acc += f;
-    }
-    acc += part;
-  } else if (w) {
-    for (uint32_t i = lane; i < valid; i += 32) acc += extract_bits_global(wd, uint64_t(i) * w, w);
-  }
-  const uint32_t cnt = valid > lane ? (valid - lane + 31) / 32 : 0u;
-  acc += D.for_base * uint64_t(cnt);
+  if (w && i0 < i1) {
+    if (w <= 32) {
+      const uint32_t m = w == 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+      uint32_t q = (i0 * w) >> 5, sh = (i0 * w) & 31;
+      uint32_t lo = __ldg(wd + q), hi = __ldg(wd + q + 1);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-  if (lane == 0) B.tsum[gt] = acc;
+      for (uint32_t j = 0; j < kPerS; j++) {
+        if (i0 + j < i1) acc += __funnelshift_r(lo, hi, sh) & m;
+        sh += w;
+        if (sh >= 32) {
+          sh -= 32;
+          q++;
+          lo = hi;
+          hi = __ldg(wd + q + 1);
+        }
+      }
+    } else {
+      for (uint32_t i = i0; i < i1; i++) acc += extract_bits_global(wd, uint64_t(i) * w, w);
+    }
+  }
+  acc += D.for_base * uint64_t(i1 > i0 ? i1 - i0 : 0u);
+  uint64_t tot;
+  block_excl_scan_u64<kThreads>(acc, warp_s, &tot);
+  if (tid == 0) B.tsum[gt] = tot;
 }
 
 // One tile: unpack + scan + prefix + transposed 16-byte stores.  T = uint32_t when every output of the launch is
@@ -132,7 +141,14 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D,
   }
   v[kPer] = run;
   uint64_t tile_total;
-  const uint64_t texcl = block_excl_scan_u64<NT>(uint64_t(run), warp_s, &tile_total);
+  uint64_t texcl;
+  if (LB) {
+    texcl = block_excl_scan_u64<NT>(uint64_t(run), warp_s, &tile_total);
+  } else {  // in T arithmetic (the LENGTHS check uses the exact tile sum from scan_sums_kernel)
+    T tt;
+    texcl = uint64_t(block_excl_scan_log<NT, T>(run, reinterpret_cast<T*>(warp_s), &tt));
+    tile_total = uint64_t(tt);
+  }
   if (LB) {
     if (tid < 32) {
       uint64_t pc, p0;
@@ -291,7 +307,7 @@ cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s) {
     scan_kernel_lb<<<b.total_tiles, kThreads, 0, s>>>(b);
     return cudaGetLastError();
   }
-  scan_sums_kernel<<<(b.total_tiles + kThreads / 32 - 1) / (kThreads / 32), kThreads, 0, s>>>(b);
+  scan_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   uint32_t max_w = 0;
