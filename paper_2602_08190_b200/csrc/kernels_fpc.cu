@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
     // the group's G fields: one 64-bit window when G*w <= 64 (w <= 32: a valid index has < 2^32 entries)
     const bool win = uint32_t(G) * w <= 64u;
     uint64_t wv = 0;
-    if (win) {
+    if (win && g0 < valid) {  // (a group past the tile's rows reads nothing: its rows are never stored)
       const uint32_t b = g0 * w, q = b >> 5, sh = b & 31;
       const uint32_t a0 = __ldg(wd + q), a1 = __ldg(wd + q + 1), a2 = __ldg(wd + q + 2);
       wv = (uint64_t(__funnelshift_r(a1, a2, sh)) << 32) | __funnelshift_r(a0, a1, sh);
@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
       uint64_t f;
       if (win) {
         f = uint32_t(wv >> (j * w)) & m32;
+      } else if (r >= valid) {
+        f = 0;
       } else if (w <= 32) {
         const uint32_t b = r * w;
         f = __funnelshift_r(__ldg(wd + (b >> 5)), __ldg(wd + (b >> 5) + 1), b & 31) & m32;

@@ -70,9 +70,10 @@ __global__ void __launch_bounds__(kThreads) scan_sums_kernel(const __grid_consta
       uint32_t lo = __ldg(wd + q), hi = __ldg(wd + q + 1);
 #pragma unroll
       for (uint32_t j = 0; j < kPerS; j++) {
-        if (i0 + j < i1) acc += __funnelshift_r(lo, hi, sh) & m;
+        if (i0 + j >= i1) break;  // never read past the tile's last field (its word + 1 is in the stream padding)
+        acc += __funnelshift_r(lo, hi, sh) & m;
         sh += w;
-        if (sh >= 32) {
+        if (sh >= 32 && i0 + j + 1 < i1) {
           sh -= 32;
           q++;
           lo = hi;

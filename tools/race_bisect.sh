@@ -1,3 +1,5 @@
+#!/bin/bash
+# the round-1 racecheck selection under compute-sanitizer racecheck in five variants (profiles/r02_racecheck.md)
 mkdir -p gpurun_out/race
 RSEL="golden or config1 or strdict_long or corrupt_strdict or corrupt_ans or lz4_overlapping_matches[1] or lz4_overlapping_matches[4] or dstride_random_runs[3]"
 for env in "X=1" "CDM_PDL=0" "CDM_SCAN_MODE=1" "CDM_SERIAL=1" "CDM_SERIAL=1 CDM_PDL=0"; do
