@@ -56,7 +56,7 @@ CONFIG4_COLS = [
     ("l_extendedprice", "Float2Int|BitPack"), ("l_discount", "Dict|BitPack"), ("l_tax", "Dict|BitPack"),
     ("l_returnflag", "ANS"), ("l_linestatus", "Dict|BitPack"), ("l_shipdate", "Dict|BitPack"),
     ("l_commitdate", "Dict|BitPack"), ("l_receiptdate", "Dict|BitPack"), ("l_shipinstruct", "Dict|BitPack"),
-    ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384),BitPack]"),
+    ("l_shipmode", "Dict|BitPack"), ("l_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]"),
     ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"), ("o_custkey", "BitPack"),
     ("o_orderstatus", "Dict|BitPack"), ("o_totalprice", "Float2Int|BitPack"), ("o_orderdate", "Dict|BitPack"),
     ("o_orderpriority", "Dict|BitPack"), ("o_clerk", "Dict|BitPack"), ("o_shippriority", "RLE|[BitPack,BitPack]"),
@@ -86,7 +86,7 @@ WORKLOADS = {
                          "BitPack],BitPack], l_quantity Dict|BitPack, l_discount Dict|BitPack)"),
     # BASELINE configs[2]: TPC-H SF=10 lineitem string columns (dictionary CHAR(n) + chunk-parallel LZ4)
     "config3": dict(sf=10.0, dtype="u8", cols=[("l_shipmode", "Dict|BitPack"), ("l_returnflag", "Dict|BitPack"),
-                                                ("l_comment", "Str|[LZ4(sub=16384),BitPack]")],
+                                                ("l_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]")],
                     desc="config 3: TPC-H SF={sf} lineitem string columns (l_shipmode/l_returnflag Dict|BitPack "
                          "CHAR(n), l_comment Str|[LZ4(16 KiB sub-chunks),BitPack])"),
     # NEXT-1 microbenchmark: the paper's ANS instance

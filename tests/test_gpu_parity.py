@@ -143,6 +143,7 @@ TPCH_CASES = [
     ("l_shipinstruct", "Dict|BitPack"),
     ("l_shipmode", "Dict|BitPack"),
     ("l_comment", "Str|[LZ4,BitPack]"),
+    ("l_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]"),  # the bench's cascade: liblz4 HC blocks (longer matches)
     ("l_comment", "Str|[Raw,BitPack]"),
     ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"),
     ("o_orderkey", "DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]"),                 # Table 2 O_ORDERKEY

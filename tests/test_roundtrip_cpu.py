@@ -25,6 +25,7 @@ CASCADES = [
     ("l_shipmode", "Dict|BitPack"),
     ("l_comment", "Str|[LZ4,BitPack]"),
     ("l_comment", "Str|[LZ4(sub=4096),BitPack]"),
+    ("l_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]"),
     ("l_comment", "Str|[Raw,BitPack]"),
     ("o_orderkey", "Delta|RLE|[BitPack,BitPack]"),
     ("o_custkey", "BitPack"),
