@@ -761,6 +761,7 @@ def main():
                     "how": "cdm_pipeline_launch + cdm_pipeline_results per step, host wall clock: every compressed "
                            "chunk copied H2D from pinned host and decoded, every chunk's error word read back",
                     "pcie_h2d_gbs_measured": round(h2d_alone, 1) if h2d_alone else None,
+                    "pcie_h2d_gbs_achieved_in_pipeline": round(tot_comp * args.steps / e2e_s / 1e9 / max(world, 1), 1),
                     "pcie_h2d_gbs_each_rank_alone": h2d_each, "pcie_h2d_gbs_all_ranks_concurrent": h2d_conc,
                     "bar_cr_x_0.8_x_pcie": round(cr * 0.8 * h2d_alone * (world if world > 1 else 1), 1)
                     if h2d_alone else None,

@@ -5,12 +5,11 @@
 // token lengths (P:276's presum).  Three launches per batch, all on the chunk-sequential family's stream:
 //   sd_sums   one CTA per 2048-token tile: stage the w-bit ids (coalesced), look up the lengths, tile sum;
 //   sd_scan   one CTA per descriptor: exclusive scan of its tile sums in place (a few thousand values);
-//   sd_expand one CTA per tile: ids -> (dictionary offset, length), block scan of the lengths gives every
-//             token's byte position in the tile; each thread assembles its tokens' bytes into 32-bit words
-//             in registers (4 dictionary bytes per step) and stores them into a shared image at the tile's
-//             global alignment (the image and the output agree mod 16), which leaves as aligned 16-byte
-//             stores, the two partial edge words byte by byte; tiles of more than kSdStage bytes store
-//             directly.  (Opt-in variants, measured slower: CDM_SD_SMEM=1, CDM_SD_EXPAND=2; see launch_strdict.)
+//   sd_expand_b (default) persistent CTAs over contiguous tile ranges with the chunk's dictionary in shared
+//             memory once per chunk; a block scan of the lengths places every token; each thread copies its 4
+//             tokens' bytes into a shared image at the tile's global alignment, which leaves as aligned 16-byte
+//             stores.  Tested alternatives (CDM_SD_EXPAND=1 / 2, measured slower): round 1's per-tile sd_expand
+//             (word assembly in registers, dictionary through L1) and the word-parallel sd_expand2.
 // The dictionary offsets were checked on the host (0, non-decreasing, ending at the token bytes), so a
 // token id < entries always names bytes inside the dictionary; an id >= entries sets CDM_ERR_DICT_INDEX and
 // expands to nothing; tokens that do not total the node's bytes set CDM_ERR_LENGTHS and a tile that would
@@ -342,6 +341,99 @@ __global__ void __launch_bounds__(kSdT2) sd_expand2_kernel(const __grid_constant
   }
 }
 
+// sd_expand_b (CDM_SD_EXPAND=3): persistent CTAs over contiguous tile ranges, the chunk's dictionary (offsets +
+// token bytes) in shared memory once per chunk, and the simplest possible copy: each thread moves its 4 tokens'
+// bytes one byte at a time from the shared dictionary into the shared output image (one LDS.U8 + one STS.U8 per
+// byte; no word assembly, no atomics: every image byte has one writer), which leaves as 16-byte stores.
+constexpr int kSdBT = 512;                  // threads per CTA
+constexpr int kSdBPer = kSdTile / kSdBT;    // 4 tokens per thread
+
+__global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constant__ SdBatch B) {
+  extern __shared__ __align__(16) uint32_t dyn_s[];  // stage image, then the dictionary (B.dict_smem > 0)
+  uint8_t* const stage_b = reinterpret_cast<uint8_t*>(dyn_s);
+  uint32_t* const dict_s = dyn_s + (kSdStage + 32) / 4;
+  __shared__ uint32_t ids_s[kIdsWords];
+  __shared__ uint64_t warp_s[kSdBT / 32];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (B.total_tiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * per, t1 = min(B.total_tiles, t0 + per);
+  int di = -1;
+  const uint32_t* offs = nullptr;
+  for (uint32_t gt = t0; gt < t1; gt++) {
+    const int dn = find_desc_sd(B, gt);
+    const SdDesc& D = B.d[dn];
+    __syncthreads();  // the previous tile is done with ids_s / the image (and the dictionary)
+    if (dn != di) {
+      di = dn;
+      offs = reinterpret_cast<const uint32_t*>(D.dict);
+      if (B.dict_smem) {
+        const uint4* src = reinterpret_cast<const uint4*>(D.dict);
+        const uint32_t bytes = 4u * (D.entries + 1u) + __ldg(offs + D.entries);
+        for (uint32_t i = tid; i < (bytes + 15) / 16; i += kSdBT) reinterpret_cast<uint4*>(dict_s)[i] = __ldg(src + i);
+        offs = dict_s;
+      }
+    }
+    const uint32_t lt = gt - D.tile0, g0 = lt * kSdTile;
+    const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
+    stage_bits<kSdBT>(ids_s, D.ids_packed, g0, nt, D.w);
+    const uint64_t O64 = __ldcg(D.tsum + lt);
+    __syncthreads();
+    uint32_t a[kSdBPer], len[kSdBPer];
+    uint32_t s = 0;
+#pragma unroll
+    for (int r = 0; r < kSdBPer; r++) {
+      a[r] = 0;
+      len[r] = 0;
+      const uint32_t k = tid * kSdBPer + r;
+      if (k < nt) {
+        const uint64_t id = D.id_base + extract_bits(ids_s, uint64_t(k) * D.w, D.w);
+        if (id < D.entries) {  // (an out-of-range id was reported by sd_sums: it expands to nothing)
+          a[r] = offs[id];
+          len[r] = offs[id + 1] - a[r];
+        }
+      }
+      s += len[r];
+    }
+    uint64_t T;
+    const uint32_t ex = uint32_t(block_excl_scan_u64<kSdBT>(s, warp_s, &T));
+    if (O64 + T > D.n_out) continue;  // inconsistent lengths (sd_scan reports them): never write outside
+    const uint32_t O = uint32_t(O64), Tt = uint32_t(T), sh = O & 15u;
+    const uint8_t* tb = reinterpret_cast<const uint8_t*>(offs + D.entries + 1u);  // token bytes
+    uint8_t* const out = D.out;
+    if (Tt > kSdStage) {  // long tokens: direct byte stores
+      uint32_t p = O + ex;
+#pragma unroll
+      for (int r = 0; r < kSdBPer; r++) {
+        for (uint32_t j = 0; j < len[r]; j++) out[p + j] = tb[a[r] + j];
+        p += len[r];
+      }
+      continue;
+    }
+    {  // image byte sh + q = tile byte q
+      uint32_t p = sh + ex;
+#pragma unroll
+      for (int r = 0; r < kSdBPer; r++) {
+        const uint8_t* src = tb + a[r];
+        for (uint32_t j = 0; j < len[r]; j++) stage_b[p + j] = src[j];
+        p += len[r];
+      }
+    }
+    __syncthreads();
+    const uint32_t end = sh + Tt, nw = (end + 15) / 16;
+    uint4* const ow = reinterpret_cast<uint4*>(out + (O - sh));
+    const uint4* const swp = reinterpret_cast<const uint4*>(stage_b);
+    for (uint32_t i = tid; i < nw; i += kSdBT) {
+      const uint32_t lo16 = 16 * i, hi16 = lo16 + 16;
+      if (lo16 >= sh && hi16 <= end) {
+        ow[i] = swp[i];
+      } else {  // an edge word shared with the neighbouring tiles: only this tile's bytes
+        uint8_t* const ob = reinterpret_cast<uint8_t*>(ow + i);
+        for (uint32_t q = max(lo16, sh); q < min(hi16, end); q++) ob[q - lo16] = stage_b[q];
+      }
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
@@ -353,22 +445,27 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
     cudaFuncSetAttribute(sd_expand2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 32 + kSdDictSmem);
     configured[dev] = true;
   }
-  // default: every kernel reads the dictionary through L1 (random tokens cost one wavefront per distinct
-  // line).  CDM_SD_SMEM=1: sd_expand copies the dictionary into shared memory per tile -- measured slower
-  // (2.4 vs 1.6 ms for o_comment SF 10: the copy is 3.6x the tile's output); persistent CTAs that copy it
-  // once lost the latency hiding of 6 resident CTAs per SM (2.3 ms).
-  static const bool smem = std::getenv("CDM_SD_SMEM") && std::getenv("CDM_SD_SMEM")[0] == '1';
   SdBatch l1 = b;
   l1.dict_smem = 0;
   sd_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   sd_scan_kernel<<<b.n, kThreads, 0, s>>>(b);
-  // default: the per-thread-token expansion (sd_expand_kernel, 1.35 ms for o_comment SF 10; CDM_SD_SMEM=1
-  // with a per-tile shared dictionary); CDM_SD_EXPAND=2: the word-parallel sd_expand2_kernel (1.68 ms:
-  // ~100 instructions per output word, issue-bound at IPC 2.7 with 2 CTAs of 512 threads per SM)
-  static const int variant = std::getenv("CDM_SD_EXPAND") ? std::atoi(std::getenv("CDM_SD_EXPAND")) : 1;
-  if (variant != 2) {
-    if (smem && b.dict_smem) sd_expand_kernel<<<b.total_tiles, kThreads, b.dict_smem, s>>>(b);
-    else sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
+  // CDM_SD_EXPAND: 3 (default) sd_expand_b, 1 round 1's per-tile sd_expand (dictionary through L1; 1.62 ms for
+  // o_comment SF 10 vs 1.57), 2 the word-parallel sd_expand2 (1.68 ms)
+  static const int variant = std::getenv("CDM_SD_EXPAND") ? std::atoi(std::getenv("CDM_SD_EXPAND")) : 3;
+  if (variant == 3) {
+    static bool conf3[kMaxDevices] = {};
+    static int occ3[kMaxDevices] = {};
+    const int dev3 = current_device();
+    if (!conf3[dev3]) {
+      cudaFuncSetAttribute(sd_expand_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 32 + kSdDictSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3[dev3], sd_expand_b_kernel, kSdBT, kSdStage + 32 + kSdDictSmem);
+      if (occ3[dev3] < 1) occ3[dev3] = 1;
+      conf3[dev3] = true;
+    }
+    const uint32_t grid = std::min<uint32_t>(b.total_tiles, uint32_t(device_sms() * occ3[dev3]));
+    sd_expand_b_kernel<<<grid, kSdBT, kSdStage + 32 + b.dict_smem, s>>>(b);
+  } else if (variant != 2) {
+    sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   } else {
     const uint32_t dyn = kSdStage + 32 + b.dict_smem;
     sd_expand2_kernel<<<b.total_ctas, kSdT2, dyn, s>>>(b);

@@ -346,10 +346,10 @@ def test_strdict_long_tokens_and_empty_strings(engine):
     check_parity(engine, "Str|[StrDict|BitPack,BitPack]", one, both=False)
 
 
-@pytest.mark.parametrize("env", [{"CDM_SD_EXPAND": "2"}, {"CDM_SD_SMEM": "1"}])
+@pytest.mark.parametrize("env", [{"CDM_SD_EXPAND": "1"}, {"CDM_SD_EXPAND": "2"}])
 def test_strdict_expand_variants(env):
-    """the opt-in String-dictionary expansions -- the word-parallel sd_expand2 kernel (CDM_SD_EXPAND=2) and the
-    per-tile shared-memory dictionary (CDM_SD_SMEM=1) -- decode the same bytes (fresh process: env read once)"""
+    """the opt-in String-dictionary expansions -- round 1's per-tile sd_expand (CDM_SD_EXPAND=1) and the
+    word-parallel sd_expand2 (CDM_SD_EXPAND=2) -- decode the same bytes (fresh process: env read once)"""
     import subprocess
     import sys
     code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
