@@ -62,7 +62,8 @@ struct ScanDesc {
   uint16_t w;
   uint8_t out_bytes;      // DELTA: 4 or 8; OFFSETS: 4
   uint8_t mode;           // ScanMode
-  uint8_t pad[4];
+  uint32_t entries;       // DELTA with dict: dictionary entries
+  const uint64_t* dict;   // DELTA over Dict|BitPack (Table 2 PS_SUPPKEY): delta_i = dict[FOR + bits_i], else null
 };
 
 struct ScanBatch {

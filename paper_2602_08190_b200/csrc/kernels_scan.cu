@@ -2,6 +2,7 @@
 //
 //   DELTA   out[i] = base + sum_{k<=i} (FOR + bits_k)            (mod 2^bits)
 //   OFFSETS out[i] = sum_{k<i} (FOR + bits_k), out[n] = the total (lengths -> int32 offsets, reading R17)
+//   DELTA over Dict|BitPack (Table 2 PS_SUPPKEY): the k-th delta is dict[FOR + bits_k]
 //
 // The paper decodes delta with PyTorch's cumsum as a separate pass.  Here the unpack is
 // fused into the scan, in one of two schedules (NEXT-3 knob TUNE_SCAN_MODE):
@@ -63,7 +64,12 @@ __global__ void __launch_bounds__(kThreads) scan_sums_kernel(const __grid_consta
   constexpr uint32_t kPerS = kScanTile / kThreads;  // 16 fields per thread
   const uint32_t i0 = tid * kPerS, i1 = min(valid, i0 + kPerS);
   uint64_t acc = 0;
-  if (w && i0 < i1) {
+  if (D.dict) {  // Delta|Dict|BitPack: the deltas are dictionary entries (an index out of range adds 0)
+    for (uint32_t i = i0; i < i1; i++) {
+      const uint64_t ix = D.for_base + (w ? extract_bits_global(wd, uint64_t(i) * w, w) : 0ull);
+      if (ix < D.entries) acc += __ldg(D.dict + ix);
+    }  // scan_tile flags it (the look-back schedule has no sums pass)
+  } else if (w && i0 < i1) {
     if (w <= 32) {
       const uint32_t m = w == 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
       uint32_t q = (i0 * w) >> 5, sh = (i0 * w) & 31;
@@ -84,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) scan_sums_kernel(const __grid_consta
       for (uint32_t i = i0; i < i1; i++) acc += extract_bits_global(wd, uint64_t(i) * w, w);
     }
   }
-  acc += D.for_base * uint64_t(i1 > i0 ? i1 - i0 : 0u);
+  if (!D.dict) acc += D.for_base * uint64_t(i1 > i0 ? i1 - i0 : 0u);
   uint64_t tot;
   block_excl_scan_u64<kThreads>(acc, warp_s, &tot);
   if (tid == 0) B.tsum[gt] = tot;
@@ -114,7 +120,20 @@ __device__ __forceinline__ void scan_tile(const ScanBatch& B, const ScanDesc& D,
   T v[kPer + 1];
   T run = 0;
   const uint32_t i0 = tid * kPer;
-  if (!W64 || w <= 32) {
+  if (D.dict) {  // Delta|Dict|BitPack: an out-of-range index adds 0 and sets CDM_ERR_DICT_INDEX
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+      T f = 0;
+      if (i0 + j < valid) {
+        const uint64_t ix = D.for_base + extract_bits(wd, uint64_t(i0 + j) * w, w);
+        if (ix < D.entries) f = T(__ldg(D.dict + ix)); else bad = true;
+      }
+      v[j] = run;
+      run += f;
+    }
+    if (bad) atomicOr(B.err + D.err_idx, 0x1u);
+  } else if (!W64 || w <= 32) {
     // a two-word bit window slides over the thread's 16 fields (one shared load per 32 bits consumed)
     uint32_t q = (i0 * w) >> 5, sh = (i0 * w) & 31;
     uint32_t lo = wd[q], hi = wd[q + 1];

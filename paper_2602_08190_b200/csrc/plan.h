@@ -219,6 +219,12 @@ inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* er
   if (is(r, DICT) && bp(kid(r, 1))) { p->kind = PlanKind::Fp; p->fp_mode = 1; p->text = "fp(unpack+FOR+dict gather)"; return true; }
   if (is(r, FLOAT2INT) && bp(kid(r, 0))) { p->kind = PlanKind::Fp; p->fp_mode = 2; p->text = "fp(unpack+FOR+float2int)"; return true; }
   if (is(r, DELTA) && bp(kid(r, 0))) { p->kind = PlanKind::Scan; p->text = "scan(unpack+FOR+delta, decoupled look-back)"; return true; }
+  // Table 2's PS_SUPPKEY (reading R36): the deltas are Dict|BitPack-coded; the gather fuses into the scan
+  if (is(r, DELTA) && is(kid(r, 0), DICT) && bp(kid(kid(r, 0), 1))) {
+    p->kind = PlanKind::Scan; p->fp_mode = 1;
+    p->text = "scan(unpack+FOR+dict gather+delta)";
+    return true;
+  }
   auto is_delta_rle = [&](const TNode* t) {
     return is(t, DELTA) && is(kid(t, 0), RLE) && bp(kid(kid(t, 0), 0)) && bp(kid(kid(t, 0), 1));
   };
@@ -231,24 +237,42 @@ inline bool compile_plan(const TNode* r, uint8_t dtype, Plan* p, std::string* er
   // with BitPack counts whose values are BitPack, (top-level RLE only) Dict|BitPack or Float2Int|BitPack, or a
   // lower level -- Delta|RLE arithmetic runs or another RLE / DeltaStride node -- up to 3 levels (Table 2's
   // L_ORDERKEY).  Each non-final level expands into an L2-resident array the next level reads.
+  // The counts may themselves be an RLE-family node (Table 2's PS_PARTKEY `RLE|[DeltaStride, RLE]`): a
+  // lower level expands them into an L2-resident u32 array.  Depth = the longest chain; at most 3.
   std::function<int(const TNode*, bool)> levels = [&](const TNode* t, bool top) -> int {
     if (is_delta_rle(t)) return 1;
-    if (!(is(t, RLE) || is(t, DSTRIDE)) || !bp(kid(t, 1))) return 0;
+    if (!(is(t, RLE) || is(t, DSTRIDE))) return 0;
+    const TNode* cn = kid(t, 1);
+    int cd = 0;
+    if (!bp(cn)) {
+      cd = levels(cn, false);
+      if (!cd) return 0;
+    }
     const TNode* v = kid(t, 0);
-    if (bp(v)) return 1;
-    if (top && is(t, RLE) && ((is(v, DICT) && bp(kid(v, 1))) || (is(v, FLOAT2INT) && bp(kid(v, 0))))) return 1;
-    const int below = levels(v, false);
-    return below && below < 3 ? below + 1 : 0;
+    int vd = 0;
+    if (!bp(v)) {
+      if (top && is(t, RLE) && ((is(v, DICT) && bp(kid(v, 1))) || (is(v, FLOAT2INT) && bp(kid(v, 0))))) {
+        if (cd) return 0;  // dictionary / Float2Int values take the single-level path only
+        return 1;
+      }
+      vd = levels(v, false);
+      if (!vd) return 0;
+    }
+    const int below = vd > cd ? vd : cd;
+    return below < 3 ? below + 1 : 0;
   };
+  auto counts_lineage = [&](const TNode* t) { return (is(t, RLE) || is(t, DSTRIDE)) && !bp(kid(t, 1)); };
   if (const int nl = levels(r, true)) {
     const TNode* v = kid(r, 0);
     p->kind = PlanKind::Rle;
     const char* what = is(r, DSTRIDE) ? "arithmetic runs start + j*stride" : "expand";
     if (nl > 1) {
       p->vmode = 3;
-      p->text = std::string(nl == 3 ? "rle level 0 + rle level 1" : "rle level 0") +
-                " (value lineage -> run values in L2) + rle level " + std::to_string(nl - 1) + " (" + what +
-                ", values = previous level's array)";
+      const bool vl = !bp(v), cl = counts_lineage(r);
+      p->text = std::string("rle lineage levels") + (vl ? " (run values -> u64 array in L2)" : "") +
+                (cl ? " (run counts -> u32 array in L2)" : "") + " + rle level " + std::to_string(nl - 1) +
+                " (" + what + (vl ? ", values = a lower level's array" : "") +
+                (cl ? ", counts = a lower level's array" : "") + ")";
     } else if (bp(v)) {
       p->vmode = 0; p->text = std::string("rle(unpack counts+values, ") + what + ")";
     } else if (is(v, DICT)) {

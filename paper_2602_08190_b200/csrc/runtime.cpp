@@ -128,6 +128,9 @@ struct RleLevel {
   bool strided = false;   // DeltaStride node: row j of run g = value_g + j * stride
   uint64_t delta_base = 0, stride = 0;
   uint32_t n = 0, nruns = 0, max_run = 0;
+  int val_src = -1;       // V_RAW: the level (index into Bound::lv) whose u64 output holds the run values
+  int cnt_src = -1;       // counts lineage (Table 2 PS_PARTKEY): the level whose u32 output holds the counts
+  bool as_counts = false; // this level's output is another level's counts (written as u32)
 };
 
 struct Bound {
@@ -303,6 +306,17 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
     case PlanKind::Scan: {
       if (!need_w48()) return fail(CDM_E_UNSUPPORTED, "Delta output width must be 4 or 8");
       b->delta_base = r.u64_at8();
+      if (b->fp_mode == FP_DICT) {  // Delta|Dict|[Raw entries (8-byte deltas), BitPack indices]
+        const int di = t.kids[0][0];
+        const Node& dn = c.nodes[di];
+        uint64_t n;
+        if (dn.n != c.rows) return bad("Dict child count mismatch");
+        if (!(e = raw_stream(c, t, t.kids[di][0], 8, &b->dict_off, &n)).empty()) return bad(e);
+        b->entries = dn.u32_at0();
+        if (dn.u32_at4() != 8 || n != b->entries) return bad("delta dictionary shape mismatch");
+        if (!(e = bind_bp(c, t, t.kids[di][1], c.rows, 64, &b->main)).empty()) return bad(e);
+        break;
+      }
       if (!(e = bind_bp(c, t, t.kids[0][0], c.rows, 64, &b->main)).empty()) return bad(e);
       break;
     }
@@ -330,7 +344,18 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
           L.max_run = nd.u32_at4();
           if (nd.codec == DSTRIDE) { L.strided = true; L.stride = nd.u64_at8(); }
           vi = t.kids[ni][0];
-          if (!(er = bind_bp(c, t, t.kids[ni][1], L.nruns, 32, &L.cnt)).empty()) return er;
+          const int ci = t.kids[ni][1];
+          if (c.nodes[ci].codec == RLE || c.nodes[ci].codec == DSTRIDE || c.nodes[ci].codec == DELTA) {
+            // the counts are themselves RLE-family coded: a lower level expands them into a u32 array that this
+            // level reads as 32-bit packed counts (FOR 0)
+            if (c.nodes[ci].n != L.nruns) return "RLE counts count mismatch";
+            if (!(er = level(ci, L.nruns, false)).empty()) return er;
+            L.cnt_src = int(b->lv.size()) - 1;
+            b->lv.back().as_counts = true;
+            L.cnt.n = L.nruns; L.cnt.w = 32; L.cnt.base = 0; L.cnt.off = 0;
+          } else if (!(er = bind_bp(c, t, ci, L.nruns, 32, &L.cnt)).empty()) {
+            return er;
+          }
           const Node& v = c.nodes[vi];
           if (v.n != L.nruns) return "RLE values count mismatch";
           if (v.codec == BITPACK) {
@@ -352,6 +377,7 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
           } else {  // a lower level produces this level's run values
             L.vmode = V_RAW;
             if (!(er = level(vi, L.nruns, false)).empty()) return er;
+            L.val_src = int(b->lv.size()) - 1;
           }
         }
         // rows without runs would leave the level's output unwritten with no tile to notice
@@ -363,7 +389,7 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
         if (e[0] == '!') return fail(CDM_E_UNSUPPORTED, e.substr(1));
         return bad(e);
       }
-      if (b->lv.size() > 3) return bad("RLE lineage deeper than 3 levels");
+      if (b->lv.size() > 4) return bad("RLE lineage of more than 4 levels");
       break;
     }
     case PlanKind::Ans: {
@@ -499,7 +525,9 @@ struct cdm_batch {
   std::vector<ScanBatch> scan;
   std::vector<SumsBatch> sums;
   std::vector<RleBatch> rle;
-  size_t rle_level0 = 0;  // rle[0, rle_level0) are level-0 (Delta|RLE value lineage) launches
+  std::vector<int> sums_phase;  // per sums batch: -1 = before round 0, r = right after round r's expansions
+  std::vector<int> rle_round;   // per rle batch: its round
+  size_t rle_level0 = 0;  // rle[0, rle_level0) are launches of the value / counts lineages (non-final rounds)
   std::vector<Lz4Batch> lz4;
   std::vector<uint32_t> lz4_max_sub;
   std::vector<AnsBatch> ans;  // runs on the chunk-sequential (LZ4) family stream
@@ -570,7 +598,7 @@ bool getenv_flag(const char* name) {
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
   B->fp.clear(); B->fp_maxw.clear(); B->fp_char.clear();
-  for (auto& kb : B->k_bytes) kb = 0; B->scan.clear(); B->sums.clear(); B->rle.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
+  for (auto& kb : B->k_bytes) kb = 0; B->scan.clear(); B->sums.clear(); B->rle.clear(); B->sums_phase.clear(); B->rle_round.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
   B->ans.clear(); B->sd.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
@@ -668,6 +696,10 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         d.out = b.offs; d.base = b.payload; d.out_bytes = 4; d.mode = SCAN_OFFSETS;
       } else {
         d.out = b.out; d.base = b.delta_base; d.out_bytes = uint8_t(b.W); d.mode = SCAN_DELTA;
+        if (b.fp_mode == FP_DICT) {
+          d.dict = reinterpret_cast<const uint64_t*>(b.dev_chunk + b.dict_off);
+          d.entries = b.entries;
+        }
       }
       tiles += d.ntiles;
     }
@@ -677,55 +709,81 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     B->scan.push_back(sb);
     scan_tiles.push_back(tiles);
   }
-  // RLE units: one per expansion level of each RLE job (deepest first).  A non-final level (the value lineage
-  // of Delta|RLE or DeltaStride nodes) expands into an L2-resident u64 array that the job's next level reads as
-  // V_RAW.  Units run in rounds aligned at the end (every job's final level in the last round); every unit has
-  // its own tile sums / prefixes, and each round's launches follow the previous round's (PDL-chained).
-  struct RleUnit { int job; int level; int round; bool final; };
+  // RLE units: one per expansion level of each RLE job (deepest first).  A non-final level expands into an
+  // L2-resident array that a later level of the job reads: its run values (u64, V_RAW; the value lineage of
+  // Delta|RLE or DeltaStride nodes) or its run counts (u32, read as 32-bit packed counts; Table 2's PS_PARTKEY).
+  // A level's depth is 1 + the deepest level it reads; units run in rounds by depth, aligned at the end (every
+  // job's final level in the last round).  Every unit has its own tile sums / prefixes: rle_sums of a level
+  // whose counts are packed in the chunk run before round 0, those of a counts-lineage level right after the
+  // round that writes its counts.  Each round's expansions follow the previous launch (PDL-chained).
+  struct RleUnit { int job; int level; int round; int sums_phase; bool final; };
   std::vector<RleUnit> units;
+  std::vector<int> job_unit0(B->jobs.size(), -1);
   int rounds = 0;
-  for (int j : rlj) rounds = std::max(rounds, int(B->jobs[j].lv.size()));
-  for (int j : rlj) {
-    const int nl = int(B->jobs[j].lv.size());
-    for (int l = 0; l < nl; l++) units.push_back({j, l, rounds - nl + l, l == nl - 1});
+  {
+    std::vector<std::vector<int>> depth(B->jobs.size());
+    for (int j : rlj) {
+      const auto& lv = B->jobs[j].lv;
+      auto& dp = depth[j];
+      dp.assign(lv.size(), 1);
+      for (size_t l = 0; l < lv.size(); l++) {
+        if (lv[l].val_src >= 0) dp[l] = std::max(dp[l], dp[lv[l].val_src] + 1);
+        if (lv[l].cnt_src >= 0) dp[l] = std::max(dp[l], dp[lv[l].cnt_src] + 1);
+      }
+      rounds = std::max(rounds, dp.back());
+    }
+    for (int j : rlj) {
+      const auto& lv = B->jobs[j].lv;
+      const auto& dp = depth[j];
+      const int nl = int(lv.size()), shift = rounds - dp.back();
+      job_unit0[j] = int(units.size());
+      for (int l = 0; l < nl; l++) {
+        const int ph = lv[l].cnt_src >= 0 ? shift + dp[lv[l].cnt_src] - 1 : -1;
+        units.push_back({j, l, shift + dp[l] - 1, ph, l == nl - 1});
+      }
+    }
   }
-  auto unit_groups = [&](int round) {  // unit indices (round -1: all), <= kMaxBatch per group
+  auto lvl = [&](int u) -> const RleLevel& { return B->jobs[units[u].job].lv[units[u].level]; };
+  auto unit_groups = [&](auto key, int k) {  // unit indices with key(u) == k, <= kMaxBatch per group
     std::vector<std::vector<int>> g;
     for (int u = 0; u < int(units.size()); u++) {
-      if (round >= 0 && units[u].round != round) continue;
+      if (key(u) != k) continue;
       if (g.empty() || g.back().size() == size_t(kMaxBatch)) g.emplace_back();
       g.back().push_back(u);
     }
     return g;
   };
-  auto lvl = [&](int u) -> const RleLevel& { return B->jobs[units[u].job].lv[units[u].level]; };
   std::vector<std::pair<int, int>> sums_at(units.size()), rle_at(units.size());  // (batch, desc) per unit
-  for (auto& g : unit_groups(-1)) {
-    SumsBatch sb{};
-    sb.err = B->err_dev;
-    uint32_t nunits = 0;
-    for (int u : g) {
-      const Bound& b = B->jobs[units[u].job];
-      const RleLevel& L = lvl(u);
-      sums_at[u] = {int(B->sums.size()), int(sb.n)};
-      SumsChunk& d = sb.d[sb.n++];
-      d.cnt_packed = b.dev_chunk + L.cnt.off; d.cnt_base = L.cnt.base; d.cnt_w = uint16_t(L.cnt.w);
-      d.linear = L.vmode == V_LINEAR;
-      if (d.linear) { d.dv_packed = b.dev_chunk + L.val.off; d.dv_base = L.val.base; d.dv_w = uint16_t(L.val.w); }
-      d.nruns = L.nruns;
-      d.rows = L.n;
-      d.tiles = uint32_t(div_up(d.nruns, kRleTile));
-      d.units = uint32_t(div_up(uint64_t(d.tiles) * kRleTile, 8192));  // rle_sums CTA: 8 warps x 1024 runs
-      d.unit0 = nunits;
-      d.err_idx = uint32_t(units[u].job);
-      nunits += d.units;
+  for (int ph = -1; ph < rounds - 1; ph++) {
+    for (auto& g : unit_groups([&](int u) { return units[u].sums_phase; }, ph)) {
+      SumsBatch sb{};
+      sb.err = B->err_dev;
+      uint32_t nunits = 0;
+      for (int u : g) {
+        const Bound& b = B->jobs[units[u].job];
+        const RleLevel& L = lvl(u);
+        sums_at[u] = {int(B->sums.size()), int(sb.n)};
+        SumsChunk& d = sb.d[sb.n++];
+        d.cnt_packed = L.cnt_src >= 0 ? nullptr : b.dev_chunk + L.cnt.off;  // lineage counts: assigned below
+        d.cnt_base = L.cnt.base; d.cnt_w = uint16_t(L.cnt.w);
+        d.linear = L.vmode == V_LINEAR;
+        if (d.linear) { d.dv_packed = b.dev_chunk + L.val.off; d.dv_base = L.val.base; d.dv_w = uint16_t(L.val.w); }
+        d.nruns = L.nruns;
+        d.rows = L.n;
+        d.tiles = uint32_t(div_up(d.nruns, kRleTile));
+        d.units = uint32_t(div_up(uint64_t(d.tiles) * kRleTile, 8192));  // rle_sums CTA: 8 warps x 1024 runs
+        d.unit0 = nunits;
+        d.err_idx = uint32_t(units[u].job);
+        nunits += d.units;
+      }
+      sb.total_units = nunits;
+      B->sums.push_back(sb);
+      B->sums_phase.push_back(ph);
     }
-    sb.total_units = nunits;
-    B->sums.push_back(sb);
   }
   for (int round = 0; round < rounds; round++) {
     if (round == rounds - 1) B->rle_level0 = B->rle.size();
-    for (auto& g : unit_groups(round)) {
+    for (auto& g : unit_groups([&](int u) { return units[u].round; }, round)) {
       RleBatch rb{};
       rb.err = B->err_dev;
       uint32_t tiles = 0, slots = 0;
@@ -734,7 +792,8 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         const RleLevel& L = lvl(u);
         rle_at[u] = {int(B->rle.size()), int(rb.n)};
         RleDesc& d = rb.d[rb.n++];
-        d.cnt_packed = b.dev_chunk + L.cnt.off; d.cnt_base = L.cnt.base; d.cnt_w = uint16_t(L.cnt.w);
+        d.cnt_packed = L.cnt_src >= 0 ? nullptr : b.dev_chunk + L.cnt.off;  // lineage counts: assigned below
+        d.cnt_base = L.cnt.base; d.cnt_w = uint16_t(L.cnt.w);
         d.val_packed = L.vmode == V_RAW ? nullptr : b.dev_chunk + L.val.off;  // V_RAW: assigned below
         d.val_base = L.val.base;
         d.val_w = uint16_t(L.val.w);
@@ -746,7 +805,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         d.stride = L.stride;
         d.delta_base = L.delta_base;
         d.out = units[u].final ? b.out : nullptr;  // non-final: the level's array, assigned below
-        d.out_bytes = units[u].final ? uint8_t(b.W) : uint8_t(8);
+        d.out_bytes = units[u].final ? uint8_t(b.W) : L.as_counts ? uint8_t(4) : uint8_t(8);
         d.n = L.n;
         d.nruns = L.nruns;
         d.tile0 = tiles;
@@ -769,6 +828,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
       rb.big.done = A.take<uint32_t>(1);
       rb.big.max_slots = slots;
       B->rle.push_back(rb);
+      B->rle_round.push_back(round);
     }
   }
   *zero_bytes = (A.off + 15) & ~size_t(15);  // launch_zero works in 16-byte words (the next take pads to 256)
@@ -785,11 +845,20 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     d.tsum = A.take<uint64_t>(size_t(d.tiles + d.units) * 2);  // tile sums, then one sum per rle_sums group
     B->rle[rle_at[u].first].d[rle_at[u].second].tsum = d.tsum;
   }
-  for (size_t u = 0; u < units.size(); u++) {
-    if (units[u].final) continue;  // units u, u + 1 are consecutive levels of one job
+  for (size_t u = 0; u < units.size(); u++) {  // each non-final level's array, wired to the level that reads it
+    if (units[u].final) continue;
     uint64_t* V = A.take<uint64_t>(size_t(lvl(int(u)).n) + 4);
     B->rle[rle_at[u].first].d[rle_at[u].second].out = V;
-    B->rle[rle_at[u + 1].first].d[rle_at[u + 1].second].val_packed = reinterpret_cast<const uint8_t*>(V);
+    const auto& lv = B->jobs[units[u].job].lv;
+    for (size_t l = 0; l < lv.size(); l++) {
+      const int c = job_unit0[units[u].job] + int(l);
+      if (lv[l].val_src == units[u].level)
+        B->rle[rle_at[c].first].d[rle_at[c].second].val_packed = reinterpret_cast<const uint8_t*>(V);
+      if (lv[l].cnt_src == units[u].level) {
+        B->rle[rle_at[c].first].d[rle_at[c].second].cnt_packed = reinterpret_cast<const uint8_t*>(V);
+        B->sums[sums_at[c].first].d[sums_at[c].second].cnt_packed = reinterpret_cast<const uint8_t*>(V);
+      }
+    }
   }
   for (auto& rb : B->rle) {
     rb.big.entries = A.take<RleBig::Entry>(rb.big.max_slots);
@@ -905,10 +974,10 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         B->k_bytes[b.casc->dtype == T_FIXED ? K_FPC : K_FP] +=
             packed(b.main) + uint64_t(b.entries) * (b.fp_mode == FP_DICT ? b.W : 0) + b.payload;
         break;
-      case PlanKind::Scan: B->k_bytes[K_SCAN] += packed(b.main) + b.payload; break;
+      case PlanKind::Scan: B->k_bytes[K_SCAN] += packed(b.main) + b.payload + (b.fp_mode == FP_DICT ? 8ull * b.entries : 0); break;
       case PlanKind::Rle: {
         uint64_t in = 0;
-        for (const RleLevel& L : b.lv) in += packed(L.cnt) + (L.vmode == V_RAW ? 0 : packed(L.val));
+        for (const RleLevel& L : b.lv) in += (L.cnt_src >= 0 ? 0 : packed(L.cnt)) + (L.vmode == V_RAW ? 0 : packed(L.val));
         if (b.lv.back().vmode == V_DICT) in += uint64_t(b.entries) * b.W;
         B->k_bytes[K_RLE_L1] += in + b.payload;
         break;
@@ -1018,12 +1087,17 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
           n++; B->fam_launches[F_SCAN]++;
         }
         break;
-      case F_RLE:
-        // sums -> expand (level-0 batches first); the expansions are programmatically dependent launches
-        for (size_t i = 0; i < B->sums.size() && !st; i++) {
-          st = timed(K_RLE_SUMS, [&] { return launch_rle_sums(B->sums[i], fs); });
-          n++; B->fam_launches[F_RLE]++;
-        }
+      case F_RLE: {
+        // sums -> expand, round by round (lineage rounds first); the expansions are programmatically dependent
+        // launches; a counts-lineage level's sums follow the round that wrote its counts
+        size_t si = 0;
+        auto sums_upto = [&](int phase) {
+          for (; si < B->sums.size() && B->sums_phase[si] <= phase && !st; si++) {
+            st = timed(K_RLE_SUMS, [&] { return launch_rle_sums(B->sums[si], fs); });
+            n++; B->fam_launches[F_RLE]++;
+          }
+        };
+        sums_upto(-1);
         for (size_t i = 0; i < B->rle.size() && !st; i++) {
           auto& rb = B->rle[i];
           st = timed(i < B->rle_level0 ? K_RLE_L0 : K_RLE_L1, [&] { return launch_rle(rb, fs); });
@@ -1032,8 +1106,10 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
             st = timed(K_RLE_BIG, [&] { return launch_rle_big(rb, fs); });
             n++; B->fam_launches[F_RLE]++;
           }
+          if (i + 1 == B->rle.size() || B->rle_round[i + 1] != B->rle_round[i]) sums_upto(B->rle_round[i]);
         }
         break;
+      }
       case F_LZ4:  // the chunk-sequential family: LZ4 and range ANS
         for (size_t i = 0; i < B->lz4.size() && !st; i++) {
           st = timed(K_LZ4, [&] { return launch_lz4(B->lz4[i], B->lz4_max_sub[i], fs); });

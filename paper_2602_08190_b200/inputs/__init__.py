@@ -3,7 +3,7 @@
 Two families, both deterministic in their seed and shared by the CUDA path's tests/bench and the oracle's
 tests (DESIGN.md "Input recipe"):
 
-* dbgen-like TPC-H lineitem / orders columns from the native counter-based generator (tpch_gen.c);
+* dbgen-like TPC-H lineitem / orders / partsupp columns from the native counter-based generator (tpch_gen.c);
   any row range of any column is generated independently.
 * microbenchmark columns shaped like the paper's experiments: the config-1 int32 column, uniform
   w-bit columns (Fig. `bitcompVSnvcomp`), RLE group-size distributions even-X,
@@ -18,13 +18,14 @@ import numpy as np
 
 from .. import _native
 
-LINEITEM, ORDERS = 0, 1
+LINEITEM, ORDERS, PARTSUPP = 0, 1, 2
 
 LINEITEM_COLS = ["l_orderkey", "l_partkey", "l_suppkey", "l_linenumber", "l_quantity", "l_extendedprice",
                  "l_discount", "l_tax", "l_returnflag", "l_linestatus", "l_shipdate", "l_commitdate",
                  "l_receiptdate", "l_shipinstruct", "l_shipmode", "l_comment"]
 ORDERS_COLS = ["o_orderkey", "o_custkey", "o_orderstatus", "o_totalprice", "o_orderdate", "o_orderpriority",
                "o_clerk", "o_shippriority", "o_comment"]
+PARTSUPP_COLS = ["ps_partkey", "ps_suppkey", "ps_availqty", "ps_supplycost", "ps_comment"]
 
 # dtype tags of the CDM1 container / C-ABI: 0 I32, 1 I64, 2 F64, 3 FIXED, 4 VARBYTES
 I32, I64, F64, FIXED, VARBYTES = 0, 1, 2, 3, 4
@@ -39,6 +40,8 @@ COLUMN_TYPES = {
     "o_orderkey": (I64, 8), "o_custkey": (I32, 4), "o_orderstatus": (FIXED, 1), "o_totalprice": (F64, 8),
     "o_orderdate": (I32, 4), "o_orderpriority": (FIXED, 15), "o_clerk": (FIXED, 15),
     "o_shippriority": (I32, 4), "o_comment": (VARBYTES, 1),
+    "ps_partkey": (I32, 4), "ps_suppkey": (I32, 4), "ps_availqty": (I32, 4), "ps_supplycost": (F64, 8),
+    "ps_comment": (VARBYTES, 1),
 }
 
 NP_DTYPE = {I32: np.int32, I64: np.int64, F64: np.float64}
@@ -99,6 +102,8 @@ class TPCH:
             table, col = LINEITEM, LINEITEM_COLS.index(name)
         elif name in ORDERS_COLS:
             table, col = ORDERS, ORDERS_COLS.index(name)
+        elif name in PARTSUPP_COLS:
+            table, col = PARTSUPP, PARTSUPP_COLS.index(name)
         else:
             raise KeyError(name)
         total = self.rows(table)

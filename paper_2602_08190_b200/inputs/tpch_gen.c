@@ -11,7 +11,9 @@
  * dbgen's RNG streams:  orders = 1.5M*SF, sparse o_orderkey (first 8 of every 32), 1..7 lines per
  * order, l_partkey U[1,200k*SF], dbgen supplier formula, quantity U[1,50], discount U{0..10}/100,
  * tax U{0..8}/100, extendedprice = qty*retail(partkey) in cents, date rules around 1995-06-17,
- * grammar-text comments of length U[10,43] (lineitem) / U[19,78] (orders).
+ * grammar-text comments of length U[10,43] (lineitem) / U[19,78] (orders) / U[49,198] (partsupp);
+ * partsupp = 4 rows per part (800K*SF): ps_partkey, dbgen's ps_suppkey formula, availqty U[1,9999],
+ * supplycost U[100,100000] cents (Table 2's PS_PARTKEY / PS_SUPPKEY / PS_SUPPLYCOST rows).
  * Dates are date32 (days since 1970-01-01): 1992-01-01 = 8035, 1995-06-17 = 9298.
  * The paper pins: L_PARTKEY packs to 25 bits at SF=100, RLE counts are 12.5% of an
  * int64 L_ORDERKEY -> ~4 lines per order.
@@ -23,7 +25,7 @@
 
 #define EXPORT __attribute__((visibility("default")))
 
-enum { T_LINEITEM = 0, T_ORDERS = 1 };
+enum { T_LINEITEM = 0, T_ORDERS = 1, T_PARTSUPP = 2 };
 enum {  /* lineitem columns */
   L_ORDERKEY = 0, L_PARTKEY, L_SUPPKEY, L_LINENUMBER, L_QUANTITY, L_EXTENDEDPRICE, L_DISCOUNT, L_TAX,
   L_RETURNFLAG, L_LINESTATUS, L_SHIPDATE, L_COMMITDATE, L_RECEIPTDATE, L_SHIPINSTRUCT, L_SHIPMODE,
@@ -32,6 +34,9 @@ enum {  /* lineitem columns */
 enum {  /* orders columns */
   O_ORDERKEY = 0, O_CUSTKEY, O_ORDERSTATUS, O_TOTALPRICE, O_ORDERDATE, O_ORDERPRIORITY, O_CLERK,
   O_SHIPPRIORITY, O_COMMENT, O_NCOLS
+};
+enum {  /* partsupp columns: 4 rows per part, PS_PARTKEY = the part's key (TPC-H 4.2.3) */
+  PS_PARTKEY = 0, PS_SUPPKEY, PS_AVAILQTY, PS_SUPPLYCOST, PS_COMMENT, PS_NCOLS
 };
 
 #define STARTDATE 8035
@@ -49,7 +54,8 @@ static inline uint64_t splitmix64(uint64_t x) {
 /* field ids for the counter-based stream */
 enum { F_LINES = 1, F_CUST, F_ODATE, F_OPRIO, F_CLERK, F_OCOMLEN, F_OCOMOFF,
        F_PART = 16, F_SUPPI, F_QTY, F_DISC, F_TAX, F_SHIPD, F_COMMITD, F_RECEIPTD, F_RFLAG,
-       F_INSTR, F_MODE, F_LCOMLEN, F_LCOMOFF, F_POOL = 40 };
+       F_INSTR, F_MODE, F_LCOMLEN, F_LCOMOFF, F_AVAILQTY = 32, F_SUPPLYCOST, F_PSCOMLEN, F_PSCOMOFF,
+       F_POOL = 40 };
 
 typedef struct {
   double sf;
@@ -153,8 +159,14 @@ EXPORT void gen_destroy(void *p) {
   free(g);
 }
 
+static inline uint64_t n_parts(const gen_ctx *g) {
+  int64_t n = (int64_t)(200000.0 * g->sf);
+  return n < 1 ? 1 : (uint64_t)n;
+}
+
 EXPORT uint64_t gen_rows(void *p, int table) {
   gen_ctx *g = (gen_ctx *)p;
+  if (table == T_PARTSUPP) return 4 * n_parts(g);
   return table == T_LINEITEM ? g->n_lines : g->n_orders;
 }
 
@@ -162,7 +174,9 @@ EXPORT uint64_t gen_rows(void *p, int table) {
 EXPORT int gen_col_width(int table, int col) {
   static const int LW[L_NCOLS] = {8, 4, 4, 4, 8, 8, 8, 8, 1, 1, 4, 4, 4, 25, 10, 0};
   static const int OW[O_NCOLS] = {8, 4, 1, 8, 4, 15, 15, 4, 0};
+  static const int PW[PS_NCOLS] = {4, 4, 4, 8, 0};
   if (table == T_LINEITEM) return (col >= 0 && col < L_NCOLS) ? LW[col] : -1;
+  if (table == T_PARTSUPP) return (col >= 0 && col < PS_NCOLS) ? PW[col] : -1;
   return (col >= 0 && col < O_NCOLS) ? OW[col] : -1;
 }
 
@@ -268,6 +282,24 @@ EXPORT int gen_fixed(void *p, int table, int col, uint64_t row0, uint64_t nrows,
     }
     return 0;
   }
+  if (table == T_PARTSUPP) {
+    /* row r = part (r / 4) + 1, supplier slot i = r % 4; the supplier formula is dbgen's (4.2.3) */
+    if (row0 + nrows > 4 * n_parts(g)) return -1;
+    int64_t nsupp = (int64_t)(10000.0 * g->sf); if (nsupp < 4) nsupp = 4;
+    for (uint64_t r = row0; r < row0 + nrows; r++) {
+      uint8_t *d = dst + (r - row0) * (uint64_t)w;
+      const int64_t part = (int64_t)(r / 4) + 1, i = (int64_t)(r % 4);
+      int32_t i32; double f;
+      switch (col) {
+        case PS_PARTKEY: i32 = (int32_t)part; memcpy(d, &i32, 4); break;
+        case PS_SUPPKEY: i32 = (int32_t)((part + i * (nsupp / 4 + (part - 1) / nsupp)) % nsupp + 1); memcpy(d, &i32, 4); break;
+        case PS_AVAILQTY: i32 = (int32_t)unif(g, F_AVAILQTY, r, 1, 9999); memcpy(d, &i32, 4); break;
+        case PS_SUPPLYCOST: f = (double)unif(g, F_SUPPLYCOST, r, 100, 100000) / 100.0; memcpy(d, &f, 8); break;
+        default: return -1;
+      }
+    }
+    return 0;
+  }
   if (row0 + nrows > g->n_orders) return -1;
   int64_t ncust = (int64_t)(150000.0 * g->sf); if (ncust < 2) ncust = 2;
   int64_t nclerk = (int64_t)(1000.0 * g->sf); if (nclerk < 1) nclerk = 1;
@@ -317,8 +349,9 @@ EXPORT int gen_fixed(void *p, int table, int col, uint64_t row0, uint64_t nrows,
 EXPORT int gen_varbytes(void *p, int table, int col, uint64_t row0, uint64_t nrows, int64_t *offsets,
                         void *out, uint64_t *payload) {
   gen_ctx *g = (gen_ctx *)p;
-  if (!((table == T_LINEITEM && col == L_COMMENT) || (table == T_ORDERS && col == O_COMMENT))) return -1;
-  uint64_t nrow_tab = table == T_LINEITEM ? g->n_lines : g->n_orders;
+  if (!((table == T_LINEITEM && col == L_COMMENT) || (table == T_ORDERS && col == O_COMMENT) ||
+        (table == T_PARTSUPP && col == PS_COMMENT))) return -1;
+  uint64_t nrow_tab = gen_rows(p, table);
   if (row0 + nrows > nrow_tab) return -1;
   uint64_t o = 0; uint32_t l = 0;
   if (table == T_LINEITEM && nrows) { o = find_order(g, row0); l = (uint32_t)(row0 - lp(g, o)); }
@@ -331,6 +364,10 @@ EXPORT int gen_varbytes(void *p, int table, int col, uint64_t row0, uint64_t nro
       id = o * 8 + l; l++;
       len = unif(g, F_LCOMLEN, id, 10, 43);
       off = unif(g, F_LCOMOFF, id, 0, POOL_BYTES - 1 - 43);
+    } else if (table == T_PARTSUPP) {
+      id = row0 + r;
+      len = unif(g, F_PSCOMLEN, id, 49, 198);
+      off = unif(g, F_PSCOMOFF, id, 0, POOL_BYTES - 1 - 198);
     } else {
       id = row0 + r;
       len = unif(g, F_OCOMLEN, id, 19, 78);

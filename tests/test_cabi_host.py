@@ -43,7 +43,10 @@ def test_kernels_are_sm100a_sass():
     ("Float2Int|BitPack", cdm.F64, "fp(unpack+FOR+float2int)"),
     ("Delta|BitPack", cdm.I64, "scan("),
     ("RLE|[BitPack,BitPack]", cdm.I32, "rle("),
-    ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 0"),
+    ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "run values -> u64 array"),
+    ("RLE|[DeltaStride|[BitPack,BitPack],RLE|[BitPack,BitPack]]", cdm.I32, "run counts -> u32 array"),
+    ("RLE|[BitPack,RLE|[BitPack,BitPack]]", cdm.I64, "counts = a lower level's array"),
+    ("Delta|Dict|BitPack", cdm.I32, "dict gather+delta"),
     ("Delta|RLE|[BitPack,BitPack]", cdm.I64, "arithmetic runs"),
     ("DeltaStride|[BitPack,BitPack]", cdm.I64, "start + j*stride"),
     ("DeltaStride|[Delta|RLE|[BitPack,BitPack],BitPack]", cdm.I64, "rle level 1 (arithmetic runs"),

@@ -172,6 +172,11 @@ TPCH_CASES = [
     ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]"),      # Table 2 O_COMMENT (NEXT-2 String-dictionary)
     ("o_comment", "Str|[StrDict|BitPack|ANS(il=1),BitPack]"),
     ("l_comment", "Str|[StrDict|BitPack,BitPack]"),
+    ("ps_partkey", "RLE|[DeltaStride|[BitPack,BitPack],RLE|[BitPack,BitPack]]"),  # Table 2 PS_PARTKEY (R35)
+    ("ps_suppkey", "Delta|Dict|BitPack"),                                          # Table 2 PS_SUPPKEY (R36)
+    ("ps_supplycost", "Float2Int|BitPack"),
+    ("ps_availqty", "BitPack"),
+    ("ps_comment", "Str|[LZ4,BitPack]"),
 ]
 
 
@@ -328,6 +333,86 @@ def test_corrupt_dstride_counts_set_error(engine):
     ch = cdm1.build(root, cdm1.I64, 8, 64, cascade_hash=_hash(spec))
     (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.I64), [ch], resident=True, expect_error=True)
     assert r["error_bits"] & cdm.ERR_RUN_SUM
+
+
+def _counts_lineage_column(seed, nr, dtype=I64, arith=False):
+    """Run counts that are themselves run-length coded (counts repeat in runs of 1..60, a few far above the
+    big-tile limit), run values random (or an arithmetic sequence, arith=True)."""
+    rng = np.random.default_rng(seed)
+    cvals = rng.integers(1, 10, size=nr // 20 + 1)
+    cvals[rng.integers(0, cvals.size, size=3)] = rng.integers(5000, 40_000, size=3)
+    counts = np.repeat(cvals, rng.integers(1, 60, size=cvals.size))[:nr]
+    vals = np.arange(counts.size, dtype=np.int64) * 3 + 17 if arith else rng.integers(-(1 << 40), 1 << 40,
+                                                                                      size=counts.size)
+    vals[1:] += (vals[1:] == vals[:-1])  # adjacent runs differ (maximal runs)
+    v = np.repeat(vals, counts)
+    return Column("cl", dtype, 8 if dtype == I64 else 4, v.size, v.astype(np.int64 if dtype == I64 else np.int32))
+
+
+@pytest.mark.parametrize("spec,arith", [
+    ("RLE|[BitPack,RLE|[BitPack,BitPack]]", False),
+    ("RLE|[RLE|[BitPack,BitPack],RLE|[BitPack,BitPack]]", False),
+    ("RLE|[DeltaStride(stride=3)|[BitPack,BitPack],RLE|[BitPack,BitPack]]", True),
+    ("RLE|[DeltaStride(stride=3)|[Delta|RLE|[BitPack,BitPack],BitPack],RLE|[BitPack,BitPack]]", True),
+    ("RLE|[BitPack,DeltaStride(stride=0)|[BitPack,BitPack]]", False),
+    ("RLE|[BitPack,Delta|RLE|[BitPack,BitPack]]", False),
+])
+def test_counts_lineage(engine, spec, arith):
+    """Table 2 PS_PARTKEY's shape (R35): the outer RLE's counts come from a lower RLE-family level (a u32 array
+    in L2, its rle_sums launched after the round that writes it), next to a value lineage of depth 0-2; many
+    tiles, ragged chunks, giant runs, int64 and int32 output."""
+    col = _counts_lineage_column(5, 400_000, arith=arith)
+    check_parity(engine, spec, col, rows_per_chunk=1_500_007)
+    c32 = _counts_lineage_column(6, 60_000, dtype=I32, arith=arith)
+    check_parity(engine, spec, c32, rows_per_chunk=250_001, both=False)
+
+
+def test_ps_partkey_sf10_full(engine):
+    """PS_PARTKEY at SF 10 (8 M rows) under Table 2's cascade: each chunk holds ONE DeltaStride run and ONE counts
+    run of 1 M entries (both lineage levels are giant runs: rle_big), expanded into 4 M rows"""
+    col = TPCH(10).column("ps_partkey")
+    check_parity(engine, "RLE|[DeltaStride|[BitPack,BitPack],RLE|[BitPack,BitPack]]", col,
+                 rows_per_chunk=1 << 22, both=False)
+
+
+def test_corrupt_counts_lineage_sets_error(engine):
+    """a counts level whose own counts overrun its element count, and an outer level whose lineage counts do
+    not sum to its rows: both are CDM_ERR_RUN_SUM"""
+    spec = "RLE|[BitPack,RLE|[BitPack,BitPack]]"
+    for inner_counts, n in (([2, 3], 20), ([2, 2], 20), ([2, 3], 21)):  # 5 counts of 4 = 20 rows is the clean case
+        cn = cdm1.Node(cdm1.RLE, 5, [cdm1.bitpack([4, 4], 3, 0), cdm1.bitpack(inner_counts, 2, 0)], nruns=2, maxrun=3)
+        root = cdm1.Node(cdm1.RLE, n, [cdm1.bitpack([1, 2, 3, 4, 5], 3, 0), cn], nruns=5, maxrun=4)
+        ch = cdm1.build(root, cdm1.I64, 8, n, cascade_hash=_hash(spec))
+        exp_ok = inner_counts == [2, 3] and n == 20
+        (payload, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.I64), [ch], resident=True,
+                                      expect_error=not exp_ok)
+        if exp_ok:
+            assert r["error_bits"] == 0 and np.array_equal(payload, oracle.decode_chunk(ch)[0])
+        else:
+            assert r["error_bits"] & cdm.ERR_RUN_SUM
+
+
+@pytest.mark.parametrize("w", [1, 7, 13])
+def test_delta_dict_scan(engine, w, scan_mode):
+    """Table 2 PS_SUPPKEY's `Delta|Dict|BitPack` (R36): the deltas are dictionary entries gathered inside the scan
+    (both H6 schedules); 2^w distinct deltas incl. negative ones (wrapping), many tiles, int64 and int32"""
+    rng = np.random.default_rng(w)
+    d = rng.integers(-(1 << 30), 1 << 30, size=1 << w)
+    n = 700_001
+    x = np.cumsum(d[rng.integers(0, d.size, size=n)]) + 12345
+    check_parity(engine, "Delta|Dict|BitPack", Column("dd", I64, 8, n, x.astype(np.int64)), rows_per_chunk=300_007)
+    check_parity(engine, "Delta|Dict|BitPack", Column("dd32", I32, 4, n, x.astype(np.int32)), both=False)
+
+
+def test_delta_dict_bad_index_sets_error(engine, scan_mode):
+    spec = "Delta|Dict|BitPack"
+    n = 9000
+    dn = cdm1.Node(cdm1.DICT, n, [cdm1.raw(np.arange(5, dtype=np.int64).tobytes(), eb=8),
+                                  cdm1.bitpack([i % 7 for i in range(n)], 3, 0)], entries=5, E=8)
+    root = cdm1.Node(cdm1.DELTA, n, [dn], base=0)
+    ch = cdm1.build(root, cdm1.I64, 8, n, cascade_hash=_hash(spec))
+    (_, _, r), = gpu_decode(engine, cdm.Cascade(spec, cdm.I64), [ch], resident=True, expect_error=True)
+    assert r["error_bits"] & cdm.ERR_DICT_INDEX
 
 
 def test_strdict_long_tokens_and_empty_strings(engine):

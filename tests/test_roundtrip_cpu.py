@@ -34,6 +34,11 @@ CASCADES = [
     ("o_shippriority", "RLE|[BitPack,BitPack]"),
     ("o_comment", "Str|[LZ4,BitPack]"),
     ("o_orderdate", "RLE|[Dict|BitPack,BitPack]"),
+    ("ps_partkey", "RLE|[DeltaStride|[BitPack,BitPack],RLE|[BitPack,BitPack]]"),  # Table 2 PS_PARTKEY (R35)
+    ("ps_suppkey", "Delta|Dict|BitPack"),                                          # Table 2 PS_SUPPKEY (R36)
+    ("ps_supplycost", "Float2Int|BitPack"),                                        # Table 2 PS_SUPPLYCOST
+    ("ps_availqty", "BitPack"),
+    ("ps_comment", "Str|[LZ4,BitPack]"),
 ]
 
 
@@ -152,3 +157,21 @@ def test_cascade_canonical_forms():
     assert encoder.canonical("Dictionary encoding | Bit-packing") == "DICT|[RAW,BITPACK|RAW]"
     assert encoder.canonical("RLE") == "RLE|[RAW,RAW]"
     assert encoder.canonical("RLE | [Bit-packing, Bit-packing]") == "RLE|[BITPACK|RAW,BITPACK|RAW]"
+
+
+def test_partsupp_generator_shape():
+    """partsupp (TPC-H 4.2.3): 4 rows per part, ps_partkey = part key, the 4 suppliers of a part distinct and in
+    [1, S]; Table 2's PS_PARTKEY cascade keeps one DeltaStride run and one counts run per chunk of whole parts"""
+    g = TPCH(0.05)
+    pk = g.column("ps_partkey").data.astype(np.int64)
+    sk = g.column("ps_suppkey").data.astype(np.int64)
+    n = pk.size
+    assert n == 4 * 10_000
+    assert np.array_equal(pk, np.arange(n) // 4 + 1)
+    S = 500
+    assert sk.min() >= 1 and sk.max() <= S
+    assert all(len(set(sk[4 * p: 4 * p + 4])) == 4 for p in range(0, n // 4, 97))
+    col = g.column("ps_partkey")
+    ch = encoder.encode_chunks("RLE|[DeltaStride|[BitPack,BitPack],RLE|[BitPack,BitPack]]", col, 20_000)
+    assert len(ch) == 2 and all(c.size < 1024 for c in ch)  # 80 KB of keys -> a few hundred bytes per chunk
+    _check(col, ch)
