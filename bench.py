@@ -89,6 +89,14 @@ WORKLOADS = {
                                                 ("l_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]")],
                     desc="config 3: TPC-H SF={sf} lineitem string columns (l_shipmode/l_returnflag Dict|BitPack "
                          "CHAR(n), l_comment Str|[LZ4(16 KiB sub-chunks),BitPack])"),
+    # NEXT-2 Table 2's PS rows: partsupp at SF=100 (80 M rows), PS_PARTKEY RLE|[DeltaStride,RLE]
+    # (count lineage, R35), PS_SUPPKEY Delta|Dict|BitPack (R36), PS_SUPPLYCOST Float2Int|BitPack, plus the other two
+    "partsupp": dict(sf=100.0, dtype="mixed",
+                     cols=[("ps_partkey", "RLE|[DeltaStride|[BitPack,BitPack],RLE|[BitPack,BitPack]]"),
+                           ("ps_suppkey", "Delta|Dict|BitPack"), ("ps_availqty", "BitPack"),
+                           ("ps_supplycost", "Float2Int|BitPack"), ("ps_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]")],
+                     desc="partsupp: TPC-H SF={sf} partsupp, all 5 columns under Table 2's PS cascades, streamed "
+                          "from pinned host"),
     # NEXT-1 microbenchmark: the paper's ANS instance
     "ans": dict(sf=10.0, dtype="u8", cols=[("l_returnflag", "ANS(chunk=4096)"), ("l_linestatus", "ANS(chunk=4096)")],
                 desc="ANS: TPC-H SF={sf} lineitem l_returnflag + l_linestatus CHAR(1) under range ANS (4 KiB chunks)"),
@@ -745,8 +753,8 @@ def main():
                "chunks": tot_chunks, "decoded_bytes_per_step": tot_decoded, "compressed_bytes_per_step": tot_comp,
                "compression_ratio": round(cr, 3),
                "parallelism": f"dp{world}: one dataset, per-rank contiguous chunk ranges (strong scaling)",
-               "l2": "inputs (21.5 GB compressed at SF=100) and outputs exceed the 126 MB L2; the device-resident "
-                     "pass also flushes L2 (256 MiB write) before each step",
+               "l2": f"inputs ({tot_comp / 1e9:.1f} GB compressed) and outputs ({tot_decoded / 1e9:.1f} GB) exceed the "
+                     "126 MB L2; the device-resident pass also flushes L2 (256 MiB write) before each step",
                "timing": "value: CUDA events on the launching stream around each cdm_pipeline_launch (sum over "
                          "steps, max over ranks); e2e: host wall clock of launch + results",
                "host": {"cpus_bound": len(cpus), "build_s": round(ds.build_s, 1), "build_workers": ds.workers,

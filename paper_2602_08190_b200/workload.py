@@ -133,7 +133,7 @@ def _encode_into(job):
 def _row_count(g, name: str) -> int:
     if name == "config1":
         return 1_000_000
-    return g.rows(0 if name.startswith("l_") else 1)
+    return g.rows(0 if name.startswith("l_") else 2 if name.startswith("ps_") else 1)
 
 
 def build(columns, sf: float, seed: int, chunk_rows: int = 1 << 22, select=None, workers: int | None = None,
