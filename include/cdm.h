@@ -262,6 +262,12 @@ CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t c
  *   "lz4_lanes"       N.P. pattern's C: lanes cooperating on one LZ4 sub-chunk: 1 (default: the paper's thread
  *                     per chunk, lz4_thread_kernel), 2, 4, 8, 16 (lane groups) or 32 (one warp per sub-chunk);
  *                     env CDM_LZ4_G sets the start value
+ *   "lz4_split"       H8 schedule: 1 (default) = the split parse/copy kernel for latency-bound LZ4 launches (owner
+ *                     lanes parse sequence headers from a shared ring, the whole warp copies literals and matches
+ *                     32 sequences at a time) and the lz4_lanes schedule for throughput-bound ones; 0 = always
+ *                     lz4_lanes; env CDM_LZ4_SPLIT sets the start value
+ *   "lz4_split_g"     sub-chunks per warp of the split kernel: 0 (default) = by launch size (latency-bound launches
+ *                     only), 1, 2, 4 or 8 = always the split kernel with that many; env CDM_LZ4_SPLIT_G
  *   "gp_ctas_per_sm"  G.P. pattern's L (Table 3 G.P. row): resident rle_kernel CTAs per SM, 0 = the kernel's own
  *                     occupancy (default), 1..8 (enforced by padding the launch's dynamic shared memory)
  *   "scan_mode"       H6 schedule (single-pass look-back vs the 2-pass baseline): 0 =

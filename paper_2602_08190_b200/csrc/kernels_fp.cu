@@ -314,6 +314,8 @@ void tune_init() {
   g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 1;
   g_tune[TUNE_SCAN_MODE] = std::getenv("CDM_SCAN_MODE") ? std::atoi(std::getenv("CDM_SCAN_MODE")) : 0;
   g_tune[TUNE_GP_CTAS_PER_SM] = 0;
+  g_tune[TUNE_LZ4_SPLIT] = std::getenv("CDM_LZ4_SPLIT") ? std::atoi(std::getenv("CDM_LZ4_SPLIT")) : 1;
+  g_tune[TUNE_LZ4_SPLIT_G] = std::getenv("CDM_LZ4_SPLIT_G") ? std::atoi(std::getenv("CDM_LZ4_SPLIT_G")) : 0;
   g_tune_init = true;
 }
 }  // namespace

@@ -520,13 +520,416 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
   if (ge & 15u) flush(ge & ~uintptr_t(15));  // the partial last block
 }
 
+// ------------------------------------------------------------------------------------------ split parse / copy
+// The thread kernel's sub-chunk chain costs ~270 instructions per LZ4 sequence because one thread both parses
+// and copies.  This schedule splits the two (knob lz4_split): a warp owns G sub-chunks; per
+// round each owner lane (lane < G) parses the next kSplitR sequences of its sub-chunk -- only the header chain
+// (token, length extensions, offset), ~20 instructions per sequence -- into a shared record table
+// {output position, literal source, literal length, match offset}; then the whole warp copies the G x kSplitR
+// sequences 32 at a time, one sequence per lane: all literals first (compressed input -> output), then the
+// matches in dependency order (a match whose source overlaps the output of a lower lane's match in the same
+// sub-chunk waits for it; sources further back were written in earlier steps).  Output goes straight to
+// global memory with aligned word stores (byte stores at a sequence's unaligned edges: lanes write disjoint
+// byte ranges); match sources are read back through the SM's L1 after __syncwarp.  G is chosen per launch so
+// that the launch has about one wave of warps (few sub-chunks per launch: 2 per warp; many: 32).
+constexpr uint32_t kSplitWarps = 4;  // warps per CTA (G = 32: 35 KB of record tables per CTA, 5 CTAs per SM)
+
+__device__ __forceinline__ uint2 ld_v2_nc(const void* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+
+// bytes [a, a + k) (k <= 16) into v (little-endian words); only the 8-byte words holding them are read
+template <bool NC>
+__device__ __forceinline__ void load16(const uint8_t* a, uint32_t k, uint32_t (&v)[4]) {
+  const uintptr_t p = reinterpret_cast<uintptr_t>(a);
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(p & ~uintptr_t(7));
+  const uint32_t f = uint32_t(p & 7u);
+  const uint2 z = make_uint2(0u, 0u);
+  const uint2 x0 = NC ? ld_v2_nc(b) : ld_v2_global(b);
+  const uint2 x1 = f + k > 8 ? (NC ? ld_v2_nc(b + 8) : ld_v2_global(b + 8)) : z;
+  const uint2 x2 = f + k > 16 ? (NC ? ld_v2_nc(b + 16) : ld_v2_global(b + 16)) : z;
+  const bool hi = f >= 4;
+  const uint32_t sh = (f & 3u) * 8u;
+  const uint32_t w0 = hi ? x0.y : x0.x, w1 = hi ? x1.x : x0.y, w2 = hi ? x1.y : x1.x, w3 = hi ? x2.x : x1.y,
+                 w4 = hi ? x2.y : x2.x;
+  v[0] = __funnelshift_r(w0, w1, sh);
+  v[1] = __funnelshift_r(w1, w2, sh);
+  v[2] = __funnelshift_r(w2, w3, sh);
+  v[3] = __funnelshift_r(w3, w4, sh);
+}
+
+// 16 bytes at shared address a (any alignment; the 4 bytes after a + 16 must be readable)
+__device__ __forceinline__ void load16s(const uint8_t* a, uint32_t (&v)[4]) {
+  const uintptr_t p = reinterpret_cast<uintptr_t>(a);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(p & ~uintptr_t(3));
+  const uint32_t sh = uint32_t(p & 3u) * 8u;
+  const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+  v[0] = __funnelshift_r(w0, w1, sh);
+  v[1] = __funnelshift_r(w1, w2, sh);
+  v[2] = __funnelshift_r(w2, w3, sh);
+  v[3] = __funnelshift_r(w3, w4, sh);
+}
+
+// k <= 16 bytes of v to dst: whole aligned words with one 4-byte store, the edge words byte by byte (the
+// neighbouring bytes belong to other lanes' sequences)
+__device__ __forceinline__ void store16(uint8_t* dst, const uint32_t (&v)[4], uint32_t k) {
+  const uintptr_t p = reinterpret_cast<uintptr_t>(dst);
+  const int a = int(p & 3u);
+  uint32_t* base = reinterpret_cast<uint32_t*>(p & ~uintptr_t(3));
+  const uint32_t sh = 8u * uint32_t(a);
+  uint32_t u[5];
+  u[0] = v[0] << sh;
+  u[1] = __funnelshift_l(v[0], v[1], sh);
+  u[2] = __funnelshift_l(v[1], v[2], sh);
+  u[3] = __funnelshift_l(v[2], v[3], sh);
+  u[4] = sh ? (v[3] >> (32u - sh)) : 0u;
+#pragma unroll
+  for (int i = 0; i < 5; i++) {
+    const int lo = 4 * i - a;  // data byte index of the word's first byte
+    if (lo >= int(k) || lo + 4 <= 0) continue;
+    if (lo >= 0 && lo + 4 <= int(k)) {
+      base[i] = u[i];
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+        if (lo + b >= 0 && lo + b < int(k)) reinterpret_cast<uint8_t*>(base + i)[b] = uint8_t(u[i] >> (8 * b));
+    }
+  }
+}
+
+template <uint32_t G, uint32_t R, uint32_t F>
+__global__ void __launch_bounds__(kSplitWarps * 32, 5) lz4_split_kernel(const __grid_constant__ Lz4Batch B) {
+  static_assert(G >= 1 && G <= 8 && (G * R) % 32 == 0, "G sub-chunks per warp, R records each per round");
+  static_assert(F % 16 == 0 && (G * F / 16) % 32 == 0, "F refill bytes per sub-chunk: whole 16-byte blocks per lane");
+  constexpr uint32_t kRing = 2 * F;           // header ring per sub-chunk (bytes)
+  constexpr uint32_t kBlk = G * F / 16 / 32;  // refill blocks per lane per round
+  __shared__ __align__(16) uint4 rec_s[kSplitWarps][G][R + 1];
+  __shared__ __align__(16) uint8_t ring_s[kSplitWarps][G][kRing];
+  __shared__ uint32_t cnt_s[kSplitWarps][G];
+  __shared__ __align__(16) uint32_t scr_s[kSplitWarps * 32][8];  // a lane's replicated short match period
+  constexpr uint32_t kStg = R >= 32 ? 2048 : 1024;               // staging bytes per step segment
+  __shared__ __align__(16) uint8_t stg_s[kSplitWarps][32 / R][kStg + 48];  // 16 guard bytes before, 32 after
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t gs = (blockIdx.x * kSplitWarps + wib) * G + lane;  // owner lanes: lane < G
+  const bool live = lane < G && gs < B.total_subs;
+  const Lz4Desc& D = B.d[find_desc_lz4(B, live ? gs : B.total_subs - 1)];
+  const uint32_t s = gs - D.sub0;
+  const uint32_t* tab = reinterpret_cast<const uint32_t*>(D.table);
+  uint64_t off = 0;
+  if (live && D.uniform) off = uint64_t(s) * D.uniform;
+  {
+    // non-uniform sub-chunks: the sum of the preceding sub-chunks' lengths, the warp cooperating per owner
+    const uint32_t act = __ballot_sync(FULL, live && !D.uniform);
+    for (uint32_t L = 0; L < G; L++) {
+      if (!(act >> L & 1u)) continue;
+      const uint32_t sL = __shfl_sync(FULL, s, L);
+      const uint64_t tL = __shfl_sync(FULL, reinterpret_cast<uint64_t>(tab), L);
+      uint64_t acc = 0;
+      for (uint32_t k = lane; k < sL; k += 32) acc += __ldg(reinterpret_cast<const uint32_t*>(tL) + 3 * k + 2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+      if (lane == L) off = acc;
+    }
+  }
+  uint32_t co = 0, cl = 0, dl = 0;
+  bool bad = false;
+  if (live) {
+    co = __ldg(tab + 3 * s); cl = __ldg(tab + 3 * s + 1); dl = __ldg(tab + 3 * s + 2);
+    bad = uint64_t(co) + cl > D.payload_bytes || off + dl > D.n || (s + 1 == D.n_sub && off + dl != D.n);
+  }
+  const uint8_t* const in = live ? D.payload + co : D.payload;
+  uint8_t* const out = live ? D.out + off : D.out;
+  bool done = !live || bad;
+  uint4* const rec = rec_s[wib][lane < G ? lane : 0];
+  uint8_t* const scr = reinterpret_cast<uint8_t*>(scr_s[threadIdx.x]);
+  // The parse reads header bytes (tokens, length extensions, offsets) from a per-sub-chunk shared ring of
+  // kRing bytes that the whole warp refills F bytes at a time: the refill loads of round r are issued right
+  // after its parse and stored into the ring after its copy phase, so their latency hides behind the copies.
+  // Positions u are relative to `abase` (the 16-aligned address at or below the sub-chunk's first byte):
+  // the ring holds [fu - kRing, fu) (fu: the loaded frontier, a multiple of 16); blocks at or past the
+  // payload's padded end are never loaded.  Literal bytes are not read by the parse.
+  const uintptr_t abase = reinterpret_cast<uintptr_t>(in) & ~uintptr_t(15);
+  const uint32_t d0 = uint32_t(reinterpret_cast<uintptr_t>(in) & 15u);
+  const uintptr_t istop = (reinterpret_cast<uintptr_t>(D.payload) + D.payload_bytes + 31) & ~uintptr_t(15);
+  uint8_t* const ring = ring_s[wib][lane < G ? lane : 0];
+  uint32_t u = d0, ue = d0 + cl;  // parse position, end of the sub-chunk's input
+  uint32_t fu = 0;                // frontier (owner lanes)
+  uint32_t op = 0;
+  // refill request of each owner: the F bytes at [rq, rq + F) (rq = ~0u: none); the warp loads them
+  auto refill_issue = [&](uint32_t rq_own, uint4 (&blk)[kBlk]) {
+#pragma unroll
+    for (uint32_t i = 0; i < kBlk; i++) {
+      const uint32_t g = (i * 32 + lane) / (F / 16), bo = (i * 32 + lane) % (F / 16);
+      const uint32_t rq = __shfl_sync(FULL, rq_own, g);
+      const uint64_t ab = __shfl_sync(FULL, uint64_t(abase), g);
+      const uint64_t stop = __shfl_sync(FULL, uint64_t(istop), g);  // sub-chunk g's payload (its own chunk's)
+      const uintptr_t a = uintptr_t(ab) + rq + 16u * bo;
+      blk[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (rq != ~0u && a + 16 <= stop) blk[i] = __ldg(reinterpret_cast<const uint4*>(a));
+    }
+  };
+  auto refill_store = [&](uint32_t rq_own, const uint4 (&blk)[kBlk]) {
+#pragma unroll
+    for (uint32_t i = 0; i < kBlk; i++) {
+      const uint32_t g = (i * 32 + lane) / (F / 16), bo = (i * 32 + lane) % (F / 16);
+      const uint32_t rq = __shfl_sync(FULL, rq_own, g);
+      if (rq != ~0u)
+        *reinterpret_cast<uint4*>(&ring_s[wib][g][(rq + 16u * bo) & (kRing - 1)]) = blk[i];
+    }
+  };
+  {  // prologue: the first kRing bytes
+    uint4 blk[kBlk];
+    refill_issue(done ? ~0u : 0u, blk);
+    refill_store(done ? ~0u : 0u, blk);
+    refill_issue(done ? ~0u : F, blk);
+    refill_store(done ? ~0u : F, blk);
+    fu = kRing;
+    __syncwarp();
+  }
+  // header byte at position v >= u: from the ring below the frontier, else (a header past a long literal run,
+  // rare) straight from global memory
+  auto rb = [&](uint32_t v) -> uint32_t {
+    return v < fu ? uint32_t(ring[v & (kRing - 1)]) : uint32_t(__ldg(reinterpret_cast<const uint8_t*>(abase + v)));
+  };
+  for (;;) {
+    // ---- parse: up to R sequence headers per owner lane
+    uint32_t n = 0;
+    if (!done) {
+      for (; n < R; n++) {
+        // fast path: no length extension, not the last sequence, header bytes inside the ring (the common
+        // case: ~25 instructions, one load latency on the chain); everything else takes the general path
+        if (u + 17 <= fu && u + 3 <= ue) {
+          const uint32_t tok = ring[u & (kRing - 1)];
+          const uint32_t lit = tok >> 4, mlc = tok & 15u, v = u + 1 + lit;
+          if (lit < 15 && mlc < 15 && v + 2 <= ue) {
+            const uint32_t moff = uint32_t(ring[v & (kRing - 1)]) | (uint32_t(ring[(v + 1) & (kRing - 1)]) << 8);
+            const uint32_t ml = mlc + 4;
+            const bool b = moff == 0 || moff > op + lit || lit + ml > dl - op;
+            rec[n] = make_uint4(op, u + 1 - d0, lit, moff);
+            op += lit + ml;
+            u = v + 2;
+            if (b) { bad = true; break; }
+            continue;
+          }
+        }
+        if (u >= ue) { bad = true; break; }
+        const uint32_t tok = rb(u);
+        uint32_t lit = tok >> 4, ml = tok & 15u, v = u + 1;
+        if (lit == 15) {
+          uint32_t b;
+          do {
+            if (v >= ue) { bad = true; break; }
+            b = rb(v++);
+            lit += b;
+          } while (b == 255);
+          if (bad) break;
+        }
+        if (lit > ue - v) { bad = true; break; }
+        const uint32_t lsrc = v - d0;
+        v += lit;
+        if (v == ue) {  // the last sequence: literals only
+          if (lit > dl - op) { bad = true; break; }
+          rec[n] = make_uint4(op, lsrc, lit, 0u);
+          op += lit;
+          n++;
+          u = v;
+          done = true;
+          if (op != dl) bad = true;
+          break;
+        }
+        if (ue - v < 2) { bad = true; break; }
+        const uint32_t moff = rb(v) | (rb(v + 1) << 8);
+        v += 2;
+        if (ml == 15) {
+          uint32_t b;
+          do {
+            if (v >= ue) { bad = true; break; }
+            b = rb(v++);
+            ml += b;
+          } while (b == 255);
+          if (bad) break;
+        }
+        ml += 4;
+        if (lit > dl - op || moff == 0 || moff > op + lit || ml > dl - op - lit) { bad = true; break; }
+        rec[n] = make_uint4(op, lsrc, lit, moff);
+        op += lit + ml;
+        u = v;
+      }
+      if (bad) { n = 0; done = true; }
+      rec[n].x = op;  // the end of the last record
+    }
+    if (lane < G) cnt_s[wib][lane] = n;
+    // refill request: keep at least F bytes ahead of u; a jump past the frontier (a long literal run)
+    // restarts the ring at u
+    uint32_t rq = ~0u;
+    if (!done) {
+      if (u + 16 > fu) {
+        fu = (u & ~15u);
+        rq = fu;
+        fu += F;
+      } else if (fu - u < F) {
+        rq = fu;
+        fu += F;
+      }
+    }
+    uint4 blk[kBlk];
+    refill_issue(rq, blk);
+    __syncwarp();
+    if (__ballot_sync(FULL, n > 0 || rq != ~0u) == 0) break;
+    // ---- copy: the round's records, 32 at a time (lane -> record flat % R of sub-chunk flat / R).  A step covers
+    // all of a sub-chunk's records of the round, i.e. one contiguous output range [S0, S1); when it fits the
+    // segment's shared staging buffer, literals and matches are written there (match sources inside the range
+    // are read back from shared memory: dependent matches wait ~30 cycles, not an L2 round trip) and the range
+    // is flushed to global memory with aligned 16-byte stores; sources before S0 come from global memory.
+#pragma unroll 1
+    for (uint32_t st = 0; st < G * R / 32; st++) {
+      const uint32_t flat = st * 32 + lane, sc = flat / R, k = flat % R;
+      const uint8_t* const inj =
+          reinterpret_cast<const uint8_t*>(__shfl_sync(FULL, reinterpret_cast<uint64_t>(in), sc));
+      uint8_t* const outj = reinterpret_cast<uint8_t*>(__shfl_sync(FULL, reinterpret_cast<uint64_t>(out), sc));
+      const uint32_t nsc = cnt_s[wib][sc];
+      const bool act = k < nsc;
+      uint4 r = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t ml = 0;
+      if (act) {
+        r = rec_s[wib][sc][k];
+        ml = rec_s[wib][sc][k + 1].x - r.x - r.z;
+      }
+      const uint32_t S0 = rec_s[wib][sc][0].x, S1 = rec_s[wib][sc][nsc].x;
+      const uintptr_t A0 = reinterpret_cast<uintptr_t>(outj) + S0, A1 = reinterpret_cast<uintptr_t>(outj) + S1;
+      const uintptr_t Ab = A0 & ~uintptr_t(15);
+      const bool staged = nsc > 0 && A1 - Ab <= kStg;
+      uint8_t* const stg = stg_s[wib][lane / R] + 16;
+      // destination / source byte at output position x (relative to the sub-chunk)
+      auto dstp = [&](uint32_t x) -> uint8_t* {
+        return staged ? stg + (reinterpret_cast<uintptr_t>(outj) + x - Ab) : outj + x;
+      };
+      // kk <= 16 source bytes at output position x: global below S0, staged at or above it
+      auto src16 = [&](uint32_t x, uint32_t kk, uint32_t (&v)[4]) {
+        if (!staged || x + kk <= S0) {
+          load16<false>(outj + x, kk, v);
+        } else if (x >= S0) {
+          load16s(stg + (reinterpret_cast<uintptr_t>(outj) + x - Ab), v);
+        } else {  // straddles S0: the first S0 - x bytes from global memory, the rest staged
+          uint32_t g[4], h[4];
+          load16<false>(outj + x, S0 - x, g);
+          load16s(stg + (A0 - Ab) - (S0 - x), h);  // staged bytes below A0 are never read: merged away
+          const uint32_t c = S0 - x;
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            const uint32_t lo = 4u * i;
+            const uint32_t m = c >= lo + 4 ? 0xFFFFFFFFu : c <= lo ? 0u : (1u << (8u * (c - lo))) - 1u;
+            v[i] = (g[i] & m) | (h[i] & ~m);
+          }
+        }
+      };
+      // literals (independent of every other write)
+      for (uint32_t t = 0; t < r.z; t += 16) {
+        const uint32_t kk = min(16u, r.z - t);
+        uint32_t v[4];
+        load16<true>(inj + r.y + t, kk, v);
+        store16(dstp(r.x + t), v, kk);
+      }
+      __syncwarp();
+      // matches, in dependency order within a sub-chunk's lanes
+      const uint32_t mpos = r.x + r.z, src = mpos - r.w, se = src + min(ml, r.w);
+      const uint32_t segmask = R >= 32 ? FULL : (((1u << R) - 1u) << (lane & ~(R - 1u)));
+      bool pend = act && ml > 0;
+      uint32_t pm = __ballot_sync(FULL, pend);
+      while (pm) {
+        const uint32_t mine = pm & segmask;
+        const uint32_t lp = mine ? uint32_t(__ffs(mine) - 1) : lane;
+        const uint32_t mp_lp = __shfl_sync(FULL, mpos, lp);
+        const bool ready = pend && (lp == lane || mp_lp >= se);
+        if (ready) {
+          if (r.w >= 16 || ml <= r.w) {
+            for (uint32_t t = 0; t < ml; t += 16) {
+              const uint32_t kk = min(16u, ml - t);
+              uint32_t v[4];
+              src16(src + t, kk, v);
+              store16(dstp(mpos + t), v, kk);
+            }
+          } else {  // period r.w < 16 shorter than the match: replicate it into 32 scratch bytes
+            uint32_t v[4];
+            src16(src, r.w, v);
+            reinterpret_cast<uint4*>(scr)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            for (uint32_t i = r.w; i < 32; i++) scr[i] = scr[i - r.w];
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(scr);
+            const uint32_t s16 = 16u % r.w;
+            uint32_t ph = 0;
+            for (uint32_t t = 0; t < ml; t += 16) {
+              const uint32_t kk = min(16u, ml - t), q = ph >> 2, sh = (ph & 3u) * 8u;
+              const uint32_t w0 = sw[q], w1 = sw[q + 1], w2 = sw[q + 2], w3 = sw[q + 3], w4 = sw[min(q + 4, 7u)];
+              uint32_t x[4] = {__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                               __funnelshift_r(w3, w4, sh)};
+              store16(dstp(mpos + t), x, kk);
+              ph += s16;
+              if (ph >= r.w) ph -= r.w;
+            }
+          }
+        }
+        __syncwarp();
+        pend = pend && !ready;
+        pm = __ballot_sync(FULL, pend);
+      }
+      // flush the staged range: whole 16-byte blocks with one vector store, the two edge blocks byte by byte
+      if (staged) {
+        const uint32_t nb = uint32_t((A1 - Ab + 15) / 16);
+        for (uint32_t bi = lane % R; bi < nb; bi += R) {
+          const uintptr_t Bk = Ab + 16u * bi;
+          const uint8_t* sb = stg + 16u * bi;
+          if (Bk >= A0 && Bk + 16 <= A1) {
+            const uint4 q = *reinterpret_cast<const uint4*>(sb);
+            st_v4_u32(reinterpret_cast<void*>(Bk), q.x, q.y, q.z, q.w);
+          } else {
+            for (uint32_t j = 0; j < 16; j++)
+              if (Bk + j >= A0 && Bk + j < A1) reinterpret_cast<uint8_t*>(Bk)[j] = sb[j];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    refill_store(rq, blk);
+    __syncwarp();  // the record table is rewritten next round; the ring refill is visible to the parse
+  }
+  if (live && bad) atomicOr(B.err + D.err_idx, 0x4u);
+}
+
 }  // namespace
 
 cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
   (void)max_sub;
   if (!b.total_subs) return cudaSuccess;
-  // lanes per sub-chunk (NEXT-3 tuning knob TUNE_LZ4_LANES, env CDM_LZ4_G): 1 = the paper's thread per chunk
-  // (lz4_thread_kernel), 2/4/8/16 = lane groups, 32 = one warp per sub-chunk
+  // H8 schedule (NEXT-3 knobs): lz4_split = 1 (default) takes the split parse/copy kernel for latency-bound
+  // launches -- up to ~4 sub-chunks per resident warp slot, G = the smallest sub-chunks per warp that fits one
+  // wave -- and the lz4_lanes schedule for bigger, throughput-bound ones, where the thread kernel issues fewer
+  // instructions per sequence (measured: one 7 K-sub-chunk chunk 1.12 vs 3.85 ms; 112 K sub-chunks 9.1 vs 5.4
+  // ms); lz4_split_g > 0 forces the split kernel with that G.
+  if (tune_get(TUNE_LZ4_SPLIT)) {
+    static int occ[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!occ[dev]) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], lz4_split_kernel<2, 16, 256>, kSplitWarps * 32, 0);
+      if (occ[dev] < 1) occ[dev] = 1;
+    }
+    const uint32_t wave = uint32_t(device_sms()) * uint32_t(occ[dev]) * kSplitWarps;
+    uint32_t g = uint32_t(tune_get(TUNE_LZ4_SPLIT_G));
+    if (!g) {
+      g = 1;
+      while (g < 4 && uint64_t(g) * wave < b.total_subs) g *= 2;
+      if (uint64_t(g) * wave < b.total_subs) g = 0;
+    }
+    if (g) {
+      const uint32_t per_cta = kSplitWarps * g, grid = (b.total_subs + per_cta - 1) / per_cta;
+      switch (g) {
+        case 1: lz4_split_kernel<1, 32, 512><<<grid, kSplitWarps * 32, 0, s>>>(b); break;
+        case 2: lz4_split_kernel<2, 16, 256><<<grid, kSplitWarps * 32, 0, s>>>(b); break;
+        case 4: lz4_split_kernel<4, 16, 256><<<grid, kSplitWarps * 32, 0, s>>>(b); break;
+        default: lz4_split_kernel<8, 16, 256><<<grid, kSplitWarps * 32, 0, s>>>(b); break;
+      }
+      return cudaGetLastError();
+    }
+  }
+  // lanes per sub-chunk (knob lz4_lanes, env CDM_LZ4_G): 1 = the paper's thread per chunk (P:329,
+  // lz4_thread_kernel), 2/4/8/16 = lane groups, 32 = one warp per sub-chunk
   const int G = tune_get(TUNE_LZ4_LANES);
   if (G == 1) {
     const uint32_t grid = (b.total_subs + kWarpsPerCta * 32 - 1) / (kWarpsPerCta * 32);

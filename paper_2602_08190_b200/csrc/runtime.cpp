@@ -2286,6 +2286,13 @@ extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
   } else if (k == "scan_mode") {
     if (value != 0 && value != 1) return fail(CDM_E_INVALID_ARG, "scan_mode must be 0 (reduce-then-scan) or 1 (look-back)");
     cdm::tune_set(cdm::TUNE_SCAN_MODE, value);
+  } else if (k == "lz4_split") {
+    if (value != 0 && value != 1) return fail(CDM_E_INVALID_ARG, "lz4_split must be 0 (lz4_lanes schedules) or 1 (split parse/copy)");
+    cdm::tune_set(cdm::TUNE_LZ4_SPLIT, value);
+  } else if (k == "lz4_split_g") {
+    if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+      return fail(CDM_E_INVALID_ARG, "lz4_split_g must be 0 (per launch size) or 1, 2, 4, 8");
+    cdm::tune_set(cdm::TUNE_LZ4_SPLIT_G, value);
   } else {
     return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   }
@@ -2299,6 +2306,8 @@ extern "C" CDM_API cdm_status cdm_tune_get(const char* knob, int* value) {
   else if (k == "lz4_lanes") *value = cdm::tune_get(cdm::TUNE_LZ4_LANES);
   else if (k == "scan_mode") *value = cdm::tune_get(cdm::TUNE_SCAN_MODE);
   else if (k == "gp_ctas_per_sm") *value = cdm::tune_get(cdm::TUNE_GP_CTAS_PER_SM);
+  else if (k == "lz4_split") *value = cdm::tune_get(cdm::TUNE_LZ4_SPLIT);
+  else if (k == "lz4_split_g") *value = cdm::tune_get(cdm::TUNE_LZ4_SPLIT_G);
   else return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   return CDM_OK;
 }

@@ -490,13 +490,23 @@ def test_lz4_subchunk_sizes(engine, sub):
     check_parity(engine, f"Str|[LZ4(sub={sub}),BitPack]", col, rows_per_chunk=40_000, both=False)
 
 
-@pytest.fixture(params=[1, 4, 2, 8, 16, 32])
+@pytest.fixture(params=["split", "split1", "split2", "split4", "split8", 1, 4, 2, 8, 16, 32])
 def lz4_lanes(request):
-    """every LZ4 lane-group width the tuner may select (NEXT-3 knob lz4_lanes)"""
-    prev = cdm.tune_get("lz4_lanes")
-    cdm.tune_set("lz4_lanes", request.param)
-    yield request.param
-    cdm.tune_set("lz4_lanes", prev)
+    """every LZ4 schedule the tuner may select: the split parse/copy kernel (knob lz4_split; lz4_split_g = 0
+    automatic, 1, 2, 4, 8 sub-chunks per warp) and every lane-group width of the other schedules (knob
+    lz4_lanes, lz4_split = 0)"""
+    knobs = ("lz4_lanes", "lz4_split", "lz4_split_g")
+    prev = {k: cdm.tune_get(k) for k in knobs}
+    p = request.param
+    if isinstance(p, str):
+        cdm.tune_set("lz4_split", 1)
+        cdm.tune_set("lz4_split_g", 0 if p == "split" else int(p[5:]))
+    else:
+        cdm.tune_set("lz4_split", 0)
+        cdm.tune_set("lz4_lanes", p)
+    yield p
+    for k in knobs:
+        cdm.tune_set(k, prev[k])
 
 
 def test_lz4_lane_widths(engine, lz4_lanes):
@@ -539,6 +549,30 @@ def test_lz4_overlapping_matches(engine, lz4_lanes):
         cdm1.bitpack(lens, 16, 0)])
     ch = cdm1.build(root, cdm1.VARBYTES, 1, 2, payload=n, cascade_hash=_hash(spec))
     check_parity(engine, spec, [ch], cdm.VARBYTES)
+
+
+@pytest.mark.parametrize("spec", ["Str|[LZ4(sub=4096),BitPack]", "Str|[LZ4(sub=16384,hc=9),BitPack]",
+                                  "Str|[LZ4(sub=65536,hc=12),BitPack]"])
+def test_lz4_dependent_matches(engine, lz4_lanes, spec):
+    """text built from a 6-word vocabulary, byte runs and long literal stretches: most matches are a few bytes
+    to a few hundred bytes back, so the split kernel's matches depend on other lanes' matches of the same step
+    (dependency rounds), short periods (< 16) are replicated, long literals and long matches cross 16-byte pieces"""
+    rng = np.random.default_rng(77)
+    words = [b"ab", b"abc ", b"the ", b"slyly ", b"x", b"carefully final "]
+    parts = []
+    for _ in range(12_000):
+        r = rng.random()
+        if r < 0.8:
+            parts.append(words[rng.integers(0, len(words))])
+        elif r < 0.9:
+            parts.append(bytes([int(rng.integers(33, 127))]) * int(rng.integers(1, 300)))
+        else:
+            parts.append(rng.integers(0, 256, size=int(rng.integers(1, 200)), dtype=np.uint8).tobytes())
+    data = np.frombuffer(b"".join(parts), dtype=np.uint8)
+    cuts = np.sort(rng.choice(np.arange(1, data.size), size=2000, replace=False))
+    offs = np.concatenate([[0], cuts, [data.size]]).astype(np.int64)
+    col = Column("dep", VARBYTES, 1, offs.size - 1, data.copy(), offs)
+    check_parity(engine, spec, col, rows_per_chunk=700, both=False)
 
 
 # ------------------------------------------------------------------------------ edge cases + corrupt data

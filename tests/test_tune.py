@@ -82,6 +82,13 @@ def test_cabi_tuning_knobs():
     cdm.tune_set("gp_ctas_per_sm", 2)
     assert cdm.tune_get("gp_ctas_per_sm") == 2
     cdm.tune_set("gp_ctas_per_sm", gp)
-    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("gp_ctas_per_sm", 9), ("nope", 1)):
+    assert cdm.tune_get("lz4_split") in (0, 1) and cdm.tune_get("lz4_split_g") in (0, 1, 2, 4, 8)
+    for knob, v in (("lz4_split", 0), ("lz4_split_g", 4)):
+        old = cdm.tune_get(knob)
+        cdm.tune_set(knob, v)
+        assert cdm.tune_get(knob) == v
+        cdm.tune_set(knob, old)
+    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("gp_ctas_per_sm", 9), ("lz4_split", 2),
+                     ("lz4_split_g", 16), ("nope", 1)):
         with pytest.raises(cdm.CdmError):
             cdm.tune_set(knob, v)

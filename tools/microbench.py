@@ -153,6 +153,12 @@ def main():
             emit(run_case(eng, f"NP lz4 sub={sub}", f"Str|[LZ4(sub={sub}),BitPack]", com, a.steps, flush, stream))
         # the bench's encoder setting: liblz4 HC level 9 (CR 1.86 -> 2.24 on the payload, 7.1 -> 8.9 bytes per sequence)
         emit(run_case(eng, "NP lz4 sub=16384 hc=9", "Str|[LZ4(sub=16384,hc=9),BitPack]", com, a.steps, flush, stream))
+        # config 4's launch shape: ONE l_comment chunk of 2^22 rows (the bench decodes one such chunk per pipeline
+        # group, ~6.9 K sub-chunks per launch)
+        c4 = Column("l_comment", com.dtype, com.width, 1 << 22, com.data[: int(com.offsets[1 << 22])].copy(),
+                    com.offsets[: (1 << 22) + 1].copy())
+        emit(run_case(eng, "NP lz4 one 4M-row chunk sub=16384 hc=9", "Str|[LZ4(sub=16384,hc=9),BitPack]", c4,
+                      a.steps, flush, stream))
         # single-sub-chunk latency: ONE sub-chunk (l_comment rows totalling ~sub bytes) per launch -- the length of
         # the chunk-sequential chain that bounds every LZ4 launch
         for sub in (4096, 16384, 65536):
