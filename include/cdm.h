@@ -268,6 +268,10 @@ CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t c
  *                     lz4_lanes; env CDM_LZ4_SPLIT sets the start value
  *   "lz4_split_g"     sub-chunks per warp of the split kernel: 0 (default) = by launch size (latency-bound launches
  *                     only), 1, 2, 4 or 8 = always the split kernel with that many; env CDM_LZ4_SPLIT_G
+ *   "lz4_spec"        H8 schedule: the speculative-parse kernel (a warp per sub-chunk of <= 16 KiB: 32 lanes walk the
+ *                     header chain from 32 segment starts, a fix-up re-walks each segment from its true entry to
+ *                     the merge point, then 32 sequences per step are copied into a shared-memory output image):
+ *                     1 (default) = for launches of at most two of its waves, 2 = always, 0 = never; env CDM_LZ4_SPEC
  *   "gp_ctas_per_sm"  G.P. pattern's L (Table 3 G.P. row): resident rle_kernel CTAs per SM, 0 = the kernel's own
  *                     occupancy (default), 1..8 (enforced by padding the launch's dynamic shared memory)
  *   "scan_mode"       H6 schedule (single-pass look-back vs the 2-pass baseline): 0 =

@@ -180,7 +180,7 @@ def checksum(dev_buf, chunk_id: int, stream=None) -> int:
 
 def tune_set(knob: str, value: int) -> None:
     """NEXT-3 launch-parameter knob (include/cdm.h: "fp_ctas_per_sm", "lz4_lanes", "lz4_split", "lz4_split_g",
-    "gp_ctas_per_sm", "scan_mode")."""
+    "lz4_spec", "gp_ctas_per_sm", "scan_mode")."""
     _check(lib().cdm_tune_set(knob.encode(), int(value)))
 
 

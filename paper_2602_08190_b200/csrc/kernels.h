@@ -256,7 +256,8 @@ cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s);
 cudaError_t launch_rle_sums(const SumsBatch& b, cudaStream_t s);
 cudaError_t launch_rle(const RleBatch& b, cudaStream_t s);
 cudaError_t launch_rle_big(const RleBatch& b, cudaStream_t s);
-cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s);
+// max_sub / max_csub: the largest decompressed / compressed sub-chunk of the batch (host-read, selects the schedule)
+cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, uint32_t max_csub, cudaStream_t s);
 cudaError_t launch_ans(const AnsBatch& b, bool interleaved, cudaStream_t s);
 // String-dictionary: tile sums -> per-descriptor exclusive scan of the sums -> expansion
 cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s);
@@ -285,6 +286,7 @@ enum TuneKnob : int {
   TUNE_GP_CTAS_PER_SM = 3,  // G.P. "L": resident rle_kernel CTAs per SM (0 = the kernel's occupancy), 1..8
   TUNE_LZ4_SPLIT = 4,       // H8 schedule: 1 = split parse (owner lane) / copy (whole warp), 0 = TUNE_LZ4_LANES
   TUNE_LZ4_SPLIT_G = 5,     // split schedule: sub-chunks per warp, 0 = per launch size, else 1/2/4/8
+  TUNE_LZ4_SPEC = 6,        // H8 schedule: speculative parallel parse, warp per sub-chunk (<= 16 KiB): 0 never, 1 small launches, 2 always
   kTuneKnobs
 };
 int tune_get(int knob);

@@ -316,6 +316,7 @@ void tune_init() {
   g_tune[TUNE_GP_CTAS_PER_SM] = 0;
   g_tune[TUNE_LZ4_SPLIT] = std::getenv("CDM_LZ4_SPLIT") ? std::atoi(std::getenv("CDM_LZ4_SPLIT")) : 1;
   g_tune[TUNE_LZ4_SPLIT_G] = std::getenv("CDM_LZ4_SPLIT_G") ? std::atoi(std::getenv("CDM_LZ4_SPLIT_G")) : 0;
+  g_tune[TUNE_LZ4_SPEC] = std::getenv("CDM_LZ4_SPEC") ? std::atoi(std::getenv("CDM_LZ4_SPEC")) : 1;
   g_tune_init = true;
 }
 }  // namespace

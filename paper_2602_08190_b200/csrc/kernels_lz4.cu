@@ -893,11 +893,405 @@ __global__ void __launch_bounds__(kSplitWarps * 32, 5) lz4_split_kernel(const __
   if (live && bad) atomicOr(B.err + D.err_idx, 0x4u);
 }
 
+
+// ------------------------------------------------------------------------------------------ speculative parse
+// Warp per sub-chunk with the header chain parsed in parallel (knob lz4_spec).  A sub-chunk's
+// sequences form a chain p -> next(p) through the compressed bytes (next = p + 1 + literal-length extension +
+// literals + 2 + match-length extension), so the N.P. decode time is (sequences) x (latency per header).
+// Here the compressed stream is cut into 32 word-aligned segments; lane j walks the chain SPECULATIVELY from its
+// segment's first byte, marking every position it visits in a shared bitmask.  Chains from a wrong start merge
+// with the true one after a few headers (next() is a function, so once two chains share a position they agree),
+// so a fix-up pass re-walks each segment from its true entry (the exit of the previous segment's true chain)
+// only until it meets a marked position; the few wrong marks before that point are cleared and the true ones set.
+// Iterated until no segment's exit changes (lane 0's chain is exact, so this ends after at most 32 rounds; in
+// practice 1-2).  The bitmask then holds exactly the true header positions; the copy phase takes them 32 at a time
+// in stream order (one sequence per lane: header parse, a warp scan of the output lengths, literals, then matches
+// in dependency order as in lz4_split_kernel) into a shared-memory image of the sub-chunk's output, so every
+// match source is a shared-memory read, and finished 16-byte blocks leave with one vector store each.
+// Sub-chunks of at most kSpecOut decompressed bytes (the launcher falls back to the other schedules otherwise);
+// compressed bytes are staged in shared memory when they fit kSpecIn, else read through L1.
+constexpr uint32_t kSpecWarps = 4;
+constexpr uint32_t kSpecOut = 16384;
+constexpr uint32_t kSpecIn = 8192;
+constexpr uint32_t kSpecMaxCl = 17408;  // >= the LZ4 bound of kSpecOut bytes
+struct SpecSmem {
+  uint8_t out[kSpecOut + 16 + 48];   // output image at alignment offset (out & 15), 16-byte blocks
+  uint8_t in[kSpecIn + 48];          // compressed bytes at alignment offset (in & 15)
+  uint32_t bits[kSpecMaxCl / 32];    // header positions
+};
+static_assert(sizeof(SpecSmem) % 16 == 0, "per-warp shared layout keeps 16-byte alignment");
+constexpr uint32_t kSpecSmem = kSpecWarps * sizeof(SpecSmem);
+
+// explicit shared-space accesses (32-bit shared addresses): the output image is only touched through these
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void reds_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// 16 bytes at shared byte address a (any alignment; the 4 bytes after a + 16 must be readable)
+__device__ __forceinline__ void sload16(uint32_t a, uint32_t (&v)[4]) {
+  const uint32_t b = a & ~3u, sh = (a & 3u) * 8u;
+  const uint32_t w0 = lds_u32(b), w1 = lds_u32(b + 4), w2 = lds_u32(b + 8), w3 = lds_u32(b + 12), w4 = lds_u32(b + 16);
+  v[0] = __funnelshift_r(w0, w1, sh);
+  v[1] = __funnelshift_r(w1, w2, sh);
+  v[2] = __funnelshift_r(w2, w3, sh);
+  v[3] = __funnelshift_r(w3, w4, sh);
+}
+// bytes [0, k) of v (1 <= k <= 16) to shared byte address a of a ZEROED image whose other bytes other lanes may
+// be writing: whole words with one store, partial words OR-ed in (only this lane's bytes are non-zero)
+__device__ __forceinline__ void sstore16(uint32_t a, const uint32_t (&v)[4], uint32_t k) {
+  const uint32_t a3 = a & 3u, sh = 8u * a3, base = a & ~3u, e = a3 + k;
+  uint32_t u[5];
+  u[0] = v[0] << sh;
+  u[1] = __funnelshift_l(v[0], v[1], sh);
+  u[2] = __funnelshift_l(v[1], v[2], sh);
+  u[3] = __funnelshift_l(v[2], v[3], sh);
+  u[4] = sh ? (v[3] >> (32u - sh)) : 0u;
+#pragma unroll
+  for (int i = 0; i < 5; i++) {
+    const int lo = max(int(a3) - 4 * i, 0), hi = min(int(e) - 4 * i, 4);
+    if (hi > lo) {
+      if (hi - lo == 4) sts_u32(base + 4 * i, u[i]);
+      else reds_or(base + 4 * i, u[i] & (((1u << (8 * (hi - lo))) - 1u) << (8 * lo)));
+    }
+  }
+}
+
+// position of the r-th (0-based) set bit of x (r < popc(x))
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t r) {
+  uint32_t pos = 0, c;
+  c = __popc(x & 0xFFFFu); if (r >= c) { r -= c; pos += 16; x >>= 16; }
+  c = __popc(x & 0xFFu);   if (r >= c) { r -= c; pos += 8;  x >>= 8; }
+  c = __popc(x & 0xFu);    if (r >= c) { r -= c; pos += 4;  x >>= 4; }
+  c = __popc(x & 0x3u);    if (r >= c) { r -= c; pos += 2;  x >>= 2; }
+  c = x & 1u;              if (r >= c) { pos += 1; }
+  return pos;
+}
+
+__global__ void __launch_bounds__(kSpecWarps * 32, 2) lz4_spec_kernel(const __grid_constant__ Lz4Batch B) {
+  extern __shared__ __align__(16) uint8_t spec_smem[];
+  SpecSmem& S = reinterpret_cast<SpecSmem*>(spec_smem)[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * kSpecWarps;
+  for (uint32_t gs = blockIdx.x * kSpecWarps + (threadIdx.x >> 5); gs < B.total_subs; gs += nwarps) {
+    const Lz4Desc& D = B.d[find_desc_lz4(B, gs)];
+    const uint32_t s = gs - D.sub0;
+    const uint32_t* tab = reinterpret_cast<const uint32_t*>(D.table);
+    uint64_t off = 0;
+    if (D.uniform) {
+      off = uint64_t(s) * D.uniform;
+    } else {
+      for (uint32_t k = lane; k < s; k += 32) off += __ldg(tab + 3 * k + 2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(FULL, off, o);
+    }
+    const uint32_t co = __ldg(tab + 3 * s), cl = __ldg(tab + 3 * s + 1), dl = __ldg(tab + 3 * s + 2);
+    if (uint64_t(co) + cl > D.payload_bytes || off + dl > D.n || (s + 1 == D.n_sub && off + dl != D.n) ||
+        dl > kSpecOut || cl == 0 || cl > kSpecMaxCl) {
+      if (lane == 0) atomicOr(B.err + D.err_idx, 0x4u);
+      continue;
+    }
+    const uint8_t* const in = D.payload + co;
+    uint8_t* const out = D.out + off;
+    const uint32_t ai = uint32_t(reinterpret_cast<uintptr_t>(in) & 15u);
+    const uint32_t ao = uint32_t(reinterpret_cast<uintptr_t>(out) & 15u);
+    const bool sin = ai + cl <= kSpecIn;
+    const uint32_t nwords = (cl + 31) / 32;
+    // ---- stage the compressed bytes (16-byte blocks below the payload's padded end) and clear the bitmask
+    if (sin) {
+      const uintptr_t ab = reinterpret_cast<uintptr_t>(in) - ai;
+      const uintptr_t istop = (reinterpret_cast<uintptr_t>(D.payload) + D.payload_bytes + 31) & ~uintptr_t(15);
+      for (uint32_t i = lane; 16 * i < ai + cl; i += 32) {
+        const uintptr_t a = ab + 16u * i;
+        const uint4 v = a + 16 <= istop ? __ldg(reinterpret_cast<const uint4*>(a)) : make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(S.in + 16 * i) = v;
+      }
+    }
+    for (uint32_t i = lane; i < nwords; i += 32) S.bits[i] = 0u;
+    const uint32_t sim = smem_addr(S.out), sinb = smem_addr(S.in) + ai;  // image block 0, input byte 0
+    for (uint32_t i = lane; 16 * i < ao + dl; i += 32) sts_v4(sim + 16 * i, make_uint4(0u, 0u, 0u, 0u));
+    __syncwarp();
+    auto ib = [&](uint32_t p) -> uint32_t { return sin ? lds_u8(sinb + p) : uint32_t(__ldg(in + p)); };
+    // next header position after a header at p < cl (cl: the chain ends with a literal-only sequence; cl + 1:
+    // the header runs past the end)
+    auto nxt = [&](uint32_t p) -> uint32_t {
+      const uint32_t t = ib(p);
+      uint32_t q = p + 1, lit = t >> 4;
+      if (lit == 15) {
+        uint32_t b;
+        do {
+          if (q >= cl) return cl + 1;
+          b = ib(q++);
+          lit += b;
+        } while (b == 255);
+      }
+      if (lit > cl - q) return cl + 1;
+      q += lit;
+      if (q == cl) return cl;
+      if (cl - q < 2) return cl + 1;
+      q += 2;
+      if ((t & 15u) == 15u) {
+        uint32_t b;
+        do {
+          if (q >= cl) return cl + 1;
+          b = ib(q++);
+        } while (b == 255);
+      }
+      return q;
+    };
+    auto marked = [&](uint32_t p) -> bool { return (S.bits[p >> 5] >> (p & 31u)) & 1u; };
+    // ---- speculative walks: lane j over segment [s0, e)
+    const uint32_t L = 32u * ((nwords + 31) / 32);
+    const uint32_t s0 = lane * L, e = min(s0 + L, cl);
+    const bool seg = s0 < cl;
+    uint32_t ex = s0;
+    if (seg) {
+      uint32_t p = s0, acc = 0;
+      while (p < e) {
+        acc |= 1u << (p & 31u);
+        const uint32_t q = nxt(p);
+        if (q >= e || (q >> 5) != (p >> 5)) { S.bits[p >> 5] = acc; acc = 0; }
+        p = q;
+      }
+      ex = p;
+    }
+    __syncwarp();
+    // ---- fix-up: entry = the previous segment's true exit; walk to the first marked position (the merge)
+    uint32_t E = ex, entry = s0, mpos = s0, tprev = s0;
+    bool walked = false;
+    for (int it = 0; it < 33; it++) {
+      const uint32_t up = __shfl_up_sync(FULL, E, 1);
+      const uint32_t t = lane == 0 ? 0u : up;
+      bool changed = false;
+      if (seg && (!walked || t != tprev)) {
+        uint32_t p = t;
+        while (p < e && !marked(p)) p = nxt(p);
+        const uint32_t nE = p < e ? ex : p;
+        entry = t;
+        mpos = p < e ? p : e;
+        changed = nE != E;
+        E = nE;
+        tprev = t;
+        walked = true;
+      }
+      if (!__any_sync(FULL, changed)) break;
+    }
+    // ---- the bitmask becomes the true chain: clear [s0, mpos), set the re-walked headers [entry, mpos)
+    if (seg && mpos != s0) {
+      const uint32_t wlo = s0 >> 5, wm = mpos >> 5;
+      for (uint32_t w = wlo; w < wm; w++) S.bits[w] = 0u;
+      if (mpos < e) S.bits[wm] &= ~((1u << (mpos & 31u)) - 1u);
+      else if (e & 31u) S.bits[wm] = 0u;  // no merge, segment ends inside a word (e == cl): that word is ours
+      for (uint32_t p = entry; p < mpos; p = nxt(p)) S.bits[p >> 5] |= 1u << (p & 31u);
+    }
+    __syncwarp();
+    // ---- copy: headers 32 at a time in stream order into the shared output image
+    const uint32_t img = sim + ao;  // shared address of output byte 0
+    const uintptr_t obase = reinterpret_cast<uintptr_t>(out) - ao;
+    auto flush = [&](uint32_t b) {  // image block b -> global (bytes of [ao, ao + dl) only)
+      const uintptr_t g = obase + 16u * b;
+      const uint4 q = lds_v4(sim + 16u * b);
+      if (16u * b >= ao && 16u * b + 16u <= ao + dl) {
+        st_v4_u32(reinterpret_cast<void*>(g), q.x, q.y, q.z, q.w);
+      } else {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        for (uint32_t j = 0; j < 16; j++)
+          if (16u * b + j >= ao && 16u * b + j < ao + dl) reinterpret_cast<uint8_t*>(g)[j] = uint8_t(w[j >> 2] >> (8 * (j & 3)));
+      }
+    };
+    uint32_t P = 0, op0 = 0, fb = 0;
+    bool bad = false, ended = false;
+    for (;;) {
+      const uint32_t w0 = P >> 5, wi = w0 + lane;
+      uint32_t word = wi < nwords ? S.bits[wi] : 0u;
+      if (lane == 0) word &= ~0u << (P & 31u);
+      const uint32_t c = __popc(word);
+      uint32_t C = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, C, o);
+        if (lane >= uint32_t(o)) C += v;
+      }
+      const uint32_t total = __shfl_sync(FULL, C, 31);
+      if (total == 0) {
+        if (w0 + 32 >= nwords) break;
+        P = 32u * (w0 + 32);
+        continue;
+      }
+      if (ended) { bad = true; break; }  // headers after the literal-only last sequence
+      const uint32_t n = min(total, 32u);
+      // lane k < n takes the k-th header: the word i with C[i-1] <= k < C[i]
+      uint32_t i = 0;
+#pragma unroll
+      for (uint32_t b = 16; b > 0; b >>= 1) {
+        const uint32_t Ci = __shfl_sync(FULL, C, i + b - 1);
+        if (Ci <= lane) i += b;
+      }
+      i = min(i, 31u);
+      const uint32_t wd = __shfl_sync(FULL, word, i), below = __shfl_sync(FULL, C - c, i);
+      const bool act = lane < n;
+      const uint32_t hp = 32u * (w0 + i) + select_bit(wd, act ? lane - below : 0u);
+      P = __shfl_sync(FULL, hp, n - 1) + 1;
+      // header
+      uint32_t lit = 0, ml = 0, moff = 0, lsrc = 0;
+      bool b = false, last = false;
+      if (act) {
+        const uint32_t t = ib(hp);
+        uint32_t q = hp + 1;
+        lit = t >> 4;
+        if (lit == 15) {
+          uint32_t x;
+          do {
+            if (q >= cl) { b = true; break; }
+            x = ib(q++);
+            lit += x;
+          } while (x == 255);
+        }
+        if (!b && lit > cl - q) b = true;
+        if (!b) {
+          lsrc = q;
+          q += lit;
+          if (q == cl) {
+            last = true;
+          } else if (cl - q < 2) {
+            b = true;
+          } else {
+            moff = ib(q) | (ib(q + 1) << 8);
+            q += 2;
+            ml = t & 15u;
+            if (ml == 15) {
+              uint32_t x;
+              do {
+                if (q >= cl) { b = true; break; }
+                x = ib(q++);
+                ml += x;
+              } while (x == 255);
+            }
+            ml += 4;
+          }
+        }
+      }
+      // output positions: exclusive scan of the sequences' lengths
+      const uint32_t len = b ? 0u : lit + ml;
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= uint32_t(o)) incl += v;
+      }
+      const uint32_t x = op0 + incl - len;
+      if (act && !b) {
+        if (uint64_t(x) + lit + ml > dl) b = true;
+        if (!last && (moff == 0 || moff > x + lit)) b = true;
+        if (last && lane != n - 1) b = true;
+      }
+      if (__any_sync(FULL, b)) { bad = true; break; }
+      ended = __any_sync(FULL, act && last);
+      op0 += __shfl_sync(FULL, incl, 31);
+      // literals
+      if (act) {
+        for (uint32_t t = 0; t < lit; t += 16) {
+          const uint32_t kk = min(16u, lit - t);
+          uint32_t v[4];
+          if (sin) sload16(sinb + lsrc + t, v);
+          else load16<true>(in + lsrc + t, kk, v);
+          sstore16(img + x + t, v, kk);
+        }
+      }
+      __syncwarp();
+      // matches in dependency order: ready when the source lies below the lowest pending match
+      const uint32_t mp = x + lit, src = mp - moff, se = src + min(ml, moff);
+      bool pend = act && ml > 0;
+      uint32_t pm = __ballot_sync(FULL, pend);
+      while (pm) {
+        const uint32_t lp = uint32_t(__ffs(pm) - 1);
+        const uint32_t mp_lp = __shfl_sync(FULL, mp, lp);
+        const bool ready = pend && (lp == lane || mp_lp >= se);
+        if (ready) {
+          if (moff >= 16 || ml <= moff) {
+            for (uint32_t t = 0; t < ml; t += 16) {
+              uint32_t v[4];
+              sload16(img + src + t, v);
+              sstore16(img + mp + t, v, min(16u, ml - t));
+            }
+          } else {  // short period: copy from a distance d (a multiple of moff) that grows as the run is written
+            uint32_t d = moff;
+            for (uint32_t t = 0; t < ml;) {
+              const uint32_t kk = min(min(16u, ml - t), d);
+              uint32_t v[4];
+              sload16(img + mp + t - d, v);
+              sstore16(img + mp + t, v, kk);
+              t += kk;
+              while (d <= t) d += moff;
+            }
+          }
+        }
+        __syncwarp();
+        pend = pend && !ready;
+        pm = __ballot_sync(FULL, pend);
+      }
+      // finished 16-byte blocks of the image leave with one vector store each
+      const uint32_t fe = (ao + op0) >> 4;
+      for (uint32_t bk = fb + lane; bk < fe; bk += 32) flush(bk);
+      fb = fe;
+    }
+    if (!bad && (!ended || op0 != dl)) bad = true;
+    if (!bad) {
+      const uint32_t fe = (ao + dl + 15) >> 4;
+      for (uint32_t bk = fb + lane; bk < fe; bk += 32) flush(bk);
+    } else if (lane == 0) {
+      atomicOr(B.err + D.err_idx, 0x4u);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
-cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, cudaStream_t s) {
-  (void)max_sub;
+cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, uint32_t max_csub, cudaStream_t s) {
   if (!b.total_subs) return cudaSuccess;
+  // lz4_spec: the speculative-parse warp-per-sub-chunk kernel (every sub-chunk must fit its shared-memory output
+  // image; persistent warps, sub-chunks strided over them).  1 (default) = for launches of at most two of its
+  // waves, where its short per-sub-chunk chain wins (one 16 KiB sub-chunk: 0.19 ms vs 0.45 split / 1.41 thread);
+  // bigger launches are throughput-bound and it issues ~40 % more instructions per sequence at 8 warps per SM
+  // (config 3's l_comment: 13.0 ms vs 5.45 ms for the thread kernel); 2 = always, 0 = never.
+  const int spec = tune_get(TUNE_LZ4_SPEC);
+  if (spec && max_sub <= kSpecOut && max_csub <= kSpecMaxCl) {
+    static int occ[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!occ[dev]) {
+      cudaFuncSetAttribute(lz4_spec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSpecSmem));
+      cudaFuncSetAttribute(lz4_spec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], lz4_spec_kernel, kSpecWarps * 32, kSpecSmem);
+      if (occ[dev] < 1) occ[dev] = 1;
+    }
+    const uint32_t slots = uint32_t(device_sms() * occ[dev]) * kSpecWarps;
+    if (spec == 2 || b.total_subs <= 2 * slots) {
+      const uint32_t need = (b.total_subs + kSpecWarps - 1) / kSpecWarps;
+      const uint32_t grid = std::min<uint32_t>(need, slots / kSpecWarps);
+      lz4_spec_kernel<<<grid, kSpecWarps * 32, kSpecSmem, s>>>(b);
+      return cudaGetLastError();
+    }
+  }
   // H8 schedule (NEXT-3 knobs): lz4_split = 1 (default) takes the split parse/copy kernel for latency-bound
   // launches -- up to ~4 sub-chunks per resident warp slot, G = the smallest sub-chunks per warp that fits one
   // wave -- and the lz4_lanes schedule for bigger, throughput-bound ones, where the thread kernel issues fewer

@@ -147,7 +147,7 @@ struct Bound {
   uint64_t delta_base = 0;
   bool lz4 = false;
   uint64_t lz_pay_off = 0, lz_pay_bytes = 0, lz_tab_off = 0, bytes_off = 0, raw_off = 0;
-  uint32_t n_sub = 0, lz_sub_bytes = 0, lz_uniform = 0;
+  uint32_t n_sub = 0, lz_sub_bytes = 0, lz_sub_cbytes = 0, lz_uniform = 0;
   bool ans = false;  // NEXT-1: the bytes come from a range-ANS node (Str child or FIXED root)
   uint64_t ans_w_off = 0, ans_w_n = 0, ans_tab_off = 0, ans_n = 0;
   uint32_t ans_nchunks = 0, ans_chunk = 0, ans_tl = 0, ans_il = 1;
@@ -448,7 +448,10 @@ cdm_status bind_job(const cdm_job& job, Bound* b) {
         b->n_sub = bn.u32_at0();
         // largest decompressed sub-chunk, read from the host copy of the table (selects the kernel variant)
         const uint8_t* tab = static_cast<const uint8_t*>(job.host_chunk) + b->lz_tab_off;
-        for (uint32_t k = 0; k < b->n_sub; k++) b->lz_sub_bytes = std::max(b->lz_sub_bytes, rd32(tab + 12ull * k + 8));
+        for (uint32_t k = 0; k < b->n_sub; k++) {
+          b->lz_sub_bytes = std::max(b->lz_sub_bytes, rd32(tab + 12ull * k + 8));
+          b->lz_sub_cbytes = std::max(b->lz_sub_cbytes, rd32(tab + 12ull * k + 4));
+        }
         // uniform sub-chunks (the encoder's layout): sub-chunk s starts at s * size, no prefix needed
         b->lz_uniform = b->n_sub ? rd32(tab + 8) : 0;
         for (uint32_t k = 0; k + 1 < b->n_sub && b->lz_uniform; k++)
@@ -529,7 +532,7 @@ struct cdm_batch {
   std::vector<int> rle_round;   // per rle batch: its round
   size_t rle_level0 = 0;  // rle[0, rle_level0) are launches of the value / counts lineages (non-final rounds)
   std::vector<Lz4Batch> lz4;
-  std::vector<uint32_t> lz4_max_sub;
+  std::vector<uint32_t> lz4_max_sub, lz4_max_csub;
   std::vector<AnsBatch> ans;  // runs on the chunk-sequential (LZ4) family stream
   std::vector<SdBatch> sd;    // String-dictionary expansions, after the ANS launches on the same stream
   struct Copy { void* dst; const void* src; size_t bytes; };
@@ -598,7 +601,7 @@ bool getenv_flag(const char* name) {
 size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   const size_t nj = B->jobs.size();
   B->fp.clear(); B->fp_maxw.clear(); B->fp_char.clear();
-  for (auto& kb : B->k_bytes) kb = 0; B->scan.clear(); B->sums.clear(); B->rle.clear(); B->sums_phase.clear(); B->rle_round.clear(); B->lz4.clear(); B->lz4_max_sub.clear();
+  for (auto& kb : B->k_bytes) kb = 0; B->scan.clear(); B->sums.clear(); B->rle.clear(); B->sums_phase.clear(); B->rle_round.clear(); B->lz4.clear(); B->lz4_max_sub.clear(); B->lz4_max_csub.clear();
   B->ans.clear(); B->sd.clear();
   B->copies.clear(); B->zero_offsets.clear();
   // ---- zeroed region: error words, ticket counters, look-back flags/values, rle big counters
@@ -945,10 +948,11 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (auto& g : groups(lzj)) {
     Lz4Batch lb{};
     lb.err = B->err_dev;
-    uint32_t subs = 0, max_sub = 0;
+    uint32_t subs = 0, max_sub = 0, max_csub = 0;
     for (int j : g) {
       const Bound& b = B->jobs[j];
       max_sub = std::max(max_sub, b.lz_sub_bytes);
+      max_csub = std::max(max_csub, b.lz_sub_cbytes);
       Lz4Desc& d = lb.d[lb.n++];
       d.payload = b.dev_chunk + b.lz_pay_off;
       d.table = b.dev_chunk + b.lz_tab_off;
@@ -964,6 +968,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     lb.total_subs = subs;
     B->lz4.push_back(lb);
     B->lz4_max_sub.push_back(max_sub);
+    B->lz4_max_csub.push_back(max_csub);
   }
   for (size_t i = 0; i < nj; i++) {
     const Bound& b = B->jobs[i];
@@ -1112,7 +1117,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
       }
       case F_LZ4:  // the chunk-sequential family: LZ4 and range ANS
         for (size_t i = 0; i < B->lz4.size() && !st; i++) {
-          st = timed(K_LZ4, [&] { return launch_lz4(B->lz4[i], B->lz4_max_sub[i], fs); });
+          st = timed(K_LZ4, [&] { return launch_lz4(B->lz4[i], B->lz4_max_sub[i], B->lz4_max_csub[i], fs); });
           n++; B->fam_launches[F_LZ4]++;
         }
         for (size_t i = 0; i < B->ans.size() && !st; i++) {
@@ -2293,6 +2298,9 @@ extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
     if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
       return fail(CDM_E_INVALID_ARG, "lz4_split_g must be 0 (per launch size) or 1, 2, 4, 8");
     cdm::tune_set(cdm::TUNE_LZ4_SPLIT_G, value);
+  } else if (k == "lz4_spec") {
+    if (value < 0 || value > 2) return fail(CDM_E_INVALID_ARG, "lz4_spec must be 0 (never), 1 (small launches) or 2 (always: speculative parallel parse)");
+    cdm::tune_set(cdm::TUNE_LZ4_SPEC, value);
   } else {
     return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   }
@@ -2308,6 +2316,7 @@ extern "C" CDM_API cdm_status cdm_tune_get(const char* knob, int* value) {
   else if (k == "gp_ctas_per_sm") *value = cdm::tune_get(cdm::TUNE_GP_CTAS_PER_SM);
   else if (k == "lz4_split") *value = cdm::tune_get(cdm::TUNE_LZ4_SPLIT);
   else if (k == "lz4_split_g") *value = cdm::tune_get(cdm::TUNE_LZ4_SPLIT_G);
+  else if (k == "lz4_spec") *value = cdm::tune_get(cdm::TUNE_LZ4_SPEC);
   else return fail(CDM_E_INVALID_ARG, "unknown tuning knob '" + k + "'");
   return CDM_OK;
 }

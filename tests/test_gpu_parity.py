@@ -490,15 +490,20 @@ def test_lz4_subchunk_sizes(engine, sub):
     check_parity(engine, f"Str|[LZ4(sub={sub}),BitPack]", col, rows_per_chunk=40_000, both=False)
 
 
-@pytest.fixture(params=["split", "split1", "split2", "split4", "split8", 1, 4, 2, 8, 16, 32])
+@pytest.fixture(params=["spec", "split", "split1", "split2", "split4", "split8", 1, 4, 2, 8, 16, 32])
 def lz4_lanes(request):
-    """every LZ4 schedule the tuner may select: the split parse/copy kernel (knob lz4_split; lz4_split_g = 0
+    """every LZ4 schedule the tuner may select: the speculative-parse kernel (knob lz4_spec, sub-chunks <= 16 KiB;
+    larger ones fall through to the split schedule), the split parse/copy kernel (knob lz4_split; lz4_split_g = 0
     automatic, 1, 2, 4, 8 sub-chunks per warp) and every lane-group width of the other schedules (knob
     lz4_lanes, lz4_split = 0)"""
-    knobs = ("lz4_lanes", "lz4_split", "lz4_split_g")
+    knobs = ("lz4_lanes", "lz4_split", "lz4_split_g", "lz4_spec")
     prev = {k: cdm.tune_get(k) for k in knobs}
     p = request.param
-    if isinstance(p, str):
+    cdm.tune_set("lz4_spec", 2 if p == "spec" else 0)
+    if p == "spec":
+        cdm.tune_set("lz4_split", 1)
+        cdm.tune_set("lz4_split_g", 0)
+    elif isinstance(p, str):
         cdm.tune_set("lz4_split", 1)
         cdm.tune_set("lz4_split_g", 0 if p == "split" else int(p[5:]))
     else:
@@ -574,6 +579,65 @@ def test_lz4_dependent_matches(engine, lz4_lanes, spec):
     col = Column("dep", VARBYTES, 1, offs.size - 1, data.copy(), offs)
     check_parity(engine, spec, col, rows_per_chunk=700, both=False)
 
+
+
+def test_lz4_long_literals_and_incompressible(engine, lz4_lanes):
+    """16 KiB sub-chunks whose compressed size exceeds the speculative kernel's shared input stage (random bytes:
+    cl > 8 KiB, read through L1), literal runs longer than a parse segment (the true chain enters a segment past
+    its end), and runs of one byte (period-1 matches of ~1 KiB)"""
+    rng = np.random.default_rng(5)
+    parts = []
+    for _ in range(900):
+        r = rng.random()
+        if r < 0.3:
+            parts.append(rng.integers(0, 256, size=int(rng.integers(500, 6000)), dtype=np.uint8).tobytes())
+        elif r < 0.5:
+            parts.append(bytes([int(rng.integers(0, 256))]) * int(rng.integers(4, 1500)))
+        else:
+            parts.append(b"furiously regular deposits " * int(rng.integers(1, 20)))
+    data = np.frombuffer(b"".join(parts), dtype=np.uint8)
+    cuts = np.sort(rng.choice(np.arange(1, data.size), size=300, replace=False))
+    offs = np.concatenate([[0], cuts, [data.size]]).astype(np.int64)
+    col = Column("lit", VARBYTES, 1, offs.size - 1, data.copy(), offs)
+    for spec in ("Str|[LZ4(sub=16384),BitPack]", "Str|[LZ4(sub=16384,hc=9),BitPack]", "Str|[LZ4(sub=8000),BitPack]"):
+        check_parity(engine, spec, col, rows_per_chunk=150, both=False)
+
+
+def _stream_span(ch, i):
+    nn = int(np.frombuffer(ch[6:8].tobytes(), np.uint16)[0])
+    off, ln = struct.unpack_from("<QQ", ch.tobytes(), 64 + 32 * nn + 16 * i)
+    return off, ln
+
+
+def test_lz4_mutated_streams_match_oracle(engine, lz4_lanes):
+    """byte mutations of valid LZ4 payloads (tokens, offsets, length extensions, literals): wherever the oracle
+    rejects the chunk the GPU sets CDM_ERR_LZ4, wherever it decodes, the GPU's bytes equal the oracle's -- the
+    speculative parse must find exactly the oracle's header chain even in garbage"""
+    rng = np.random.default_rng(11)
+    col = TPCH(0.002).column("l_comment")
+    spec = "Str|[LZ4(sub=16384,hc=9),BitPack]"
+    base = encoder.encode_chunks(spec, col, 3000)[:4]
+    chunks = []
+    for k in range(48):
+        ch = base[k % len(base)].copy()
+        off, ln = _stream_span(ch, 0)  # the LZ4 payload (first raw stream)
+        for _ in range(int(rng.integers(1, 4))):
+            pos = off + int(rng.integers(0, ln))
+            ch[pos] = rng.integers(0, 256) if rng.random() < 0.7 else ch[pos] ^ (1 << int(rng.integers(0, 8)))
+        chunks.append(ch)
+    casc = cdm.Cascade(spec, VARBYTES)
+    got = gpu_decode(engine, casc, chunks, resident=True, expect_error=True)
+    n_err = 0
+    for ch, (payload, offs, r) in zip(chunks, got):
+        try:
+            exp, _ = oracle.decode_chunk(ch)
+        except oracle.OracleError:
+            n_err += 1
+            assert r["error_bits"] & cdm.ERR_LZ4, "oracle rejects the block, GPU did not flag it"
+            continue
+        assert r["error_bits"] == 0
+        assert np.array_equal(payload, exp)
+    assert 0 < n_err < len(chunks)
 
 # ------------------------------------------------------------------------------ edge cases + corrupt data
 def test_empty_and_tiny(engine):

@@ -83,12 +83,13 @@ def test_cabi_tuning_knobs():
     assert cdm.tune_get("gp_ctas_per_sm") == 2
     cdm.tune_set("gp_ctas_per_sm", gp)
     assert cdm.tune_get("lz4_split") in (0, 1) and cdm.tune_get("lz4_split_g") in (0, 1, 2, 4, 8)
-    for knob, v in (("lz4_split", 0), ("lz4_split_g", 4)):
+    assert cdm.tune_get("lz4_spec") == 1
+    for knob, v in (("lz4_split", 0), ("lz4_split_g", 4), ("lz4_spec", 2), ("lz4_spec", 0)):
         old = cdm.tune_get(knob)
         cdm.tune_set(knob, v)
         assert cdm.tune_get(knob) == v
         cdm.tune_set(knob, old)
     for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("gp_ctas_per_sm", 9), ("lz4_split", 2),
-                     ("lz4_split_g", 16), ("nope", 1)):
+                     ("lz4_split_g", 16), ("lz4_spec", 3), ("nope", 1)):
         with pytest.raises(cdm.CdmError):
             cdm.tune_set(knob, v)
