@@ -269,16 +269,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) lz4_group_kernel(const __gr
 // kernel has at most one dependent global round trip (a far match source); everything else is shared memory:
 //  * the compressed stream is prefetched 16-byte block by block into a 64-byte per-thread input ring, two
 //    blocks ahead in registers (the loads are in flight while earlier sequences decode);
-//  * output bytes go to a 64-byte per-thread output ring indexed by global address bits; a completed 16-byte
-//    block of the global output leaves the ring with ONE 16-byte store (byte stores only at the sub-chunk's
-//    unaligned head and tail);
-//  * a literal run or match moves up to 16 bytes per step; match sources within 48 bytes come from the output
-//    ring, farther ones from global memory (three 8-byte loads in flight together), where the thread's own
+//  * output bytes go to an OR-byte per-thread output ring (128) indexed by global address bits; a completed
+//    FB-byte block (32: a whole L2 sector) of the global output leaves the ring with FB / 16 vector stores (byte
+//    stores only at the sub-chunk's unaligned head and tail);
+//  * a literal run or match moves up to 16 bytes per step; match sources within kLzNear bytes (96) come from the
+//    output ring, farther ones from global memory (three 8-byte loads in flight together), where the thread's own
 //    earlier 16-byte stores already are (same-thread program order).  An overlapping match (offset < 16)
 //    moves `offset` bytes per step, so every source byte precedes the bytes being written.
 // A warp instruction advances 32 sub-chunks (vs one per warp for lz4_kernel).
-constexpr uint32_t kLzRing = 64;   // ring bytes per thread (input and output each)
-constexpr uint32_t kLzNear = 48;   // match offsets up to this are read from the output ring
+constexpr uint32_t kLzRing = 64;   // input ring bytes per thread
 
 __device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the thread's own earlier stores)
   uint2 v;
@@ -286,8 +285,12 @@ __device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the
   return v;
 }
 
+// OR: output ring bytes per thread, FB: output block bytes (flushed with FB / 16 vector stores once complete)
+template <uint32_t OR, uint32_t FB>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const __grid_constant__ Lz4Batch B) {
-  __shared__ __align__(16) uint8_t oring_s[kWarpsPerCta * 32 * kLzRing];
+  static_assert((OR == 64 && FB == 16) || (OR == 128 && FB == 32), "ring / block pairs");
+  constexpr uint32_t kLzNear = OR == 64 ? 48 : 96;  // match offsets up to this are read from the output ring
+  __shared__ __align__(16) uint8_t oring_s[kWarpsPerCta * 32 * OR];
   __shared__ __align__(16) uint8_t iring_s[kWarpsPerCta * 32 * kLzRing];
   const uint32_t gs = blockIdx.x * (kWarpsPerCta * 32) + threadIdx.x;
   const uint32_t lane = threadIdx.x & 31;
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
     atomicOr(B.err + D.err_idx, 0x4u);
     return;
   }
-  uint8_t* const oring = oring_s + threadIdx.x * kLzRing;
+  uint8_t* const oring = oring_s + threadIdx.x * OR;
   uint8_t* const iring = iring_s + threadIdx.x * kLzRing;
   const uint32_t* const orw = reinterpret_cast<const uint32_t*>(oring);
   const uint32_t* const irw = reinterpret_cast<const uint32_t*>(iring);
@@ -346,12 +349,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
     }
   };
   auto in_u8 = [&](uint32_t p) -> uint32_t { return iring[(ia0 + p) & (kLzRing - 1)]; };
-  // 16 ring bytes from global address a (words q..q+4 of the ring, funnel-shifted)
-  auto ring16 = [&](const uint32_t* rw, uintptr_t a, uint32_t (&v)[4]) {
+  // 16 ring bytes from global address a (words q..q+4 of a ring of RB bytes, funnel-shifted)
+  auto ring16 = [&](const uint32_t* rw, uint32_t rb, uintptr_t a, uint32_t (&v)[4]) {
     const uint32_t q = uint32_t(a >> 2), sh = uint32_t(a & 3u) * 8u;
     uint32_t w[5];
 #pragma unroll
-    for (int i = 0; i < 5; i++) w[i] = rw[(q + i) & (kLzRing / 4 - 1)];
+    for (int i = 0; i < 5; i++) w[i] = rw[(q + i) & (rb / 4 - 1)];
 #pragma unroll
     for (int i = 0; i < 4; i++) v[i] = __funnelshift_r(w[i], w[i + 1], sh);
   };
@@ -359,13 +362,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
   // ---- output: global addresses [ga0, ga0 + dl)
   uint8_t* const out = D.out + off;
   const uintptr_t ga0 = reinterpret_cast<uintptr_t>(out), ge = ga0 + dl;
-  auto flush = [&](uintptr_t blk) {  // block [blk, blk + 16) leaves the ring (bytes inside [ga0, ge) only)
-    const uint8_t* r = oring + (blk & (kLzRing - 1));
-    if (blk >= ga0 && blk + 16 <= ge) {
-      const uint4 v = *reinterpret_cast<const uint4*>(r);
-      st_v4_u32(reinterpret_cast<void*>(blk), v.x, v.y, v.z, v.w);
+  auto flush = [&](uintptr_t blk) {  // block [blk, blk + FB) leaves the ring (bytes inside [ga0, ge) only)
+    const uint8_t* r = oring + (blk & (OR - 1));
+    if (blk >= ga0 && blk + FB <= ge) {
+#pragma unroll
+      for (uint32_t h = 0; h < FB; h += 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(r + h);
+        st_v4_u32(reinterpret_cast<void*>(blk + h), v.x, v.y, v.z, v.w);
+      }
     } else {
-      for (uint32_t b = 0; b < 16; b++)
+      for (uint32_t b = 0; b < FB; b++)
         if (blk + b >= ga0 && blk + b < ge) reinterpret_cast<uint8_t*>(blk)[b] = r[b];
     }
   };
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
   // Append k <= 16 bytes (v, little-endian) at output position op: the bytes are shifted into the 8-byte word
   // containing op (its bytes below op are kept from the ring's copy of that word) and whole 8-byte words are
   // stored into the ring (no byte stores); bytes past op + k in the last word are scratch, overwritten by later
-  // appends before any read (they alias ring bytes more than 48 behind, which no near match reads).
+  // appends before any read (they alias ring bytes more than OR - 24 behind: flushed, and no near match reads them).
   uint64_t acc = 0;  // the ring word holding output bytes [(ga0 + op) & ~7, ga0 + op)
   auto put16 = [&](uint32_t op, const uint32_t (&v)[4], uint32_t k) {
     const uintptr_t ga = ga0 + op;
@@ -436,12 +442,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
     const uint64_t w2 = fill ? (v23 >> (64u - sh)) : 0ull;
     uint64_t* rw8 = reinterpret_cast<uint64_t*>(oring);
     const uint32_t q = uint32_t(ga >> 3), words = (fill + k + 7u) >> 3;  // words touched: 1..3
-    rw8[q & (kLzRing / 8 - 1)] = w0;
-    if (words > 1) rw8[(q + 1) & (kLzRing / 8 - 1)] = w1;
-    if (words > 2) rw8[(q + 2) & (kLzRing / 8 - 1)] = w2;
+    rw8[q & (OR / 8 - 1)] = w0;
+    if (words > 1) rw8[(q + 1) & (OR / 8 - 1)] = w1;
+    if (words > 2) rw8[(q + 2) & (OR / 8 - 1)] = w2;
     const uint32_t last = (fill + k) >> 3;  // index of the word holding the new end position
     acc = last == 0 ? w0 : last == 1 ? w1 : w2;
-    if ((ga & 15u) + k >= 16u) flush(ga & ~uintptr_t(15));
+    if ((ga & (FB - 1)) + k >= FB) flush(ga & ~uintptr_t(FB - 1));
   };
   auto far_load = [&](uintptr_t src, uint2& x0, uint2& x1, uint2& x2) {  // bytes [src & ~7, +24)
     const uintptr_t a8 = src & ~uintptr_t(7);
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
       const uint32_t k = min(16u, T.lit - done);
       ensure(ia0 + T.lit_src + done + 16);
       uint32_t v[4];
-      ring16(irw, ia0 + T.lit_src + done, v);
+      ring16(irw, kLzRing, ia0 + T.lit_src + done, v);
       put16(op, v, k);
       op += k;
       done += k;
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
     if (!N.last && N.lit <= 16 && (N.token & 15) != 15) {
       if (!tail(N)) { bad = true; break; }
       const uint32_t opm = op + T.ml + N.lit;  // N's match position
-      const uintptr_t flushed = (ga0 + op) & ~uintptr_t(15);
+      const uintptr_t flushed = (ga0 + op) & ~uintptr_t(FB - 1);
       if (N.moff > kLzNear && N.moff <= opm && ga0 + opm - N.moff + 16 <= flushed) {
         far_load(ga0 + opm - N.moff, N.x0, N.x1, N.x2);
         N.pre = true;
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
       const uintptr_t src = ga0 + op - T.moff;
       uint32_t v[4];
       if (T.moff <= kLzNear) {
-        ring16(orw, src, v);
+        ring16(orw, OR, src, v);
       } else if (done == 0 && T.pre) {
         far_words(src, T.x0, T.x1, T.x2, v);
       } else {
@@ -517,7 +523,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
     atomicOr(B.err + D.err_idx, 0x4u);
     return;
   }
-  if (ge & 15u) flush(ge & ~uintptr_t(15));  // the partial last block
+  if (ge & (FB - 1)) flush(ge & ~uintptr_t(FB - 1));  // the partial last block
 }
 
 // ------------------------------------------------------------------------------------------ split parse / copy
@@ -1327,7 +1333,9 @@ cudaError_t launch_lz4(const Lz4Batch& b, uint32_t max_sub, uint32_t max_csub, c
   const int G = tune_get(TUNE_LZ4_LANES);
   if (G == 1) {
     const uint32_t grid = (b.total_subs + kWarpsPerCta * 32 - 1) / (kWarpsPerCta * 32);
-    lz4_thread_kernel<<<grid, kWarpsPerCta * 32, 0, s>>>(b);
+    // 128-byte output rings flushed in 32-byte (whole-sector) blocks: config 3's l_comment 5.36 -> 4.87 ms vs
+    // 64-byte rings / 16-byte blocks (more matches served from the ring: offsets <= 96 instead of <= 48)
+    lz4_thread_kernel<128, 32><<<grid, kWarpsPerCta * 32, 0, s>>>(b);
     return cudaGetLastError();
   }
   if (G != 32) {
