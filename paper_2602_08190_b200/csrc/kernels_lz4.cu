@@ -284,6 +284,13 @@ __device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the
   asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
   return v;
 }
+// far-match source loads: L1::evict_first (the window of one thread is re-read at most a few times; measured on
+// config 3's l_comment: 4.71 vs 4.84 ms and 20.1 vs 22.0 GB of DRAM reads; .cg / L1::no_allocate: 6.2 / 5.9 ms)
+__device__ __forceinline__ uint2 ld_v2_far(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.L1::evict_first.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
 
 // OR: output ring bytes per thread, FB: output block bytes (flushed with FB / 16 vector stores once complete)
 template <uint32_t OR, uint32_t FB>
@@ -451,9 +458,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) lz4_thread_kernel(const 
   };
   auto far_load = [&](uintptr_t src, uint2& x0, uint2& x1, uint2& x2) {  // bytes [src & ~7, +24)
     const uintptr_t a8 = src & ~uintptr_t(7);
-    x0 = ld_v2_global(reinterpret_cast<const void*>(a8));
-    x1 = ld_v2_global(reinterpret_cast<const void*>(a8 + 8));
-    x2 = ld_v2_global(reinterpret_cast<const void*>(a8 + 16));
+    x0 = ld_v2_far(reinterpret_cast<const void*>(a8));
+    x1 = ld_v2_far(reinterpret_cast<const void*>(a8 + 8));
+    x2 = ld_v2_far(reinterpret_cast<const void*>(a8 + 16));
   };
   auto far_words = [&](uintptr_t src, const uint2& x0, const uint2& x1, const uint2& x2, uint32_t (&v)[4]) {
     const bool hi = (src & 4u) != 0;

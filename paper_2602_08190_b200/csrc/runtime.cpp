@@ -498,6 +498,9 @@ struct Alloc {  // bump allocator over one device arena; pass 1 sizes, pass 2 as
 
 // ============================================================================ device batches
 enum Family { F_FP = 0, F_SCAN = 1, F_RLE = 2, F_LZ4 = 3, F_COPY = 4 };
+// kernel streams: one per family, plus S_ANS for the range-ANS -> String-dictionary chain, which is independent of
+// the LZ4 launches (its times and launches are reported under F_LZ4, the chunk-sequential family)
+constexpr int S_ANS = 5, kStreams = 6;
 
 // Stream priority of a kernel family.  CDM_RLE_PRIO=hi: the latency-bound RLE chain (sums -> scan -> expand)
 // gets its CTAs scheduled first and the bandwidth-bound families fill the SMs it leaves idle; lo: the
@@ -553,7 +556,7 @@ struct cdm_batch {
   cudaStream_t* fam = nullptr;     // the family streams concurrent kernel families fork onto
   // fork/join events: independent kernel families run concurrently on the engine's family streams
   cudaEvent_t fork = nullptr;
-  cudaEvent_t join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t join[kStreams] = {};
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -1037,8 +1040,8 @@ cudaEvent_t ev_get(cdm_batch* B, size_t k) {
 cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   uint32_t n = 0;
   size_t evk = B->pending.size() * 2;
-  const bool has[5] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty() || !B->ans.empty() || !B->sd.empty(),
-                       !B->copies.empty() || !B->zero_offsets.empty()};
+  const bool has[kStreams] = {!B->fp.empty(), !B->scan.empty(), !B->rle.empty(), !B->lz4.empty(),
+                              !B->copies.empty() || !B->zero_offsets.empty(), !B->ans.empty() || !B->sd.empty()};
   int nfam = 0;
   for (bool h : has) nfam += h;
   // error words, tickets, look-back words and counters start at zero (one tiny kernel, not a memset)
@@ -1057,8 +1060,9 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
     }
     CUDA_TRY(cudaEventRecord(B->fork, s));
   }
-  for (int fam = 0; fam < 5; fam++) {
+  for (int fam = 0; fam < kStreams; fam++) {
     if (!has[fam]) continue;
+    const int acct = fam == S_ANS ? F_LZ4 : fam;  // the family the times and launches are reported under
     cudaStream_t fs = fork ? B->fam[fam] : s;
     if (fork) CUDA_TRY(cudaStreamWaitEvent(fs, B->fork, 0));
     cudaEvent_t ta = nullptr;
@@ -1115,11 +1119,13 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
         }
         break;
       }
-      case F_LZ4:  // the chunk-sequential family: LZ4 and range ANS
+      case F_LZ4:  // the chunk-sequential family: LZ4 here, range ANS (+ String-dictionary) on S_ANS
         for (size_t i = 0; i < B->lz4.size() && !st; i++) {
           st = timed(K_LZ4, [&] { return launch_lz4(B->lz4[i], B->lz4_max_sub[i], B->lz4_max_csub[i], fs); });
           n++; B->fam_launches[F_LZ4]++;
         }
+        break;
+      case S_ANS:
         for (size_t i = 0; i < B->ans.size() && !st; i++) {
           st = timed(K_ANS, [&] { return launch_ans(B->ans[i], B->ans[i].n && B->ans[i].d[0].il == 32, fs); });
           n++; B->fam_launches[F_LZ4]++;
@@ -1148,7 +1154,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
     if (fam_t) {
       cudaEvent_t tb = ev_get(B, evk++);
       CUDA_TRY(cudaEventRecordWithFlags(tb, fs, evflags));
-      B->pending.push_back({fam, ta, tb});
+      B->pending.push_back({acct, ta, tb});
     }
     if (fork) {
       CUDA_TRY(cudaEventRecord(B->join[fam], fs));
@@ -1190,7 +1196,7 @@ struct cdm_engine {
     // decode + family streams of this slot: groups in different slots decode concurrently (a latency-bound
     // RLE group does not hold back the bandwidth-bound group behind it); shared when the user passed one
     cudaStream_t ds = nullptr;
-    cudaStream_t fam[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t fam[kStreams] = {};
     bool own_streams = false;
   };
   std::vector<Slot> slots;
@@ -1209,7 +1215,7 @@ struct cdm_engine {
   std::map<uint64_t, Ticket> tickets;
   uint64_t next_ticket = 1, next_group = 1;
   std::vector<cudaEvent_t> event_pool;
-  cudaStream_t fam[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // concurrent kernel families
+  cudaStream_t fam[kStreams] = {};  // concurrent kernel families
   uint32_t* err_host = nullptr;  // pinned (mapped) ring of per-chunk error words
   uint32_t* err_mapped = nullptr;  // its device alias: harvest_kernel stores there
   uint32_t err_ring = 0, err_next = 0;
@@ -1279,7 +1285,7 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   int prio_lo = 0, prio_hi = 0;  // numerically: least (lowest) and greatest (highest) priority
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   auto make_fams = [&](cudaStream_t* fam) -> cudaError_t {
-    for (int f = 0; f < 5; f++) {
+    for (int f = 0; f < kStreams; f++) {
       cudaError_t ce = cudaStreamCreateWithPriority(&fam[f], cudaStreamNonBlocking, fam_priority(f, prio_lo, prio_hi));
       if (ce != cudaSuccess) return ce;
     }
@@ -1290,7 +1296,7 @@ extern "C" CDM_API cdm_status cdm_engine_create(int device, const cdm_engine_opt
   for (auto& s : e->slots) {
     if (o.decode_stream) {  // the caller's decode stream orders every group
       s.ds = e->decode;
-      for (int f = 0; f < 5; f++) s.fam[f] = e->fam[f];
+      for (int f = 0; f < kStreams; f++) s.fam[f] = e->fam[f];
     } else {
       CUDA_TRY(cudaStreamCreateWithPriority(&s.ds, cudaStreamNonBlocking, prio_hi));
       CUDA_TRY(make_fams(s.fam));
@@ -1859,10 +1865,10 @@ extern "C" CDM_API cdm_status cdm_pipeline_create(cdm_engine* e, const cdm_job* 
   const size_t lanes = std::min<size_t>(std::max<size_t>(groups.size(), 1), max_lanes);
   cudaStream_t origin = mk(prio_hi), copy = mk(prio_hi);
   std::vector<cudaStream_t> ds(lanes);
-  std::vector<std::array<cudaStream_t, 5>> fam(lanes);
+  std::vector<std::array<cudaStream_t, kStreams>> fam(lanes);
   for (size_t l = 0; l < lanes; l++) {
     ds[l] = mk(prio_hi);
-    for (int f = 0; f < 5; f++) fam[l][f] = mk(fam_priority(f, prio_lo, prio_hi));
+    for (int f = 0; f < kStreams; f++) fam[l][f] = mk(fam_priority(f, prio_lo, prio_hi));
   }
   for (auto x : P->streams) if (!x) return fail(CDM_E_CUDA, "pipeline stream creation failed");
   std::vector<cudaEvent_t> copied(groups.size());
