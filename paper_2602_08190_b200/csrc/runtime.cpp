@@ -501,6 +501,8 @@ enum Family { F_FP = 0, F_SCAN = 1, F_RLE = 2, F_LZ4 = 3, F_COPY = 4 };
 // kernel streams: one per family, plus S_ANS for the range-ANS -> String-dictionary chain, which is independent of
 // the LZ4 launches (its times and launches are reported under F_LZ4, the chunk-sequential family)
 constexpr int S_ANS = 5, kStreams = 6;
+constexpr uint64_t kLz4BigSubs = 65536;  // LZ4 sub-chunks per batch from which LZ4 runs in a phase of its own
+constexpr int kBigPhaseMode = 2;  // [LZ4, ANS->String-dictionary] then [FP, scan, RLE, copy]
 
 // Stream priority of a kernel family.  CDM_RLE_PRIO=hi: the latency-bound RLE chain (sums -> scan -> expand)
 // gets its CTAs scheduled first and the bandwidth-bound families fill the SMs it leaves idle; lo: the
@@ -508,9 +510,14 @@ constexpr int S_ANS = 5, kStreams = 6;
 static int fam_priority(int f, int lo, int hi) {
   static const int mode = [] {
     const char* v = std::getenv("CDM_RLE_PRIO");
+    const char* w = std::getenv("CDM_FAM_PRIO");
+    if (w && std::string(w) == "lz4hi") return 2;
+    if (w && std::string(w) == "lz4lo") return 3;
     return v && v[0] == 'h' ? 1 : 0;
   }();
   if (mode == 1) return f == F_RLE ? hi : lo;
+  if (mode == 2) return f == F_LZ4 ? hi : lo;
+  if (mode == 3) return f == F_LZ4 || f == F_RLE ? lo : hi;
   return f == F_RLE ? lo : hi;
 }
 
@@ -1053,15 +1060,31 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
   // of later groups (and the engine's bookkeeping kernels) get SMs as soon as an RLE CTA retires
   // per-kernel timing (mode 2) runs the families one after another, so each launch's events time it alone
   const bool fork = (nfam > 1 || has[F_RLE]) && B->fam && !serial && !(B->timing && B->timing_mode == 2);
-  if (fork) {
-    if (!B->fork) {
-      CUDA_TRY(cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming));
-      for (auto& ev : B->join) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    }
-    CUDA_TRY(cudaEventRecord(B->fork, s));
+  if (fork && !B->fork) {
+    CUDA_TRY(cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming));
+    for (auto& ev : B->join) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
+  // phases: the families of one phase run concurrently, phases one after another.  A throughput-bound LZ4
+  // launch (>= kLz4BigSubs sub-chunks: its threads hold the SMs for the whole launch and re-read their match
+  // windows from DRAM) slows every family running beside it, so big batches give it a phase of its own
+  // (config 4, SF 30, device-resident: one phase 854 GB/s, all serial 1090, [LZ4 + ANS/String-dictionary] then
+  // [FP, scan, RLE] 1149); small batches keep one phase (SF 1 / 3: one phase 706 / 707 vs serial 542 / 654)
+  static const int phase_mode = std::getenv("CDM_PHASES") ? std::atoi(std::getenv("CDM_PHASES")) : -1;
+  uint64_t lz4_subs = 0;
+  for (const auto& lb : B->lz4) lz4_subs += lb.total_subs;
+  int mode = phase_mode >= 0 ? phase_mode : (lz4_subs >= kLz4BigSubs ? kBigPhaseMode : 0);
+  int phase[kStreams] = {0, 0, 0, 0, 0, 0};
+  switch (mode) {
+    case 1: phase[F_LZ4] = 0; phase[F_FP] = phase[F_SCAN] = phase[F_RLE] = phase[F_COPY] = phase[S_ANS] = 1; break;
+    case 2: phase[F_LZ4] = phase[S_ANS] = 0; phase[F_FP] = phase[F_SCAN] = phase[F_RLE] = phase[F_COPY] = 1; break;
+    case 3: phase[F_FP] = phase[F_SCAN] = phase[F_RLE] = phase[F_COPY] = 0; phase[F_LZ4] = phase[S_ANS] = 1; break;
+    case 4: phase[F_FP] = phase[F_SCAN] = phase[F_RLE] = phase[F_COPY] = phase[S_ANS] = 0; phase[F_LZ4] = 1; break;
+    default: break;
+  }
+  for (int ph = 0; ph < 2; ph++) {
+  if (fork) CUDA_TRY(cudaEventRecord(B->fork, s));
   for (int fam = 0; fam < kStreams; fam++) {
-    if (!has[fam]) continue;
+    if (!has[fam] || phase[fam] != ph) continue;
     const int acct = fam == S_ANS ? F_LZ4 : fam;  // the family the times and launches are reported under
     cudaStream_t fs = fork ? B->fam[fam] : s;
     if (fork) CUDA_TRY(cudaStreamWaitEvent(fs, B->fork, 0));
@@ -1160,6 +1183,7 @@ cdm_status batch_enqueue(cdm_batch* B, cudaStream_t s, uint32_t* nl) {
       CUDA_TRY(cudaEventRecord(B->join[fam], fs));
       CUDA_TRY(cudaStreamWaitEvent(s, B->join[fam], 0));
     }
+  }
   }
   if (nl) *nl = n;
   return CDM_OK;
