@@ -183,12 +183,16 @@ struct Lz4Desc {
   uint32_t uniform;        // > 0: every sub-chunk but the last decompresses to exactly this many bytes
 };
 
+// LZ4 launches take up to kMaxLz4Batch chunks (a 14 KB __grid_constant__ parameter): the thread kernel's CTAs
+// retire in waves of one sub-chunk chain each, so fewer, larger launches leave fewer partly idle drain waves
+constexpr int kMaxLz4Batch = 256;
 struct Lz4Batch {
   uint32_t n;
   uint32_t total_subs;
   uint32_t* err;
-  Lz4Desc d[kMaxBatch];
+  Lz4Desc d[kMaxLz4Batch];
 };
+static_assert(sizeof(Lz4Batch) <= 32000, "kernel parameter limit");
 
 // ---------------------------------------------------------------- NEXT-1: chunk-sequential range ANS
 struct AnsDesc {

@@ -640,10 +640,10 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
         break;
     }
   }
-  auto groups = [](const std::vector<int>& v) {
+  auto groups = [](const std::vector<int>& v, size_t cap = kMaxBatch) {
     std::vector<std::vector<int>> g;
-    for (size_t i = 0; i < v.size(); i += kMaxBatch)
-      g.emplace_back(v.begin() + i, v.begin() + std::min(v.size(), i + size_t(kMaxBatch)));
+    for (size_t i = 0; i < v.size(); i += cap)
+      g.emplace_back(v.begin() + i, v.begin() + std::min(v.size(), i + cap));
     return g;
   };
   // FP: numeric rows and FIXED (CHAR(n)) rows in separate launches (separate kernel kinds)
@@ -955,7 +955,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     B->sd.push_back(sb);
   }
   // LZ4
-  for (auto& g : groups(lzj)) {
+  for (auto& g : groups(lzj, kMaxLz4Batch)) {
     Lz4Batch lb{};
     lb.err = B->err_dev;
     uint32_t subs = 0, max_sub = 0, max_csub = 0;
