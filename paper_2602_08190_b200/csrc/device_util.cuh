@@ -340,5 +340,90 @@ __device__ __forceinline__ void block_excl_scan_pair(uint64_t a, uint64_t b, uin
   *eb = py + y - b;
 }
 
+
+// ---- byte-granular 16-byte moves (LZ4, String-dictionary)
+__device__ __forceinline__ uint2 ld_v2_global(const void* p) {  // coherent (the thread's own earlier stores)
+  uint2 v;
+  asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint2 ld_v2_nc(const void* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+
+// bytes [a, a + k) (k <= 16) into v (little-endian words); only the 8-byte words holding them are read
+template <bool NC>
+__device__ __forceinline__ void load16(const uint8_t* a, uint32_t k, uint32_t (&v)[4]) {
+  const uintptr_t p = reinterpret_cast<uintptr_t>(a);
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(p & ~uintptr_t(7));
+  const uint32_t f = uint32_t(p & 7u);
+  const uint2 z = make_uint2(0u, 0u);
+  const uint2 x0 = NC ? ld_v2_nc(b) : ld_v2_global(b);
+  const uint2 x1 = f + k > 8 ? (NC ? ld_v2_nc(b + 8) : ld_v2_global(b + 8)) : z;
+  const uint2 x2 = f + k > 16 ? (NC ? ld_v2_nc(b + 16) : ld_v2_global(b + 16)) : z;
+  const bool hi = f >= 4;
+  const uint32_t sh = (f & 3u) * 8u;
+  const uint32_t w0 = hi ? x0.y : x0.x, w1 = hi ? x1.x : x0.y, w2 = hi ? x1.y : x1.x, w3 = hi ? x2.x : x1.y,
+                 w4 = hi ? x2.y : x2.x;
+  v[0] = __funnelshift_r(w0, w1, sh);
+  v[1] = __funnelshift_r(w1, w2, sh);
+  v[2] = __funnelshift_r(w2, w3, sh);
+  v[3] = __funnelshift_r(w3, w4, sh);
+}
+
+// explicit shared-space accesses (32-bit shared addresses): the output image is only touched through these
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void reds_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// 16 bytes at shared byte address a (any alignment; the 4 bytes after a + 16 must be readable)
+__device__ __forceinline__ void sload16(uint32_t a, uint32_t (&v)[4]) {
+  const uint32_t b = a & ~3u, sh = (a & 3u) * 8u;
+  const uint32_t w0 = lds_u32(b), w1 = lds_u32(b + 4), w2 = lds_u32(b + 8), w3 = lds_u32(b + 12), w4 = lds_u32(b + 16);
+  v[0] = __funnelshift_r(w0, w1, sh);
+  v[1] = __funnelshift_r(w1, w2, sh);
+  v[2] = __funnelshift_r(w2, w3, sh);
+  v[3] = __funnelshift_r(w3, w4, sh);
+}
+// bytes [0, k) of v (1 <= k <= 16) to shared byte address a of a ZEROED image whose other bytes other lanes may
+// be writing: whole words with one store, partial words OR-ed in (only this lane's bytes are non-zero)
+__device__ __forceinline__ void sstore16(uint32_t a, const uint32_t (&v)[4], uint32_t k) {
+  const uint32_t a3 = a & 3u, sh = 8u * a3, base = a & ~3u, e = a3 + k;
+  uint32_t u[5];
+  u[0] = v[0] << sh;
+  u[1] = __funnelshift_l(v[0], v[1], sh);
+  u[2] = __funnelshift_l(v[1], v[2], sh);
+  u[3] = __funnelshift_l(v[2], v[3], sh);
+  u[4] = sh ? (v[3] >> (32u - sh)) : 0u;
+#pragma unroll
+  for (int i = 0; i < 5; i++) {
+    const int lo = max(int(a3) - 4 * i, 0), hi = min(int(e) - 4 * i, 4);
+    if (hi > lo) {
+      if (hi - lo == 4) sts_u32(base + 4 * i, u[i]);
+      else reds_or(base + 4 * i, u[i] & (((1u << (8 * (hi - lo))) - 1u) << (8 * lo)));
+    }
+  }
+}
+
+
 }  // namespace dev
 }  // namespace cdm

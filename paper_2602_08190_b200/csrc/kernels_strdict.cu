@@ -409,12 +409,25 @@ __global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constan
       }
       continue;
     }
-    {  // image byte sh + q = tile byte q
-      uint32_t p = sh + ex;
+    // image byte sh + q = tile byte q.  The image is zeroed, then every token is moved 16 bytes at a time (the
+    // dictionary read at any alignment: five words + funnel shifts) and written as whole words, its edge words
+    // OR-ed in (the neighbouring tokens' bytes in them belong to other threads)
+    const uint32_t simg = smem_addr(stage_b);
+    for (uint32_t i = tid; 16 * i < sh + Tt; i += kSdBT) sts_v4(simg + 16 * i, make_uint4(0u, 0u, 0u, 0u));
+    __syncthreads();
+    {
+      uint32_t p = simg + sh + ex;
+      const bool dsm = B.dict_smem != 0;
+      const uint32_t stb = dsm ? smem_addr(tb) : 0u;
 #pragma unroll
       for (int r = 0; r < kSdBPer; r++) {
-        const uint8_t* src = tb + a[r];
-        for (uint32_t j = 0; j < len[r]; j++) stage_b[p + j] = src[j];
+        for (uint32_t t = 0; t < len[r]; t += 16) {
+          const uint32_t kk = min(16u, len[r] - t);
+          uint32_t v[4];
+          if (dsm) sload16(stb + a[r] + t, v);
+          else load16<true>(tb + a[r] + t, kk, v);
+          sstore16(p + t, v, kk);
+        }
         p += len[r];
       }
     }
@@ -457,13 +470,13 @@ cudaError_t launch_strdict(const SdBatch& b, cudaStream_t s) {
     static int occ3[kMaxDevices] = {};
     const int dev3 = current_device();
     if (!conf3[dev3]) {
-      cudaFuncSetAttribute(sd_expand_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 32 + kSdDictSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3[dev3], sd_expand_b_kernel, kSdBT, kSdStage + 32 + kSdDictSmem);
+      cudaFuncSetAttribute(sd_expand_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSdStage + 64 + kSdDictSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3[dev3], sd_expand_b_kernel, kSdBT, kSdStage + 64 + kSdDictSmem);
       if (occ3[dev3] < 1) occ3[dev3] = 1;
       conf3[dev3] = true;
     }
     const uint32_t grid = std::min<uint32_t>(b.total_tiles, uint32_t(device_sms() * occ3[dev3]));
-    sd_expand_b_kernel<<<grid, kSdBT, kSdStage + 32 + b.dict_smem, s>>>(b);
+    sd_expand_b_kernel<<<grid, kSdBT, kSdStage + 32 + b.dict_smem + (b.dict_smem ? 32 : 0), s>>>(b);
   } else if (variant != 2) {
     sd_expand_kernel<<<b.total_tiles, kThreads, 0, s>>>(l1);
   } else {
