@@ -15,6 +15,8 @@
 // instruction.  Small dictionaries (the TPC-H flags, modes, priorities: <= 100 B) are read from shared
 // memory, large ones (o_clerk: ~1.5 MB per chunk) through the read-only path.  Persistent CTAs walk
 // contiguous ranges of (tile, pass) units of 256*G rows.  Widths without an instantiation use fp_kernel's generic byte path.
+#include <cstdlib>
+
 #include "device_util.cuh"
 #include "kernels.h"
 
@@ -61,11 +63,23 @@ __device__ __forceinline__ uint4 lds128(const uint32_t* p) {
   return v;
 }
 
-// DSM: every dictionary of the launch fits kCharDictSmem and is read from shared memory
-template <int E, bool DSM>
+// Pre-shifted dictionaries (PRE): for the few-entry dictionaries of the TPC-H CHAR(n) columns (modes, priorities,
+// instructions: 4-7 entries) the shared copy holds every entry at each of the 4 byte alignments a row can start
+// at inside its group, zero-padded to PB = 16 / 32 bytes: table[s][idx] = the entry's bytes at byte offset s.
+// A row then costs one or two 16-byte shared loads and an OR per word (no funnel shifts, no edge masks).
+template <int E>
+struct PreShape {
+  static constexpr int PB = E + 3 <= 16 ? 16 : 32;      // padded bytes per shifted entry
+  static constexpr int MAXE = kCharDictSmem / (4 * PB);  // entries that fit the shared table
+};
+
+// DSM: every dictionary of the launch fits kCharDictSmem and is read from shared memory; PRE (implies DSM):
+// every dictionary has at most PreShape<E>::MAXE entries and is read from the pre-shifted table
+template <int E, bool DSM, bool PRE>
 __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ FpBatch B, uint32_t total_units) {
   using S = CharShape<E>;
   constexpr int NW = S::NW, G = S::G;
+  constexpr int PB = PreShape<E>::PB;
   // shared: [DSM: 4 guard words + dictionary words + 4 guard words] [!DIRECT: 8 warps x 32 groups x NW words]
   extern __shared__ __align__(16) uint32_t sm[];
   constexpr uint32_t kDictWords = DSM ? kCharDictSmem / 4 + 8 : 0;
@@ -93,10 +107,24 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
     const uint32_t m32 = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
     if (DSM && di != staged_di) {  // CTA-uniform: stage this chunk's dictionary (guard words stay zero)
       __syncthreads();             // nobody still reads the previous dictionary
-      const uint32_t nwords = (entries * uint32_t(E) + 3) / 4;
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(D.dict);
-      for (uint32_t q = tid; q < nwords + 8; q += kThreads)
-        dict_s[q] = (q >= 4 && q - 4 < nwords) ? __ldg(src + (q - 4)) : 0u;
+      if (PRE) {  // table word (s, idx, m): bytes 4m..4m+3 of entry idx placed at byte offset s
+        const uint32_t per_s = entries * (PB / 4), nwords = 4 * per_s;
+        for (uint32_t q = tid; q < nwords; q += kThreads) {
+          const uint32_t sft = q / per_s, r = q % per_s, idx = r / (PB / 4), m = r % (PB / 4);
+          uint32_t x = 0;
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            const int src = int(4 * m + b) - int(sft);
+            if (src >= 0 && src < E) x |= uint32_t(__ldg(D.dict + size_t(idx) * E + src)) << (8 * b);
+          }
+          dict_s[q] = x;
+        }
+      } else {
+        const uint32_t nwords = (entries * uint32_t(E) + 3) / 4;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(D.dict);
+        for (uint32_t q = tid; q < nwords + 8; q += kThreads)
+          dict_s[q] = (q >= 4 && q - 4 < nwords) ? __ldg(src + (q - 4)) : 0u;
+      }
       __syncthreads();
       staged_di = di;
     }
@@ -146,6 +174,19 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
       }
       // row j occupies group bytes [j*E, j*E + E): words q0..q1, starting at byte s of word q0
       const int s = (j * E) & 3, q0 = (j * E) >> 2, q1 = (j * E + E - 1) >> 2;
+      if (PRE) {  // the entry pre-shifted to byte s: whole words, zero outside the row
+        const uint32_t* t = dict_s + (uint32_t(s) * entries + idx) * (PB / 4);
+#pragma unroll
+        for (int h = 0; h < PB / 16; h++) {
+          if (4 * h > q1 - q0) break;
+          const uint4 x = lds128(t + 4 * h);
+          const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int m = 0; m < 4; m++)
+            if (4 * h + m <= q1 - q0) word[q0 + 4 * h + m] |= xw[m];
+        }
+        continue;
+      }
       const int64_t a = int64_t(idx) * E - s;  // dictionary byte that lands on group byte 4*q0
       const int64_t aw = a >> 2;                // >= -1 (guard word)
       const uint32_t sh = uint32_t(a) & 3u;
@@ -202,12 +243,17 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
 template <int E>
 cudaError_t launch_fpc_e(const FpBatch& b, cudaStream_t s) {
   using S = CharShape<E>;
-  bool dsm = true;
-  for (uint32_t i = 0; i < b.n; i++) dsm = dsm && uint64_t(b.d[i].entries) * E <= kCharDictSmem;
+  bool dsm = true, pre = E > 2;
+  for (uint32_t i = 0; i < b.n; i++) {
+    dsm = dsm && uint64_t(b.d[i].entries) * E <= kCharDictSmem;
+    pre = pre && b.d[i].entries <= uint32_t(PreShape<E>::MAXE);
+  }
+  static const bool no_pre = std::getenv("CDM_FPC_PRE") && std::getenv("CDM_FPC_PRE")[0] == '0';
+  pre = pre && !no_pre;
   const uint32_t smem = (dsm ? (kCharDictSmem + 32) : 0) + (S::DIRECT ? 0 : 8 * 32 * S::NW * 4);
-  auto kern = dsm ? fpc_kernel<E, true> : fpc_kernel<E, false>;
-  static bool configured[kMaxDevices][2] = {};
-  bool& conf = configured[current_device()][dsm];
+  auto kern = pre ? fpc_kernel<E, true, true> : dsm ? fpc_kernel<E, true, false> : fpc_kernel<E, false, false>;
+  static bool configured[kMaxDevices][3] = {};
+  bool& conf = configured[current_device()][pre ? 2 : dsm];
   if (!conf) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     conf = true;

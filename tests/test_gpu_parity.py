@@ -663,6 +663,34 @@ def test_corrupt_dict_index_sets_error(engine):
         assert r["error_bits"] & cdm.ERR_DICT_INDEX
 
 
+@pytest.mark.parametrize("E", [10, 15, 25])
+def test_corrupt_char_dict_index_sets_error(engine, E):
+    """CHAR(n) rows (row-group kernel, pre-shifted table): an index past the dictionary sets CDM_ERR_DICT_INDEX"""
+    spec = "Dict|BitPack"
+    words = np.frombuffer(b"".join(bytes([65 + k]) * E for k in range(4)), dtype=np.uint8)
+    n = 9000
+    root = cdm1.Node(cdm1.DICT, n, [cdm1.raw(words.tobytes(), eb=E),
+                                    cdm1.bitpack([i % 5 for i in range(n)], 3, 0)], entries=4, E=E)
+    ch = cdm1.build(root, cdm1.FIXED, E, n, cascade_hash=_hash(spec))
+    casc = cdm.Cascade(spec, cdm1.FIXED, E)
+    for resident in (False, True):
+        (_, _, r), = gpu_decode(engine, casc, [ch], resident=resident, expect_error=True)
+        assert r["error_bits"] & cdm.ERR_DICT_INDEX
+
+
+def test_char_rows_plain_shared_dictionary_variant():
+    """CDM_FPC_PRE=0 (fresh process): the TPC-H CHAR(n) columns through the plain shared dictionary copy"""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
+            "from paper_2602_08190_b200.inputs import TPCH; e = cdm.Engine(0); g = TPCH(0.02); "
+            "[t.check_parity(e, 'Dict|BitPack', g.column(n), rows_per_chunk=50_001, both=False) for n in "
+            "('l_shipmode', 'l_shipinstruct', 'o_orderpriority')]; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_FPC_PRE": "0"}, capture_output=True,
+                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_corrupt_run_sum_sets_error(engine):
     spec = "RLE|[BitPack,BitPack]"
     for counts in ([3] * 4000, [3] * 4000 + [10 ** 6]):
@@ -679,8 +707,9 @@ def test_corrupt_run_sum_sets_error(engine):
 # 25) and the generic byte path's (5, 7, 12, 31) -- with a tiny dictionary (shared-memory path), a large one
 # (o_clerk-like, read through L1/L2) and an out-of-range index free column; ragged tails across several tiles.
 @pytest.mark.parametrize("E", [1, 2, 3, 5, 7, 10, 12, 15, 25, 31])
-@pytest.mark.parametrize("entries", [3, 7, 2000])
+@pytest.mark.parametrize("entries", [3, 7, 300, 2000])
 def test_char_rows_every_width(engine, E, entries):
+    """entries 3 / 7: the pre-shifted shared table (E >= 3), 300: the plain shared copy, 2000: read through L1"""
     rng = np.random.default_rng(E * 1000 + entries)
     words = rng.integers(32, 127, size=(entries, E), dtype=np.uint8)
     words = np.unique(words, axis=0)
