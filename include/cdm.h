@@ -275,8 +275,9 @@ CDM_API cdm_status cdm_checksum(const void *dev_data, uint64_t bytes, uint64_t c
  *   "gp_ctas_per_sm"  G.P. pattern's L (Table 3 G.P. row): resident rle_kernel CTAs per SM, 0 = the kernel's own
  *                     occupancy (default), 1..8 (enforced by padding the launch's dynamic shared memory)
  *   "scan_mode"       H6 schedule (single-pass look-back vs the 2-pass baseline): 0 =
- *                     reduce-then-scan (tile sums, then a persistent scan; default), 1 = single-pass decoupled
- *                     look-back (one tile per CTA in ticket order); env CDM_SCAN_MODE sets the start value
+ *                     reduce-then-scan (tile sums, then a persistent scan), 1 = single-pass decoupled look-back
+ *                     (one tile per CTA in ticket order), 2 = warp tiles (default: 512-value warp-tile sums, a
+ *                     per-chunk scan of them, then one warp per tile with no CTA barrier); env CDM_SCAN_MODE
  * Errors: CDM_E_INVALID_ARG for an unknown knob, a value outside its set, or a null pointer. */
 CDM_API cdm_status cdm_tune_set(const char *knob, int value);
 CDM_API cdm_status cdm_tune_get(const char *knob, int *value);

@@ -286,7 +286,7 @@ cudaError_t launch_checksum(const void* p, uint64_t bytes, uint64_t chunk_id, ui
 enum TuneKnob : int {
   TUNE_FP_CTAS_PER_SM = 0,  // F.P. "L": persistent fp_kernel CTAs per SM (0 = adaptive 2/3/4)
   TUNE_LZ4_LANES = 1,       // N.P. "C": lanes per LZ4 sub-chunk: 1 (thread per sub-chunk), 2..16 (lane groups), 32
-  TUNE_SCAN_MODE = 2,       // H6 schedule: 0 reduce-then-scan (tile sums + persistent scan), 1 decoupled look-back
+  TUNE_SCAN_MODE = 2,       // H6 schedule: 0 reduce-then-scan, 1 decoupled look-back, 2 warp tiles (3 passes, default)
   TUNE_GP_CTAS_PER_SM = 3,  // G.P. "L": resident rle_kernel CTAs per SM (0 = the kernel's occupancy), 1..8
   TUNE_LZ4_SPLIT = 4,       // H8 schedule: 1 = split parse (owner lane) / copy (whole warp), 0 = TUNE_LZ4_LANES
   TUNE_LZ4_SPLIT_G = 5,     // split schedule: sub-chunks per warp, 0 = per launch size, else 1/2/4/8

@@ -312,7 +312,7 @@ void tune_init() {
   if (g_tune_init) return;
   g_tune[TUNE_FP_CTAS_PER_SM] = std::getenv("CDM_FP_CTAS_PER_SM") ? std::atoi(std::getenv("CDM_FP_CTAS_PER_SM")) : 0;
   g_tune[TUNE_LZ4_LANES] = std::getenv("CDM_LZ4_G") ? std::atoi(std::getenv("CDM_LZ4_G")) : 1;
-  g_tune[TUNE_SCAN_MODE] = std::getenv("CDM_SCAN_MODE") ? std::atoi(std::getenv("CDM_SCAN_MODE")) : 0;
+  g_tune[TUNE_SCAN_MODE] = std::getenv("CDM_SCAN_MODE") ? std::atoi(std::getenv("CDM_SCAN_MODE")) : 2;
   g_tune[TUNE_GP_CTAS_PER_SM] = 0;
   g_tune[TUNE_LZ4_SPLIT] = std::getenv("CDM_LZ4_SPLIT") ? std::atoi(std::getenv("CDM_LZ4_SPLIT")) : 1;
   g_tune[TUNE_LZ4_SPLIT_G] = std::getenv("CDM_LZ4_SPLIT_G") ? std::atoi(std::getenv("CDM_LZ4_SPLIT_G")) : 0;

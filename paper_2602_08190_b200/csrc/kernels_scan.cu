@@ -314,6 +314,175 @@ __global__ void __launch_bounds__(kThreads) scan_kernel_lb(const __grid_constant
                                    0);
 }
 
+// ------------------------------------------------------------------------------------------ warp tiles (3 passes)
+// scan_mode 2: the scan without any CTA-wide barrier.  Warp tiles of kSub = 512 values (16 per
+// lane): pass 1 (scan_wsums_kernel) writes every warp tile's exact sum, pass 2 (scan_wprefix_kernel, one CTA per
+// chunk) scans a chunk's warp-tile sums in place (and checks / writes the offsets' total), pass 3
+// (scan_warp_kernel) gives every warp tile to one warp: its 16 fields per lane are unpacked from global memory
+// through a sliding two-word window, scanned in registers and across the warp with shuffles, offset by the tile's
+// prefix, and leave through a per-warp shared stage as 16-byte stores (__syncwarp only).
+constexpr uint32_t kSub = 512;
+constexpr uint32_t kSubPer = kSub / 32;  // 16 values per lane
+constexpr uint32_t kSubPerTile = kScanTile / kSub;
+
+// the lane's kSubPer fields (FOR added; dictionary entries for Delta|Dict|BitPack) of elements [e0, e0 + nv),
+// unpacked from global memory through a sliding two-word window
+template <typename T>
+__device__ __forceinline__ void lane_fields(const ScanDesc& D, uint64_t e0, uint32_t nv, T (&f)[kSubPer], bool& bad) {
+  const uint32_t w = D.w;
+  const uint32_t* wd = reinterpret_cast<const uint32_t*>(D.packed);
+  if (D.dict) {
+#pragma unroll
+    for (uint32_t j = 0; j < kSubPer; j++) {
+      f[j] = 0;
+      if (j < nv) {
+        const uint64_t ix = D.for_base + (w ? extract_bits_global(wd, (e0 + j) * w, w) : 0ull);
+        if (ix < D.entries) f[j] = T(__ldg(D.dict + ix)); else bad = true;
+      }
+    }
+    return;
+  }
+  const T fb = T(D.for_base);
+  if (w == 0) {
+#pragma unroll
+    for (uint32_t j = 0; j < kSubPer; j++) f[j] = j < nv ? fb : T(0);
+  } else if (w <= 32) {
+    const uint32_t m = w == 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+    const uint64_t b0 = e0 * w;
+    uint64_t q = b0 >> 5;
+    uint32_t sh = uint32_t(b0 & 31);
+    uint32_t lo = nv ? __ldg(wd + q) : 0u, hi = nv ? __ldg(wd + q + 1) : 0u;
+#pragma unroll
+    for (uint32_t j = 0; j < kSubPer; j++) {
+      f[j] = j < nv ? fb + T(__funnelshift_r(lo, hi, sh) & m) : T(0);
+      sh += w;
+      if (sh >= 32) {
+        sh -= 32;
+        q++;
+        lo = hi;
+        hi = j + 1 < nv ? __ldg(wd + q + 1) : 0u;  // never past the last field's word + 1 (stream padding)
+      }
+    }
+  } else {
+#pragma unroll
+    for (uint32_t j = 0; j < kSubPer; j++) f[j] = j < nv ? fb + T(extract_bits_global(wd, (e0 + j) * w, w)) : T(0);
+  }
+}
+
+__device__ __forceinline__ uint32_t chunk_subs(const ScanDesc& D) { return (D.n + kSub - 1) / kSub; }
+
+// pass 1: one warp per warp tile (sub-tiles of a chunk are numbered from kSubPerTile * tile0)
+__global__ void __launch_bounds__(kThreads) scan_wsums_kernel(const __grid_constant__ ScanBatch B) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gs = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (gs >= B.total_tiles * kSubPerTile) return;
+  const ScanDesc& D = B.d[find_desc_scan(B, gs / kSubPerTile)];
+  const uint32_t ls = gs - D.tile0 * kSubPerTile;
+  if (ls >= chunk_subs(D)) return;
+  const uint64_t e0 = uint64_t(ls) * kSub + lane * kSubPer;
+  const uint32_t nv = e0 < D.n ? uint32_t(min(uint64_t(kSubPer), uint64_t(D.n) - e0)) : 0u;
+  uint64_t f[kSubPer];
+  bool bad = false;
+  lane_fields<uint64_t>(D, e0, nv, f, bad);
+  uint64_t acc = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kSubPer; j++) acc += f[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if (lane == 0) B.tsum[gs] = acc;
+  if (bad) atomicOr(B.err + D.err_idx, 0x1u);
+}
+
+// pass 2: one CTA per chunk: exclusive scan of its warp-tile sums in place; the offsets' total is checked against
+// the node's byte count (CDM_ERR_LENGTHS) and written as out[n]
+constexpr int kPfxThreads = 1024;
+__global__ void __launch_bounds__(kPfxThreads) scan_wprefix_kernel(const __grid_constant__ ScanBatch B) {
+  __shared__ uint64_t warp_s[kPfxThreads / 32];
+  const ScanDesc& D = B.d[blockIdx.x];
+  uint64_t* ts = B.tsum + uint64_t(D.tile0) * kSubPerTile;
+  const uint32_t ns = chunk_subs(D), per = (ns + kPfxThreads - 1) / kPfxThreads;
+  const uint32_t i0 = min(ns, threadIdx.x * per), i1 = min(ns, i0 + per);
+  uint64_t sum = 0;
+  for (uint32_t i = i0; i < i1; i++) sum += __ldcg(ts + i);
+  uint64_t tot;
+  uint64_t run = block_excl_scan_u64<kPfxThreads>(sum, warp_s, &tot);
+  for (uint32_t i = i0; i < i1; i++) {
+    const uint64_t v = __ldcg(ts + i);
+    ts[i] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0 && D.mode == SCAN_OFFSETS) {
+    if (tot != D.base) atomicOr(B.err + D.err_idx, 0x8u);  // CDM_ERR_LENGTHS
+    reinterpret_cast<int32_t*>(D.out)[D.n] = int32_t(uint32_t(tot));
+  }
+}
+
+// pass 3: one warp per warp tile
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 4) scan_warp_kernel(const __grid_constant__ ScanBatch B) {
+  constexpr uint32_t kStage = kSub + kSub / 16;  // one pad slot per 16 values: conflict-free lane rows
+  __shared__ __align__(16) T stage_s[kThreads / 32][kStage];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t gs = blockIdx.x * (kThreads / 32) + wib;
+  if (gs >= B.total_tiles * kSubPerTile) return;
+  const ScanDesc& D = B.d[find_desc_scan(B, gs / kSubPerTile)];
+  const uint32_t ls = gs - D.tile0 * kSubPerTile;
+  if (ls >= chunk_subs(D)) return;
+  const uint64_t s0 = uint64_t(ls) * kSub, e0 = s0 + lane * kSubPer;
+  const uint32_t valid = uint32_t(min(uint64_t(kSub), uint64_t(D.n) - s0));
+  const uint32_t nv = e0 < D.n ? uint32_t(min(uint64_t(kSubPer), uint64_t(D.n) - e0)) : 0u;
+  T f[kSubPer];
+  bool bad = false;  // (reported by pass 1)
+  lane_fields<T>(D, e0, nv, f, bad);
+  T run = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kSubPer; j++) {
+    const T x = f[j];
+    f[j] = run;  // exclusive within the lane
+    run += x;
+  }
+  T incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T v = __shfl_up_sync(FULL, incl, o);
+    if (lane >= uint32_t(o)) incl += v;
+  }
+  const bool delta = D.mode == SCAN_DELTA;
+  const T add = T((delta ? D.base : 0ull) + B.tsum[gs]) + (incl - run);
+  T* const st = stage_s[wib];
+  // DELTA: base + inclusive sum (exclusive + own field); OFFSETS: the exclusive sum
+#pragma unroll
+  for (uint32_t j = 0; j < kSubPer; j++) {
+    const T nxt = j + 1 < kSubPer ? f[j + 1] : run;
+    st[lane * 17 + j] = add + (delta ? nxt : f[j]);
+  }
+  __syncwarp();
+  // 4 values per 16 bytes (T = 4) or 2 (T = 8): coalesced vector stores of the warp tile's contiguous outputs
+  if (D.out_bytes == 8) {
+    uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + s0;
+    for (uint32_t k = lane; 2 * k < valid; k += 32) {
+      const uint32_t i = 2 * k;
+      const uint64_t a = uint64_t(st[i + (i >> 4)]);
+      if (i + 2 <= valid) st_v2_u64(o + i, a, uint64_t(st[i + 1 + ((i + 1) >> 4)]));
+      else o[i] = a;
+    }
+  } else {
+    uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + s0;
+    for (uint32_t k = lane; 4 * k < valid; k += 32) {
+      const uint32_t i = 4 * k;
+      uint32_t r[4];
+#pragma unroll
+      for (uint32_t j = 0; j < 4; j++) r[j] = uint32_t(st[(i + j) + ((i + j) >> 4)]);
+      if (i + 4 <= valid) {
+        st_v4_u32(o + i, r[0], r[1], r[2], r[3]);
+      } else {
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++) if (i + j < valid) o[i + j] = r[j];
+      }
+    }
+  }
+}
+
 bool pdl_on() {
   static const bool pdl = !(std::getenv("CDM_PDL") && std::getenv("CDM_PDL")[0] == '0');
   return pdl;
@@ -325,6 +494,16 @@ cudaError_t launch_scan(const ScanBatch& b, cudaStream_t s) {
   if (!b.total_tiles) return cudaSuccess;
   if (tune_get(TUNE_SCAN_MODE) == 1) {
     scan_kernel_lb<<<b.total_tiles, kThreads, 0, s>>>(b);
+    return cudaGetLastError();
+  }
+  if (tune_get(TUNE_SCAN_MODE) == 2) {
+    bool w64 = false;
+    for (uint32_t i = 0; i < b.n; i++) w64 = w64 || b.d[i].out_bytes == 8;
+    const uint32_t grid = (b.total_tiles * kSubPerTile + kThreads / 32 - 1) / (kThreads / 32);
+    scan_wsums_kernel<<<grid, kThreads, 0, s>>>(b);
+    scan_wprefix_kernel<<<b.n, kPfxThreads, 0, s>>>(b);
+    if (w64) scan_warp_kernel<uint64_t><<<grid, kThreads, 0, s>>>(b);
+    else scan_warp_kernel<uint32_t><<<grid, kThreads, 0, s>>>(b);
     return cudaGetLastError();
   }
   scan_sums_kernel<<<b.total_tiles, kThreads, 0, s>>>(b);

@@ -852,7 +852,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     for (auto& rb : B->rle) rb.trace = A.take<uint64_t>(size_t(rb.total_tiles) * 8);
   }
   // ---- non-zeroed region: scan tile sums (reduce-then-scan), RLE tile sums + prefixes, big-tile slots, lineage
-  for (size_t i = 0; i < B->scan.size(); i++) B->scan[i].tsum = A.take<uint64_t>(scan_tiles[i]);
+  for (size_t i = 0; i < B->scan.size(); i++) B->scan[i].tsum = A.take<uint64_t>(size_t(scan_tiles[i]) * 8);  // 8: warp tiles per tile (scan_mode 2)
   for (size_t u = 0; u < units.size(); u++) {
     SumsChunk& d = B->sums[sums_at[u].first].d[sums_at[u].second];
     d.tsum = A.take<uint64_t>(size_t(d.tiles + d.units) * 2);  // tile sums, then one sum per rle_sums group
@@ -2319,7 +2319,7 @@ extern "C" CDM_API cdm_status cdm_tune_set(const char* knob, int value) {
     if (value < 0 || value > 8) return fail(CDM_E_INVALID_ARG, "gp_ctas_per_sm must be 0..8");
     cdm::tune_set(cdm::TUNE_GP_CTAS_PER_SM, value);
   } else if (k == "scan_mode") {
-    if (value != 0 && value != 1) return fail(CDM_E_INVALID_ARG, "scan_mode must be 0 (reduce-then-scan) or 1 (look-back)");
+    if (value < 0 || value > 2) return fail(CDM_E_INVALID_ARG, "scan_mode must be 0 (reduce-then-scan), 1 (look-back) or 2 (warp tiles)");
     cdm::tune_set(cdm::TUNE_SCAN_MODE, value);
   } else if (k == "lz4_split") {
     if (value != 0 && value != 1) return fail(CDM_E_INVALID_ARG, "lz4_split must be 0 (lz4_lanes schedules) or 1 (split parse/copy)");

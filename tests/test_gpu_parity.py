@@ -235,9 +235,10 @@ def test_config1_parity(engine):
     check_parity(engine, "BitPack", config1_column())
 
 
-@pytest.fixture(params=[0, 1])
+@pytest.fixture(params=[0, 1, 2])
 def scan_mode(request):
-    """both H6 schedules (NEXT-3 knob scan_mode): 0 reduce-then-scan, 1 single-pass decoupled look-back"""
+    """every H6 schedule (NEXT-3 knob scan_mode): 0 reduce-then-scan, 1 single-pass decoupled look-back, 2 warp
+    tiles (three passes, no CTA barriers)"""
     prev = cdm.tune_get("scan_mode")
     cdm.tune_set("scan_mode", request.param)
     yield request.param

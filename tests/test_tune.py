@@ -65,7 +65,7 @@ def test_pruned_stops_at_first_decline_even_if_not_global():
 
 def test_cabi_tuning_knobs():
     assert cdm.tune_get("lz4_lanes") in (1, 2, 4, 8, 16, 32)
-    assert cdm.tune_get("scan_mode") in (0, 1)
+    assert cdm.tune_get("scan_mode") in (0, 1, 2)
     old = cdm.tune_get("fp_ctas_per_sm")
     cdm.tune_set("fp_ctas_per_sm", 3)
     assert cdm.tune_get("fp_ctas_per_sm") == 3
@@ -89,7 +89,7 @@ def test_cabi_tuning_knobs():
         cdm.tune_set(knob, v)
         assert cdm.tune_get(knob) == v
         cdm.tune_set(knob, old)
-    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 2), ("gp_ctas_per_sm", 9), ("lz4_split", 2),
+    for knob, v in (("fp_ctas_per_sm", 17), ("lz4_lanes", 5), ("scan_mode", 3), ("gp_ctas_per_sm", 9), ("lz4_split", 2),
                      ("lz4_split_g", 16), ("lz4_spec", 3), ("nope", 1)):
         with pytest.raises(cdm.CdmError):
             cdm.tune_set(knob, v)
