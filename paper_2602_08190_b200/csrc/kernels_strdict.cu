@@ -352,17 +352,46 @@ __global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constan
   extern __shared__ __align__(16) uint32_t dyn_s[];  // stage image, then the dictionary (B.dict_smem > 0)
   uint8_t* const stage_b = reinterpret_cast<uint8_t*>(dyn_s);
   uint32_t* const dict_s = dyn_s + (kSdStage + 32) / 4;
-  __shared__ uint32_t ids_s[kIdsWords];
+  __shared__ uint32_t ids2_s[2][kIdsWords];
   __shared__ uint64_t warp_s[kSdBT / 32];
   const uint32_t tid = threadIdx.x;
   const uint32_t per = (B.total_tiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * per, t1 = min(B.total_tiles, t0 + per);
   int di = -1;
   const uint32_t* offs = nullptr;
-  for (uint32_t gt = t0; gt < t1; gt++) {
+  // the next tile's packed ids and output offset are loaded into registers while this tile expands, and
+  // written to the other ids buffer at the top of the next iteration (their latency hides behind a tile)
+  constexpr int kPre = (kIdsWords + kSdBT - 1) / kSdBT;
+  uint32_t pre[kPre];
+  uint64_t pre_o = 0;
+  auto issue = [&](uint32_t t) {
+    const SdDesc& Dn = B.d[find_desc_sd(B, t)];
+    const uint32_t ltn = t - Dn.tile0, ntn = min(uint32_t(kSdTile), Dn.ntok - ltn * kSdTile);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(Dn.ids_packed) + ((uint64_t(ltn) * kSdTile * Dn.w) >> 5);
+    const uint32_t nw = Dn.w ? uint32_t((uint64_t(ntn) * Dn.w + 31) / 32) + 2 : 0u;
+#pragma unroll
+    for (int i = 0; i < kPre; i++) {
+      const uint32_t k = tid + uint32_t(i) * kSdBT;
+      pre[i] = k < nw ? __ldg(src + k) : 0u;
+    }
+    pre_o = __ldcg(Dn.tsum + ltn);
+  };
+  auto commit = [&](uint32_t buf) {
+#pragma unroll
+    for (int i = 0; i < kPre; i++) {
+      const uint32_t k = tid + uint32_t(i) * kSdBT;
+      if (k < kIdsWords) ids2_s[buf][k] = pre[i];
+    }
+  };
+  if (t0 < t1) issue(t0);
+  for (uint32_t gt = t0, it = 0; gt < t1; gt++, it++) {
     const int dn = find_desc_sd(B, gt);
     const SdDesc& D = B.d[dn];
-    __syncthreads();  // the previous tile is done with ids_s / the image (and the dictionary)
+    uint32_t* const ids_s = ids2_s[it & 1];
+    commit(it & 1);   // this tile's ids (its buffer was last read two tiles ago, before the previous barrier)
+    const uint64_t O64 = pre_o;
+    __syncthreads();  // the previous tile is done with the image (and the dictionary); this tile's ids are in
+    if (gt + 1 < t1) issue(gt + 1);
     if (dn != di) {
       di = dn;
       offs = reinterpret_cast<const uint32_t*>(D.dict);
@@ -375,9 +404,7 @@ __global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constan
     }
     const uint32_t lt = gt - D.tile0, g0 = lt * kSdTile;
     const uint32_t nt = min(uint32_t(kSdTile), D.ntok - g0);
-    stage_bits<kSdBT>(ids_s, D.ids_packed, g0, nt, D.w);
-    const uint64_t O64 = __ldcg(D.tsum + lt);
-    __syncthreads();
+    __syncthreads();  // the dictionary staged above (when the chunk changed) is complete
     uint32_t a[kSdBPer], len[kSdBPer];
     uint32_t s = 0;
 #pragma unroll
