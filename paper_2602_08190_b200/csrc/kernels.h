@@ -39,13 +39,17 @@ struct FpDesc {
   uint8_t pad[6];
 };
 
+// FP launches take up to kMaxFpBatch chunks (a 16 KB __grid_constant__ parameter): fewer persistent launches, fewer
+// drain tails between them
+constexpr int kMaxFpBatch = 256;
 struct FpBatch {
   uint32_t n;
   uint32_t total_tiles;
   uint32_t pair_map;      // 8-byte rows: pair-interleaved lane mapping (set by launch_fp)
   uint32_t* err;          // per-chunk error words
-  FpDesc d[kMaxBatch];
+  FpDesc d[kMaxFpBatch];
 };
+static_assert(sizeof(FpBatch) <= 32000, "kernel parameter limit");
 
 // ---------------------------------------------------------------- H6: scan-dependent delta / offsets
 enum ScanMode : uint8_t { SCAN_DELTA = 0, SCAN_OFFSETS = 1 };

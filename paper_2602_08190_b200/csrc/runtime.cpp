@@ -649,15 +649,26 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   // FP: numeric rows and FIXED (CHAR(n)) rows in separate launches (separate kernel kinds)
   std::vector<int> fp_num, fp_chr;
   for (int j : fpj) (B->jobs[j].casc->dtype == T_FIXED ? fp_chr : fp_num).push_back(j);
-  std::vector<std::vector<int>> fp_groups = groups(fp_num);
+  // numeric launches: up to kMaxFpBatch chunks of similar bit width (a launch's staging buffers are sized by its
+  // widest stream)
+  std::stable_sort(fp_num.begin(), fp_num.end(), [&](int a, int c) { return B->jobs[a].main.w < B->jobs[c].main.w; });
+  std::vector<std::vector<int>> fp_groups = groups(fp_num, kMaxFpBatch);
   const size_t n_num_groups = fp_groups.size();
-  {  // CHAR(n) launches hold one row width each (the row-group kernel is specialised on it)
+  {  // CHAR(n) launches hold one row width each (the row-group kernel is specialised on it) and one dictionary class
+     // (the kernel picks its shared-memory variant by the launch's largest dictionary: o_clerk's 1.5 MB ones must
+     // not pull the few-entry ones of the same width off the pre-shifted tables)
+    auto cls = [&](int j) {
+      const Bound& b = B->jobs[j];
+      const uint64_t bytes = uint64_t(b.entries) * b.W;
+      return bytes > 16384 ? 0 : b.entries > 128 ? 1 : 2;
+    };
+    auto key = [&](int j) { return std::make_pair(B->jobs[j].W, cls(j)); };
     std::vector<int> by_w(fp_chr);
-    std::stable_sort(by_w.begin(), by_w.end(), [&](int a, int c) { return B->jobs[a].W < B->jobs[c].W; });
+    std::stable_sort(by_w.begin(), by_w.end(), [&](int a, int c) { return key(a) < key(c); });
     for (size_t i = 0; i < by_w.size();) {
       size_t k = i;
-      while (k < by_w.size() && B->jobs[by_w[k]].W == B->jobs[by_w[i]].W) k++;
-      for (auto& g : groups(std::vector<int>(by_w.begin() + i, by_w.begin() + k))) fp_groups.push_back(g);
+      while (k < by_w.size() && key(by_w[k]) == key(by_w[i])) k++;
+      for (auto& g : groups(std::vector<int>(by_w.begin() + i, by_w.begin() + k), kMaxFpBatch)) fp_groups.push_back(g);
       i = k;
     }
   }
