@@ -520,6 +520,59 @@ def test_lz4_lane_widths(engine, lz4_lanes):
     check_parity(engine, "Str|[LZ4(sub=4096),BitPack]", col, rows_per_chunk=30_001, both=False)
 
 
+MIXED_CASES = [("l_comment", "Str|[LZ4(sub=16384,hc=9),BitPack]"), ("l_quantity", "Dict|BitPack"),
+               ("l_shipmode", "Dict|BitPack"), ("l_orderkey", "RLE|[Delta|RLE|[BitPack,BitPack],BitPack]"),
+               ("o_orderkey", "Delta|BitPack"), ("l_returnflag", "ANS"), ("o_comment", "Str|[StrDict|BitPack|ANS,BitPack]"),
+               ("l_extendedprice", "Float2Int|BitPack")]
+
+
+def mixed_batch_parity(engine, sf=0.01, rows_per_chunk=20_000, graph=False):
+    """every kernel family in ONE device batch (one cdm_batch: all family streams, the phase schedule), each
+    chunk's bytes and offsets against the oracle"""
+    g = TPCH(sf)
+    decs, exp = [], []
+    for name, spec in MIXED_CASES:
+        col = g.column(name)
+        casc = cdm.Cascade(spec, col.dtype, col.width)
+        for ch in encoder.encode_chunks(spec, col, rows_per_chunk):
+            out, offs, info = _outputs(ch)
+            decs.append(cdm.Decode(casc, cdm.pinned(ch), out, offs, dev_chunk=torch.from_numpy(ch).cuda()))
+            exp.append((name, ch, out, offs, info))
+    torch.cuda.synchronize()
+    b = cdm.Batch(engine, decs)
+    if graph:
+        b.set_graph(True)
+    stream = torch.cuda.Stream()
+    for _ in range(2 if graph else 1):
+        b.launch(stream)
+        res = b.results(stream)
+    b.close()
+    torch.cuda.synchronize()
+    for (name, ch, out, offs, info), r in zip(exp, res):
+        e, eo = oracle.decode_chunk(ch)
+        assert r["error_bits"] == 0, name
+        assert np.array_equal(out.cpu().numpy()[: info["payload_bytes"]], e), name
+        if eo is not None:
+            assert np.array_equal(offs.cpu().numpy()[: eo.size], eo), name
+
+
+def test_mixed_batch(engine):
+    mixed_batch_parity(engine)
+    mixed_batch_parity(engine, graph=True)
+
+
+@pytest.mark.parametrize("phases", ["1", "2", "3", "4"])
+def test_mixed_batch_phase_schedules(phases):
+    """every phase split of the batch schedule (CDM_PHASES; big batches use 2 by default, small ones one phase)
+    decodes the same bytes (fresh process: the mode is read once)"""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
+            "e = cdm.Engine(0); t.mixed_batch_parity(e); t.mixed_batch_parity(e, graph=True); print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_PHASES": phases}, capture_output=True,
+                       text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
 def test_fp_pair_mapping_variant():
     """the opt-in pair-interleaved FP lane mapping (CDM_FP_PAIR=1) decodes the same rows (fresh process)"""
     import subprocess
