@@ -4,6 +4,7 @@ The B200 build fixes S (256 threads per CTA) and the tile shapes at compile time
   F.P.  L = persistent fp_kernel CTAs per SM (knob fp_ctas_per_sm) in 2^0..2^4     (Table 3: L 2^0..2^4)
   G.P.  L = resident rle_kernel CTAs per SM (knob gp_ctas_per_sm) in 2^0..2^3   (Table 3: G.P. L = numCUs, S x C)
   N.P.  C = lanes per LZ4 sub-chunk (knob lz4_lanes) in {1, 2, 4, 8, 16, 32}       (Table 3: C 2^0..2^10)
+        x the speculative-parse schedule (knob lz4_spec: 0 off, 2 always)
   H6    the scan schedule (knob scan_mode): reduce-then-scan vs single-pass look-back vs warp tiles
 Each evaluation builds a fresh graph-mode batch over the workload (so the knob is captured), times K replays
 with CUDA events after a 256 MiB L2-flush write each, and returns decoded GB/s.
@@ -73,12 +74,13 @@ def main():
         "GP": ({"gp_ctas_per_sm": [1, 2, 4, 8]},
                [("RLE|[BitPack,BitPack]", rle_column("even-4", 1 << 26, I64)),
                 ("RLE|[Delta|RLE|[BitPack,BitPack],BitPack]", g.column("l_orderkey"))]),
-        "NP": ({"lz4_lanes": [1, 2, 4, 8, 16, 32]}, [("Str|[LZ4(sub=16384),BitPack]", g.column("l_comment"))]),
+        "NP": ({"lz4_lanes": [1, 2, 4, 8, 16, 32], "lz4_spec": [0, 2]},
+               [("Str|[LZ4(sub=16384,hc=9),BitPack]", g.column("l_comment"))]),
         "SCAN": ({"scan_mode": [0, 1, 2]}, [("Delta|BitPack", g.column("o_orderkey")),
                                          ("Str|[Raw,BitPack]", g.column("l_comment"))]),
     }
     rows = []
-    defaults = {k: cdm.tune_get(k) for k in ("fp_ctas_per_sm", "lz4_lanes", "scan_mode", "gp_ctas_per_sm")}
+    defaults = {k: cdm.tune_get(k) for k in ("fp_ctas_per_sm", "lz4_lanes", "lz4_spec", "scan_mode", "gp_ctas_per_sm")}
     for pat, (space, cols) in cases.items():
         ev = make_eval(eng, cols, a.steps, flush, stream, list(space))
         bf = tune.brute_force(space, ev)
