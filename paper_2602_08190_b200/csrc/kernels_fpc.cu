@@ -190,10 +190,29 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
       const int64_t a = int64_t(idx) * E - s;  // dictionary byte that lands on group byte 4*q0
       const int64_t aw = a >> 2;                // >= -1 (guard word)
       const uint32_t sh = uint32_t(a) & 3u;
-      uint32_t prev = dword(aw);
+      // large dictionaries (read through L1: the row kernel is L1-wavefront bound there): the words aw .. aw +
+      // q1 - q0 + 1 arrive as whole 16-byte chunks (one L1 wavefront per chunk instead of per word); word aw + m
+      // is W[r0 + m], picked with selects.  Chunks are 16-byte aligned inside the dictionary stream's padding.
+      constexpr int NCHM = ((E + 2) / 4 + 4) / 4 + 1;
+      uint32_t W[4 * NCHM];
+      const uint32_t r0 = uint32_t(aw & 3);
+      if (!DSM) {
+        const uint4* dg4 = reinterpret_cast<const uint4*>(D.dict) + (aw >> 2);
+        const uint32_t nch = (r0 + uint32_t(q1 - q0) + 1) / 4 + 1;
+#pragma unroll
+        for (int c = 0; c < NCHM; c++) {
+          const uint4 x = uint32_t(c) < nch ? __ldg(dg4 + c) : make_uint4(0u, 0u, 0u, 0u);
+          W[4 * c] = x.x; W[4 * c + 1] = x.y; W[4 * c + 2] = x.z; W[4 * c + 3] = x.w;
+        }
+      }
+      auto rword = [&](int m) -> uint32_t {  // dictionary word aw + m
+        if (DSM) return dword(aw + m);
+        return r0 == 0 ? W[m] : r0 == 1 ? W[m + 1] : r0 == 2 ? W[m + 2] : W[m + 3];
+      };
+      uint32_t prev = rword(0);
 #pragma unroll
       for (int m = 0; m <= q1 - q0; m++) {
-        const uint32_t nxt = dword(aw + m + 1);
+        const uint32_t nxt = rword(m + 1);
         uint32_t x = __funnelshift_r(prev, nxt, 8 * sh);
         prev = nxt;
         if (m == 0 && s) x &= 0xFFFFFFFFu << (8 * s);
