@@ -561,15 +561,17 @@ def test_mixed_batch(engine):
     mixed_batch_parity(engine, graph=True)
 
 
-@pytest.mark.parametrize("phases", ["1", "2", "3", "4"])
-def test_mixed_batch_phase_schedules(phases):
-    """every phase split of the batch schedule (CDM_PHASES; big batches use 2 by default, small ones one phase)
-    decodes the same bytes (fresh process: the mode is read once)"""
+@pytest.mark.parametrize("env", [{"CDM_PHASES": "1"}, {"CDM_PHASES": "2"}, {"CDM_PHASES": "3"}, {"CDM_PHASES": "4"},
+                                 {"CDM_SERIAL": "1"}, {"CDM_PDL": "0"}, {"CDM_RLE_PRIO": "hi"}])
+def test_mixed_batch_phase_schedules(env):
+    """every phase split of the batch schedule (CDM_PHASES; big batches use 2 by default, small ones one phase),
+    the serial schedule, launches without programmatic dependencies and the RLE stream at high priority decode
+    the same bytes (fresh process: the switches are read once)"""
     import subprocess
     import sys
     code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t; from paper_2602_08190_b200 import cdm; "
             "e = cdm.Engine(0); t.mixed_batch_parity(e); t.mixed_batch_parity(e, graph=True); print('ok')")
-    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "CDM_PHASES": phases}, capture_output=True,
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
                        text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
