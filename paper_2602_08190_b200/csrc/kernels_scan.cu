@@ -402,14 +402,33 @@ __global__ void __launch_bounds__(kPfxThreads) scan_wprefix_kernel(const __grid_
   uint64_t* ts = B.tsum + uint64_t(D.tile0) * kSubPerTile;
   const uint32_t ns = chunk_subs(D), per = (ns + kPfxThreads - 1) / kPfxThreads;
   const uint32_t i0 = min(ns, threadIdx.x * per), i1 = min(ns, i0 + per);
+  // up to 8 sums per thread (chunks of <= 4 M values) are read once, all loads in flight together
+  constexpr uint32_t R = 8;
+  uint64_t v[R];
   uint64_t sum = 0;
-  for (uint32_t i = i0; i < i1; i++) sum += __ldcg(ts + i);
+  if (per <= R) {
+#pragma unroll
+    for (uint32_t r = 0; r < R; r++) {
+      v[r] = i0 + r < i1 ? __ldcg(ts + i0 + r) : 0ull;
+      sum += v[r];
+    }
+  } else {
+    for (uint32_t i = i0; i < i1; i++) sum += __ldcg(ts + i);
+  }
   uint64_t tot;
   uint64_t run = block_excl_scan_u64<kPfxThreads>(sum, warp_s, &tot);
-  for (uint32_t i = i0; i < i1; i++) {
-    const uint64_t v = __ldcg(ts + i);
-    ts[i] = run;
-    run += v;
+  if (per <= R) {
+#pragma unroll
+    for (uint32_t r = 0; r < R; r++) {
+      if (i0 + r < i1) ts[i0 + r] = run;
+      run += v[r];
+    }
+  } else {
+    for (uint32_t i = i0; i < i1; i++) {
+      const uint64_t x = __ldcg(ts + i);
+      ts[i] = run;
+      run += x;
+    }
   }
   if (threadIdx.x == 0 && D.mode == SCAN_OFFSETS) {
     if (tot != D.base) atomicOr(B.err + D.err_idx, 0x8u);  // CDM_ERR_LENGTHS

@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2 evidence: ncu --set full of the config-4 LZ4 launch (traffic per launch), launch list of the headline bench
-TAG=${1:-r02k}
+TAG=${1:-r02q}
 mkdir -p gpurun_out
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:lz4_thread -c 1 -o gpurun_out/c4_lz4_${TAG} -f \
   python tools/one_batch.py 1 config4 > gpurun_out/ncu_c4lz4_${TAG}.log 2>&1
