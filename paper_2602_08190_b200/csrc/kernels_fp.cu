@@ -60,9 +60,15 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
   __syncthreads();
 
   uint32_t tile = blockIdx.x;
+  // a CTA's tiles increase, so the descriptor of the current / next tile only moves forward from one search
+  int dcur = tile < B.total_tiles ? find_desc_fp(B, tile) : 0, dnext = dcur;
+  auto advance = [&](int d, uint32_t t) {
+    while (d + 1 < int(B.n) && B.d[d + 1].tile0 <= t) d++;
+    return d;
+  };
   // prologue: stage the first tile
   if (tid == 0 && tile < B.total_tiles) {
-    const int di = find_desc_fp(B, tile);
+    const int di = dcur;
     const FpDesc& D = B.d[di];
     const uint32_t lt = tile - D.tile0;
     const uint32_t nb = stage_bytes(D, lt);
@@ -73,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
     const uint32_t s = it & 1;
     const uint32_t next = tile + gridDim.x;
     if (tid == 0 && next < B.total_tiles) {  // stage s^1 was released by the __syncthreads ending it-1
-      const int dn = find_desc_fp(B, next);
+      dnext = advance(dnext, next);
+      const int dn = dnext;
       const FpDesc& Dn = B.d[dn];
       const uint32_t ltn = next - Dn.tile0;
       const uint32_t nb = stage_bytes(Dn, ltn);
@@ -82,7 +89,8 @@ __global__ void __launch_bounds__(kThreads, 4) fp_kernel(const __grid_constant__
       if (nb) tma_load_1d(smem + (s ^ 1) * stage_bytes_alloc, Dn.packed + uint64_t(ltn) * (kFpTile / 8) * Dn.w, nb,
                           &bar[s ^ 1]);
     }
-    const int di = find_desc_fp(B, tile);
+    dcur = advance(dcur, tile);
+    const int di = dcur;
     const FpDesc& D = B.d[di];
     // descriptor fields in registers (param-space reads with a dynamic index cost a load per use)
     const uint32_t lt = tile - D.tile0;
