@@ -91,9 +91,12 @@ __global__ void __launch_bounds__(kThreads) fpc_kernel(const __grid_constant__ F
   // a contiguous range of units per CTA: the chunk (and its staged dictionary) changes rarely
   const uint32_t upc = (total_units + gridDim.x - 1) / gridDim.x;
   const uint32_t u_end = min(total_units, (blockIdx.x + 1) * upc);
+  int dcur = -1;  // the CTA's units increase: the descriptor moves forward from one search
   for (uint32_t u = blockIdx.x * upc; u < u_end; u++) {
     const uint32_t tile = u / S::UPT, pass = u % S::UPT;
-    const int di = find_desc_fpc(B, tile);
+    if (dcur < 0) dcur = find_desc_fpc(B, tile);
+    while (dcur + 1 < int(B.n) && B.d[dcur + 1].tile0 <= tile) dcur++;
+    const int di = dcur;
     const FpDesc& D = B.d[di];
     const uint32_t lt = tile - D.tile0;
     const uint64_t tile_start = uint64_t(lt) * kFpTile;

@@ -364,8 +364,10 @@ __global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constan
   constexpr int kPre = (kIdsWords + kSdBT - 1) / kSdBT;
   uint32_t pre[kPre];
   uint64_t pre_o = 0;
+  int dnext = t0 < t1 ? find_desc_sd(B, t0) : 0, dcur = dnext;  // tiles increase: descriptors move forward
   auto issue = [&](uint32_t t) {
-    const SdDesc& Dn = B.d[find_desc_sd(B, t)];
+    while (dnext + 1 < int(B.n) && B.d[dnext + 1].tile0 <= t) dnext++;
+    const SdDesc& Dn = B.d[dnext];
     const uint32_t ltn = t - Dn.tile0, ntn = min(uint32_t(kSdTile), Dn.ntok - ltn * kSdTile);
     const uint32_t* src = reinterpret_cast<const uint32_t*>(Dn.ids_packed) + ((uint64_t(ltn) * kSdTile * Dn.w) >> 5);
     const uint32_t nw = Dn.w ? uint32_t((uint64_t(ntn) * Dn.w + 31) / 32) + 2 : 0u;
@@ -385,7 +387,8 @@ __global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constan
   };
   if (t0 < t1) issue(t0);
   for (uint32_t gt = t0, it = 0; gt < t1; gt++, it++) {
-    const int dn = find_desc_sd(B, gt);
+    while (dcur + 1 < int(B.n) && B.d[dcur + 1].tile0 <= gt) dcur++;
+    const int dn = dcur;
     const SdDesc& D = B.d[dn];
     uint32_t* const ids_s = ids2_s[it & 1];
     commit(it & 1);   // this tile's ids (its buffer was last read two tiles ago, before the previous barrier)
