@@ -381,12 +381,23 @@ __global__ void __launch_bounds__(kThreads) scan_wsums_kernel(const __grid_const
   if (ls >= chunk_subs(D)) return;
   const uint64_t e0 = uint64_t(ls) * kSub + lane * kSubPer;
   const uint32_t nv = e0 < D.n ? uint32_t(min(uint64_t(kSubPer), uint64_t(D.n) - e0)) : 0u;
-  uint64_t f[kSubPer];
   bool bad = false;
-  lane_fields<uint64_t>(D, e0, nv, f, bad);
   uint64_t acc = 0;
+  if (!D.dict && D.w <= 27) {  // 16 fields < 2^27 sum in 32 bits; the FOR base is added once per field after
+    ScanDesc Dz = D;
+    Dz.for_base = 0;
+    uint32_t f[kSubPer];
+    lane_fields<uint32_t>(Dz, e0, nv, f, bad);
+    uint32_t a32 = 0;
 #pragma unroll
-  for (uint32_t j = 0; j < kSubPer; j++) acc += f[j];
+    for (uint32_t j = 0; j < kSubPer; j++) a32 += f[j];
+    acc = uint64_t(a32) + D.for_base * uint64_t(nv);
+  } else {
+    uint64_t f[kSubPer];
+    lane_fields<uint64_t>(D, e0, nv, f, bad);
+#pragma unroll
+    for (uint32_t j = 0; j < kSubPer; j++) acc += f[j];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
   if (lane == 0) B.tsum[gs] = acc;
@@ -439,8 +450,7 @@ __global__ void __launch_bounds__(kPfxThreads) scan_wprefix_kernel(const __grid_
 // pass 3: one warp per warp tile
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 4) scan_warp_kernel(const __grid_constant__ ScanBatch B) {
-  constexpr uint32_t kStage = kSub + kSub / 16;  // one pad slot per 16 values: conflict-free lane rows
-  __shared__ __align__(16) T stage_s[kThreads / 32][kStage];
+  __shared__ __align__(16) T stage_s[kThreads / 32][kSub];  // a warp tile's results as 16-byte chunks
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t gs = blockIdx.x * (kThreads / 32) + wib;
   if (gs >= B.total_tiles * kSubPerTile) return;
@@ -468,35 +478,50 @@ __global__ void __launch_bounds__(kThreads, 4) scan_warp_kernel(const __grid_con
   }
   const bool delta = D.mode == SCAN_DELTA;
   const T add = T((delta ? D.base : 0ull) + B.tsum[gs]) + (incl - run);
-  T* const st = stage_s[wib];
   // DELTA: base + inclusive sum (exclusive + own field); OFFSETS: the exclusive sum
 #pragma unroll
   for (uint32_t j = 0; j < kSubPer; j++) {
     const T nxt = j + 1 < kSubPer ? f[j + 1] : run;
-    st[lane * 17 + j] = add + (delta ? nxt : f[j]);
+    f[j] = add + (delta ? nxt : f[j]);
   }
-  __syncwarp();
-  // 4 values per 16 bytes (T = 4) or 2 (T = 8): coalesced vector stores of the warp tile's contiguous outputs
-  if (D.out_bytes == 8) {
-    uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + s0;
-    for (uint32_t k = lane; 2 * k < valid; k += 32) {
-      const uint32_t i = 2 * k;
-      const uint64_t a = uint64_t(st[i + (i >> 4)]);
-      if (i + 2 <= valid) st_v2_u64(o + i, a, uint64_t(st[i + 1 + ((i + 1) >> 4)]));
-      else o[i] = a;
+  // the lane's 16 results leave through the warp's stage as 16-byte chunks: lane L writes its chunks c at slot
+  // L * CPL + (c ^ swizzle(L)) (conflict-free), then every lane stores the warp tile's chunks 32 apart (coalesced)
+  uint4* const stq = reinterpret_cast<uint4*>(stage_s[wib]);
+  if (sizeof(T) == 8 && D.out_bytes == 8) {
+#pragma unroll
+    for (uint32_t c = 0; c < 8; c++) {
+      const uint64_t a = uint64_t(f[2 * c]), b = uint64_t(f[2 * c + 1]);
+      stq[lane * 8 + (c ^ (lane & 7))] = make_uint4(uint32_t(a), uint32_t(a >> 32), uint32_t(b), uint32_t(b >> 32));
     }
-  } else {
+    __syncwarp();
+    uint64_t* o = reinterpret_cast<uint64_t*>(D.out) + s0;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; k++) {
+      const uint32_t q = k * 32 + lane, L = q >> 3, c = q & 7;
+      if (2 * q >= valid) break;
+      const uint4 x = stq[L * 8 + (c ^ (L & 7))];
+      const uint64_t a = uint64_t(x.x) | (uint64_t(x.y) << 32), b = uint64_t(x.z) | (uint64_t(x.w) << 32);
+      if (2 * q + 2 <= valid) st_v2_u64(o + 2 * q, a, b);
+      else o[2 * q] = a;
+    }
+  } else {  // 4-byte outputs (values mod 2^32)
+#pragma unroll
+    for (uint32_t c = 0; c < 4; c++)
+      stq[lane * 4 + (c ^ ((lane >> 1) & 3))] =
+          make_uint4(uint32_t(f[4 * c]), uint32_t(f[4 * c + 1]), uint32_t(f[4 * c + 2]), uint32_t(f[4 * c + 3]));
+    __syncwarp();
     uint32_t* o = reinterpret_cast<uint32_t*>(D.out) + s0;
-    for (uint32_t k = lane; 4 * k < valid; k += 32) {
-      const uint32_t i = 4 * k;
-      uint32_t r[4];
 #pragma unroll
-      for (uint32_t j = 0; j < 4; j++) r[j] = uint32_t(st[(i + j) + ((i + j) >> 4)]);
-      if (i + 4 <= valid) {
-        st_v4_u32(o + i, r[0], r[1], r[2], r[3]);
+    for (uint32_t k = 0; k < 4; k++) {
+      const uint32_t q = k * 32 + lane, L = q >> 2, c = q & 3;
+      if (4 * q >= valid) break;
+      const uint4 x = stq[L * 4 + (c ^ ((L >> 1) & 3))];
+      if (4 * q + 4 <= valid) {
+        st_v4_u32(o + 4 * q, x.x, x.y, x.z, x.w);
       } else {
+        const uint32_t r[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (uint32_t j = 0; j < 4; j++) if (i + j < valid) o[i + j] = r[j];
+        for (uint32_t j = 0; j < 4; j++) if (4 * q + j < valid) o[4 * q + j] = r[j];
       }
     }
   }
