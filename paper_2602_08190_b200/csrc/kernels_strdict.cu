@@ -46,17 +46,44 @@ __device__ __forceinline__ void load_dict(const SdDesc& D, uint32_t bytes, uint3
 
 // this thread's tokens kb .. kb + 7 of a tile (ids staged in shared words): dictionary offsets and lengths
 // (0 for a bad id).  `offs` is the dictionary in shared memory or global memory (generic loads).
+// A thread's N consecutive w-bit ids (w <= 32) from staged words through a sliding two-word window (one shared load
+// per 32 bits consumed instead of a 64-bit extraction per id); ids past nt read as 0.
+template <int N>
+__device__ __forceinline__ void window_ids(const uint32_t* ids_s, uint32_t kb, uint32_t nt, uint32_t w, uint32_t (&f)[N]) {
+  if (w == 0) {
+#pragma unroll
+    for (int r = 0; r < N; r++) f[r] = 0;
+    return;
+  }
+  const uint32_t m = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+  uint32_t q = (kb * w) >> 5, sh = (kb * w) & 31;  // kb * w < 2^32: a tile holds 2048 ids of <= 32 bits
+  uint32_t lo = ids_s[q], hi = ids_s[q + 1];
+#pragma unroll
+  for (int r = 0; r < N; r++) {
+    f[r] = kb + r < nt ? __funnelshift_r(lo, hi, sh) & m : 0u;
+    sh += w;
+    if (sh >= 32) {
+      sh -= 32;
+      q++;
+      lo = hi;
+      hi = kb + r + 1 < nt ? ids_s[q + 1] : 0u;  // (stage_bits copies two words past the last id)
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t load_tokens(const SdDesc& D, const uint32_t* offs, const uint32_t* ids_s, uint32_t nt,
                                                 uint32_t kb, uint32_t (&a)[kSdPer], uint32_t (&len)[kSdPer], bool& bad) {
   const uint32_t w = D.w;
   uint32_t sum = 0;
+  uint32_t fid[kSdPer];
+  window_ids<kSdPer>(ids_s, kb, nt, w, fid);
 #pragma unroll
   for (int r = 0; r < kSdPer; r++) {
     a[r] = 0;
     len[r] = 0;
     const uint32_t k = kb + r;
     if (k < nt) {
-      const uint64_t id = D.id_base + extract_bits(ids_s, uint64_t(k) * w, w);
+      const uint64_t id = D.id_base + fid[r];
       if (id < D.entries) {
         a[r] = offs[id];
         len[r] = offs[id + 1] - a[r];
@@ -410,13 +437,15 @@ __global__ void __launch_bounds__(kSdBT) sd_expand_b_kernel(const __grid_constan
     __syncthreads();  // the dictionary staged above (when the chunk changed) is complete
     uint32_t a[kSdBPer], len[kSdBPer];
     uint32_t s = 0;
+    uint32_t fid[kSdBPer];
+    window_ids<kSdBPer>(ids_s, tid * kSdBPer, nt, D.w, fid);
 #pragma unroll
     for (int r = 0; r < kSdBPer; r++) {
       a[r] = 0;
       len[r] = 0;
       const uint32_t k = tid * kSdBPer + r;
       if (k < nt) {
-        const uint64_t id = D.id_base + extract_bits(ids_s, uint64_t(k) * D.w, D.w);
+        const uint64_t id = D.id_base + fid[r];
         if (id < D.entries) {  // (an out-of-range id was reported by sd_sums: it expands to nothing)
           a[r] = offs[id];
           len[r] = offs[id + 1] - a[r];
