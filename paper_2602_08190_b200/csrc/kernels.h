@@ -213,13 +213,15 @@ struct AnsDesc {
   uint32_t il;             // interleaved states per chunk: 1 (thread per chunk) or 32 (warp per chunk)
 };
 
+constexpr int kMaxAnsBatch = 256;  // column chunks per ANS launch (a 16 KB grid-constant parameter)
 struct AnsBatch {  // one batch holds chunks of one interleave (il) only
   uint32_t n;
   uint32_t total_tiles;
   uint32_t cpw;      // il = 32: chunks per warp (a CTA's slot table serves kThreads/32 * cpw chunks)
   uint32_t* err;
-  AnsDesc d[kMaxBatch];
+  AnsDesc d[kMaxAnsBatch];
 };
+static_assert(sizeof(AnsBatch) <= 32000, "kernel parameter limit");
 
 // ---------------------------------------------------------------- NEXT-2: String-dictionary expansion
 // PAPER.md:498 ("each unique word serve as a group in [the Group-Parallel pattern] and expands according to the

@@ -892,7 +892,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
   for (int il : {1, 32}) {
     std::vector<int> sel;
     for (int j : anj) if (B->jobs[j].ans_il == uint32_t(il)) sel.push_back(j);
-    for (auto& g : groups(sel)) {
+    for (auto& g : groups(sel, kMaxAnsBatch)) {
       AnsBatch ab{};
       ab.err = B->err_dev;
       uint32_t tiles = 0;
