@@ -247,14 +247,16 @@ struct SdDesc {
 
 constexpr int kSdCtaTiles = 4;        // sd_expand: tiles per CTA (the dictionary is copied once per CTA)
 
+constexpr int kMaxSdBatch = 256;  // column chunks per String-dictionary launch (an 18 KB grid-constant parameter)
 struct SdBatch {
   uint32_t n;
   uint32_t total_tiles;
   uint32_t total_ctas;         // sd_expand grid
   uint32_t dict_smem;          // largest dictionary stream rounded to 16 B + 16 if all fit kSdDictSmem, else 0 (L1)
   uint32_t* err;
-  SdDesc d[kMaxBatch];
+  SdDesc d[kMaxSdBatch];
 };
+static_assert(sizeof(SdBatch) <= 32000, "kernel parameter limit");
 
 // ---------------------------------------------------------------- launchers (return cudaGetLastError)
 cudaError_t launch_fp(const FpBatch& b, uint32_t max_w, cudaStream_t s);

@@ -930,7 +930,7 @@ size_t layout_batch(cdm_batch* B, Alloc& A, size_t* zero_bytes) {
     }
   }
   // String-dictionary: one tile per kSdTile tokens; the tile sums (then their prefix) live in the arena
-  for (auto& g : groups(sdj)) {
+  for (auto& g : groups(sdj, kMaxSdBatch)) {
     SdBatch sb{};
     sb.err = B->err_dev;
     uint32_t tiles = 0, dmax = 0, ctas = 0;
